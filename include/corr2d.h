@@ -1,0 +1,147 @@
+/*
+ * corr2d.h -- C ABI of libcorr2d.so, the B200 (sm_100a) implementation of the
+ * corr2D Fourier-route hot path (arXiv 1808.00685; reference Python package
+ * `corrtwo` 0.1.0, files cited relative to /root/reference/pkg/src/corrtwo/).
+ *
+ * Plain C: raw device pointers, sizes and a cudaStream_t (passed as void*).
+ * No torch types.  Every entry point returns CORR2D_OK (0) or a status code;
+ * corr2d_last_error() returns the message of the last failure on the calling
+ * thread.  The Python drop-in (paper_1808_00685_b200/_abi.py) maps the codes
+ * onto the reference's exception classes (errors.py:4-36):
+ *   CORR2D_ERR_DATA -> DataError, CORR2D_ERR_NUMERIC / _OOM -> NumericError.
+ *
+ * Data conventions (match the reference layouts):
+ *   raw intensities : m_in x n, row-major, row j = spectrum at t_j, leading
+ *                     dimension ld_raw (elements)              dataset.py:54-56
+ *   dynamic values  : m x n row-major, float64                 preprocess.py:90-120
+ *   half spectra    : K x n complex128 interleaved (re, im), K = m/2 + 1
+ *                                                              fourier.py:61-82
+ *   sync / async    : n1 x n2 row-major planes (float64, or float32 for the
+ *                     fp32 path), leading dimension ld_out     fourier.py:123
+ *
+ * Packed spectra (the intermediate between the two kernels):
+ * for each spectral channel a row of mp >= m "slots" (real packing of the
+ * half spectrum, depth exactly m, zero padded to mp):
+ *   slot s <  K      : Re Y(w = s)
+ *   slot K <= s < m  : Im Y(w = s - K + 1)
+ * Operand A_phi carries Norm*weight(w)*[Re | Im], A_psi Norm*weight(w)*[Im | -Re]
+ * and B the plain [Re | Im]; then sync = A_phi . B^T and async = A_psi . B^T
+ * exactly reproduce  Norm * sum_w weight(w) Y1 conj(Y2)  (fourier.py:107-123).
+ */
+#ifndef CORR2D_H
+#define CORR2D_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CORR2D_ABI_VERSION 1
+
+enum corr2d_status {
+  CORR2D_OK = 0,
+  CORR2D_ERR_DATA = 1,        /* invalid argument / shape       -> DataError    */
+  CORR2D_ERR_NUMERIC = 2,     /* non-finite, zero variance      -> NumericError */
+  CORR2D_ERR_OOM = 3,         /* device allocation failed       -> NumericError */
+  CORR2D_ERR_CUDA = 4,        /* CUDA runtime / launch failure  -> RuntimeError */
+  CORR2D_ERR_UNSUPPORTED = 5  /* shape outside the kernel's range               */
+};
+
+enum corr2d_dtype { CORR2D_F64 = 0, CORR2D_F32 = 1 };
+
+enum corr2d_resample { CORR2D_RESAMPLE_NONE = 0, CORR2D_RESAMPLE_LINEAR = 1, CORR2D_RESAMPLE_MATRIX = 2 };
+
+enum corr2d_pack {
+  CORR2D_PACK_NONE = 0,
+  CORR2D_PACK_F64 = 1,       /* float64 operands (fp64 DMMA contraction)            */
+  CORR2D_PACK_BF16X2 = 2     /* bf16 hi/lo split planes (bf16x3 tcgen05 contraction) */
+};
+
+enum corr2d_ref_mode { CORR2D_REF_MEAN = 0, CORR2D_REF_PROVIDED = 1, CORR2D_REF_NONE = 2 };
+
+/* pack role bits */
+#define CORR2D_ROLE_A 1      /* write A_phi and A_psi (row operand, dataset 1)  */
+#define CORR2D_ROLE_B 2      /* write B (column operand, dataset 2)             */
+
+/* status word layout written by corr2d_prep (device int32[4]) */
+#define CORR2D_ST_NONFINITE 0     /* count of non-finite raw values              */
+#define CORR2D_ST_ZEROVAR 1       /* count of zero-variance channels (alpha > 0)  */
+#define CORR2D_ST_FIRST_ZEROVAR 2 /* INT32_MAX - smallest zero-variance channel, 0 if none */
+
+/* ---------------------------------------------------------------- misc ---- */
+const char* corr2d_last_error(void);
+int corr2d_abi_version(void);
+/* Number of SMs, compute capability of `device`.  Fails with CORR2D_ERR_CUDA
+ * when no device is present. */
+int corr2d_device_info(int device, int* sms, int* cc_major, int* cc_minor);
+/* Packed depth (slots per channel) the contraction kernels need for m. */
+int corr2d_packed_depth(int m, int pack_kind);
+/* Prime/radix factorisation used by the perturbation-axis FFT (for tests). */
+int corr2d_fft_factors(int m, int* factors, int max_factors);
+
+/* ------------------------------------------------------ K1: preprocess ---- */
+/*
+ * One pass over the raw intensities, one CTA per tile of spectral channels:
+ *   resample (preprocess.py:155-195; linear via host-computed idx/frac exactly
+ *   as _interp_linear :147-152, or a dense m x m_in matrix for the natural
+ *   spline :174-175) -> reference (mean :123-125 or provided :56-64) ->
+ *   sigma about it (:198-211, only when alpha > 0; sigma_out receives the
+ *   sigma BEFORE zero-variance substitution so the host can name the dead
+ *   channels) -> divide by sigma**alpha
+ *   (:214-259) -> [optional] real DFT of length m along the perturbation axis
+ *   (fourier.py:73, mixed-radix Stockham in shared memory) -> packing.
+ *
+ * ref_mode CORR2D_REF_NONE treats `raw` as already-dynamic values (no
+ * reference subtraction): with alpha = 0 the entry used by dft_channels /
+ * correlate_ft on DynamicSpectra, with sigma_in the one used by apply_scaling.
+ * sigma_in (optional, n) replaces the computed sigma.
+ * Any output pointer may be NULL.  `status` (device int32[4]; reset on the
+ * stream by this call) receives the counters above; the host raises the
+ * reference's errors from them after the stream synchronises.
+ */
+int corr2d_prep(
+    int in_dtype, const void* raw, int64_t ld_raw, int m_in, int n,
+    int resample_kind, const int32_t* lin_idx, const double* lin_frac,
+    const double* resample_matrix, int m,
+    int ref_mode, const double* ref_in, const double* sigma_in, double alpha, int substitute_zero_var,
+    double norm_const, int pack_kind, int pack_roles,
+    void* a_phi, void* a_psi, void* b, int64_t ld_pack, int64_t split_plane,
+    double* values_out, int64_t ld_values, double* half_out,
+    double* ref_out, double* sigma_out, int32_t* status, void* stream);
+
+/* ------------------------------------------------------- K2: contract ---- */
+/*
+ * sync/async = A_phi . B^T / A_psi . B^T over packed depth mp
+ * (fourier.py:107-123: weighted half-spectrum cross sum x Norm, split).
+ * Output rows [row0, row1) of the n1 x n2 result are written to
+ * phi/psi + (i - row0) * ld_out (a rank's row shard, engine_core.py:106-112).
+ * homo != 0: the row operand and the column operand are the same dataset;
+ * tiles in the shard's own diagonal square are computed once and mirrored,
+ * so sync is exactly symmetric and async exactly skew-symmetric with a zero
+ * diagonal (dataset.py:159-170).  stats (device uint64[3], reset on the
+ * stream by this call) receives
+ * [0] = max|sync| and [1] = max|async| as IEEE bits (uint64), [2] = count of
+ * non-finite outputs (engine_core.py:139-140).
+ */
+int corr2d_contract_f64(
+    const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,
+    int n1, int n2, int mp, int homo, int row0, int row1,
+    double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream);
+
+/*
+ * fp32 path: operands are bf16 hi/lo planes (lo plane at +split_a elements
+ * for A_phi / A_psi, +split_b for B), products hi*hi + hi*lo + lo*hi accumulated in fp32 in TMEM by
+ * tcgen05.mma (kind::f16), fp32 sync/async planes.  Same row/homo contract
+ * as corr2d_contract_f64.  mp must be a multiple of 64.
+ */
+int corr2d_contract_bf16x3(
+    const void* a_phi, const void* a_psi, const void* b, int64_t ld_pack,
+    int64_t split_a, int64_t split_b,
+    int n1, int n2, int mp, int homo, int row0, int row1,
+    float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CORR2D_H */

@@ -1,0 +1,255 @@
+// K2 (fp64) -- packed-spectrum contraction  sync = A_phi . B^T,  async = A_psi . B^T.
+//
+// Restates the hot loop of correlate_ft (fourier.py:107-123): the weighted
+// half-spectrum complex cross sum  Norm * sum_w weight(w) Y1(nu1,w) conj(Y2(nu2,w))
+// in OpenBLAS zgemm row blocks (engine_core.py:114-127), then the Re/Im split.
+// Here the complex contraction over K bins is an exact real contraction over
+// the packed depth m (see include/corr2d.h), done on the FP64 tensor pipe
+// (mma.sync m16n8k4 f64 -> SASS DMMA.8x8x4; B200 has no tcgen05 f64 kind).
+//
+// CTA tile 64 x 64 output elements of BOTH planes, 4 warps of 32 x 32.
+// Operands stream through shared memory in depth chunks of 64 (cp.async);
+// the epilogue stages both planes in shared memory and writes them as
+// coalesced 256 B row segments -- and, for homo tiles above the diagonal,
+// also the mirrored tile (sync^T, -async^T), so the result is exactly
+// symmetric / skew-symmetric (dataset.py:159-170) and half the tiles are
+// never computed.  Finite check and max|.| are fused into the same pass
+// (engine_core.py:139-140).
+#include "common.cuh"
+
+#include <cmath>
+
+namespace corr2d {
+
+constexpr int kBM = 64;
+constexpr int kBN = 64;
+constexpr int kKC = 64;            // depth chunk
+constexpr int kKS = kKC + 4;       // smem row stride (doubles): conflict-free fragments
+constexpr int kCS = kBN + 1;       // epilogue staging stride
+constexpr int kThreads = 128;
+
+enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2 };
+
+struct ContractParams {
+  const double* a_phi;
+  const double* a_psi;
+  const double* b;
+  long long ld_pack;
+  int n1, n2, mp;
+  int homo;
+  int row0, row1;
+  int I0, I1, T;  // row-tile range of the shard, number of column tiles
+  double* phi;
+  double* psi;
+  long long ld_out;
+  unsigned long long* stats;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gsrc), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+      "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Decode the linear block index into (row tile I, column tile J, mode).
+__device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int& J, int& mode) {
+  const long long b = blockIdx.x;
+  if (!p.homo) {
+    I = p.I0 + (int)(b / p.T);
+    J = (int)(b % p.T);
+    mode = kPlain;
+    return;
+  }
+  // row tile I0 + d owns columns [0, I0) U [I0 + d, T): count T - d.
+  // S(d) = d T - d (d - 1) / 2 tiles precede it.
+  const double T = (double)p.T;
+  const double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)b;
+  long long d = (long long)floor(((2.0 * T + 1.0) - sqrt(fmax(disc, 0.0))) * 0.5);
+  auto S = [&](long long dd) { return dd * (long long)p.T - dd * (dd - 1) / 2; };
+  if (d < 0) d = 0;
+  while (d > 0 && S(d) > b) --d;
+  while (S(d + 1) <= b) ++d;
+  I = p.I0 + (int)d;
+  const long long o = b - S(d);
+  if (o < p.I0) {
+    J = (int)o;
+    mode = kPlain;
+  } else {
+    J = I + (int)(o - p.I0);
+    mode = (J == I) ? kDiag : (J < p.I1 ? kMirror : kPlain);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const ContractParams p) {
+  extern __shared__ __align__(16) double sm[];
+  double* As = sm;                     // [kBM][kKS]  A_phi
+  double* Ps = As + kBM * kKS;         // [kBM][kKS]  A_psi
+  double* Bs = Ps + kBM * kKS;         // [kBN][kKS]  B
+
+  int I, J, mode;
+  decode_tile(p, I, J, mode);
+  const int i0 = I * kBM, j0 = J * kBN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int lr = lane >> 2, lk = lane & 3;
+
+  double acc_phi[2][4][4], acc_psi[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int bq = 0; bq < 4; ++bq)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc_phi[a][bq][c] = acc_psi[a][bq][c] = 0.0;
+
+  for (int k0 = 0; k0 < p.mp; k0 += kKC) {
+    const int kc = min(kKC, p.mp - k0);  // multiple of 4
+    const int vec = kc / 2;              // 16-byte chunks per row
+    if (k0 > 0) __syncthreads();
+    for (int idx = tid; idx < kBM * vec; idx += kThreads) {
+      const int r = idx / vec, v = idx - r * vec;
+      const int gi = i0 + r, gj = j0 + r;
+      const bool va = gi < p.n1, vb = gj < p.n2;
+      const long long oa = (long long)(va ? gi : 0) * p.ld_pack + k0 + 2 * v;
+      const long long ob = (long long)(vb ? gj : 0) * p.ld_pack + k0 + 2 * v;
+      cp_async16(As + r * kKS + 2 * v, p.a_phi + oa, va);
+      cp_async16(Ps + r * kKS + 2 * v, p.a_psi + oa, va);
+      cp_async16(Bs + r * kKS + 2 * v, p.b + ob, vb);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < kc; kk += 4) {
+      double ap[2][2], as[2][2], bf[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int r = wm * 32 + mt * 16 + lr;
+        ap[mt][0] = As[r * kKS + kk + lk];
+        ap[mt][1] = As[(r + 8) * kKS + kk + lk];
+        as[mt][0] = Ps[r * kKS + kk + lk];
+        as[mt][1] = Ps[(r + 8) * kKS + kk + lk];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          dmma_16x8x4(acc_phi[mt][nt], ap[mt][0], ap[mt][1], bf[nt]);
+          dmma_16x8x4(acc_psi[mt][nt], as[mt][0], as[mt][1], bf[nt]);
+        }
+    }
+  }
+
+  // ---- epilogue: stage both planes, then coalesced (and mirrored) writes ----
+  __syncthreads();
+  double* Cphi = sm;                   // [kBM][kCS]
+  double* Cpsi = sm + kBM * kCS;       // [kBM][kCS]
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int r = wm * 32 + mt * 16 + lr;
+      const int c = wn * 32 + nt * 8 + 2 * lk;
+      Cphi[r * kCS + c] = acc_phi[mt][nt][0];
+      Cphi[r * kCS + c + 1] = acc_phi[mt][nt][1];
+      Cphi[(r + 8) * kCS + c] = acc_phi[mt][nt][2];
+      Cphi[(r + 8) * kCS + c + 1] = acc_phi[mt][nt][3];
+      Cpsi[r * kCS + c] = acc_psi[mt][nt][0];
+      Cpsi[r * kCS + c + 1] = acc_psi[mt][nt][1];
+      Cpsi[(r + 8) * kCS + c] = acc_psi[mt][nt][2];
+      Cpsi[(r + 8) * kCS + c + 1] = acc_psi[mt][nt][3];
+    }
+  __syncthreads();
+
+  double mphi = 0.0, mpsi = 0.0;
+  int bad = 0;
+  for (int idx = tid; idx < kBM * kBN; idx += kThreads) {
+    const int r = idx >> 6, c = idx & 63;
+    const int gi = i0 + r, gj = j0 + c;
+    if (gi >= p.row1 || gj >= p.n2) continue;
+    double vphi, vpsi;
+    if (mode == kDiag) {
+      if (r <= c) { vphi = Cphi[r * kCS + c]; } else { vphi = Cphi[c * kCS + r]; }
+      if (r < c) vpsi = Cpsi[r * kCS + c];
+      else if (r == c) vpsi = 0.0;
+      else vpsi = -Cpsi[c * kCS + r];
+    } else {
+      vphi = Cphi[r * kCS + c];
+      vpsi = Cpsi[r * kCS + c];
+    }
+    const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
+    __stcs(p.phi + o, vphi);
+    __stcs(p.psi + o, vpsi);
+    mphi = fmax(mphi, fabs(vphi));
+    mpsi = fmax(mpsi, fabs(vpsi));
+    bad += !(isfinite(vphi) && isfinite(vpsi));
+  }
+  if (mode == kMirror) {
+    // out[j][i] = sync[i][j], -async[i][j] for the tile below the diagonal
+    for (int idx = tid; idx < kBM * kBN; idx += kThreads) {
+      const int rr = idx >> 6, cc = idx & 63;   // rr: column of C, cc: row of C
+      const int gi = j0 + rr, gj = i0 + cc;
+      if (gi >= p.row1 || gj >= p.n2) continue;
+      const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
+      __stcs(p.phi + o, Cphi[cc * kCS + rr]);
+      __stcs(p.psi + o, -Cpsi[cc * kCS + rr]);
+    }
+  }
+  mphi = warp_max(mphi);
+  mpsi = warp_max(mpsi);
+  bad = warp_sum(bad);
+  if (lane == 0) {
+    atomic_max_abs(&p.stats[0], mphi);
+    atomic_max_abs(&p.stats[1], mpsi);
+    if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
+  }
+}
+
+}  // namespace corr2d
+
+using namespace corr2d;
+
+extern "C" int corr2d_contract_f64(
+    const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,
+    int n1, int n2, int mp, int homo, int row0, int row1,
+    double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
+  if (!a_phi || !a_psi || !b || !phi || !psi || !stats)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: null pointer");
+  if (n1 < 1 || n2 < 1 || mp < 4 || (mp % 4) != 0)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: bad sizes (mp must be a positive multiple of 4)");
+  if (ld_pack < mp || (ld_pack % 2) != 0)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: ld_pack must be even and >= mp");
+  if (row0 < 0 || row1 > n1 || row0 >= row1)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: bad row range");
+  if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: ld_out < n2");
+  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: homo needs n1 == n2");
+  if (row0 % kBM != 0 || (row1 != n1 && row1 % kBM != 0))
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: row shard bounds must be multiples of 64 (or n1)");
+  ContractParams p{};
+  p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack;
+  p.n1 = n1; p.n2 = n2; p.mp = mp; p.homo = homo; p.row0 = row0; p.row1 = row1;
+  p.I0 = row0 / kBM; p.I1 = (row1 + kBM - 1) / kBM; p.T = (n2 + kBN - 1) / kBN;
+  p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
+  long long tiles;
+  const long long R = p.I1 - p.I0;
+  if (homo) tiles = R * p.T - R * (R - 1) / 2;   // sum_{d<R} (T - d)
+  else tiles = R * p.T;
+  if (tiles <= 0 || tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_contract_f64: tile count out of range");
+  const size_t smem = 3 * (size_t)kBM * kKS * sizeof(double);
+  cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
+  contract_f64_kernel<<<(unsigned)tiles, kThreads, smem, st>>>(p);
+  return check_launch("contract_f64_kernel");
+}

@@ -1,0 +1,386 @@
+// K1 -- fused preprocessing + perturbation-axis DFT + operand packing.
+//
+// Reference path restated here (files under /root/reference/pkg/src/corrtwo/):
+//   resample_equidistant / resample_to_axis / _interp_linear  preprocess.py:147-195
+//   mean_reference / ReferenceSpec.resolve / dynamic_spectra  preprocess.py:56-64,123-137
+//   stddev_spectrum                                           preprocess.py:198-211
+//   apply_scaling (sigma**alpha, zero-variance policy)        preprocess.py:214-259
+//   dft_channels (scipy.fft.rfft along axis 0)                fourier.py:61-82
+//   half_spectrum_weights, weighted1 = half1.T * w, x Norm    fourier.py:50-58,107,121
+//
+// Every step is local to one spectral channel (a column of the m x n matrix),
+// so one CTA owns a tile of C consecutive channels: the raw m_in x C block is
+// read once with coalesced row segments, everything else happens in shared
+// memory, and the packed operand rows are written once.  The elementwise
+// arithmetic uses explicit round-to-nearest intrinsics (no FMA contraction) and
+// the reference's summation order (sequential over the perturbation axis, as
+// numpy's axis-0 reduction), so values / reference / sigma reproduce the
+// reference bit-for-bit; the FFT is a mixed-radix Stockham transform.
+#include "common.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <vector>
+
+namespace corr2d {
+
+constexpr int kPrepThreads = 256;
+constexpr int kMaxFactors = 24;
+
+struct PrepParams {
+  const void* raw;
+  int in_f32;
+  long long ld_raw;
+  int m_in, n;
+  int resample_kind;
+  const int* lin_idx;
+  const double* lin_frac;
+  const double* rs_mat;
+  int m;
+  int ref_mode;            // CORR2D_REF_MEAN / _PROVIDED / _NONE
+  const double* ref_in;
+  const double* sigma_in;  // optional provided sigma (apply_scaling)
+  double alpha;
+  int substitute;
+  double norm;
+  int pack_kind, pack_roles;
+  void* a_phi;
+  void* a_psi;
+  void* b;
+  long long ld_pack, split_plane;
+  int mp;
+  double* values_out;
+  long long ld_values;
+  double* half_out;
+  double* ref_out;
+  double* sigma_out;
+  int* status;
+  int do_fft;
+  int C;
+  int nfactors;
+  int factors[kMaxFactors];
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+__device__ __forceinline__ void store_pack(const PrepParams& p, void* base, long long idx, double v) {
+  if (p.pack_kind == CORR2D_PACK_F64) {
+    static_cast<double*>(base)[idx] = v;
+  } else {
+    __nv_bfloat16 hi = __double2bfloat16(v);
+    double rest = v - (double)__bfloat162float(hi);
+    __nv_bfloat16 lo = __double2bfloat16(rest);
+    static_cast<__nv_bfloat16*>(base)[idx] = hi;
+    static_cast<__nv_bfloat16*>(base)[idx + p.split_plane] = lo;
+  }
+}
+
+__global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) {
+  extern __shared__ __align__(16) double smem[];
+  const int C = p.C, CP = C + 1, m = p.m, m_in = p.m_in;
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, p.n - c0);
+  const int tid = threadIdx.x;
+
+  double2* bufA = reinterpret_cast<double2*>(smem);
+  double2* bufB = bufA + (size_t)m * CP;
+  double2* tw = bufB + (size_t)m * CP;
+  double* raw_s = reinterpret_cast<double*>(tw + m);
+  const bool resample = (p.resample_kind != CORR2D_RESAMPLE_NONE);
+  double* cstat = raw_s + (resample ? (size_t)m_in * CP : 0);  // [C] ref, [C] scale
+
+  // twiddles W[q] = exp(-2 pi i q / m)
+  if (p.do_fft) {
+    for (int q = tid; q < m; q += blockDim.x) {
+      double s, c;
+      sincospi(-2.0 * (double)q / (double)m, &s, &c);
+      tw[q] = make_double2(c, s);
+    }
+  }
+
+  // 1. load the raw m_in x nc block (coalesced row segments), count non-finite
+  int bad = 0;
+  for (int idx = tid; idx < m_in * C; idx += blockDim.x) {
+    const int r = idx / C, c = idx - r * C;
+    double v = 0.0;
+    if (c < nc) {
+      const long long off = (long long)r * p.ld_raw + c0 + c;
+      v = p.in_f32 ? (double)__ldg(static_cast<const float*>(p.raw) + off)
+                   : __ldg(static_cast<const double*>(p.raw) + off);
+      bad += !isfinite(v);
+    }
+    if (resample) raw_s[r * CP + c] = v;
+    else bufA[r * CP + c] = make_double2(v, 0.0);
+  }
+  bad = warp_sum(bad);
+  if ((tid & 31) == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
+  __syncthreads();
+
+  // 2. resample onto the equidistant axis
+  if (resample) {
+    for (int idx = tid; idx < m * C; idx += blockDim.x) {
+      const int k = idx / C, c = idx - k * C;
+      double v;
+      if (p.resample_kind == CORR2D_RESAMPLE_LINEAR) {
+        // values[idx] + frac * (values[idx + 1] - values[idx])   (preprocess.py:152)
+        const int i = __ldg(p.lin_idx + k);
+        const double f = __ldg(p.lin_frac + k);
+        const double v0 = raw_s[i * CP + c], v1 = raw_s[(i + 1) * CP + c];
+        v = __dadd_rn(v0, __dmul_rn(f, __dsub_rn(v1, v0)));
+      } else {
+        const double* row = p.rs_mat + (size_t)k * m_in;
+        double acc = 0.0;
+        for (int j = 0; j < m_in; ++j) acc = fma(__ldg(row + j), raw_s[j * CP + c], acc);
+        v = acc;
+      }
+      bufA[k * CP + c] = make_double2(v, 0.0);
+    }
+    __syncthreads();
+  }
+
+  // 3. per-channel reference / sigma / scale (sequential over the axis, as numpy)
+  if (p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0) {
+    for (int c = tid; c < nc; c += blockDim.x) {
+      double ref;
+      if (p.ref_mode == CORR2D_REF_PROVIDED) {
+        ref = __ldg(p.ref_in + c0 + c);
+      } else if (p.ref_mode == CORR2D_REF_NONE) {
+        ref = 0.0;
+      } else {
+        double s = 0.0;
+        for (int k = 0; k < m; ++k) s = __dadd_rn(s, bufA[k * CP + c].x);
+        ref = __ddiv_rn(s, (double)m);
+      }
+      double scale = 1.0;
+      if (p.alpha > 0.0) {
+        double sigma;
+        if (p.sigma_in) {
+          sigma = __ldg(p.sigma_in + c0 + c);
+        } else {
+          double ss = 0.0;
+          for (int k = 0; k < m; ++k) {
+            const double d = __dsub_rn(bufA[k * CP + c].x, ref);
+            ss = __dadd_rn(ss, __dmul_rn(d, d));
+          }
+          sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
+        }
+        if (p.sigma_out) p.sigma_out[c0 + c] = sigma;  // before substitution
+        if (sigma == 0.0) {
+          atomicAdd(&p.status[CORR2D_ST_ZEROVAR], 1);
+          atomicMax(&p.status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - (c0 + c));
+          if (p.substitute) sigma = 1.0;
+        }
+        // numpy's power fast paths: x**0.5 -> sqrt, x**1 -> x
+        scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
+      }
+      if (p.ref_out) p.ref_out[c0 + c] = ref;
+      cstat[c] = ref;
+      cstat[C + c] = scale;
+    }
+    __syncthreads();
+    const bool scaled = p.alpha > 0.0;
+    for (int idx = tid; idx < m * C; idx += blockDim.x) {
+      const int k = idx / C, c = idx - k * C;
+      if (c >= nc) continue;
+      double v = bufA[k * CP + c].x;
+      if (p.ref_mode != CORR2D_REF_NONE) v = __dsub_rn(v, cstat[c]);
+      if (scaled) v = __ddiv_rn(v, cstat[C + c]);
+      bufA[k * CP + c].x = v;
+    }
+    __syncthreads();
+  }
+
+  if (p.values_out) {
+    for (int idx = tid; idx < m * C; idx += blockDim.x) {
+      const int k = idx / C, c = idx - k * C;
+      if (c < nc) p.values_out[(long long)k * p.ld_values + c0 + c] = bufA[k * CP + c].x;
+    }
+  }
+  if (!p.do_fft) return;
+
+  // 4. DFT along the perturbation axis: Stockham autosort, mixed radix.
+  //    Stage with radix r and current sub-length Ns: output (j, u) gathers
+  //    sum_t in[j + t m/r] * W[t e mod m],  e = (m / (Ns r)) (j mod Ns + u Ns).
+  double2* in = bufA;
+  double2* out = bufB;
+  int Ns = 1;
+  for (int f = 0; f < p.nfactors; ++f) {
+    const int r = p.factors[f];
+    const int stride = m / r;
+    const int span = m / (Ns * r);
+    for (int idx = tid; idx < m * C; idx += blockDim.x) {
+      const int c = idx % C;
+      const int rest = idx / C;
+      const int u = rest % r, j = rest / r;
+      const int k = j % Ns;
+      const int e = span * (k + u * Ns);
+      double2 acc = make_double2(0.0, 0.0);
+      int q = 0;
+      for (int t = 0; t < r; ++t) {
+        const double2 x = in[(j + t * stride) * CP + c];
+        const double2 w = tw[q];
+        acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
+        acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
+        q += e;
+        if (q >= m) q -= m;
+      }
+      out[((j / Ns) * Ns * r + k + u * Ns) * CP + c] = acc;
+    }
+    __syncthreads();
+    double2* t = in; in = out; out = t;
+    Ns *= r;
+  }
+  const double2* X = in;
+  const int K = m / 2 + 1;
+  const bool even = (m % 2) == 0;
+
+  if (p.half_out) {
+    for (int idx = tid; idx < K * C; idx += blockDim.x) {
+      const int w = idx / C, c = idx - w * C;
+      if (c >= nc) continue;
+      double2 v = X[w * CP + c];
+      if (w == 0 || (even && w == m / 2)) v.y = 0.0;  // rfft: exactly real there
+      reinterpret_cast<double2*>(p.half_out)[(long long)w * p.n + c0 + c] = v;
+    }
+  }
+
+  // 5. pack slots: s < K -> Re Y(s); K <= s < m -> Im Y(s - K + 1); rest 0.
+  if (p.pack_kind != CORR2D_PACK_NONE) {
+    const int mp = p.mp;
+    for (int idx = tid; idx < nc * mp; idx += blockDim.x) {
+      const int c = idx / mp, s = idx - c * mp;
+      double vphi = 0.0, vpsi = 0.0, vb = 0.0;
+      if (s < m) {
+        int w;
+        bool re;
+        if (s < K) { w = s; re = true; } else { w = s - K + 1; re = false; }
+        const double2 y = X[w * CP + c];
+        const double R = y.x;
+        const double I = (w == 0 || (even && w == m / 2)) ? 0.0 : y.y;
+        const bool dbl = !(w == 0 || (even && w == m / 2));
+        double nr = p.norm * R, ni = p.norm * I;
+        if (dbl) { nr *= 2.0; ni *= 2.0; }
+        if (re) { vphi = nr; vpsi = ni; vb = R; }
+        else    { vphi = ni; vpsi = -nr; vb = I; }
+      }
+      const long long row = (long long)(c0 + c) * p.ld_pack + s;
+      if (p.pack_roles & CORR2D_ROLE_A) {
+        store_pack(p, p.a_phi, row, vphi);
+        store_pack(p, p.a_psi, row, vpsi);
+      }
+      if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, vb);
+    }
+  }
+}
+
+static int fft_factorize(int m, int* f, int maxf) {
+  int k = 0;
+  for (int r : {8, 4, 2}) {
+    while (m % r == 0 && m > 1) {
+      if (k >= maxf) return -1;
+      f[k++] = r;
+      m /= r;
+    }
+  }
+  for (int q = 3; m > 1; q += 2) {
+    while (m % q == 0) {
+      if (k >= maxf) return -1;
+      f[k++] = q;
+      m /= q;
+    }
+    if ((long long)q * q > m && m > 1) {  // remaining m is prime
+      if (k >= maxf) return -1;
+      f[k++] = m;
+      m = 1;
+    }
+  }
+  return k;
+}
+
+static size_t prep_smem_bytes(int m, int m_in, int C, bool resample) {
+  const size_t CP = C + 1;
+  size_t b = 2 * (size_t)m * CP * sizeof(double2) + (size_t)m * sizeof(double2);
+  if (resample) b += (size_t)m_in * CP * sizeof(double);
+  b += 2 * (size_t)C * sizeof(double);
+  return b;
+}
+
+}  // namespace corr2d
+
+using namespace corr2d;
+
+extern "C" int corr2d_fft_factors(int m, int* factors, int max_factors) {
+  if (m < 1) return fail(CORR2D_ERR_DATA, "fft length must be >= 1");
+  int tmp[kMaxFactors];
+  int k = fft_factorize(m, tmp, kMaxFactors);
+  if (k < 0) return fail(CORR2D_ERR_UNSUPPORTED, "too many FFT factors");
+  for (int i = 0; i < k && i < max_factors; ++i) factors[i] = tmp[i];
+  return k;
+}
+
+extern "C" int corr2d_packed_depth(int m, int pack_kind) {
+  if (m < 2) return fail(CORR2D_ERR_DATA, "need m >= 2");
+  if (pack_kind == CORR2D_PACK_BF16X2) return (m + 63) / 64 * 64;
+  return (m + 3) / 4 * 4;
+}
+
+extern "C" int corr2d_prep(
+    int in_dtype, const void* raw, int64_t ld_raw, int m_in, int n,
+    int resample_kind, const int32_t* lin_idx, const double* lin_frac,
+    const double* resample_matrix, int m,
+    int ref_mode, const double* ref_in, const double* sigma_in, double alpha, int substitute_zero_var,
+    double norm_const, int pack_kind, int pack_roles,
+    void* a_phi, void* a_psi, void* b, int64_t ld_pack, int64_t split_plane,
+    double* values_out, int64_t ld_values, double* half_out,
+    double* ref_out, double* sigma_out, int32_t* status, void* stream) {
+  if (!raw || !status) return fail(CORR2D_ERR_DATA, "corr2d_prep: raw and status are required");
+  if (m_in < 2 || n < 1 || m < 2) return fail(CORR2D_ERR_DATA, "corr2d_prep: need m >= 2 and n >= 1");
+  if (in_dtype != CORR2D_F64 && in_dtype != CORR2D_F32) return fail(CORR2D_ERR_DATA, "corr2d_prep: bad dtype");
+  if (resample_kind == CORR2D_RESAMPLE_NONE && m != m_in)
+    return fail(CORR2D_ERR_DATA, "corr2d_prep: m != m_in without resampling");
+  if (resample_kind == CORR2D_RESAMPLE_LINEAR && (!lin_idx || !lin_frac))
+    return fail(CORR2D_ERR_DATA, "corr2d_prep: linear resampling needs idx/frac");
+  if (resample_kind == CORR2D_RESAMPLE_MATRIX && !resample_matrix)
+    return fail(CORR2D_ERR_DATA, "corr2d_prep: matrix resampling needs the matrix");
+  if (ld_raw < n) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_raw < n");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(CORR2D_ERR_DATA, "scaling exponent must lie in [0, 1]");
+
+  PrepParams p{};
+  p.raw = raw; p.in_f32 = (in_dtype == CORR2D_F32); p.ld_raw = ld_raw; p.m_in = m_in; p.n = n;
+  p.resample_kind = resample_kind; p.lin_idx = lin_idx; p.lin_frac = lin_frac; p.rs_mat = resample_matrix;
+  if (ref_mode < CORR2D_REF_MEAN || ref_mode > CORR2D_REF_NONE) return fail(CORR2D_ERR_DATA, "corr2d_prep: bad ref_mode");
+  if (ref_mode == CORR2D_REF_PROVIDED && !ref_in) return fail(CORR2D_ERR_DATA, "corr2d_prep: provided reference missing");
+  p.m = m; p.ref_mode = ref_mode; p.ref_in = ref_in; p.sigma_in = sigma_in; p.alpha = alpha;
+  p.substitute = substitute_zero_var; p.norm = norm_const;
+  p.pack_kind = pack_kind; p.pack_roles = pack_roles;
+  p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack; p.split_plane = split_plane;
+  p.values_out = values_out; p.ld_values = ld_values; p.half_out = half_out;
+  p.ref_out = ref_out; p.sigma_out = sigma_out; p.status = status;
+  p.do_fft = (half_out != nullptr) || (pack_kind != CORR2D_PACK_NONE);
+  if (pack_kind != CORR2D_PACK_NONE) {
+    p.mp = corr2d_packed_depth(m, pack_kind);
+    if (ld_pack < p.mp) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_pack < packed depth");
+    if ((pack_roles & CORR2D_ROLE_A) && (!a_phi || !a_psi)) return fail(CORR2D_ERR_DATA, "corr2d_prep: A operands missing");
+    if ((pack_roles & CORR2D_ROLE_B) && !b) return fail(CORR2D_ERR_DATA, "corr2d_prep: B operand missing");
+  }
+  if (values_out && ld_values < n) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_values < n");
+  p.nfactors = fft_factorize(m, p.factors, kMaxFactors);
+  if (p.nfactors < 0) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_prep: FFT factorisation failed");
+
+  const bool resample = resample_kind != CORR2D_RESAMPLE_NONE;
+  int C = 32;
+  const size_t budget = 100 * 1024;
+  while (C > 1 && prep_smem_bytes(m, m_in, C, resample) > budget) C /= 2;
+  size_t smem = prep_smem_bytes(m, m_in, C, resample);
+  if (smem > 220 * 1024)
+    return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_prep: m too large for the shared-memory FFT (m <= ~4096)");
+  p.C = C;
+  cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), st) != cudaSuccess) return check_launch("status reset");
+  const int grid = (n + C - 1) / C;
+  prep_kernel<<<grid, kPrepThreads, smem, st>>>(p);
+  return check_launch("prep_kernel");
+}

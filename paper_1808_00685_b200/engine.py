@@ -1,0 +1,365 @@
+"""Device orchestration: buffers, launches and error checks around libcorr2d.
+
+PyTorch is used only as plumbing -- device allocation (caching allocator),
+the current CUDA stream, pinned host buffers and CUDA graphs.  All arithmetic
+of the hot path runs in the hand-written sm_100a kernels behind the C ABI.
+
+The central object is :class:`CorrelationPlan`: for one problem shape it owns
+the packed-operand workspaces and the output planes, ``launch()`` enqueues the
+whole device pipeline on the current stream without synchronising (so it can
+be captured in a CUDA graph), and ``finish()`` synchronises, turns the device
+status words into the reference's exceptions and copies results to the host.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .errors import DataError, NumericError
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+        _torch = t
+    return _torch
+
+
+def require_device(device=None):
+    """The CUDA device to run on; raises BackendUnavailable without one."""
+    t = torch()
+    lib = _abi.load()
+    if not t.cuda.is_available():
+        raise _abi.BackendUnavailable("no CUDA device visible: the corr2d GPU path has no CPU fallback")
+    dev = t.device("cuda", t.cuda.current_device() if device is None else int(device))
+    return lib, dev
+
+
+def stream_handle():
+    return ctypes_void(torch().cuda.current_stream().cuda_stream)
+
+
+def ctypes_void(x):
+    return None if x is None or x == 0 else int(x)
+
+
+def ptr(t):
+    return None if t is None else int(t.data_ptr())
+
+
+def to_device(arr, dev, dtype=None):
+    t = torch()
+    if isinstance(arr, t.Tensor):
+        out = arr.to(device=dev, dtype=dtype or arr.dtype)
+        return out.contiguous()
+    a = np.ascontiguousarray(arr)
+    host = t.from_numpy(a)
+    if dtype is not None and host.dtype != dtype:
+        host = host.to(dtype)
+    return host.to(dev, non_blocking=False)
+
+
+# --------------------------------------------------------------------------
+# resampling plans (host side, tiny: O(m * m_in))
+# --------------------------------------------------------------------------
+
+@dataclass
+class ResamplePlan:
+    kind: int                     # _abi.RESAMPLE_*
+    t_new: np.ndarray
+    lin_idx: np.ndarray | None = None
+    lin_frac: np.ndarray | None = None
+    matrix: np.ndarray | None = None
+    _dev: dict | None = None
+
+    def device(self, dev):
+        if self._dev is None:
+            self._dev = {}
+        key = str(dev)
+        if key not in self._dev:
+            t = torch()
+            d = {}
+            if self.lin_idx is not None:
+                d["idx"] = to_device(self.lin_idx.astype(np.int32), dev)
+                d["frac"] = to_device(self.lin_frac.astype(np.float64), dev)
+            if self.matrix is not None:
+                d["mat"] = to_device(np.ascontiguousarray(self.matrix, dtype=np.float64), dev)
+            self._dev[key] = d
+        return self._dev[key]
+
+
+def linear_plan(t_old: np.ndarray, t_new: np.ndarray) -> ResamplePlan:
+    """Index/fraction pairs computed with the reference's own numpy ops
+    (preprocess.py:149-151), so the device interpolation matches bit-for-bit."""
+    t_old = np.asarray(t_old, dtype=np.float64)
+    t_new = np.asarray(t_new, dtype=np.float64)
+    idx = np.clip(np.searchsorted(t_old, t_new, side="right") - 1, 0, t_old.size - 2)
+    lo, hi = t_old[idx], t_old[idx + 1]
+    frac = (t_new - lo) / (hi - lo)
+    return ResamplePlan(_abi.RESAMPLE_LINEAR, t_new, lin_idx=idx, lin_frac=frac)
+
+
+def spline_matrix(t_old: np.ndarray, t_new: np.ndarray) -> np.ndarray:
+    """Natural cubic spline (zero end curvature) as a dense len(t_new) x len(t_old)
+    linear map: value(t_new) = S @ y.  Restates preprocess.py:174-175
+    (scipy CubicSpline, bc_type="natural") via the moment equations
+      h_{i-1} M_{i-1} + 2 (h_{i-1} + h_i) M_i + h_i M_{i+1} = 6 (d_i - d_{i-1}),
+    solved once for all unit data vectors."""
+    x = np.asarray(t_old, dtype=np.float64)
+    q = np.asarray(t_new, dtype=np.float64)
+    n = x.size
+    h = np.diff(x)
+    ident = np.eye(n)
+    moments = np.zeros((n, n))
+    if n > 2:
+        k = n - 2
+        lhs = np.diag(2.0 * (h[:-1] + h[1:]))
+        if k > 1:
+            lhs += np.diag(h[1:-1], 1) + np.diag(h[1:-1], -1)
+        slope = (ident[1:] - ident[:-1]) / h[:, None]          # (n-1) x n divided differences
+        moments[1:-1] = np.linalg.solve(lhs, 6.0 * (slope[1:] - slope[:-1]))
+    seg = np.clip(np.searchsorted(x, q, side="right") - 1, 0, n - 2)
+    d = (q - x[seg])[:, None]
+    hs = h[seg][:, None]
+    y0, y1 = ident[seg], ident[seg + 1]
+    m0, m1 = moments[seg], moments[seg + 1]
+    b = (y1 - y0) / hs - hs * (2.0 * m0 + m1) / 6.0
+    return y0 + d * (b + d * (m0 / 2.0 + d * (m1 - m0) / (6.0 * hs)))
+
+
+def resample_plan(t_old, target_count: int, interpolant: str) -> ResamplePlan:
+    """np.linspace(t[0], t[-1], N) target axis (preprocess.py:195); linear when
+    requested or m < 3 (:171), natural spline otherwise."""
+    t_old = np.asarray(t_old, dtype=np.float64)
+    t_new = np.linspace(t_old[0], t_old[-1], int(target_count))
+    return axis_plan(t_old, t_new, interpolant)
+
+
+def axis_plan(t_old, t_new, interpolant: str) -> ResamplePlan:
+    t_old = np.asarray(t_old, dtype=np.float64)
+    t_new = np.asarray(t_new, dtype=np.float64)
+    if t_new[0] < t_old[0] or t_new[-1] > t_old[-1]:
+        raise DataError(
+            f"target axis [{t_new[0]:g}, {t_new[-1]:g}] extends beyond "
+            f"the data range [{t_old[0]:g}, {t_old[-1]:g}]")
+    if interpolant == "linear" or t_old.size < 3:
+        return linear_plan(t_old, t_new)
+    if interpolant == "spline":
+        return ResamplePlan(_abi.RESAMPLE_MATRIX, t_new, matrix=spline_matrix(t_old, t_new))
+    raise DataError(f"unknown interpolant {interpolant!r}")
+
+
+# --------------------------------------------------------------------------
+# K1 launcher
+# --------------------------------------------------------------------------
+
+@dataclass
+class PrepRecipe:
+    """How one dataset becomes packed operands / dynamic values on the device."""
+    m_in: int
+    m: int
+    ref_mode: int = _abi.REF_MEAN     # REF_NONE: input already dynamic
+    resample: ResamplePlan | None = None
+    ref_in: object = None             # device tensor (n,) for REF_PROVIDED
+    sigma_in: object = None           # device tensor (n,): provided sigma
+    alpha: float = 0.0
+    substitute: bool = False
+
+
+def launch_prep(lib, raw, recipe: PrepRecipe, *, norm=0.0, pack_kind=_abi.PACK_NONE, roles=0,
+                a_phi=None, a_psi=None, b=None, ld_pack=0, split_plane=0,
+                values_out=None, half_out=None, ref_out=None, sigma_out=None, status=None):
+    t = torch()
+    if raw.dtype == t.float64:
+        in_dtype = _abi.F64
+    elif raw.dtype == t.float32:
+        in_dtype = _abi.F32
+    else:
+        raise DataError(f"unsupported intensity dtype {raw.dtype}")
+    m_in, n = raw.shape
+    rs = recipe.resample
+    rsd = rs.device(raw.device) if rs is not None else {}
+    code = lib.corr2d_prep(
+        in_dtype, ptr(raw), raw.stride(0), m_in, n,
+        rs.kind if rs is not None else _abi.RESAMPLE_NONE,
+        ptr(rsd.get("idx")), ptr(rsd.get("frac")), ptr(rsd.get("mat")), recipe.m,
+        int(recipe.ref_mode), ptr(recipe.ref_in), ptr(recipe.sigma_in), float(recipe.alpha),
+        1 if recipe.substitute else 0, float(norm), pack_kind, roles,
+        ptr(a_phi), ptr(a_psi), ptr(b), int(ld_pack), int(split_plane),
+        ptr(values_out), n if values_out is not None else 0, ptr(half_out),
+        ptr(ref_out), ptr(sigma_out), ptr(status), stream_handle())
+    _abi.check(code, lib)
+
+
+def decode_status(st: np.ndarray):
+    """(nonfinite count, zero-variance count, first zero-variance channel or -1)."""
+    first = int(st[_abi.ST_FIRST_ZEROVAR])
+    return int(st[_abi.ST_NONFINITE]), int(st[_abi.ST_ZEROVAR]), (_abi.INT32_MAX - first) if first else -1
+
+
+def handle_zero_variance(spectral_axis, sigma_raw: np.ndarray, alpha: float, substitute: bool):
+    """apply_scaling's zero-variance policy (preprocess.py:238-254), given the
+    device sigma BEFORE substitution.  Raises NumericError ("error" policy) or
+    warns and returns the substituted sigma ("substitute" policy)."""
+    dead = sigma_raw == 0.0
+    if not dead.any():
+        return sigma_raw
+    positions = np.asarray(spectral_axis)[dead]
+    shown = ", ".join(f"{p:g}" for p in positions[:5])
+    if not substitute:
+        more = " ..." if positions.size > 5 else ""
+        raise NumericError(f"zero-variance spectral channel(s) at {shown}{more}; "
+                           f"cannot scale with alpha = {alpha:g}")
+    warnings.warn(f"substituting sigma = 1 for zero-variance channel(s) at {shown}",
+                  RuntimeWarning, stacklevel=4)
+    return np.where(dead, 1.0, sigma_raw)
+
+
+# --------------------------------------------------------------------------
+# the correlation plan (K1 x {1,2} -> K2)
+# --------------------------------------------------------------------------
+
+class CorrelationPlan:
+    """Device pipeline for one correlation shape.
+
+    inputs  : one (homo) or two (hetero) device tensors m_in x n (f64 or f32)
+    outputs : sync / async planes for rows [row0, row1) x n2 (f64 or f32)
+    """
+
+    def __init__(self, *, n1, n2, m, recipe1: PrepRecipe, recipe2: PrepRecipe | None,
+                 norm: float, dtype="float64", rows=None, device=None, want_ref=True,
+                 want_sigma=False):
+        self.lib, self.dev = require_device(device)
+        t = torch()
+        self.homo = recipe2 is None
+        if self.homo and n1 != n2:
+            raise DataError("homo correlation needs n1 == n2")
+        self.n1, self.n2, self.m = int(n1), int(n2), int(m)
+        self.recipe1, self.recipe2 = recipe1, recipe2
+        self.norm = float(norm)
+        self.dtype = np.dtype(dtype)
+        if self.dtype == np.float64:
+            self.pack_kind, odt, pdt = _abi.PACK_F64, t.float64, t.float64
+        elif self.dtype == np.float32:
+            self.pack_kind, odt, pdt = _abi.PACK_BF16X2, t.float32, t.bfloat16
+        else:
+            raise DataError(f"unsupported compute dtype {dtype}")
+        self.mp = self.lib.corr2d_packed_depth(self.m, self.pack_kind)
+        if self.mp <= 0:
+            _abi.check(_abi.ERR_DATA, self.lib)
+        self.row0, self.row1 = (0, self.n1) if rows is None else (int(rows[0]), int(rows[1]))
+        planes = 1 if self.pack_kind == _abi.PACK_F64 else 2
+        self.split1 = self.n1 * self.mp
+        self.split2 = self.n2 * self.mp
+        dev = self.dev
+        self.a_phi = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
+        self.a_psi = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
+        self.b = self.a_phi.new_empty((planes, self.n2, self.mp)) if not self.homo else None
+        self.b_homo = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev) if self.homo else None
+        nrows = self.row1 - self.row0
+        try:
+            self.phi = t.empty((nrows, self.n2), dtype=odt, device=dev)
+            self.psi = t.empty((nrows, self.n2), dtype=odt, device=dev)
+        except t.cuda.OutOfMemoryError:
+            raise NumericError(
+                f"out of memory assembling the complex correlation matrix; it needs "
+                f"16*{self.n1}*{self.n2} bytes = {16 * self.n1 * self.n2 / 1e9:.2f} GB") from None
+        self.stats = t.zeros(4, dtype=t.int64, device=dev)
+        self.status1 = t.zeros(4, dtype=t.int32, device=dev)
+        self.status2 = t.zeros(4, dtype=t.int32, device=dev)
+        self.ref1 = t.empty(self.n1, dtype=t.float64, device=dev) if want_ref else None
+        self.ref2 = (t.empty(self.n2, dtype=t.float64, device=dev) if (want_ref and not self.homo) else None)
+        self.sigma1 = t.empty(self.n1, dtype=t.float64, device=dev) if want_sigma else None
+        self.sigma2 = (t.empty(self.n2, dtype=t.float64, device=dev) if (want_sigma and not self.homo) else None)
+        self.raw1 = self.raw2 = None
+
+    @property
+    def bop(self):
+        return self.b_homo if self.homo else self.b
+
+    def bind(self, raw1, raw2=None):
+        if raw1.shape[1] != self.n1 or (raw2 is not None and raw2.shape[1] != self.n2):
+            raise DataError("bound inputs do not match the plan's shape")
+        self.raw1, self.raw2 = raw1, raw2
+        return self
+
+    def launch(self):
+        """Enqueue K1 (x1 or x2) and K2 on the current stream; no host sync."""
+        lib = self.lib
+        roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
+        launch_prep(lib, self.raw1, self.recipe1, norm=self.norm, pack_kind=self.pack_kind, roles=roles1,
+                    a_phi=self.a_phi, a_psi=self.a_psi, b=self.b_homo if self.homo else None,
+                    ld_pack=self.mp, split_plane=self.split1, ref_out=self.ref1,
+                    sigma_out=self.sigma1, status=self.status1)
+        if not self.homo:
+            launch_prep(lib, self.raw2, self.recipe2, norm=self.norm, pack_kind=self.pack_kind,
+                        roles=_abi.ROLE_B, b=self.b, ld_pack=self.mp, split_plane=self.split2,
+                        ref_out=self.ref2, sigma_out=self.sigma2, status=self.status2)
+        self.launch_contract()
+
+    def launch_contract(self):
+        lib = self.lib
+        homo = 1 if self.homo else 0
+        if self.pack_kind == _abi.PACK_F64:
+            code = lib.corr2d_contract_f64(
+                ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.mp, self.n1, self.n2, self.mp,
+                homo, self.row0, self.row1, ptr(self.phi), ptr(self.psi), self.n2,
+                ptr(self.stats), stream_handle())
+        else:
+            code = lib.corr2d_contract_bf16x3(
+                ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.mp, self.split1,
+                self.split1 if self.homo else self.split2, self.n1, self.n2, self.mp, homo,
+                self.row0, self.row1, ptr(self.phi), ptr(self.psi), self.n2,
+                ptr(self.stats), stream_handle())
+        _abi.check(code, lib)
+
+    def check(self, axes=(None, None), labels=("first", "second")):
+        """After the stream synchronised: raise the reference's errors, apply
+        the zero-variance policy; returns host (ref1, ref2, sigma1, sigma2, stats)."""
+        sts = [self.status1.cpu().numpy()]
+        if not self.homo:
+            sts.append(self.status2.cpu().numpy())
+        for st, lab in zip(sts, labels):
+            if int(st[_abi.ST_NONFINITE]):
+                raise NumericError(f"{lab} dynamic-spectra matrix contains non-finite values")
+        sig = []
+        for recipe, sdev, axis in ((self.recipe1, self.sigma1, axes[0]), (self.recipe2, self.sigma2, axes[1])):
+            if recipe is None or sdev is None:
+                sig.append(None)
+                continue
+            sig.append(handle_zero_variance(axis, sdev.cpu().numpy(), recipe.alpha, recipe.substitute))
+        stats = self.stats.cpu().numpy()
+        if int(stats[2]):
+            raise NumericError("correlation produced non-finite values")
+        info = {"max_abs_sync": float(stats[0:1].view(np.float64)[0]),
+                "max_abs_async": float(stats[1:2].view(np.float64)[0])}
+        ref1 = self.ref1.cpu().numpy() if self.ref1 is not None else None
+        ref2 = self.ref2.cpu().numpy() if self.ref2 is not None else ref1
+        if self.homo:
+            sig.append(None)
+            sig[1] = sig[0]
+        return ref1, ref2, sig[0], sig[1], info
+
+    def fetch(self, out=None):
+        """Device -> host copy of both planes (into `out` or fresh pinned buffers)."""
+        t = torch()
+        if out is None:
+            hs = t.empty(self.phi.shape, dtype=self.phi.dtype, pin_memory=True)
+            ha = t.empty(self.psi.shape, dtype=self.psi.dtype, pin_memory=True)
+        else:
+            hs, ha = (t.from_numpy(o) if isinstance(o, np.ndarray) else o for o in out)
+        hs.copy_(self.phi, non_blocking=True)
+        ha.copy_(self.psi, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        return hs.numpy(), ha.numpy()
+
+
+def sync():
+    torch().cuda.current_stream().synchronize()

@@ -1,0 +1,81 @@
+"""The C-ABI library: loads on a CPU-only host, exports every symbol
+include/corr2d.h declares, host-only helpers work, and compute entry points
+fail loudly (no CPU fallback) when no GPU is present."""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_1808_00685_b200 import _abi
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "corr2d.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(corr2d_\w+)\(", text, re.M)))
+
+
+def test_header_declares_abi_exports():
+    assert set(declared_symbols()) == set(_abi.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _abi.load()
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_has_no_torch_dependency():
+    out = subprocess.run(["ldd", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "torch" not in out and "c10" not in out
+
+
+def test_sm100a_cubin_present():
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_helpers():
+    lib = _abi.load()
+    assert lib.corr2d_abi_version() == 1
+    assert lib.corr2d_packed_depth(11, _abi.PACK_F64) == 12
+    assert lib.corr2d_packed_depth(64, _abi.PACK_F64) == 64
+    assert lib.corr2d_packed_depth(512, _abi.PACK_BF16X2) == 512
+    assert lib.corr2d_packed_depth(37, _abi.PACK_BF16X2) == 64
+    buf = (ctypes.c_int * 24)()
+    k = lib.corr2d_fft_factors(512, buf, 24)
+    assert list(buf[:k]) == [8, 8, 8]
+    k = lib.corr2d_fft_factors(1000, buf, 24)
+    assert sorted(buf[:k]) == [5, 5, 5, 8]
+    k = lib.corr2d_fft_factors(509, buf, 24)
+    assert list(buf[:k]) == [509]
+
+
+def test_argument_errors_map_to_data_error():
+    lib = _abi.load()
+    code = lib.corr2d_contract_f64(None, None, None, 0, 1, 1, 4, 0, 0, 1, None, None, 1, None, None)
+    assert code == _abi.ERR_DATA
+    with pytest.raises(_abi.DataError, match="null pointer"):
+        _abi.check(code, lib)
+
+
+def test_gpu_entry_points_fail_loudly_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import numpy as np
+    import paper_1808_00685_b200 as P
+    dyn = P.DynamicSpectra(np.arange(4.0), np.arange(6.0), np.ones((6, 4)), np.zeros(4))
+    with pytest.raises(_abi.BackendUnavailable):
+        P.correlate_ft(dyn)
+    lib = _abi.load()
+    sms = ctypes.c_int()
+    assert lib.corr2d_device_info(0, ctypes.byref(sms), None, None) == _abi.ERR_CUDA
