@@ -130,15 +130,19 @@ int corr2d_contract_f64(
     double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
 /*
- * fp32 path: operands are bf16 hi/lo planes (lo plane at +split_a elements
- * for A_phi / A_psi, +split_b for B), products hi*hi + hi*lo + lo*hi accumulated in fp32 in TMEM by
- * tcgen05.mma (kind::f16), fp32 sync/async planes.  Same row/homo contract
- * as corr2d_contract_f64.  mp must be a multiple of 64.
+ * fp32 path (tcgen05 tensor cores).  Operands are K1's CORR2D_PACK_BF16X2
+ * "pair" layout: per channel [Re' | Im'] halves of mp/2 slots each (Re'[s] =
+ * Re Y(s), Im'[0] = Re Y(m/2) for even m else 0, Im'[s] = Im Y(s)), every slot
+ * scaled by sqrt(Norm * weight), stored as bf16 hi / lo planes (lo plane at
+ * +split_a elements for `a`, +split_b for `b`; a == b for homo).  Products
+ * hi*hi + hi*lo + lo*hi accumulate in fp32 in TMEM (tcgen05.mma kind::f16);
+ * async uses the same tiles with the Re/Im halves swapped (negate-A), the even-m
+ * Nyquist x DC cross term is removed in the epilogue.  Same row / homo /
+ * stats contract as corr2d_contract_f64, shard bounds multiples of 128.
  */
 int corr2d_contract_bf16x3(
-    const void* a_phi, const void* a_psi, const void* b, int64_t ld_pack,
-    int64_t split_a, int64_t split_b,
-    int n1, int n2, int mp, int homo, int row0, int row1,
+    const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
+    int n1, int n2, int mp, int m, int homo, int row0, int row1,
     float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
 #ifdef __cplusplus

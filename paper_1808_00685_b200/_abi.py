@@ -62,7 +62,7 @@ def _declare(lib):
         c_void, c_void, c_i64, c_void, c_void,
     ]
     lib.corr2d_contract_bf16x3.argtypes = [
-        c_void, c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, c_int,
+        c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
         c_void, c_void, c_i64, c_void, c_void,
     ]
     for name in ("corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",

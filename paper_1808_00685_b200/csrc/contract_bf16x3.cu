@@ -1,9 +1,481 @@
-// placeholder -- replaced by the tcgen05 kernel
+// K2c (fp32 results) -- packed-spectrum contraction on the 5th-gen tensor cores.
+//
+// Same contract as K2 fp64 (fourier.py:107-123: Norm * sum_w weight(w)
+// Y1 conj(Y2), split into sync / async planes), computed with tcgen05.mma
+// kind::f16 (BF16 inputs, FP32 accumulators in TMEM).  Each packed spectrum
+// value x (float64 from K1) is split x = hi + lo with hi = bf16(x),
+// lo = bf16(x - hi); the products hi*hi + hi*lo + lo*hi carry ~16 mantissa
+// bits, i.e. ~1e-5 relative to max|sync| -- inside the 1e-4 fp32 budget that
+// single-pass TF32/BF16 would miss on band-limited data.
+//
+// Operand format (K1, CORR2D_PACK_BF16X2): per channel [Re' | Im'] halves of
+// hp slots, scaled by sqrt(Norm * weight), so the same packed array serves as
+// row operand A and column operand B and
+//   sync  = A_re . B_re^T + A_im . B_im^T
+//   async = A_im . B_re^T - A_re . B_im^T      (negate-A bit of the idesc)
+// come from the SAME shared-memory tiles; Im'[0] holds the Nyquist real part
+// (even m), whose spurious async cross term with DC is removed in the
+// epilogue (rank-2 correction).
+//
+// Kernel shape: persistent, one CTA per SM, 6 warps --
+//   warp 0   : TMA producer (3-stage mbarrier ring, 64 KB/stage, SWIZZLE_64B)
+//   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-5: epilogue (tcgen05.ld -> registers -> smem -> coalesced stores,
+//              mirrored transpose for homo tiles, fused max|.| / finite check)
+// TMEM holds two accumulator sets (sync 128 + async 128 columns each) so the
+// epilogue of tile t overlaps the MMAs of tile t+1.
 #include "common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace corr2d {
+namespace tc {
+
+constexpr int BM = 128;                 // output rows per tile (TMEM lanes)
+constexpr int BN = 128;                 // output cols per tile
+constexpr int KB = 32;                  // slots per k-block (64 B rows, SWIZZLE_64B)
+constexpr int STAGES = 3;
+constexpr int TILE_BYTES = BM * KB * 2; // 8 KB: one (operand, half, plane) tile
+constexpr int STAGE_BYTES = 8 * TILE_BYTES;
+constexpr int EPI_PITCH = 33;
+constexpr int THREADS = 192;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BM * EPI_PITCH * 4 +
+                              2 * BN * 4 + 16 * 8 + 16;
+
+// kTransOnly: a tile left of the shard's diagonal square is computed as its
+// globally-upper mirror (operand tiles swapped) and only the transpose is
+// written, so every element has the value the unsharded call computes.
+enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2, kTransOnly = 3 };
+
+struct Params {
+  int n1, n2, hp, homo, even;
+  int row0, row1, I0, I1, T;
+  long long ntiles;
+  const __nv_bfloat16* a;
+  const __nv_bfloat16* b;
+  long long ld_pack, split_a, split_b;
+  float* phi;
+  float* psi;
+  long long ld_out;
+  unsigned long long* stats;
+};
+
+// ------------------------------------------------------------- PTX helpers --
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}\n" ::"r"(su32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+
+// K-major, SWIZZLE_64B canonical layout: rows of 64 B, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;                 // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;        // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;                 // layout: SWIZZLE_64B
+  return d;
+}
+
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, both K-major, M=128, N=128
+__host__ __device__ constexpr uint32_t idesc_bf16(bool neg_a) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (neg_a ? (1u << 13) : 0u) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// Same tile enumeration as the fp64 kernel (contract_f64.cu), tile = 128.
+__device__ __forceinline__ void decode_tile(const Params& p, long long b, int& I, int& J, int& mode) {
+  if (!p.homo) {
+    I = p.I0 + (int)(b / p.T);
+    J = (int)(b % p.T);
+    mode = kPlain;
+    return;
+  }
+  const double T = (double)p.T;
+  const double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)b;
+  long long d = (long long)floor(((2.0 * T + 1.0) - sqrt(fmax(disc, 0.0))) * 0.5);
+  auto S = [&](long long dd) { return dd * (long long)p.T - dd * (dd - 1) / 2; };
+  if (d < 0) d = 0;
+  while (d > 0 && S(d) > b) --d;
+  while (S(d + 1) <= b) ++d;
+  I = p.I0 + (int)d;
+  const long long o = b - S(d);
+  if (o < p.I0) {
+    J = I;           // own rows: written through the transpose
+    I = (int)o;      // row-operand tile outside the shard
+    mode = kTransOnly;
+  } else {
+    J = I + (int)(o - p.I0);
+    mode = (J == I) ? kDiag : (J < p.I1 ? kMirror : kPlain);
+  }
+}
+
+__device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+__global__ void __launch_bounds__(THREADS, 1)
+contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                       const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stages = smem;
+  float* epi = reinterpret_cast<float*>(stages + STAGES * STAGE_BYTES);
+  float* col_re0 = epi + BM * EPI_PITCH;
+  float* col_im0 = col_re0 + BN;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
+  uint64_t* full = bars;                 // [STAGES]
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nkb = p.hp / KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer --
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        int I, J, mode;
+        decode_tile(p, t, I, J, mode);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* base = stages + stage * STAGE_BYTES;
+          const int kre = kb * KB, kim = p.hp + kb * KB;
+          tma_load_3d(base + 0 * TILE_BYTES, &tmap_a, kre, I * BM, 0, &full[stage]);
+          tma_load_3d(base + 1 * TILE_BYTES, &tmap_a, kre, I * BM, 1, &full[stage]);
+          tma_load_3d(base + 2 * TILE_BYTES, &tmap_a, kim, I * BM, 0, &full[stage]);
+          tma_load_3d(base + 3 * TILE_BYTES, &tmap_a, kim, I * BM, 1, &full[stage]);
+          tma_load_3d(base + 4 * TILE_BYTES, &tmap_b, kre, J * BN, 0, &full[stage]);
+          tma_load_3d(base + 5 * TILE_BYTES, &tmap_b, kre, J * BN, 1, &full[stage]);
+          tma_load_3d(base + 6 * TILE_BYTES, &tmap_b, kim, J * BN, 0, &full[stage]);
+          tma_load_3d(base + 7 * TILE_BYTES, &tmap_b, kim, J * BN, 1, &full[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer --
+    constexpr uint32_t ID = idesc_bf16(false), IDN = idesc_bf16(true);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_phi = tmem_base + acc * 256, d_psi = d_phi + 128;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t base = su32(stages + stage * STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < KB / 16; ++ks) {
+            const uint32_t off = ks * 32;  // 16 bf16 = 32 bytes along K
+            const uint64_t are_h = desc_sw64(base + 0 * TILE_BYTES + off), are_l = desc_sw64(base + 1 * TILE_BYTES + off);
+            const uint64_t aim_h = desc_sw64(base + 2 * TILE_BYTES + off), aim_l = desc_sw64(base + 3 * TILE_BYTES + off);
+            const uint64_t bre_h = desc_sw64(base + 4 * TILE_BYTES + off), bre_l = desc_sw64(base + 5 * TILE_BYTES + off);
+            const uint64_t bim_h = desc_sw64(base + 6 * TILE_BYTES + off), bim_l = desc_sw64(base + 7 * TILE_BYTES + off);
+            const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+            // sync  += Re.Re + Im.Im          (hi.hi + hi.lo + lo.hi each)
+            umma_bf16(d_phi, are_h, bre_h, ID, acc0);
+            umma_bf16(d_phi, are_h, bre_l, ID, 1);
+            umma_bf16(d_phi, are_l, bre_h, ID, 1);
+            umma_bf16(d_phi, aim_h, bim_h, ID, 1);
+            umma_bf16(d_phi, aim_h, bim_l, ID, 1);
+            umma_bf16(d_phi, aim_l, bim_h, ID, 1);
+            // async += Im.Re - Re.Im
+            umma_bf16(d_psi, aim_h, bre_h, ID, acc0);
+            umma_bf16(d_psi, aim_h, bre_l, ID, 1);
+            umma_bf16(d_psi, aim_l, bre_h, ID, 1);
+            umma_bf16(d_psi, are_h, bim_h, IDN, 1);
+            umma_bf16(d_psi, are_h, bim_l, IDN, 1);
+            umma_bf16(d_psi, are_l, bim_h, IDN, 1);
+          }
+          umma_commit(&empty[stage]);                 // smem stage free when these finish
+          if (kb == nkb - 1) umma_commit(&tfull[acc]); // accumulators ready
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // --------------------------------------------------------- epilogue --
+    const int q = warp & 3;                    // TMEM lane quadrant of this warp
+    const int r = q * 32 + lane;               // tile row owned by this thread
+    const int eid = threadIdx.x - 64;          // 0..127
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    float mphi = 0.f, mpsi = 0.f;
+    unsigned bad = 0;
+    for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      int I, J, mode;
+      decode_tile(p, t, I, J, mode);
+      const int i0 = I * BM, j0 = J * BN;
+      float row_re0 = 0.f, row_im0 = 0.f;
+      if (p.even) {
+        const int gi = i0 + r;
+        if (gi < p.n1) {
+          const __nv_bfloat16* ar = p.a + (long long)gi * p.ld_pack;
+          row_re0 = bf2f(ar[0]) + bf2f(ar[p.split_a]);
+          row_im0 = bf2f(ar[p.hp]) + bf2f(ar[p.hp + p.split_a]);
+        }
+        const int gj = j0 + eid;
+        float cre = 0.f, cim = 0.f;
+        if (gj < p.n2) {
+          const __nv_bfloat16* br = p.b + (long long)gj * p.ld_pack;
+          cre = bf2f(br[0]) + bf2f(br[p.split_b]);
+          cim = bf2f(br[p.hp]) + bf2f(br[p.hp + p.split_b]);
+        }
+        epi_bar();   // previous tile finished reading col_* vectors
+        col_re0[eid] = cre;
+        col_im0[eid] = cim;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int plane = 0; plane < 2; ++plane) {
+        float* out = plane == 0 ? p.phi : p.psi;
+        const float tsign = plane == 0 ? 1.f : -1.f;
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tbase + plane * 128 + c * 32, v);
+          epi_bar();  // staging buffer free
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            float x = __uint_as_float(v[k]);
+            if (plane == 1 && p.even) x -= row_im0 * col_re0[c * 32 + k] - row_re0 * col_im0[c * 32 + k];
+            epi[r * EPI_PITCH + k] = x;
+          }
+          epi_bar();
+          const int cbase = j0 + c * 32;
+          if (mode == kPlain || mode == kMirror) {
+            // direct tile: 128 rows x 32 cols, float4 along the row
+#pragma unroll 2
+            for (int it = 0; it < 8; ++it) {
+              const int idx = eid + it * 128;
+              const int rr = idx >> 3, k4 = (idx & 7) * 4;
+              const int gi = i0 + rr, gj = cbase + k4;
+              float4 w = make_float4(epi[rr * EPI_PITCH + k4], epi[rr * EPI_PITCH + k4 + 1],
+                                     epi[rr * EPI_PITCH + k4 + 2], epi[rr * EPI_PITCH + k4 + 3]);
+              const float mx = fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w)));
+              if (gi < p.row1) {
+                float* dst = out + (long long)(gi - p.row0) * p.ld_out + gj;
+                if (gj + 3 < p.n2 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+                  __stcs(reinterpret_cast<float4*>(dst), w);
+                  if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
+                  bad += !(isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w));
+                } else {
+                  const float ww[4] = {w.x, w.y, w.z, w.w};
+                  for (int u = 0; u < 4; ++u)
+                    if (gj + u < p.n2) {
+                      __stcs(dst + u, ww[u]);
+                      if (plane == 0) mphi = fmaxf(mphi, fabsf(ww[u])); else mpsi = fmaxf(mpsi, fabsf(ww[u]));
+                      bad += !isfinite(ww[u]);
+                    }
+                }
+              }
+            }
+          } else if (mode == kDiag) {
+            for (int it = 0; it < 32; ++it) {
+              const int idx = eid + it * 128;
+              const int rr = idx >> 5, k = idx & 31;
+              const int gi = i0 + rr, gj = cbase + k, cc = c * 32 + k;
+              if (gi >= p.row1 || gj >= p.n2 || rr > cc) continue;
+              float x = epi[rr * EPI_PITCH + k];
+              if (rr == cc && plane == 1) x = 0.f;
+              __stcs(out + (long long)(gi - p.row0) * p.ld_out + gj, x);
+              if (plane == 0) mphi = fmaxf(mphi, fabsf(x)); else mpsi = fmaxf(mpsi, fabsf(x));
+              bad += !isfinite(x);
+            }
+          }
+          if (mode != kPlain) {
+            // mirrored tile: out[j][i] = sync[i][j], -async[i][j]; rows j in this chunk
+            for (int it = 0; it < 32; ++it) {
+              const int idx = eid + it * 128;
+              const int k = idx >> 7, rr = idx & 127;
+              const int gi = cbase + k, gj = i0 + rr, cc = c * 32 + k;
+              if (gi >= p.row1 || gj >= p.n2 || (mode == kDiag && rr >= cc)) continue;
+              const float x = tsign * epi[rr * EPI_PITCH + k];
+              __stcs(out + (long long)(gi - p.row0) * p.ld_out + gj, x);
+              if (mode == kTransOnly) {
+                if (plane == 0) mphi = fmaxf(mphi, fabsf(x)); else mpsi = fmaxf(mpsi, fabsf(x));
+                bad += !isfinite(x);
+              }
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    // reductions
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mphi = fmaxf(mphi, __shfl_xor_sync(0xffffffffu, mphi, o));
+      mpsi = fmaxf(mpsi, __shfl_xor_sync(0xffffffffu, mpsi, o));
+      bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+      atomic_max_abs(&p.stats[0], (double)mphi);
+      atomic_max_abs(&p.stats[1], (double)mpsi);
+      if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* base, long long ld, long long rows, long long split) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)split * 2};
+  cuuint32_t box[3] = {KB, BM, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CORR2D_OK;
+}
+
+}  // namespace tc
+}  // namespace corr2d
+
 using namespace corr2d;
+
 extern "C" int corr2d_contract_bf16x3(
-    const void*, const void*, const void*, int64_t, int64_t, int64_t,
-    int, int, int, int, int, int,
-    float*, float*, int64_t, unsigned long long*, void*) {
-  return fail(CORR2D_ERR_UNSUPPORTED, "not built yet");
+    const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
+    int n1, int n2, int mp, int m, int homo, int row0, int row1,
+    float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
+  using namespace corr2d::tc;
+  if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: null pointer");
+  if (n1 < 1 || n2 < 1 || m < 2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad sizes");
+  if (mp != corr2d_packed_depth(m, CORR2D_PACK_BF16X2) || ld_pack < mp || (ld_pack % 64) != 0)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: packed depth / ld_pack mismatch (ld_pack % 64 == 0)");
+  if (split_a < (long long)n1 * ld_pack || split_b < (long long)n2 * ld_pack || (split_a % 8) || (split_b % 8))
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad plane split");
+  if (row0 < 0 || row1 > n1 || row0 >= row1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad row range");
+  if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: ld_out < n2");
+  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: homo needs n1 == n2");
+  if (row0 % BM != 0 || (row1 != n1 && row1 % BM != 0))
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: row shard bounds must be multiples of 128 (or n1)");
+  Params p{};
+  p.n1 = n1; p.n2 = n2; p.hp = mp / 2; p.homo = homo; p.even = (m % 2) == 0;
+  p.row0 = row0; p.row1 = row1; p.I0 = row0 / BM; p.I1 = (row1 + BM - 1) / BM; p.T = (n2 + BN - 1) / BN;
+  const long long R = p.I1 - p.I0;
+  p.ntiles = homo ? R * p.T - R * (R - 1) / 2 : R * p.T;
+  p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
+  p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
+  p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, a, ld_pack, n1, split_a);
+  if (rc) return rc;
+  rc = make_map(&mb, b, ld_pack, n2, split_b);
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(contract_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
+  const long long grid = p.ntiles < sms ? p.ntiles : sms;
+  contract_bf16x3_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  return check_launch("contract_bf16x3_kernel");
 }

@@ -28,7 +28,10 @@ constexpr int kKS = kKC + 4;       // smem row stride (doubles): conflict-free f
 constexpr int kCS = kBN + 1;       // epilogue staging stride
 constexpr int kThreads = 128;
 
-enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2 };
+// kTransOnly: a tile left of the shard's diagonal square is computed as its
+// globally-upper mirror (operand tiles swapped) and only the transpose is
+// written, so every element has the value the unsharded call computes.
+enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2, kTransOnly = 3 };
 
 struct ContractParams {
   const double* a_phi;
@@ -83,8 +86,9 @@ __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int
   I = p.I0 + (int)d;
   const long long o = b - S(d);
   if (o < p.I0) {
-    J = (int)o;
-    mode = kPlain;
+    J = I;           // own rows: written through the transpose
+    I = (int)o;      // row-operand tile outside the shard
+    mode = kTransOnly;
   } else {
     J = I + (int)(o - p.I0);
     mode = (J == I) ? kDiag : (J < p.I1 ? kMirror : kPlain);
@@ -175,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
   double mphi = 0.0, mpsi = 0.0;
   int bad = 0;
   for (int idx = tid; idx < kBM * kBN; idx += kThreads) {
+    if (mode == kTransOnly) break;
     const int r = idx >> 6, c = idx & 63;
     const int gi = i0 + r, gj = j0 + c;
     if (gi >= p.row1 || gj >= p.n2) continue;
@@ -195,15 +200,21 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
     mpsi = fmax(mpsi, fabs(vpsi));
     bad += !(isfinite(vphi) && isfinite(vpsi));
   }
-  if (mode == kMirror) {
+  if (mode == kMirror || mode == kTransOnly) {
     // out[j][i] = sync[i][j], -async[i][j] for the tile below the diagonal
     for (int idx = tid; idx < kBM * kBN; idx += kThreads) {
       const int rr = idx >> 6, cc = idx & 63;   // rr: column of C, cc: row of C
       const int gi = j0 + rr, gj = i0 + cc;
-      if (gi >= p.row1 || gj >= p.n2) continue;
+      if (gi >= p.row1 || gj >= p.n2 || gi < p.row0) continue;
       const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
-      __stcs(p.phi + o, Cphi[cc * kCS + rr]);
-      __stcs(p.psi + o, -Cpsi[cc * kCS + rr]);
+      const double vphi = Cphi[cc * kCS + rr], vpsi = -Cpsi[cc * kCS + rr];
+      __stcs(p.phi + o, vphi);
+      __stcs(p.psi + o, vpsi);
+      if (mode == kTransOnly) {
+        mphi = fmax(mphi, fabs(vphi));
+        mpsi = fmax(mpsi, fabs(vpsi));
+        bad += !(isfinite(vphi) && isfinite(vpsi));
+      }
     }
   }
   mphi = warp_max(mphi);

@@ -246,8 +246,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     }
   }
 
-  // 5. pack slots: s < K -> Re Y(s); K <= s < m -> Im Y(s - K + 1); rest 0.
-  if (p.pack_kind != CORR2D_PACK_NONE) {
+  // 5a. fp64 slot layout: s < K -> Re Y(s); K <= s < m -> Im Y(s - K + 1); rest 0.
+  if (p.pack_kind == CORR2D_PACK_F64) {
     const int mp = p.mp;
     for (int idx = tid; idx < nc * mp; idx += blockDim.x) {
       const int c = idx / mp, s = idx - c * mp;
@@ -271,6 +271,28 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         store_pack(p, p.a_psi, row, vpsi);
       }
       if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, vb);
+    }
+  }
+  // 5b. bf16 pair layout (see corr2d.h): [Re' | Im'] halves of hp slots each,
+  //     Re'[s] = R_s (s < h), Im'[0] = R_{m/2} (even m) or 0, Im'[s] = I_s,
+  //     every slot scaled by sqrt(Norm * weight) so A and B share one format.
+  if (p.pack_kind == CORR2D_PACK_BF16X2) {
+    const int hp = p.mp / 2;
+    const int h = even ? m / 2 : (m + 1) / 2;
+    const double sn1 = sqrt(p.norm), sn2 = sqrt(2.0 * p.norm);
+    for (int idx = tid; idx < nc * p.mp; idx += blockDim.x) {
+      const int c = idx / p.mp, s = idx - c * p.mp;
+      double v = 0.0;
+      if (s < hp) {
+        if (s < h) v = X[s * CP + c].x * (s == 0 ? sn1 : sn2);
+      } else {
+        const int q = s - hp;
+        if (q == 0) v = even ? X[(m / 2) * CP + c].x * sn1 : 0.0;
+        else if (q < h) v = X[q * CP + c].y * sn2;
+      }
+      const long long row = (long long)(c0 + c) * p.ld_pack + s;
+      if (p.pack_roles & CORR2D_ROLE_A) store_pack(p, p.a_phi, row, v);
+      if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, v);
     }
   }
 }
@@ -322,7 +344,10 @@ extern "C" int corr2d_fft_factors(int m, int* factors, int max_factors) {
 
 extern "C" int corr2d_packed_depth(int m, int pack_kind) {
   if (m < 2) return fail(CORR2D_ERR_DATA, "need m >= 2");
-  if (pack_kind == CORR2D_PACK_BF16X2) return (m + 63) / 64 * 64;
+  if (pack_kind == CORR2D_PACK_BF16X2) {
+    const int h = (m % 2 == 0) ? m / 2 : (m + 1) / 2;
+    return 2 * ((h + 31) / 32 * 32);
+  }
   return (m + 3) / 4 * 4;
 }
 
@@ -362,7 +387,8 @@ extern "C" int corr2d_prep(
   if (pack_kind != CORR2D_PACK_NONE) {
     p.mp = corr2d_packed_depth(m, pack_kind);
     if (ld_pack < p.mp) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_pack < packed depth");
-    if ((pack_roles & CORR2D_ROLE_A) && (!a_phi || !a_psi)) return fail(CORR2D_ERR_DATA, "corr2d_prep: A operands missing");
+    if ((pack_roles & CORR2D_ROLE_A) && (!a_phi || (pack_kind == CORR2D_PACK_F64 && !a_psi)))
+      return fail(CORR2D_ERR_DATA, "corr2d_prep: A operands missing");
     if ((pack_roles & CORR2D_ROLE_B) && !b) return fail(CORR2D_ERR_DATA, "corr2d_prep: B operand missing");
   }
   if (values_out && ld_values < n) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_values < n");

@@ -38,7 +38,12 @@ def require_device(device=None):
     lib = _abi.load()
     if not t.cuda.is_available():
         raise _abi.BackendUnavailable("no CUDA device visible: the corr2d GPU path has no CPU fallback")
-    dev = t.device("cuda", t.cuda.current_device() if device is None else int(device))
+    if device is None:
+        dev = t.device("cuda", t.cuda.current_device())
+    elif isinstance(device, t.device):
+        dev = device if device.index is not None else t.device("cuda", t.cuda.current_device())
+    else:
+        dev = t.device("cuda", int(device))
     return lib, dev
 
 
@@ -260,9 +265,14 @@ class CorrelationPlan:
         self.split2 = self.n2 * self.mp
         dev = self.dev
         self.a_phi = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
-        self.a_psi = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
+        bf16 = self.pack_kind == _abi.PACK_BF16X2
+        # bf16 pair layout: one format for both roles (a_psi unused, homo B == A)
+        self.a_psi = None if bf16 else t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
         self.b = self.a_phi.new_empty((planes, self.n2, self.mp)) if not self.homo else None
-        self.b_homo = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev) if self.homo else None
+        if self.homo:
+            self.b_homo = self.a_phi if bf16 else t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
+        else:
+            self.b_homo = None
         nrows = self.row1 - self.row0
         try:
             self.phi = t.empty((nrows, self.n2), dtype=odt, device=dev)
@@ -294,6 +304,8 @@ class CorrelationPlan:
         """Enqueue K1 (x1 or x2) and K2 on the current stream; no host sync."""
         lib = self.lib
         roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
+        if self.pack_kind == _abi.PACK_BF16X2 and self.homo:
+            roles1 = _abi.ROLE_A
         launch_prep(lib, self.raw1, self.recipe1, norm=self.norm, pack_kind=self.pack_kind, roles=roles1,
                     a_phi=self.a_phi, a_psi=self.a_psi, b=self.b_homo if self.homo else None,
                     ld_pack=self.mp, split_plane=self.split1, ref_out=self.ref1,
@@ -314,8 +326,8 @@ class CorrelationPlan:
                 ptr(self.stats), stream_handle())
         else:
             code = lib.corr2d_contract_bf16x3(
-                ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.mp, self.split1,
-                self.split1 if self.homo else self.split2, self.n1, self.n2, self.mp, homo,
+                ptr(self.a_phi), ptr(self.bop), self.mp, self.split1,
+                self.split1 if self.homo else self.split2, self.n1, self.n2, self.mp, self.m, homo,
                 self.row0, self.row1, ptr(self.phi), ptr(self.psi), self.n2,
                 ptr(self.stats), stream_handle())
         _abi.check(code, lib)

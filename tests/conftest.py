@@ -24,8 +24,11 @@ def golden_names(prefix):
 
 
 def rel_err(got, want, scale=None):
-    got = np.asarray(got, dtype=np.float64)
-    want = np.asarray(want, dtype=np.float64)
+    got = np.asarray(got)
+    want = np.asarray(want)
+    if not (np.iscomplexobj(got) or np.iscomplexobj(want)):
+        got = got.astype(np.float64)
+        want = want.astype(np.float64)
     if scale is None:
         scale = max(float(np.abs(want).max()), 1e-300)
     return float(np.abs(got - want).max()) / scale

@@ -82,7 +82,10 @@ def test_preprocess_variants(name):
     spline = resample is not None and resample.interpolant is P.InterpolantKind.CUBIC_SPLINE and g["t"].size > 2
     if "t_used" in g:
         assert np.array_equal(dyn.perturbation_axis, g["t_used"])
-    if spline:   # dense spline matrix vs scipy's banded solve: rounding-level
+    if alpha not in (0.0, 0.5, 1.0):  # CUDA pow vs libm pow: last-ulp differences
+        assert rel_err(dyn.values, g["values"]) <= 1e-14
+        assert np.array_equal(dyn.reference_used, g["ref"]) and np.array_equal(dyn.sigma, g["sigma"])
+    elif spline:   # dense spline matrix vs scipy's banded solve: rounding-level
         assert rel_err(dyn.values, g["values"]) <= 1e-12
         assert rel_err(dyn.reference_used, g["ref"]) <= 1e-12
     else:        # same operations, same order: bitwise
