@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""Benchmark of the corr2D Fourier-route hot path on B200 (BASELINE.json metric:
+complex Phi+iPsi output elements per second, GElem/s, plus roofline fraction).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl b200|reference]
+
+A step = one pass of the hot path over one batch of the config's synthetic
+input: K1 (resample -> reference -> sigma**alpha -> DFT -> pack) for every
+dataset + K2 (contraction -> sync/async planes), inputs resident in HBM.
+Default workload: config 5 (32768^2 complex map, fp32 planes from the bf16x3
+tcgen05 kernel) -- the largest map, the one BASELINE.json's scaling target is
+quoted on; it fits one GPU.  Outputs (8.6 GB per step) are far larger than the
+126 MB L2, so each step starts with a cold L2.
+
+Multi-GPU (torchrun, one process per GPU, NCCL): the homo tile enumeration is
+split into equal contiguous tile ranges; every rank re-runs the cheap K1 over
+all channels (cheaper than exchanging the packed spectra, so no data-path
+collective) and computes only its tiles.  Total work is fixed: "strong".
+
+--impl reference: the reference CPU path (oracle port of corrtwo's
+preprocess_dataset + correlate_ft, oracle/corr2d_oracle.py) on rank 0 with all
+host threads, each step a bounded row-block sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+# FP64 tensor (DMMA) peak measured on this pool by tools/microbench/peaks.cu
+# (mma.sync m16n8k16 f64, 148 SMs): 37.0 TFLOP/s; DFMA 33.7 TFLOP/s.
+FP64_DMMA_TFLOPS = 37.03
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["_source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+# --------------------------------------------------------------------------
+# workload description
+# --------------------------------------------------------------------------
+
+def workload(cfg):
+    from paper_1808_00685_b200 import configs
+    case = configs.make(cfg)
+    m = case.m
+    k_bins = m // 2 + 1
+    n1, n2 = case.n1, case.n2
+    out_elem_bytes = 8 if case.dtype == "float32" else 16
+    in_bytes = case.set1.intensities.nbytes + (case.set2.intensities.nbytes if case.set2 is not None else 0)
+    return case, dict(m=m, K=k_bins, n1=n1, n2=n2, elems=n1 * n2, out_bytes=n1 * n2 * out_elem_bytes,
+                      in_bytes=in_bytes, flops=8.0 * k_bins * n1 * n2)
+
+
+def roofline_peak(case, peaks):
+    """(bound, peak, unit) for the dominant (contraction) kernel."""
+    if case.dtype == "float32":      # bf16x3 on the f16 tensor pipe
+        return "tensor", float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])), "TFLOP/s"
+    return "tensor", FP64_DMMA_TFLOPS, "TFLOP/s"
+
+
+# --------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# --------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index=0):
+        self.dev = device_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i].lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------
+# reference (CPU) arm and cpu_baseline
+# --------------------------------------------------------------------------
+
+def cpu_sample(case, rows, threads):
+    """Oracle port of preprocess_dataset + correlate_ft on a row block of the
+    map (row-block oracle: rows R of the full result), `threads` workers."""
+    from oracle import corr2d_oracle as O
+    s1 = case.set1
+    t0 = time.perf_counter()
+    _, v1, _, _ = O.preprocess(s1.perturbation_axis, s1.intensities.astype(np.float64),
+                               resample=case.resample, kind=case.interpolant, alpha=case.alpha)
+    v2 = v1
+    if case.set2 is not None:
+        _, v2, _, _ = O.preprocess(case.set2.perturbation_axis, case.set2.intensities,
+                                   resample=case.resample, kind=case.interpolant, alpha=case.alpha)
+    O.correlate_ft(v1[:, :rows], v2, workers=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_rows_for(case, budget_s, threads):
+    """Rows of the map whose oracle run takes about `budget_s` on this host."""
+    n1 = case.n1
+    probe = min(n1, 128)
+    dt = cpu_sample(case, probe, threads)
+    if probe == n1:
+        return n1, dt
+    per_row = max(dt / probe, 1e-9)
+    return int(min(n1, max(probe, budget_s / per_row))), dt
+
+
+def run_reference(args, case, wl, rank):
+    from oracle import corr2d_oracle as O
+    if rank != 0:
+        return
+    threads = O.host_threads()
+    budget = max(0.2, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    rows, _ = cpu_rows_for(case, budget, threads)
+    for _ in range(args.warmup):
+        cpu_sample(case, rows, threads)
+    times = [cpu_sample(case, rows, threads) for _ in range(args.steps)]
+    elems = rows * wl["n2"]
+    total = sum(times)
+    value = elems * len(times) / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GElem/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY App. A)",
+        "config": config_block(case, wl, args),
+        "cpu_baseline": {"value": value, "unit": "GElem/s", "cores": threads, "kind": "port",
+                         "sample": f"rows 0..{rows} of the {wl['n1']}x{wl['n2']} map per step "
+                                   f"(full preprocess + rfft of both operands + row-block zgemm, "
+                                   f"oracle/corr2d_oracle.py = corrtwo 0.1.0 restated, numpy/scipy)"},
+        "e2e": {"value": value, "unit": "GElem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# B200 arm
+# --------------------------------------------------------------------------
+
+METRIC = "complex Phi+iPsi outputs/sec (GElem/s) and % of HBM / tensor-core roofline"
+
+
+def config_block(case, wl, args):
+    return {"workload": case.name, "config_index": case.cfg, "m": wl["m"], "K_bins": wl["K"],
+            "n1": wl["n1"], "n2": wl["n2"], "homo": case.homo, "resample": case.resample,
+            "alpha": case.alpha, "compute": "bf16x3 tcgen05 -> fp32 planes" if case.dtype == "float32"
+            else "fp64 DMMA -> fp64 planes",
+            "l2": "outputs per step >> 126 MB L2 (cold L2 each step)" if wl["out_bytes"] > 4 * 126e6
+            else "L2 flushed between timed steps (256 MB write)",
+            "parallelism": f"tile-range x{args.gpus}" if args.gpus > 1 else "single GPU"}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def tile_range(total, world, rank):
+    edges = np.linspace(0, total, world + 1).astype(np.int64)
+    return int(edges[rank]), int(edges[rank + 1])
+
+
+def homo_tile_count(n, tile):
+    T = (n + tile - 1) // tile
+    return T * (T + 1) // 2
+
+
+def run_b200(args, case, wl, world, rank, local):
+    import torch
+    import paper_1808_00685_b200 as P
+    from paper_1808_00685_b200 import api, engine
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    dt = np.float32 if case.dtype == "float32" else np.float64
+    s1 = case.set1
+    ds1 = P.SpectralDataset(s1.spectral_axis, s1.perturbation_axis, s1.intensities, dtype=dt)
+    ds2 = None
+    if case.set2 is not None:
+        ds2 = P.SpectralDataset(case.set2.spectral_axis, case.set2.perturbation_axis, case.set2.intensities, dtype=dt)
+    spec = P.PreprocessSpec(
+        resample=None if case.resample is None else P.ResampleSpec(case.resample, P.InterpolantKind.from_name(case.interpolant)),
+        scaling_exponent=case.alpha)
+    tile = 128 if case.dtype == "float32" else 64
+    tiles = None
+    if world > 1 and case.homo:
+        tiles = tile_range(homo_tile_count(wl["n1"], tile), world, rank)
+    elif world > 1:
+        tiles = tile_range(((wl["n1"] + tile - 1) // tile) * ((wl["n2"] + tile - 1) // tile), world, rank)
+    plan, homo = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev)
+    if tiles is not None:
+        plan.tile0, plan.tile1 = tiles
+    stream = torch.cuda.current_stream()
+
+    # ---- parity gate before timing (bench.py:98-115 style): sampled rows vs the oracle
+    plan.launch()
+    torch.cuda.synchronize()
+    plan.check(axes=(ds1.spectral_axis, (ds2 or ds1).spectral_axis))
+    parity = parity_gate(case, plan, world) if rank == 0 and world == 1 else None
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        plan.launch()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device time, barrier + sync on both sides
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for k in range(args.steps):
+            # K1 launches, then K2 bracketed by events on the launching stream
+            plan.launch_prep_only()
+            kev[k][0].record(stream)
+            plan.launch_contract()
+            kev[k][1].record(stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = ev0.elapsed_time(ev1)
+    k2_ms = [a.elapsed_time(b) for a, b in kev]
+    ms_max = allreduce_max(ms, world)
+    k2_avg = allreduce_max(float(np.mean(k2_ms)), world)
+
+    # ---- e2e through the public API: pinned host inputs -> planes in pinned host memory
+    e2e = run_e2e(args, case, ds1, ds2, world, rank, dev) if world == 1 else None
+
+    if rank != 0:
+        return
+    elems_total = wl["elems"] * args.steps
+    value = elems_total / (ms_max * 1e-3) / 1e9
+    peaks = measured_peaks()
+    bound, peak, unit = roofline_peak(case, peaks)
+    achieved = wl["flops"] / (k2_avg * 1e-3) / 1e12
+    traffic = load_traffic(case.cfg)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GElem/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16x3->f32 (fp64 prep)" if case.dtype == "float32" else "f64",
+        "data": "synthetic (seeded generators, SURVEY.md App. A; no public dataset)",
+        "config": config_block(case, wl, args),
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "contract_bf16x3_kernel" if case.dtype == "float32" else "contract_f64_kernel",
+                     "kernel_ms": k2_avg, "algorithmic": "8*K flops per complex output element",
+                     "hbm_floor_ms": (wl["out_bytes"] + wl["in_bytes"]) / (peaks["hbm_gbs"] * 1e9) * 1e3,
+                     "peak_source": peaks["_source"] + ("" if case.dtype == "float32" else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
+        "clocks": clocks.summary(),
+        "gpu_launches": plan.launches_per_step * args.steps,
+        "parity": parity,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_line(case, wl)
+    print(json.dumps(line), flush=True)
+
+
+def parity_gate(case, plan, world):
+    """Sampled output rows vs the CPU oracle (row-block form) before timing."""
+    from oracle import corr2d_oracle as O
+    s1 = case.set1
+    _, v1, _, _ = O.preprocess(s1.perturbation_axis, s1.intensities.astype(np.float64), resample=case.resample,
+                               kind=case.interpolant, alpha=case.alpha)
+    v2 = v1
+    if case.set2 is not None:
+        _, v2, _, _ = O.preprocess(case.set2.perturbation_axis, case.set2.intensities, resample=case.resample,
+                                   kind=case.interpolant, alpha=case.alpha)
+    rows = np.unique(np.linspace(0, case.n1 - 1, 3).astype(int))
+    worst = 0.0
+    scale = 0.0
+    for r in rows:
+        s, a, _ = O.correlate_ft(v1[:, r:r + 1], v2)
+        gs = plan.phi[r].double().cpu().numpy()
+        ga = plan.psi[r].double().cpu().numpy()
+        worst = max(worst, float(np.abs(gs - s[0]).max()), float(np.abs(ga - a[0]).max()))
+        scale = max(scale, float(np.abs(s).max()), float(np.abs(a).max()))
+    st = plan.stats.cpu().numpy()
+    scale = max(scale, float(st[0:1].view(np.float64)[0]))
+    tol = 1e-4 if case.dtype == "float32" else 1e-10
+    err = worst / scale
+    if err > tol:
+        raise SystemExit(f"parity gate failed: max rel err {err:.3e} > {tol}")
+    return {"max_rel_err": err, "tol": tol, "rows_checked": [int(r) for r in rows]}
+
+
+def run_e2e(args, case, ds1, ds2, world, rank, dev):
+    """Public-API call per step: corr2d() on pinned host intensities (H2D inside)
+    writing both planes into pinned host buffers (D2H inside)."""
+    import torch
+    import paper_1808_00685_b200 as P
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    h1 = P.SpectralDataset(ds1.spectral_axis, ds1.perturbation_axis, pin(ds1.intensities), dtype=ds1.dtype)
+    h2 = None if ds2 is None else P.SpectralDataset(ds2.spectral_axis, ds2.perturbation_axis, pin(ds2.intensities), dtype=ds2.dtype)
+    odt = torch.float32 if case.dtype == "float32" else torch.float64
+    n1, n2 = case.n1, case.n2
+    hs = torch.empty((n1, n2), dtype=odt, pin_memory=True)
+    ha = torch.empty((n1, n2), dtype=odt, pin_memory=True)
+    kw = dict(resample=case.resample, interpolant=case.interpolant, alpha=case.alpha, dtype=case.dtype,
+              out=(hs, ha), device=dev)
+    steps = max(1, min(args.steps, args.e2e_steps))
+    for _ in range(max(1, min(args.warmup, 2))):
+        P.corr2d(h1, h2, **kw)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = P.corr2d(h1, h2, **kw)
+        _ = float(res.sync[0, 0])  # the result is on the host
+    dt = time.perf_counter() - t0
+    h2d = ds1.intensities.nbytes + (ds2.intensities.nbytes if ds2 is not None else 0)
+    d2h = 2 * n1 * n2 * (4 if case.dtype == "float32" else 8)
+    return {"value": n1 * n2 * steps / dt / 1e9, "unit": "GElem/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": 1e3 * dt / steps,
+            "api": "paper_1808_00685_b200.corr2d(ds, ..., out=(pinned, pinned))"}
+
+
+def cpu_baseline_line(case, wl):
+    from oracle import corr2d_oracle as O
+    threads = O.host_threads()
+    rows, _ = cpu_rows_for(case, 10.0, threads)
+    dt = cpu_sample(case, rows, threads)
+    return {"value": rows * wl["n2"] / dt / 1e9, "unit": "GElem/s", "cores": threads, "kind": "port",
+            "sample": f"rows 0..{rows} of the {wl['n1']}x{wl['n2']} map ({dt:.1f} s; preprocess + rfft + "
+                      f"row-block zgemm via the oracle restatement of corrtwo 0.1.0)"}
+
+
+def load_traffic(cfg):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get(str(cfg))
+    return None
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    case, wl = workload(args.config)
+    if args.impl == "reference":
+        run_reference(args, case, wl, rank)
+        return
+    world, rank, local = dist_setup(args)
+    try:
+        run_b200(args, case, wl, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

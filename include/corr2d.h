@@ -126,7 +126,7 @@ int corr2d_prep(
  */
 int corr2d_contract_f64(
     const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,
-    int n1, int n2, int mp, int homo, int row0, int row1,
+    int n1, int n2, int mp, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
 /*
@@ -142,7 +142,7 @@ int corr2d_contract_f64(
  */
 int corr2d_contract_bf16x3(
     const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
-    int n1, int n2, int mp, int m, int homo, int row0, int row1,
+    int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
 #ifdef __cplusplus

@@ -58,12 +58,12 @@ def _declare(lib):
         c_void, c_void, c_void, c_void,              # ref_out sigma_out status stream
     ]
     lib.corr2d_contract_f64.argtypes = [
-        c_void, c_void, c_void, c_i64, c_int, c_int, c_int, c_int, c_int, c_int,
+        c_void, c_void, c_void, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_i64, c_i64,
         c_void, c_void, c_i64, c_void, c_void,
     ]
     lib.corr2d_contract_bf16x3.argtypes = [
         c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
-        c_void, c_void, c_i64, c_void, c_void,
+        c_i64, c_i64, c_void, c_void, c_i64, c_void, c_void,
     ]
     for name in ("corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
                  "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors"):

@@ -52,7 +52,7 @@ enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2, kTransOnly = 3 };
 struct Params {
   int n1, n2, hp, homo, even;
   int row0, row1, I0, I1, T;
-  long long ntiles;
+  long long tile0, ntiles;  // tiles [tile0, ntiles) of the enumeration
   const __nv_bfloat16* a;
   const __nv_bfloat16* b;
   long long ld_pack, split_a, split_b;
@@ -204,7 +204,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+      for (long long t = p.tile0 + blockIdx.x; t < p.ntiles; t += gridDim.x) {
         int I, J, mode;
         decode_tile(p, t, I, J, mode);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -231,7 +231,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    for (long long t = p.tile0 + blockIdx.x; t < p.ntiles; t += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_phi = tmem_base + acc * 256, d_psi = d_phi + 128;
@@ -281,7 +281,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     uint32_t acc_phase = 0;
     float mphi = 0.f, mpsi = 0.f;
     unsigned bad = 0;
-    for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+    for (long long t = p.tile0 + blockIdx.x; t < p.ntiles; t += gridDim.x) {
       int I, J, mode;
       decode_tile(p, t, I, J, mode);
       const int i0 = I * BM, j0 = J * BN;
@@ -442,7 +442,7 @@ using namespace corr2d;
 
 extern "C" int corr2d_contract_bf16x3(
     const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
-    int n1, int n2, int mp, int m, int homo, int row0, int row1,
+    int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
   using namespace corr2d::tc;
   if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: null pointer");
@@ -460,7 +460,11 @@ extern "C" int corr2d_contract_bf16x3(
   p.n1 = n1; p.n2 = n2; p.hp = mp / 2; p.homo = homo; p.even = (m % 2) == 0;
   p.row0 = row0; p.row1 = row1; p.I0 = row0 / BM; p.I1 = (row1 + BM - 1) / BM; p.T = (n2 + BN - 1) / BN;
   const long long R = p.I1 - p.I0;
-  p.ntiles = homo ? R * p.T - R * (R - 1) / 2 : R * p.T;
+  const long long total = homo ? R * p.T - R * (R - 1) / 2 : R * p.T;
+  if (tile1 < 0 || tile1 > total) tile1 = total;
+  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad tile range");
+  p.tile0 = tile0;
+  p.ntiles = tile1;
   p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
   p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
@@ -475,7 +479,9 @@ extern "C" int corr2d_contract_bf16x3(
   cudaFuncSetAttribute(contract_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
-  const long long grid = p.ntiles < sms ? p.ntiles : sms;
+  const long long work = p.ntiles - p.tile0;
+  if (work == 0) return CORR2D_OK;
+  const long long grid = work < sms ? work : sms;
   contract_bf16x3_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, p);
   return check_launch("contract_bf16x3_kernel");
 }

@@ -42,6 +42,7 @@ struct ContractParams {
   int homo;
   int row0, row1;
   int I0, I1, T;  // row-tile range of the shard, number of column tiles
+  long long tile0;  // first tile of this launch (tile-range partition)
   double* phi;
   double* psi;
   long long ld_out;
@@ -67,7 +68,7 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 
 // Decode the linear block index into (row tile I, column tile J, mode).
 __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int& J, int& mode) {
-  const long long b = blockIdx.x;
+  const long long b = p.tile0 + blockIdx.x;
   if (!p.homo) {
     I = p.I0 + (int)(b / p.T);
     J = (int)(b % p.T);
@@ -233,7 +234,7 @@ using namespace corr2d;
 
 extern "C" int corr2d_contract_f64(
     const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,
-    int n1, int n2, int mp, int homo, int row0, int row1,
+    int n1, int n2, int mp, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
   if (!a_phi || !a_psi || !b || !phi || !psi || !stats)
     return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: null pointer");
@@ -256,11 +257,16 @@ extern "C" int corr2d_contract_f64(
   const long long R = p.I1 - p.I0;
   if (homo) tiles = R * p.T - R * (R - 1) / 2;   // sum_{d<R} (T - d)
   else tiles = R * p.T;
-  if (tiles <= 0 || tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_contract_f64: tile count out of range");
+  if (tile1 < 0 || tile1 > tiles) tile1 = tiles;
+  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: bad tile range");
+  p.tile0 = tile0;
+  tiles = tile1 - tile0;
+  if (tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_contract_f64: tile count out of range");
   const size_t smem = 3 * (size_t)kBM * kKS * sizeof(double);
   cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
+  if (tiles == 0) return CORR2D_OK;
   contract_f64_kernel<<<(unsigned)tiles, kThreads, smem, st>>>(p);
   return check_launch("contract_f64_kernel");
 }

@@ -240,7 +240,7 @@ class CorrelationPlan:
 
     def __init__(self, *, n1, n2, m, recipe1: PrepRecipe, recipe2: PrepRecipe | None,
                  norm: float, dtype="float64", rows=None, device=None, want_ref=True,
-                 want_sigma=False):
+                 want_sigma=False, tiles=None):
         self.lib, self.dev = require_device(device)
         t = torch()
         self.homo = recipe2 is None
@@ -260,6 +260,8 @@ class CorrelationPlan:
         if self.mp <= 0:
             _abi.check(_abi.ERR_DATA, self.lib)
         self.row0, self.row1 = (0, self.n1) if rows is None else (int(rows[0]), int(rows[1]))
+        # tile-range partition of the (shard's) tile enumeration; -1 = to the end
+        self.tile0, self.tile1 = (0, -1) if tiles is None else (int(tiles[0]), int(tiles[1]))
         planes = 1 if self.pack_kind == _abi.PACK_F64 else 2
         self.split1 = self.n1 * self.mp
         self.split2 = self.n2 * self.mp
@@ -300,8 +302,17 @@ class CorrelationPlan:
         self.raw1, self.raw2 = raw1, raw2
         return self
 
+    @property
+    def launches_per_step(self) -> int:
+        """Kernels of ours one launch() enqueues: K1 per dataset + K2."""
+        return (1 if self.homo else 2) + 1
+
     def launch(self):
         """Enqueue K1 (x1 or x2) and K2 on the current stream; no host sync."""
+        self.launch_prep_only()
+        self.launch_contract()
+
+    def launch_prep_only(self):
         lib = self.lib
         roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
         if self.pack_kind == _abi.PACK_BF16X2 and self.homo:
@@ -314,7 +325,6 @@ class CorrelationPlan:
             launch_prep(lib, self.raw2, self.recipe2, norm=self.norm, pack_kind=self.pack_kind,
                         roles=_abi.ROLE_B, b=self.b, ld_pack=self.mp, split_plane=self.split2,
                         ref_out=self.ref2, sigma_out=self.sigma2, status=self.status2)
-        self.launch_contract()
 
     def launch_contract(self):
         lib = self.lib
@@ -322,13 +332,13 @@ class CorrelationPlan:
         if self.pack_kind == _abi.PACK_F64:
             code = lib.corr2d_contract_f64(
                 ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.mp, self.n1, self.n2, self.mp,
-                homo, self.row0, self.row1, ptr(self.phi), ptr(self.psi), self.n2,
-                ptr(self.stats), stream_handle())
+                homo, self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi),
+                self.n2, ptr(self.stats), stream_handle())
         else:
             code = lib.corr2d_contract_bf16x3(
                 ptr(self.a_phi), ptr(self.bop), self.mp, self.split1,
                 self.split1 if self.homo else self.split2, self.n1, self.n2, self.mp, self.m, homo,
-                self.row0, self.row1, ptr(self.phi), ptr(self.psi), self.n2,
+                self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
                 ptr(self.stats), stream_handle())
         _abi.check(code, lib)
 

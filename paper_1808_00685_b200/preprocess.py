@@ -154,15 +154,9 @@ def _is_tensor(x) -> bool:
 # --------------------------------------------------------------------------
 
 def _raw_device(ds: SpectralDataset, dev):
-    dev_cache = getattr(ds, "_corr2d_dev", None)
-    if dev_cache is not None and dev_cache[0] is ds.intensities and dev_cache[1].device == dev:
-        return dev_cache[1]
-    t = engine.to_device(ds.intensities, dev)
-    try:
-        ds._corr2d_dev = (ds.intensities, t)
-    except AttributeError:  # pragma: no cover
-        pass
-    return t
+    """Upload the intensities for this call (pinned host arrays copy at full
+    PCIe rate).  No hidden cache: every call moves its inputs."""
+    return engine.to_device(ds.intensities, dev)
 
 
 def _run_prep(ds_values_dev, recipe: engine.PrepRecipe, *, want_values=True, want_ref=False,

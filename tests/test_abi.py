@@ -61,7 +61,7 @@ def test_host_helpers():
 
 def test_argument_errors_map_to_data_error():
     lib = _abi.load()
-    code = lib.corr2d_contract_f64(None, None, None, 0, 1, 1, 4, 0, 0, 1, None, None, 1, None, None)
+    code = lib.corr2d_contract_f64(None, None, None, 0, 1, 1, 4, 0, 0, 1, 0, -1, None, None, 1, None, None)
     assert code == _abi.ERR_DATA
     with pytest.raises(_abi.DataError, match="null pointer"):
         _abi.check(code, lib)
