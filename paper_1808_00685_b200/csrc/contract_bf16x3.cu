@@ -20,8 +20,9 @@
 // Kernel shape: persistent, one CTA per SM, 6 warps --
 //   warp 0   : TMA producer (3-stage mbarrier ring, 64 KB/stage, SWIZZLE_64B)
 //   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5: epilogue (tcgen05.ld -> registers -> smem -> coalesced stores,
-//              mirrored transpose for homo tiles, fused max|.| / finite check)
+//   warps 2-5: epilogue (tcgen05.ld -> registers -> global stores: own-row
+//              STG.128 for the tile, warp-coalesced columns for its mirror,
+//              fused max|.| / finite check)
 // TMEM holds two accumulator sets (sync 128 + async 128 columns each) so the
 // epilogue of tile t overlaps the MMAs of tile t+1.
 #include "common.cuh"
@@ -38,11 +39,9 @@ constexpr int KB = 32;                  // slots per k-block (64 B rows, SWIZZLE
 constexpr int STAGES = 3;
 constexpr int TILE_BYTES = BM * KB * 2; // 8 KB: one (operand, half, plane) tile
 constexpr int STAGE_BYTES = 8 * TILE_BYTES;
-constexpr int EPI_PITCH = 33;
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BM * EPI_PITCH * 4 +
-                              2 * BN * 4 + 16 * 8 + 16;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 2 * BN * 4 + 16 * 8 + 16;
 
 // kTransOnly: a tile left of the shard's diagonal square is computed as its
 // globally-upper mirror (operand tiles swapped) and only the transpose is
@@ -167,11 +166,11 @@ __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float
 __global__ void __launch_bounds__(THREADS, 1)
 contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        const Params p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // keep the shared address space visible to the compiler (LDS/STS, not LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;
-  float* epi = reinterpret_cast<float*>(stages + STAGES * STAGE_BYTES);
-  float* col_re0 = epi + BM * EPI_PITCH;
+  float* col_re0 = reinterpret_cast<float*>(stages + STAGES * STAGE_BYTES);
   float* col_im0 = col_re0 + BN;
   uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
   uint64_t* full = bars;                 // [STAGES]
@@ -274,20 +273,23 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     }
   } else {
     // --------------------------------------------------------- epilogue --
+    // Thread r owns tile row r (TMEM lane r).  Direct tile: each thread writes
+    // its own 128-B row segments (STG.128); mirrored tile: for every column k
+    // a warp writes 32 consecutive floats of output row (j0 + k) -- both
+    // straight from registers, no shared-memory staging, no block barriers.
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int r = q * 32 + lane;               // tile row owned by this thread
     const int eid = threadIdx.x - 64;          // 0..127
     int acc = 0;
     uint32_t acc_phase = 0;
-    float mphi = 0.f, mpsi = 0.f;
-    unsigned bad = 0;
+    float mphi = 0.f, mpsi = 0.f, chk = 0.f;
     for (long long t = p.tile0 + blockIdx.x; t < p.ntiles; t += gridDim.x) {
       int I, J, mode;
       decode_tile(p, t, I, J, mode);
       const int i0 = I * BM, j0 = J * BN;
+      const int gi = i0 + r;                   // direct row / mirrored column
       float row_re0 = 0.f, row_im0 = 0.f;
       if (p.even) {
-        const int gi = i0 + r;
         if (gi < p.n1) {
           const __nv_bfloat16* ar = p.a + (long long)gi * p.ld_pack;
           row_re0 = bf2f(ar[0]) + bf2f(ar[p.split_a]);
@@ -303,7 +305,10 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         epi_bar();   // previous tile finished reading col_* vectors
         col_re0[eid] = cre;
         col_im0[eid] = cim;
+        epi_bar();
       }
+      const bool direct = (mode != kTransOnly) && gi < p.row1;
+      const bool mirror = (mode != kPlain) && gi < p.n2;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
@@ -311,75 +316,58 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       for (int plane = 0; plane < 2; ++plane) {
         float* out = plane == 0 ? p.phi : p.psi;
         const float tsign = plane == 0 ? 1.f : -1.f;
+        float mx = 0.f;
 #pragma unroll 1
         for (int c = 0; c < BN / 32; ++c) {
-          uint32_t v[32];
-          tmem_ld32(tbase + plane * 128 + c * 32, v);
-          epi_bar();  // staging buffer free
+          uint32_t u[32];
+          tmem_ld32(tbase + plane * 128 + c * 32, u);
+          float v[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(u[k]);
+          if (plane == 1 && p.even) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              v[k] -= row_im0 * col_re0[c * 32 + k] - row_re0 * col_im0[c * 32 + k];
+          }
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
-            float x = __uint_as_float(v[k]);
-            if (plane == 1 && p.even) x -= row_im0 * col_re0[c * 32 + k] - row_re0 * col_im0[c * 32 + k];
-            epi[r * EPI_PITCH + k] = x;
+            mx = fmaxf(mx, fabsf(v[k]));
+            chk = fmaf(v[k], 0.f, chk);   // NaN / Inf propagate into chk
           }
-          epi_bar();
           const int cbase = j0 + c * 32;
-          if (mode == kPlain || mode == kMirror) {
-            // direct tile: 128 rows x 32 cols, float4 along the row
-#pragma unroll 2
-            for (int it = 0; it < 8; ++it) {
-              const int idx = eid + it * 128;
-              const int rr = idx >> 3, k4 = (idx & 7) * 4;
-              const int gi = i0 + rr, gj = cbase + k4;
-              float4 w = make_float4(epi[rr * EPI_PITCH + k4], epi[rr * EPI_PITCH + k4 + 1],
-                                     epi[rr * EPI_PITCH + k4 + 2], epi[rr * EPI_PITCH + k4 + 3]);
-              const float mx = fmaxf(fmaxf(fabsf(w.x), fabsf(w.y)), fmaxf(fabsf(w.z), fabsf(w.w)));
-              if (gi < p.row1) {
-                float* dst = out + (long long)(gi - p.row0) * p.ld_out + gj;
-                if (gj + 3 < p.n2 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-                  __stcs(reinterpret_cast<float4*>(dst), w);
-                  if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
-                  bad += !(isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w));
-                } else {
-                  const float ww[4] = {w.x, w.y, w.z, w.w};
-                  for (int u = 0; u < 4; ++u)
-                    if (gj + u < p.n2) {
-                      __stcs(dst + u, ww[u]);
-                      if (plane == 0) mphi = fmaxf(mphi, fabsf(ww[u])); else mpsi = fmaxf(mpsi, fabsf(ww[u]));
-                      bad += !isfinite(ww[u]);
-                    }
-                }
-              }
+          if (mode == kDiag) {
+            // upper triangle (r <= column) direct, strict upper mirrored, async diagonal 0
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const int cc = c * 32 + k;
+              if (r == cc && plane == 1) v[k] = 0.f;
+              if (direct && r <= cc && cbase + k < p.n2)
+                __stcs(out + (long long)(gi - p.row0) * p.ld_out + cbase + k, v[k]);
+              if (mirror && r < cc && cbase + k < p.row1)
+                __stcs(out + (long long)(cbase + k - p.row0) * p.ld_out + gi, tsign * v[k]);
             }
-          } else if (mode == kDiag) {
-            for (int it = 0; it < 32; ++it) {
-              const int idx = eid + it * 128;
-              const int rr = idx >> 5, k = idx & 31;
-              const int gi = i0 + rr, gj = cbase + k, cc = c * 32 + k;
-              if (gi >= p.row1 || gj >= p.n2 || rr > cc) continue;
-              float x = epi[rr * EPI_PITCH + k];
-              if (rr == cc && plane == 1) x = 0.f;
-              __stcs(out + (long long)(gi - p.row0) * p.ld_out + gj, x);
-              if (plane == 0) mphi = fmaxf(mphi, fabsf(x)); else mpsi = fmaxf(mpsi, fabsf(x));
-              bad += !isfinite(x);
+            continue;
+          }
+          if (direct) {
+            float* dst = out + (long long)(gi - p.row0) * p.ld_out + cbase;
+            if (cbase + 31 < p.n2 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+              for (int k = 0; k < 32; k += 4)
+                __stcs(reinterpret_cast<float4*>(dst + k), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
+            } else {
+#pragma unroll
+              for (int k = 0; k < 32; ++k)
+                if (cbase + k < p.n2) __stcs(dst + k, v[k]);
             }
           }
-          if (mode != kPlain) {
-            // mirrored tile: out[j][i] = sync[i][j], -async[i][j]; rows j in this chunk
-            for (int it = 0; it < 32; ++it) {
-              const int idx = eid + it * 128;
-              const int k = idx >> 7, rr = idx & 127;
-              const int gi = cbase + k, gj = i0 + rr, cc = c * 32 + k;
-              if (gi >= p.row1 || gj >= p.n2 || (mode == kDiag && rr >= cc)) continue;
-              const float x = tsign * epi[rr * EPI_PITCH + k];
-              __stcs(out + (long long)(gi - p.row0) * p.ld_out + gj, x);
-              if (mode == kTransOnly) {
-                if (plane == 0) mphi = fmaxf(mphi, fabsf(x)); else mpsi = fmaxf(mpsi, fabsf(x));
-                bad += !isfinite(x);
-              }
-            }
+          if (mirror) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (cbase + k < p.row1)
+                __stcs(out + (long long)(cbase + k - p.row0) * p.ld_out + gi, tsign * v[k]);
           }
         }
+        if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
       }
       tc_fence_before();
       __syncwarp();
@@ -388,6 +376,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       if (acc == 0) acc_phase ^= 1;
     }
     // reductions
+    unsigned bad = (chk == 0.f) ? 0u : 1u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       mphi = fmaxf(mphi, __shfl_xor_sync(0xffffffffu, mphi, o));
