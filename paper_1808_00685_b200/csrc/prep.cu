@@ -62,8 +62,11 @@ struct PrepParams {
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a * (-i)
 
 __device__ __forceinline__ void store_pack(const PrepParams& p, void* base, long long idx, double v) {
   if (p.pack_kind == CORR2D_PACK_F64) {
@@ -77,22 +80,106 @@ __device__ __forceinline__ void store_pack(const PrepParams& p, void* base, long
   }
 }
 
+// In-register forward DFTs of length 2, 4, 8 (natural order in and out).
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+  const double2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+__device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
+  const double2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_mi(csub(x1, x3));
+  x0 = cadd(t0, t2);
+  x2 = csub(t0, t2);
+  x1 = cadd(t1, t3);
+  x3 = csub(t1, t3);
+}
+template <int R> __device__ __forceinline__ void dft_r(double2 (&x)[R]);
+template <> __device__ __forceinline__ void dft_r<2>(double2 (&x)[2]) { dft2(x[0], x[1]); }
+template <> __device__ __forceinline__ void dft_r<4>(double2 (&x)[4]) { dft4(x[0], x[1], x[2], x[3]); }
+template <> __device__ __forceinline__ void dft_r<8>(double2 (&x)[8]) {
+  constexpr double h = 0.70710678118654752440;  // sqrt(1/2)
+  dft4(x[0], x[2], x[4], x[6]);                   // evens E0..E3 in x0,x2,x4,x6
+  dft4(x[1], x[3], x[5], x[7]);                   // odds  O0..O3 in x1,x3,x5,x7
+  const double2 o1 = make_double2(h * (x[3].x + x[3].y), h * (x[3].y - x[3].x));     // W8^1 O1
+  const double2 o2 = mul_mi(x[5]);                                                  // W8^2 O2
+  const double2 o3 = make_double2(h * (x[7].y - x[7].x), -h * (x[7].x + x[7].y));    // W8^3 O3
+  const double2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6], o0 = x[1];
+  x[0] = cadd(e0, o0); x[4] = csub(e0, o0);
+  x[1] = cadd(e1, o1); x[5] = csub(e1, o1);
+  x[2] = cadd(e2, o2); x[6] = csub(e2, o2);
+  x[3] = cadd(e3, o3); x[7] = csub(e3, o3);
+}
+
+// One Stockham stage of radix R over CH interleaved columns (pairs of channels).
+//   output (j, u) = sum_t in[j + t m/R] W_m^{t k span} W_R^{t u},  k = j mod Ns
+template <int R>
+__device__ __forceinline__ void stage_r(const double2* __restrict__ in, double2* __restrict__ out,
+                                        const double2* __restrict__ tw, int m, int Ns, int CH, int CPc) {
+  const int stride = m / R, span = m / (Ns * R);
+  for (int idx = threadIdx.x; idx < stride * CH; idx += blockDim.x) {
+    const int pc = idx % CH, j = idx / CH, k = j % Ns;
+    double2 x[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) x[t] = in[(j + t * stride) * CPc + pc];
+    if (k) {
+#pragma unroll
+      for (int t = 1; t < R; ++t) x[t] = cmul(x[t], tw[t * k * span]);
+    }
+    dft_r<R>(x);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int u = 0; u < R; ++u) out[(base + u * Ns) * CPc + pc] = x[u];
+  }
+}
+
+// Any other radix (3, 5, 7, 11, ... and large primes): one output per item.
+__device__ __forceinline__ void stage_generic(const double2* __restrict__ in, double2* __restrict__ out,
+                                              const double2* __restrict__ tw, int m, int r, int Ns, int CH, int CPc) {
+  const int stride = m / r, span = m / (Ns * r);
+  for (int idx = threadIdx.x; idx < m * CH; idx += blockDim.x) {
+    const int pc = idx % CH, rest = idx / CH;
+    const int u = rest % r, j = rest / r, k = j % Ns;
+    const int e = span * (k + u * Ns);
+    double2 acc = make_double2(0.0, 0.0);
+    int q = 0;
+    for (int t = 0; t < r; ++t) {
+      const double2 x = in[(j + t * stride) * CPc + pc], w = tw[q];
+      acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
+      acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
+      q += e;
+      if (q >= m) q -= m;
+    }
+    out[((j / Ns) * Ns * r + k + u * Ns) * CPc + pc] = acc;
+  }
+}
+
+// Spectrum of channel c at bin w from the paired transform Z = FFT(x_even + i x_odd).
+__device__ __forceinline__ double2 channel_bin(const double2* X, int w, int c, int m, int CPc) {
+  const double2 z = X[w * CPc + (c >> 1)];
+  const double2 zr = X[((m - w) % m) * CPc + (c >> 1)];
+  if ((c & 1) == 0) return make_double2(0.5 * (z.x + zr.x), 0.5 * (z.y - zr.y));   // (Z + conj Zr)/2
+  return make_double2(0.5 * (z.y + zr.y), -0.5 * (z.x - zr.x));                     // (Z - conj Zr)/(2i)
+}
+
 __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) {
   extern __shared__ __align__(16) double smem[];
-  const int C = p.C, CP = C + 1, m = p.m, m_in = p.m_in;
+  const int C = p.C, CH = C / 2, CPc = CH + 1, RS = 2 * CPc;   // RS: real-view row stride
+  const int m = p.m, m_in = p.m_in;
   const int c0 = blockIdx.x * C;
   const int nc = min(C, p.n - c0);
   const int tid = threadIdx.x;
 
+  // bufA / bufB: m x CPc complex; the real view of bufA holds channel c of row k
+  // at [k * RS + c], so channels (2p, 2p+1) ARE the complex column p.
   double2* bufA = reinterpret_cast<double2*>(smem);
-  double2* bufB = bufA + (size_t)m * CP;
-  double2* tw = bufB + (size_t)m * CP;
+  double2* bufB = bufA + (size_t)m * CPc;
+  double2* tw = bufB + (size_t)m * CPc;
   double* raw_s = reinterpret_cast<double*>(tw + m);
   const bool resample = (p.resample_kind != CORR2D_RESAMPLE_NONE);
-  double* cstat = raw_s + (resample ? (size_t)m_in * CP : 0);  // [C] ref, [C] scale
+  double* cstat = raw_s + (resample ? (size_t)m_in * (C + 1) : 0);  // [C] ref, [C] scale
+  double* rv = reinterpret_cast<double*>(bufA);
 
-  // twiddles W[q] = exp(-2 pi i q / m)
-  if (p.do_fft) {
+  if (p.do_fft) {  // twiddles W[q] = exp(-2 pi i q / m)
     for (int q = tid; q < m; q += blockDim.x) {
       double s, c;
       sincospi(-2.0 * (double)q / (double)m, &s, &c);
@@ -100,7 +187,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     }
   }
 
-  // 1. load the raw m_in x nc block (coalesced row segments), count non-finite
+  // 1. load the raw m_in x C block (row segments of C channels), count non-finite
   int bad = 0;
   for (int idx = tid; idx < m_in * C; idx += blockDim.x) {
     const int r = idx / C, c = idx - r * C;
@@ -111,8 +198,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
                    : __ldg(static_cast<const double*>(p.raw) + off);
       bad += !isfinite(v);
     }
-    if (resample) raw_s[r * CP + c] = v;
-    else bufA[r * CP + c] = make_double2(v, 0.0);
+    if (resample) raw_s[r * (C + 1) + c] = v;
+    else rv[r * RS + c] = v;
   }
   bad = warp_sum(bad);
   if ((tid & 31) == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
@@ -127,22 +214,24 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         // values[idx] + frac * (values[idx + 1] - values[idx])   (preprocess.py:152)
         const int i = __ldg(p.lin_idx + k);
         const double f = __ldg(p.lin_frac + k);
-        const double v0 = raw_s[i * CP + c], v1 = raw_s[(i + 1) * CP + c];
+        const double v0 = raw_s[i * (C + 1) + c], v1 = raw_s[(i + 1) * (C + 1) + c];
         v = __dadd_rn(v0, __dmul_rn(f, __dsub_rn(v1, v0)));
       } else {
         const double* row = p.rs_mat + (size_t)k * m_in;
         double acc = 0.0;
-        for (int j = 0; j < m_in; ++j) acc = fma(__ldg(row + j), raw_s[j * CP + c], acc);
+        for (int j = 0; j < m_in; ++j) acc = fma(__ldg(row + j), raw_s[j * (C + 1) + c], acc);
         v = acc;
       }
-      bufA[k * CP + c] = make_double2(v, 0.0);
+      rv[k * RS + c] = v;
     }
     __syncthreads();
   }
 
-  // 3. per-channel reference / sigma / scale (sequential over the axis, as numpy)
+  // 3. per-channel reference / sigma / scale: left-to-right sums over the
+  //    perturbation axis (numpy's axis-0 order), loads batched ahead of the adds
   if (p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0) {
     for (int c = tid; c < nc; c += blockDim.x) {
+      const double* col = rv + c;
       double ref;
       if (p.ref_mode == CORR2D_REF_PROVIDED) {
         ref = __ldg(p.ref_in + c0 + c);
@@ -150,7 +239,15 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         ref = 0.0;
       } else {
         double s = 0.0;
-        for (int k = 0; k < m; ++k) s = __dadd_rn(s, bufA[k * CP + c].x);
+        int k = 0;
+        for (; k + 8 <= m; k += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = col[(k + u) * RS];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+        }
+        for (; k < m; ++k) s = __dadd_rn(s, col[k * RS]);
         ref = __ddiv_rn(s, (double)m);
       }
       double scale = 1.0;
@@ -160,8 +257,16 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
           sigma = __ldg(p.sigma_in + c0 + c);
         } else {
           double ss = 0.0;
-          for (int k = 0; k < m; ++k) {
-            const double d = __dsub_rn(bufA[k * CP + c].x, ref);
+          int k = 0;
+          for (; k + 8 <= m; k += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __dsub_rn(col[(k + u) * RS], ref);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) ss = __dadd_rn(ss, __dmul_rn(v[u], v[u]));
+          }
+          for (; k < m; ++k) {
+            const double d = __dsub_rn(col[k * RS], ref);
             ss = __dadd_rn(ss, __dmul_rn(d, d));
           }
           sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
@@ -183,11 +288,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     const bool scaled = p.alpha > 0.0;
     for (int idx = tid; idx < m * C; idx += blockDim.x) {
       const int k = idx / C, c = idx - k * C;
-      if (c >= nc) continue;
-      double v = bufA[k * CP + c].x;
-      if (p.ref_mode != CORR2D_REF_NONE) v = __dsub_rn(v, cstat[c]);
-      if (scaled) v = __ddiv_rn(v, cstat[C + c]);
-      bufA[k * CP + c].x = v;
+      double v = rv[k * RS + c];
+      if (c < nc) {
+        if (p.ref_mode != CORR2D_REF_NONE) v = __dsub_rn(v, cstat[c]);
+        if (scaled) v = __ddiv_rn(v, cstat[C + c]);
+      }
+      rv[k * RS + c] = v;
     }
     __syncthreads();
   }
@@ -195,39 +301,22 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   if (p.values_out) {
     for (int idx = tid; idx < m * C; idx += blockDim.x) {
       const int k = idx / C, c = idx - k * C;
-      if (c < nc) p.values_out[(long long)k * p.ld_values + c0 + c] = bufA[k * CP + c].x;
+      if (c < nc) p.values_out[(long long)k * p.ld_values + c0 + c] = rv[k * RS + c];
     }
   }
   if (!p.do_fft) return;
 
-  // 4. DFT along the perturbation axis: Stockham autosort, mixed radix.
-  //    Stage with radix r and current sub-length Ns: output (j, u) gathers
-  //    sum_t in[j + t m/r] * W[t e mod m],  e = (m / (Ns r)) (j mod Ns + u Ns).
+  // 4. DFT along the perturbation axis: two real channels per complex
+  //    transform, mixed-radix Stockham autosort (radix 8/4/2 in registers).
   double2* in = bufA;
   double2* out = bufB;
   int Ns = 1;
   for (int f = 0; f < p.nfactors; ++f) {
     const int r = p.factors[f];
-    const int stride = m / r;
-    const int span = m / (Ns * r);
-    for (int idx = tid; idx < m * C; idx += blockDim.x) {
-      const int c = idx % C;
-      const int rest = idx / C;
-      const int u = rest % r, j = rest / r;
-      const int k = j % Ns;
-      const int e = span * (k + u * Ns);
-      double2 acc = make_double2(0.0, 0.0);
-      int q = 0;
-      for (int t = 0; t < r; ++t) {
-        const double2 x = in[(j + t * stride) * CP + c];
-        const double2 w = tw[q];
-        acc.x = fma(x.x, w.x, fma(-x.y, w.y, acc.x));
-        acc.y = fma(x.x, w.y, fma(x.y, w.x, acc.y));
-        q += e;
-        if (q >= m) q -= m;
-      }
-      out[((j / Ns) * Ns * r + k + u * Ns) * CP + c] = acc;
-    }
+    if (r == 8) stage_r<8>(in, out, tw, m, Ns, CH, CPc);
+    else if (r == 4) stage_r<4>(in, out, tw, m, Ns, CH, CPc);
+    else if (r == 2) stage_r<2>(in, out, tw, m, Ns, CH, CPc);
+    else stage_generic(in, out, tw, m, r, Ns, CH, CPc);
     __syncthreads();
     double2* t = in; in = out; out = t;
     Ns *= r;
@@ -240,7 +329,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     for (int idx = tid; idx < K * C; idx += blockDim.x) {
       const int w = idx / C, c = idx - w * C;
       if (c >= nc) continue;
-      double2 v = X[w * CP + c];
+      double2 v = channel_bin(X, w, c, m, CPc);
       if (w == 0 || (even && w == m / 2)) v.y = 0.0;  // rfft: exactly real there
       reinterpret_cast<double2*>(p.half_out)[(long long)w * p.n + c0 + c] = v;
     }
@@ -256,12 +345,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         int w;
         bool re;
         if (s < K) { w = s; re = true; } else { w = s - K + 1; re = false; }
-        const double2 y = X[w * CP + c];
+        const double2 y = channel_bin(X, w, c, m, CPc);
+        const bool edge = (w == 0 || (even && w == m / 2));
         const double R = y.x;
-        const double I = (w == 0 || (even && w == m / 2)) ? 0.0 : y.y;
-        const bool dbl = !(w == 0 || (even && w == m / 2));
+        const double I = edge ? 0.0 : y.y;
         double nr = p.norm * R, ni = p.norm * I;
-        if (dbl) { nr *= 2.0; ni *= 2.0; }
+        if (!edge) { nr *= 2.0; ni *= 2.0; }
         if (re) { vphi = nr; vpsi = ni; vb = R; }
         else    { vphi = ni; vpsi = -nr; vb = I; }
       }
@@ -284,11 +373,11 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       const int c = idx / p.mp, s = idx - c * p.mp;
       double v = 0.0;
       if (s < hp) {
-        if (s < h) v = X[s * CP + c].x * (s == 0 ? sn1 : sn2);
+        if (s < h) v = channel_bin(X, s, c, m, CPc).x * (s == 0 ? sn1 : sn2);
       } else {
         const int q = s - hp;
-        if (q == 0) v = even ? X[(m / 2) * CP + c].x * sn1 : 0.0;
-        else if (q < h) v = X[q * CP + c].y * sn2;
+        if (q == 0) v = even ? channel_bin(X, m / 2, c, m, CPc).x * sn1 : 0.0;
+        else if (q < h) v = channel_bin(X, q, c, m, CPc).y * sn2;
       }
       const long long row = (long long)(c0 + c) * p.ld_pack + s;
       if (p.pack_roles & CORR2D_ROLE_A) store_pack(p, p.a_phi, row, v);
@@ -322,9 +411,9 @@ static int fft_factorize(int m, int* f, int maxf) {
 }
 
 static size_t prep_smem_bytes(int m, int m_in, int C, bool resample) {
-  const size_t CP = C + 1;
-  size_t b = 2 * (size_t)m * CP * sizeof(double2) + (size_t)m * sizeof(double2);
-  if (resample) b += (size_t)m_in * CP * sizeof(double);
+  const size_t CPc = C / 2 + 1;
+  size_t b = 2 * (size_t)m * CPc * sizeof(double2) + (size_t)m * sizeof(double2);
+  if (resample) b += (size_t)m_in * (C + 1) * sizeof(double);
   b += 2 * (size_t)C * sizeof(double);
   return b;
 }
@@ -396,9 +485,9 @@ extern "C" int corr2d_prep(
   if (p.nfactors < 0) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_prep: FFT factorisation failed");
 
   const bool resample = resample_kind != CORR2D_RESAMPLE_NONE;
-  int C = 32;
+  int C = 64;
   const size_t budget = 100 * 1024;
-  while (C > 1 && prep_smem_bytes(m, m_in, C, resample) > budget) C /= 2;
+  while (C > 2 && prep_smem_bytes(m, m_in, C, resample) > budget) C /= 2;
   size_t smem = prep_smem_bytes(m, m_in, C, resample);
   if (smem > 220 * 1024)
     return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_prep: m too large for the shared-memory FFT (m <= ~4096)");
