@@ -221,20 +221,11 @@ def dist_setup(args):
     return world, rank, local
 
 
-def tile_range(total, world, rank):
-    edges = np.linspace(0, total, world + 1).astype(np.int64)
-    return int(edges[rank]), int(edges[rank + 1])
-
-
-def homo_tile_count(n, tile):
-    T = (n + tile - 1) // tile
-    return T * (T + 1) // 2
-
-
 def run_b200(args, case, wl, world, rank, local):
     import torch
     import paper_1808_00685_b200 as P
     from paper_1808_00685_b200 import api, engine
+    from paper_1808_00685_b200.engine_core import homo_tile_count, tile_range
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)

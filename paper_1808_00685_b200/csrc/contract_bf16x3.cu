@@ -18,17 +18,21 @@
 // epilogue (rank-2 correction).
 //
 // Kernel shape: persistent, one CTA per SM, 6 warps --
-//   warp 0   : TMA producer (3-stage mbarrier ring, 64 KB/stage, SWIZZLE_64B)
+//   warp 0   : TMA producer (3-stage mbarrier ring, 64 KB/stage, SWIZZLE_64B,
+//              operands kept in L2 with an evict_last policy)
 //   warp 1   : TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2-5: epilogue (tcgen05.ld -> registers -> global stores: own-row
-//              STG.128 for the tile, warp-coalesced columns for its mirror,
-//              fused max|.| / finite check)
+//   warps 2-5: epilogue: tcgen05.ld (16-column chunks) -> registers ->
+//              swizzled smem staging -> TMA bulk-tensor stores of the tile
+//              AND of its mirrored transpose (evict_first), fused max|.| /
+//              finite check; diagonal tiles use masked register stores.
 // TMEM holds two accumulator sets (sync 128 + async 128 columns each) so the
 // epilogue of tile t overlaps the MMAs of tile t+1.
 #include "common.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cstring>
 
 namespace corr2d {
 namespace tc {
@@ -39,9 +43,13 @@ constexpr int KB = 32;                  // slots per k-block (64 B rows, SWIZZLE
 constexpr int STAGES = 3;
 constexpr int TILE_BYTES = BM * KB * 2; // 8 KB: one (operand, half, plane) tile
 constexpr int STAGE_BYTES = 8 * TILE_BYTES;
+constexpr int CH = 16;                  // epilogue chunk: 16 output columns
+constexpr int STG_DIRECT = BM * CH * 4; // 8 KB: 128 rows x 64 B, SWIZZLE_64B
+constexpr int STG_MIRROR = CH * BM * 4; // 8 KB: 16 rows x 512 B
+constexpr int STG_BYTES = 2 * (STG_DIRECT + STG_MIRROR);
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 2 * BN * 4 + 16 * 8 + 16;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 2 * BN * 4 + 16 * 8 + 16;
 
 // kTransOnly: a tile left of the shard's diagonal square is computed as its
 // globally-upper mirror (operand tiles swapped) and only the transpose is
@@ -49,7 +57,7 @@ constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 2 * 
 enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2, kTransOnly = 3 };
 
 struct Params {
-  int n1, n2, hp, homo, even;
+  int n1, n2, hp, homo, even, tma_store;
   int row0, row1, I0, I1, T;
   long long tile0, ntiles;  // tiles [tile0, ntiles) of the enumeration
   const __nv_bfloat16* a;
@@ -59,6 +67,10 @@ struct Params {
   float* psi;
   long long ld_out;
   unsigned long long* stats;
+};
+
+struct OutMaps {  // TMA maps of the output planes: [plane][direct, mirror]
+  CUtensorMap m[2][2];
 };
 
 // ------------------------------------------------------------- PTX helpers --
@@ -82,12 +94,36 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "bra LAB_WAIT;\n\t"
       "DONE:\n\t}\n" ::"r"(su32(bar)), "r"(parity) : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
+                                            uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
-      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n"
+      ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(src)), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -119,18 +155,15 @@ __host__ __device__ constexpr uint32_t idesc_bf16(bool neg_a) {
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
@@ -165,12 +198,13 @@ __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float
 
 __global__ void __launch_bounds__(THREADS, 1)
 contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                       const Params p) {
+                       const __grid_constant__ OutMaps outm, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // keep the shared address space visible to the compiler (LDS/STS, not LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;
-  float* col_re0 = reinterpret_cast<float*>(stages + STAGES * STAGE_BYTES);
+  uint8_t* staging = stages + STAGES * STAGE_BYTES;  // [2] x {direct 8 KB, mirror 8 KB}
+  float* col_re0 = reinterpret_cast<float*>(staging + STG_BYTES);
   float* col_im0 = col_re0 + BN;
   uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
   uint64_t* full = bars;                 // [STAGES]
@@ -201,6 +235,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer --
     if (lane == 0) {
+      const uint64_t keep = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (long long t = p.tile0 + blockIdx.x; t < p.ntiles; t += gridDim.x) {
@@ -211,14 +246,14 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           uint8_t* base = stages + stage * STAGE_BYTES;
           const int kre = kb * KB, kim = p.hp + kb * KB;
-          tma_load_3d(base + 0 * TILE_BYTES, &tmap_a, kre, I * BM, 0, &full[stage]);
-          tma_load_3d(base + 1 * TILE_BYTES, &tmap_a, kre, I * BM, 1, &full[stage]);
-          tma_load_3d(base + 2 * TILE_BYTES, &tmap_a, kim, I * BM, 0, &full[stage]);
-          tma_load_3d(base + 3 * TILE_BYTES, &tmap_a, kim, I * BM, 1, &full[stage]);
-          tma_load_3d(base + 4 * TILE_BYTES, &tmap_b, kre, J * BN, 0, &full[stage]);
-          tma_load_3d(base + 5 * TILE_BYTES, &tmap_b, kre, J * BN, 1, &full[stage]);
-          tma_load_3d(base + 6 * TILE_BYTES, &tmap_b, kim, J * BN, 0, &full[stage]);
-          tma_load_3d(base + 7 * TILE_BYTES, &tmap_b, kim, J * BN, 1, &full[stage]);
+          tma_load_3d(base + 0 * TILE_BYTES, &tmap_a, kre, I * BM, 0, &full[stage], keep);
+          tma_load_3d(base + 1 * TILE_BYTES, &tmap_a, kre, I * BM, 1, &full[stage], keep);
+          tma_load_3d(base + 2 * TILE_BYTES, &tmap_a, kim, I * BM, 0, &full[stage], keep);
+          tma_load_3d(base + 3 * TILE_BYTES, &tmap_a, kim, I * BM, 1, &full[stage], keep);
+          tma_load_3d(base + 4 * TILE_BYTES, &tmap_b, kre, J * BN, 0, &full[stage], keep);
+          tma_load_3d(base + 5 * TILE_BYTES, &tmap_b, kre, J * BN, 1, &full[stage], keep);
+          tma_load_3d(base + 6 * TILE_BYTES, &tmap_b, kim, J * BN, 0, &full[stage], keep);
+          tma_load_3d(base + 7 * TILE_BYTES, &tmap_b, kim, J * BN, 1, &full[stage], keep);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -273,15 +308,19 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     }
   } else {
     // --------------------------------------------------------- epilogue --
-    // Thread r owns tile row r (TMEM lane r).  Direct tile: each thread writes
-    // its own 128-B row segments (STG.128); mirrored tile: for every column k
-    // a warp writes 32 consecutive floats of output row (j0 + k) -- both
-    // straight from registers, no shared-memory staging, no block barriers.
+    // Thread r owns tile row r (TMEM lane r).  Per 16-column chunk it stages
+    // its 16 values twice in shared memory -- as row r of the direct box
+    // (SWIZZLE_64B, 4 conflict-free STS.128) and as column r of the mirrored
+    // box (16 rows x 512 B, consecutive lanes -> consecutive words) -- then one
+    // thread issues the two TMA stores.  Two staging buffers alternate so the
+    // next chunk is written while the bulk-store engine drains the previous.
     const int q = warp & 3;                    // TMEM lane quadrant of this warp
     const int r = q * 32 + lane;               // tile row owned by this thread
     const int eid = threadIdx.x - 64;          // 0..127
+    const uint64_t drop = policy_evict_first();
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t chunk_no = 0;
     float mphi = 0.f, mpsi = 0.f, chk = 0.f;
     for (long long t = p.tile0 + blockIdx.x; t < p.ntiles; t += gridDim.x) {
       int I, J, mode;
@@ -309,6 +348,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       }
       const bool direct = (mode != kTransOnly) && gi < p.row1;
       const bool mirror = (mode != kPlain) && gi < p.n2;
+      const bool use_tma = p.tma_store && mode != kDiag;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
@@ -318,28 +358,58 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         const float tsign = plane == 0 ? 1.f : -1.f;
         float mx = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld32(tbase + plane * 128 + c * 32, u);
-          float v[32];
+        for (int c = 0; c < BN / CH; ++c) {
+          uint32_t u[16];
+          tmem_ld16(tbase + plane * 128 + c * CH, u);
+          tmem_wait_ld();
+          float v[16];
 #pragma unroll
-          for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(u[k]);
+          for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(u[k]);
           if (plane == 1 && p.even) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k)
-              v[k] -= row_im0 * col_re0[c * 32 + k] - row_re0 * col_im0[c * 32 + k];
+            for (int k = 0; k < 16; ++k)
+              v[k] -= row_im0 * col_re0[c * CH + k] - row_re0 * col_im0[c * CH + k];
           }
 #pragma unroll
-          for (int k = 0; k < 32; ++k) {
+          for (int k = 0; k < 16; ++k) {
             mx = fmaxf(mx, fabsf(v[k]));
             chk = fmaf(v[k], 0.f, chk);   // NaN / Inf propagate into chk
           }
-          const int cbase = j0 + c * 32;
+          const int cbase = j0 + c * CH;
+          if (use_tma) {
+            const int buf = chunk_no & 1;
+            uint8_t* sd = staging + buf * (STG_DIRECT + STG_MIRROR);
+            float* sm_mirror = reinterpret_cast<float*>(sd + STG_DIRECT);
+            if (eid == 0) bulk_wait_read<1>();   // this buffer's previous stores have read smem
+            epi_bar();
+            if (mode != kTransOnly) {
+              // direct box row r: 4 x 16 B chunks, swizzled chunk index j ^ ((r >> 1) & 3)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int pj = j ^ ((r >> 1) & 3);
+                *reinterpret_cast<float4*>(sd + r * 64 + pj * 16) =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              }
+            }
+            if (mode != kPlain) {   // mirrored box: sync^T, -async^T
+#pragma unroll
+              for (int k = 0; k < 16; ++k) sm_mirror[k * BM + r] = tsign * v[k];
+            }
+            fence_async_smem();
+            epi_bar();
+            if (eid == 0) {
+              if (mode != kTransOnly) tma_store_2d(&outm.m[plane][0], sd, cbase, i0 - p.row0, drop);
+              if (mode != kPlain) tma_store_2d(&outm.m[plane][1], sm_mirror, i0, cbase - p.row0, drop);
+              bulk_commit();
+            }
+            ++chunk_no;
+            continue;
+          }
           if (mode == kDiag) {
             // upper triangle (r <= column) direct, strict upper mirrored, async diagonal 0
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const int cc = c * 32 + k;
+            for (int k = 0; k < 16; ++k) {
+              const int cc = c * CH + k;
               if (r == cc && plane == 1) v[k] = 0.f;
               if (direct && r <= cc && cbase + k < p.n2)
                 __stcs(out + (long long)(gi - p.row0) * p.ld_out + cbase + k, v[k]);
@@ -349,20 +419,13 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             continue;
           }
           if (direct) {
-            float* dst = out + (long long)(gi - p.row0) * p.ld_out + cbase;
-            if (cbase + 31 < p.n2 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
-              for (int k = 0; k < 32; k += 4)
-                __stcs(reinterpret_cast<float4*>(dst + k), make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]));
-            } else {
-#pragma unroll
-              for (int k = 0; k < 32; ++k)
-                if (cbase + k < p.n2) __stcs(dst + k, v[k]);
-            }
+            for (int k = 0; k < 16; ++k)
+              if (cbase + k < p.n2) __stcs(out + (long long)(gi - p.row0) * p.ld_out + cbase + k, v[k]);
           }
           if (mirror) {
 #pragma unroll
-            for (int k = 0; k < 32; ++k)
+            for (int k = 0; k < 16; ++k)
               if (cbase + k < p.row1)
                 __stcs(out + (long long)(cbase + k - p.row0) * p.ld_out + gi, tsign * v[k]);
           }
@@ -375,6 +438,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (eid == 0) bulk_wait_all();
     // reductions
     unsigned bad = (chk == 0.f) ? 0u : 1u;
 #pragma unroll
@@ -410,7 +474,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static int make_map(CUtensorMap* map, const void* base, long long ld, long long rows, long long split) {
+static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows, long long split) {
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 2};
@@ -421,6 +485,22 @@ static int make_map(CUtensorMap* map, const void* base, long long ld, long long 
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return CORR2D_OK;
+}
+
+// Output plane (rows x cols fp32, leading dimension ld): direct box 16 x 128
+// (SWIZZLE_64B) or mirror box 128 x 16 (no swizzle).
+static int make_output_map(CUtensorMap* map, float* base, long long ld, long long rows, long long cols, bool mirror) {
+  auto fn = encode_fn();
+  if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {mirror ? (cuuint32_t)BM : (cuuint32_t)CH, mirror ? (cuuint32_t)CH : (cuuint32_t)BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, mirror ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed (" + std::to_string((int)r) + ")");
   return CORR2D_OK;
 }
 
@@ -458,10 +538,26 @@ extern "C" int corr2d_contract_bf16x3(
   p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
   CUtensorMap ma, mb;
-  int rc = make_map(&ma, a, ld_pack, n1, split_a);
+  int rc = make_operand_map(&ma, a, ld_pack, n1, split_a);
   if (rc) return rc;
-  rc = make_map(&mb, b, ld_pack, n2, split_b);
+  rc = make_operand_map(&mb, b, ld_pack, n2, split_b);
   if (rc) return rc;
+  // TMA stores need 16-byte aligned planes and a leading dimension that is a
+  // multiple of 4 floats; otherwise the epilogue stores from registers.
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
+  const bool aligned = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(phi) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(psi) & 15) == 0);
+  p.tma_store = 0;
+  if (aligned) {
+    const long long rows = row1 - row0;
+    float* planes[2] = {phi, psi};
+    rc = 0;
+    for (int pl = 0; pl < 2 && !rc; ++pl)
+      for (int mi = 0; mi < 2 && !rc; ++mi) rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, mi == 1);
+    if (rc) return rc;
+    p.tma_store = 1;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -471,6 +567,6 @@ extern "C" int corr2d_contract_bf16x3(
   const long long work = p.ntiles - p.tile0;
   if (work == 0) return CORR2D_OK;
   const long long grid = work < sms ? work : sms;
-  contract_bf16x3_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, p);
+  contract_bf16x3_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, om, p);
   return check_launch("contract_bf16x3_kernel");
 }

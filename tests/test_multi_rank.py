@@ -1,0 +1,106 @@
+"""Multi-rank logic on the CPU: the tile-range partition used by bench.py for
+N GPUs (every output element written exactly once, by exactly one rank), the
+row-shard partition of correlate_ft(rows=...), and the torch.distributed
+plumbing (world_size 2, gloo, 127.0.0.1)."""
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1808_00685_b200.engine_core import (DIAG, MIRROR, PLAIN, TRANS_ONLY, homo_tile_count,
+                                               homo_tile_decode, tile_aligned_blocks, tile_range)
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def coverage(n, tile, row0, row1, tiles):
+    """Count how often each output element of rows [row0, row1) is written
+    by the tiles `tiles` of the shard's enumeration (kernel semantics)."""
+    cnt = np.zeros((n, n), dtype=np.int32)
+    for b in tiles:
+        I, J, mode = homo_tile_decode(b, n, tile, row0, row1)
+        i0, j0 = I * tile, J * tile
+        for r in range(tile):
+            for c in range(tile):
+                gi, gj = i0 + r, j0 + c
+                if mode != TRANS_ONLY and gi < row1 and gj < n and (mode != DIAG or r <= c):
+                    cnt[gi, gj] += 1
+                if mode in (MIRROR, DIAG, TRANS_ONLY) and gj < row1 and gj >= row0 and gi < n and (mode != DIAG or r < c):
+                    cnt[gj, gi] += 1
+    return cnt
+
+
+@pytest.mark.parametrize("n,tile", [(64, 16), (70, 16), (33, 8)])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_tile_ranges_cover_map_exactly_once(n, tile, world):
+    total = homo_tile_count(n, tile)
+    acc = np.zeros((n, n), dtype=np.int32)
+    for rank in range(world):
+        t0, t1 = tile_range(total, world, rank)
+        acc += coverage(n, tile, 0, n, range(t0, t1))
+    assert np.all(acc == 1)
+
+
+@pytest.mark.parametrize("n,tile,parts", [(70, 16, 2), (64, 16, 4), (33, 8, 3)])
+def test_row_shards_cover_their_rows_exactly_once(n, tile, parts):
+    for row0, row1 in tile_aligned_blocks(n, parts, tile):
+        total = homo_tile_count(n, tile, row0, row1)
+        cnt = coverage(n, tile, row0, row1, range(total))
+        assert np.all(cnt[row0:row1] == 1)
+        assert np.all(cnt[:row0] == 0) and np.all(cnt[row1:] == 0)
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    sys.path.insert(0, str(ROOT))
+    import bench
+    total = homo_tile_count(32768, 128)
+    t0, t1 = tile_range(total, world, rank)
+    mine = torch.tensor([t1 - t0], dtype=torch.int64)
+    dist.all_reduce(mine)
+    mx = bench.allreduce_max(float(rank + 1) * 1.5, world)
+    bench.barrier(world)
+    if rank == 0:
+        out.put((int(mine.item()), total, mx))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_partition_and_max_over_ranks():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    covered, total, mx = q.get(timeout=5)
+    assert covered == total
+    assert mx == 3.0
+
+
+def test_reference_arm_under_torchrun_prints_one_line():
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29617", str(ROOT / "bench.py"),
+           "--impl", "reference", "--gpus", "2", "--config", "1", "--steps", "1", "--warmup", "0"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
