@@ -225,7 +225,7 @@ def run_b200(args, case, wl, world, rank, local):
     import torch
     import paper_1808_00685_b200 as P
     from paper_1808_00685_b200 import api, engine
-    from paper_1808_00685_b200.engine_core import homo_tile_count, tile_range
+    from paper_1808_00685_b200.engine_core import tile_range
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -238,15 +238,10 @@ def run_b200(args, case, wl, world, rank, local):
     spec = P.PreprocessSpec(
         resample=None if case.resample is None else P.ResampleSpec(case.resample, P.InterpolantKind.from_name(case.interpolant)),
         scaling_exponent=case.alpha)
-    tile = 128 if case.dtype == "float32" else 64
-    tiles = None
-    if world > 1 and case.homo:
-        tiles = tile_range(homo_tile_count(wl["n1"], tile), world, rank)
-    elif world > 1:
-        tiles = tile_range(((wl["n1"] + tile - 1) // tile) * ((wl["n2"] + tile - 1) // tile), world, rank)
     plan, homo = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev)
-    if tiles is not None:
-        plan.tile0, plan.tile1 = tiles
+    if world > 1:
+        # equal contiguous share of the contraction kernel's own tile enumeration
+        plan.tile0, plan.tile1 = tile_range(plan.tile_count(), world, rank)
     stream = torch.cuda.current_stream()
 
     # ---- parity gate before timing (bench.py:98-115 style): sampled rows vs the oracle

@@ -145,6 +145,17 @@ int corr2d_contract_bf16x3(
     int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
+/*
+ * Number of tiles in the enumeration corr2d_contract_f64 / _bf16x3 would use for
+ * this call (the [tile0, tile1) range of the contract calls indexes it): the
+ * unit of the multi-GPU tile-range partition.  -1 on bad arguments.  For
+ * pack_kind BF16X2 and a whole-map call with ld_out % 4 == 0 this is the
+ * 2-SM (CTA-pair) enumeration; CORR2D_BF16_1SM=1 in the environment forces the
+ * 1-SM kernel.
+ */
+int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int row0, int row1,
+                                   int64_t ld_out);
+
 #ifdef __cplusplus
 }
 #endif

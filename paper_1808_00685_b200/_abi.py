@@ -28,6 +28,7 @@ INT32_MAX = 2**31 - 1
 EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
+    "corr2d_contract_tile_count",
 )
 
 
@@ -65,6 +66,8 @@ def _declare(lib):
         c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
         c_i64, c_i64, c_void, c_void, c_i64, c_void, c_void,
     ]
+    lib.corr2d_contract_tile_count.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_i64]
+    lib.corr2d_contract_tile_count.restype = c_i64
     for name in ("corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
                  "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors"):
         getattr(lib, name).restype = c_int

@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 namespace corr2d {
@@ -462,6 +463,402 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   }
 }
 
+// =====================================================================
+// 2-SM variant: a CTA pair (cluster of 2) issues tcgen05.mma.cta_group::2
+// with M = 256 (128 rows per CTA) and N = 256 = [sync cols | async cols] of
+// one 128-channel column tile:
+//   x: A_re x [B_re ; -B_im]  -> [ A_re.B_re | -A_re.B_im ]
+//   y: A_im x [B_im ;  B_re]  -> [ A_im.B_im |  A_im.B_re ]
+// CTA0 holds the first half of each B operand (B_re, B_im), CTA1 the second
+// (-B_im, B_re; the negated copy is the third "half" of the packed row), so
+// each SM reads 8 KB of shared memory per 128-cycle MMA (64 B/cycle, half of
+// the 1-SM M=128/N=128 shape) and both planes come out of one accumulator.
+// =====================================================================
+
+struct Params2 {
+  int n1, n2, hp, homo, even, tma_store;
+  int T1, T2;             // 128-row / 128-col tile counts
+  long long tile0, tile1; // pair-tile range
+  const __nv_bfloat16* a;
+  const __nv_bfloat16* b;
+  long long ld_pack, split_a, split_b;
+  float* phi;
+  float* psi;
+  long long ld_out;
+  unsigned long long* stats;
+};
+
+enum PairMode { kSkip = 4 };
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t num_clusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(out) : "r"(saddr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(cluster_addr), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                uint32_t leader_bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 msk;\n\tmov.b16 msk, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], msk;\n\t}\n"
+      ::"r"(su32(bar)) : "memory");
+}
+// M = 256 (pair), N = 256
+__host__ __device__ constexpr uint32_t idesc_bf16_2sm() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+// Grouped raster order: row pairs are taken kGroup at a time and, inside a
+// group, column tiles J are walked in order with the group's pairs
+// consecutive -- concurrent clusters then share a handful of B column tiles
+// and the group's A rows stay L2-resident (the plain row-major triangle
+// re-streamed every B tile from DRAM once per row pair).
+constexpr int kGroup = 16;
+
+// pair-tile b -> (row-pair P, column tile J); per-CTA mode for row tile 2P + rank.
+// Homo: row pair P covers columns J in [2P, T); inside group g (pairs gG..gG+Gg-1)
+// columns 2gG + 2k + e (k < Gg-1, e in {0,1}) hold the k+1 pairs gG..gG+k (ramp),
+// later columns hold all Gg pairs.  Mirrored in engine_core.pair_tile_decode.
+__device__ __forceinline__ void decode_pair(const Params2& p, long long b, uint32_t rank, int& P, int& J, int& mode) {
+  const long long G = kGroup;
+  const long long npairs = (p.T1 + 1) / 2;
+  if (!p.homo) {
+    const long long g = b / (G * p.T2);
+    const long long Gg = (npairs - g * G < G) ? npairs - g * G : G;
+    const long long o = b - g * G * p.T2;
+    J = (int)(o / Gg);
+    P = (int)(g * G + o % Gg);
+    mode = (2 * P + (int)rank < p.T1) ? kPlain : kSkip;
+    return;
+  }
+  const long long T = p.T2;
+  const long long ngroups = (npairs + G - 1) / G;
+  // S(g) = g G (T - G + 1) - G^2 g (g - 1): tiles in the full groups before g
+  auto S = [&](long long g) { return g * G * (T - G + 1) - G * G * g * (g - 1); };
+  const double A2 = (double)(G * G), B1 = (double)(G * (T - G + 1) + G * G);
+  const double disc = B1 * B1 - 4.0 * A2 * (double)b;
+  long long g = (long long)floor((B1 - sqrt(fmax(disc, 0.0))) / (2.0 * A2));
+  if (g < 0) g = 0;
+  if (g > ngroups - 1) g = ngroups - 1;
+  while (g > 0 && S(g) > b) --g;
+  while (g + 1 < ngroups && S(g + 1) <= b) ++g;
+  const long long Gg = (npairs - g * G < G) ? npairs - g * G : G;
+  const long long o = b - S(g);
+  const long long ramp = (Gg - 1) * Gg;
+  if (o < ramp) {
+    long long k = (long long)floor((sqrt(4.0 * (double)o + 1.0) - 1.0) * 0.5);
+    while (k > 0 && k * (k + 1) > o) --k;
+    while ((k + 1) * (k + 2) <= o) ++k;
+    const long long rem = o - k * (k + 1);
+    J = (int)(2 * g * G + 2 * k + rem / (k + 1));
+    P = (int)(g * G + rem % (k + 1));
+  } else {
+    const long long o2 = o - ramp;
+    J = (int)(2 * g * G + 2 * (Gg - 1) + o2 / Gg);
+    P = (int)(g * G + o2 % Gg);
+  }
+  const int i = 2 * P + (int)rank;
+  if (i >= p.T1 || J < i) mode = kSkip;
+  else mode = (J == i) ? kDiag : kMirror;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                           const __grid_constant__ OutMaps outm, const Params2 p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* stages = smem;
+  uint8_t* staging = stages + STAGES * STAGE_BYTES;
+  float* col_re0 = reinterpret_cast<float*>(staging + STG_BYTES);
+  float* col_im0 = col_re0 + BN;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
+  uint64_t* full = bars;                 // [STAGES] (used in the leader)
+  uint64_t* empty = bars + STAGES;       // [STAGES]
+  uint64_t* tfull = bars + 2 * STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2] (used in the leader)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const long long cid = cluster_id_x(), ncl = num_clusters_x();
+  const int nkb = p.hp / KB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------- TMA producer (both CTAs) --
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
+        int P, J, mode;
+        decode_pair(p, t, rank, P, J, mode);
+        const int arow = (2 * P + (int)rank) * BM, brow = J * BN;
+        // CTA0: Bx = Re', By = Im'    CTA1: Bx = -Im', By = Re'
+        const int kx = leader ? 0 : 2 * p.hp, ky = leader ? p.hp : 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t lbar = mapa_rank(su32(&full[stage]), 0);
+          mbar_expect_tx_remote(lbar, STAGE_BYTES);
+          uint8_t* base = stages + stage * STAGE_BYTES;
+          const int k0 = kb * KB;
+          tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
+          tma_load_3d_2sm(base + 1 * TILE_BYTES, &tmap_a, k0, arow, 1, lbar, keep);
+          tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 0, lbar, keep);
+          tma_load_3d_2sm(base + 3 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 1, lbar, keep);
+          tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, kx + k0, brow, 0, lbar, keep);
+          tma_load_3d_2sm(base + 5 * TILE_BYTES, &tmap_b, kx + k0, brow, 1, lbar, keep);
+          tma_load_3d_2sm(base + 6 * TILE_BYTES, &tmap_b, ky + k0, brow, 0, lbar, keep);
+          tma_load_3d_2sm(base + 7 * TILE_BYTES, &tmap_b, ky + k0, brow, 1, lbar, keep);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------- MMA issuer (leader) --
+    if (leader) {
+      constexpr uint32_t ID = idesc_bf16_2sm();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * 256;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t base = su32(stages + stage * STAGE_BYTES);
+#pragma unroll
+            for (int ks = 0; ks < KB / 16; ++ks) {
+              const uint32_t off = ks * 32;
+              const uint64_t are_h = desc_sw64(base + 0 * TILE_BYTES + off), are_l = desc_sw64(base + 1 * TILE_BYTES + off);
+              const uint64_t aim_h = desc_sw64(base + 2 * TILE_BYTES + off), aim_l = desc_sw64(base + 3 * TILE_BYTES + off);
+              const uint64_t bx_h = desc_sw64(base + 4 * TILE_BYTES + off), bx_l = desc_sw64(base + 5 * TILE_BYTES + off);
+              const uint64_t by_h = desc_sw64(base + 6 * TILE_BYTES + off), by_l = desc_sw64(base + 7 * TILE_BYTES + off);
+              const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+              umma2_bf16(d, are_h, bx_h, ID, acc0);
+              umma2_bf16(d, are_h, bx_l, ID, 1);
+              umma2_bf16(d, are_l, bx_h, ID, 1);
+              umma2_bf16(d, aim_h, by_h, ID, 1);
+              umma2_bf16(d, aim_h, by_l, ID, 1);
+              umma2_bf16(d, aim_l, by_h, ID, 1);
+            }
+            umma2_commit_both(&empty[stage]);
+            if (kb == nkb - 1) umma2_commit_both(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ----------------------------------------------- epilogue (both CTAs) --
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int eid = threadIdx.x - 64;
+    const uint64_t drop = policy_evict_first();
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    uint32_t chunk_no = 0;
+    float mphi = 0.f, mpsi = 0.f, chk = 0.f;
+    for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
+      int P, J, mode;
+      decode_pair(p, t, rank, P, J, mode);
+      const int i0 = (2 * P + (int)rank) * BM, j0 = J * BN;
+      const int gi = i0 + r;
+      if (mode != kSkip) {
+        float row_re0 = 0.f, row_im0 = 0.f;
+        if (p.even) {
+          if (gi < p.n1) {
+            const __nv_bfloat16* ar = p.a + (long long)gi * p.ld_pack;
+            row_re0 = bf2f(ar[0]) + bf2f(ar[p.split_a]);
+            row_im0 = bf2f(ar[p.hp]) + bf2f(ar[p.hp + p.split_a]);
+          }
+          const int gj = j0 + eid;
+          float cre = 0.f, cim = 0.f;
+          if (gj < p.n2) {
+            const __nv_bfloat16* br = p.b + (long long)gj * p.ld_pack;
+            cre = bf2f(br[0]) + bf2f(br[p.split_b]);
+            cim = bf2f(br[p.hp]) + bf2f(br[p.hp + p.split_b]);
+          }
+          epi_bar();
+          col_re0[eid] = cre;
+          col_im0[eid] = cim;
+          epi_bar();
+        }
+        const bool direct = gi < p.n1;
+        const bool mirror = (mode != kPlain) && gi < p.n2;
+        const bool use_tma = p.tma_store && mode != kDiag;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+#pragma unroll 1
+        for (int plane = 0; plane < 2; ++plane) {
+          float* out = plane == 0 ? p.phi : p.psi;
+          const float tsign = plane == 0 ? 1.f : -1.f;
+          float mx = 0.f;
+#pragma unroll 1
+          for (int c = 0; c < BN / CH; ++c) {
+            uint32_t u[16];
+            tmem_ld16(tbase + plane * 128 + c * CH, u);
+            tmem_wait_ld();
+            float v[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(u[k]);
+            if (plane == 1 && p.even) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                v[k] -= row_im0 * col_re0[c * CH + k] - row_re0 * col_im0[c * CH + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              mx = fmaxf(mx, fabsf(v[k]));
+              chk = fmaf(v[k], 0.f, chk);
+            }
+            const int cbase = j0 + c * CH;
+            if (use_tma) {
+              const int buf = chunk_no & 1;
+              uint8_t* sd = staging + buf * (STG_DIRECT + STG_MIRROR);
+              float* sm_mirror = reinterpret_cast<float*>(sd + STG_DIRECT);
+              if (eid == 0) bulk_wait_read<1>();
+              epi_bar();
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int pj = j ^ ((r >> 1) & 3);
+                *reinterpret_cast<float4*>(sd + r * 64 + pj * 16) =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              }
+              if (mode != kPlain) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) sm_mirror[k * BM + r] = tsign * v[k];
+              }
+              fence_async_smem();
+              epi_bar();
+              if (eid == 0) {
+                tma_store_2d(&outm.m[plane][0], sd, cbase, i0, drop);
+                if (mode != kPlain) tma_store_2d(&outm.m[plane][1], sm_mirror, i0, cbase, drop);
+                bulk_commit();
+              }
+              ++chunk_no;
+              continue;
+            }
+            if (mode == kDiag) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const int cc = c * CH + k;
+                if (r == cc && plane == 1) v[k] = 0.f;
+                if (direct && r <= cc && cbase + k < p.n2)
+                  __stcs(out + (long long)gi * p.ld_out + cbase + k, v[k]);
+                if (mirror && r < cc && cbase + k < p.n1)
+                  __stcs(out + (long long)(cbase + k) * p.ld_out + gi, tsign * v[k]);
+              }
+              continue;
+            }
+            if (direct) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                if (cbase + k < p.n2) __stcs(out + (long long)gi * p.ld_out + cbase + k, v[k]);
+            }
+            if (mirror) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                if (cbase + k < p.n1) __stcs(out + (long long)(cbase + k) * p.ld_out + gi, tsign * v[k]);
+            }
+          }
+          if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
+        }
+      } else {
+        mbar_wait(&tfull[acc], acc_phase);   // lower-triangle half of a pair tile: nothing to write
+        tc_fence_after();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(mapa_rank(su32(&tempty[acc]), 0));
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (eid == 0) bulk_wait_all();
+    unsigned bad = (chk == 0.f) ? 0u : 1u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mphi = fmaxf(mphi, __shfl_xor_sync(0xffffffffu, mphi, o));
+      mpsi = fmaxf(mpsi, __shfl_xor_sync(0xffffffffu, mpsi, o));
+      bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if (lane == 0) {
+      atomic_max_abs(&p.stats[0], (double)mphi);
+      atomic_max_abs(&p.stats[1], (double)mpsi);
+      if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -509,6 +906,37 @@ static int make_output_map(CUtensorMap* map, float* base, long long ld, long lon
 
 using namespace corr2d;
 
+static bool use_2sm(int n1, int row0, int row1, bool tma_ok) {
+  const char* env = getenv("CORR2D_BF16_1SM");
+  if (env && env[0] == '1') return false;
+  return tma_ok && row0 == 0 && row1 == n1;
+}
+
+static long long tiles_1sm(int n1, int n2, int homo, int row0, int row1) {
+  using namespace corr2d::tc;
+  const long long T = (n2 + BN - 1) / BN;
+  const long long R = (row1 + BM - 1) / BM - row0 / BM;
+  return homo ? R * T - R * (R - 1) / 2 : R * T;
+}
+
+static long long tiles_2sm(int n1, int n2, int homo) {
+  using namespace corr2d::tc;
+  const long long T1 = (n1 + BM - 1) / BM, T2 = (n2 + BN - 1) / BN;
+  const long long P = (T1 + 1) / 2;
+  return homo ? P * T2 - P * (P - 1) : P * T2;
+}
+
+extern "C" int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int row0, int row1,
+                                              int64_t ld_out) {
+  if (n1 < 1 || n2 < 1 || row0 < 0 || row1 > n1 || row0 >= row1) return -1;
+  if (pack_kind == CORR2D_PACK_F64) {
+    const long long T = (n2 + 63) / 64, R = (row1 + 63) / 64 - row0 / 64;
+    return homo ? R * T - R * (R - 1) / 2 : R * T;
+  }
+  if (use_2sm(n1, row0, row1, ld_out % 4 == 0)) return tiles_2sm(n1, n2, homo);
+  return tiles_1sm(n1, n2, homo, row0, row1);
+}
+
 extern "C" int corr2d_contract_bf16x3(
     const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
     int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
@@ -516,8 +944,8 @@ extern "C" int corr2d_contract_bf16x3(
   using namespace corr2d::tc;
   if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: null pointer");
   if (n1 < 1 || n2 < 1 || m < 2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad sizes");
-  if (mp != corr2d_packed_depth(m, CORR2D_PACK_BF16X2) || ld_pack < mp || (ld_pack % 64) != 0)
-    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: packed depth / ld_pack mismatch (ld_pack % 64 == 0)");
+  if (mp != corr2d_packed_depth(m, CORR2D_PACK_BF16X2) || ld_pack < mp || (ld_pack % 32) != 0)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: packed depth / ld_pack mismatch (ld_pack % 32 == 0)");
   if (split_a < (long long)n1 * ld_pack || split_b < (long long)n2 * ld_pack || (split_a % 8) || (split_b % 8))
     return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad plane split");
   if (row0 < 0 || row1 > n1 || row0 >= row1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad row range");
@@ -525,18 +953,6 @@ extern "C" int corr2d_contract_bf16x3(
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: homo needs n1 == n2");
   if (row0 % BM != 0 || (row1 != n1 && row1 % BM != 0))
     return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: row shard bounds must be multiples of 128 (or n1)");
-  Params p{};
-  p.n1 = n1; p.n2 = n2; p.hp = mp / 2; p.homo = homo; p.even = (m % 2) == 0;
-  p.row0 = row0; p.row1 = row1; p.I0 = row0 / BM; p.I1 = (row1 + BM - 1) / BM; p.T = (n2 + BN - 1) / BN;
-  const long long R = p.I1 - p.I0;
-  const long long total = homo ? R * p.T - R * (R - 1) / 2 : R * p.T;
-  if (tile1 < 0 || tile1 > total) tile1 = total;
-  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad tile range");
-  p.tile0 = tile0;
-  p.ntiles = tile1;
-  p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
-  p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
-  p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
   CUtensorMap ma, mb;
   int rc = make_operand_map(&ma, a, ld_pack, n1, split_a);
   if (rc) return rc;
@@ -548,24 +964,46 @@ extern "C" int corr2d_contract_bf16x3(
   memset(&om, 0, sizeof(om));
   const bool aligned = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(phi) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(psi) & 15) == 0);
-  p.tma_store = 0;
   if (aligned) {
     const long long rows = row1 - row0;
     float* planes[2] = {phi, psi};
-    rc = 0;
     for (int pl = 0; pl < 2 && !rc; ++pl)
       for (int mi = 0; mi < 2 && !rc; ++mi) rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, mi == 1);
     if (rc) return rc;
-    p.tma_store = 1;
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute(contract_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
-  const long long work = p.ntiles - p.tile0;
+  const bool two_sm = use_2sm(n1, row0, row1, aligned);
+  const long long total = two_sm ? tiles_2sm(n1, n2, homo) : tiles_1sm(n1, n2, homo, row0, row1);
+  if (tile1 < 0 || tile1 > total) tile1 = total;
+  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad tile range");
+  const long long work = tile1 - tile0;
   if (work == 0) return CORR2D_OK;
+  if (two_sm) {
+    Params2 p{};
+    p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = 1;
+    p.T1 = (n1 + BM - 1) / BM; p.T2 = (n2 + BN - 1) / BN;
+    p.tile0 = tile0; p.tile1 = tile1;
+    p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
+    p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
+    p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
+    cudaFuncSetAttribute(contract_bf16x3_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    const long long clusters = work < sms / 2 ? work : sms / 2;
+    contract_bf16x3_2sm_kernel<<<(unsigned)(2 * clusters), THREADS, SMEM_BYTES, st>>>(ma, mb, om, p);
+    return check_launch("contract_bf16x3_2sm_kernel");
+  }
+  Params p{};
+  p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = aligned ? 1 : 0;
+  p.row0 = row0; p.row1 = row1; p.I0 = row0 / BM; p.I1 = (row1 + BM - 1) / BM; p.T = (n2 + BN - 1) / BN;
+  p.tile0 = tile0;
+  p.ntiles = tile1;
+  p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
+  p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
+  p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
+  cudaFuncSetAttribute(contract_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   const long long grid = work < sms ? work : sms;
   contract_bf16x3_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, om, p);
   return check_launch("contract_bf16x3_kernel");

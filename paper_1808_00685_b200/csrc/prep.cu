@@ -188,18 +188,35 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   }
 
   // 1. load the raw m_in x C block (row segments of C channels), count non-finite
+  //    (8 independent loads in flight per thread before the shared stores)
   int bad = 0;
-  for (int idx = tid; idx < m_in * C; idx += blockDim.x) {
-    const int r = idx / C, c = idx - r * C;
-    double v = 0.0;
-    if (c < nc) {
-      const long long off = (long long)r * p.ld_raw + c0 + c;
-      v = p.in_f32 ? (double)__ldg(static_cast<const float*>(p.raw) + off)
-                   : __ldg(static_cast<const double*>(p.raw) + off);
-      bad += !isfinite(v);
+  constexpr int U = 8;
+  const int total_in = m_in * C;
+  for (int base = tid; base < total_in; base += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * blockDim.x;
+      v[u] = 0.0;
+      if (idx < total_in) {
+        const int r = idx / C, c = idx - r * C;
+        if (c < nc) {
+          const long long off = (long long)r * p.ld_raw + c0 + c;
+          v[u] = p.in_f32 ? (double)__ldg(static_cast<const float*>(p.raw) + off)
+                          : __ldg(static_cast<const double*>(p.raw) + off);
+        }
+      }
     }
-    if (resample) raw_s[r * (C + 1) + c] = v;
-    else rv[r * RS + c] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < total_in) {
+        const int r = idx / C, c = idx - r * C;
+        bad += !isfinite(v[u]);
+        if (resample) raw_s[r * (C + 1) + c] = v[u];
+        else rv[r * RS + c] = v[u];
+      }
+    }
   }
   bad = warp_sum(bad);
   if ((tid & 31) == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
@@ -362,11 +379,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, vb);
     }
   }
-  // 5b. bf16 pair layout (see corr2d.h): [Re' | Im'] halves of hp slots each,
+  // 5b. bf16 layout (see corr2d.h): [Re' | Im' | -Im'] thirds of hp slots each,
   //     Re'[s] = R_s (s < h), Im'[0] = R_{m/2} (even m) or 0, Im'[s] = I_s,
-  //     every slot scaled by sqrt(Norm * weight) so A and B share one format.
+  //     every slot scaled by sqrt(Norm * weight) so A and B share one format;
+  //     the negated copy feeds the conj() half of the 2-SM N=256 MMA.
   if (p.pack_kind == CORR2D_PACK_BF16X2) {
-    const int hp = p.mp / 2;
+    const int hp = p.mp / 3;
     const int h = even ? m / 2 : (m + 1) / 2;
     const double sn1 = sqrt(p.norm), sn2 = sqrt(2.0 * p.norm);
     for (int idx = tid; idx < nc * p.mp; idx += blockDim.x) {
@@ -375,9 +393,10 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       if (s < hp) {
         if (s < h) v = channel_bin(X, s, c, m, CPc).x * (s == 0 ? sn1 : sn2);
       } else {
-        const int q = s - hp;
+        const int q = (s < 2 * hp) ? s - hp : s - 2 * hp;
         if (q == 0) v = even ? channel_bin(X, m / 2, c, m, CPc).x * sn1 : 0.0;
         else if (q < h) v = channel_bin(X, q, c, m, CPc).y * sn2;
+        if (s >= 2 * hp) v = -v;
       }
       const long long row = (long long)(c0 + c) * p.ld_pack + s;
       if (p.pack_roles & CORR2D_ROLE_A) store_pack(p, p.a_phi, row, v);
@@ -435,7 +454,7 @@ extern "C" int corr2d_packed_depth(int m, int pack_kind) {
   if (m < 2) return fail(CORR2D_ERR_DATA, "need m >= 2");
   if (pack_kind == CORR2D_PACK_BF16X2) {
     const int h = (m % 2 == 0) ? m / 2 : (m + 1) / 2;
-    return 2 * ((h + 31) / 32 * 32);
+    return 3 * ((h + 31) / 32 * 32);
   }
   return (m + 3) / 4 * 4;
 }

@@ -302,6 +302,15 @@ class CorrelationPlan:
         self.raw1, self.raw2 = raw1, raw2
         return self
 
+    def tile_count(self) -> int:
+        """Tiles in the contraction kernel's enumeration for this plan (the unit
+        of the multi-GPU tile-range partition; include/corr2d.h)."""
+        n = self.lib.corr2d_contract_tile_count(self.pack_kind, self.n1, self.n2, 1 if self.homo else 0,
+                                                self.row0, self.row1, self.n2)
+        if n < 0:
+            raise DataError("bad contraction shape")
+        return int(n)
+
     @property
     def launches_per_step(self) -> int:
         """Kernels of ours one launch() enqueues: K1 per dataset + K2."""

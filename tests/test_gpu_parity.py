@@ -223,3 +223,34 @@ def test_fp32_path_small():
         sc = scale_of(s, a)
         assert rel_err(res.sync, s, sc) <= TOL32 and rel_err(res.asyn, a, sc) <= TOL32
         assert np.array_equal(res.sync, res.sync.T) and np.array_equal(res.asyn, -res.asyn.T)
+
+
+def test_fp32_tile_ranges_and_both_tensor_core_kernels(monkeypatch):
+    """Tile-range partition (multi-GPU unit) is bit-identical to the whole map,
+    for the 2-SM (CTA pair) kernel and the 1-SM kernel; both match the oracle."""
+    from paper_1808_00685_b200 import engine
+    from paper_1808_00685_b200.engine_core import tile_range
+    rng = np.random.default_rng(21)
+    v = rng.normal(size=(64, 700))
+    s, a, _ = O.correlate_ft(v)
+    sc = scale_of(s, a)
+    for one_sm in ("0", "1"):
+        monkeypatch.setenv("CORR2D_BF16_1SM", one_sm)
+        d = dyn_from_values(v)
+        full = P.correlate_ft(d, dtype="float32")
+        assert rel_err(full.sync, s, sc) <= TOL32 and rel_err(full.asyn, a, sc) <= TOL32
+        assert np.array_equal(full.sync, full.sync.T) and np.array_equal(full.asyn, -full.asyn.T)
+        recipe = engine.PrepRecipe(m_in=64, m=64, ref_mode=P._abi.REF_NONE)
+        plan = engine.CorrelationPlan(n1=700, n2=700, m=64, recipe1=recipe, recipe2=None,
+                                      norm=1.0 / (np.pi * 63), dtype="float32", want_ref=False)
+        plan.bind(d.device_values(plan.dev))
+        plan.launch_prep_only()
+        total = plan.tile_count()
+        plan.phi.zero_()
+        plan.psi.zero_()
+        for rank in range(3):
+            plan.tile0, plan.tile1 = tile_range(total, 3, rank)
+            plan.launch_contract()
+        engine.sync()
+        assert np.array_equal(plan.phi.cpu().numpy(), full.sync)
+        assert np.array_equal(plan.psi.cpu().numpy(), full.asyn)

@@ -104,3 +104,45 @@ def test_reference_arm_under_torchrun_prints_one_line():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def pair_coverage(n1, n2, tile, homo, tiles, G):
+    from paper_1808_00685_b200.engine_core import SKIP, pair_tile_decode
+    T1, T2 = -(-n1 // tile), -(-n2 // tile)
+    cnt = np.zeros((n1, n2), dtype=np.int32)
+    for b in tiles:
+        for rank in (0, 1):
+            P, J, mode = pair_tile_decode(b, T1, T2, homo, rank, G)
+            if mode == SKIP:
+                continue
+            i0, j0 = (2 * P + rank) * tile, J * tile
+            r, c = np.meshgrid(np.arange(tile), np.arange(tile), indexing="ij")
+            gi, gj = i0 + r, j0 + c
+            ok = (gi < n1) & (gj < n2)
+            direct = ok & ((r <= c) if mode == DIAG else True)
+            cnt[gi[direct], gj[direct]] += 1
+            if mode in (MIRROR, DIAG):
+                mir = ok & ((r < c) if mode == DIAG else True) & (gj < n1) & (gi < n2)
+                cnt[gj[mir], gi[mir]] += 1
+    return cnt
+
+
+@pytest.mark.parametrize("n,tile,G", [(64, 8, 2), (72, 8, 3), (40, 8, 16), (130, 8, 4)])
+@pytest.mark.parametrize("world", [1, 3])
+def test_pair_tiles_cover_homo_map_once(n, tile, G, world):
+    from paper_1808_00685_b200.engine_core import pair_tile_count
+    T = -(-n // tile)
+    total = pair_tile_count(T, T, True)
+    acc = np.zeros((n, n), dtype=np.int32)
+    for rank in range(world):
+        t0, t1 = tile_range(total, world, rank)
+        acc += pair_coverage(n, n, tile, True, range(t0, t1), G)
+    assert np.all(acc == 1)
+
+
+@pytest.mark.parametrize("n1,n2,G", [(64, 40, 2), (72, 24, 16), (24, 72, 3)])
+def test_pair_tiles_cover_hetero_map_once(n1, n2, G):
+    from paper_1808_00685_b200.engine_core import pair_tile_count
+    T1, T2 = -(-n1 // 8), -(-n2 // 8)
+    acc = pair_coverage(n1, n2, 8, False, range(pair_tile_count(T1, T2, False)), G)
+    assert np.all(acc == 1)
