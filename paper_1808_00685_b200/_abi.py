@@ -8,6 +8,7 @@ raises :class:`BackendUnavailable` with the reason.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -79,7 +80,8 @@ def load(path: Path | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # CORR2D_LIB: load an alternative build (experiments only)
+        p = Path(path) if path else Path(os.environ.get("CORR2D_LIB", LIB_PATH))
         if not p.exists():
             raise BackendUnavailable(
                 f"{p} is not built; run `python -m paper_1808_00685_b200.build` "

@@ -41,7 +41,10 @@ namespace tc {
 constexpr int BM = 128;                 // output rows per tile (TMEM lanes)
 constexpr int BN = 128;                 // output cols per tile
 constexpr int KB = 32;                  // slots per k-block (64 B rows, SWIZZLE_64B)
-constexpr int STAGES = 3;
+#ifndef CORR2D_BF16_STAGES
+#define CORR2D_BF16_STAGES 3
+#endif
+constexpr int STAGES = CORR2D_BF16_STAGES;
 constexpr int TILE_BYTES = BM * KB * 2; // 8 KB: one (operand, half, plane) tile
 constexpr int STAGE_BYTES = 8 * TILE_BYTES;
 constexpr int CH = 16;                  // epilogue chunk: 16 output columns
@@ -104,6 +107,14 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
   return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t store_policy(int kind) {
+  return kind == 0 ? policy_evict_first() : (kind == 1 ? policy_evict_normal() : policy_evict_last());
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar,
                                             uint64_t pol) {
@@ -196,6 +207,102 @@ __device__ __forceinline__ void decode_tile(const Params& p, long long b, int& I
 }
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// Per-warp epilogue staging: the warp owning TMEM lanes 32q..32q+31 stages its
+// 32 rows x 16 columns twice -- as the direct box (32 rows x 64 B, SWIZZLE_64B:
+// 16-B chunk j of row l lands at j ^ ((l >> 1) & 3), conflict-free STS.128) and
+// as the mirrored box (16 rows x 128 B, lane-contiguous STS.32) -- and lane 0
+// issues the TMA stores.  Two buffers alternate; only __syncwarp, no CTA barrier.
+constexpr int WSTG_DIRECT = 32 * CH * 4;                   // 2 KB
+constexpr int WSTG_MIRROR = CH * 32 * 4;                   // 2 KB
+constexpr int WSTG = 2 * (WSTG_DIRECT + WSTG_MIRROR);      // 8 KB per epilogue warp
+static_assert(4 * WSTG == STG_BYTES, "staging budget");
+
+__device__ __forceinline__ void warp_store_chunk(uint8_t* wstg, uint32_t& chunk_no, const float (&v)[16], int lane,
+                                                 bool do_direct, bool do_mirror, float tsign,
+                                                 const CUtensorMap* map_direct, const CUtensorMap* map_mirror,
+                                                 int dcol, int drow, int mcol, int mrow, uint64_t pol) {
+  uint8_t* sd = wstg + (chunk_no & 1) * (WSTG_DIRECT + WSTG_MIRROR);
+  float* smir = reinterpret_cast<float*>(sd + WSTG_DIRECT);
+  if (lane == 0) bulk_wait_read<1>();   // this buffer's previous stores have read it
+  __syncwarp();
+  if (do_direct) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int pj = j ^ ((lane >> 1) & 3);
+      *reinterpret_cast<float4*>(sd + lane * 64 + pj * 16) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+  }
+  if (do_mirror) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) smir[k * 32 + lane] = tsign * v[k];
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (do_direct) tma_store_2d(map_direct, sd, dcol, drow, pol);
+    if (do_mirror) tma_store_2d(map_mirror, smir, mcol, mrow, pol);
+    bulk_commit();
+  }
+  ++chunk_no;
+}
+
+// Both planes of one 16-column chunk in one go (2-SM epilogue): one 8 KB
+// per-warp buffer {sync direct, async direct, sync mirror, async mirror}, one
+// proxy fence and up to four TMA stores.  The buffer is reused only after the
+// previous chunk's stores have read it (by then the next TMEM loads and the
+// arithmetic of this chunk have already hidden that latency).
+__device__ __forceinline__ void stage_and_store_pair(uint8_t* wst, int lane, const float (&vp)[16], const float (&vs)[16],
+                                                     bool mirror, const OutMaps& om, int cbase, int row0q, uint64_t pol) {
+  uint8_t* dphi = wst;
+  uint8_t* dpsi = wst + WSTG_DIRECT;
+  float* mphi = reinterpret_cast<float*>(wst + 2 * WSTG_DIRECT);
+  float* mpsi = reinterpret_cast<float*>(wst + 2 * WSTG_DIRECT + WSTG_MIRROR);
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int off = lane * 64 + (j ^ ((lane >> 1) & 3)) * 16;
+    *reinterpret_cast<float4*>(dphi + off) = make_float4(vp[4 * j], vp[4 * j + 1], vp[4 * j + 2], vp[4 * j + 3]);
+    *reinterpret_cast<float4*>(dpsi + off) = make_float4(vs[4 * j], vs[4 * j + 1], vs[4 * j + 2], vs[4 * j + 3]);
+  }
+  if (mirror) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      mphi[k * 32 + lane] = vp[k];
+      mpsi[k * 32 + lane] = -vs[k];
+    }
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(&om.m[0][0], dphi, cbase, row0q, pol);
+    tma_store_2d(&om.m[1][0], dpsi, cbase, row0q, pol);
+    if (mirror) {
+      tma_store_2d(&om.m[0][1], mphi, row0q, cbase, pol);
+      tma_store_2d(&om.m[1][1], mpsi, row0q, cbase, pol);
+    }
+    bulk_commit();
+  }
+}
+
+// sync chunk c -> u[0..15], async chunk c -> u[16..31]
+__device__ __forceinline__ void tmem_ld16x2(uint32_t tbase, int c, uint32_t (&u)[32]) {
+  uint32_t (&lo)[16] = *reinterpret_cast<uint32_t(*)[16]>(&u[0]);
+  uint32_t (&hi)[16] = *reinterpret_cast<uint32_t(*)[16]>(&u[16]);
+  tmem_ld16(tbase + c * CH, lo);
+  tmem_ld16(tbase + 128 + c * CH, hi);
+}
+// tcgen05.wait::ld with the loaded registers as in/out operands, so no use of
+// them can be scheduled before the wait.
+__device__ __forceinline__ void tmem_wait_ld_tie(uint32_t (&u)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
+                 "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15]),
+                 "+r"(u[16]), "+r"(u[17]), "+r"(u[18]), "+r"(u[19]), "+r"(u[20]), "+r"(u[21]), "+r"(u[22]), "+r"(u[23]),
+                 "+r"(u[24]), "+r"(u[25]), "+r"(u[26]), "+r"(u[27]), "+r"(u[28]), "+r"(u[29]), "+r"(u[30]), "+r"(u[31])
+               :: "memory");
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
 contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
@@ -378,32 +485,9 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           }
           const int cbase = j0 + c * CH;
           if (use_tma) {
-            const int buf = chunk_no & 1;
-            uint8_t* sd = staging + buf * (STG_DIRECT + STG_MIRROR);
-            float* sm_mirror = reinterpret_cast<float*>(sd + STG_DIRECT);
-            if (eid == 0) bulk_wait_read<1>();   // this buffer's previous stores have read smem
-            epi_bar();
-            if (mode != kTransOnly) {
-              // direct box row r: 4 x 16 B chunks, swizzled chunk index j ^ ((r >> 1) & 3)
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int pj = j ^ ((r >> 1) & 3);
-                *reinterpret_cast<float4*>(sd + r * 64 + pj * 16) =
-                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-              }
-            }
-            if (mode != kPlain) {   // mirrored box: sync^T, -async^T
-#pragma unroll
-              for (int k = 0; k < 16; ++k) sm_mirror[k * BM + r] = tsign * v[k];
-            }
-            fence_async_smem();
-            epi_bar();
-            if (eid == 0) {
-              if (mode != kTransOnly) tma_store_2d(&outm.m[plane][0], sd, cbase, i0 - p.row0, drop);
-              if (mode != kPlain) tma_store_2d(&outm.m[plane][1], sm_mirror, i0, cbase - p.row0, drop);
-              bulk_commit();
-            }
-            ++chunk_no;
+            warp_store_chunk(staging + q * WSTG, chunk_no, v, lane, mode != kTransOnly, mode != kPlain, tsign,
+                             &outm.m[plane][0], &outm.m[plane][1], cbase, i0 + 32 * q - p.row0,
+                             i0 + 32 * q, cbase - p.row0, drop);
             continue;
           }
           if (mode == kDiag) {
@@ -439,7 +523,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (eid == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
     // reductions
     unsigned bad = (chk == 0.f) ? 0u : 1u;
 #pragma unroll
@@ -477,6 +561,8 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
 
 struct Params2 {
   int n1, n2, hp, homo, even, tma_store;
+  int store_pol;          // L2 policy of the output stores: 0 evict_first, 1 normal, 2 evict_last
+  int dbg;                // profiling switches: 1 = no output stores, 2 = no MMAs (results invalid)
   int T1, T2;             // 128-row / 128-col tile counts
   long long tile0, tile1; // pair-tile range
   const __nv_bfloat16* a;
@@ -693,6 +779,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               const uint64_t bx_h = desc_sw64(base + 4 * TILE_BYTES + off), bx_l = desc_sw64(base + 5 * TILE_BYTES + off);
               const uint64_t by_h = desc_sw64(base + 6 * TILE_BYTES + off), by_l = desc_sw64(base + 7 * TILE_BYTES + off);
               const uint32_t acc0 = (kb | ks) ? 1u : 0u;
+              if (p.dbg & 2) continue;
               umma2_bf16(d, are_h, bx_h, ID, acc0);
               umma2_bf16(d, are_h, bx_l, ID, 1);
               umma2_bf16(d, are_l, bx_h, ID, 1);
@@ -715,7 +802,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const int eid = threadIdx.x - 64;
-    const uint64_t drop = policy_evict_first();
+    const uint64_t drop = store_policy(p.store_pol);
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t chunk_no = 0;
@@ -751,6 +838,41 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
+        if (use_tma) {
+          // Software pipeline over 16-column chunks: the TMEM loads of chunk c+1
+          // (sync and async) are in flight while chunk c is corrected, reduced,
+          // staged and handed to the TMA store engine.
+          uint8_t* wst = staging + q * WSTG;
+          const bool mir = mode != kPlain;
+          auto process = [&](const uint32_t (&u)[32], int c) {
+            float vp[16], vs[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) { vp[k] = __uint_as_float(u[k]); vs[k] = __uint_as_float(u[16 + k]); }
+            if (p.even) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) vs[k] -= row_im0 * col_re0[c * CH + k] - row_re0 * col_im0[c * CH + k];
+            }
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+              mphi = fmaxf(mphi, fabsf(vp[k]));
+              mpsi = fmaxf(mpsi, fabsf(vs[k]));
+              chk = fmaf(vp[k], 0.f, fmaf(vs[k], 0.f, chk));
+            }
+            const int cbase = j0 + c * CH;
+            if (!(p.dbg & 1)) stage_and_store_pair(wst, lane, vp, vs, mir, outm, cbase, i0 + 32 * q, drop);
+          };
+          uint32_t ua[32], ub[32];
+          tmem_ld16x2(tbase, 0, ua);
+#pragma unroll 1
+          for (int c = 0; c < BN / CH; c += 2) {
+            tmem_wait_ld_tie(ua);
+            tmem_ld16x2(tbase, c + 1, ub);
+            process(ua, c);
+            tmem_wait_ld_tie(ub);
+            if (c + 2 < BN / CH) tmem_ld16x2(tbase, c + 2, ua);
+            process(ub, c + 1);
+          }
+        } else
 #pragma unroll 1
         for (int plane = 0; plane < 2; ++plane) {
           float* out = plane == 0 ? p.phi : p.psi;
@@ -775,32 +897,6 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               chk = fmaf(v[k], 0.f, chk);
             }
             const int cbase = j0 + c * CH;
-            if (use_tma) {
-              const int buf = chunk_no & 1;
-              uint8_t* sd = staging + buf * (STG_DIRECT + STG_MIRROR);
-              float* sm_mirror = reinterpret_cast<float*>(sd + STG_DIRECT);
-              if (eid == 0) bulk_wait_read<1>();
-              epi_bar();
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int pj = j ^ ((r >> 1) & 3);
-                *reinterpret_cast<float4*>(sd + r * 64 + pj * 16) =
-                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-              }
-              if (mode != kPlain) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) sm_mirror[k * BM + r] = tsign * v[k];
-              }
-              fence_async_smem();
-              epi_bar();
-              if (eid == 0) {
-                tma_store_2d(&outm.m[plane][0], sd, cbase, i0, drop);
-                if (mode != kPlain) tma_store_2d(&outm.m[plane][1], sm_mirror, i0, cbase, drop);
-                bulk_commit();
-              }
-              ++chunk_no;
-              continue;
-            }
             if (mode == kDiag) {
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
@@ -836,7 +932,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (eid == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_all();
     unsigned bad = (chk == 0.f) ? 0u : 1u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -886,13 +982,13 @@ static int make_operand_map(CUtensorMap* map, const void* base, long long ld, lo
 }
 
 // Output plane (rows x cols fp32, leading dimension ld): direct box 16 x 128
-// (SWIZZLE_64B) or mirror box 128 x 16 (no swizzle).
+// (SWIZZLE_64B) or mirror box 32 x 16 (no swizzle), one box per epilogue warp.
 static int make_output_map(CUtensorMap* map, float* base, long long ld, long long rows, long long cols, bool mirror) {
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {mirror ? (cuuint32_t)BM : (cuuint32_t)CH, mirror ? (cuuint32_t)CH : (cuuint32_t)BM};
+  cuuint32_t box[2] = {mirror ? 32u : (cuuint32_t)CH, mirror ? (cuuint32_t)CH : 32u};   // per-warp boxes
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, mirror ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -985,6 +1081,10 @@ extern "C" int corr2d_contract_bf16x3(
   if (two_sm) {
     Params2 p{};
     p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = 1;
+    const char* sp = getenv("CORR2D_STORE_POLICY");
+    p.store_pol = sp ? atoi(sp) : 0;
+    const char* dbg = getenv("CORR2D_DEBUG_SKIP");
+    p.dbg = dbg ? atoi(dbg) : 0;
     p.T1 = (n1 + BM - 1) / BM; p.T2 = (n2 + BN - 1) / BN;
     p.tile0 = tile0; p.tile1 = tile1;
     p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);

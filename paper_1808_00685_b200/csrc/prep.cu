@@ -25,6 +25,7 @@
 namespace corr2d {
 
 constexpr int kPrepThreads = 256;
+constexpr int kSeqStatsMax = 128;  // longest axis summed strictly left to right
 constexpr int kMaxFactors = 24;
 
 struct PrepParams {
@@ -244,10 +245,25 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     __syncthreads();
   }
 
-  // 3. per-channel reference / sigma / scale: left-to-right sums over the
-  //    perturbation axis (numpy's axis-0 order), loads batched ahead of the adds
+  // 3. per-channel reference / sigma / scale.  For m <= kSeqStatsMax one thread
+  //    per channel sums left to right over the perturbation axis (numpy's
+  //    axis-0 order: values / reference / sigma match the reference bit for
+  //    bit); longer axes use one warp per channel (strided partial sums + a
+  //    fixed xor tree: deterministic, within a few ulp of numpy).
   if (p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0) {
-    for (int c = tid; c < nc; c += blockDim.x) {
+    const bool wide = m > kSeqStatsMax;
+    const int lanes = wide ? 32 : 1;
+    const int lane = wide ? (tid & 31) : 0;
+    const int worker = wide ? (tid >> 5) : tid;
+    const int nworkers = wide ? (int)(blockDim.x >> 5) : (int)blockDim.x;
+    auto reduce = [&](double s) {
+      if (wide) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+      }
+      return s;
+    };
+    for (int c = worker; c < nc; c += nworkers) {
       const double* col = rv + c;
       double ref;
       if (p.ref_mode == CORR2D_REF_PROVIDED) {
@@ -256,16 +272,9 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         ref = 0.0;
       } else {
         double s = 0.0;
-        int k = 0;
-        for (; k + 8 <= m; k += 8) {
-          double v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = col[(k + u) * RS];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
-        }
-        for (; k < m; ++k) s = __dadd_rn(s, col[k * RS]);
-        ref = __ddiv_rn(s, (double)m);
+#pragma unroll 8
+        for (int k = lane; k < m; k += lanes) s = __dadd_rn(s, col[k * RS]);
+        ref = __ddiv_rn(reduce(s), (double)m);
       }
       double scale = 1.0;
       if (p.alpha > 0.0) {
@@ -274,20 +283,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
           sigma = __ldg(p.sigma_in + c0 + c);
         } else {
           double ss = 0.0;
-          int k = 0;
-          for (; k + 8 <= m; k += 8) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = __dsub_rn(col[(k + u) * RS], ref);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) ss = __dadd_rn(ss, __dmul_rn(v[u], v[u]));
-          }
-          for (; k < m; ++k) {
+#pragma unroll 8
+          for (int k = lane; k < m; k += lanes) {
             const double d = __dsub_rn(col[k * RS], ref);
             ss = __dadd_rn(ss, __dmul_rn(d, d));
           }
-          sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
+          sigma = __dsqrt_rn(__ddiv_rn(reduce(ss), (double)(m - 1)));
         }
+        if (lane != 0) continue;
         if (p.sigma_out) p.sigma_out[c0 + c] = sigma;  // before substitution
         if (sigma == 0.0) {
           atomicAdd(&p.status[CORR2D_ST_ZEROVAR], 1);
@@ -297,6 +300,7 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         // numpy's power fast paths: x**0.5 -> sqrt, x**1 -> x
         scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
       }
+      if (lane != 0) continue;
       if (p.ref_out) p.ref_out[c0 + c] = ref;
       cstat[c] = ref;
       cstat[C + c] = scale;
@@ -384,23 +388,43 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   //     every slot scaled by sqrt(Norm * weight) so A and B share one format;
   //     the negated copy feeds the conj() half of the 2-SM N=256 MMA.
   if (p.pack_kind == CORR2D_PACK_BF16X2) {
+    // one item = 4 consecutive slots q..q+3 of one channel: each bin is read
+    // once and written as 8-byte (4 x bf16) vectors into the 3 thirds x 2 planes
     const int hp = p.mp / 3;
     const int h = even ? m / 2 : (m + 1) / 2;
     const double sn1 = sqrt(p.norm), sn2 = sqrt(2.0 * p.norm);
-    for (int idx = tid; idx < nc * p.mp; idx += blockDim.x) {
-      const int c = idx / p.mp, s = idx - c * p.mp;
-      double v = 0.0;
-      if (s < hp) {
-        if (s < h) v = channel_bin(X, s, c, m, CPc).x * (s == 0 ? sn1 : sn2);
-      } else {
-        const int q = (s < 2 * hp) ? s - hp : s - 2 * hp;
-        if (q == 0) v = even ? channel_bin(X, m / 2, c, m, CPc).x * sn1 : 0.0;
-        else if (q < h) v = channel_bin(X, q, c, m, CPc).y * sn2;
-        if (s >= 2 * hp) v = -v;
+    const int q4n = hp / 4;
+    for (int idx = tid; idx < nc * q4n; idx += blockDim.x) {
+      const int c = idx / q4n, q0 = (idx - c * q4n) * 4;
+      // [third][plane] x 4 slots
+      __align__(8) __nv_bfloat16 v[3][2][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u;
+        double vr = 0.0, vi = 0.0;
+        if (q < h) {
+          const double2 y = channel_bin(X, q, c, m, CPc);
+          vr = y.x * (q == 0 ? sn1 : sn2);
+          vi = (q == 0) ? (even ? channel_bin(X, m / 2, c, m, CPc).x * sn1 : 0.0) : y.y * sn2;
+        }
+        const __nv_bfloat16 rh = __double2bfloat16(vr), ih = __double2bfloat16(vi);
+        const __nv_bfloat16 rl = __double2bfloat16(vr - (double)__bfloat162float(rh));
+        const __nv_bfloat16 il = __double2bfloat16(vi - (double)__bfloat162float(ih));
+        v[0][0][u] = rh; v[0][1][u] = rl;
+        v[1][0][u] = ih; v[1][1][u] = il;
+        v[2][0][u] = __hneg(ih); v[2][1][u] = __hneg(il);
       }
-      const long long row = (long long)(c0 + c) * p.ld_pack + s;
-      if (p.pack_roles & CORR2D_ROLE_A) store_pack(p, p.a_phi, row, v);
-      if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, v);
+      const long long o = (long long)(c0 + c) * p.ld_pack + q0;
+      auto put = [&](void* base) {
+        __nv_bfloat16* b = static_cast<__nv_bfloat16*>(base);
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3)
+#pragma unroll
+          for (int pl = 0; pl < 2; ++pl)
+            *reinterpret_cast<uint2*>(b + o + t3 * hp + pl * p.split_plane) = *reinterpret_cast<const uint2*>(v[t3][pl]);
+      };
+      if (p.pack_roles & CORR2D_ROLE_A) put(p.a_phi);
+      if (p.pack_roles & CORR2D_ROLE_B) put(p.b);
     }
   }
 }

@@ -32,8 +32,12 @@ def test_homo_pipeline_matches_reference(name):
     g = golden(name)
     ds = P.SpectralDataset(g["nu"], g["t"], g["raw"])
     dyn = P.preprocess_dataset(ds)
-    assert np.array_equal(dyn.reference_used, g["ref"])      # sequential mean, bitwise
-    assert np.array_equal(dyn.values, g["values"])
+    if ds.m <= 128:   # left-to-right mean over the axis: bitwise equal to numpy
+        assert np.array_equal(dyn.reference_used, g["ref"])
+        assert np.array_equal(dyn.values, g["values"])
+    else:             # warp-parallel sums for long axes: a few ulp
+        assert rel_err(dyn.reference_used, g["ref"]) <= 1e-14
+        assert rel_err(dyn.values, g["values"]) <= 1e-14
     ws = P.dft_channels(dyn)
     assert rel_err(ws.half_spectrum1, g["half"]) <= 1e-13
     assert np.all(ws.half_spectrum1[0].imag == 0)
