@@ -354,14 +354,11 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           uint8_t* base = stages + stage * STAGE_BYTES;
           const int kre = kb * KB, kim = p.hp + kb * KB;
+          // each box carries both planes: hi tile then lo tile, contiguous
           tma_load_3d(base + 0 * TILE_BYTES, &tmap_a, kre, I * BM, 0, &full[stage], keep);
-          tma_load_3d(base + 1 * TILE_BYTES, &tmap_a, kre, I * BM, 1, &full[stage], keep);
           tma_load_3d(base + 2 * TILE_BYTES, &tmap_a, kim, I * BM, 0, &full[stage], keep);
-          tma_load_3d(base + 3 * TILE_BYTES, &tmap_a, kim, I * BM, 1, &full[stage], keep);
           tma_load_3d(base + 4 * TILE_BYTES, &tmap_b, kre, J * BN, 0, &full[stage], keep);
-          tma_load_3d(base + 5 * TILE_BYTES, &tmap_b, kre, J * BN, 1, &full[stage], keep);
           tma_load_3d(base + 6 * TILE_BYTES, &tmap_b, kim, J * BN, 0, &full[stage], keep);
-          tma_load_3d(base + 7 * TILE_BYTES, &tmap_b, kim, J * BN, 1, &full[stage], keep);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -686,7 +683,82 @@ __device__ __forceinline__ void decode_pair(const Params2& p, long long b, uint3
   else mode = (J == i) ? kDiag : kMirror;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+// NPAIR = 2: a cluster of two CTA pairs computing pair tiles (P, 2Jp) and
+// (P, 2Jp+1) -- the same A rows -- so the A operand is TMA-multicast from the
+// first pair's CTAs into both pairs (25 % less L2 -> SM operand traffic).
+// Cluster tile b -> (row pair P, column-pair Jp), grouped raster order as
+// decode_pair(), triangle Jp >= P for homo.  Mirrored in engine_core.quad_tile_decode.
+__device__ __forceinline__ void decode_quad(const Params2& p, long long b, int& P, int& Jp) {
+  const long long G = kGroup;
+  const long long npairs = (p.T1 + 1) / 2, T2p = (p.T2 + 1) / 2;
+  if (!p.homo) {
+    const long long g = b / (G * T2p);
+    const long long Gg = (npairs - g * G < G) ? npairs - g * G : G;
+    const long long o = b - g * G * T2p;
+    Jp = (int)(o / Gg);
+    P = (int)(g * G + o % Gg);
+    return;
+  }
+  const long long ngroups = (npairs + G - 1) / G;
+  auto S = [&](long long g) { return g * G * T2p - G * G * g * (g - 1) / 2 - g * G * (G - 1) / 2; };
+  const double A2 = 0.5 * (double)(G * G), B1 = (double)(G * T2p) + 0.5 * (double)(G * G) - 0.5 * (double)(G * (G - 1));
+  const double disc = B1 * B1 - 4.0 * A2 * (double)b;
+  long long g = (long long)floor((B1 - sqrt(fmax(disc, 0.0))) / (2.0 * A2));
+  if (g < 0) g = 0;
+  if (g > ngroups - 1) g = ngroups - 1;
+  while (g > 0 && S(g) > b) --g;
+  while (g + 1 < ngroups && S(g + 1) <= b) ++g;
+  const long long Gg = (npairs - g * G < G) ? npairs - g * G : G;
+  const long long o = b - S(g);
+  const long long ramp = Gg * (Gg + 1) / 2;
+  if (o < ramp) {
+    long long k = (long long)floor((sqrt(8.0 * (double)o + 1.0) - 1.0) * 0.5);
+    while (k > 0 && k * (k + 1) / 2 > o) --k;
+    while ((k + 1) * (k + 2) / 2 <= o) ++k;
+    Jp = (int)(g * G + k);
+    P = (int)(g * G + (o - k * (k + 1) / 2));
+  } else {
+    const long long o2 = o - ramp;
+    Jp = (int)(g * G + Gg + o2 / Gg);
+    P = (int)(g * G + o2 % Gg);
+  }
+}
+
+// Tile of CTA `rank` of the cluster for cluster tile b: row tile i, column tile J, mode.
+template <int NPAIR>
+__device__ __forceinline__ void cluster_tile(const Params2& p, long long b, uint32_t rank, int& P, int& J, int& mode) {
+  if (NPAIR == 1) {
+    decode_pair(p, b, rank, P, J, mode);
+    return;
+  }
+  int Jp;
+  decode_quad(p, b, P, Jp);
+  J = 2 * Jp + (int)(rank >> 1);
+  const int i = 2 * P + (int)(rank & 1);
+  if (i >= p.T1 || J >= p.T2 || (p.homo && J < i)) mode = kSkip;
+  else if (!p.homo) mode = kPlain;
+  else mode = (J == i) ? kDiag : kMirror;
+}
+
+__device__ __forceinline__ void tma_load_3d_2sm_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                   uint32_t bar_local, uint16_t mask, uint64_t pol) {
+  // multicast to every CTA in `mask`; complete_tx lands on each destination
+  // pair leader's barrier at this offset (peer bit cleared, as CUTLASS does)
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;\n"
+      ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2),
+        "r"(bar_local & 0xFEFFFFFFu), "h"(mask), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_commit_mask(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      ::"r"(su32(bar)), "h"(mask) : "memory");
+}
+
+template <int NPAIR>
+__global__ void __launch_bounds__(THREADS, 1)
 contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                            const __grid_constant__ OutMaps outm, const Params2 p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -696,20 +768,24 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
   float* col_re0 = reinterpret_cast<float*>(staging + STG_BYTES);
   float* col_im0 = col_re0 + BN;
   uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
-  uint64_t* full = bars;                 // [STAGES] (used in the leader)
+  uint64_t* full = bars;                 // [STAGES] (used in the pair leader)
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;          // [2] (used in the leader)
+  uint64_t* tempty = tfull + 2;          // [2] (used in the pair leader)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
+  const uint32_t prank = rank & 1;               // CTA within its pair
+  const uint32_t lrank = rank & ~1u;             // the pair leader
+  const bool leader = prank == 0;
+  const uint16_t pair_mask = (uint16_t)(3u << lrank);
+  const uint16_t all_mask = (uint16_t)((1u << (2 * NPAIR)) - 1);
   const long long cid = cluster_id_x(), ncl = num_clusters_x();
   const int nkb = p.hp / KB;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], NPAIR); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
@@ -732,24 +808,34 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
       uint32_t phase = 0;
       for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
         int P, J, mode;
-        decode_pair(p, t, rank, P, J, mode);
-        const int arow = (2 * P + (int)rank) * BM, brow = J * BN;
-        // CTA0: Bx = Re', By = Im'    CTA1: Bx = -Im', By = Re'
+        cluster_tile<NPAIR>(p, t, rank, P, J, mode);
+        const int arow = (2 * P + (int)prank) * BM, brow = J * BN;
+        // pair CTA0: Bx = Re', By = Im'    pair CTA1: Bx = -Im', By = Re'
         const int kx = leader ? 0 : 2 * p.hp, ky = leader ? p.hp : 0;
+        // NPAIR == 2: the first pair's CTAs load A for both pairs (multicast)
+        const bool load_a = (NPAIR == 1) || rank < 2;
+        const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          const uint32_t lbar = mapa_rank(su32(&full[stage]), 0);
+          const uint32_t lbar = mapa_rank(su32(&full[stage]), lrank);
+          if (p.dbg & 4) {            // profiling: no operand traffic at all
+            mbar_arrive_remote(lbar);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx_remote(lbar, STAGE_BYTES);
           uint8_t* base = stages + stage * STAGE_BYTES;
           const int k0 = kb * KB;
-          tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
-          tma_load_3d_2sm(base + 1 * TILE_BYTES, &tmap_a, k0, arow, 1, lbar, keep);
-          tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 0, lbar, keep);
-          tma_load_3d_2sm(base + 3 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 1, lbar, keep);
+          // each box carries both planes: hi tile then lo tile, contiguous
+          if (NPAIR == 1) {
+            tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
+            tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 0, lbar, keep);
+          } else if (load_a) {
+            tma_load_3d_2sm_mc(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, su32(&full[stage]), a_mask, keep);
+            tma_load_3d_2sm_mc(base + 2 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 0, su32(&full[stage]), a_mask, keep);
+          }
           tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, kx + k0, brow, 0, lbar, keep);
-          tma_load_3d_2sm(base + 5 * TILE_BYTES, &tmap_b, kx + k0, brow, 1, lbar, keep);
           tma_load_3d_2sm(base + 6 * TILE_BYTES, &tmap_b, ky + k0, brow, 0, lbar, keep);
-          tma_load_3d_2sm(base + 7 * TILE_BYTES, &tmap_b, ky + k0, brow, 1, lbar, keep);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -787,8 +873,11 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               umma2_bf16(d, aim_h, by_l, ID, 1);
               umma2_bf16(d, aim_l, by_h, ID, 1);
             }
-            umma2_commit_both(&empty[stage]);
-            if (kb == nkb - 1) umma2_commit_both(&tfull[acc]);
+            // stage s is free only when every pair of the cluster has consumed it
+            // (NPAIR == 2: A was multicast into both pairs); the accumulator is
+            // handed to this pair's two epilogues
+            umma2_commit_mask(&empty[stage], all_mask);
+            if (kb == nkb - 1) umma2_commit_mask(&tfull[acc], pair_mask);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -805,12 +894,11 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
     const uint64_t drop = store_policy(p.store_pol);
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t chunk_no = 0;
     float mphi = 0.f, mpsi = 0.f, chk = 0.f;
     for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
       int P, J, mode;
-      decode_pair(p, t, rank, P, J, mode);
-      const int i0 = (2 * P + (int)rank) * BM, j0 = J * BN;
+      cluster_tile<NPAIR>(p, t, rank, P, J, mode);
+      const int i0 = (2 * P + (int)prank) * BM, j0 = J * BN;
       const int gi = i0 + r;
       if (mode != kSkip) {
         float row_re0 = 0.f, row_im0 = 0.f;
@@ -928,7 +1016,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_remote(mapa_rank(su32(&tempty[acc]), 0));
+      if (lane == 0) mbar_arrive_remote(mapa_rank(su32(&tempty[acc]), lrank));
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -972,7 +1060,7 @@ static int make_operand_map(CUtensorMap* map, const void* base, long long ld, lo
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 2};
   cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)split * 2};
-  cuuint32_t box[3] = {KB, BM, 1};
+  cuuint32_t box[3] = {KB, BM, 2};   // both bf16 planes in one box
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1002,10 +1090,25 @@ static int make_output_map(CUtensorMap* map, float* base, long long ld, long lon
 
 using namespace corr2d;
 
-static bool use_2sm(int n1, int row0, int row1, bool tma_ok) {
+// 0: 1-SM kernel (row shards, unaligned outputs); 1: CTA pairs (default for
+// whole maps); 2: clusters of two CTA pairs sharing A by TMA multicast.
+// Measured on B200, cfg5: pairs 3.36 ms, A-multicast quads 3.64 ms (fewer
+// co-resident clusters, coupled pairs) -- the quads stay selectable with
+// CORR2D_BF16_QUADS=1; CORR2D_BF16_1SM=1 forces the 1-SM kernel.
+static int bf16_variant(int n1, int row0, int row1, bool tma_ok) {
   const char* env = getenv("CORR2D_BF16_1SM");
-  if (env && env[0] == '1') return false;
-  return tma_ok && row0 == 0 && row1 == n1;
+  if ((env && env[0] == '1') || !tma_ok || row0 != 0 || row1 != n1) return 0;
+  const char* quads = getenv("CORR2D_BF16_QUADS");
+  if (quads && quads[0] == '1') return 2;
+  return 1;
+}
+static bool use_2sm(int n1, int row0, int row1, bool tma_ok) { return bf16_variant(n1, row0, row1, tma_ok) != 0; }
+
+static long long tiles_quad(int n1, int n2, int homo) {
+  using namespace corr2d::tc;
+  const long long T1 = (n1 + BM - 1) / BM, T2 = (n2 + BN - 1) / BN;
+  const long long P = (T1 + 1) / 2, T2p = (T2 + 1) / 2;
+  return homo ? P * T2p - P * (P - 1) / 2 : P * T2p;
 }
 
 static long long tiles_1sm(int n1, int n2, int homo, int row0, int row1) {
@@ -1029,7 +1132,9 @@ extern "C" int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int
     const long long T = (n2 + 63) / 64, R = (row1 + 63) / 64 - row0 / 64;
     return homo ? R * T - R * (R - 1) / 2 : R * T;
   }
-  if (use_2sm(n1, row0, row1, ld_out % 4 == 0)) return tiles_2sm(n1, n2, homo);
+  const int v = bf16_variant(n1, row0, row1, ld_out % 4 == 0);
+  if (v == 2) return tiles_quad(n1, n2, homo);
+  if (v == 1) return tiles_2sm(n1, n2, homo);
   return tiles_1sm(n1, n2, homo, row0, row1);
 }
 
@@ -1072,8 +1177,10 @@ extern "C" int corr2d_contract_bf16x3(
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
-  const bool two_sm = use_2sm(n1, row0, row1, aligned);
-  const long long total = two_sm ? tiles_2sm(n1, n2, homo) : tiles_1sm(n1, n2, homo, row0, row1);
+  const int variant = bf16_variant(n1, row0, row1, aligned);
+  const bool two_sm = variant != 0;
+  const long long total = variant == 2 ? tiles_quad(n1, n2, homo)
+                        : (variant == 1 ? tiles_2sm(n1, n2, homo) : tiles_1sm(n1, n2, homo, row0, row1));
   if (tile1 < 0 || tile1 > total) tile1 = total;
   if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad tile range");
   const long long work = tile1 - tile0;
@@ -1090,10 +1197,32 @@ extern "C" int corr2d_contract_bf16x3(
     p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
     p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
     p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
-    cudaFuncSetAttribute(contract_bf16x3_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
-    const long long clusters = work < sms / 2 ? work : sms / 2;
-    contract_bf16x3_2sm_kernel<<<(unsigned)(2 * clusters), THREADS, SMEM_BYTES, st>>>(ma, mb, om, p);
-    return check_launch("contract_bf16x3_2sm_kernel");
+    const int csize = 2 * variant;  // CTAs per cluster
+    auto kern = variant == 2 ? contract_bf16x3_2sm_kernel<2> : contract_bf16x3_2sm_kernel<1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csize;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    // persistent: as many clusters as can be co-resident (cluster placement
+    // can leave SMs of a GPC unused), never more than the work
+    int max_clusters = 0;
+    cfg.gridDim = dim3(csize * (sms / csize));
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg) != cudaSuccess || max_clusters < 1) {
+      cudaGetLastError();
+      max_clusters = sms / csize;
+    }
+    const long long clusters = work < max_clusters ? work : max_clusters;
+    cfg.gridDim = dim3((unsigned)(csize * clusters));
+    cudaLaunchKernelEx(&cfg, kern, ma, mb, om, p);
+    return check_launch(variant == 2 ? "contract_bf16x3_2sm_kernel<2>" : "contract_bf16x3_2sm_kernel<1>");
   }
   Params p{};
   p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = aligned ? 1 : 0;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <vector>
 
 namespace corr2d {
@@ -189,35 +190,31 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   }
 
   // 1. load the raw m_in x C block (row segments of C channels), count non-finite
-  //    (8 independent loads in flight per thread before the shared stores)
+  //    All element copies are issued as cp.async (no register round trip), so
+  //    the whole block is in flight at once; then one conversion pass.
   int bad = 0;
-  constexpr int U = 8;
   const int total_in = m_in * C;
-  for (int base = tid; base < total_in; base += U * blockDim.x) {
-    double v[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = base + u * blockDim.x;
-      v[u] = 0.0;
-      if (idx < total_in) {
-        const int r = idx / C, c = idx - r * C;
-        if (c < nc) {
-          const long long off = (long long)r * p.ld_raw + c0 + c;
-          v[u] = p.in_f32 ? (double)__ldg(static_cast<const float*>(p.raw) + off)
-                          : __ldg(static_cast<const double*>(p.raw) + off);
-        }
-      }
+  const int esz = p.in_f32 ? 4 : 8;
+  uint8_t* landing = reinterpret_cast<uint8_t*>(cstat + 2 * C);
+  for (int idx = tid; idx < total_in; idx += blockDim.x) {
+    const int r = idx / C, c = idx - r * C;
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(landing + (size_t)idx * esz));
+    if (c < nc) {
+      const char* src = static_cast<const char*>(p.raw) + ((long long)r * p.ld_raw + c0 + c) * esz;
+      if (esz == 4) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src) : "memory");
+      else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = base + u * blockDim.x;
-      if (idx < total_in) {
-        const int r = idx / C, c = idx - r * C;
-        bad += !isfinite(v[u]);
-        if (resample) raw_s[r * (C + 1) + c] = v[u];
-        else rv[r * RS + c] = v[u];
-      }
-    }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  for (int idx = tid; idx < total_in; idx += blockDim.x) {
+    const int r = idx / C, c = idx - r * C;
+    double v = 0.0;
+    if (c < nc) v = p.in_f32 ? (double)reinterpret_cast<const float*>(landing)[idx]
+                             : reinterpret_cast<const double*>(landing)[idx];
+    bad += !isfinite(v);
+    if (resample) raw_s[r * (C + 1) + c] = v;
+    else rv[r * RS + c] = v;
   }
   bad = warp_sum(bad);
   if ((tid & 31) == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
@@ -453,11 +450,12 @@ static int fft_factorize(int m, int* f, int maxf) {
   return k;
 }
 
-static size_t prep_smem_bytes(int m, int m_in, int C, bool resample) {
+static size_t prep_smem_bytes(int m, int m_in, int C, bool resample, int in_bytes) {
   const size_t CPc = C / 2 + 1;
   size_t b = 2 * (size_t)m * CPc * sizeof(double2) + (size_t)m * sizeof(double2);
   if (resample) b += (size_t)m_in * (C + 1) * sizeof(double);
   b += 2 * (size_t)C * sizeof(double);
+  b += (size_t)m_in * C * in_bytes;  // cp.async landing zone of the raw block
   return b;
 }
 
@@ -529,9 +527,14 @@ extern "C" int corr2d_prep(
 
   const bool resample = resample_kind != CORR2D_RESAMPLE_NONE;
   int C = 64;
-  const size_t budget = 100 * 1024;
-  while (C > 2 && prep_smem_bytes(m, m_in, C, resample) > budget) C /= 2;
-  size_t smem = prep_smem_bytes(m, m_in, C, resample);
+  const int in_bytes = (in_dtype == CORR2D_F32) ? 4 : 8;
+  const size_t budget = 110 * 1024;
+  while (C > 2 && prep_smem_bytes(m, m_in, C, resample, in_bytes) > budget) C /= 2;
+  if (const char* e = getenv("CORR2D_PREP_C")) {  // experiments: channels per CTA
+    const int forced = atoi(e);
+    if (forced >= 2 && forced <= 64 && (forced % 2) == 0) C = forced;
+  }
+  size_t smem = prep_smem_bytes(m, m_in, C, resample, in_bytes);
   if (smem > 220 * 1024)
     return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_prep: m too large for the shared-memory FFT (m <= ~4096)");
   p.C = C;

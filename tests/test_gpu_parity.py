@@ -238,8 +238,9 @@ def test_fp32_tile_ranges_and_both_tensor_core_kernels(monkeypatch):
     v = rng.normal(size=(64, 700))
     s, a, _ = O.correlate_ft(v)
     sc = scale_of(s, a)
-    for one_sm in ("0", "1"):
+    for one_sm, quads in (("0", "0"), ("0", "1"), ("1", "0")):   # pairs, A-multicast quads, 1-SM
         monkeypatch.setenv("CORR2D_BF16_1SM", one_sm)
+        monkeypatch.setenv("CORR2D_BF16_QUADS", quads)
         d = dyn_from_values(v)
         full = P.correlate_ft(d, dtype="float32")
         assert rel_err(full.sync, s, sc) <= TOL32 and rel_err(full.asyn, a, sc) <= TOL32

@@ -106,16 +106,19 @@ def test_reference_arm_under_torchrun_prints_one_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0
 
 
-def pair_coverage(n1, n2, tile, homo, tiles, G):
-    from paper_1808_00685_b200.engine_core import SKIP, pair_tile_decode
+def pair_coverage(n1, n2, tile, homo, tiles, G, quad=False):
+    from paper_1808_00685_b200.engine_core import SKIP, pair_tile_decode, quad_tile_decode
     T1, T2 = -(-n1 // tile), -(-n2 // tile)
     cnt = np.zeros((n1, n2), dtype=np.int32)
     for b in tiles:
-        for rank in (0, 1):
-            P, J, mode = pair_tile_decode(b, T1, T2, homo, rank, G)
+        for rank in ((0, 1, 2, 3) if quad else (0, 1)):
+            if quad:
+                P, J, mode = quad_tile_decode(b, T1, T2, homo, rank, G)
+            else:
+                P, J, mode = pair_tile_decode(b, T1, T2, homo, rank, G)
             if mode == SKIP:
                 continue
-            i0, j0 = (2 * P + rank) * tile, J * tile
+            i0, j0 = (2 * P + (rank & 1)) * tile, J * tile
             r, c = np.meshgrid(np.arange(tile), np.arange(tile), indexing="ij")
             gi, gj = i0 + r, j0 + c
             ok = (gi < n1) & (gj < n2)
@@ -145,4 +148,25 @@ def test_pair_tiles_cover_hetero_map_once(n1, n2, G):
     from paper_1808_00685_b200.engine_core import pair_tile_count
     T1, T2 = -(-n1 // 8), -(-n2 // 8)
     acc = pair_coverage(n1, n2, 8, False, range(pair_tile_count(T1, T2, False)), G)
+    assert np.all(acc == 1)
+
+
+@pytest.mark.parametrize("n,G", [(64, 2), (72, 3), (40, 16), (130, 4), (88, 1)])
+@pytest.mark.parametrize("world", [1, 3])
+def test_quad_tiles_cover_homo_map_once(n, G, world):
+    from paper_1808_00685_b200.engine_core import quad_tile_count
+    T = -(-n // 8)
+    total = quad_tile_count(T, T, True)
+    acc = np.zeros((n, n), dtype=np.int32)
+    for rank in range(world):
+        t0, t1 = tile_range(total, world, rank)
+        acc += pair_coverage(n, n, 8, True, range(t0, t1), G, quad=True)
+    assert np.all(acc == 1)
+
+
+@pytest.mark.parametrize("n1,n2,G", [(64, 40, 2), (72, 24, 16), (24, 72, 3), (40, 56, 1)])
+def test_quad_tiles_cover_hetero_map_once(n1, n2, G):
+    from paper_1808_00685_b200.engine_core import quad_tile_count
+    T1, T2 = -(-n1 // 8), -(-n2 // 8)
+    acc = pair_coverage(n1, n2, 8, False, range(quad_tile_count(T1, T2, False)), G, quad=True)
     assert np.all(acc == 1)
