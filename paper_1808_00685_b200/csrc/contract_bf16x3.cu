@@ -54,6 +54,14 @@ constexpr int STG_BYTES = 2 * (STG_DIRECT + STG_MIRROR);
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 2 * BN * 4 + 16 * 8 + 16;
+// CTA-pair kernels: 2 operand stages, 32-column epilogue chunks staged per warp as
+// {sync tile, async tile, sync mirror, async mirror} boxes of 32 x 32 fp32 (SWIZZLE_128B)
+constexpr int STAGES2 = 2;
+constexpr int CH2 = 32;
+constexpr int BOX2 = 32 * CH2 * 4;           // 4 KB
+constexpr int WSTG2 = 4 * BOX2;              // 16 KB per epilogue warp
+constexpr int STG2_BYTES = 4 * WSTG2;        // 64 KB
+constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE_BYTES + STG2_BYTES + 2 * BN * 4 + 16 * 8 + 16;
 
 // kTransOnly: a tile left of the shard's diagonal square is computed as its
 // globally-upper mirror (operand tiles swapped) and only the transpose is
@@ -167,6 +175,17 @@ __host__ __device__ constexpr uint32_t idesc_bf16(bool neg_a) {
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
@@ -271,6 +290,45 @@ __device__ __forceinline__ void stage_and_store_pair(uint8_t* wst, int lane, con
     for (int k = 0; k < 16; ++k) {
       mphi[k * 32 + lane] = vp[k];
       mpsi[k * 32 + lane] = -vs[k];
+    }
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(&om.m[0][0], dphi, cbase, row0q, pol);
+    tma_store_2d(&om.m[1][0], dpsi, cbase, row0q, pol);
+    if (mirror) {
+      tma_store_2d(&om.m[0][1], mphi, row0q, cbase, pol);
+      tma_store_2d(&om.m[1][1], mpsi, row0q, cbase, pol);
+    }
+    bulk_commit();
+  }
+}
+
+// 32-column chunk of both planes (CTA-pair kernels): four 32 x 32 fp32 boxes in
+// SWIZZLE_128B layout -- tile rows are lane-owned (8 conflict-free STS.128, the
+// 16-B chunk j of row l at j ^ (l & 7)), mirror rows are column-owned (element
+// (k, lane) at chunk (lane >> 2) ^ (k & 7), word lane & 3: conflict-free STS.32).
+__device__ __forceinline__ void stage_and_store_32(uint8_t* wst, int lane, const float (&vp)[32], const float (&vs)[32],
+                                                   bool mirror, const OutMaps& om, int cbase, int row0q, uint64_t pol) {
+  uint8_t* dphi = wst;
+  uint8_t* dpsi = wst + BOX2;
+  uint8_t* mphi = wst + 2 * BOX2;
+  uint8_t* mpsi = wst + 3 * BOX2;
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int off = lane * 128 + ((j ^ (lane & 7)) * 16);
+    *reinterpret_cast<float4*>(dphi + off) = make_float4(vp[4 * j], vp[4 * j + 1], vp[4 * j + 2], vp[4 * j + 3]);
+    *reinterpret_cast<float4*>(dpsi + off) = make_float4(vs[4 * j], vs[4 * j + 1], vs[4 * j + 2], vs[4 * j + 3]);
+  }
+  if (mirror) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int off = k * 128 + (((lane >> 2) ^ (k & 7)) * 16) + (lane & 3) * 4;
+      *reinterpret_cast<float*>(mphi + off) = vp[k];
+      *reinterpret_cast<float*>(mpsi + off) = -vs[k];
     }
   }
   fence_async_smem();
@@ -761,11 +819,14 @@ template <int NPAIR>
 __global__ void __launch_bounds__(THREADS, 1)
 contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                            const __grid_constant__ OutMaps outm, const Params2 p) {
+  // 2 operand stages (measured as fast as 3 here) leave room for 32-column
+  // epilogue chunks: 128-B row segments in both the tile and its mirror.
+  constexpr int STAGES = STAGES2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;
   uint8_t* staging = stages + STAGES * STAGE_BYTES;
-  float* col_re0 = reinterpret_cast<float*>(staging + STG_BYTES);
+  float* col_re0 = reinterpret_cast<float*>(staging + STG2_BYTES);
   float* col_im0 = col_re0 + BN;
   uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
   uint64_t* full = bars;                 // [STAGES] (used in the pair leader)
@@ -927,38 +988,32 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
         if (use_tma) {
-          // Software pipeline over 16-column chunks: the TMEM loads of chunk c+1
-          // (sync and async) are in flight while chunk c is corrected, reduced,
-          // staged and handed to the TMA store engine.
-          uint8_t* wst = staging + q * WSTG;
+          // 32-column chunks: both planes loaded from TMEM, corrected, reduced,
+          // staged as four 32 x 32 boxes (128-B rows) and handed to the TMA
+          // store engine; the buffer is reclaimed one chunk later.
+          uint8_t* wst = staging + q * WSTG2;
           const bool mir = mode != kPlain;
-          auto process = [&](const uint32_t (&u)[32], int c) {
-            float vp[16], vs[16];
+#pragma unroll 1
+          for (int c = 0; c < BN / CH2; ++c) {
+            uint32_t ua[32], ub[32];
+            tmem_ld32(tbase + c * CH2, ua);
+            tmem_ld32(tbase + 128 + c * CH2, ub);
+            tmem_wait_ld_tie(ua);
+            tmem_wait_ld_tie(ub);
+            float vp[32], vs[32];
 #pragma unroll
-            for (int k = 0; k < 16; ++k) { vp[k] = __uint_as_float(u[k]); vs[k] = __uint_as_float(u[16 + k]); }
+            for (int k = 0; k < 32; ++k) { vp[k] = __uint_as_float(ua[k]); vs[k] = __uint_as_float(ub[k]); }
             if (p.even) {
 #pragma unroll
-              for (int k = 0; k < 16; ++k) vs[k] -= row_im0 * col_re0[c * CH + k] - row_re0 * col_im0[c * CH + k];
+              for (int k = 0; k < 32; ++k) vs[k] -= row_im0 * col_re0[c * CH2 + k] - row_re0 * col_im0[c * CH2 + k];
             }
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < 32; ++k) {
               mphi = fmaxf(mphi, fabsf(vp[k]));
               mpsi = fmaxf(mpsi, fabsf(vs[k]));
               chk = fmaf(vp[k], 0.f, fmaf(vs[k], 0.f, chk));
             }
-            const int cbase = j0 + c * CH;
-            if (!(p.dbg & 1)) stage_and_store_pair(wst, lane, vp, vs, mir, outm, cbase, i0 + 32 * q, drop);
-          };
-          uint32_t ua[32], ub[32];
-          tmem_ld16x2(tbase, 0, ua);
-#pragma unroll 1
-          for (int c = 0; c < BN / CH; c += 2) {
-            tmem_wait_ld_tie(ua);
-            tmem_ld16x2(tbase, c + 1, ub);
-            process(ua, c);
-            tmem_wait_ld_tie(ub);
-            if (c + 2 < BN / CH) tmem_ld16x2(tbase, c + 2, ua);
-            process(ub, c + 1);
+            if (!(p.dbg & 1)) stage_and_store_32(wst, lane, vp, vs, mir, outm, j0 + c * CH2, i0 + 32 * q, drop);
           }
         } else
 #pragma unroll 1
@@ -1069,18 +1124,20 @@ static int make_operand_map(CUtensorMap* map, const void* base, long long ld, lo
   return CORR2D_OK;
 }
 
-// Output plane (rows x cols fp32, leading dimension ld): direct box 16 x 128
-// (SWIZZLE_64B) or mirror box 32 x 16 (no swizzle), one box per epilogue warp.
-static int make_output_map(CUtensorMap* map, float* base, long long ld, long long rows, long long cols, bool mirror) {
+// Output plane (rows x cols fp32, leading dimension ld), one box per epilogue warp:
+// kind 0 = 1-SM direct 16 x 32 (SWIZZLE_64B), 1 = 1-SM mirror 32 x 16 (no
+// swizzle), 2 = CTA-pair 32 x 32 boxes (SWIZZLE_128B) for tile and mirror.
+static int make_output_map(CUtensorMap* map, float* base, long long ld, long long rows, long long cols, int kind) {
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {mirror ? 32u : (cuuint32_t)CH, mirror ? (cuuint32_t)CH : 32u};   // per-warp boxes
+  cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)CH : 32u, kind == 1 ? (cuuint32_t)CH : 32u};
   cuuint32_t estr[2] = {1, 1};
+  const CUtensorMapSwizzle sw = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_64B
+                              : (kind == 1 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, mirror ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_64B,
-                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed (" + std::to_string((int)r) + ")");
   return CORR2D_OK;
 }
@@ -1167,9 +1224,11 @@ extern "C" int corr2d_contract_bf16x3(
                        ((reinterpret_cast<uintptr_t>(psi) & 15) == 0);
   if (aligned) {
     const long long rows = row1 - row0;
+    const bool pair_kernel = bf16_variant(n1, row0, row1, true) != 0;
     float* planes[2] = {phi, psi};
     for (int pl = 0; pl < 2 && !rc; ++pl)
-      for (int mi = 0; mi < 2 && !rc; ++mi) rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, mi == 1);
+      for (int mi = 0; mi < 2 && !rc; ++mi)
+        rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, pair_kernel ? 2 : mi);
     if (rc) return rc;
   }
   int dev = 0, sms = 148;
@@ -1199,7 +1258,7 @@ extern "C" int corr2d_contract_bf16x3(
     p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
     const int csize = 2 * variant;  // CTAs per cluster
     auto kern = variant == 2 ? contract_bf16x3_2sm_kernel<2> : contract_bf16x3_2sm_kernel<1>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1207,7 +1266,7 @@ extern "C" int corr2d_contract_bf16x3(
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.blockDim = dim3(THREADS);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = SMEM2_BYTES;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
