@@ -56,12 +56,25 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 2 * BN * 4 + 16 * 8 + 16;
 // CTA-pair kernels: 2 operand stages, 32-column epilogue chunks staged per warp as
 // {sync tile, async tile, sync mirror, async mirror} boxes of 32 x 32 fp32 (SWIZZLE_128B)
+// Operand stages: 2 x 64 KB of 32-slot boxes (64-B rows, SWIZZLE_64B).  Measured
+// alternatives on cfg5: 4 x 32 KB of 16-slot boxes (SWIZZLE_32B) 5.25 ms -- the
+// narrow TMA boxes and the doubled per-stage handshakes cost more than the
+// deeper ring gains; 3 x 64 KB only fits with half the epilogue staging.
+constexpr int KB2 = 32;
+constexpr int TILE2_BYTES = BM * KB2 * 2;    // 8 KB
+constexpr int STAGE2_BYTES = 8 * TILE2_BYTES;
 constexpr int STAGES2 = 2;
 constexpr int CH2 = 32;
 constexpr int BOX2 = 32 * CH2 * 4;           // 4 KB
 constexpr int WSTG2 = 4 * BOX2;              // 16 KB per epilogue warp
 constexpr int STG2_BYTES = 4 * WSTG2;        // 64 KB
-constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE_BYTES + STG2_BYTES + 2 * BN * 4 + 16 * 8 + 16;
+constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 2 * BN * 4 + 16 * 8 + 16;
+// Epilogue warps of the CTA-pair kernels: 4 (each warp both planes of its lane
+// quadrant) or 8 (warps 2-5 sync, 6-9 async).  Measured on cfg5: 4 -> 3.26 ms,
+// 8 -> 3.37 ms; the staging budget is the same 64 KB either way.
+constexpr int EPI_WARPS2 = 4;
+constexpr int PPW2 = 8 / EPI_WARPS2;         // planes per epilogue warp
+constexpr int THREADS2 = 64 + 32 * EPI_WARPS2;
 
 // kTransOnly: a tile left of the shard's diagonal square is computed as its
 // globally-upper mirror (operand tiles swapped) and only the transpose is
@@ -166,6 +179,17 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
   d |= (uint64_t)(512 >> 4) << 32;        // stride byte offset: next 8-row group
   d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
   d |= (uint64_t)4 << 61;                 // layout: SWIZZLE_64B
+  return d;
+}
+
+// K-major, SWIZZLE_32B canonical layout: rows of 32 B, 8-row groups 256 B apart.
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;                 // layout: SWIZZLE_32B
   return d;
 }
 
@@ -343,6 +367,38 @@ __device__ __forceinline__ void stage_and_store_32(uint8_t* wst, int lane, const
     bulk_commit();
   }
 }
+
+// One plane of a 32-column chunk (8-warp epilogue of the CTA-pair kernels):
+// tile box and mirror box, 32 x 32 fp32 each, SWIZZLE_128B.
+// PENDING: store groups of this lane that may still be reading OTHER buffers.
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane, const float (&v)[32], bool mirror,
+                                                         float tsign, const CUtensorMap* map_direct,
+                                                         const CUtensorMap* map_mirror, int cbase, int row0q,
+                                                         uint64_t pol) {
+  uint8_t* dbox = wst;
+  uint8_t* mbox = wst + BOX2;
+  if (lane == 0) bulk_wait_read<PENDING>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(dbox + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  if (mirror) {
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      *reinterpret_cast<float*>(mbox + k * 128 + (((lane >> 2) ^ (k & 7)) * 16) + (lane & 3) * 4) = tsign * v[k];
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map_direct, dbox, cbase, row0q, pol);
+    if (mirror) tma_store_2d(map_mirror, mbox, row0q, cbase, pol);
+    bulk_commit();
+  }
+}
+
+__device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS2) : "memory"); }
 
 // sync chunk c -> u[0..15], async chunk c -> u[16..31]
 __device__ __forceinline__ void tmem_ld16x2(uint32_t tbase, int c, uint32_t (&u)[32]) {
@@ -816,12 +872,15 @@ __device__ __forceinline__ void umma2_commit_mask(uint64_t* bar, uint16_t mask) 
 }
 
 template <int NPAIR>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(THREADS2, 1)
 contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                            const __grid_constant__ OutMaps outm, const Params2 p) {
-  // 2 operand stages (measured as fast as 3 here) leave room for 32-column
-  // epilogue chunks: 128-B row segments in both the tile and its mirror.
+  // 4 operand stages of 16 slots (128 KB) + 32-column epilogue chunks
+  // (128-B row segments in both the tile and its mirror).
   constexpr int STAGES = STAGES2;
+  constexpr int KB = KB2;
+  constexpr int TILE_BYTES = TILE2_BYTES;
+  constexpr int STAGE_BYTES = STAGE2_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* stages = smem;
@@ -847,7 +906,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], NPAIR); }
-    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 2 * EPI_WARPS2); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmap_b)) : "memory");
@@ -921,10 +980,11 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
 #pragma unroll
             for (int ks = 0; ks < KB / 16; ++ks) {
               const uint32_t off = ks * 32;
-              const uint64_t are_h = desc_sw64(base + 0 * TILE_BYTES + off), are_l = desc_sw64(base + 1 * TILE_BYTES + off);
-              const uint64_t aim_h = desc_sw64(base + 2 * TILE_BYTES + off), aim_l = desc_sw64(base + 3 * TILE_BYTES + off);
-              const uint64_t bx_h = desc_sw64(base + 4 * TILE_BYTES + off), bx_l = desc_sw64(base + 5 * TILE_BYTES + off);
-              const uint64_t by_h = desc_sw64(base + 6 * TILE_BYTES + off), by_l = desc_sw64(base + 7 * TILE_BYTES + off);
+              auto desc = [](uint32_t a) { return KB == 16 ? desc_sw32(a) : desc_sw64(a); };
+              const uint64_t are_h = desc(base + 0 * TILE_BYTES + off), are_l = desc(base + 1 * TILE_BYTES + off);
+              const uint64_t aim_h = desc(base + 2 * TILE_BYTES + off), aim_l = desc(base + 3 * TILE_BYTES + off);
+              const uint64_t bx_h = desc(base + 4 * TILE_BYTES + off), bx_l = desc(base + 5 * TILE_BYTES + off);
+              const uint64_t by_h = desc(base + 6 * TILE_BYTES + off), by_l = desc(base + 7 * TILE_BYTES + off);
               const uint32_t acc0 = (kb | ks) ? 1u : 0u;
               if (p.dbg & 2) continue;
               umma2_bf16(d, are_h, bx_h, ID, acc0);
@@ -949,9 +1009,13 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
     }
   } else {
     // ----------------------------------------------- epilogue (both CTAs) --
+    // 8 warps: quadrant q = warp & 3 of the TMEM lanes, plane pw = sync (warps
+    // 2-5) or async (warps 6-9) -- twice the TMEM-read / store-issue
+    // parallelism of one warp per quadrant.
     const int q = warp & 3;
+    const int pw = (warp - 2) >> 2;
     const int r = q * 32 + lane;
-    const int eid = threadIdx.x - 64;
+    const int eid = threadIdx.x - 64;          // 0..255
     const uint64_t drop = store_policy(p.store_pol);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -971,15 +1035,17 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
           }
           const int gj = j0 + eid;
           float cre = 0.f, cim = 0.f;
-          if (gj < p.n2) {
+          if (eid < BN && gj < p.n2) {
             const __nv_bfloat16* br = p.b + (long long)gj * p.ld_pack;
             cre = bf2f(br[0]) + bf2f(br[p.split_b]);
             cim = bf2f(br[p.hp]) + bf2f(br[p.hp + p.split_b]);
           }
-          epi_bar();
-          col_re0[eid] = cre;
-          col_im0[eid] = cim;
-          epi_bar();
+          epi_bar256();
+          if (eid < BN) {
+            col_re0[eid] = cre;
+            col_im0[eid] = cim;
+          }
+          epi_bar256();
         }
         const bool direct = gi < p.n1;
         const bool mirror = (mode != kPlain) && gi < p.n2;
@@ -988,36 +1054,41 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
         if (use_tma) {
-          // 32-column chunks: both planes loaded from TMEM, corrected, reduced,
-          // staged as four 32 x 32 boxes (128-B rows) and handed to the TMA
-          // store engine; the buffer is reclaimed one chunk later.
-          uint8_t* wst = staging + q * WSTG2;
+          // 32-column chunks of this warp's plane: TMEM -> registers ->
+          // correction / reduction -> two 32 x 32 boxes (tile + mirror, 128-B
+          // rows) -> TMA stores; the buffer is reclaimed one chunk later.
           const bool mir = mode != kPlain;
 #pragma unroll 1
-          for (int c = 0; c < BN / CH2; ++c) {
-            uint32_t ua[32], ub[32];
-            tmem_ld32(tbase + c * CH2, ua);
-            tmem_ld32(tbase + 128 + c * CH2, ub);
-            tmem_wait_ld_tie(ua);
-            tmem_wait_ld_tie(ub);
-            float vp[32], vs[32];
+          for (int plane = pw; plane < pw + PPW2; ++plane) {
+            uint8_t* wst = staging + ((warp - 2) * PPW2 + (plane - pw)) * (2 * BOX2);
+            const float tsign = plane == 0 ? 1.f : -1.f;
+            float mx = 0.f;
+#pragma unroll 1
+            for (int c = 0; c < BN / CH2; ++c) {
+              uint32_t ua[32];
+              tmem_ld32(tbase + plane * 128 + c * CH2, ua);
+              tmem_wait_ld_tie(ua);
+              float v[32];
 #pragma unroll
-            for (int k = 0; k < 32; ++k) { vp[k] = __uint_as_float(ua[k]); vs[k] = __uint_as_float(ub[k]); }
-            if (p.even) {
+              for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(ua[k]);
+              if (plane == 1 && p.even) {
 #pragma unroll
-              for (int k = 0; k < 32; ++k) vs[k] -= row_im0 * col_re0[c * CH2 + k] - row_re0 * col_im0[c * CH2 + k];
+                for (int k = 0; k < 32; ++k) v[k] -= row_im0 * col_re0[c * CH2 + k] - row_re0 * col_im0[c * CH2 + k];
+              }
+#pragma unroll
+              for (int k = 0; k < 32; ++k) {
+                mx = fmaxf(mx, fabsf(v[k]));
+                chk = fmaf(v[k], 0.f, chk);
+              }
+              if (!(p.dbg & 1))
+                stage_and_store_32_plane<PPW2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
+                                                   j0 + c * CH2, i0 + 32 * q, drop);
             }
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              mphi = fmaxf(mphi, fabsf(vp[k]));
-              mpsi = fmaxf(mpsi, fabsf(vs[k]));
-              chk = fmaf(vp[k], 0.f, fmaf(vs[k], 0.f, chk));
-            }
-            if (!(p.dbg & 1)) stage_and_store_32(wst, lane, vp, vs, mir, outm, j0 + c * CH2, i0 + 32 * q, drop);
+            if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
           }
         } else
 #pragma unroll 1
-        for (int plane = 0; plane < 2; ++plane) {
+        for (int plane = pw; plane < pw + PPW2; ++plane) {
           float* out = plane == 0 ? p.phi : p.psi;
           const float tsign = plane == 0 ? 1.f : -1.f;
           float mx = 0.f;
@@ -1110,16 +1181,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows, long long split) {
+// Operand boxes carry both bf16 planes: {KB, 128 rows, 2} with SWIZZLE_64B
+// (1-SM kernel, KB = 32) or {KB2, 128, 2} with SWIZZLE_32B (CTA-pair kernels).
+static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows, long long split,
+                            bool pair_kernel) {
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 2};
   cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)split * 2};
-  cuuint32_t box[3] = {KB, BM, 2};   // both bf16 planes in one box
+  cuuint32_t box[3] = {pair_kernel ? (cuuint32_t)KB2 : (cuuint32_t)KB, BM, 2};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  (pair_kernel && KB2 == 16) ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return CORR2D_OK;
 }
@@ -1211,20 +1286,20 @@ extern "C" int corr2d_contract_bf16x3(
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: homo needs n1 == n2");
   if (row0 % BM != 0 || (row1 != n1 && row1 % BM != 0))
     return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: row shard bounds must be multiples of 128 (or n1)");
-  CUtensorMap ma, mb;
-  int rc = make_operand_map(&ma, a, ld_pack, n1, split_a);
-  if (rc) return rc;
-  rc = make_operand_map(&mb, b, ld_pack, n2, split_b);
-  if (rc) return rc;
   // TMA stores need 16-byte aligned planes and a leading dimension that is a
   // multiple of 4 floats; otherwise the epilogue stores from registers.
-  OutMaps om;
-  memset(&om, 0, sizeof(om));
   const bool aligned = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(phi) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(psi) & 15) == 0);
+  const bool pair_kernel = bf16_variant(n1, row0, row1, aligned) != 0;
+  CUtensorMap ma, mb;
+  int rc = make_operand_map(&ma, a, ld_pack, n1, split_a, pair_kernel);
+  if (rc) return rc;
+  rc = make_operand_map(&mb, b, ld_pack, n2, split_b, pair_kernel);
+  if (rc) return rc;
+  OutMaps om;
+  memset(&om, 0, sizeof(om));
   if (aligned) {
     const long long rows = row1 - row0;
-    const bool pair_kernel = bf16_variant(n1, row0, row1, true) != 0;
     float* planes[2] = {phi, psi};
     for (int pl = 0; pl < 2 && !rc; ++pl)
       for (int mi = 0; mi < 2 && !rc; ++mi)
@@ -1265,7 +1340,7 @@ extern "C" int corr2d_contract_bf16x3(
     attr[0].val.clusterDim.x = csize;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(THREADS2);
     cfg.dynamicSmemBytes = SMEM2_BYTES;
     cfg.stream = st;
     cfg.attrs = attr;
