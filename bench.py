@@ -100,6 +100,9 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:   # sampler is live before timing starts
+                time.sleep(0.02)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
@@ -250,31 +253,56 @@ def run_b200(args, case, wl, world, rank, local):
     plan.check(axes=(ds1.spectral_axis, (ds2 or ds1).spectral_axis))
     parity = parity_gate(case, plan, world) if rank == 0 and world == 1 else None
 
-    # ---- warmup
-    for _ in range(args.warmup):
-        plan.launch()
+    # ---- the step as a CUDA graph (K1 + K2 launches, no host work in the loop);
+    #      a second graph with K2 alone times the contraction kernel
+    step_graph, k2_graph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream(device=dev)
+    cap.wait_stream(stream)
+    with torch.cuda.stream(cap):
+        plan.launch()                     # settle allocator / attributes before capture
+        with torch.cuda.graph(step_graph, stream=cap):
+            plan.launch()
+        with torch.cuda.graph(k2_graph, stream=cap):
+            plan.launch_contract()
+    stream.wait_stream(cap)
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, device time, barrier + sync on both sides
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    barrier(world)
-    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
+        # ---- warmup (W steps), then keep the GPU under the same load for
+        #      ~0.3 s so the clock sampler sees the steady state around the timed region
+        for _ in range(args.warmup):
+            step_graph.replay()
+        torch.cuda.synchronize()
+        t_load = time.time()
+        while time.time() - t_load < 0.3:
+            step_graph.replay()
+            torch.cuda.synchronize()
+
+        # ---- timed region: exactly K steps, device time, barrier + sync on both sides
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize()
         ev0.record(stream)
-        for k in range(args.steps):
-            # K1 launches, then K2 bracketed by events on the launching stream
-            plan.launch_prep_only()
-            kev[k][0].record(stream)
-            plan.launch_contract()
-            kev[k][1].record(stream)
+        for _ in range(args.steps):
+            step_graph.replay()
         ev1.record(stream)
         torch.cuda.synchronize()
-    barrier(world)
-    ms = ev0.elapsed_time(ev1)
-    k2_ms = [a.elapsed_time(b) for a, b in kev]
+        barrier(world)
+        ms = ev0.elapsed_time(ev1)
+
+        # ---- contraction kernel alone, K back-to-back launches on the same stream
+        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ka.record(stream)
+        for _ in range(args.steps):
+            k2_graph.replay()
+        kb.record(stream)
+        torch.cuda.synchronize()
+        t_load = time.time()
+        while time.time() - t_load < 0.3:
+            step_graph.replay()
+            torch.cuda.synchronize()
     ms_max = allreduce_max(ms, world)
-    k2_avg = allreduce_max(float(np.mean(k2_ms)), world)
+    k2_avg = allreduce_max(ka.elapsed_time(kb) / args.steps, world)
 
     # ---- e2e through the public API: pinned host inputs -> planes in pinned host memory
     e2e = run_e2e(args, case, ds1, ds2, world, rank, dev) if world == 1 else None

@@ -1056,15 +1056,17 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         if (use_tma) {
           // 32-column chunks of this warp's plane: TMEM -> registers ->
           // correction / reduction -> two 32 x 32 boxes (tile + mirror, 128-B
-          // rows) -> TMA stores; the buffer is reclaimed one chunk later.
+          // rows) -> TMA stores.  Planes alternate inside the chunk loop, so
+          // with one buffer per plane the group that last read this buffer is
+          // PPW2 - 1 commits back (that is what the wait allows in flight).
           const bool mir = mode != kPlain;
 #pragma unroll 1
-          for (int plane = pw; plane < pw + PPW2; ++plane) {
-            uint8_t* wst = staging + ((warp - 2) * PPW2 + (plane - pw)) * (2 * BOX2);
-            const float tsign = plane == 0 ? 1.f : -1.f;
-            float mx = 0.f;
+          for (int c = 0; c < BN / CH2; ++c) {
 #pragma unroll 1
-            for (int c = 0; c < BN / CH2; ++c) {
+            for (int plane = pw; plane < pw + PPW2; ++plane) {
+              uint8_t* wst = staging + ((warp - 2) * PPW2 + (plane - pw)) * (2 * BOX2);
+              const float tsign = plane == 0 ? 1.f : -1.f;
+              float mx = 0.f;
               uint32_t ua[32];
               tmem_ld32(tbase + plane * 128 + c * CH2, ua);
               tmem_wait_ld_tie(ua);
@@ -1083,8 +1085,8 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               if (!(p.dbg & 1))
                 stage_and_store_32_plane<PPW2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
                                                    j0 + c * CH2, i0 + 32 * q, drop);
+              if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
             }
-            if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
           }
         } else
 #pragma unroll 1

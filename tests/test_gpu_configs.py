@@ -62,3 +62,20 @@ def test_config_exact_symmetry(k):
     assert torch.equal(a[ti, tj], -a[tj, ti])
     assert torch.count_nonzero(torch.diagonal(a)).item() == 0
     assert torch.isfinite(s).all().item() and torch.isfinite(a).all().item()
+
+
+def test_cfg5_whole_map_two_independent_kernels(monkeypatch):
+    """Whole 32768^2 map: the CTA-pair kernel against the 1-SM kernel (different
+    tile shapes, epilogues and accumulation order) -- catches any corrupted tile
+    anywhere in the map, not only in the sampled reference rows."""
+    import torch
+    monkeypatch.setenv("CORR2D_BF16_1SM", "0")
+    _, a = run_config(5, return_device=True)
+    monkeypatch.setenv("CORR2D_BF16_1SM", "1")
+    _, b = run_config(5, return_device=True)
+    scale = float(torch.abs(a.sync).max())
+    for x, y in ((a.sync, b.sync), (a.asyn, b.asyn)):
+        diff = 0.0
+        for r0 in range(0, x.shape[0], 4096):
+            diff = max(diff, float(torch.abs(x[r0:r0 + 4096] - y[r0:r0 + 4096]).max()))
+        assert diff <= 2e-5 * scale, diff / scale
