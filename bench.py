@@ -324,7 +324,7 @@ def run_b200(args, case, wl, world, rank, local):
         "config": config_block(case, wl, args),
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "contract_bf16x3_kernel" if case.dtype == "float32" else "contract_f64_kernel",
+                     "kernel": contract_kernel_name(case),
                      "kernel_ms": k2_avg, "algorithmic": "8*K flops per complex output element",
                      "hbm_floor_ms": (wl["out_bytes"] + wl["in_bytes"]) / (peaks["hbm_gbs"] * 1e9) * 1e3,
                      "peak_source": peaks["_source"] + ("" if case.dtype == "float32" else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
@@ -405,6 +405,17 @@ def cpu_baseline_line(case, wl):
     return {"value": rows * wl["n2"] / dt / 1e9, "unit": "GElem/s", "cores": threads, "kind": "port",
             "sample": f"rows 0..{rows} of the {wl['n1']}x{wl['n2']} map ({dt:.1f} s; preprocess + rfft + "
                       f"row-block zgemm via the oracle restatement of corrtwo 0.1.0)"}
+
+
+def contract_kernel_name(case):
+    """The contraction kernel the C ABI dispatches to (bf16_variant() in contract_bf16x3.cu)."""
+    if case.dtype != "float32":
+        return "contract_f64_kernel"
+    if os.environ.get("CORR2D_BF16_1SM") == "1":
+        return "contract_bf16x3_kernel"
+    if os.environ.get("CORR2D_BF16_QUADS") == "1":
+        return "contract_bf16x3_2sm_kernel<2>"
+    return "contract_bf16x3_2sm_kernel<1>"
 
 
 def load_traffic(cfg):
