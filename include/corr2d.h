@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CORR2D_ABI_VERSION 1
+#define CORR2D_ABI_VERSION 2
 
 enum corr2d_status {
   CORR2D_OK = 0,
@@ -55,7 +55,7 @@ enum corr2d_resample { CORR2D_RESAMPLE_NONE = 0, CORR2D_RESAMPLE_LINEAR = 1, COR
 enum corr2d_pack {
   CORR2D_PACK_NONE = 0,
   CORR2D_PACK_F64 = 1,       /* float64 operands (fp64 DMMA contraction)            */
-  CORR2D_PACK_BF16X2 = 2     /* bf16 hi/lo split planes (bf16x3 tcgen05 contraction) */
+  CORR2D_PACK_BF16X2 = 2     /* bf16 hi/lo, k-block interleaved (bf16x3 tcgen05 contraction) */
 };
 
 enum corr2d_ref_mode { CORR2D_REF_MEAN = 0, CORR2D_REF_PROVIDED = 1, CORR2D_REF_NONE = 2 };
@@ -75,7 +75,9 @@ int corr2d_abi_version(void);
 /* Number of SMs, compute capability of `device`.  Fails with CORR2D_ERR_CUDA
  * when no device is present. */
 int corr2d_device_info(int device, int* sms, int* cc_major, int* cc_minor);
-/* Packed depth (slots per channel) the contraction kernels need for m. */
+/* Packed depth (slots per channel) the contraction kernels need for m.  A
+ * CORR2D_PACK_BF16X2 row stores every slot twice (hi and lo), i.e. 2 * depth
+ * bf16 values. */
 int corr2d_packed_depth(int m, int pack_kind);
 /* Prime/radix factorisation used by the perturbation-axis FFT (for tests). */
 int corr2d_fft_factors(int m, int* factors, int max_factors);
@@ -96,6 +98,10 @@ int corr2d_fft_factors(int m, int* factors, int max_factors);
  * reference subtraction): with alpha = 0 the entry used by dft_channels /
  * correlate_ft on DynamicSpectra, with sigma_in the one used by apply_scaling.
  * sigma_in (optional, n) replaces the computed sigma.
+ * Packing: ld_pack is the row pitch of the packed operands in elements
+ * (>= mp for F64; >= 2 * mp + 64 and a multiple of 64 for BF16X2, whose layout is
+ * described at corr2d_contract_bf16x3).  split_plane is unused (ABI v1 kept
+ * the bf16 lo values in a separate plane; v2 interleaves them).
  * Any output pointer may be NULL.  `status` (device int32[4]; reset on the
  * stream by this call) receives the counters above; the host raises the
  * reference's errors from them after the stream synchronises.
@@ -131,14 +137,20 @@ int corr2d_contract_f64(
 
 /*
  * fp32 path (tcgen05 tensor cores).  Operands are K1's CORR2D_PACK_BF16X2
- * "pair" layout: per channel [Re' | Im'] halves of mp/2 slots each (Re'[s] =
- * Re Y(s), Im'[0] = Re Y(m/2) for even m else 0, Im'[s] = Im Y(s)), every slot
- * scaled by sqrt(Norm * weight), stored as bf16 hi / lo planes (lo plane at
- * +split_a elements for `a`, +split_b for `b`; a == b for homo).  Products
- * hi*hi + hi*lo + lo*hi accumulate in fp32 in TMEM (tcgen05.mma kind::f16);
- * async uses the same tiles with the Re/Im halves swapped (negate-A), the even-m
- * Nyquist x DC cross term is removed in the epilogue.  Same row / homo /
- * stats contract as corr2d_contract_f64, shard bounds multiples of 128.
+ * layout: per channel three thirds [Re' | Im' | -Im'] of hp = mp/3 slots
+ * (Re'[s] = Re Y(s), Im'[0] = Re Y(m/2) for even m else 0, Im'[s] = Im Y(s)),
+ * every slot scaled by sqrt(Norm * weight) and split x = hi + lo into two
+ * bf16 values.  In memory each third is a run of 32-slot blocks of 64 bf16,
+ * [hi of the 32 slots | lo of the 32 slots], so slot s of third t has its hi
+ * at t*2*hp + (s/32)*64 + s%32 and its lo 32 elements later; one 128-byte
+ * TMA box row then feeds both halves of a k-block.  Row pitch ld_pack >=
+ * 2*mp + 64 (multiple of 64): K1 stores float32 (hi + lo) of Re'[0] and Im'[0]
+ * at element 2*mp of the row (the epilogue's Nyquist correction operands).
+ * a == b for homo; split_a / split_b are unused (ABI v1).
+ * Products hi*hi + hi*lo + lo*hi accumulate in fp32 in TMEM (tcgen05.mma
+ * kind::f16); the even-m Nyquist x DC cross term is removed in the epilogue.
+ * Same row / homo / stats contract as corr2d_contract_f64, shard bounds
+ * multiples of 128.
  */
 int corr2d_contract_bf16x3(
     const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,

@@ -32,6 +32,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -61,14 +62,35 @@ constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_
 // narrow TMA boxes and the doubled per-stage handshakes cost more than the
 // deeper ring gains; 3 x 64 KB only fits with half the epilogue staging.
 constexpr int KB2 = 32;
+static_assert(KB2 == KB, "operand boxes are 2*KB bf16 wide in both kernels");
 constexpr int TILE2_BYTES = BM * KB2 * 2;    // 8 KB
-constexpr int STAGE2_BYTES = 8 * TILE2_BYTES;
-constexpr int STAGES2 = 2;
+// CORR2D_SPLIT2 = 2: a ring slot holds half a k-block -- (A_re, Bx) or (A_im, By),
+// 32 KB -- so more, finer slots fit next to the epilogue staging.
+#ifndef CORR2D_SPLIT2
+#define CORR2D_SPLIT2 1
+#endif
+constexpr int SPLIT2 = CORR2D_SPLIT2;
+constexpr int STAGE2_BYTES = 8 * TILE2_BYTES / SPLIT2;
+#ifndef CORR2D_PAIR_MREG
+#define CORR2D_PAIR_MREG 0
+#endif
+#ifndef CORR2D_STAGES2
+#define CORR2D_STAGES2 3
+#endif
+constexpr int STAGES2 = CORR2D_STAGES2;
 constexpr int CH2 = 32;
 constexpr int BOX2 = 32 * CH2 * 4;           // 4 KB
-constexpr int WSTG2 = 4 * BOX2;              // 16 KB per epilogue warp
+// mirror from registers: only the direct boxes are staged (8 KB per warp)
+// CORR2D_PAIR_STG1: one staging buffer (tile + mirror box) per warp shared by
+// both planes -- half the staging, each store waits for the previous one's read
+#ifndef CORR2D_PAIR_STG1
+#define CORR2D_PAIR_STG1 1
+#endif
+constexpr int NBUF2 = CORR2D_PAIR_STG1 ? 1 : 2;  // staging buffers per epilogue warp
+constexpr int WSTG2 = (CORR2D_PAIR_MREG ? 1 : 2) * NBUF2 * BOX2;
 constexpr int STG2_BYTES = 4 * WSTG2;        // 64 KB
-constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 2 * BN * 4 + 16 * 8 + 16;
+constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 2 * BN * 4 + (2 * STAGES2 + 4) * 8 + 16;
+static_assert(SMEM2_BYTES <= 232448, "CTA-pair kernel shared memory");
 // Epilogue warps of the CTA-pair kernels: 4 (each warp both planes of its lane
 // quadrant) or 8 (warps 2-5 sync, 6-9 async).  Measured on cfg5: 4 -> 3.26 ms,
 // 8 -> 3.37 ms; the staging budget is the same 64 KB either way.
@@ -182,6 +204,19 @@ __device__ __forceinline__ uint64_t desc_sw64(uint32_t saddr) {
   return d;
 }
 
+// K-major, SWIZZLE_128B canonical layout: rows of 128 B, 8-row groups 1024 B apart.
+// The operand rows hold [hi 32 slots | lo 32 slots]: the hi operand starts at
+// byte 0 of the row, the lo operand at byte 64 (K advance inside the atom).
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;                 // layout: SWIZZLE_128B
+  return d;
+}
+
 // K-major, SWIZZLE_32B canonical layout: rows of 32 B, 8-row groups 256 B apart.
 __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
   uint64_t d = 0;
@@ -250,6 +285,12 @@ __device__ __forceinline__ void decode_tile(const Params& p, long long b, int& I
 }
 
 __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// fp32 (hi + lo) of Re'[0] and Im'[0] that K1 stores after the 2*mp packed
+// values of every BF16X2 row (the epilogue's Nyquist x DC correction operands)
+__device__ __forceinline__ float2 dc_nyq(const __nv_bfloat16* base, long long row, long long ld, int hp) {
+  return *reinterpret_cast<const float2*>(base + row * ld + 6 * hp);
+}
 
 // Per-warp epilogue staging: the warp owning TMEM lanes 32q..32q+31 stages its
 // 32 rows x 16 columns twice -- as the direct box (32 rows x 64 B, SWIZZLE_64B:
@@ -398,6 +439,37 @@ __device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane,
   }
 }
 
+// Same chunk, mirror written straight from registers: lane = tile row i holds
+// columns j..j+31, so for each k the warp's 32 values of mirror row j+k are
+// consecutive -- one full 128-B line per store instruction, no staging.
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_32_plane_mreg(uint8_t* wst, int lane, const float (&v)[32], bool mirror,
+                                                              float tsign, const CUtensorMap* map_direct,
+                                                              float* plane, long long ld_out, int n, int cbase,
+                                                              int row0q, uint64_t pol) {
+  if (lane == 0) bulk_wait_read<PENDING>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(wst + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map_direct, wst, cbase, row0q, pol);
+    bulk_commit();
+  }
+  if (mirror && row0q + lane < n) {
+    float* dst = plane + (long long)cbase * ld_out + row0q + lane;
+    const int kmax = n - cbase < 32 ? n - cbase : 32;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < kmax)
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(dst + (long long)k * ld_out),
+                     "f"(tsign * v[k]), "l"(pol) : "memory");
+  }
+}
+
 __device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS2) : "memory"); }
 
 // sync chunk c -> u[0..15], async chunk c -> u[16..31]
@@ -467,8 +539,8 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], STAGE_BYTES);
           uint8_t* base = stages + stage * STAGE_BYTES;
-          const int kre = kb * KB, kim = p.hp + kb * KB;
-          // each box carries both planes: hi tile then lo tile, contiguous
+          const int kre = kb * 2 * KB, kim = 2 * p.hp + kb * 2 * KB;
+          // each box: 128 rows x [hi 32 | lo 32] slots (128-B rows, SWIZZLE_128B)
           tma_load_3d(base + 0 * TILE_BYTES, &tmap_a, kre, I * BM, 0, &full[stage], keep);
           tma_load_3d(base + 2 * TILE_BYTES, &tmap_a, kim, I * BM, 0, &full[stage], keep);
           tma_load_3d(base + 4 * TILE_BYTES, &tmap_b, kre, J * BN, 0, &full[stage], keep);
@@ -496,10 +568,10 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
 #pragma unroll
           for (int ks = 0; ks < KB / 16; ++ks) {
             const uint32_t off = ks * 32;  // 16 bf16 = 32 bytes along K
-            const uint64_t are_h = desc_sw64(base + 0 * TILE_BYTES + off), are_l = desc_sw64(base + 1 * TILE_BYTES + off);
-            const uint64_t aim_h = desc_sw64(base + 2 * TILE_BYTES + off), aim_l = desc_sw64(base + 3 * TILE_BYTES + off);
-            const uint64_t bre_h = desc_sw64(base + 4 * TILE_BYTES + off), bre_l = desc_sw64(base + 5 * TILE_BYTES + off);
-            const uint64_t bim_h = desc_sw64(base + 6 * TILE_BYTES + off), bim_l = desc_sw64(base + 7 * TILE_BYTES + off);
+            const uint64_t are_h = desc_sw128(base + 0 * TILE_BYTES + off), are_l = desc_sw128(base + 0 * TILE_BYTES + 64 + off);
+            const uint64_t aim_h = desc_sw128(base + 2 * TILE_BYTES + off), aim_l = desc_sw128(base + 2 * TILE_BYTES + 64 + off);
+            const uint64_t bre_h = desc_sw128(base + 4 * TILE_BYTES + off), bre_l = desc_sw128(base + 4 * TILE_BYTES + 64 + off);
+            const uint64_t bim_h = desc_sw128(base + 6 * TILE_BYTES + off), bim_l = desc_sw128(base + 6 * TILE_BYTES + 64 + off);
             const uint32_t acc0 = (kb | ks) ? 1u : 0u;
             // sync  += Re.Re + Im.Im          (hi.hi + hi.lo + lo.hi each)
             umma_bf16(d_phi, are_h, bre_h, ID, acc0);
@@ -549,16 +621,16 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       float row_re0 = 0.f, row_im0 = 0.f;
       if (p.even) {
         if (gi < p.n1) {
-          const __nv_bfloat16* ar = p.a + (long long)gi * p.ld_pack;
-          row_re0 = bf2f(ar[0]) + bf2f(ar[p.split_a]);
-          row_im0 = bf2f(ar[p.hp]) + bf2f(ar[p.hp + p.split_a]);
+          const float2 d = dc_nyq(p.a, gi, p.ld_pack, p.hp);
+          row_re0 = d.x;
+          row_im0 = d.y;
         }
         const int gj = j0 + eid;
         float cre = 0.f, cim = 0.f;
         if (gj < p.n2) {
-          const __nv_bfloat16* br = p.b + (long long)gj * p.ld_pack;
-          cre = bf2f(br[0]) + bf2f(br[p.split_b]);
-          cim = bf2f(br[p.hp]) + bf2f(br[p.hp + p.split_b]);
+          const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+          cre = d.x;
+          cim = d.y;
         }
         epi_bar();   // previous tile finished reading col_* vectors
         col_re0[eid] = cre;
@@ -674,7 +746,9 @@ struct Params2 {
   int n1, n2, hp, homo, even, tma_store;
   int store_pol;          // L2 policy of the output stores: 0 evict_first, 1 normal, 2 evict_last
   int dbg;                // profiling switches: 1 = no output stores, 2 = no MMAs (results invalid)
-  int T1, T2;             // 128-row / 128-col tile counts
+  int mirror_reg;         // mirror tiles stored from registers (coalesced st.global) instead of TMA
+  long long* trace;       // profiling (CORR2D_TRACE=1): per-CTA stall cycles, 8 counters each
+  int T1, T2;            // 128-row / 128-col tile counts
   long long tile0, tile1; // pair-tile range
   const __nv_bfloat16* a;
   const __nv_bfloat16* b;
@@ -686,6 +760,17 @@ struct Params2 {
 };
 
 enum PairMode { kSkip = 4 };
+
+// Profiling: mbar_wait that adds the cycles it spent to a counter.
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long long* acc) {
+  if (acc == nullptr) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  *acc += clock64() - t0;
+}
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -711,11 +796,11 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(cluster_addr), "r"(bytes)
+  asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;\n" ::"r"(cluster_addr), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                                 uint32_t leader_bar, uint64_t pol) {
@@ -839,6 +924,71 @@ __device__ __forceinline__ void decode_quad(const Params2& p, long long b, int& 
 }
 
 // Tile of CTA `rank` of the cluster for cluster tile b: row tile i, column tile J, mode.
+// Incremental form of decode_pair for a persistent CTA that visits tiles
+// b, b + d, b + 2d, ...: (group, offset) advance with 32-bit arithmetic only;
+// the closed-form decode runs once.  Same enumeration as decode_pair.
+struct PairWalk {
+  int g, o, G, npairs, ngroups, T2, homo;
+  __device__ __forceinline__ int size(int gg) const {
+    const int Gg = min(G, npairs - gg * G);
+    return homo ? Gg * (Gg - 1) + Gg * (T2 - 2 * gg * G - 2 * Gg + 2) : Gg * T2;
+  }
+  __device__ __forceinline__ void init(const Params2& p, long long b) {
+    G = kGroup;
+    npairs = (p.T1 + 1) / 2;
+    ngroups = (npairs + G - 1) / G;
+    T2 = p.T2;
+    homo = p.homo;
+    g = 0;
+    long long base = 0;
+    if (homo) {
+      const long long T = p.T2, GG = G;
+      auto S = [&](long long gg) { return gg * GG * (T - GG + 1) - GG * GG * gg * (gg - 1); };
+      const double A2 = (double)(GG * GG), B1 = (double)(GG * (T - GG + 1) + GG * GG);
+      const double disc = B1 * B1 - 4.0 * A2 * (double)b;
+      long long gg = (long long)floor((B1 - sqrt(fmax(disc, 0.0))) / (2.0 * A2));
+      if (gg < 0) gg = 0;
+      if (gg > ngroups - 1) gg = ngroups - 1;
+      while (gg > 0 && S(gg) > b) --gg;
+      while (gg + 1 < ngroups && S(gg + 1) <= b) ++gg;
+      g = (int)gg;
+      base = S(gg);
+    } else {
+      g = (int)(b / ((long long)G * T2));
+      base = (long long)g * G * T2;
+    }
+    o = (int)(b - base);
+  }
+  __device__ __forceinline__ void advance(int d) {
+    o += d;
+    while (g < ngroups && o >= size(g)) { o -= size(g); ++g; }
+  }
+  __device__ __forceinline__ void get(const Params2& p, uint32_t rank, int& P, int& J, int& mode) const {
+    const int Gg = min(G, npairs - g * G);
+    if (!homo) {
+      J = o / Gg;
+      P = g * G + o % Gg;
+      mode = (2 * P + (int)rank < p.T1) ? kPlain : kSkip;
+      return;
+    }
+    const int ramp = (Gg - 1) * Gg;
+    if (o < ramp) {
+      int k = 0;
+      while ((k + 1) * (k + 2) <= o) ++k;
+      const int rem = o - k * (k + 1);
+      J = 2 * g * G + 2 * k + rem / (k + 1);
+      P = g * G + rem % (k + 1);
+    } else {
+      const int o2 = o - ramp;
+      J = 2 * g * G + 2 * (Gg - 1) + o2 / Gg;
+      P = g * G + o2 % Gg;
+    }
+    const int i = 2 * P + (int)rank;
+    if (i >= p.T1 || J < i) mode = kSkip;
+    else mode = (J == i) ? kDiag : kMirror;
+  }
+};
+
 template <int NPAIR>
 __device__ __forceinline__ void cluster_tile(const Params2& p, long long b, uint32_t rank, int& P, int& J, int& mode) {
   if (NPAIR == 1) {
@@ -870,6 +1020,36 @@ __device__ __forceinline__ void umma2_commit_mask(uint64_t* bar, uint16_t mask) 
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
       ::"r"(su32(bar)), "h"(mask) : "memory");
 }
+
+// Even-m Nyquist x DC correction operands of one pair tile for one epilogue
+// lane: its row (re0, im0) and the columns j0 + lane + 32 c (c < 4).  Loaded a
+// tile ahead so the L2 latency is hidden behind the previous tile's stores.
+struct NyqOperands {
+  // raw loads; consumed only in finish(), so they are not waited on where issued
+  float2 rw, cl[4];
+  float row_re0, row_im0, cre4[4], cim4[4];
+  __device__ __forceinline__ void load(const Params2& p, int gi, int j0, int lane) {
+    rw = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cl[k] = make_float2(0.f, 0.f);
+    if (!p.even) return;
+    if (gi < p.n1) rw = dc_nyq(p.a, gi, p.ld_pack, p.hp);
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const int gj = j0 + 32 * c4 + lane;
+      if (gj < p.n2) cl[c4] = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+    }
+  }
+  __device__ __forceinline__ void finish() {
+    row_re0 = rw.x;
+    row_im0 = rw.y;
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      cre4[c4] = cl[c4].x;
+      cim4[c4] = cl[c4].y;
+    }
+  }
+};
 
 template <int NPAIR>
 __global__ void __launch_bounds__(THREADS2, 1)
@@ -903,6 +1083,9 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
   const uint16_t all_mask = (uint16_t)((1u << (2 * NPAIR)) - 1);
   const long long cid = cluster_id_x(), ncl = num_clusters_x();
   const int nkb = p.hp / KB;
+  long long* tr = p.trace ? p.trace + blockIdx.x * 16 : nullptr;
+  long long tr_wait = 0, tr_wait2 = 0, tr_store = 0, tr_dec = 0, tr_pre = 0;
+  const long long tr_t0 = clock64();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 2); mbar_init(&empty[s], NPAIR); }
@@ -926,17 +1109,21 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
       const uint64_t keep = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
+      PairWalk walk;
+      walk.init(p, p.tile0 + cid);
+      for (long long t = p.tile0 + cid; t < p.tile1; t += ncl, walk.advance((int)ncl)) {
         int P, J, mode;
-        cluster_tile<NPAIR>(p, t, rank, P, J, mode);
+        if (NPAIR == 1) walk.get(p, rank, P, J, mode);
+        else cluster_tile<NPAIR>(p, t, rank, P, J, mode);
         const int arow = (2 * P + (int)prank) * BM, brow = J * BN;
         // pair CTA0: Bx = Re', By = Im'    pair CTA1: Bx = -Im', By = Re'
-        const int kx = leader ? 0 : 2 * p.hp, ky = leader ? p.hp : 0;
+        const int kx = leader ? 0 : 4 * p.hp, ky = leader ? 2 * p.hp : 0;  // third t at 2 * t * hp
         // NPAIR == 2: the first pair's CTAs load A for both pairs (multicast)
         const bool load_a = (NPAIR == 1) || rank < 2;
         const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+        for (int h = 0; h < nkb * SPLIT2; ++h) {
+          const int kb = h / SPLIT2, part = h % SPLIT2;
+          mbar_wait_t(&empty[stage], phase ^ 1, tr ? &tr_wait : nullptr);
           const uint32_t lbar = mapa_rank(su32(&full[stage]), lrank);
           if (p.dbg & 4) {            // profiling: no operand traffic at all
             mbar_arrive_remote(lbar);
@@ -945,17 +1132,22 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
           }
           mbar_expect_tx_remote(lbar, STAGE_BYTES);
           uint8_t* base = stages + stage * STAGE_BYTES;
-          const int k0 = kb * KB;
-          // each box carries both planes: hi tile then lo tile, contiguous
-          if (NPAIR == 1) {
+          const int k0 = kb * 2 * KB;
+          // each box: 128 rows x [hi KB | lo KB] slots (128-B rows, SWIZZLE_128B)
+          if (SPLIT2 == 2) {
+            tma_load_3d_2sm(base, &tmap_a, part * 2 * p.hp + k0, arow, 0, lbar, keep);
+            tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_b, (part ? ky : kx) + k0, brow, 0, lbar, keep);
+          } else if (NPAIR == 1) {
             tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
-            tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 0, lbar, keep);
+            tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, 2 * p.hp + k0, arow, 0, lbar, keep);
           } else if (load_a) {
             tma_load_3d_2sm_mc(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, su32(&full[stage]), a_mask, keep);
-            tma_load_3d_2sm_mc(base + 2 * TILE_BYTES, &tmap_a, p.hp + k0, arow, 0, su32(&full[stage]), a_mask, keep);
+            tma_load_3d_2sm_mc(base + 2 * TILE_BYTES, &tmap_a, 2 * p.hp + k0, arow, 0, su32(&full[stage]), a_mask, keep);
           }
-          tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, kx + k0, brow, 0, lbar, keep);
-          tma_load_3d_2sm(base + 6 * TILE_BYTES, &tmap_b, ky + k0, brow, 0, lbar, keep);
+          if (SPLIT2 == 1) {
+            tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, kx + k0, brow, 0, lbar, keep);
+            tma_load_3d_2sm(base + 6 * TILE_BYTES, &tmap_b, ky + k0, brow, 0, lbar, keep);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -969,22 +1161,36 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
       int acc = 0;
       uint32_t acc_phase = 0;
       for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait_t(&tempty[acc], acc_phase ^ 1, tr ? &tr_wait2 : nullptr);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * 256;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+        for (int h = 0; h < nkb * SPLIT2; ++h) {
+          const int kb = h;  // (SPLIT2 == 2: half k-block index)
+          mbar_wait_t(&full[stage], phase, tr ? &tr_wait : nullptr);
           tc_fence_after();
-          if (lane == 0) {
+          if (lane == 0 && SPLIT2 == 2) {
             const uint32_t base = su32(stages + stage * STAGE_BYTES);
 #pragma unroll
             for (int ks = 0; ks < KB / 16; ++ks) {
               const uint32_t off = ks * 32;
-              auto desc = [](uint32_t a) { return KB == 16 ? desc_sw32(a) : desc_sw64(a); };
-              const uint64_t are_h = desc(base + 0 * TILE_BYTES + off), are_l = desc(base + 1 * TILE_BYTES + off);
-              const uint64_t aim_h = desc(base + 2 * TILE_BYTES + off), aim_l = desc(base + 3 * TILE_BYTES + off);
-              const uint64_t bx_h = desc(base + 4 * TILE_BYTES + off), bx_l = desc(base + 5 * TILE_BYTES + off);
-              const uint64_t by_h = desc(base + 6 * TILE_BYTES + off), by_l = desc(base + 7 * TILE_BYTES + off);
+              const uint64_t a_h = desc_sw128(base + off), a_l = desc_sw128(base + 64 + off);
+              const uint64_t b_h = desc_sw128(base + 2 * TILE_BYTES + off), b_l = desc_sw128(base + 2 * TILE_BYTES + 64 + off);
+              if (p.dbg & 2) continue;
+              umma2_bf16(d, a_h, b_h, ID, (h | ks) ? 1u : 0u);
+              umma2_bf16(d, a_h, b_l, ID, 1);
+              umma2_bf16(d, a_l, b_h, ID, 1);
+            }
+            umma2_commit_mask(&empty[stage], all_mask);
+            if (h == nkb * SPLIT2 - 1) umma2_commit_mask(&tfull[acc], pair_mask);
+          } else if (lane == 0) {
+            const uint32_t base = su32(stages + stage * STAGE_BYTES);
+#pragma unroll
+            for (int ks = 0; ks < KB / 16; ++ks) {
+              const uint32_t off = ks * 32;
+              const uint64_t are_h = desc_sw128(base + 0 * TILE_BYTES + off), are_l = desc_sw128(base + 0 * TILE_BYTES + 64 + off);
+              const uint64_t aim_h = desc_sw128(base + 2 * TILE_BYTES + off), aim_l = desc_sw128(base + 2 * TILE_BYTES + 64 + off);
+              const uint64_t bx_h = desc_sw128(base + 4 * TILE_BYTES + off), bx_l = desc_sw128(base + 4 * TILE_BYTES + 64 + off);
+              const uint64_t by_h = desc_sw128(base + 6 * TILE_BYTES + off), by_l = desc_sw128(base + 6 * TILE_BYTES + 64 + off);
               const uint32_t acc0 = (kb | ks) ? 1u : 0u;
               if (p.dbg & 2) continue;
               umma2_bf16(d, are_h, bx_h, ID, acc0);
@@ -1020,37 +1226,59 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
     int acc = 0;
     uint32_t acc_phase = 0;
     float mphi = 0.f, mpsi = 0.f, chk = 0.f;
+    PairWalk walk;
+    walk.init(p, p.tile0 + cid);
+    // the NEXT tile's correction operands are prefetched one tile ahead
+    NyqOperands nyq_next;
+    int P, J, mode;
+    if (p.tile0 + cid < p.tile1) {
+      if (NPAIR == 1) walk.get(p, rank, P, J, mode);
+      else cluster_tile<NPAIR>(p, p.tile0 + cid, rank, P, J, mode);
+      nyq_next.load(p, (2 * P + (int)prank) * BM + r, J * BN, lane);
+    }
     for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
-      int P, J, mode;
-      cluster_tile<NPAIR>(p, t, rank, P, J, mode);
+      const long long tp0 = tr ? clock64() : 0;
+      NyqOperands nyq = nyq_next;
       const int i0 = (2 * P + (int)prank) * BM, j0 = J * BN;
       const int gi = i0 + r;
-      if (mode != kSkip) {
-        float row_re0 = 0.f, row_im0 = 0.f;
+      const int cur_mode = mode;
+      // decode and prefetch the next tile of this CTA
+      if (t + ncl < p.tile1) {
+        walk.advance((int)ncl);
+        if (NPAIR == 1) walk.get(p, rank, P, J, mode);
+        else cluster_tile<NPAIR>(p, t + ncl, rank, P, J, mode);
+        if (mode != kSkip) nyq_next.load(p, (2 * P + (int)prank) * BM + r, J * BN, lane);
+      }
+      if (tr) tr_dec += clock64() - tp0;
+      if (cur_mode != kSkip) {
+        const int mode = cur_mode;
+        const bool use_tma = p.tma_store && mode != kDiag;
+        // even-m Nyquist x DC correction operands: this lane's row, and (TMA
+        // path) columns j0 + lane + 32 c held per lane and broadcast by
+        // shuffles -- no CTA-wide barrier on the common path
+        nyq.finish();
+        const float row_re0 = nyq.row_re0, row_im0 = nyq.row_im0;
         if (p.even) {
-          if (gi < p.n1) {
-            const __nv_bfloat16* ar = p.a + (long long)gi * p.ld_pack;
-            row_re0 = bf2f(ar[0]) + bf2f(ar[p.split_a]);
-            row_im0 = bf2f(ar[p.hp]) + bf2f(ar[p.hp + p.split_a]);
+          if (!use_tma) {
+            const int gj = j0 + eid;
+            float cre = 0.f, cim = 0.f;
+            if (eid < BN && gj < p.n2) {
+              const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+              cre = d.x;
+              cim = d.y;
+            }
+            epi_bar256();   // diagonal tiles only: every epilogue warp of the CTA takes this branch
+            if (eid < BN) {
+              col_re0[eid] = cre;
+              col_im0[eid] = cim;
+            }
+            epi_bar256();
           }
-          const int gj = j0 + eid;
-          float cre = 0.f, cim = 0.f;
-          if (eid < BN && gj < p.n2) {
-            const __nv_bfloat16* br = p.b + (long long)gj * p.ld_pack;
-            cre = bf2f(br[0]) + bf2f(br[p.split_b]);
-            cim = bf2f(br[p.hp]) + bf2f(br[p.hp + p.split_b]);
-          }
-          epi_bar256();
-          if (eid < BN) {
-            col_re0[eid] = cre;
-            col_im0[eid] = cim;
-          }
-          epi_bar256();
         }
         const bool direct = gi < p.n1;
         const bool mirror = (mode != kPlain) && gi < p.n2;
-        const bool use_tma = p.tma_store && mode != kDiag;
-        mbar_wait(&tfull[acc], acc_phase);
+        if (tr) tr_pre += clock64() - tp0;
+        mbar_wait_t(&tfull[acc], acc_phase, tr ? &tr_wait : nullptr);
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
         if (use_tma) {
@@ -1064,27 +1292,52 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
           for (int c = 0; c < BN / CH2; ++c) {
 #pragma unroll 1
             for (int plane = pw; plane < pw + PPW2; ++plane) {
-              uint8_t* wst = staging + ((warp - 2) * PPW2 + (plane - pw)) * (2 * BOX2);
+              uint8_t* wst = staging + (warp - 2) * WSTG2 + (NBUF2 == 1 ? 0 : (plane - pw)) * (WSTG2 / NBUF2);
               const float tsign = plane == 0 ? 1.f : -1.f;
               float mx = 0.f;
               uint32_t ua[32];
+              const long long tq0 = tr ? clock64() : 0;
               tmem_ld32(tbase + plane * 128 + c * CH2, ua);
               tmem_wait_ld_tie(ua);
+              if (tr) tr_wait2 += clock64() - tq0;
               float v[32];
 #pragma unroll
               for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(ua[k]);
               if (plane == 1 && p.even) {
+                float cr = nyq.cre4[0], ci = nyq.cim4[0];
+                if (c == 1) { cr = nyq.cre4[1]; ci = nyq.cim4[1]; }
+                if (c == 2) { cr = nyq.cre4[2]; ci = nyq.cim4[2]; }
+                if (c == 3) { cr = nyq.cre4[3]; ci = nyq.cim4[3]; }
 #pragma unroll
-                for (int k = 0; k < 32; ++k) v[k] -= row_im0 * col_re0[c * CH2 + k] - row_re0 * col_im0[c * CH2 + k];
+                for (int k = 0; k < 32; ++k)
+                  v[k] -= row_im0 * __shfl_sync(0xffffffffu, cr, k) - row_re0 * __shfl_sync(0xffffffffu, ci, k);
               }
+              {
+                // max |v| and the finite check in one integer-max tree: |v|'s
+                // bit pattern orders like |v|, and Inf / NaN patterns exceed
+                // every finite one
+                uint32_t mb[16];
 #pragma unroll
-              for (int k = 0; k < 32; ++k) {
-                mx = fmaxf(mx, fabsf(v[k]));
-                chk = fmaf(v[k], 0.f, chk);
+                for (int k = 0; k < 16; ++k)
+                  mb[k] = max(__float_as_uint(v[k]) & 0x7fffffffu, __float_as_uint(v[k + 16]) & 0x7fffffffu);
+#pragma unroll
+                for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+                  for (int k = 0; k < w; ++k) mb[k] = max(mb[k], mb[k + w]);
+                if (mb[0] >= 0x7f800000u) chk = __int_as_float(0x7fc00000);
+                else mx = __uint_as_float(mb[0]);
               }
-              if (!(p.dbg & 1))
-                stage_and_store_32_plane<PPW2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
+              const long long ts0 = tr ? clock64() : 0;
+              if (p.dbg & 1) {
+              } else if (p.mirror_reg) {
+                stage_and_store_32_plane_mreg<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
+                                                        plane == 0 ? p.phi : p.psi, p.ld_out, p.n1,
+                                                        j0 + c * CH2, i0 + 32 * q, drop);
+              } else {
+                stage_and_store_32_plane<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
                                                    j0 + c * CH2, i0 + 32 * q, drop);
+              }
+              if (tr) tr_store += clock64() - ts0;
               if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
             }
           }
@@ -1164,6 +1417,11 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
   }
 
   tc_fence_before();
+  if (tr && lane == 0) {
+    if (warp == 0) { tr[0] = tr_wait; tr[4] = clock64() - tr_t0; }
+    if (warp == 1) { tr[1] = tr_wait; tr[2] = tr_wait2; }
+    if (warp == 2) { tr[3] = tr_wait; tr[5] = tr_wait2; tr[6] = tr_store; tr[7] = tr_dec; tr[8] = tr_pre; }
+  }
   cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
@@ -1183,19 +1441,19 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Operand boxes carry both bf16 planes: {KB, 128 rows, 2} with SWIZZLE_64B
-// (1-SM kernel, KB = 32) or {KB2, 128, 2} with SWIZZLE_32B (CTA-pair kernels).
-static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows, long long split,
-                            bool pair_kernel) {
+// Operand boxes: 128 rows x 64 bf16 = one 32-slot k-block of one third with its
+// hi and lo halves ([hi 32 | lo 32], 128-B rows, SWIZZLE_128B).  Measured with
+// tools/microbench/tmaloads.cu: 128-B box rows stream L2 -> SMEM at ~20 TB/s
+// chip-wide, the former 64-B rows (separate hi / lo planes) at ~11 TB/s.
+static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows) {
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 2};
-  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)split * 2};
-  cuuint32_t box[3] = {pair_kernel ? (cuuint32_t)KB2 : (cuuint32_t)KB, BM, 2};
+  cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * (cuuint64_t)rows};
+  cuuint32_t box[3] = {2 * KB, BM, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  (pair_kernel && KB2 == 16) ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return CORR2D_OK;
@@ -1279,10 +1537,11 @@ extern "C" int corr2d_contract_bf16x3(
   using namespace corr2d::tc;
   if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: null pointer");
   if (n1 < 1 || n2 < 1 || m < 2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad sizes");
-  if (mp != corr2d_packed_depth(m, CORR2D_PACK_BF16X2) || ld_pack < mp || (ld_pack % 32) != 0)
-    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: packed depth / ld_pack mismatch (ld_pack % 32 == 0)");
-  if (split_a < (long long)n1 * ld_pack || split_b < (long long)n2 * ld_pack || (split_a % 8) || (split_b % 8))
-    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad plane split");
+  (void)split_a;
+  (void)split_b;  // planes are interleaved per k-block (ABI v2); kept for signature stability
+  if (mp != corr2d_packed_depth(m, CORR2D_PACK_BF16X2) || ld_pack < 2 * (long long)mp + 64 || (ld_pack % 64) != 0)
+    return fail(CORR2D_ERR_DATA,
+                "corr2d_contract_bf16x3: packed depth / ld_pack mismatch (ld_pack >= 2*mp + 64, % 64 == 0)");
   if (row0 < 0 || row1 > n1 || row0 >= row1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad row range");
   if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: ld_out < n2");
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: homo needs n1 == n2");
@@ -1294,9 +1553,9 @@ extern "C" int corr2d_contract_bf16x3(
                        ((reinterpret_cast<uintptr_t>(psi) & 15) == 0);
   const bool pair_kernel = bf16_variant(n1, row0, row1, aligned) != 0;
   CUtensorMap ma, mb;
-  int rc = make_operand_map(&ma, a, ld_pack, n1, split_a, pair_kernel);
+  int rc = make_operand_map(&ma, a, ld_pack, n1);
   if (rc) return rc;
-  rc = make_operand_map(&mb, b, ld_pack, n2, split_b, pair_kernel);
+  rc = make_operand_map(&mb, b, ld_pack, n2);
   if (rc) return rc;
   OutMaps om;
   memset(&om, 0, sizeof(om));
@@ -1328,7 +1587,16 @@ extern "C" int corr2d_contract_bf16x3(
     p.store_pol = sp ? atoi(sp) : 0;
     const char* dbg = getenv("CORR2D_DEBUG_SKIP");
     p.dbg = dbg ? atoi(dbg) : 0;
-    p.T1 = (n1 + BM - 1) / BM; p.T2 = (n2 + BN - 1) / BN;
+    const char* mreg = getenv("CORR2D_MIRROR_REG");
+    p.mirror_reg = CORR2D_PAIR_MREG ? 1 : (mreg ? atoi(mreg) : 0);
+    static long long* trace_buf = nullptr;
+    const char* trc = getenv("CORR2D_TRACE");
+    if (trc && trc[0] == '1') {
+      if (!trace_buf) cudaMalloc(&trace_buf, 1024 * 16 * sizeof(long long));
+      cudaMemsetAsync(trace_buf, 0, 1024 * 16 * sizeof(long long), st);
+      p.trace = trace_buf;
+    }
+    p.T1 =(n1 + BM - 1) / BM; p.T2 = (n2 + BN - 1) / BN;
     p.tile0 = tile0; p.tile1 = tile1;
     p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
     p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
@@ -1358,6 +1626,18 @@ extern "C" int corr2d_contract_bf16x3(
     const long long clusters = work < max_clusters ? work : max_clusters;
     cfg.gridDim = dim3((unsigned)(csize * clusters));
     cudaLaunchKernelEx(&cfg, kern, ma, mb, om, p);
+    if (p.trace) {  // profiling: average stall cycles per CTA role
+      static long long h[1024 * 16];
+      cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const int nb = (int)cfg.gridDim.x;
+      double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int c = 0; c < nb; ++c)
+        for (int k = 0; k < 9; ++k) acc[k] += (double)h[c * 16 + k] / nb;
+      fprintf(stderr, "trace: total %.0f cyc | producer wait-empty %.0f | mma wait-full %.0f (leaders x2) "
+              "wait-tempty %.0f | epi wait-tfull %.0f tmem-ld %.0f store %.0f decode %.0f preamble %.0f\n", acc[4], acc[0],
+              2 * acc[1], 2 * acc[2], acc[3], acc[5], acc[6], acc[7], acc[8]);
+    }
     return check_launch(variant == 2 ? "contract_bf16x3_2sm_kernel<2>" : "contract_bf16x3_2sm_kernel<1>");
   }
   Params p{};

@@ -70,16 +70,8 @@ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 mul_mi(double2 a) { return make_double2(a.y, -a.x); }   // a * (-i)
 
-__device__ __forceinline__ void store_pack(const PrepParams& p, void* base, long long idx, double v) {
-  if (p.pack_kind == CORR2D_PACK_F64) {
-    static_cast<double*>(base)[idx] = v;
-  } else {
-    __nv_bfloat16 hi = __double2bfloat16(v);
-    double rest = v - (double)__bfloat162float(hi);
-    __nv_bfloat16 lo = __double2bfloat16(rest);
-    static_cast<__nv_bfloat16*>(base)[idx] = hi;
-    static_cast<__nv_bfloat16*>(base)[idx + p.split_plane] = lo;
-  }
+__device__ __forceinline__ void store_pack(const PrepParams&, void* base, long long idx, double v) {
+  static_cast<double*>(base)[idx] = v;   // CORR2D_PACK_F64 (bf16 packing is vectorised below)
 }
 
 // In-register forward DFTs of length 2, 4, 8 (natural order in and out).
@@ -411,14 +403,20 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
         v[1][0][u] = ih; v[1][1][u] = il;
         v[2][0][u] = __hneg(ih); v[2][1][u] = __hneg(il);
       }
-      const long long o = (long long)(c0 + c) * p.ld_pack + q0;
+      // row layout: third t, 32-slot block k -> [hi 32 | lo 32] at t*2hp + 64k
+      const long long o = (long long)(c0 + c) * p.ld_pack + (q0 >> 5) * 64 + (q0 & 31);
+      // after the 2*mp packed values: fp32 (hi + lo) of Re'[0] and Im'[0], the
+      // contraction epilogue's Nyquist x DC correction operands
+      const float2 dcn = make_float2(__bfloat162float(v[0][0][0]) + __bfloat162float(v[0][1][0]),
+                                     __bfloat162float(v[1][0][0]) + __bfloat162float(v[1][1][0]));
       auto put = [&](void* base) {
         __nv_bfloat16* b = static_cast<__nv_bfloat16*>(base);
 #pragma unroll
         for (int t3 = 0; t3 < 3; ++t3)
 #pragma unroll
           for (int pl = 0; pl < 2; ++pl)
-            *reinterpret_cast<uint2*>(b + o + t3 * hp + pl * p.split_plane) = *reinterpret_cast<const uint2*>(v[t3][pl]);
+            *reinterpret_cast<uint2*>(b + o + t3 * 2 * hp + pl * 32) = *reinterpret_cast<const uint2*>(v[t3][pl]);
+        if (q0 == 0) *reinterpret_cast<float2*>(b + (long long)(c0 + c) * p.ld_pack + 6 * hp) = dcn;
       };
       if (p.pack_roles & CORR2D_ROLE_A) put(p.a_phi);
       if (p.pack_roles & CORR2D_ROLE_B) put(p.b);
@@ -516,7 +514,12 @@ extern "C" int corr2d_prep(
   p.do_fft = (half_out != nullptr) || (pack_kind != CORR2D_PACK_NONE);
   if (pack_kind != CORR2D_PACK_NONE) {
     p.mp = corr2d_packed_depth(m, pack_kind);
-    if (ld_pack < p.mp) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_pack < packed depth");
+    if (pack_kind == CORR2D_PACK_BF16X2) {
+      if (ld_pack < 2 * (long long)p.mp + 64 || ld_pack % 64)
+        return fail(CORR2D_ERR_DATA, "corr2d_prep: bf16 ld_pack must be >= 2 * packed depth + 64 and a multiple of 64");
+    } else if (ld_pack < p.mp) {
+      return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_pack < packed depth");
+    }
     if ((pack_roles & CORR2D_ROLE_A) && (!a_phi || (pack_kind == CORR2D_PACK_F64 && !a_psi)))
       return fail(CORR2D_ERR_DATA, "corr2d_prep: A operands missing");
     if ((pack_roles & CORR2D_ROLE_B) && !b) return fail(CORR2D_ERR_DATA, "corr2d_prep: B operand missing");

@@ -262,17 +262,18 @@ class CorrelationPlan:
         self.row0, self.row1 = (0, self.n1) if rows is None else (int(rows[0]), int(rows[1]))
         # tile-range partition of the (shard's) tile enumeration; -1 = to the end
         self.tile0, self.tile1 = (0, -1) if tiles is None else (int(tiles[0]), int(tiles[1]))
-        planes = 1 if self.pack_kind == _abi.PACK_F64 else 2
-        self.split1 = self.n1 * self.mp
-        self.split2 = self.n2 * self.mp
-        dev = self.dev
-        self.a_phi = t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
         bf16 = self.pack_kind == _abi.PACK_BF16X2
-        # bf16 pair layout: one format for both roles (a_psi unused, homo B == A)
-        self.a_psi = None if bf16 else t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
-        self.b = self.a_phi.new_empty((planes, self.n2, self.mp)) if not self.homo else None
+        # row pitch of the packed operands: bf16 rows carry hi and lo of every
+        # slot, interleaved per 32-slot block, then the fp32 DC / Nyquist pair
+        # in a 128-byte pad (include/corr2d.h)
+        self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
+        dev = self.dev
+        self.a_phi = t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
+        # bf16: one format for both roles (a_psi unused, homo B == A)
+        self.a_psi = None if bf16 else t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
+        self.b = self.a_phi.new_empty((self.n2, self.ld_pack)) if not self.homo else None
         if self.homo:
-            self.b_homo = self.a_phi if bf16 else t.empty((planes, self.n1, self.mp), dtype=pdt, device=dev)
+            self.b_homo = self.a_phi if bf16 else t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
         else:
             self.b_homo = None
         nrows = self.row1 - self.row0
@@ -328,11 +329,11 @@ class CorrelationPlan:
             roles1 = _abi.ROLE_A
         launch_prep(lib, self.raw1, self.recipe1, norm=self.norm, pack_kind=self.pack_kind, roles=roles1,
                     a_phi=self.a_phi, a_psi=self.a_psi, b=self.b_homo if self.homo else None,
-                    ld_pack=self.mp, split_plane=self.split1, ref_out=self.ref1,
+                    ld_pack=self.ld_pack, ref_out=self.ref1,
                     sigma_out=self.sigma1, status=self.status1)
         if not self.homo:
             launch_prep(lib, self.raw2, self.recipe2, norm=self.norm, pack_kind=self.pack_kind,
-                        roles=_abi.ROLE_B, b=self.b, ld_pack=self.mp, split_plane=self.split2,
+                        roles=_abi.ROLE_B, b=self.b, ld_pack=self.ld_pack,
                         ref_out=self.ref2, sigma_out=self.sigma2, status=self.status2)
 
     def launch_contract(self):
@@ -340,13 +341,12 @@ class CorrelationPlan:
         homo = 1 if self.homo else 0
         if self.pack_kind == _abi.PACK_F64:
             code = lib.corr2d_contract_f64(
-                ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.mp, self.n1, self.n2, self.mp,
+                ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.ld_pack, self.n1, self.n2, self.mp,
                 homo, self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi),
                 self.n2, ptr(self.stats), stream_handle())
         else:
             code = lib.corr2d_contract_bf16x3(
-                ptr(self.a_phi), ptr(self.bop), self.mp, self.split1,
-                self.split1 if self.homo else self.split2, self.n1, self.n2, self.mp, self.m, homo,
+                ptr(self.a_phi), ptr(self.bop), self.ld_pack, 0, 0, self.n1, self.n2, self.mp, self.m, homo,
                 self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
                 ptr(self.stats), stream_handle())
         _abi.check(code, lib)

@@ -45,7 +45,7 @@ def test_sm100a_cubin_present():
 
 def test_host_helpers():
     lib = _abi.load()
-    assert lib.corr2d_abi_version() == 1
+    assert lib.corr2d_abi_version() == 2
     assert lib.corr2d_packed_depth(11, _abi.PACK_F64) == 12
     assert lib.corr2d_packed_depth(64, _abi.PACK_F64) == 64
     assert lib.corr2d_packed_depth(512, _abi.PACK_BF16X2) == 768   # [Re' | Im' | -Im'], 256 each
