@@ -78,8 +78,15 @@ constexpr int STAGE2_BYTES = 8 * TILE2_BYTES / SPLIT2;
 #define CORR2D_STAGES2 3
 #endif
 constexpr int STAGES2 = CORR2D_STAGES2;
-constexpr int CH2 = 32;
-constexpr int BOX2 = 32 * CH2 * 4;           // 4 KB
+#ifndef CORR2D_CH2
+#define CORR2D_CH2 32
+#endif
+#ifndef CORR2D_EPI_WARPS2
+#define CORR2D_EPI_WARPS2 4
+#endif
+constexpr int CH2 = CORR2D_CH2;              // epilogue chunk width (16 or 32 columns)
+static_assert(CH2 == 16 || CH2 == 32, "epilogue chunk");
+constexpr int BOX2 = 32 * CH2 * 4;           // one 32-row box: 4 KB (CH2 32) / 2 KB (CH2 16)
 // mirror from registers: only the direct boxes are staged (8 KB per warp)
 // CORR2D_PAIR_STG1: one staging buffer (tile + mirror box) per warp shared by
 // both planes -- half the staging, each store waits for the previous one's read
@@ -88,13 +95,13 @@ constexpr int BOX2 = 32 * CH2 * 4;           // 4 KB
 #endif
 constexpr int NBUF2 = CORR2D_PAIR_STG1 ? 1 : 2;  // staging buffers per epilogue warp
 constexpr int WSTG2 = (CORR2D_PAIR_MREG ? 1 : 2) * NBUF2 * BOX2;
-constexpr int STG2_BYTES = 4 * WSTG2;        // 64 KB
+constexpr int STG2_BYTES = CORR2D_EPI_WARPS2 * WSTG2;
 constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 2 * BN * 4 + (2 * STAGES2 + 4) * 8 + 16;
 static_assert(SMEM2_BYTES <= 232448, "CTA-pair kernel shared memory");
 // Epilogue warps of the CTA-pair kernels: 4 (each warp both planes of its lane
 // quadrant) or 8 (warps 2-5 sync, 6-9 async).  Measured on cfg5: 4 -> 3.26 ms,
 // 8 -> 3.37 ms; the staging budget is the same 64 KB either way.
-constexpr int EPI_WARPS2 = 4;
+constexpr int EPI_WARPS2 = CORR2D_EPI_WARPS2;
 constexpr int PPW2 = 8 / EPI_WARPS2;         // planes per epilogue warp
 constexpr int THREADS2 = 64 + 32 * EPI_WARPS2;
 
@@ -253,6 +260,8 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t (&v)[32]) { tmem_ld32(taddr, v); }
+__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16(taddr, v); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
@@ -470,6 +479,60 @@ __device__ __forceinline__ void stage_and_store_32_plane_mreg(uint8_t* wst, int 
   }
 }
 
+// 16-column variant: direct box 32 rows x 64 B (SWIZZLE_64B: 16-B chunk j of
+// row l at j ^ ((l >> 1) & 3)) and mirror box 16 rows x 128 B (SWIZZLE_128B).
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_16_plane(uint8_t* wst, int lane, const float (&v)[16], bool mirror,
+                                                         float tsign, const CUtensorMap* map_direct,
+                                                         const CUtensorMap* map_mirror, int cbase, int row0q,
+                                                         uint64_t pol) {
+  uint8_t* dbox = wst;
+  uint8_t* mbox = wst + 2048;
+  if (lane == 0) bulk_wait_read<PENDING>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<float4*>(dbox + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  if (mirror) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      *reinterpret_cast<float*>(mbox + k * 128 + (((lane >> 2) ^ (k & 7)) * 16) + (lane & 3) * 4) = tsign * v[k];
+  }
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map_direct, dbox, cbase, row0q, pol);
+    if (mirror) tma_store_2d(map_mirror, mbox, row0q, cbase, pol);
+    bulk_commit();
+  }
+}
+
+// overloads by chunk width, so the chunk loop compiles for either CH2
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_plane(uint8_t* w, int l, const float (&v)[32], bool m, float s,
+                                                      const CUtensorMap* md, const CUtensorMap* mm, int c, int r,
+                                                      uint64_t pol) {
+  stage_and_store_32_plane<PENDING>(w, l, v, m, s, md, mm, c, r, pol);
+}
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_plane(uint8_t* w, int l, const float (&v)[16], bool m, float s,
+                                                      const CUtensorMap* md, const CUtensorMap* mm, int c, int r,
+                                                      uint64_t pol) {
+  stage_and_store_16_plane<PENDING>(w, l, v, m, s, md, mm, c, r, pol);
+}
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_mreg(uint8_t* w, int l, const float (&v)[32], bool m, float s,
+                                                     const CUtensorMap* md, float* pl, long long ld, int n, int c,
+                                                     int r, uint64_t pol) {
+  stage_and_store_32_plane_mreg<PENDING>(w, l, v, m, s, md, pl, ld, n, c, r, pol);
+}
+template <int PENDING>
+__device__ __forceinline__ void stage_and_store_mreg(uint8_t*, int, const float (&)[16], bool, float,
+                                                     const CUtensorMap*, float*, long long, int, int, int, uint64_t) {
+  __trap();  // register-mirror path exists for 32-column chunks only
+}
+
 __device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS2) : "memory"); }
 
 // sync chunk c -> u[0..15], async chunk c -> u[16..31]
@@ -487,6 +550,12 @@ __device__ __forceinline__ void tmem_wait_ld_tie(uint32_t (&u)[32]) {
                  "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15]),
                  "+r"(u[16]), "+r"(u[17]), "+r"(u[18]), "+r"(u[19]), "+r"(u[20]), "+r"(u[21]), "+r"(u[22]), "+r"(u[23]),
                  "+r"(u[24]), "+r"(u[25]), "+r"(u[26]), "+r"(u[27]), "+r"(u[28]), "+r"(u[29]), "+r"(u[30]), "+r"(u[31])
+               :: "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld_tie(uint32_t (&u)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
+                 "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15])
                :: "memory");
 }
 
@@ -1295,33 +1364,34 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               uint8_t* wst = staging + (warp - 2) * WSTG2 + (NBUF2 == 1 ? 0 : (plane - pw)) * (WSTG2 / NBUF2);
               const float tsign = plane == 0 ? 1.f : -1.f;
               float mx = 0.f;
-              uint32_t ua[32];
+              uint32_t ua[CH2];
               const long long tq0 = tr ? clock64() : 0;
-              tmem_ld32(tbase + plane * 128 + c * CH2, ua);
+              tmem_ld_n(tbase + plane * 128 + c * CH2, ua);
               tmem_wait_ld_tie(ua);
               if (tr) tr_wait2 += clock64() - tq0;
-              float v[32];
+              float v[CH2];
 #pragma unroll
-              for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(ua[k]);
+              for (int k = 0; k < CH2; ++k) v[k] = __uint_as_float(ua[k]);
               if (plane == 1 && p.even) {
+                const int c4 = (c * CH2) >> 5, l0 = (c * CH2) & 31;
                 float cr = nyq.cre4[0], ci = nyq.cim4[0];
-                if (c == 1) { cr = nyq.cre4[1]; ci = nyq.cim4[1]; }
-                if (c == 2) { cr = nyq.cre4[2]; ci = nyq.cim4[2]; }
-                if (c == 3) { cr = nyq.cre4[3]; ci = nyq.cim4[3]; }
+                if (c4 == 1) { cr = nyq.cre4[1]; ci = nyq.cim4[1]; }
+                if (c4 == 2) { cr = nyq.cre4[2]; ci = nyq.cim4[2]; }
+                if (c4 == 3) { cr = nyq.cre4[3]; ci = nyq.cim4[3]; }
 #pragma unroll
-                for (int k = 0; k < 32; ++k)
-                  v[k] -= row_im0 * __shfl_sync(0xffffffffu, cr, k) - row_re0 * __shfl_sync(0xffffffffu, ci, k);
+                for (int k = 0; k < CH2; ++k)
+                  v[k] -= row_im0 * __shfl_sync(0xffffffffu, cr, l0 + k) - row_re0 * __shfl_sync(0xffffffffu, ci, l0 + k);
               }
               {
                 // max |v| and the finite check in one integer-max tree: |v|'s
                 // bit pattern orders like |v|, and Inf / NaN patterns exceed
                 // every finite one
-                uint32_t mb[16];
+                uint32_t mb[CH2 / 2];
 #pragma unroll
-                for (int k = 0; k < 16; ++k)
-                  mb[k] = max(__float_as_uint(v[k]) & 0x7fffffffu, __float_as_uint(v[k + 16]) & 0x7fffffffu);
+                for (int k = 0; k < CH2 / 2; ++k)
+                  mb[k] = max(__float_as_uint(v[k]) & 0x7fffffffu, __float_as_uint(v[k + CH2 / 2]) & 0x7fffffffu);
 #pragma unroll
-                for (int w = 8; w > 0; w >>= 1)
+                for (int w = CH2 / 4; w > 0; w >>= 1)
 #pragma unroll
                   for (int k = 0; k < w; ++k) mb[k] = max(mb[k], mb[k + w]);
                 if (mb[0] >= 0x7f800000u) chk = __int_as_float(0x7fc00000);
@@ -1329,13 +1399,16 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               }
               const long long ts0 = tr ? clock64() : 0;
               if (p.dbg & 1) {
+              } else if (CH2 == 16) {
+                stage_and_store_plane<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
+                                                 &outm.m[plane][1], j0 + c * CH2, i0 + 32 * q, drop);
               } else if (p.mirror_reg) {
-                stage_and_store_32_plane_mreg<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
-                                                        plane == 0 ? p.phi : p.psi, p.ld_out, p.n1,
-                                                        j0 + c * CH2, i0 + 32 * q, drop);
+                stage_and_store_mreg<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
+                                                plane == 0 ? p.phi : p.psi, p.ld_out, p.n1,
+                                                j0 + c * CH2, i0 + 32 * q, drop);
               } else {
-                stage_and_store_32_plane<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
-                                                   j0 + c * CH2, i0 + 32 * q, drop);
+                stage_and_store_plane<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
+                                                 j0 + c * CH2, i0 + 32 * q, drop);
               }
               if (tr) tr_store += clock64() - ts0;
               if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
@@ -1463,13 +1536,16 @@ static int make_operand_map(CUtensorMap* map, const void* base, long long ld, lo
 // kind 0 = 1-SM direct 16 x 32 (SWIZZLE_64B), 1 = 1-SM mirror 32 x 16 (no
 // swizzle), 2 = CTA-pair 32 x 32 boxes (SWIZZLE_128B) for tile and mirror.
 static int make_output_map(CUtensorMap* map, float* base, long long ld, long long rows, long long cols, int kind) {
+  // kind 3 / 4: CTA-pair kernels with 16-column chunks -- direct 16 x 32
+  // (SWIZZLE_64B), mirror 32 x 16 (SWIZZLE_128B)
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)CH : 32u, kind == 1 ? (cuuint32_t)CH : 32u};
+  cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)CH : (kind == 3 ? 16u : 32u),
+                       kind == 1 ? (cuuint32_t)CH : (kind == 4 ? 16u : 32u)};
   cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapSwizzle sw = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_64B
+  const CUtensorMapSwizzle sw = (kind == 0 || kind == 3) ? CU_TENSOR_MAP_SWIZZLE_64B
                               : (kind == 1 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1564,7 +1640,7 @@ extern "C" int corr2d_contract_bf16x3(
     float* planes[2] = {phi, psi};
     for (int pl = 0; pl < 2 && !rc; ++pl)
       for (int mi = 0; mi < 2 && !rc; ++mi)
-        rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, pair_kernel ? 2 : mi);
+        rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, pair_kernel ? (CH2 == 32 ? 2 : 3 + mi) : mi);
     if (rc) return rc;
   }
   int dev = 0, sms = 148;
