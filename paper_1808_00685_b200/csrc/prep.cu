@@ -18,6 +18,8 @@
 // reference bit-for-bit; the FFT is a mixed-radix Stockham transform.
 #include "common.cuh"
 
+#include <cstdio>
+
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -58,6 +60,7 @@ struct PrepParams {
   double* sigma_out;
   int* status;
   int do_fft;
+  long long* trace;        // profiling (CORR2D_PREP_TRACE=1): per-phase cycles, summed over CTAs
   int C;
   int nfactors;
   int factors[kMaxFactors];
@@ -106,15 +109,29 @@ template <> __device__ __forceinline__ void dft_r<8>(double2 (&x)[8]) {
 
 // One Stockham stage of radix R over CH interleaved columns (pairs of channels).
 //   output (j, u) = sum_t in[j + t m/R] W_m^{t k span} W_R^{t u},  k = j mod Ns
-template <int R>
+// NORM (first stage only): the loaded values are (v - ref) / scale of their
+// channel -- the same two IEEE operations as the separate normalisation pass,
+// so the results are identical; cst = [C refs | C scales].
+template <int R, bool NORM = false>
 __device__ __forceinline__ void stage_r(const double2* __restrict__ in, double2* __restrict__ out,
-                                        const double2* __restrict__ tw, int m, int Ns, int CH, int CPc) {
+                                        const double2* __restrict__ tw, int m, int Ns, int CH, int CPc,
+                                        const double* __restrict__ cst = nullptr, int C = 0, bool sub = false,
+                                        bool scaled = false) {
   const int stride = m / R, span = m / (Ns * R);
+  const int chs = 31 - __clz(CH);  // CH is a power of two
   for (int idx = threadIdx.x; idx < stride * CH; idx += blockDim.x) {
-    const int pc = idx % CH, j = idx / CH, k = j % Ns;
+    const int pc = idx & (CH - 1), j = idx >> chs, k = j % Ns;
     double2 x[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) x[t] = in[(j + t * stride) * CPc + pc];
+    if (NORM) {
+      const double r0 = cst[2 * pc], r1 = cst[2 * pc + 1], s0 = cst[C + 2 * pc], s1 = cst[C + 2 * pc + 1];
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        if (sub) { x[t].x = __dsub_rn(x[t].x, r0); x[t].y = __dsub_rn(x[t].y, r1); }
+        if (scaled) { x[t].x = __ddiv_rn(x[t].x, s0); x[t].y = __ddiv_rn(x[t].y, s1); }
+      }
+    }
     if (k) {
 #pragma unroll
       for (int t = 1; t < R; ++t) x[t] = cmul(x[t], tw[t * k * span]);
@@ -162,6 +179,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   const int c0 = blockIdx.x * C;
   const int nc = min(C, p.n - c0);
   const int tid = threadIdx.x;
+  long long tr_t = (p.trace && tid == 0) ? clock64() : 0;
+  auto mark = [&](int ph) {
+    if (p.trace && tid == 0) {
+      const long long now = clock64();
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + ph), (unsigned long long)(now - tr_t));
+      tr_t = now;
+    }
+  };
 
   // bufA / bufB: m x CPc complex; the real view of bufA holds channel c of row k
   // at [k * RS + c], so channels (2p, 2p+1) ARE the complex column p.
@@ -187,9 +212,48 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   int bad = 0;
   const int total_in = m_in * C;
   const int esz = p.in_f32 ? 4 : 8;
+  const int csh = 31 - __clz(C);  // C is a power of two
   uint8_t* landing = reinterpret_cast<uint8_t*>(cstat + 2 * C);
-  for (int idx = tid; idx < total_in; idx += blockDim.x) {
-    const int r = idx / C, c = idx - r * C;
+  // full, 16-B aligned blocks: 16-byte vector loads straight into registers,
+  // converted and written to the FFT buffer (or the resampling input) at once
+  const bool vec = (C % 4 == 0) && nc == C && ((reinterpret_cast<uintptr_t>(p.raw) & 15) == 0) &&
+                   (((long long)p.ld_raw * esz) % 16 == 0) && (((long long)c0 * esz) % 16 == 0);
+  if (vec) {
+    const int V = 16 / esz, vsh = p.in_f32 ? 2 : 1;   // channels per vector
+    const int vpr_sh = csh - vsh;                     // log2(vectors per row)
+    const int total_v = total_in >> vsh;
+    constexpr int U = 4;
+    for (int base = tid; base < total_v; base += U * blockDim.x) {
+      float4 f[U];
+      double2 d[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx < total_v) {
+          const int r = idx >> vpr_sh, g = idx & ((1 << vpr_sh) - 1);
+          const long long off = (long long)r * p.ld_raw + c0 + g * V;
+          if (p.in_f32) f[u] = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(p.raw) + off));
+          else d[u] = __ldg(reinterpret_cast<const double2*>(static_cast<const double*>(p.raw) + off));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx >= total_v) continue;
+        const int r = idx >> vpr_sh, c = (idx & ((1 << vpr_sh) - 1)) * V;
+        double v[4];
+        if (p.in_f32) { v[0] = f[u].x; v[1] = f[u].y; v[2] = f[u].z; v[3] = f[u].w; }
+        else { v[0] = d[u].x; v[1] = d[u].y; v[2] = v[3] = 0.0; }
+        double* dst = resample ? raw_s + r * (C + 1) + c : rv + r * RS + c;
+        for (int e = 0; e < V; ++e) {
+          bad += !isfinite(v[e]);
+          dst[e] = v[e];
+        }
+      }
+    }
+  }
+  for (int idx = tid; idx < (vec ? 0 : total_in); idx += blockDim.x) {
+    const int r = idx >> csh, c = idx & (C - 1);
     const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(landing + (size_t)idx * esz));
     if (c < nc) {
       const char* src = static_cast<const char*>(p.raw) + ((long long)r * p.ld_raw + c0 + c) * esz;
@@ -197,10 +261,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
     }
   }
+  mark(0);
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
-  for (int idx = tid; idx < total_in; idx += blockDim.x) {
-    const int r = idx / C, c = idx - r * C;
+  mark(1);
+  for (int idx = tid; idx < (vec ? 0 : total_in); idx += blockDim.x) {
+    const int r = idx >> csh, c = idx & (C - 1);
     double v = 0.0;
     if (c < nc) v = p.in_f32 ? (double)reinterpret_cast<const float*>(landing)[idx]
                              : reinterpret_cast<const double*>(landing)[idx];
@@ -211,11 +277,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   bad = warp_sum(bad);
   if ((tid & 31) == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
   __syncthreads();
+  mark(2);
 
   // 2. resample onto the equidistant axis
   if (resample) {
     for (int idx = tid; idx < m * C; idx += blockDim.x) {
-      const int k = idx / C, c = idx - k * C;
+      const int k = idx >> csh, c = idx & (C - 1);
       double v;
       if (p.resample_kind == CORR2D_RESAMPLE_LINEAR) {
         // values[idx] + frac * (values[idx + 1] - values[idx])   (preprocess.py:152)
@@ -239,7 +306,11 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   //    axis-0 order: values / reference / sigma match the reference bit for
   //    bit); longer axes use one warp per channel (strided partial sums + a
   //    fixed xor tree: deterministic, within a few ulp of numpy).
-  if (p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0) {
+  // the normalisation is folded into the first FFT stage when nothing else
+  // needs the normalised values (m even: the first stage is radix 8/4/2)
+  const bool normalise = p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0;
+  const bool fuse_norm = normalise && p.do_fft && !p.values_out && (m % 2 == 0);
+  if (normalise) {
     const bool wide = m > kSeqStatsMax;
     const int lanes = wide ? 32 : 1;
     const int lane = wide ? (tid & 31) : 0;
@@ -294,10 +365,15 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       cstat[c] = ref;
       cstat[C + c] = scale;
     }
+    if (fuse_norm && tid >= nc && tid < C) {  // padding channels of a tail block stay 0
+      cstat[tid] = 0.0;
+      cstat[C + tid] = 1.0;
+    }
     __syncthreads();
+    mark(3);
     const bool scaled = p.alpha > 0.0;
-    for (int idx = tid; idx < m * C; idx += blockDim.x) {
-      const int k = idx / C, c = idx - k * C;
+    for (int idx = tid; idx < (fuse_norm ? 0 : m * C); idx += blockDim.x) {
+      const int k = idx >> csh, c = idx & (C - 1);
       double v = rv[k * RS + c];
       if (c < nc) {
         if (p.ref_mode != CORR2D_REF_NONE) v = __dsub_rn(v, cstat[c]);
@@ -306,11 +382,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       rv[k * RS + c] = v;
     }
     __syncthreads();
+    mark(4);
   }
 
   if (p.values_out) {
     for (int idx = tid; idx < m * C; idx += blockDim.x) {
-      const int k = idx / C, c = idx - k * C;
+      const int k = idx >> csh, c = idx & (C - 1);
       if (c < nc) p.values_out[(long long)k * p.ld_values + c0 + c] = rv[k * RS + c];
     }
   }
@@ -323,7 +400,12 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   int Ns = 1;
   for (int f = 0; f < p.nfactors; ++f) {
     const int r = p.factors[f];
-    if (r == 8) stage_r<8>(in, out, tw, m, Ns, CH, CPc);
+    if (f == 0 && fuse_norm) {
+      const bool sub = p.ref_mode != CORR2D_REF_NONE, scaled = p.alpha > 0.0;
+      if (r == 8) stage_r<8, true>(in, out, tw, m, Ns, CH, CPc, cstat, C, sub, scaled);
+      else if (r == 4) stage_r<4, true>(in, out, tw, m, Ns, CH, CPc, cstat, C, sub, scaled);
+      else stage_r<2, true>(in, out, tw, m, Ns, CH, CPc, cstat, C, sub, scaled);
+    } else if (r == 8) stage_r<8>(in, out, tw, m, Ns, CH, CPc);
     else if (r == 4) stage_r<4>(in, out, tw, m, Ns, CH, CPc);
     else if (r == 2) stage_r<2>(in, out, tw, m, Ns, CH, CPc);
     else stage_generic(in, out, tw, m, r, Ns, CH, CPc);
@@ -331,13 +413,14 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     double2* t = in; in = out; out = t;
     Ns *= r;
   }
+  mark(5);
   const double2* X = in;
   const int K = m / 2 + 1;
   const bool even = (m % 2) == 0;
 
   if (p.half_out) {
     for (int idx = tid; idx < K * C; idx += blockDim.x) {
-      const int w = idx / C, c = idx - w * C;
+      const int w = idx >> csh, c = idx & (C - 1);
       if (c >= nc) continue;
       double2 v = channel_bin(X, w, c, m, CPc);
       if (w == 0 || (even && w == m / 2)) v.y = 0.0;  // rfft: exactly real there
@@ -348,8 +431,10 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   // 5a. fp64 slot layout: s < K -> Re Y(s); K <= s < m -> Im Y(s - K + 1); rest 0.
   if (p.pack_kind == CORR2D_PACK_F64) {
     const int mp = p.mp;
+    const bool p2 = (mp & (mp - 1)) == 0;
+    const int msh = 31 - __clz(mp);
     for (int idx = tid; idx < nc * mp; idx += blockDim.x) {
-      const int c = idx / mp, s = idx - c * mp;
+      const int c = p2 ? idx >> msh : idx / mp, s = idx - c * mp;
       double vphi = 0.0, vpsi = 0.0, vb = 0.0;
       if (s < m) {
         int w;
@@ -383,8 +468,10 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
     const int h = even ? m / 2 : (m + 1) / 2;
     const double sn1 = sqrt(p.norm), sn2 = sqrt(2.0 * p.norm);
     const int q4n = hp / 4;
+    const bool p2 = (q4n & (q4n - 1)) == 0;
+    const int qsh = 31 - __clz(q4n);
     for (int idx = tid; idx < nc * q4n; idx += blockDim.x) {
-      const int c = idx / q4n, q0 = (idx - c * q4n) * 4;
+      const int c = p2 ? idx >> qsh : idx / q4n, q0 = (idx - c * q4n) * 4;
       // [third][plane] x 4 slots
       __align__(8) __nv_bfloat16 v[3][2][4];
 #pragma unroll
@@ -422,6 +509,8 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       if (p.pack_roles & CORR2D_ROLE_B) put(p.b);
     }
   }
+  __syncthreads();
+  mark(6);
 }
 
 static int fft_factorize(int m, int* f, int maxf) {
@@ -535,7 +624,7 @@ extern "C" int corr2d_prep(
   while (C > 2 && prep_smem_bytes(m, m_in, C, resample, in_bytes) > budget) C /= 2;
   if (const char* e = getenv("CORR2D_PREP_C")) {  // experiments: channels per CTA
     const int forced = atoi(e);
-    if (forced >= 2 && forced <= 64 && (forced % 2) == 0) C = forced;
+    if (forced >= 2 && forced <= 64 && (forced & (forced - 1)) == 0) C = forced;
   }
   size_t smem = prep_smem_bytes(m, m_in, C, resample, in_bytes);
   if (smem > 220 * 1024)
@@ -545,6 +634,21 @@ extern "C" int corr2d_prep(
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), st) != cudaSuccess) return check_launch("status reset");
   const int grid = (n + C - 1) / C;
+  static long long* trace_buf = nullptr;
+  const char* trc = getenv("CORR2D_PREP_TRACE");
+  if (trc && trc[0] == '1') {
+    if (!trace_buf) cudaMalloc(&trace_buf, 16 * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0, 16 * sizeof(long long), st);
+    p.trace = trace_buf;
+  }
   prep_kernel<<<grid, kPrepThreads, smem, st>>>(p);
+  if (p.trace) {
+    long long h[16];
+    cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "prep trace (cycles/CTA, C=%d grid=%d): issue %.0f wait %.0f convert %.0f stats %.0f normalise %.0f "
+            "fft %.0f pack %.0f\n", C, grid, (double)h[0] / grid, (double)h[1] / grid, (double)h[2] / grid,
+            (double)h[3] / grid, (double)h[4] / grid, (double)h[5] / grid, (double)h[6] / grid);
+  }
   return check_launch("prep_kernel");
 }
