@@ -55,7 +55,8 @@ enum corr2d_resample { CORR2D_RESAMPLE_NONE = 0, CORR2D_RESAMPLE_LINEAR = 1, COR
 enum corr2d_pack {
   CORR2D_PACK_NONE = 0,
   CORR2D_PACK_F64 = 1,       /* float64 operands (fp64 DMMA contraction)            */
-  CORR2D_PACK_BF16X2 = 2     /* bf16 hi/lo, k-block interleaved (bf16x3 tcgen05 contraction) */
+  CORR2D_PACK_BF16X2 = 2,    /* bf16 hi/lo, k-block interleaved (bf16x3 tcgen05 contraction) */
+  CORR2D_PACK_F64_TIME = 3   /* float64 time-domain values, no DFT (Hilbert route, hilbert.py) */
 };
 
 enum corr2d_ref_mode { CORR2D_REF_MEAN = 0, CORR2D_REF_PROVIDED = 1, CORR2D_REF_NONE = 2 };
@@ -98,6 +99,11 @@ int corr2d_fft_factors(int m, int* factors, int max_factors);
  * reference subtraction): with alpha = 0 the entry used by dft_channels /
  * correlate_ft on DynamicSpectra, with sigma_in the one used by apply_scaling.
  * sigma_in (optional, n) replaces the computed sigma.
+ * CORR2D_PACK_F64_TIME (Hilbert route, hilbert.py:92-115): no DFT; slot s < m of
+ * a row holds the dynamic value y(t_s) -- A_phi = norm_const * y (ROLE_A), B = y
+ * (ROLE_B), zero padded to mp = corr2d_packed_depth(m, ...); a_psi is unused
+ * (the caller forms A_psi = -norm_const * N y with one corr2d_contract_f64 call
+ * against the Hilbert-Noda matrix, since async = Y1^T N Y2 = (-N Y1)^T Y2).
  * Packing: ld_pack is the row pitch of the packed operands in elements
  * (>= mp for F64; >= 2 * mp + 64 and a multiple of 64 for BF16X2, whose layout is
  * described at corr2d_contract_bf16x3).  split_plane is unused (ABI v1 kept

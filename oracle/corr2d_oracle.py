@@ -228,6 +228,32 @@ def correlate_ft(values1, values2=None, norm: float | None = None, workers: int 
     return corr.real.copy(), corr.imag.copy(), constant
 
 
+def hilbert_noda_matrix(m: int) -> np.ndarray:
+    """hilbert.py:40-48 -- N[j, k] = 1/(pi (k - j)), 0 on the diagonal."""
+    idx = np.arange(m)
+    with np.errstate(divide="ignore"):
+        n = 1.0 / (np.pi * (idx[None, :] - idx[:, None]))
+    np.fill_diagonal(n, 0.0)
+    return n
+
+
+def correlate_ht(values1, values2=None, norm: float | None = None):
+    """hilbert.py:92-115 -- returns (sync, asyn, constant).
+
+    sync = Norm * Y1^T Y2, async = Norm * Y1^T (N Y2), Norm default 1/(m - 1)
+    (the dense N of hilbert.py:51-53; the reference's Toeplitz branch above
+    m = 4096 applies the same matrix).
+    """
+    values1 = np.asarray(values1, dtype=float)
+    values2 = values1 if values2 is None else np.asarray(values2, dtype=float)
+    m = values1.shape[0]
+    constant = unit_constant(m) if norm is None else float(norm)
+    transformed = hilbert_noda_matrix(m) @ values2
+    sync = constant * (values1.T @ values2)
+    asyn = constant * (values1.T @ transformed)
+    return sync, asyn, constant
+
+
 class _Null:
     def __enter__(self):
         return self

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcorr2d.so"
 OK, ERR_DATA, ERR_NUMERIC, ERR_OOM, ERR_CUDA, ERR_UNSUPPORTED = range(6)
 F64, F32 = 0, 1
 RESAMPLE_NONE, RESAMPLE_LINEAR, RESAMPLE_MATRIX = 0, 1, 2
-PACK_NONE, PACK_F64, PACK_BF16X2 = 0, 1, 2
+PACK_NONE, PACK_F64, PACK_BF16X2, PACK_F64_TIME = 0, 1, 2, 3
 ROLE_A, ROLE_B = 1, 2
 REF_MEAN, REF_PROVIDED, REF_NONE = 0, 1, 2
 ST_NONFINITE, ST_ZEROVAR, ST_FIRST_ZEROVAR = 0, 1, 2

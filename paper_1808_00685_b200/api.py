@@ -13,6 +13,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _abi, engine
+from . import engine as _engine_mod
 from .dataset import CorrelationSpectra, SpectralDataset
 from .engine_core import NormalizationSpec
 from .errors import DataError
@@ -31,9 +32,9 @@ def _reference_spec(reference) -> ReferenceSpec:
     return ReferenceSpec.provided(reference)
 
 
-def _norm_spec(norm) -> NormalizationSpec:
-    if norm is None:
-        return NormalizationSpec.noda()
+def _norm_spec(norm, engine_name="fourier") -> NormalizationSpec:
+    if norm is None:  # cli.py:334-340: noda for the Fourier route, unit for Hilbert
+        return NormalizationSpec.noda() if engine_name == "fourier" else NormalizationSpec.unit()
     if isinstance(norm, NormalizationSpec):
         return norm
     if isinstance(norm, str):
@@ -42,7 +43,8 @@ def _norm_spec(norm) -> NormalizationSpec:
 
 
 def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: PreprocessSpec, *,
-               norm=None, on_zero_variance="error", dtype="float64", rows=None, device=None):
+               norm=None, on_zero_variance="error", dtype="float64", rows=None, device=None,
+               engine_name="fourier"):
     """A bound :class:`engine.CorrelationPlan` for the fused raw -> planes pipeline."""
     from .preprocess import _raw_device, _recipe_for
     _, dev = engine.require_device(device)
@@ -57,10 +59,13 @@ def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: Preproce
             raise DataError("perturbation axes differ between the two inputs; resample both "
                             "onto a common axis before correlating")
     m = r1.m
-    constant = _norm_spec(norm).constant(m)
+    if engine_name not in ("fourier", "hilbert"):
+        raise DataError(f"unknown engine {engine_name!r} (use 'fourier' or 'hilbert')")
+    constant = _norm_spec(norm, engine_name).constant(m)
     plan = engine.CorrelationPlan(
         n1=ds1.n, n2=(ds1 if homo else ds2).n, m=m, recipe1=r1, recipe2=r2, norm=constant,
-        dtype=dtype, rows=rows, device=dev, want_ref=True, want_sigma=r1.alpha > 0.0)
+        dtype=dtype, rows=rows, device=dev, want_ref=True, want_sigma=r1.alpha > 0.0,
+        route=engine_name)
     plan.bind(_raw_device(ds1, dev), None if homo else _raw_device(ds2, dev))
     plan.constant = constant
     plan.t_axis = plan1.t_new if plan1 is not None else ds1.perturbation_axis
@@ -71,13 +76,15 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
            resample: int | None = None, resample_to_common: int | None = None,
            interpolant: str = "spline", alpha: float = 0.0, norm=None, workers: int = 1,
            on_zero_variance: str = "error", dtype="float64", out=None,
-           return_device: bool = False, device=None) -> CorrelationSpectra:
+           return_device: bool = False, device=None, engine: str = "fourier") -> CorrelationSpectra:
     """Generalised 2D correlation of one (homo) or two (hetero) spectral series.
 
     Keyword arguments follow the reference CLI (`corrtwo correlate`): reference
     ("mean" or a vector), resample (target count), resample_to_common,
     interpolant ("spline" | "linear"), alpha (scaling exponent), norm
-    (NormalizationSpec, "noda" | "unit" | "custom:c", or a float).
+    (NormalizationSpec, "noda" | "unit" | "custom:c", or a float; default noda
+    for the Fourier route, unit for the Hilbert route), engine ("fourier" |
+    "hilbert", cli.py:332-344; the Hilbert route computes in float64).
     """
     if workers < 1:
         raise DataError("correlate: --workers must be >= 1")
@@ -94,14 +101,14 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
                           resample=None if resample is None else ResampleSpec(int(resample), kind),
                           scaling_exponent=float(alpha))
     plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
-                            dtype=dtype, device=device)
+                            dtype=dtype, device=device, engine_name=engine)
     plan.launch()
-    engine.sync()
+    _engine_mod.sync()
     dsb = ds1 if homo else ds2
     ref1, ref2, _, _, info = plan.check(axes=(ds1.spectral_axis, dsb.spectral_axis),
                                         labels=("first", "second"))
     meta = dict(axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, ref1=ref1, ref2=ref2,
-                normalization=plan.constant, engine="fourier", is_homo=homo,
+                normalization=plan.constant, engine=engine, is_homo=homo,
                 scaling_exponent=float(alpha) if alpha > 0 else 0.0, stats=info)
     if return_device:
         return DeviceCorrelationSpectra(plan, meta)

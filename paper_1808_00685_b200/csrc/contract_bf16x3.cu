@@ -421,6 +421,9 @@ __device__ __forceinline__ void stage_and_store_32(uint8_t* wst, int lane, const
 // One plane of a 32-column chunk (8-warp epilogue of the CTA-pair kernels):
 // tile box and mirror box, 32 x 32 fp32 each, SWIZZLE_128B.
 // PENDING: store groups of this lane that may still be reading OTHER buffers.
+#ifndef CORR2D_SPLIT_GROUPS
+#define CORR2D_SPLIT_GROUPS 0
+#endif
 template <int PENDING>
 __device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane, const float (&v)[32], bool mirror,
                                                          float tsign, const CUtensorMap* map_direct,
@@ -428,6 +431,39 @@ __device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane,
                                                          uint64_t pol) {
   uint8_t* dbox = wst;
   uint8_t* mbox = wst + BOX2;
+  if (CORR2D_SPLIT_GROUPS && PENDING == 0) {
+    // single buffer, tile and mirror boxes in separate bulk groups: staging the
+    // tile box waits only for the previous tile box's read (the previous
+    // mirror box may still be in flight), and vice versa
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(dbox + lane * 128 + ((j ^ (lane & 7)) * 16)) =
+          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(map_direct, dbox, cbase, row0q, pol);
+      bulk_commit();
+    }
+    if (!mirror) {
+      if (lane == 0) bulk_commit();  // keep two groups per chunk
+      return;
+    }
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      *reinterpret_cast<float*>(mbox + k * 128 + (((lane >> 2) ^ (k & 7)) * 16) + (lane & 3) * 4) = tsign * v[k];
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(map_mirror, mbox, row0q, cbase, pol);
+      bulk_commit();
+    }
+    return;
+  }
   if (lane == 0) bulk_wait_read<PENDING>();
   __syncwarp();
 #pragma unroll

@@ -391,6 +391,19 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       if (c < nc) p.values_out[(long long)k * p.ld_values + c0 + c] = rv[k * RS + c];
     }
   }
+  // 5c. time-domain packing for the Hilbert route (no DFT): slot s < m holds
+  //     the dynamic value y(t_s) -- A_phi = Norm * y, B = y; zero padded to mp
+  if (p.pack_kind == CORR2D_PACK_F64_TIME) {
+    const int mp = p.mp;
+    for (int idx = tid; idx < nc * mp; idx += blockDim.x) {
+      const int c = idx / mp, s = idx - c * mp;
+      const double v = s < m ? rv[s * RS + c] : 0.0;
+      const long long row = (long long)(c0 + c) * p.ld_pack + s;
+      if (p.pack_roles & CORR2D_ROLE_A) static_cast<double*>(p.a_phi)[row] = p.norm * v;
+      if (p.pack_roles & CORR2D_ROLE_B) static_cast<double*>(p.b)[row] = v;
+    }
+    return;
+  }
   if (!p.do_fft) return;
 
   // 4. DFT along the perturbation axis: two real channels per complex
@@ -600,7 +613,9 @@ extern "C" int corr2d_prep(
   p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack; p.split_plane = split_plane;
   p.values_out = values_out; p.ld_values = ld_values; p.half_out = half_out;
   p.ref_out = ref_out; p.sigma_out = sigma_out; p.status = status;
-  p.do_fft = (half_out != nullptr) || (pack_kind != CORR2D_PACK_NONE);
+  if (pack_kind < CORR2D_PACK_NONE || pack_kind > CORR2D_PACK_F64_TIME)
+    return fail(CORR2D_ERR_DATA, "corr2d_prep: bad pack_kind");
+  p.do_fft = (half_out != nullptr) || (pack_kind == CORR2D_PACK_F64 || pack_kind == CORR2D_PACK_BF16X2);
   if (pack_kind != CORR2D_PACK_NONE) {
     p.mp = corr2d_packed_depth(m, pack_kind);
     if (pack_kind == CORR2D_PACK_BF16X2) {

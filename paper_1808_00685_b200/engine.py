@@ -231,6 +231,18 @@ def handle_zero_variance(spectral_axis, sigma_raw: np.ndarray, alpha: float, sub
 # the correlation plan (K1 x {1,2} -> K2)
 # --------------------------------------------------------------------------
 
+def _noda_rows(m: int, ld: int) -> np.ndarray:
+    """-N as m rows of ld float64 (zero padded): N[j, k] = 1 / (pi (k - j)),
+    0 on the diagonal -- the Hilbert-Noda matrix of hilbert.py:40-48."""
+    idx = np.arange(m)
+    with np.errstate(divide="ignore"):
+        n = 1.0 / (np.pi * (idx[None, :] - idx[:, None]))
+    np.fill_diagonal(n, 0.0)
+    out = np.zeros((m, ld))
+    out[:, :m] = -n
+    return out
+
+
 class CorrelationPlan:
     """Device pipeline for one correlation shape.
 
@@ -240,7 +252,7 @@ class CorrelationPlan:
 
     def __init__(self, *, n1, n2, m, recipe1: PrepRecipe, recipe2: PrepRecipe | None,
                  norm: float, dtype="float64", rows=None, device=None, want_ref=True,
-                 want_sigma=False, tiles=None):
+                 want_sigma=False, tiles=None, route="fourier"):
         self.lib, self.dev = require_device(device)
         t = torch()
         self.homo = recipe2 is None
@@ -250,7 +262,15 @@ class CorrelationPlan:
         self.recipe1, self.recipe2 = recipe1, recipe2
         self.norm = float(norm)
         self.dtype = np.dtype(dtype)
-        if self.dtype == np.float64:
+        if route not in ("fourier", "hilbert"):
+            raise DataError(f"unknown route {route!r}")
+        self.route = route
+        if route == "hilbert":
+            # Hilbert-Noda route (hilbert.py:92-115): time-domain operands, fp64 only
+            if self.dtype != np.float64:
+                raise DataError("the Hilbert route computes in float64 only")
+            self.pack_kind, odt, pdt = _abi.PACK_F64_TIME, t.float64, t.float64
+        elif self.dtype == np.float64:
             self.pack_kind, odt, pdt = _abi.PACK_F64, t.float64, t.float64
         elif self.dtype == np.float32:
             self.pack_kind, odt, pdt = _abi.PACK_BF16X2, t.float32, t.bfloat16
@@ -271,6 +291,13 @@ class CorrelationPlan:
         self.a_phi = t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
         # bf16: one format for both roles (a_psi unused, homo B == A)
         self.a_psi = None if bf16 else t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
+        if route == "hilbert":
+            # A_psi = -Norm * (N y1) comes from one contraction of A_phi = Norm * y1
+            # against the rows of -N (m x mp, zero padded); columns m..mp of
+            # A_psi are never written and stay 0
+            self.a_psi = t.zeros((self.n1, self.ld_pack), dtype=pdt, device=dev)
+            self.noda_neg = t.from_numpy(_noda_rows(self.m, self.ld_pack)).to(dev)
+            self.noda_scratch = t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
         self.b = self.a_phi.new_empty((self.n2, self.ld_pack)) if not self.homo else None
         if self.homo:
             self.b_homo = self.a_phi if bf16 else t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
@@ -315,7 +342,7 @@ class CorrelationPlan:
     @property
     def launches_per_step(self) -> int:
         """Kernels of ours one launch() enqueues: K1 per dataset + K2."""
-        return (1 if self.homo else 2) + 1
+        return (1 if self.homo else 2) + (2 if self.route == "hilbert" else 1)
 
     def launch(self):
         """Enqueue K1 (x1 or x2) and K2 on the current stream; no host sync."""
@@ -339,7 +366,14 @@ class CorrelationPlan:
     def launch_contract(self):
         lib = self.lib
         homo = 1 if self.homo else 0
-        if self.pack_kind == _abi.PACK_F64:
+        if self.route == "hilbert":
+            # A_psi[i, s] = sum_k A_phi[i, k] * (-N[s, k]) = -Norm (N y1)[s, i]
+            code = lib.corr2d_contract_f64(
+                ptr(self.a_phi), ptr(self.a_phi), ptr(self.noda_neg), self.ld_pack, self.n1, self.m, self.mp,
+                0, 0, self.n1, 0, -1, ptr(self.a_psi), ptr(self.noda_scratch), self.ld_pack,
+                ptr(self.stats), stream_handle())
+            _abi.check(code, lib)
+        if self.pack_kind in (_abi.PACK_F64, _abi.PACK_F64_TIME):
             code = lib.corr2d_contract_f64(
                 ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.ld_pack, self.n1, self.n2, self.mp,
                 homo, self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi),

@@ -30,7 +30,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 import corrtwo  # noqa: E402  (the reference)
 from corrtwo import (  # noqa: E402
     DynamicSpectra, InterpolantKind, NormalizationSpec, PreprocessSpec, ReferenceSpec,
-    ResampleSpec, SpectralDataset, correlate_ft, dft_channels, preprocess_dataset,
+    ResampleSpec, SpectralDataset, correlate_ft, correlate_ht, dft_channels, preprocess_dataset,
 )
 
 from paper_1808_00685_b200 import configs  # noqa: E402  (seeded generators only)
@@ -124,6 +124,26 @@ def small_cases(manifest):
     save("norm_unit_custom", values=vals, sync_unit=r1.sync, asyn_unit=r1.asyn,
          sync_custom=r2.sync, asyn_custom=r2.asyn)
     manifest["norm_unit_custom"] = {"kind": "norm"}
+    # Hilbert route -- hilbert.py:92-115, test_cross_engine.py:26-65
+    for m, n1, n2 in [(2, 5, 5), (11, 13, 13), (21, 17, 17), (64, 20, 20), (128, 9, 9),
+                      (8, 4, 6), (37, 21, 29)]:
+        t = np.linspace(0.0, 7.0, m)
+        ds1 = SpectralDataset(np.arange(n1, dtype=float), t, rng.normal(size=(m, n1)))
+        homo = n1 == n2
+        ds2 = None if homo else SpectralDataset(np.arange(n2, dtype=float) + 0.25, t.copy(),
+                                                rng.normal(size=(m, n2)))
+        d1 = preprocess_dataset(ds1)
+        d2 = None if homo else preprocess_dataset(ds2)
+        res = correlate_ht(d1, d2)
+        ft = correlate_ft(d1, d2)
+        name = f"hilbert_m{m}_{n1}x{n2}"
+        save(name, t=t, nu1=ds1.spectral_axis, raw1=ds1.intensities,
+             raw2=ds1.intensities if homo else ds2.intensities,
+             nu2=ds1.spectral_axis if homo else ds2.spectral_axis,
+             values1=d1.values, values2=d1.values if homo else d2.values,
+             sync=res.sync, asyn=res.asyn, norm=np.float64(res.normalization),
+             ft_sync=ft.sync, ft_norm=np.float64(ft.normalization))
+        manifest[name] = {"kind": "hilbert", "m": m, "n1": n1, "n2": n2, "homo": homo}
 
 
 def config_cases(manifest):

@@ -111,3 +111,17 @@ def test_oracle_config_rows(k):
         s, a, _ = O.correlate_ft(v1[:, r:r + 1], v2, rows=None)
         assert np.array_equal(s[0], g["sync_rows"][i])
         assert np.array_equal(a[0], g["asyn_rows"][i])
+
+
+@pytest.mark.parametrize("name", golden_names("hilbert_"))
+def test_oracle_hilbert(name):
+    """oracle.correlate_ht against the reference's correlate_ht (hilbert.py:92-115)."""
+    g = golden(name)
+    sync, asyn, c = O.correlate_ht(g["values1"], g["values2"])
+    assert c == float(g["norm"])
+    scale = float(np.abs(g["sync"]).max())
+    assert rel_err(sync, g["sync"], scale) <= 1e-15
+    assert rel_err(asyn, g["asyn"], scale) <= 1e-15
+    # the reference's own cross-engine identity (test_cross_engine.py:26-43)
+    m = g["values1"].shape[0]
+    assert rel_err(g["ft_sync"], (m / np.pi) * g["sync"], scale * m / np.pi) <= 1e-10
