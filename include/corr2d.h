@@ -174,6 +174,28 @@ int corr2d_contract_bf16x3(
 int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int row0, int row1,
                                    int64_t ld_out);
 
+/* ------------------------------------------------- K3: peak candidates ---- */
+/*
+ * max |x| over an n1 x n2 plane (dtype CORR2D_F64 / CORR2D_F32, leading
+ * dimension ld) into *out_dev (device double, reset by this call).  Used by
+ * find_peaks for maps that did not come with K2's fused statistics.
+ */
+int corr2d_plane_absmax(int dtype, const void* x, int64_t ld, int n1, int n2, double* out_dev, void* stream);
+
+/*
+ * Cross-peak candidates of a correlation map (analysis.py:136-201): strict
+ * 8-neighbourhood local maxima of |sync| above thr_sync OR of |async| above
+ * thr_async, the map padded with -inf (analysis.py:136-149); homo != 0 keeps
+ * k > i only.  Each candidate's row-major linear index i * n2 + k is appended
+ * to out_idx (device int64[capacity]) in no particular order; *count (device
+ * uint64, reset by this call) receives the total, which may exceed capacity
+ * (the caller then retries with a larger buffer).  Pass thr = +inf to exclude
+ * a plane whose maximum is 0 (analysis.py:186-194).
+ */
+int corr2d_find_peaks(int dtype, const void* sync, const void* asyn, int64_t ld, int n1, int n2, int homo,
+                      double thr_sync, double thr_async, int64_t* out_idx, int64_t capacity,
+                      unsigned long long* count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,6 +12,8 @@ point raises ``BackendUnavailable``.
 __version__ = "0.1.0"
 
 from ._abi import BackendUnavailable
+from .analysis import (AutoPeak, CrossPeak, CrossPeakVerdict, PeakReport, Verdict, classify_cross_peak,
+                       find_peaks)
 from .api import corr2d
 from .dataset import CorrelationSpectra, SpectralDataset
 from .engine_core import NormalizationSpec, check_pair, is_same_dynamic, row_blocks
@@ -25,7 +27,8 @@ from .preprocess import (DynamicSpectra, InterpolantKind, PreprocessSpec, Refere
                          resample_to_axis, stddev_spectrum)
 
 __all__ = [
-    "BackendUnavailable", "CorrelationSpectra", "CorrtwoError", "DataError", "DeviceCorrelationSpectra",
+    "AutoPeak", "BackendUnavailable", "CorrelationSpectra", "CrossPeak", "CrossPeakVerdict", "PeakReport",
+    "Verdict", "classify_cross_peak", "find_peaks", "CorrtwoError", "DataError", "DeviceCorrelationSpectra",
     "DynamicSpectra", "FourierWorkspace", "InterpolantKind", "NormalizationSpec", "NumericError",
     "ParseError", "PreprocessSpec", "ReferenceSpec", "ResampleSpec", "SpectralDataset",
     "apply_scaling", "check_pair", "correlate_ft", "correlate_ht", "corr2d", "default_target_count",

@@ -29,7 +29,7 @@ INT32_MAX = 2**31 - 1
 EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
-    "corr2d_contract_tile_count",
+    "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
 )
 
 
@@ -69,8 +69,12 @@ def _declare(lib):
     ]
     lib.corr2d_contract_tile_count.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_i64]
     lib.corr2d_contract_tile_count.restype = c_i64
+    lib.corr2d_plane_absmax.argtypes = [c_int, c_void, c_i64, c_int, c_int, c_void, c_void]
+    lib.corr2d_find_peaks.argtypes = [c_int, c_void, c_void, c_i64, c_int, c_int, c_int, c_double, c_double,
+                                      c_void, c_i64, c_void, c_void]
     for name in ("corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
-                 "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors"):
+                 "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
+                 "corr2d_plane_absmax", "corr2d_find_peaks"):
         getattr(lib, name).restype = c_int
 
 

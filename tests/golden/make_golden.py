@@ -144,6 +144,29 @@ def small_cases(manifest):
              sync=res.sync, asyn=res.asyn, norm=np.float64(res.normalization),
              ft_sync=ft.sync, ft_norm=np.float64(ft.normalization))
         manifest[name] = {"kind": "hilbert", "m": m, "n1": n1, "n2": n2, "homo": homo}
+    # find_peaks -- analysis.py:152-201 on banded data
+    from corrtwo import find_peaks
+    cases = [("peaks_cfg1_homo", configs.make(1), None, 0.05),
+             ("peaks_cfg2_hetero", configs.make(2), "set2", 0.1)]
+    for name, case, other, thr in cases:
+        s1 = case.set1
+        ds1 = SpectralDataset(s1.spectral_axis, s1.perturbation_axis, s1.intensities)
+        d1 = preprocess_dataset(ds1)
+        d2 = None
+        if other:
+            s2 = case.set2
+            d2 = preprocess_dataset(SpectralDataset(s2.spectral_axis, s2.perturbation_axis, s2.intensities))
+        res = correlate_ft(d1, d2)
+        rep = find_peaks(res, thr)
+        # the maps themselves are not stored: tests rebuild them bit-for-bit with the
+        # oracle from the seeded config inputs (pinned by test_oracle_golden.py)
+        save(name, threshold=np.float64(thr), eps=np.float64(rep.eps), homo=np.bool_(res.is_homo),
+             auto_nu=np.array([p.nu for p in rep.auto_peaks], dtype=float),
+             auto_phi=np.array([p.phi for p in rep.auto_peaks], dtype=float),
+             cross=np.array([[p.nu1, p.nu2, p.phi, p.psi] for p in rep.cross_peaks], dtype=float).reshape(-1, 4),
+             verdicts=np.array([str(p.verdict) for p in rep.cross_peaks]),
+             table=np.array(rep.to_table()), long_form=np.frombuffer(rep.to_long_form(), dtype=np.uint8))
+        manifest[name] = {"kind": "peaks", "auto": len(rep.auto_peaks), "cross": len(rep.cross_peaks)}
 
 
 def config_cases(manifest):
