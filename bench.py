@@ -13,9 +13,12 @@ quoted on; it fits one GPU.  Outputs (8.6 GB per step) are far larger than the
 126 MB L2, so each step starts with a cold L2.
 
 Multi-GPU (torchrun, one process per GPU, NCCL): the homo tile enumeration is
-split into equal contiguous tile ranges; every rank re-runs the cheap K1 over
-all channels (cheaper than exchanging the packed spectra, so no data-path
-collective) and computes only its tiles.  Total work is fixed: "strong".
+split into equal contiguous tile ranges (every tile computed once, mirrors
+included, so total work equals the 1-GPU work).  The packed spectra come from
+K1 on each rank's channel chunk plus one in-place NCCL all-gather over NVLink
+(--spectra allgather, the default) or from K1 over all channels on
+every rank with no collective (--spectra recompute).  Total work is fixed:
+"strong".
 
 --impl reference: the reference CPU path (oracle port of corrtwo's
 preprocess_dataset + correlate_ft, oracle/corr2d_oracle.py) on rank 0 with all
@@ -207,7 +210,7 @@ def config_block(case, wl, args):
             else "fp64 DMMA -> fp64 planes",
             "l2": "outputs per step >> 126 MB L2 (cold L2 each step)" if wl["out_bytes"] > 4 * 126e6
             else "L2 flushed between timed steps (256 MB write)",
-            "parallelism": f"tile-range x{args.gpus}" if args.gpus > 1 else "single GPU"}
+            "parallelism": (f"tile-range x{args.gpus}, spectra {args.spectra}" if args.gpus > 1 else "single GPU")}
 
 
 def dist_setup(args):
@@ -241,7 +244,11 @@ def run_b200(args, case, wl, world, rank, local):
     spec = P.PreprocessSpec(
         resample=None if case.resample is None else P.ResampleSpec(case.resample, P.InterpolantKind.from_name(case.interpolant)),
         scaling_exponent=case.alpha)
-    plan, homo = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev)
+    # N > 1: K1 on this rank's channel chunk + one NCCL all-gather of the packed
+    # spectra (--spectra allgather), or K1 over all channels on every
+    # rank with no collective at all (--spectra recompute)
+    shard = (rank, world) if world > 1 and args.spectra == "allgather" else None
+    plan, homo = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev, spectra_shard=shard)
     if world > 1:
         # equal contiguous share of the contraction kernel's own tile enumeration
         plan.tile0, plan.tile1 = tile_range(plan.tile_count(), world, rank)
@@ -451,6 +458,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--spectra", default="allgather", choices=["allgather", "recompute"],
+                    help="N > 1: shard K1 + NCCL all-gather of the packed spectra, or recompute K1 on every rank")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -19,6 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
+from .engine_core import channel_chunk, gather_rows
 from .errors import DataError, NumericError
 
 _torch = None
@@ -252,9 +253,13 @@ class CorrelationPlan:
 
     def __init__(self, *, n1, n2, m, recipe1: PrepRecipe, recipe2: PrepRecipe | None,
                  norm: float, dtype="float64", rows=None, device=None, want_ref=True,
-                 want_sigma=False, tiles=None, route="fourier"):
+                 want_sigma=False, tiles=None, route="fourier", spectra_shard=None):
         self.lib, self.dev = require_device(device)
         t = torch()
+        # spectra_shard=(rank, world): K1 runs on this rank's channel chunk only and
+        # the packed spectra are all-gathered in place; the
+        # buffers then hold world * chunk rows, the tail rows zero
+        self.shard = tuple(spectra_shard) if spectra_shard and spectra_shard[1] > 1 else None
         self.homo = recipe2 is None
         if self.homo and n1 != n2:
             raise DataError("homo correlation needs n1 == n2")
@@ -288,19 +293,21 @@ class CorrelationPlan:
         # in a 128-byte pad (include/corr2d.h)
         self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
         dev = self.dev
-        self.a_phi = t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
+        R1, R2 = self._rows(self.n1), self._rows(self.n2)
+        alloc = t.zeros if self.shard else t.empty
+        self.a_phi = alloc((R1, self.ld_pack), dtype=pdt, device=dev)
         # bf16: one format for both roles (a_psi unused, homo B == A)
-        self.a_psi = None if bf16 else t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
+        self.a_psi = None if bf16 else alloc((R1, self.ld_pack), dtype=pdt, device=dev)
         if route == "hilbert":
             # A_psi = -Norm * (N y1) comes from one contraction of A_phi = Norm * y1
             # against the rows of -N (m x mp, zero padded); columns m..mp of
             # A_psi are never written and stay 0
-            self.a_psi = t.zeros((self.n1, self.ld_pack), dtype=pdt, device=dev)
+            self.a_psi = t.zeros((R1, self.ld_pack), dtype=pdt, device=dev)
             self.noda_neg = t.from_numpy(_noda_rows(self.m, self.ld_pack)).to(dev)
             self.noda_scratch = t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
-        self.b = self.a_phi.new_empty((self.n2, self.ld_pack)) if not self.homo else None
+        self.b = alloc((R2, self.ld_pack), dtype=pdt, device=dev) if not self.homo else None
         if self.homo:
-            self.b_homo = self.a_phi if bf16 else t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
+            self.b_homo = self.a_phi if bf16 else alloc((R1, self.ld_pack), dtype=pdt, device=dev)
         else:
             self.b_homo = None
         nrows = self.row1 - self.row0
@@ -314,11 +321,17 @@ class CorrelationPlan:
         self.stats = t.zeros(4, dtype=t.int64, device=dev)
         self.status1 = t.zeros(4, dtype=t.int32, device=dev)
         self.status2 = t.zeros(4, dtype=t.int32, device=dev)
-        self.ref1 = t.empty(self.n1, dtype=t.float64, device=dev) if want_ref else None
-        self.ref2 = (t.empty(self.n2, dtype=t.float64, device=dev) if (want_ref and not self.homo) else None)
-        self.sigma1 = t.empty(self.n1, dtype=t.float64, device=dev) if want_sigma else None
-        self.sigma2 = (t.empty(self.n2, dtype=t.float64, device=dev) if (want_sigma and not self.homo) else None)
+        self.ref1 = alloc(R1, dtype=t.float64, device=dev) if want_ref else None
+        self.ref2 = (alloc(R2, dtype=t.float64, device=dev) if (want_ref and not self.homo) else None)
+        self.sigma1 = alloc(R1, dtype=t.float64, device=dev) if want_sigma else None
+        self.sigma2 = (alloc(R2, dtype=t.float64, device=dev) if (want_sigma and not self.homo) else None)
         self.raw1 = self.raw2 = None
+
+    def _rows(self, n):
+        if self.shard is None:
+            return n
+        rank, world = self.shard
+        return channel_chunk(n, world, rank)[2] * world
 
     @property
     def bop(self):
@@ -354,6 +367,13 @@ class CorrelationPlan:
         roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
         if self.pack_kind == _abi.PACK_BF16X2 and self.homo:
             roles1 = _abi.ROLE_A
+        if self.shard is not None:
+            self._prep_sharded(self.raw1, self.recipe1, self.n1, roles1, self.a_phi, self.a_psi,
+                               self.b_homo if self.homo else None, self.ref1, self.sigma1, self.status1)
+            if not self.homo:
+                self._prep_sharded(self.raw2, self.recipe2, self.n2, _abi.ROLE_B, None, None, self.b,
+                                   self.ref2, self.sigma2, self.status2)
+            return
         launch_prep(lib, self.raw1, self.recipe1, norm=self.norm, pack_kind=self.pack_kind, roles=roles1,
                     a_phi=self.a_phi, a_psi=self.a_psi, b=self.b_homo if self.homo else None,
                     ld_pack=self.ld_pack, ref_out=self.ref1,
@@ -362,6 +382,32 @@ class CorrelationPlan:
             launch_prep(lib, self.raw2, self.recipe2, norm=self.norm, pack_kind=self.pack_kind,
                         roles=_abi.ROLE_B, b=self.b, ld_pack=self.ld_pack,
                         ref_out=self.ref2, sigma_out=self.sigma2, status=self.status2)
+
+    def _prep_sharded(self, raw, recipe, n, roles, a_phi, a_psi, b, ref, sigma, status):
+        """K1 over this rank's channel chunk, then one in-place all-gather per
+        packed buffer (and of ref / sigma); status words are all-reduced."""
+        import dataclasses
+
+        import torch.distributed as dist
+        rank, world = self.shard
+        c0, c1, chunk = channel_chunk(n, world, rank)
+        if c1 > c0:
+            sl = dataclasses.replace(
+                recipe, ref_in=None if recipe.ref_in is None else recipe.ref_in[c0:c1],
+                sigma_in=None if recipe.sigma_in is None else recipe.sigma_in[c0:c1])
+            rows = (lambda x: None if x is None else x[c0:])
+            launch_prep(self.lib, raw[:, c0:c1], sl, norm=self.norm, pack_kind=self.pack_kind, roles=roles,
+                        a_phi=rows(a_phi), a_psi=rows(a_psi), b=rows(b), ld_pack=self.ld_pack,
+                        ref_out=rows(ref), sigma_out=rows(sigma), status=status)
+        else:
+            status.zero_()
+        seen = set()
+        for buf in (a_phi, a_psi, b, ref, sigma):
+            if buf is not None and buf.data_ptr() not in seen:
+                seen.add(buf.data_ptr())
+                gather_rows(buf, chunk, world, rank)
+        dist.all_reduce(status[:2], op=dist.ReduceOp.SUM)
+        dist.all_reduce(status[2:3], op=dist.ReduceOp.MAX)
 
     def launch_contract(self):
         lib = self.lib
@@ -395,18 +441,19 @@ class CorrelationPlan:
             if int(st[_abi.ST_NONFINITE]):
                 raise NumericError(f"{lab} dynamic-spectra matrix contains non-finite values")
         sig = []
-        for recipe, sdev, axis in ((self.recipe1, self.sigma1, axes[0]), (self.recipe2, self.sigma2, axes[1])):
+        for recipe, sdev, axis, n in ((self.recipe1, self.sigma1, axes[0], self.n1),
+                                      (self.recipe2, self.sigma2, axes[1], self.n2)):
             if recipe is None or sdev is None:
                 sig.append(None)
                 continue
-            sig.append(handle_zero_variance(axis, sdev.cpu().numpy(), recipe.alpha, recipe.substitute))
+            sig.append(handle_zero_variance(axis, sdev[:n].cpu().numpy(), recipe.alpha, recipe.substitute))
         stats = self.stats.cpu().numpy()
         if int(stats[2]):
             raise NumericError("correlation produced non-finite values")
         info = {"max_abs_sync": float(stats[0:1].view(np.float64)[0]),
                 "max_abs_async": float(stats[1:2].view(np.float64)[0])}
-        ref1 = self.ref1.cpu().numpy() if self.ref1 is not None else None
-        ref2 = self.ref2.cpu().numpy() if self.ref2 is not None else ref1
+        ref1 = self.ref1[:self.n1].cpu().numpy() if self.ref1 is not None else None
+        ref2 = self.ref2[:self.n2].cpu().numpy() if self.ref2 is not None else ref1
         if self.homo:
             sig.append(None)
             sig[1] = sig[0]

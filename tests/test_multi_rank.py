@@ -170,3 +170,55 @@ def test_quad_tiles_cover_hetero_map_once(n1, n2, G):
     T1, T2 = -(-n1 // 8), -(-n2 // 8)
     acc = pair_coverage(n1, n2, 8, False, range(quad_tile_count(T1, T2, False)), G, quad=True)
     assert np.all(acc == 1)
+
+
+def _gather_worker(rank, world, port, n, out):
+    """Each rank fills only its channel chunk of a (world*chunk) x L buffer (as
+    K1 does with spectra_shard) plus its status word; after gather_rows and the
+    status all-reduce every rank holds the full buffer and the combined status."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    from paper_1808_00685_b200.engine_core import channel_chunk, gather_rows
+    c0, c1, chunk = channel_chunk(n, world, rank)
+    buf = torch.zeros(world * chunk, 5, dtype=torch.float64)
+    for c in range(c0, c1):
+        buf[c] = torch.arange(5, dtype=torch.float64) + 10.0 * c
+    gather_rows(buf, chunk, world, rank)
+    status = torch.tensor([rank, 1 if rank == 1 else 0, 2**31 - 1 - 7 * (rank + 1), 0], dtype=torch.int32)
+    dist.all_reduce(status[:2], op=dist.ReduceOp.SUM)
+    dist.all_reduce(status[2:3], op=dist.ReduceOp.MAX)
+    out.put((rank, buf.numpy().copy(), status.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 10), (3, 10), (3, 2)])
+def test_gloo_sharded_spectra_allgather(world, n):
+    import socket
+    from paper_1808_00685_b200.engine_core import channel_chunk
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    chunk = channel_chunk(n, world, 0)[2]
+    want = np.zeros((world * chunk, 5))
+    for c in range(n):
+        want[c] = np.arange(5) + 10.0 * c
+    for rank, buf, st in res:
+        assert np.array_equal(buf, want)
+        assert st[0] == sum(range(world)) and st[1] == 1 and st[2] == 2**31 - 1 - 7
+    # chunks tile the channels exactly once
+    seen = np.zeros(n, dtype=int)
+    for r in range(world):
+        c0, c1, _ = channel_chunk(n, world, r)
+        seen[c0:c1] += 1
+    assert np.all(seen == 1)
