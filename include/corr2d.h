@@ -196,6 +196,28 @@ int corr2d_find_peaks(int dtype, const void* sync, const void* asyn, int64_t ld,
                       double thr_sync, double thr_async, int64_t* out_idx, int64_t capacity,
                       unsigned long long* count, void* stream);
 
+/* ------------------------------------- result serialization (host code) ---- */
+/*
+ * repr(float(x)) of the reference's format_number (dataset.py:34-36): shortest
+ * round-trip decimal digits laid out with CPython's repr rules.  x[0..n) are
+ * formatted back to back into out (capacity cap bytes); offsets[i + 1] is the
+ * end of item i (offsets has n + 1 entries).
+ */
+int corr2d_format_repr(const double* x, int64_t n, char* out, int64_t cap, int64_t* offsets);
+
+/*
+ * Rows [r0, r1) of a serialized correlation table (write_correlation,
+ * dataset.py:303-341): matrix-pair lines "repr(nu1)<d>repr(m[i,0])<d>..." or,
+ * with long_form != 0, one "nu1,nu2,sync,async" line per element (matrix =
+ * sync, matrix2 = async).  Host pointers; dtype CORR2D_F64 or CORR2D_F32
+ * (float32 values are written as the float64 they convert to, like
+ * repr(float(np.float32))).  `threads` host threads.  *written receives the
+ * byte count; if it exceeds cap the call fails and nothing is copied.
+ */
+int corr2d_format_rows(int dtype, const double* axis1, const double* axis2, const void* matrix,
+                       const void* matrix2, int64_t ld, int n2, int r0, int r1, char delim, int long_form,
+                       int threads, char* out, int64_t cap, int64_t* written);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,8 @@ from .errors import CorrtwoError, DataError, NumericError, ParseError
 from .fourier import (DeviceCorrelationSpectra, FourierWorkspace, correlate_ft, dft_channels,
                       half_spectrum_weights)
 from .hilbert import correlate_ht, hilbert_noda_matrix, hilbert_transform, sync_direct
+from .serialize import (LONG_FORM, MATRIX_PAIR, correlation_paths, format_number, save_correlation,
+                        write_correlation)
 from .preprocess import (DynamicSpectra, InterpolantKind, PreprocessSpec, ReferenceSpec,
                          ResampleSpec, apply_scaling, default_target_count, dynamic_spectra,
                          mean_reference, preprocess_dataset, resample_equidistant,
@@ -35,5 +37,6 @@ __all__ = [
     "dft_channels", "dynamic_spectra", "half_spectrum_weights", "hilbert_noda_matrix",
     "hilbert_transform", "is_same_dynamic",
     "mean_reference", "preprocess_dataset", "resample_equidistant", "resample_to_axis",
-    "row_blocks", "stddev_spectrum", "sync_direct",
+    "row_blocks", "stddev_spectrum", "sync_direct", "LONG_FORM", "MATRIX_PAIR", "correlation_paths",
+    "format_number", "save_correlation", "write_correlation",
 ]

@@ -30,6 +30,7 @@ EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
     "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
+    "corr2d_format_repr", "corr2d_format_rows",
 )
 
 
@@ -72,7 +73,11 @@ def _declare(lib):
     lib.corr2d_plane_absmax.argtypes = [c_int, c_void, c_i64, c_int, c_int, c_void, c_void]
     lib.corr2d_find_peaks.argtypes = [c_int, c_void, c_void, c_i64, c_int, c_int, c_int, c_double, c_double,
                                       c_void, c_i64, c_void, c_void]
-    for name in ("corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
+    lib.corr2d_format_repr.argtypes = [c_void, c_i64, c_void, c_i64, c_void]
+    lib.corr2d_format_rows.argtypes = [c_int, c_void, c_void, c_void, c_void, c_i64, c_int, c_int, c_int,
+                                       ctypes.c_char, c_int, c_int, c_void, c_i64, c_void]
+    for name in ("corr2d_format_repr", "corr2d_format_rows",
+                 "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
                  "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
                  "corr2d_plane_absmax", "corr2d_find_peaks"):
         getattr(lib, name).restype = c_int

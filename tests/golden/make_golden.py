@@ -167,6 +167,29 @@ def small_cases(manifest):
              verdicts=np.array([str(p.verdict) for p in rep.cross_peaks]),
              table=np.array(rep.to_table()), long_form=np.frombuffer(rep.to_long_form(), dtype=np.uint8))
         manifest[name] = {"kind": "peaks", "auto": len(rep.auto_peaks), "cross": len(rep.cross_peaks)}
+    # serialization -- dataset.py:292-341 byte for byte
+    from corrtwo.dataset import write_correlation
+    ser = [("ser_homo_m64", "homo_m64_n20", "matrix-pair", ","),
+           ("ser_hetero_m21", "hetero_m21_37x29", "matrix-pair", ";"),
+           ("ser_long_m11", "homo_m11_n13", "long-form", ",")]
+    for name, src, fmt, delim in ser:
+        g = np.load(HERE / f"{src}.npz")
+        n1, n2 = g["sync"].shape
+        t = g["t"]
+        ax1 = g["nu"] if "nu" in g else g["nu1"]
+        ax2 = g["nu"] if "nu" in g else g["nu2"]
+        d1 = DynamicSpectra(ax1, t, np.zeros((t.size, n1)), np.linspace(-1.0, 1.0, n1) / 3.0)
+        d2 = DynamicSpectra(ax2, t, np.zeros((t.size, n2)), np.linspace(2.0, 5.0, n2) / 7.0)
+        from corrtwo import CorrelationSpectra
+        res = CorrelationSpectra(axis1=ax1, axis2=ax2, sync=g["sync"], asyn=g["asyn"], ref1=d1.reference_used,
+                                 ref2=d2.reference_used if n1 != n2 or "nu1" in g else d1.reference_used,
+                                 normalization=float(g["norm"]), engine="fourier", is_homo="nu" in g,
+                                 scaling_exponent=0.0)
+        payload = write_correlation(res, fmt, delim)
+        save(name, src=np.array(src), fmt=np.array(fmt), delim=np.array(delim),
+             ref1=res.ref1, ref2=res.ref2,
+             **{k.replace(".", "_"): np.frombuffer(v, dtype=np.uint8) for k, v in payload.items()})
+        manifest[name] = {"kind": "serialize", "src": src, "fmt": fmt}
 
 
 def config_cases(manifest):
