@@ -162,14 +162,16 @@ extern "C" int corr2d_format_rows(int dtype, const double* axis1, const double* 
   for (int t = 1; t < threads; ++t) pool.emplace_back(work, t);
   work(0);
   for (auto& th : pool) th.join();
-  int64_t total = 0;
-  for (auto& p : parts) total += (int64_t)p.size();
+  std::vector<int64_t> offs(threads + 1, 0);
+  for (int t = 0; t < threads; ++t) offs[t + 1] = offs[t] + (int64_t)parts[t].size();
+  const int64_t total = offs[threads];
   *written = total;
   if (total > cap) return fail(CORR2D_ERR_DATA, "corr2d_format_rows: buffer too small");
-  int64_t pos = 0;
-  for (auto& p : parts) {
-    memcpy(out + pos, p.data(), p.size());
-    pos += (int64_t)p.size();
-  }
+  // parallel gather of the per-thread parts into the caller's buffer
+  auto copy = [&](int t) { memcpy(out + offs[t], parts[t].data(), parts[t].size()); };
+  pool.clear();
+  for (int t = 1; t < threads; ++t) pool.emplace_back(copy, t);
+  copy(0);
+  for (auto& th : pool) th.join();
   return CORR2D_OK;
 }

@@ -78,21 +78,23 @@ def _table_blocks(result, matrix, matrix2, delimiter: str, long_form: bool):
     rows = max(1, _BLOCK_BYTES // per_row)
     threads = _threads()
     written = ctypes.c_int64(0)
+    buf = np.empty(0, dtype=np.uint8)      # reused across blocks, never zero-filled
     for r0 in range(0, n1, rows):
         r1 = min(n1, r0 + rows)
         cap = (r1 - r0) * per_row + 64
         while True:
-            buf = ctypes.create_string_buffer(cap)
+            if buf.size < cap:
+                buf = np.empty(cap, dtype=np.uint8)
             code = lib.corr2d_format_rows(dt, ax1.ctypes.data, ax2.ctypes.data, m1.ctypes.data,
                                           None if m2 is None else m2.ctypes.data, ld, n2, r0, r1,
-                                          delimiter.encode(), 1 if long_form else 0, threads, buf, cap,
-                                          ctypes.byref(written))
+                                          delimiter.encode(), 1 if long_form else 0, threads, buf.ctypes.data,
+                                          buf.size, ctypes.byref(written))
             if code == 0:
                 break
-            if written.value <= cap:
+            if written.value <= buf.size:
                 _abi.check(code, lib)
             cap = written.value
-        yield buf.raw[:written.value]
+        yield memoryview(buf)[:written.value]
 
 
 def _payload_parts(result, fmt: str, delimiter: str):
@@ -121,7 +123,7 @@ def _payload_parts(result, fmt: str, delimiter: str):
 def write_correlation(result, fmt: str = MATRIX_PAIR, delimiter: str = ",") -> dict[str, bytes]:
     """Serialize a correlation result: ``{"sync.csv", "async.csv"}`` payloads
     (matrix-pair) or ``{"corr.csv"}`` (long-form), as dataset.py:311-341."""
-    return {k: b"".join(v) for k, v in _payload_parts(result, fmt, delimiter).items()}
+    return {k: b"".join(bytes(c) for c in v) for k, v in _payload_parts(result, fmt, delimiter).items()}
 
 
 def correlation_paths(stem, fmt: str = MATRIX_PAIR) -> dict[str, Path]:
