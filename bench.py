@@ -76,10 +76,17 @@ def workload(cfg):
 
 
 def roofline_peak(case, peaks):
-    """(bound, peak, unit) for the dominant (contraction) kernel."""
+    """(bound, peak, unit, burst peak) for the dominant (contraction) kernel.
+    K2 is timed over back-to-back graph replays (tens of ms of tensor work), so
+    the bf16 kernel runs in the power-capped regime: its denominator is the
+    SUSTAINED measured bf16 figure (MEASURED_PEAKS.json, B200_PROFILING.md);
+    the burst figure is reported beside it.  FP64 DMMA does not reach the cap
+    (cfg3 holds 1965 MHz): one measured figure."""
     if case.dtype == "float32":      # bf16x3 on the f16 tensor pipe
-        return "tensor", float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])), "TFLOP/s"
-    return "tensor", FP64_DMMA_TFLOPS, "TFLOP/s"
+        burst = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+        sus = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
+        return "tensor", sus, "TFLOP/s", burst
+    return "tensor", FP64_DMMA_TFLOPS, "TFLOP/s", FP64_DMMA_TFLOPS
 
 
 # --------------------------------------------------------------------------
@@ -319,7 +326,7 @@ def run_b200(args, case, wl, world, rank, local):
     elems_total = wl["elems"] * args.steps
     value = elems_total / (ms_max * 1e-3) / 1e9
     peaks = measured_peaks()
-    bound, peak, unit = roofline_peak(case, peaks)
+    bound, peak, unit, peak_burst = roofline_peak(case, peaks)
     achieved = wl["flops"] / (k2_avg * 1e-3) / 1e12
     traffic = load_traffic(case.cfg)
     line = {
@@ -331,10 +338,12 @@ def run_b200(args, case, wl, world, rank, local):
         "config": config_block(case, wl, args),
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
+                     "peak_burst": peak_burst, "frac_vs_burst": achieved / peak_burst,
                      "kernel": contract_kernel_name(case),
                      "kernel_ms": k2_avg, "algorithmic": "8*K flops per complex output element",
                      "hbm_floor_ms": (wl["out_bytes"] + wl["in_bytes"]) / (peaks["hbm_gbs"] * 1e9) * 1e3,
-                     "peak_source": peaks["_source"] + ("" if case.dtype == "float32" else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
+                     "peak_source": peaks["_source"] + (" (bf16 sustained; burst in peak_burst)" if case.dtype == "float32"
+                                                        else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
         "clocks": clocks.summary(),
         "gpu_launches": plan.launches_per_step * args.steps,
         "parity": parity,

@@ -564,9 +564,32 @@ __device__ __forceinline__ void stage_and_store_mreg(uint8_t* w, int l, const fl
   stage_and_store_32_plane_mreg<PENDING>(w, l, v, m, s, md, pl, ld, n, c, r, pol);
 }
 template <int PENDING>
-__device__ __forceinline__ void stage_and_store_mreg(uint8_t*, int, const float (&)[16], bool, float,
-                                                     const CUtensorMap*, float*, long long, int, int, int, uint64_t) {
-  __trap();  // register-mirror path exists for 32-column chunks only
+__device__ __forceinline__ void stage_and_store_mreg(uint8_t* wst, int lane, const float (&v)[16], bool mirror,
+                                                     float tsign, const CUtensorMap* map_direct, float* plane,
+                                                     long long ld_out, int n, int cbase, int row0q, uint64_t pol) {
+  // 16-column chunk: direct box 32 rows x 64 B (SWIZZLE_64B) by TMA, mirror rows
+  // straight from registers (one 128-B line per store instruction)
+  if (lane == 0) bulk_wait_read<PENDING>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    *reinterpret_cast<float4*>(wst + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
+        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  fence_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map_direct, wst, cbase, row0q, pol);
+    bulk_commit();
+  }
+  if (mirror && row0q + lane < n) {
+    float* dst = plane + (long long)cbase * ld_out + row0q + lane;
+    const int kmax = n - cbase < 16 ? n - cbase : 16;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < kmax)
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(dst + (long long)k * ld_out),
+                     "f"(tsign * v[k]), "l"(pol) : "memory");
+  }
 }
 
 __device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS2) : "memory"); }
@@ -1397,7 +1420,10 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
           for (int c = 0; c < BN / CH2; ++c) {
 #pragma unroll 1
             for (int plane = pw; plane < pw + PPW2; ++plane) {
-              uint8_t* wst = staging + (warp - 2) * WSTG2 + (NBUF2 == 1 ? 0 : (plane - pw)) * (WSTG2 / NBUF2);
+              // buffers alternate between the planes (4 epilogue warps) or the
+              // chunks (8 warps, one plane each)
+              const int bsel = NBUF2 == 1 ? 0 : (PPW2 == 1 ? (c & 1) : (plane - pw));
+              uint8_t* wst = staging + (warp - 2) * WSTG2 + bsel * (WSTG2 / NBUF2);
               const float tsign = plane == 0 ? 1.f : -1.f;
               float mx = 0.f;
               uint32_t ua[CH2];
@@ -1435,9 +1461,6 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               }
               const long long ts0 = tr ? clock64() : 0;
               if (p.dbg & 1) {
-              } else if (CH2 == 16) {
-                stage_and_store_plane<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
-                                                 &outm.m[plane][1], j0 + c * CH2, i0 + 32 * q, drop);
               } else if (p.mirror_reg) {
                 stage_and_store_mreg<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
                                                 plane == 0 ? p.phi : p.psi, p.ld_out, p.n1,
