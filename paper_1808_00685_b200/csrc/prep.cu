@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 namespace corr2d {
@@ -526,6 +527,446 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
   mark(6);
 }
 
+// ---------------------------------------------------------------------------
+// K1 fast path: one warp per channel pair, the whole length-m transform in
+// registers.  m = 32 R (R = 2, 4, 8, 16), no resampling, CORR2D_PACK_BF16X2 or
+// CORR2D_PACK_F64 (m <= 128).  A CTA of 8 warps takes 16 channels: the raw
+// m x 16 block is staged in shared memory channel-major (conflict-free column
+// reads), each warp pulls its two channels into registers as z = x_even + i x_odd
+// (lane l holds samples l + 32 t), takes the per-channel statistics in the same
+// summation order as the generic kernel (so reference / sigma / values are the
+// same bits), and runs the four-step FFT m = R x 32: a length-R DFT in registers,
+// twiddles W_m^(l k1), a length-32 DIF butterfly network across lanes (shuffles;
+// lane l ends with X[k1 + R bitrev5(l)]).  The two real spectra are split with
+// one xor-31 shuffle, packed into a shared-memory row image and written with
+// 16-byte stores.  Numerically a different FFT than the generic kernel's
+// Stockham passes (both ~1e-16 relative).
+// ---------------------------------------------------------------------------
+constexpr int kFastThreads = 256;
+constexpr int kFastCh = 16;
+
+// complex helpers for the single-precision transform of the bf16 packing path
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 mul_mi(float2 a) { return make_float2(a.y, -a.x); }
+template <typename C2> __device__ __forceinline__ C2 cmake(double a, double b);
+template <> __device__ __forceinline__ double2 cmake<double2>(double a, double b) { return make_double2(a, b); }
+template <> __device__ __forceinline__ float2 cmake<float2>(double a, double b) { return make_float2((float)a, (float)b); }
+
+template <typename C2> __device__ __forceinline__ void gdft2(C2& a, C2& b) {
+  const C2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+template <typename C2> __device__ __forceinline__ void gdft4(C2& x0, C2& x1, C2& x2, C2& x3) {
+  const C2 t0 = cadd(x0, x2), t1 = csub(x0, x2), t2 = cadd(x1, x3), t3 = mul_mi(csub(x1, x3));
+  x0 = cadd(t0, t2);
+  x2 = csub(t0, t2);
+  x1 = cadd(t1, t3);
+  x3 = csub(t1, t3);
+}
+// length-R DFT in registers, natural order in and out (R = 2, 4, 8, 16);
+// tw = W_m^q table of the compute type
+template <int R, typename C2> __device__ __forceinline__ void gdft(C2 (&x)[R], const C2* __restrict__ tw, int m) {
+  if constexpr (R == 2) {
+    gdft2(x[0], x[1]);
+  } else if constexpr (R == 4) {
+    gdft4(x[0], x[1], x[2], x[3]);
+  } else if constexpr (R == 8) {
+    // 8 = 2 x 4: evens / odds by radix 4, then W8 twiddles and a radix-2 combine
+    gdft4(x[0], x[2], x[4], x[6]);
+    gdft4(x[1], x[3], x[5], x[7]);
+    const int step = m / 8;
+    const C2 o0 = x[1], o1 = cmul(x[3], tw[step]), o2 = cmul(x[5], tw[2 * step]), o3 = cmul(x[7], tw[3 * step]);
+    const C2 e0 = x[0], e1 = x[2], e2 = x[4], e3 = x[6];
+    x[0] = cadd(e0, o0); x[4] = csub(e0, o0);
+    x[1] = cadd(e1, o1); x[5] = csub(e1, o1);
+    x[2] = cadd(e2, o2); x[6] = csub(e2, o2);
+    x[3] = cadd(e3, o3); x[7] = csub(e3, o3);
+  } else {
+    // 16 = 4 x 4: y[t1][u] = DFT4_t2 x[t1 + 4 t2]; y *= W16^(t1 u); X[u + 4 v] = DFT4_t1 y
+    C2 y[4][4];
+#pragma unroll
+    for (int t1 = 0; t1 < 4; ++t1) {
+#pragma unroll
+      for (int t2 = 0; t2 < 4; ++t2) y[t1][t2] = x[t1 + 4 * t2];
+      gdft4(y[t1][0], y[t1][1], y[t1][2], y[t1][3]);
+    }
+    const int step = m / 16;
+#pragma unroll
+    for (int t1 = 1; t1 < 4; ++t1)
+#pragma unroll
+      for (int u = 1; u < 4; ++u) y[t1][u] = cmul(y[t1][u], tw[t1 * u * step]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      C2 a = y[0][u], b = y[1][u], c = y[2][u], d = y[3][u];
+      gdft4(a, b, c, d);
+      x[u] = a; x[u + 4] = b; x[u + 8] = c; x[u + 12] = d;
+    }
+  }
+}
+
+__device__ __forceinline__ double2 shfl_c(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ double2 shfl_xor_c(double2 v, int mask) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
+}
+__device__ __forceinline__ float2 shfl_c(float2 v, int src) {
+  return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+__device__ __forceinline__ float2 shfl_xor_c(float2 v, int mask) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
+}
+
+// BF: CORR2D_PACK_BF16X2 -- the transform runs in fp32 (the spectra are then
+// split into bf16 hi + lo, ~16 bits, far below fp32's rounding), else fp64.
+template <int R, typename TIN, bool BF>
+__global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepParams p) {
+  constexpr int M = 32 * R;
+  using C2 = typename std::conditional<BF, float2, double2>::type;
+  using CT = typename std::conditional<BF, float, double>::type;
+  extern __shared__ __align__(16) double smem[];
+  C2* tw = reinterpret_cast<C2*>(smem);                               // M
+  uint8_t* work = reinterpret_cast<uint8_t*>(smem) + M * sizeof(double2);   // raw block, later row images
+  TIN* raw_s = reinterpret_cast<TIN*>(work);                           // [16][M + 1]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c0 = blockIdx.x * kFastCh;
+  const int nc = min(kFastCh, p.n - c0);
+  long long tr_t = (p.trace && tid == 0) ? clock64() : 0;
+  auto mark = [&](int ph) {
+    if (p.trace && tid == 0) {
+      const long long now = clock64();
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + ph), (unsigned long long)(now - tr_t));
+      tr_t = now;
+    }
+  };
+
+  for (int q = tid; q < M; q += kFastThreads) {
+    double sv, cv;
+    sincospi(-2.0 * (double)q / (double)M, &sv, &cv);
+    tw[q] = cmake<C2>(cv, sv);
+  }
+  // raw block, channel-major in shared memory; full aligned blocks use 16-byte
+  // loads, all of a thread's loads issued before the first store
+  int bad = 0;
+  const TIN* raw = static_cast<const TIN*>(p.raw);
+  constexpr int V = 16 / (int)sizeof(TIN), G = kFastCh / V;      // channels per vector, vectors per row
+  const bool vec = nc == kFastCh && ((reinterpret_cast<uintptr_t>(raw) & 15) == 0) &&
+                   ((p.ld_raw * (long long)sizeof(TIN)) % 16 == 0);
+  if (vec) {
+    constexpr int PER = M * G / kFastThreads;                     // vectors per thread
+    uint4 buf[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = tid + u * kFastThreads, r = idx / G, g = idx % G;
+      buf[u] = __ldcs(reinterpret_cast<const uint4*>(raw + (long long)r * p.ld_raw + c0 + g * V));
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = tid + u * kFastThreads, r = idx / G, g = idx % G;
+      const TIN* v = reinterpret_cast<const TIN*>(&buf[u]);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        bad += !isfinite((double)v[e]);
+        raw_s[(g * V + e) * (M + 1) + r] = v[e];
+      }
+    }
+  } else {
+    for (int idx = tid; idx < M * kFastCh; idx += kFastThreads) {
+      const int r = idx >> 4, c = idx & 15;
+      TIN v = (TIN)0;
+      if (c < nc) {
+        v = raw[(long long)r * p.ld_raw + c0 + c];
+        bad += !isfinite((double)v);
+      }
+      raw_s[c * (M + 1) + r] = v;
+    }
+  }
+  bad = warp_sum(bad);
+  if (lane == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
+  __syncthreads();
+  mark(0);
+
+  // this warp's channel pair, samples l + 32 t
+  double xv[2][R];
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int t = 0; t < R; ++t) xv[e][t] = (double)raw_s[(2 * warp + e) * (M + 1) + lane + 32 * t];
+
+  // per-channel statistics (generic kernel's summation orders), normalisation
+  const bool normalise = p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0;
+  if (normalise) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 2 * warp + e;
+      if (c >= nc) continue;   // padding channels stay 0 (warp-uniform branch)
+      const TIN* col = raw_s + c * (M + 1);
+      double ref = 0.0;
+      if (p.ref_mode == CORR2D_REF_PROVIDED) {
+        ref = c < nc ? __ldg(p.ref_in + c0 + c) : 0.0;
+      } else if (p.ref_mode == CORR2D_REF_MEAN) {
+        double sum = 0.0;
+        if (M <= kSeqStatsMax) {        // numpy's axis-0 order, left to right
+          if (lane == 0) {
+            double cv[M];
+#pragma unroll
+            for (int k = 0; k < M; ++k) cv[k] = (double)col[k];
+#pragma unroll
+            for (int k = 0; k < M; ++k) sum = __dadd_rn(sum, cv[k]);
+          }
+          sum = __shfl_sync(0xffffffffu, sum, 0);
+        } else {                        // lane partials over k = lane + 32 t, xor tree
+#pragma unroll
+          for (int t = 0; t < R; ++t) sum = __dadd_rn(sum, xv[e][t]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        }
+        ref = __ddiv_rn(sum, (double)M);
+      }
+      double scale = 1.0;
+      if (p.alpha > 0.0) {
+        double sigma;
+        if (p.sigma_in) {
+          sigma = c < nc ? __ldg(p.sigma_in + c0 + c) : 1.0;
+        } else {
+          double ss = 0.0;
+          if (M <= kSeqStatsMax) {
+            if (lane == 0) {
+              double dv[M];
+#pragma unroll
+              for (int k = 0; k < M; ++k) {
+                const double d = __dsub_rn((double)col[k], ref);
+                dv[k] = __dmul_rn(d, d);
+              }
+#pragma unroll
+              for (int k = 0; k < M; ++k) ss = __dadd_rn(ss, dv[k]);
+            }
+            ss = __shfl_sync(0xffffffffu, ss, 0);
+          } else {
+#pragma unroll
+            for (int t = 0; t < R; ++t) {
+              const double d = __dsub_rn(xv[e][t], ref);
+              ss = __dadd_rn(ss, __dmul_rn(d, d));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+          }
+          sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(M - 1)));
+        }
+        if (lane == 0 && c < nc) {
+          if (p.sigma_out) p.sigma_out[c0 + c] = sigma;
+          if (sigma == 0.0) {
+            atomicAdd(&p.status[CORR2D_ST_ZEROVAR], 1);
+            atomicMax(&p.status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - (c0 + c));
+          }
+        }
+        if (sigma == 0.0 && p.substitute) sigma = 1.0;
+        scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
+      }
+      if (lane == 0 && c < nc && p.ref_out) p.ref_out[c0 + c] = ref;
+      const bool sub = p.ref_mode != CORR2D_REF_NONE, scaled = p.alpha > 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        if (sub) xv[e][t] = __dsub_rn(xv[e][t], ref);
+        if (scaled) xv[e][t] = __ddiv_rn(xv[e][t], scale);
+      }
+    }
+  }
+
+  mark(1);
+  // four-step FFT of z = x_even + i x_odd (compute type CT)
+  C2 z[R];
+#pragma unroll
+  for (int t = 0; t < R; ++t) z[t] = cmake<C2>(xv[0][t], xv[1][t]);
+  gdft<R, C2>(z, tw, M);
+  {
+    // W_m^(lane k1) by recurrence from W_m^lane: one shared-memory load instead
+    // of R - 1 strided (bank-conflicting) table reads
+    const C2 w1 = tw[lane];
+    C2 wk = w1;
+#pragma unroll
+    for (int k1 = 1; k1 < R; ++k1) {
+      z[k1] = cmul(z[k1], wk);
+      if (k1 + 1 < R) wk = cmul(wk, w1);
+    }
+  }
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1) {   // length-32 DIF across lanes
+    const C2 w = tw[(lane & (h - 1)) * (M / (2 * h))];
+    const bool upper = (lane & h) != 0;
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) {
+      const C2 o = shfl_xor_c(z[k1], h);
+      z[k1] = upper ? cmul(csub(o, z[k1]), w) : cadd(z[k1], o);
+    }
+  }
+  // lane holds Z[k1 + R k2], k2 = bitrev5(lane), k1 = 0..R-1 (R consecutive
+  // bins); the two real spectra at bin q need Z[m - q]: lane ^ 31, register
+  // R - k1 (k1 > 0), or lane bitrev5(-k2 mod 32), register 0 (k1 = 0)
+  const int k2 = (int)(__brev((unsigned)lane) >> 27);
+  const int src0 = (int)(__brev((unsigned)((32 - k2) & 31)) >> 27);
+  auto split = [&](int k1, C2& ye, C2& yo) {
+    const C2 zr = k1 == 0 ? shfl_c(z[0], src0) : shfl_xor_c(z[R - k1], 31);
+    ye = cmake<C2>(0.5 * ((double)z[k1].x + (double)zr.x), 0.5 * ((double)z[k1].y - (double)zr.y));
+    yo = cmake<C2>(0.5 * ((double)z[k1].y + (double)zr.y), -0.5 * ((double)z[k1].x - (double)zr.x));
+  };
+  mark(2);
+  __syncthreads();  // raw block consumed: the area now holds the packed row images
+
+  const int H = M / 2;
+  if constexpr (BF) {
+    // row image: thirds [Re' | Im' | -Im'] of hp = H slots, 32-slot blocks
+    // [hi 32 | lo 32], then float2 (hi + lo of Re'[0], Im'[0]) at 6 hp.  A
+    // lane's R consecutive bins land as 2R contiguous bytes per (third, plane);
+    // 16-byte chunks are XOR-swizzled within each 128-byte line by the line
+    // index (bank spread), undone by the copy-out.
+    const int hp = H;
+    const int img = 6 * hp * 2 + 128;
+    auto swz = [](int byte) { return byte ^ (((byte >> 7) & 7) << 4); };
+    const float sn1 = (float)sqrt(p.norm), sn2 = (float)sqrt(2.0 * p.norm);
+    C2 ye[R], yo[R];
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) split(k1, ye[k1], yo[k1]);
+    const float nyq0 = __shfl_sync(0xffffffffu, (float)ye[0].x, 1);   // bin m/2: register 0 of lane 1
+    const float nyq1 = __shfl_sync(0xffffffffu, (float)yo[0].x, 1);
+    const int q0 = R * k2;
+    if (q0 < H) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        uint8_t* rb = work + (size_t)(2 * warp + e) * img;
+        __align__(16) __nv_bfloat16 re_h[R], re_l[R], im_h[R], im_l[R], ng_h[R], ng_l[R];
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) {
+          const C2 y = e ? yo[k1] : ye[k1];
+          const int q = q0 + k1;
+          const float vr = (float)y.x * (q == 0 ? sn1 : sn2);
+          const float vi = q == 0 ? (e ? nyq1 : nyq0) * sn1 : (float)y.y * sn2;
+          re_h[k1] = __float2bfloat16_rn(vr);
+          re_l[k1] = __float2bfloat16_rn(vr - __bfloat162float(re_h[k1]));
+          im_h[k1] = __float2bfloat16_rn(vi);
+          im_l[k1] = __float2bfloat16_rn(vi - __bfloat162float(im_h[k1]));
+          ng_h[k1] = __hneg(im_h[k1]);
+          ng_l[k1] = __hneg(im_l[k1]);
+        }
+        const int o = ((q0 >> 5) * 64 + (q0 & 31)) * 2;    // byte offset of bin q0 in a third
+        auto put = [&](int off, const __nv_bfloat16 (&v)[R]) {
+          if constexpr (2 * R >= 16) {
+#pragma unroll
+            for (int j = 0; j < 2 * R / 16; ++j)
+              *reinterpret_cast<uint4*>(rb + swz(off + 16 * j)) = reinterpret_cast<const uint4*>(v)[j];
+          } else if constexpr (2 * R == 8) {
+            *reinterpret_cast<uint2*>(rb + swz(off)) = *reinterpret_cast<const uint2*>(v);
+          } else {
+            *reinterpret_cast<uint32_t*>(rb + swz(off)) = *reinterpret_cast<const uint32_t*>(v);
+          }
+        };
+        put(o, re_h); put(o + 64, re_l);
+        put(4 * hp + o, im_h); put(4 * hp + o + 64, im_l);
+        put(8 * hp + o, ng_h); put(8 * hp + o + 64, ng_l);
+        if (q0 == 0)
+          *reinterpret_cast<float2*>(rb + swz(12 * hp)) =
+              make_float2(__bfloat162float(re_h[0]) + __bfloat162float(re_l[0]),
+                          __bfloat162float(im_h[0]) + __bfloat162float(im_l[0]));
+      }
+    }
+    __syncwarp();
+    const int vec = (6 * hp * 2 + 8 + 15) / 16;      // 16-byte chunks incl. the float2 pad
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 2 * warp + e;
+      if (c >= nc) continue;
+      const uint8_t* src = work + (size_t)c * img;
+      for (int role = 0; role < 2; ++role) {
+        if (!(p.pack_roles & (role ? CORR2D_ROLE_B : CORR2D_ROLE_A))) continue;
+        __nv_bfloat16* base = static_cast<__nv_bfloat16*>(role ? p.b : p.a_phi);
+        uint4* dst = reinterpret_cast<uint4*>(base + (long long)(c0 + c) * p.ld_pack);
+        for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(src + swz(16 * i));
+      }
+    }
+  } else {
+    // CORR2D_PACK_F64 (M <= 128): slot s < K -> Re Y(s), K <= s < m -> Im Y(s - K + 1);
+    // images A_phi | A_psi | B of M doubles each
+    const int K = H + 1;
+    const int img = 3 * M * 8;
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) {
+      C2 yy[2];
+      split(k1, yy[0], yy[1]);
+      const int w = k1 + R * k2;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (w > H) continue;
+        double* row = reinterpret_cast<double*>(work + (size_t)(2 * warp + e) * img);
+        const C2 y = yy[e];
+        const bool edge = (w == 0 || w == H);
+        const double Rv = y.x, Iv = edge ? 0.0 : (double)y.y;
+        double nr = p.norm * Rv, ni = p.norm * Iv;
+        if (!edge) { nr *= 2.0; ni *= 2.0; }
+        row[w] = nr; row[M + w] = ni; row[2 * M + w] = Rv;                  // Re slot s = w
+        if (!edge) {
+          const int s = K + w - 1;                                          // Im slot
+          row[s] = ni; row[M + s] = -nr; row[2 * M + s] = Iv;
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 2 * warp + e;
+      if (c >= nc) continue;
+      const double* src = reinterpret_cast<const double*>(work + (size_t)c * img);
+      const long long o = (long long)(c0 + c) * p.ld_pack;
+      for (int s = lane; s < M; s += 32) {
+        if (p.pack_roles & CORR2D_ROLE_A) {
+          static_cast<double*>(p.a_phi)[o + s] = src[s];
+          static_cast<double*>(p.a_psi)[o + s] = src[M + s];
+        }
+        if (p.pack_roles & CORR2D_ROLE_B) static_cast<double*>(p.b)[o + s] = src[2 * M + s];
+      }
+    }
+  }
+  mark(3);
+}
+
+static bool fast_eligible(const PrepParams& p) {
+  if (const char* e = getenv("CORR2D_PREP_FAST"))
+    if (e[0] == '0') return false;
+  if (p.resample_kind != CORR2D_RESAMPLE_NONE || p.values_out || p.half_out) return false;
+  if (p.m != 64 && p.m != 128 && p.m != 256 && p.m != 512) return false;
+  if (p.pack_kind == CORR2D_PACK_BF16X2) return p.mp == 3 * (p.m / 2);
+  return p.pack_kind == CORR2D_PACK_F64 && p.m <= 128 && p.mp == p.m;
+}
+
+static size_t fast_smem(const PrepParams& p) {
+  const int M = p.m;
+  const size_t raw = (size_t)kFastCh * (M + 1) * (p.in_f32 ? 4 : 8);
+  const size_t img = p.pack_kind == CORR2D_PACK_BF16X2 ? (size_t)kFastCh * (6 * (M / 2) * 2 + 128)
+                                                       : (size_t)kFastCh * 3 * M * 8;
+  return (size_t)M * sizeof(double2) + (raw > img ? raw : img);
+}
+
+template <int R, bool BF>
+static void launch_fast_rb(const PrepParams& p, size_t smem, cudaStream_t st) {
+  const int grid = (p.n + kFastCh - 1) / kFastCh;
+  if (p.in_f32) {
+    cudaFuncSetAttribute(prep_fast_kernel<R, float, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    prep_fast_kernel<R, float, BF><<<grid, kFastThreads, smem, st>>>(p);
+  } else {
+    cudaFuncSetAttribute(prep_fast_kernel<R, double, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    prep_fast_kernel<R, double, BF><<<grid, kFastThreads, smem, st>>>(p);
+  }
+}
+template <int R>
+static void launch_fast_r(const PrepParams& p, size_t smem, cudaStream_t st) {
+  if (p.pack_kind == CORR2D_PACK_BF16X2) launch_fast_rb<R, true>(p, smem, st);
+  else if constexpr (R <= 4) launch_fast_rb<R, false>(p, smem, st);   // F64 packing: m <= 128
+}
+
 static int fft_factorize(int m, int* f, int maxf) {
   int k = 0;
   for (int r : {8, 4, 2}) {
@@ -631,6 +1072,34 @@ extern "C" int corr2d_prep(
   if (values_out && ld_values < n) return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_values < n");
   p.nfactors = fft_factorize(m, p.factors, kMaxFactors);
   if (p.nfactors < 0) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_prep: FFT factorisation failed");
+
+  if (fast_eligible(p)) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    static long long* ftrace = nullptr;
+    const char* ftrc = getenv("CORR2D_PREP_TRACE");
+    if (ftrc && ftrc[0] == '1') {
+      if (!ftrace) cudaMalloc(&ftrace, 16 * sizeof(long long));
+      cudaMemsetAsync(ftrace, 0, 16 * sizeof(long long), st);
+      p.trace = ftrace;
+    }
+    if (cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), st) != cudaSuccess) return check_launch("status reset");
+    const size_t smem = fast_smem(p);
+    switch (m) {
+      case 64: launch_fast_r<2>(p, smem, st); break;
+      case 128: launch_fast_r<4>(p, smem, st); break;
+      case 256: launch_fast_r<8>(p, smem, st); break;
+      default: launch_fast_r<16>(p, smem, st); break;
+    }
+    if (p.trace) {
+      long long h[16];
+      cudaMemcpyAsync(h, p.trace, sizeof(h), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const double g = (double)((n + kFastCh - 1) / kFastCh);
+      fprintf(stderr, "prep fast trace (cycles/CTA, grid=%.0f): load %.0f stats %.0f fft %.0f pack %.0f\n", g,
+              h[0] / g, h[1] / g, h[2] / g, h[3] / g);
+    }
+    return check_launch("prep_fast_kernel");
+  }
 
   const bool resample = resample_kind != CORR2D_RESAMPLE_NONE;
   int C = 64;
