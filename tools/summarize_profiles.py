@@ -120,6 +120,12 @@ def main():
             k = con[-1]
             traffic[cfg] = k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
     tpath.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
+    for rep in sorted(src.glob("full_peaks*.ncu-rep")):
+        (dst / f"{rnd}_ncu_{rep.stem[5:]}.json").write_text(json.dumps(ncu_raw(rep), indent=1) + "\n")
+    ex = src / "extras.json"
+    if ex.exists():
+        lines = [json.loads(l) for l in ex.read_text().splitlines() if l.startswith("{")]
+        (dst / f"{rnd}_extras.json").write_text(json.dumps(lines, indent=1) + "\n")
     print("wrote", sorted(p.name for p in dst.iterdir()))
 
 
