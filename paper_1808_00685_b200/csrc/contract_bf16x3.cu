@@ -55,53 +55,27 @@ constexpr int STG_BYTES = 2 * (STG_DIRECT + STG_MIRROR);
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 2 * BN * 4 + 16 * 8 + 16;
-// CTA-pair kernels: 2 operand stages, 32-column epilogue chunks staged per warp as
-// {sync tile, async tile, sync mirror, async mirror} boxes of 32 x 32 fp32 (SWIZZLE_128B)
-// Operand stages: 2 x 64 KB of 32-slot boxes (64-B rows, SWIZZLE_64B).  Measured
-// alternatives on cfg5: 4 x 32 KB of 16-slot boxes (SWIZZLE_32B) 5.25 ms -- the
-// narrow TMA boxes and the doubled per-stage handshakes cost more than the
-// deeper ring gains; 3 x 64 KB only fits with half the epilogue staging.
+// CTA-pair kernels: 3 operand stages of 64 KB (4 boxes of 128 rows x [hi 32 | lo 32]
+// slots, 128-B rows, SWIZZLE_128B); epilogue chunks of 32 columns staged per warp
+// as a tile box and a mirror box of 32 x 32 fp32 (SWIZZLE_128B).  Variants measured
+// slower on cfg5 and removed: 16-slot boxes in 4 x 32 KB stages, half-k-block
+// ring slots, 16-column chunks, 8 epilogue warps, register-written mirrors, split
+// tile / mirror bulk groups, 2 stages with double-buffered staging.
 constexpr int KB2 = 32;
 static_assert(KB2 == KB, "operand boxes are 2*KB bf16 wide in both kernels");
 constexpr int TILE2_BYTES = BM * KB2 * 2;    // 8 KB
-// CORR2D_SPLIT2 = 2: a ring slot holds half a k-block -- (A_re, Bx) or (A_im, By),
-// 32 KB -- so more, finer slots fit next to the epilogue staging.
-#ifndef CORR2D_SPLIT2
-#define CORR2D_SPLIT2 1
-#endif
-constexpr int SPLIT2 = CORR2D_SPLIT2;
-constexpr int STAGE2_BYTES = 8 * TILE2_BYTES / SPLIT2;
-#ifndef CORR2D_PAIR_MREG
-#define CORR2D_PAIR_MREG 0
-#endif
-#ifndef CORR2D_STAGES2
-#define CORR2D_STAGES2 3
-#endif
-constexpr int STAGES2 = CORR2D_STAGES2;
-#ifndef CORR2D_CH2
-#define CORR2D_CH2 32
-#endif
-#ifndef CORR2D_EPI_WARPS2
-#define CORR2D_EPI_WARPS2 4
-#endif
-constexpr int CH2 = CORR2D_CH2;              // epilogue chunk width (16 or 32 columns)
-static_assert(CH2 == 16 || CH2 == 32, "epilogue chunk");
-constexpr int BOX2 = 32 * CH2 * 4;           // one 32-row box: 4 KB (CH2 32) / 2 KB (CH2 16)
-// mirror from registers: only the direct boxes are staged (8 KB per warp)
-// CORR2D_PAIR_STG1: one staging buffer (tile + mirror box) per warp shared by
-// both planes -- half the staging, each store waits for the previous one's read
-#ifndef CORR2D_PAIR_STG1
-#define CORR2D_PAIR_STG1 1
-#endif
-constexpr int NBUF2 = CORR2D_PAIR_STG1 ? 1 : 2;  // staging buffers per epilogue warp
-constexpr int WSTG2 = (CORR2D_PAIR_MREG ? 1 : 2) * NBUF2 * BOX2;
-constexpr int STG2_BYTES = CORR2D_EPI_WARPS2 * WSTG2;
+constexpr int STAGE2_BYTES = 8 * TILE2_BYTES;
+constexpr int STAGES2 = 3;
+constexpr int CH2 = 32;                      // epilogue chunk width (columns)
+constexpr int BOX2 = 32 * CH2 * 4;           // one 32 x 32 fp32 box: 4 KB
+// one staging buffer (tile box + mirror box) per epilogue warp, shared by both
+// planes: each store waits for the previous one's smem read, but the 32 KB
+// saved buys the third operand stage (measured: 2.67 vs 2.80 ms on cfg5)
+constexpr int WSTG2 = 2 * BOX2;
+constexpr int EPI_WARPS2 = 4;
+constexpr int STG2_BYTES = EPI_WARPS2 * WSTG2;
 constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 2 * BN * 4 + (2 * STAGES2 + 4) * 8 + 16;
 static_assert(SMEM2_BYTES <= 232448, "CTA-pair kernel shared memory");
-// Epilogue warps of the CTA-pair kernels: 4 (each warp both planes of its lane
-// quadrant) or 8 (warps 2-5 sync, 6-9 async).  Measured on cfg5: 4 -> 3.26 ms,
-// 8 -> 3.37 ms; the staging budget is the same 64 KB either way.
-constexpr int EPI_WARPS2 = CORR2D_EPI_WARPS2;
 constexpr int PPW2 = 8 / EPI_WARPS2;         // planes per epilogue warp
 constexpr int THREADS2 = 64 + 32 * EPI_WARPS2;
 
@@ -260,8 +234,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t (&v)[32]) { tmem_ld32(taddr, v); }
-__device__ __forceinline__ void tmem_ld_n(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16(taddr, v); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
@@ -421,9 +393,6 @@ __device__ __forceinline__ void stage_and_store_32(uint8_t* wst, int lane, const
 // One plane of a 32-column chunk (8-warp epilogue of the CTA-pair kernels):
 // tile box and mirror box, 32 x 32 fp32 each, SWIZZLE_128B.
 // PENDING: store groups of this lane that may still be reading OTHER buffers.
-#ifndef CORR2D_SPLIT_GROUPS
-#define CORR2D_SPLIT_GROUPS 0
-#endif
 template <int PENDING>
 __device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane, const float (&v)[32], bool mirror,
                                                          float tsign, const CUtensorMap* map_direct,
@@ -431,39 +400,6 @@ __device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane,
                                                          uint64_t pol) {
   uint8_t* dbox = wst;
   uint8_t* mbox = wst + BOX2;
-  if (CORR2D_SPLIT_GROUPS && PENDING == 0) {
-    // single buffer, tile and mirror boxes in separate bulk groups: staging the
-    // tile box waits only for the previous tile box's read (the previous
-    // mirror box may still be in flight), and vice versa
-    if (lane == 0) bulk_wait_read<1>();
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      *reinterpret_cast<float4*>(dbox + lane * 128 + ((j ^ (lane & 7)) * 16)) =
-          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(map_direct, dbox, cbase, row0q, pol);
-      bulk_commit();
-    }
-    if (!mirror) {
-      if (lane == 0) bulk_commit();  // keep two groups per chunk
-      return;
-    }
-    if (lane == 0) bulk_wait_read<1>();
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      *reinterpret_cast<float*>(mbox + k * 128 + (((lane >> 2) ^ (k & 7)) * 16) + (lane & 3) * 4) = tsign * v[k];
-    fence_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_2d(map_mirror, mbox, row0q, cbase, pol);
-      bulk_commit();
-    }
-    return;
-  }
   if (lane == 0) bulk_wait_read<PENDING>();
   __syncwarp();
 #pragma unroll
@@ -484,114 +420,6 @@ __device__ __forceinline__ void stage_and_store_32_plane(uint8_t* wst, int lane,
   }
 }
 
-// Same chunk, mirror written straight from registers: lane = tile row i holds
-// columns j..j+31, so for each k the warp's 32 values of mirror row j+k are
-// consecutive -- one full 128-B line per store instruction, no staging.
-template <int PENDING>
-__device__ __forceinline__ void stage_and_store_32_plane_mreg(uint8_t* wst, int lane, const float (&v)[32], bool mirror,
-                                                              float tsign, const CUtensorMap* map_direct,
-                                                              float* plane, long long ld_out, int n, int cbase,
-                                                              int row0q, uint64_t pol) {
-  if (lane == 0) bulk_wait_read<PENDING>();
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<float4*>(wst + lane * 128 + ((j ^ (lane & 7)) * 16)) =
-        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  fence_async_smem();
-  __syncwarp();
-  if (lane == 0) {
-    tma_store_2d(map_direct, wst, cbase, row0q, pol);
-    bulk_commit();
-  }
-  if (mirror && row0q + lane < n) {
-    float* dst = plane + (long long)cbase * ld_out + row0q + lane;
-    const int kmax = n - cbase < 32 ? n - cbase : 32;
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      if (k < kmax)
-        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(dst + (long long)k * ld_out),
-                     "f"(tsign * v[k]), "l"(pol) : "memory");
-  }
-}
-
-// 16-column variant: direct box 32 rows x 64 B (SWIZZLE_64B: 16-B chunk j of
-// row l at j ^ ((l >> 1) & 3)) and mirror box 16 rows x 128 B (SWIZZLE_128B).
-template <int PENDING>
-__device__ __forceinline__ void stage_and_store_16_plane(uint8_t* wst, int lane, const float (&v)[16], bool mirror,
-                                                         float tsign, const CUtensorMap* map_direct,
-                                                         const CUtensorMap* map_mirror, int cbase, int row0q,
-                                                         uint64_t pol) {
-  uint8_t* dbox = wst;
-  uint8_t* mbox = wst + 2048;
-  if (lane == 0) bulk_wait_read<PENDING>();
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    *reinterpret_cast<float4*>(dbox + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
-        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  if (mirror) {
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      *reinterpret_cast<float*>(mbox + k * 128 + (((lane >> 2) ^ (k & 7)) * 16) + (lane & 3) * 4) = tsign * v[k];
-  }
-  fence_async_smem();
-  __syncwarp();
-  if (lane == 0) {
-    tma_store_2d(map_direct, dbox, cbase, row0q, pol);
-    if (mirror) tma_store_2d(map_mirror, mbox, row0q, cbase, pol);
-    bulk_commit();
-  }
-}
-
-// overloads by chunk width, so the chunk loop compiles for either CH2
-template <int PENDING>
-__device__ __forceinline__ void stage_and_store_plane(uint8_t* w, int l, const float (&v)[32], bool m, float s,
-                                                      const CUtensorMap* md, const CUtensorMap* mm, int c, int r,
-                                                      uint64_t pol) {
-  stage_and_store_32_plane<PENDING>(w, l, v, m, s, md, mm, c, r, pol);
-}
-template <int PENDING>
-__device__ __forceinline__ void stage_and_store_plane(uint8_t* w, int l, const float (&v)[16], bool m, float s,
-                                                      const CUtensorMap* md, const CUtensorMap* mm, int c, int r,
-                                                      uint64_t pol) {
-  stage_and_store_16_plane<PENDING>(w, l, v, m, s, md, mm, c, r, pol);
-}
-template <int PENDING>
-__device__ __forceinline__ void stage_and_store_mreg(uint8_t* w, int l, const float (&v)[32], bool m, float s,
-                                                     const CUtensorMap* md, float* pl, long long ld, int n, int c,
-                                                     int r, uint64_t pol) {
-  stage_and_store_32_plane_mreg<PENDING>(w, l, v, m, s, md, pl, ld, n, c, r, pol);
-}
-template <int PENDING>
-__device__ __forceinline__ void stage_and_store_mreg(uint8_t* wst, int lane, const float (&v)[16], bool mirror,
-                                                     float tsign, const CUtensorMap* map_direct, float* plane,
-                                                     long long ld_out, int n, int cbase, int row0q, uint64_t pol) {
-  // 16-column chunk: direct box 32 rows x 64 B (SWIZZLE_64B) by TMA, mirror rows
-  // straight from registers (one 128-B line per store instruction)
-  if (lane == 0) bulk_wait_read<PENDING>();
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-    *reinterpret_cast<float4*>(wst + lane * 64 + ((j ^ ((lane >> 1) & 3)) * 16)) =
-        make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  fence_async_smem();
-  __syncwarp();
-  if (lane == 0) {
-    tma_store_2d(map_direct, wst, cbase, row0q, pol);
-    bulk_commit();
-  }
-  if (mirror && row0q + lane < n) {
-    float* dst = plane + (long long)cbase * ld_out + row0q + lane;
-    const int kmax = n - cbase < 16 ? n - cbase : 16;
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < kmax)
-        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;\n" ::"l"(dst + (long long)k * ld_out),
-                     "f"(tsign * v[k]), "l"(pol) : "memory");
-  }
-}
-
 __device__ __forceinline__ void epi_bar256() { asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS2) : "memory"); }
 
 // sync chunk c -> u[0..15], async chunk c -> u[16..31]
@@ -609,12 +437,6 @@ __device__ __forceinline__ void tmem_wait_ld_tie(uint32_t (&u)[32]) {
                  "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15]),
                  "+r"(u[16]), "+r"(u[17]), "+r"(u[18]), "+r"(u[19]), "+r"(u[20]), "+r"(u[21]), "+r"(u[22]), "+r"(u[23]),
                  "+r"(u[24]), "+r"(u[25]), "+r"(u[26]), "+r"(u[27]), "+r"(u[28]), "+r"(u[29]), "+r"(u[30]), "+r"(u[31])
-               :: "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld_tie(uint32_t (&u)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]), "+r"(u[7]),
-                 "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]), "+r"(u[14]), "+r"(u[15])
                :: "memory");
 }
 
@@ -874,7 +696,6 @@ struct Params2 {
   int n1, n2, hp, homo, even, tma_store;
   int store_pol;          // L2 policy of the output stores: 0 evict_first, 1 normal, 2 evict_last
   int dbg;                // profiling switches: 1 = no output stores, 2 = no MMAs (results invalid)
-  int mirror_reg;         // mirror tiles stored from registers (coalesced st.global) instead of TMA
   long long* trace;       // profiling (CORR2D_TRACE=1): per-CTA stall cycles, 8 counters each
   int T1, T2;            // 128-row / 128-col tile counts
   long long tile0, tile1; // pair-tile range
@@ -1249,8 +1070,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         // NPAIR == 2: the first pair's CTAs load A for both pairs (multicast)
         const bool load_a = (NPAIR == 1) || rank < 2;
         const uint16_t a_mask = (uint16_t)((1u << rank) | (1u << (rank + 2)));
-        for (int h = 0; h < nkb * SPLIT2; ++h) {
-          const int kb = h / SPLIT2, part = h % SPLIT2;
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_t(&empty[stage], phase ^ 1, tr ? &tr_wait : nullptr);
           const uint32_t lbar = mapa_rank(su32(&full[stage]), lrank);
           if (p.dbg & 4) {            // profiling: no operand traffic at all
@@ -1262,20 +1082,15 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
           uint8_t* base = stages + stage * STAGE_BYTES;
           const int k0 = kb * 2 * KB;
           // each box: 128 rows x [hi KB | lo KB] slots (128-B rows, SWIZZLE_128B)
-          if (SPLIT2 == 2) {
-            tma_load_3d_2sm(base, &tmap_a, part * 2 * p.hp + k0, arow, 0, lbar, keep);
-            tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_b, (part ? ky : kx) + k0, brow, 0, lbar, keep);
-          } else if (NPAIR == 1) {
+          if (NPAIR == 1) {
             tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
             tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, 2 * p.hp + k0, arow, 0, lbar, keep);
           } else if (load_a) {
             tma_load_3d_2sm_mc(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, su32(&full[stage]), a_mask, keep);
             tma_load_3d_2sm_mc(base + 2 * TILE_BYTES, &tmap_a, 2 * p.hp + k0, arow, 0, su32(&full[stage]), a_mask, keep);
           }
-          if (SPLIT2 == 1) {
-            tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, kx + k0, brow, 0, lbar, keep);
-            tma_load_3d_2sm(base + 6 * TILE_BYTES, &tmap_b, ky + k0, brow, 0, lbar, keep);
-          }
+          tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, kx + k0, brow, 0, lbar, keep);
+          tma_load_3d_2sm(base + 6 * TILE_BYTES, &tmap_b, ky + k0, brow, 0, lbar, keep);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -1292,25 +1107,10 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         mbar_wait_t(&tempty[acc], acc_phase ^ 1, tr ? &tr_wait2 : nullptr);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * 256;
-        for (int h = 0; h < nkb * SPLIT2; ++h) {
-          const int kb = h;  // (SPLIT2 == 2: half k-block index)
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_t(&full[stage], phase, tr ? &tr_wait : nullptr);
           tc_fence_after();
-          if (lane == 0 && SPLIT2 == 2) {
-            const uint32_t base = su32(stages + stage * STAGE_BYTES);
-#pragma unroll
-            for (int ks = 0; ks < KB / 16; ++ks) {
-              const uint32_t off = ks * 32;
-              const uint64_t a_h = desc_sw128(base + off), a_l = desc_sw128(base + 64 + off);
-              const uint64_t b_h = desc_sw128(base + 2 * TILE_BYTES + off), b_l = desc_sw128(base + 2 * TILE_BYTES + 64 + off);
-              if (p.dbg & 2) continue;
-              umma2_bf16(d, a_h, b_h, ID, (h | ks) ? 1u : 0u);
-              umma2_bf16(d, a_h, b_l, ID, 1);
-              umma2_bf16(d, a_l, b_h, ID, 1);
-            }
-            umma2_commit_mask(&empty[stage], all_mask);
-            if (h == nkb * SPLIT2 - 1) umma2_commit_mask(&tfull[acc], pair_mask);
-          } else if (lane == 0) {
+          if (lane == 0) {
             const uint32_t base = su32(stages + stage * STAGE_BYTES);
 #pragma unroll
             for (int ks = 0; ks < KB / 16; ++ks) {
@@ -1410,25 +1210,21 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         tc_fence_after();
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * 256;
         if (use_tma) {
-          // 32-column chunks of this warp's plane: TMEM -> registers ->
+          // 32-column chunks of both planes (alternating): TMEM -> registers ->
           // correction / reduction -> two 32 x 32 boxes (tile + mirror, 128-B
-          // rows) -> TMA stores.  Planes alternate inside the chunk loop, so
-          // with one buffer per plane the group that last read this buffer is
-          // PPW2 - 1 commits back (that is what the wait allows in flight).
+          // rows) in the warp's one staging buffer -> TMA stores; each chunk
+          // waits for the previous chunk's boxes to have been read.
           const bool mir = mode != kPlain;
 #pragma unroll 1
           for (int c = 0; c < BN / CH2; ++c) {
 #pragma unroll 1
             for (int plane = pw; plane < pw + PPW2; ++plane) {
-              // buffers alternate between the planes (4 epilogue warps) or the
-              // chunks (8 warps, one plane each)
-              const int bsel = NBUF2 == 1 ? 0 : (PPW2 == 1 ? (c & 1) : (plane - pw));
-              uint8_t* wst = staging + (warp - 2) * WSTG2 + bsel * (WSTG2 / NBUF2);
+              uint8_t* wst = staging + (warp - 2) * WSTG2;
               const float tsign = plane == 0 ? 1.f : -1.f;
               float mx = 0.f;
               uint32_t ua[CH2];
               const long long tq0 = tr ? clock64() : 0;
-              tmem_ld_n(tbase + plane * 128 + c * CH2, ua);
+              tmem_ld32(tbase + plane * 128 + c * CH2, ua);
               tmem_wait_ld_tie(ua);
               if (tr) tr_wait2 += clock64() - tq0;
               float v[CH2];
@@ -1460,15 +1256,9 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
                 else mx = __uint_as_float(mb[0]);
               }
               const long long ts0 = tr ? clock64() : 0;
-              if (p.dbg & 1) {
-              } else if (p.mirror_reg) {
-                stage_and_store_mreg<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0],
-                                                plane == 0 ? p.phi : p.psi, p.ld_out, p.n1,
-                                                j0 + c * CH2, i0 + 32 * q, drop);
-              } else {
-                stage_and_store_plane<NBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
-                                                 j0 + c * CH2, i0 + 32 * q, drop);
-              }
+              if (!(p.dbg & 1))
+                stage_and_store_32_plane<0>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
+                                            j0 + c * CH2, i0 + 32 * q, drop);
               if (tr) tr_store += clock64() - ts0;
               if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
             }
@@ -1595,16 +1385,13 @@ static int make_operand_map(CUtensorMap* map, const void* base, long long ld, lo
 // kind 0 = 1-SM direct 16 x 32 (SWIZZLE_64B), 1 = 1-SM mirror 32 x 16 (no
 // swizzle), 2 = CTA-pair 32 x 32 boxes (SWIZZLE_128B) for tile and mirror.
 static int make_output_map(CUtensorMap* map, float* base, long long ld, long long rows, long long cols, int kind) {
-  // kind 3 / 4: CTA-pair kernels with 16-column chunks -- direct 16 x 32
-  // (SWIZZLE_64B), mirror 32 x 16 (SWIZZLE_128B)
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)CH : (kind == 3 ? 16u : 32u),
-                       kind == 1 ? (cuuint32_t)CH : (kind == 4 ? 16u : 32u)};
+  cuuint32_t box[2] = {kind == 0 ? (cuuint32_t)CH : 32u, kind == 1 ? (cuuint32_t)CH : 32u};
   cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapSwizzle sw = (kind == 0 || kind == 3) ? CU_TENSOR_MAP_SWIZZLE_64B
+  const CUtensorMapSwizzle sw = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_64B
                               : (kind == 1 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1699,7 +1486,7 @@ extern "C" int corr2d_contract_bf16x3(
     float* planes[2] = {phi, psi};
     for (int pl = 0; pl < 2 && !rc; ++pl)
       for (int mi = 0; mi < 2 && !rc; ++mi)
-        rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, pair_kernel ? (CH2 == 32 ? 2 : 3 + mi) : mi);
+        rc = make_output_map(&om.m[pl][mi], planes[pl], ld_out, rows, n2, pair_kernel ? 2 : mi);
     if (rc) return rc;
   }
   int dev = 0, sms = 148;
@@ -1722,8 +1509,6 @@ extern "C" int corr2d_contract_bf16x3(
     p.store_pol = sp ? atoi(sp) : 0;
     const char* dbg = getenv("CORR2D_DEBUG_SKIP");
     p.dbg = dbg ? atoi(dbg) : 0;
-    const char* mreg = getenv("CORR2D_MIRROR_REG");
-    p.mirror_reg = CORR2D_PAIR_MREG ? 1 : (mreg ? atoi(mreg) : 0);
     static long long* trace_buf = nullptr;
     const char* trc = getenv("CORR2D_TRACE");
     if (trc && trc[0] == '1') {
