@@ -18,6 +18,7 @@
 #include "common.cuh"
 
 #include <cmath>
+#include <cstdlib>
 
 namespace corr2d {
 
@@ -93,6 +94,63 @@ __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int
   } else {
     J = I + (int)(o - p.I0);
     mode = (J == I) ? kDiag : (J < p.I1 ? kMirror : kPlain);
+  }
+}
+
+// Both planes of a staged 64 x 64 tile (row pitch kCS) -> global memory as
+// coalesced 256-B row segments, plus the mirrored tile (sync^T, -async^T) of
+// homo tiles above the diagonal; fused max|.| / finite check into p.stats.
+__device__ __forceinline__ void write_tile(const ContractParams& p, int mode, int i0, int j0,
+                                           const double* Cphi, const double* Cpsi, int tid, int nthreads,
+                                           int lane) {
+  double mphi = 0.0, mpsi = 0.0;
+  int bad = 0;
+  for (int idx = tid; idx < kBM * kBN; idx += nthreads) {
+    if (mode == kTransOnly) break;
+    const int r = idx >> 6, c = idx & 63;
+    const int gi = i0 + r, gj = j0 + c;
+    if (gi >= p.row1 || gj >= p.n2) continue;
+    double vphi, vpsi;
+    if (mode == kDiag) {
+      if (r <= c) { vphi = Cphi[r * kCS + c]; } else { vphi = Cphi[c * kCS + r]; }
+      if (r < c) vpsi = Cpsi[r * kCS + c];
+      else if (r == c) vpsi = 0.0;
+      else vpsi = -Cpsi[c * kCS + r];
+    } else {
+      vphi = Cphi[r * kCS + c];
+      vpsi = Cpsi[r * kCS + c];
+    }
+    const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
+    __stcs(p.phi + o, vphi);
+    __stcs(p.psi + o, vpsi);
+    mphi = fmax(mphi, fabs(vphi));
+    mpsi = fmax(mpsi, fabs(vpsi));
+    bad += !(isfinite(vphi) && isfinite(vpsi));
+  }
+  if (mode == kMirror || mode == kTransOnly) {
+    // out[j][i] = sync[i][j], -async[i][j] for the tile below the diagonal
+    for (int idx = tid; idx < kBM * kBN; idx += nthreads) {
+      const int rr = idx >> 6, cc = idx & 63;   // rr: column of C, cc: row of C
+      const int gi = j0 + rr, gj = i0 + cc;
+      if (gi >= p.row1 || gj >= p.n2 || gi < p.row0) continue;
+      const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
+      const double vphi = Cphi[cc * kCS + rr], vpsi = -Cpsi[cc * kCS + rr];
+      __stcs(p.phi + o, vphi);
+      __stcs(p.psi + o, vpsi);
+      if (mode == kTransOnly) {
+        mphi = fmax(mphi, fabs(vphi));
+        mpsi = fmax(mpsi, fabs(vpsi));
+        bad += !(isfinite(vphi) && isfinite(vpsi));
+      }
+    }
+  }
+  mphi = warp_max(mphi);
+  mpsi = warp_max(mpsi);
+  bad = warp_sum(bad);
+  if (lane == 0) {
+    atomic_max_abs(&p.stats[0], mphi);
+    atomic_max_abs(&p.stats[1], mpsi);
+    if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
   }
 }
 
@@ -177,55 +235,7 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
     }
   __syncthreads();
 
-  double mphi = 0.0, mpsi = 0.0;
-  int bad = 0;
-  for (int idx = tid; idx < kBM * kBN; idx += kThreads) {
-    if (mode == kTransOnly) break;
-    const int r = idx >> 6, c = idx & 63;
-    const int gi = i0 + r, gj = j0 + c;
-    if (gi >= p.row1 || gj >= p.n2) continue;
-    double vphi, vpsi;
-    if (mode == kDiag) {
-      if (r <= c) { vphi = Cphi[r * kCS + c]; } else { vphi = Cphi[c * kCS + r]; }
-      if (r < c) vpsi = Cpsi[r * kCS + c];
-      else if (r == c) vpsi = 0.0;
-      else vpsi = -Cpsi[c * kCS + r];
-    } else {
-      vphi = Cphi[r * kCS + c];
-      vpsi = Cpsi[r * kCS + c];
-    }
-    const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
-    __stcs(p.phi + o, vphi);
-    __stcs(p.psi + o, vpsi);
-    mphi = fmax(mphi, fabs(vphi));
-    mpsi = fmax(mpsi, fabs(vpsi));
-    bad += !(isfinite(vphi) && isfinite(vpsi));
-  }
-  if (mode == kMirror || mode == kTransOnly) {
-    // out[j][i] = sync[i][j], -async[i][j] for the tile below the diagonal
-    for (int idx = tid; idx < kBM * kBN; idx += kThreads) {
-      const int rr = idx >> 6, cc = idx & 63;   // rr: column of C, cc: row of C
-      const int gi = j0 + rr, gj = i0 + cc;
-      if (gi >= p.row1 || gj >= p.n2 || gi < p.row0) continue;
-      const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
-      const double vphi = Cphi[cc * kCS + rr], vpsi = -Cpsi[cc * kCS + rr];
-      __stcs(p.phi + o, vphi);
-      __stcs(p.psi + o, vpsi);
-      if (mode == kTransOnly) {
-        mphi = fmax(mphi, fabs(vphi));
-        mpsi = fmax(mpsi, fabs(vpsi));
-        bad += !(isfinite(vphi) && isfinite(vpsi));
-      }
-    }
-  }
-  mphi = warp_max(mphi);
-  mpsi = warp_max(mpsi);
-  bad = warp_sum(bad);
-  if (lane == 0) {
-    atomic_max_abs(&p.stats[0], mphi);
-    atomic_max_abs(&p.stats[1], mpsi);
-    if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
-  }
+  write_tile(p, mode, i0, j0, Cphi, Cpsi, tid, kThreads, lane);
 }
 
 }  // namespace corr2d
@@ -262,11 +272,11 @@ extern "C" int corr2d_contract_f64(
   p.tile0 = tile0;
   tiles = tile1 - tile0;
   if (tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_contract_f64: tile count out of range");
-  const size_t smem = 3 * (size_t)kBM * kKS * sizeof(double);
-  cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
   if (tiles == 0) return CORR2D_OK;
+  const size_t smem = 3 * (size_t)kBM * kKS * sizeof(double);
+  cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   contract_f64_kernel<<<(unsigned)tiles, kThreads, smem, st>>>(p);
   return check_launch("contract_f64_kernel");
 }
