@@ -267,71 +267,79 @@ def run_b200(args, case, wl, world, rank, local):
     plan.check(axes=(ds1.spectral_axis, (ds2 or ds1).spectral_axis))
     parity = parity_gate(case, plan, world) if rank == 0 and world == 1 else None
 
-    # ---- the step as a CUDA graph (K1 + K2 launches, no host work in the loop);
-    #      a second graph with K2 alone times the contraction kernel
-    step_graph, k2_graph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    # ---- CUDA graphs: one step (K1, with the spectra all-gather for N > 1,
+    #      then K2) for warm-up / load, and the whole timed region unrolled into
+    #      one graph: K steps, each bracketed by event-record nodes (start, K1|K2
+    #      boundary, end) so per-step times and the contraction kernel's own
+    #      duration are measured live inside the timed steps, back to back;
+    #      maps that fit in L2 get a 256 MB write between steps, outside the
+    #      step's events, so every timed step starts from a cold L2.
+    flush = wl["out_bytes"] + wl["in_bytes"] <= 4 * 126e6
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    step_graph, timed_graph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+    evs = [tuple(torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)) for _ in range(args.steps)]
     cap = torch.cuda.Stream(device=dev)
     cap.wait_stream(stream)
     with torch.cuda.stream(cap):
         plan.launch()                     # settle allocator / attributes before capture
         with torch.cuda.graph(step_graph, stream=cap):
             plan.launch()
-        with torch.cuda.graph(k2_graph, stream=cap):
-            plan.launch_contract()
+        with torch.cuda.graph(timed_graph, stream=cap):
+            for a, mid, b in evs:
+                if flush:
+                    flush_buf.fill_(1)
+                a.record(cap)
+                plan.launch_prep_only()
+                mid.record(cap)
+                plan.launch_contract()
+                b.record(cap)
     stream.wait_stream(cap)
     torch.cuda.synchronize()
 
-    with ClockSampler(local) as clocks:
-        # ---- warmup (W steps), then keep the GPU under the same load for
-        #      ~0.3 s so the clock sampler sees the steady state around the timed region
-        for _ in range(args.warmup):
-            step_graph.replay()
-        torch.cuda.synchronize()
-        t_load = time.time()
-        while time.time() - t_load < 0.3:
-            step_graph.replay()
-            torch.cuda.synchronize()
+    def step():
+        step_graph.replay()
 
-        # ---- timed region: exactly K steps, device time, barrier + sync on both sides.
-        #      Per-step events give median / best; maps that fit in L2 get a
-        #      256 MB write between steps, outside the step's event pair, so
-        #      every timed step starts from a cold L2.
-        flush = wl["out_bytes"] + wl["in_bytes"] <= 4 * 126e6
-        flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        barrier(world)
-        torch.cuda.synchronize()
-        for a, b in evs:
-            if flush:
-                flush_buf.fill_(1)
-            a.record(stream)
-            step_graph.replay()
-            b.record(stream)
-        torch.cuda.synchronize()
-        barrier(world)
-        per_step = [a.elapsed_time(b) for a, b in evs]
-        if os.environ.get("BENCH_DUMP_STEPS"):
-            print("per-step ms:", [round(x, 4) for x in per_step], file=sys.stderr)
-        ms = sum(per_step)
-
-        # ---- contraction kernel alone, K launches on the same stream (L2 flushed
-        #      between them, outside the event pairs, when the map fits in L2)
-        kevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for a, b in kevs:
-            if flush:
-                flush_buf.fill_(1)
-            a.record(stream)
-            k2_graph.replay()
-            b.record(stream)
-        torch.cuda.synchronize()
-        t_load = time.time()
-        while time.time() - t_load < 0.3:
-            step_graph.replay()
+    def measure():
+        with ClockSampler(local) as clocks:
+            # ---- warmup (W steps), then keep the GPU under the same load for
+            #      ~0.3 s so the clock sampler sees the steady state around the timed region
+            for _ in range(args.warmup):
+                step()
             torch.cuda.synchronize()
+            t_load = time.time()
+            while time.time() - t_load < 0.3:
+                step()
+                torch.cuda.synchronize()
+
+            # ---- timed region: exactly K steps (one graph replay), device time,
+            #      barrier + sync on both sides
+            barrier(world)
+            torch.cuda.synchronize()
+            timed_graph.replay()
+            torch.cuda.synchronize()
+            barrier(world)
+            per_step = [a.elapsed_time(b) for a, _, b in evs]
+            per_k2 = [mid.elapsed_time(b) for _, mid, b in evs]
+            if os.environ.get("BENCH_DUMP_STEPS"):
+                print("per-step ms:", [round(x, 4) for x in per_step], file=sys.stderr)
+            t_load = time.time()
+            while time.time() - t_load < 0.3:
+                step()
+                torch.cuda.synchronize()
+        return per_step, per_k2, clocks.summary()
+
+    # a run that saw thermal / hardware slowdown is re-measured once (all ranks
+    # together); sw_power_cap is kept and reported
+    per_step, per_k2, clock_summary = measure()
+    slow = sorted({"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(clock_summary["reasons"]))
+    if allreduce_max(1.0 if slow else 0.0, world) > 0:
+        per_step, per_k2, clock_summary = measure()
+        clock_summary["remeasured_after"] = slow or ["slowdown on another rank"]
+    ms = sum(per_step)
     ms_max = allreduce_max(ms, world)
     step_median = allreduce_max(statistics.median(per_step), world)
     step_best = allreduce_max(min(per_step), world)
-    k2_avg = allreduce_max(sum(a.elapsed_time(b) for a, b in kevs) / args.steps, world)
+    k2_avg = allreduce_max(sum(per_k2) / args.steps, world)
 
     # ---- e2e through the public API: pinned host inputs -> planes in pinned host memory
     e2e = run_e2e(args, case, ds1, ds2, world, rank, dev) if world == 1 else None
@@ -373,7 +381,7 @@ def run_b200(args, case, wl, world, rank, local):
                      "hbm_floor_ms": (wl["out_bytes"] + wl["in_bytes"]) / (peaks["hbm_gbs"] * 1e9) * 1e3,
                      "peak_source": peaks["_source"] + (" (bf16 sustained; burst in peak_burst)" if case.dtype == "float32"
                                                         else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
-        "clocks": clocks.summary(),
+        "clocks": clock_summary,
         "gpu_launches": plan.launches_per_step * args.steps,
         "parity": parity,
     }
