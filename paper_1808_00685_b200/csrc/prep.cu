@@ -840,18 +840,28 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
       for (int e = 0; e < 2; ++e) {
         uint8_t* rb = work + (size_t)(2 * warp + e) * img;
         __align__(16) __nv_bfloat16 re_h[R], re_l[R], im_h[R], im_l[R], ng_h[R], ng_l[R];
+        // two adjacent bins per conversion instruction (F2FP pack)
 #pragma unroll
-        for (int k1 = 0; k1 < R; ++k1) {
-          const C2 y = e ? yo[k1] : ye[k1];
-          const int q = q0 + k1;
-          const float vr = (float)y.x * (q == 0 ? sn1 : sn2);
-          const float vi = q == 0 ? (e ? nyq1 : nyq0) * sn1 : (float)y.y * sn2;
-          re_h[k1] = __float2bfloat16_rn(vr);
-          re_l[k1] = __float2bfloat16_rn(vr - __bfloat162float(re_h[k1]));
-          im_h[k1] = __float2bfloat16_rn(vi);
-          im_l[k1] = __float2bfloat16_rn(vi - __bfloat162float(im_h[k1]));
-          ng_h[k1] = __hneg(im_h[k1]);
-          ng_l[k1] = __hneg(im_l[k1]);
+        for (int k1 = 0; k1 < R; k1 += 2) {
+          float vr[2], vi[2];
+#pragma unroll
+          for (int d = 0; d < 2; ++d) {
+            const C2 y = e ? yo[k1 + d] : ye[k1 + d];
+            const int q = q0 + k1 + d;
+            vr[d] = (float)y.x * (q == 0 ? sn1 : sn2);
+            vi[d] = q == 0 ? (e ? nyq1 : nyq0) * sn1 : (float)y.y * sn2;
+          }
+          const __nv_bfloat162 rh = __floats2bfloat162_rn(vr[0], vr[1]);
+          const __nv_bfloat162 ih = __floats2bfloat162_rn(vi[0], vi[1]);
+          const float2 rhf = __bfloat1622float2(rh), ihf = __bfloat1622float2(ih);
+          const __nv_bfloat162 rl = __floats2bfloat162_rn(vr[0] - rhf.x, vr[1] - rhf.y);
+          const __nv_bfloat162 il = __floats2bfloat162_rn(vi[0] - ihf.x, vi[1] - ihf.y);
+          *reinterpret_cast<__nv_bfloat162*>(&re_h[k1]) = rh;
+          *reinterpret_cast<__nv_bfloat162*>(&re_l[k1]) = rl;
+          *reinterpret_cast<__nv_bfloat162*>(&im_h[k1]) = ih;
+          *reinterpret_cast<__nv_bfloat162*>(&im_l[k1]) = il;
+          *reinterpret_cast<__nv_bfloat162*>(&ng_h[k1]) = __hneg2(ih);
+          *reinterpret_cast<__nv_bfloat162*>(&ng_l[k1]) = __hneg2(il);
         }
         const int o = ((q0 >> 5) * 64 + (q0 & 31)) * 2;    // byte offset of bin q0 in a third
         auto put = [&](int off, const __nv_bfloat16 (&v)[R]) {
