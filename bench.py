@@ -378,6 +378,7 @@ def run_b200(args, case, wl, world, rank, local):
                      "kernel_ms": k2_avg,
                      "algorithmic": ("output + input bytes" if bound == "hbm" else "8*K flops per complex output element"),
                      "t_roof_ms": max(t_hbm, t_tc) * 1e3,
+                     "executed": executed_flops(plan, case, tc_peak, k2_avg),
                      "hbm_floor_ms": (wl["out_bytes"] + wl["in_bytes"]) / (peaks["hbm_gbs"] * 1e9) * 1e3,
                      "peak_source": peaks["_source"] + (" (bf16 sustained; burst in peak_burst)" if case.dtype == "float32"
                                                         else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
@@ -458,6 +459,23 @@ def cpu_baseline_line(case, wl):
     return {"value": rows * wl["n2"] / dt / 1e9, "unit": "GElem/s", "cores": threads, "kind": "port",
             "sample": f"rows 0..{rows} of the {wl['n1']}x{wl['n2']} map ({dt:.1f} s; preprocess + rfft + "
                       f"row-block zgemm via the oracle restatement of corrtwo 0.1.0)"}
+
+
+def executed_flops(plan, case, tc_peak, k2_ms):
+    """Tensor-pipe flops K2 actually issues (not the algorithmic 8K per element):
+    bf16x3 = 3 products x (x, y) MMAs of M=256, N=256 over the packed depth per
+    CTA-pair tile, homo triangle only; fp64 = both planes of every 64 x 64 tile
+    over the packed depth.  Rate vs the same measured peak shows how busy the
+    tensor pipe is, independent of the split / symmetry factors."""
+    tiles = plan.tile_count()
+    if case.dtype == "float32":
+        hp = plan.mp // 3
+        per_tile = 3 * 2 * 2 * 256 * 256 * hp              # 3 products, x + y MMAs, 2 flops/MAC, depth hp
+    else:
+        per_tile = 2 * 2 * 64 * 64 * plan.mp                # two planes, 2 flops/MAC
+    f = float(tiles) * per_tile
+    return {"flops": f, "tflops": f / (k2_ms * 1e-3) / 1e12, "frac_of_peak": f / (k2_ms * 1e-3) / 1e12 / tc_peak,
+            "per_element_vs_algorithmic": f / (case.n1 * case.n2 * 8.0 * (case.m // 2 + 1))}
 
 
 def contract_kernel_name(case):

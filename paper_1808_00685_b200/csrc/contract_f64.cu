@@ -24,10 +24,25 @@ namespace corr2d {
 
 constexpr int kBM = 64;
 constexpr int kBN = 64;
-constexpr int kKC = 64;            // depth chunk
+// depth chunk 32 + at least 3 CTAs / SM: the DMMA accumulate chains are
+// latency-bound (ncu: "wait" stalls), so resident warps matter more than
+// depth per chunk -- measured cfg3 1.91 -> 1.61 ms, cfg4 0.51 -> 0.42 ms
+#ifndef CORR2D_F64_KC
+#define CORR2D_F64_KC 32
+#endif
+#ifndef CORR2D_F64_MINB
+#define CORR2D_F64_MINB 3
+#endif
+constexpr int kKC = CORR2D_F64_KC; // depth chunk
 constexpr int kKS = kKC + 4;       // smem row stride (doubles): conflict-free fragments
 constexpr int kCS = kBN + 1;       // epilogue staging stride
-constexpr int kThreads = 128;
+// MT m16 row tiles per warp: 2 -> 4 warps of 32 x 32 (128 threads); 1 -> 8 warps
+// of 16 x 32 (256 threads, half the accumulator registers per thread)
+#ifndef CORR2D_F64_MT
+#define CORR2D_F64_MT 2
+#endif
+constexpr int kMT = CORR2D_F64_MT;
+constexpr int kThreads = 32 * 2 * (64 / (16 * kMT));
 
 // kTransOnly: a tile left of the shard's diagonal square is computed as its
 // globally-upper mirror (operand tiles swapped) and only the transpose is
@@ -154,7 +169,7 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const ContractParams p) {
+__global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel(const ContractParams p) {
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                     // [kBM][kKS]  A_phi
   double* Ps = As + kBM * kKS;         // [kBM][kKS]  A_psi
@@ -164,12 +179,12 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
   decode_tile(p, I, J, mode);
   const int i0 = I * kBM, j0 = J * kBN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp >> 1, wn = warp & 1;   // rows wm * 16 MT .., columns wn * 32 ..
   const int lr = lane >> 2, lk = lane & 3;
 
-  double acc_phi[2][4][4], acc_psi[2][4][4];
+  double acc_phi[kMT][4][4], acc_psi[kMT][4][4];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < kMT; ++a)
 #pragma unroll
     for (int bq = 0; bq < 4; ++bq)
 #pragma unroll
@@ -195,8 +210,8 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
     for (int kk = 0; kk < kc; kk += 4) {
       double ap[2][2], as[2][2], bf[4];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-        const int r = wm * 32 + mt * 16 + lr;
+      for (int mt = 0; mt < kMT; ++mt) {
+        const int r = wm * 16 * kMT + mt * 16 + lr;
         ap[mt][0] = As[r * kKS + kk + lk];
         ap[mt][1] = As[(r + 8) * kKS + kk + lk];
         as[mt][0] = Ps[r * kKS + kk + lk];
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           dmma_16x8x4(acc_phi[mt][nt], ap[mt][0], ap[mt][1], bf[nt]);
@@ -219,10 +234,10 @@ __global__ void __launch_bounds__(kThreads, 2) contract_f64_kernel(const Contrac
   double* Cphi = sm;                   // [kBM][kCS]
   double* Cpsi = sm + kBM * kCS;       // [kBM][kCS]
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
-      const int r = wm * 32 + mt * 16 + lr;
+      const int r = wm * 16 * kMT + mt * 16 + lr;
       const int c = wn * 32 + nt * 8 + 2 * lk;
       Cphi[r * kCS + c] = acc_phi[mt][nt][0];
       Cphi[r * kCS + c + 1] = acc_phi[mt][nt][1];
@@ -275,7 +290,9 @@ extern "C" int corr2d_contract_f64(
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
   if (tiles == 0) return CORR2D_OK;
-  const size_t smem = 3 * (size_t)kBM * kKS * sizeof(double);
+  const size_t smem_ops = 3 * (size_t)kBM * kKS * sizeof(double);
+  const size_t smem_epi = 2 * (size_t)kBM * kCS * sizeof(double);
+  const size_t smem = smem_ops > smem_epi ? smem_ops : smem_epi;
   cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   contract_f64_kernel<<<(unsigned)tiles, kThreads, smem, st>>>(p);
   return check_launch("contract_f64_kernel");
