@@ -259,3 +259,41 @@ def test_fp32_tile_ranges_and_both_tensor_core_kernels(monkeypatch):
         engine.sync()
         assert np.array_equal(plan.phi.cpu().numpy(), full.sync)
         assert np.array_equal(plan.psi.cpu().numpy(), full.asyn)
+
+
+@pytest.mark.parametrize("n1,n2,m", [(300, 257, 64), (129, 1000, 37), (700, 65, 512), (5, 3, 2), (1025, 511, 21)])
+def test_fp32_hetero_ragged(n1, n2, m):
+    """bf16x3 path, hetero: CTA-pair kernel for aligned planes, the register-store
+    epilogue for n2 % 4 != 0, odd / even m, tiny and ragged shapes."""
+    rng = np.random.default_rng(n1 * 7 + n2 * 13 + m)
+    v1 = rng.normal(size=(m, n1))
+    v2 = rng.normal(size=(m, n2))
+    d1 = P.DynamicSpectra(np.arange(n1, dtype=float), np.arange(m, dtype=float), v1, np.zeros(n1))
+    d2 = P.DynamicSpectra(np.arange(n2, dtype=float) + .5, np.arange(m, dtype=float), v2, np.zeros(n2))
+    res = P.correlate_ft(d1, d2, dtype="float32")
+    s, a, _ = O.correlate_ft(v1, v2)
+    sc = scale_of(s, a)
+    assert res.sync.shape == (n1, n2)
+    assert rel_err(res.sync, s, sc) <= TOL32 and rel_err(res.asyn, a, sc) <= TOL32
+
+
+def test_fp32_row_shards_match_whole_map():
+    """Row shards (the 1-SM kernel with transpose-only tiles) reproduce the
+    whole fp32 map bit for bit."""
+    from paper_1808_00685_b200.engine_core import tile_aligned_blocks
+    v = np.random.default_rng(8).normal(size=(96, 600))
+    d = dyn_from_values(v)
+    full = P.correlate_ft(d, dtype="float32", return_device=True)
+    whole1 = None
+    import os
+    os.environ["CORR2D_BF16_1SM"] = "1"
+    try:
+        whole1 = P.correlate_ft(d, dtype="float32").sync
+        for r0, r1 in tile_aligned_blocks(600, 3, 128):
+            sh = P.correlate_ft(d, dtype="float32", rows=(r0, r1), return_device=True)
+            assert np.array_equal(sh.sync.cpu().numpy(), whole1[r0:r1])
+    finally:
+        del os.environ["CORR2D_BF16_1SM"]
+    s, a, _ = O.correlate_ft(v)
+    sc = scale_of(s, a)
+    assert rel_err(full.sync.cpu().numpy(), s, sc) <= TOL32 and rel_err(whole1, s, sc) <= TOL32
