@@ -100,11 +100,30 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
     spec = PreprocessSpec(reference=_reference_spec(reference),
                           resample=None if resample is None else ResampleSpec(int(resample), kind),
                           scaling_exponent=float(alpha))
+    homo = ds2 is None or ds2 is ds1 or ds1.equals(ds2)
+    dsb = ds1 if homo else ds2
+    blocks = None
+    if not return_device:
+        _, dev = _engine_mod.require_device(device)
+        odt = np.dtype(dtype)
+        blocks = _engine_mod.stream_blocks(ds1.n, dsb.n, odt.itemsize, _engine_mod.device_budget(dev))
+        if blocks is not None:        # planes larger than device memory: stream row blocks
+            def make_plan(rws):
+                return build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance, dtype=dtype,
+                                  device=device, engine_name=engine, rows=rws)[0]
+            s, a, info, first = _engine_mod.run_streamed(
+                make_plan, ds1.n, dsb.n, odt, blocks, out,
+                check=lambda pl: pl.check(axes=(ds1.spectral_axis, dsb.spectral_axis), labels=("first", "second")))
+            constant = _norm_spec(norm, engine).constant(spec.resample.target_count if spec.resample
+                                                         else ds1.perturbation_axis.size)
+            return CorrelationSpectra._trusted(
+                sync=s, asyn=a, axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, ref1=first[0], ref2=first[1],
+                normalization=constant, engine=engine, is_homo=homo,
+                scaling_exponent=float(alpha) if alpha > 0 else 0.0, stats=info)
     plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
                             dtype=dtype, device=device, engine_name=engine)
     plan.launch()
     _engine_mod.sync()
-    dsb = ds1 if homo else ds2
     ref1, ref2, _, _, info = plan.check(axes=(ds1.spectral_axis, dsb.spectral_axis),
                                         labels=("first", "second"))
     meta = dict(axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, ref1=ref1, ref2=ref2,

@@ -113,16 +113,27 @@ def correlate_ft(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers
     _, dev = engine.require_device(device)
     m = dyn1.m
     recipe = engine.PrepRecipe(m_in=m, m=m, ref_mode=_abi.REF_NONE)
-    plan = engine.CorrelationPlan(n1=dyn1.n, n2=dyn2.n, m=m, recipe1=recipe,
-                                  recipe2=None if homo else recipe, norm=constant, dtype=dtype,
-                                  rows=rows, device=dev, want_ref=False)
-    plan.bind(dyn1.device_values(dev), None if homo else dyn2.device_values(dev))
+
+    def make_plan(rws):
+        pl = engine.CorrelationPlan(n1=dyn1.n, n2=dyn2.n, m=m, recipe1=recipe,
+                                    recipe2=None if homo else recipe, norm=constant, dtype=dtype,
+                                    rows=rws, device=dev, want_ref=False)
+        return pl.bind(dyn1.device_values(dev), None if homo else dyn2.device_values(dev))
+
+    meta = dict(axis1=dyn1.spectral_axis, axis2=dyn2.spectral_axis, ref1=dyn1.reference_used,
+                ref2=dyn2.reference_used, normalization=constant, engine="fourier",
+                is_homo=homo, scaling_exponent=dyn1.scaling_exponent)
+    if not return_device and rows is None:
+        odt = np.dtype(dtype)
+        blocks = engine.stream_blocks(dyn1.n, dyn2.n, odt.itemsize, engine.device_budget(dev))
+        if blocks is not None:        # planes larger than device memory: stream row blocks
+            s, a, info, _ = engine.run_streamed(make_plan, dyn1.n, dyn2.n, odt, blocks, out)
+            return CorrelationSpectra._trusted(sync=s, asyn=a, stats=info, **meta)
+    plan = make_plan(rows)
     plan.launch()
     engine.sync()
     *_, info = plan.check()
-    meta = dict(axis1=dyn1.spectral_axis, axis2=dyn2.spectral_axis, ref1=dyn1.reference_used,
-                ref2=dyn2.reference_used, normalization=constant, engine="fourier",
-                is_homo=homo, scaling_exponent=dyn1.scaling_exponent, stats=info)
+    meta["stats"] = info
     if return_device:
         return DeviceCorrelationSpectra(plan, meta)
     if rows is not None and (plan.row0, plan.row1) != (0, dyn1.n):

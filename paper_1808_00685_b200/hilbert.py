@@ -59,13 +59,26 @@ def correlate_ht(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers
     (hilbert.py:92-115).  Same keyword-only extras as ``correlate_ft``."""
     if workers < 1:
         raise DataError(f"workers must be >= 1, got {workers}")
-    plan, homo, dyn2, constant = _plan(dyn1, dyn2, norm, rows, device)
+    homo = dyn2 is None or is_same_dynamic(dyn1, dyn2)
+    d2 = None if homo else dyn2
+    dynb = dyn1 if homo else dyn2
+    check_pair(dyn1, dynb)
+    constant = (norm or NormalizationSpec.unit()).constant(dyn1.m)
+    meta = dict(axis1=dyn1.spectral_axis, axis2=dynb.spectral_axis, ref1=dyn1.reference_used,
+                ref2=dynb.reference_used, normalization=constant, engine="hilbert",
+                is_homo=homo, scaling_exponent=dyn1.scaling_exponent)
+    if not return_device and rows is None:
+        _, dev = engine.require_device(device)
+        blocks = engine.stream_blocks(dyn1.n, dynb.n, 8, engine.device_budget(dev))
+        if blocks is not None:        # planes larger than device memory: stream row blocks
+            s, a, info, _ = engine.run_streamed(lambda rws: _plan(dyn1, d2, norm, rws, device)[0],
+                                                dyn1.n, dynb.n, np.float64, blocks, out)
+            return CorrelationSpectra._trusted(sync=s, asyn=a, stats=info, **meta)
+    plan, homo, dyn2, constant = _plan(dyn1, d2, norm, rows, device)
     plan.launch()
     engine.sync()
     *_, info = plan.check()
-    meta = dict(axis1=dyn1.spectral_axis, axis2=dyn2.spectral_axis, ref1=dyn1.reference_used,
-                ref2=dyn2.reference_used, normalization=constant, engine="hilbert",
-                is_homo=homo, scaling_exponent=dyn1.scaling_exponent, stats=info)
+    meta["stats"] = info
     if return_device:
         return DeviceCorrelationSpectra(plan, meta)
     if rows is not None and (plan.row0, plan.row1) != (0, dyn1.n):
