@@ -162,7 +162,22 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
   mphi = warp_max(mphi);
   mpsi = warp_max(mpsi);
   bad = warp_sum(bad);
+  // one set of atomics per CTA (tens of thousands of CTAs hit the same three words)
+  __shared__ double red_m[2][8];
+  __shared__ int red_b[8];
+  const int w = tid >> 5, nw = nthreads >> 5;
   if (lane == 0) {
+    red_m[0][w] = mphi;
+    red_m[1][w] = mpsi;
+    red_b[w] = bad;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = 1; i < nw; ++i) {
+      mphi = fmax(mphi, red_m[0][i]);
+      mpsi = fmax(mpsi, red_m[1][i]);
+      bad += red_b[i];
+    }
     atomic_max_abs(&p.stats[0], mphi);
     atomic_max_abs(&p.stats[1], mpsi);
     if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
