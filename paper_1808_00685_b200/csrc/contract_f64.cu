@@ -59,6 +59,7 @@ struct ContractParams {
   int row0, row1;
   int I0, I1, T;  // row-tile range of the shard, number of column tiles
   long long tile0;  // first tile of this launch (tile-range partition)
+  int vec_direct;   // planes 16-B aligned with an even ld_out: direct tiles from registers
   double* phi;
   double* psi;
   long long ld_out;
@@ -115,13 +116,16 @@ __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int
 // Both planes of a staged 64 x 64 tile (row pitch kCS) -> global memory as
 // coalesced 256-B row segments, plus the mirrored tile (sync^T, -async^T) of
 // homo tiles above the diagonal; fused max|.| / finite check into p.stats.
+// direct_done: the direct tile was already written from registers by the
+// caller, whose max / finite partials come in through mphi0 / mpsi0 / bad0.
 __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, int i0, int j0,
                                            const double* Cphi, const double* Cpsi, int tid, int nthreads,
-                                           int lane) {
-  double mphi = 0.0, mpsi = 0.0;
-  int bad = 0;
+                                           int lane, bool direct_done = false, double mphi0 = 0.0,
+                                           double mpsi0 = 0.0, int bad0 = 0) {
+  double mphi = mphi0, mpsi = mpsi0;
+  int bad = bad0;
   for (int idx = tid; idx < kBM * kBN; idx += nthreads) {
-    if (mode == kTransOnly) break;
+    if (mode == kTransOnly || direct_done) break;
     const int r = idx >> 6, c = idx & 63;
     const int gi = i0 + r, gj = j0 + c;
     if (gi >= p.row1 || gj >= p.n2) continue;
@@ -244,7 +248,46 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
     }
   }
 
-  // ---- epilogue: stage both planes, then coalesced (and mirrored) writes ----
+  // ---- epilogue.  Plain / mirrored tiles write their direct part straight
+  //      from the DMMA fragments (a thread holds 2 adjacent columns of 2 rows:
+  //      16-byte stores, 8 x 64-B row segments per warp instruction); the planes
+  //      are staged in shared memory for the transposed mirror and for the
+  //      symmetrised diagonal tiles, then written as coalesced rows ----
+  const bool reg_direct = p.vec_direct && (mode == kPlain || mode == kMirror);
+  double dphi = 0.0, dpsi = 0.0;
+  int dbad = 0;
+  if (reg_direct) {
+#pragma unroll
+    for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gi = i0 + wm * 16 * kMT + mt * 16 + lr + 8 * h;
+          const int gj = j0 + wn * 32 + nt * 8 + 2 * lk;
+          if (gi >= p.row1 || gj >= p.n2) continue;
+          const double f0 = acc_phi[mt][nt][2 * h], f1 = acc_phi[mt][nt][2 * h + 1];
+          const double s0 = acc_psi[mt][nt][2 * h], s1 = acc_psi[mt][nt][2 * h + 1];
+          const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
+          if (gj + 1 < p.n2) {
+            __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
+            __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
+            dphi = fmax(dphi, fmax(fabs(f0), fabs(f1)));
+            dpsi = fmax(dpsi, fmax(fabs(s0), fabs(s1)));
+            dbad += !(isfinite(f0) && isfinite(f1) && isfinite(s0) && isfinite(s1));
+          } else {
+            __stcs(p.phi + o, f0);
+            __stcs(p.psi + o, s0);
+            dphi = fmax(dphi, fabs(f0));
+            dpsi = fmax(dpsi, fabs(s0));
+            dbad += !(isfinite(f0) && isfinite(s0));
+          }
+        }
+    if (mode == kPlain) {       // nothing left to stage
+      write_tile(p, kPlain, i0, j0, nullptr, nullptr, tid, kThreads, lane, true, dphi, dpsi, dbad);
+      return;
+    }
+  }
   __syncthreads();
   double* Cphi = sm;                   // [kBM][kCS]
   double* Cpsi = sm + kBM * kCS;       // [kBM][kCS]
@@ -265,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
     }
   __syncthreads();
 
-  write_tile(p, mode, i0, j0, Cphi, Cpsi, tid, kThreads, lane);
+  write_tile(p, mode, i0, j0, Cphi, Cpsi, tid, kThreads, lane, reg_direct, dphi, dpsi, dbad);
 }
 
 }  // namespace corr2d
@@ -293,6 +336,7 @@ extern "C" int corr2d_contract_f64(
   p.n1 = n1; p.n2 = n2; p.mp = mp; p.homo = homo; p.row0 = row0; p.row1 = row1;
   p.I0 = row0 / kBM; p.I1 = (row1 + kBM - 1) / kBM; p.T = (n2 + kBN - 1) / kBN;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
+  p.vec_direct = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
   long long tiles;
   const long long R = p.I1 - p.I0;
   if (homo) tiles = R * p.T - R * (R - 1) / 2;   // sum_{d<R} (T - d)
