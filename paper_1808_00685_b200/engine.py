@@ -533,7 +533,9 @@ def copy_d2h(pairs, streams: int = 4, chunk_bytes: int = 256 << 20):
     t = torch()
     cur = t.cuda.current_stream()
     dev = cur.device
-    pool = _copy_streams.setdefault(dev, [t.cuda.Stream(device=dev) for _ in range(streams)])
+    pool = _copy_streams.get(dev)
+    if pool is None:
+        pool = _copy_streams[dev] = [t.cuda.Stream(device=dev) for _ in range(streams)]
     ready = t.cuda.Event()
     ready.record(cur)
     for st in pool:
