@@ -126,7 +126,76 @@ def main():
     if ex.exists():
         lines = [json.loads(l) for l in ex.read_text().splitlines() if l.startswith("{")]
         (dst / f"{rnd}_extras.json").write_text(json.dumps(lines, indent=1) + "\n")
+    readme(rnd, dst)
     print("wrote", sorted(p.name for p in dst.iterdir()))
+
+
+def _load(path):
+    return json.loads(path.read_text()) if path.exists() else None
+
+
+def readme(rnd, dst):
+    """profiles/README.md from the round's JSON files (no hand-edited numbers)."""
+    L = [f"# profiles/ -- round {rnd[1:]} evidence (B200, 1 GPU)", "",
+         f"Produced by `tools/profile_round.sh` under gpurun and summarised by "
+         f"`tools/summarize_profiles.py {rnd}`; every number below is read from the JSON files here.", "",
+         f"Files: `{rnd}_bench_cfg{{1..5}}.json` (bench.py lines), `{rnd}_bench_reference_cfg5.json` "
+         f"(reference arm), `{rnd}_launches_cfg5.csv` + `{rnd}_launch_shares_cfg5.json` (ncu launch list of "
+         f"the headline command), `{rnd}_ncu_cfg{{5,3}}.json`, `{rnd}_ncu_peaks5.json` (selected metrics of "
+         f"`ncu --set full` captures), `{rnd}_extras.json` (tools/bench_extras.py: Hilbert route, find_peaks, "
+         f"serialization), `traffic.json` (dram bytes per K2 launch, read by bench.py for `roofline.traffic`).",
+         "", "## Headline (bench.py, CUDA events over a graph of K steps, clocks sampled during the timed region)",
+         "", "| config | ms/step | GElem/s | K2 ms | roofline frac | executed frac | e2e GElem/s | SM MHz (reasons) |",
+         "|---|---|---|---|---|---|---|---|"]
+    b5 = None
+    for c in range(1, 6):
+        b = _load(dst / f"{rnd}_bench_cfg{c}.json")
+        if b is None:
+            continue
+        if c == 5:
+            b5 = b
+        r, ck = b["roofline"], b["clocks"]
+        ex = r.get("executed", {}).get("frac_of_peak")
+        L.append(f"| {b['config']['workload']} | {b['ms_per_step']:.4f} | {b['value']:.1f} | "
+                 f"{r.get('kernel_ms', float('nan')):.4f} | {r['frac']:.3f} ({r['bound']}, {r['peak']:g} {r['unit']}) | "
+                 f"{'-' if ex is None else f'{ex:.3f}'} | {b['e2e']['value']:.2f} | "
+                 f"{ck['sm_mhz']:.0f} {','.join(ck['reasons']) or '-'} |")
+    L.append("")
+    L.append("* roofline frac = algorithmic work / K2 time / measured peak (MEASURED_PEAKS.json). fp64 configs "
+             "exceed 1.0 because the homo map is computed once per mirrored tile pair (algorithmic flops count "
+             "the full map); executed frac counts the flops the kernel actually issues (bf16x3: three MMA "
+             "products, padded K).")
+    ref = _load(dst / f"{rnd}_bench_reference_cfg5.json")
+    if ref and b5:
+        L.append(f"* Reference arm ({ref['cpu_baseline']['kind']} on {ref['cpu_baseline']['cores']} host threads, "
+                 f"{ref['cpu_baseline']['sample'][:60]}...): {ref['value']:.4f} GElem/s -> e2e speed-up "
+                 f"{b5['e2e']['value'] / ref['value']:.0f}x (the e2e step is PCIe-bound: "
+                 f"{b5['e2e']['d2h_bytes_per_step'] / 1e9:.1f} GB of planes D2H per step); device-resident "
+                 f"value / reference = {b5['value'] / ref['value']:.0f}x.")
+    if b5:
+        cb = b5["cpu_baseline"]
+        L.append(f"* cpu_baseline in the cfg5 line: {cb['value']:.4f} GElem/s ({cb['cores']} threads, {cb['sample']}).")
+    L += ["", "## ncu (cold, serialised launches; per-launch numbers)", "",
+          "| kernel | config | duration ms | DRAM read MB | DRAM write MB | tensor pipe active % | SM MHz |",
+          "|---|---|---|---|---|---|---|"]
+    for tag in ("cfg5", "cfg3", "peaks5"):
+        ks = _load(dst / f"{rnd}_ncu_{tag}.json") or []
+        for k in ks:
+            tp = k.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 0.0)
+            hz = k.get("sm__cycles_elapsed.avg.per_second", 0.0)
+            hz_mhz = hz * (1e3 if k.get("sm__cycles_elapsed.avg.per_second.unit") == "Ghz" else
+                           1e-6 if k.get("sm__cycles_elapsed.avg.per_second.unit") == "hz" else 1)
+            L.append(f"| `{k['kernel'][:60]}` | {tag} | {k['gpu__time_duration.sum']:.4f} | "
+                     f"{k['dram__bytes_read.sum'] / 1e6:.1f} | {k['dram__bytes_write.sum'] / 1e6:.1f} | "
+                     f"{tp if isinstance(tp, str) else f'{tp:.1f}'} | {hz_mhz:.0f} |")
+    sh = _load(dst / f"{rnd}_launch_shares_cfg5.json")
+    if sh:
+        L += ["", "* Launch shares of the cfg5 step (ncu launch list): " + ", ".join(
+            f"{k.split('(')[0].replace('void ', '')} {v['share'] * 100:.1f}%" for k, v in sh["kernels"].items())]
+    ex = _load(dst / f"{rnd}_extras.json")
+    if ex:
+        L += ["", "## SURVEY 8f rows (tools/bench_extras.py)", ""] + [f"* `{json.dumps(e)}`" for e in ex]
+    (dst / "README.md").write_text("\n".join(L) + "\n")
 
 
 if __name__ == "__main__":
