@@ -7,8 +7,8 @@ complex Phi+iPsi output elements per second, GElem/s, plus roofline fraction).
 A step = one pass of the hot path over one batch of the config's synthetic
 input: K1 (resample -> reference -> sigma**alpha -> DFT -> pack) for every
 dataset + K2 (contraction -> sync/async planes), inputs resident in HBM.
-Default workload: config 5 (32768^2 complex map, fp32 planes from the bf16x3
-tcgen05 kernel) -- the largest map, the one BASELINE.json's scaling target is
+Default workload: config 5 (32768^2 complex map, fp32 planes from the
+fp16 + e4m3 (F16F8) tcgen05 kernel) -- the largest map, the one BASELINE.json's scaling target is
 quoted on; it fits one GPU.  Outputs (8.6 GB per step) are far larger than the
 126 MB L2, so each step starts with a cold L2.
 
@@ -82,7 +82,7 @@ def roofline_peak(case, peaks):
     SUSTAINED measured bf16 figure (MEASURED_PEAKS.json, B200_PROFILING.md);
     the burst figure is reported beside it.  FP64 DMMA does not reach the cap
     (cfg3 holds 1965 MHz): one measured figure."""
-    if case.dtype == "float32":      # bf16x3 on the f16 tensor pipe
+    if case.dtype == "float32":      # fp16 / bf16 MMAs on the tensor pipe (e4m3 ones at twice the rate)
         burst = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
         sus = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
         return "tensor", sus, "TFLOP/s", burst
@@ -213,7 +213,7 @@ METRIC = "complex Phi+iPsi outputs/sec (GElem/s) and % of HBM / tensor-core roof
 def config_block(case, wl, args):
     return {"workload": case.name, "config_index": case.cfg, "m": wl["m"], "K_bins": wl["K"],
             "n1": wl["n1"], "n2": wl["n2"], "homo": case.homo, "resample": case.resample,
-            "alpha": case.alpha, "compute": "bf16x3 tcgen05 -> fp32 planes" if case.dtype == "float32"
+            "alpha": case.alpha, "compute": f"{fp32_format()} tcgen05 -> fp32 planes" if case.dtype == "float32"
             else "fp64 DMMA -> fp64 planes",
             "l2": "outputs per step >> 126 MB L2 (cold L2 each step)" if wl["out_bytes"] + wl["in_bytes"] > 4 * 126e6
             else "L2 flushed between timed steps (256 MB write outside each step's event pair)",
@@ -368,7 +368,7 @@ def run_b200(args, case, wl, world, rank, local):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "ms_per_step_median": step_median, "ms_per_step_best": step_best,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "bf16x3->f32 (fp64 prep)" if case.dtype == "float32" else "f64",
+        "dtype": f"{fp32_format()}->f32" if case.dtype == "float32" else "f64",
         "data": "synthetic (seeded generators, SURVEY.md App. A; no public dataset)",
         "config": config_block(case, wl, args),
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
@@ -464,13 +464,16 @@ def cpu_baseline_line(case, wl):
 def executed_flops(plan, case, tc_peak, k2_ms):
     """Tensor-pipe flops K2 actually issues (not the algorithmic 8K per element):
     bf16x3 = 3 products x (x, y) MMAs of M=256, N=256 over the packed depth per
-    CTA-pair tile, homo triangle only; fp64 = both planes of every 64 x 64 tile
-    over the packed depth.  Rate vs the same measured peak shows how busy the
-    tensor pipe is, independent of the split / symmetry factors."""
+    CTA-pair tile, homo triangle only; f16f8 = the fp16 hi.hi product plus two
+    e4m3 cross products, each e4m3 MAC counted as half an fp16 one (twice the
+    rate), i.e. 2 fp16-equivalent products; fp64 = both planes of every 64 x 64
+    tile over the packed depth.  Rate vs the same measured (bf16) peak shows how
+    busy the tensor pipe is, independent of the split / symmetry factors."""
     tiles = plan.tile_count()
     if case.dtype == "float32":
         hp = plan.mp // 3
-        per_tile = 3 * 2 * 2 * 256 * 256 * hp              # 3 products, x + y MMAs, 2 flops/MAC, depth hp
+        products = 3 if fp32_format() == "bf16x3" else 2
+        per_tile = products * 2 * 2 * 256 * 256 * hp       # products, x + y MMAs, 2 flops/MAC, depth hp
     else:
         per_tile = 2 * 2 * 64 * 64 * plan.mp                # two planes, 2 flops/MAC
     f = float(tiles) * per_tile
@@ -478,15 +481,20 @@ def executed_flops(plan, case, tc_peak, k2_ms):
             "per_element_vs_algorithmic": f / (case.n1 * case.n2 * 8.0 * (case.m // 2 + 1))}
 
 
+def fp32_format():
+    """Operand format of the fp32 tensor-core path (engine.fp32_pack_kind)."""
+    return os.environ.get("CORR2D_FP32_FORMAT", "f16f8").lower()
+
+
 def contract_kernel_name(case):
-    """The contraction kernel the C ABI dispatches to (bf16_variant() in contract_bf16x3.cu)."""
+    """The contraction kernel the C ABI dispatches to (bf16_variant() in contract_tc.cu)."""
     if case.dtype != "float32":
         return "contract_f64_kernel"
     if os.environ.get("CORR2D_BF16_1SM") == "1":
-        return "contract_bf16x3_kernel"
+        return "contract_tc_kernel"
     if os.environ.get("CORR2D_BF16_QUADS") == "1":
-        return "contract_bf16x3_2sm_kernel<2>"
-    return "contract_bf16x3_2sm_kernel<1>"
+        return "contract_tc_2sm_kernel<2>"
+    return "contract_tc_2sm_kernel<1>"
 
 
 def load_traffic(cfg):

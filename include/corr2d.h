@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CORR2D_ABI_VERSION 2
+#define CORR2D_ABI_VERSION 3
 
 enum corr2d_status {
   CORR2D_OK = 0,
@@ -56,7 +56,8 @@ enum corr2d_pack {
   CORR2D_PACK_NONE = 0,
   CORR2D_PACK_F64 = 1,       /* float64 operands (fp64 DMMA contraction)            */
   CORR2D_PACK_BF16X2 = 2,    /* bf16 hi/lo, k-block interleaved (bf16x3 tcgen05 contraction) */
-  CORR2D_PACK_F64_TIME = 3   /* float64 time-domain values, no DFT (Hilbert route, hilbert.py) */
+  CORR2D_PACK_F64_TIME = 3,  /* float64 time-domain values, no DFT (Hilbert route, hilbert.py) */
+  CORR2D_PACK_F16F8 = 4      /* scaled fp16 hi + e4m3 hi / residual (fp16+fp8 tcgen05 contraction) */
 };
 
 enum corr2d_ref_mode { CORR2D_REF_MEAN = 0, CORR2D_REF_PROVIDED = 1, CORR2D_REF_NONE = 2 };
@@ -105,8 +106,8 @@ int corr2d_fft_factors(int m, int* factors, int max_factors);
  * (the caller forms A_psi = -norm_const * N y with one corr2d_contract_f64 call
  * against the Hilbert-Noda matrix, since async = Y1^T N Y2 = (-N Y1)^T Y2).
  * Packing: ld_pack is the row pitch of the packed operands in elements
- * (>= mp for F64; >= 2 * mp + 64 and a multiple of 64 for BF16X2, whose layout is
- * described at corr2d_contract_bf16x3).  split_plane is unused (ABI v1 kept
+ * (>= mp for F64; for BF16X2 and F16F8, in 2-byte units, >= 2 * mp + 64 and a
+ * multiple of 64; both layouts are described at corr2d_contract_tc).  split_plane is unused (ABI v1 kept
  * the bf16 lo values in a separate plane; v2 interleaves them).
  * Any output pointer may be NULL.  `status` (device int32[4]; reset on the
  * stream by this call) receives the counters above; the host raises the
@@ -142,22 +143,31 @@ int corr2d_contract_f64(
     double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
 /*
- * fp32 path (tcgen05 tensor cores).  Operands are K1's CORR2D_PACK_BF16X2
- * layout: per channel three thirds [Re' | Im' | -Im'] of hp = mp/3 slots
- * (Re'[s] = Re Y(s), Im'[0] = Re Y(m/2) for even m else 0, Im'[s] = Im Y(s)),
- * every slot scaled by sqrt(Norm * weight) and split x = hi + lo into two
- * bf16 values.  In memory each third is a run of 32-slot blocks of 64 bf16,
- * [hi of the 32 slots | lo of the 32 slots], so slot s of third t has its hi
- * at t*2*hp + (s/32)*64 + s%32 and its lo 32 elements later; one 128-byte
- * TMA box row then feeds both halves of a k-block.  Row pitch ld_pack >=
- * 2*mp + 64 (multiple of 64): K1 stores float32 (hi + lo) of Re'[0] and Im'[0]
- * at element 2*mp of the row (the epilogue's Nyquist correction operands).
- * a == b for homo; split_a / split_b are unused (ABI v1).
- * Products hi*hi + hi*lo + lo*hi accumulate in fp32 in TMEM (tcgen05.mma
- * kind::f16); the even-m Nyquist x DC cross term is removed in the epilogue.
- * Same row / homo / stats contract as corr2d_contract_f64, shard bounds
- * multiples of 128.
+ * fp32 path (tcgen05 tensor cores).  Operands are K1's CORR2D_PACK_BF16X2 or
+ * CORR2D_PACK_F16F8 rows: per channel three thirds [Re' | Im' | -Im'] of
+ * hp = mp/3 slots (Re'[s] = Re Y(s), Im'[0] = Re Y(m/2) for even m else 0,
+ * Im'[s] = Im Y(s)), every slot scaled by sqrt(Norm * weight).  Each third is
+ * a run of 32-slot blocks of 128 bytes, so one 128-byte TMA box row feeds a
+ * whole k-block; row pitch ld_pack (2-byte units) >= 2*mp + 64, multiple of 64.
+ *   BF16X2: block = [bf16 hi of the 32 slots | bf16 lo], x = hi + lo; products
+ *     hi*hi + hi*lo + lo*hi (tcgen05.mma kind::f16).  Row pad at element 2*mp:
+ *     float32 (hi + lo) of Re'[0] and Im'[0].
+ *   F16F8: the channel is scaled by sc = 2^s (max|x| sc in [2^7, 2^8)); block =
+ *     [fp16(x sc) * 2^5 of the 32 slots (64 B) | e4m3(x sc) (32 B) |
+ *     e4m3((x sc - fp16(x sc)) * 2^10) (32 B)]; products hi*hi (kind::f16) +
+ *     e4m3 hi * e4m3 residual both ways (kind::f8f6f4, twice the rate), all at
+ *     scale 2^10 sc_i sc_j, undone in the epilogue.  Row pad at element 2*mp:
+ *     float32 Re'[0], Im'[0] (unscaled) and 2^-(s+5).
+ * FP32 accumulators in TMEM; the even-m Nyquist x DC cross term is removed in
+ * the epilogue.  a == b for homo.  Same row / homo / stats contract as
+ * corr2d_contract_f64, shard bounds multiples of 128.
  */
+int corr2d_contract_tc(
+    int pack_kind, const void* a, const void* b, int64_t ld_pack,
+    int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
+    float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream);
+
+/* corr2d_contract_tc(CORR2D_PACK_BF16X2, ...); split_a / split_b are unused (ABI v1). */
 int corr2d_contract_bf16x3(
     const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
     int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
@@ -167,7 +177,7 @@ int corr2d_contract_bf16x3(
  * Number of tiles in the enumeration corr2d_contract_f64 / _bf16x3 would use for
  * this call (the [tile0, tile1) range of the contract calls indexes it): the
  * unit of the multi-GPU tile-range partition.  -1 on bad arguments.  For
- * pack_kind BF16X2 and a whole-map call with ld_out % 4 == 0 this is the
+ * pack_kind BF16X2 / F16F8 and a whole-map call with ld_out % 4 == 0 this is the
  * 2-SM (CTA-pair) enumeration; CORR2D_BF16_1SM=1 in the environment forces the
  * 1-SM kernel.
  */

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcorr2d.so"
 OK, ERR_DATA, ERR_NUMERIC, ERR_OOM, ERR_CUDA, ERR_UNSUPPORTED = range(6)
 F64, F32 = 0, 1
 RESAMPLE_NONE, RESAMPLE_LINEAR, RESAMPLE_MATRIX = 0, 1, 2
-PACK_NONE, PACK_F64, PACK_BF16X2, PACK_F64_TIME = 0, 1, 2, 3
+PACK_NONE, PACK_F64, PACK_BF16X2, PACK_F64_TIME, PACK_F16F8 = 0, 1, 2, 3, 4
 ROLE_A, ROLE_B = 1, 2
 REF_MEAN, REF_PROVIDED, REF_NONE = 0, 1, 2
 ST_NONFINITE, ST_ZEROVAR, ST_FIRST_ZEROVAR = 0, 1, 2
@@ -29,7 +29,7 @@ INT32_MAX = 2**31 - 1
 EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
-    "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
+    "corr2d_contract_tc", "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
     "corr2d_format_repr", "corr2d_format_rows",
 )
 
@@ -68,6 +68,10 @@ def _declare(lib):
         c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
         c_i64, c_i64, c_void, c_void, c_i64, c_void, c_void,
     ]
+    lib.corr2d_contract_tc.argtypes = [
+        c_int, c_void, c_void, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+        c_i64, c_i64, c_void, c_void, c_i64, c_void, c_void,
+    ]
     lib.corr2d_contract_tile_count.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_i64]
     lib.corr2d_contract_tile_count.restype = c_i64
     lib.corr2d_plane_absmax.argtypes = [c_int, c_void, c_i64, c_int, c_int, c_void, c_void]
@@ -78,7 +82,7 @@ def _declare(lib):
                                        ctypes.c_char, c_int, c_int, c_void, c_i64, c_void]
     for name in ("corr2d_format_repr", "corr2d_format_rows",
                  "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
-                 "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
+                 "corr2d_contract_tc", "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
                  "corr2d_plane_absmax", "corr2d_find_peaks"):
         getattr(lib, name).restype = c_int
 

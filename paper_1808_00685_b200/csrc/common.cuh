@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_fp8.h>
 #include <stdint.h>
 #include <string>
 
@@ -31,6 +33,29 @@ __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// ---- CORR2D_PACK_F16F8 (see corr2d.h): per-channel power-of-two scale sc with
+// max|x| * sc in [2^7, 2^8); each scaled slot x is stored as fp16(x) * 2^5, the
+// e4m3 copy of x and e4m3((x - fp16(x)) * 2^10), so every tensor-core product
+// (fp16 hi.hi and the two e4m3 cross terms) lands at scale 2^10 sc_i sc_j.
+// Shift s of sc = 2^s from the bit pattern of max|x|; 0 for an all-zero or
+// non-finite channel.
+__device__ __forceinline__ int f16f8_shift(uint32_t maxbits) {
+  if (maxbits == 0u || maxbits >= 0x7f800000u) return 0;
+  const int s = 7 - ((int)(maxbits >> 23) - 127);
+  return s < -120 ? -120 : (s > 120 ? 120 : s);
+}
+__device__ __forceinline__ float pow2f(int s) { return __uint_as_float((uint32_t)(127 + s) << 23); }
+
+// Two adjacent scaled slots -> fp16 hi x 2^5 (2 halves), e4m3 hi, e4m3 residual x 2^10.
+__device__ __forceinline__ void f16f8_split2(float x0, float x1, uint32_t& h16, uint16_t& h8, uint16_t& l8) {
+  const __half2 h = __floats2half2_rn(x0 * 32.f, x1 * 32.f);
+  const float2 hf = __half22float2(h);
+  const float r0 = x0 - hf.x * 0.03125f, r1 = x1 - hf.y * 0.03125f;
+  h16 = *reinterpret_cast<const uint32_t*>(&h);
+  h8 = (uint16_t)__nv_cvt_float2_to_fp8x2(make_float2(x0, x1), __NV_SATFINITE, __NV_E4M3);
+  l8 = (uint16_t)__nv_cvt_float2_to_fp8x2(make_float2(r0 * 1024.f, r1 * 1024.f), __NV_SATFINITE, __NV_E4M3);
 }
 
 }  // namespace corr2d

@@ -1,11 +1,15 @@
 // K2c (fp32 results) -- packed-spectrum contraction on the 5th-gen tensor cores.
 //
 // Same contract as K2 fp64 (fourier.py:107-123: Norm * sum_w weight(w)
-// Y1 conj(Y2), split into sync / async planes), computed with tcgen05.mma
-// kind::f16 (BF16 inputs, FP32 accumulators in TMEM).  Each packed spectrum
-// value x (float64 from K1) is split x = hi + lo with hi = bf16(x),
-// lo = bf16(x - hi); the products hi*hi + hi*lo + lo*hi carry ~16 mantissa
-// bits, i.e. ~1e-5 relative to max|sync| -- inside the 1e-4 fp32 budget that
+// Y1 conj(Y2), split into sync / async planes), FP32 accumulators in TMEM,
+// from one of two operand formats written by K1 (include/corr2d.h):
+//   CORR2D_PACK_F16F8 (default): per-channel power-of-two scale sc, then
+//     fp16 hi.hi (tcgen05.mma kind::f16) + e4m3 hi x e4m3 residual both ways
+//     (kind::f8f6f4, twice the fp16 rate): ~15 bits per product, 8 MMAs per
+//     k-block; the epilogue multiplies by 2^-(s_i+5) 2^-(s_j+5).
+//   CORR2D_PACK_BF16X2: x = hi + lo in bf16, hi*hi + hi*lo + lo*hi (kind::f16):
+//     ~16 bits per product, 12 MMAs per k-block.
+// Both stay well inside the 1e-4 (relative to max|sync|) fp32 budget that
 // single-pass TF32/BF16 would miss on band-limited data.
 //
 // Operand format (K1, CORR2D_PACK_BF16X2): per channel [Re' | Im'] halves of
@@ -54,7 +58,7 @@ constexpr int STG_MIRROR = CH * BM * 4; // 8 KB: 16 rows x 512 B
 constexpr int STG_BYTES = 2 * (STG_DIRECT + STG_MIRROR);
 constexpr int THREADS = 192;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 2 * BN * 4 + 16 * 8 + 16;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_BYTES + 3 * BN * 4 + 16 * 8 + 16;
 // CTA-pair kernels: 3 operand stages of 64 KB (4 boxes of 128 rows x [hi 32 | lo 32]
 // slots, 128-B rows, SWIZZLE_128B); epilogue chunks of 32 columns staged per warp
 // as a tile box and a mirror box of 32 x 32 fp32 (SWIZZLE_128B).  Variants measured
@@ -65,16 +69,23 @@ constexpr int KB2 = 32;
 static_assert(KB2 == KB, "operand boxes are 2*KB bf16 wide in both kernels");
 constexpr int TILE2_BYTES = BM * KB2 * 2;    // 8 KB
 constexpr int STAGE2_BYTES = 8 * TILE2_BYTES;
-constexpr int STAGES2 = 3;
+#ifndef CORR2D_PAIR_STAGES
+#define CORR2D_PAIR_STAGES 3
+#endif
+#ifndef CORR2D_PAIR_STGBUF
+#define CORR2D_PAIR_STGBUF 1
+#endif
+constexpr int STAGES2 = CORR2D_PAIR_STAGES;
+constexpr int STGBUF2 = CORR2D_PAIR_STGBUF;   // staging buffers per epilogue warp
 constexpr int CH2 = 32;                      // epilogue chunk width (columns)
 constexpr int BOX2 = 32 * CH2 * 4;           // one 32 x 32 fp32 box: 4 KB
 // one staging buffer (tile box + mirror box) per epilogue warp, shared by both
 // planes: each store waits for the previous one's smem read, but the 32 KB
 // saved buys the third operand stage (measured: 2.67 vs 2.80 ms on cfg5)
-constexpr int WSTG2 = 2 * BOX2;
+constexpr int WSTG2 = 2 * BOX2 * STGBUF2;
 constexpr int EPI_WARPS2 = 4;
 constexpr int STG2_BYTES = EPI_WARPS2 * WSTG2;
-constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 2 * BN * 4 + (2 * STAGES2 + 4) * 8 + 16;
+constexpr size_t SMEM2_BYTES = 1024 + STAGES2 * STAGE2_BYTES + STG2_BYTES + 3 * BN * 4 + (2 * STAGES2 + 4) * 8 + 16;
 static_assert(SMEM2_BYTES <= 232448, "CTA-pair kernel shared memory");
 constexpr int PPW2 = 8 / EPI_WARPS2;         // planes per epilogue warp
 constexpr int THREADS2 = 64 + 32 * EPI_WARPS2;
@@ -86,6 +97,7 @@ enum TileMode { kPlain = 0, kMirror = 1, kDiag = 2, kTransOnly = 3 };
 
 struct Params {
   int n1, n2, hp, homo, even, tma_store;
+  int f8;                   // operands in CORR2D_PACK_F16F8 layout (else BF16X2)
   int row0, row1, I0, I1, T;
   long long tile0, ntiles;  // tiles [tile0, ntiles) of the enumeration
   const __nv_bfloat16* a;
@@ -163,11 +175,18 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+__device__ __forceinline__ void umma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+}
+__device__ __forceinline__ void umma_f8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}\n"
       ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -213,6 +232,11 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
 __host__ __device__ constexpr uint32_t idesc_bf16(bool neg_a) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (neg_a ? (1u << 13) : 0u) |
          ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+// F16 x F16 (kind::f16) and E4M3 x E4M3 (kind::f8f6f4) -> F32 share one encoding
+// (format fields 0); the kind comes from the instruction.
+__host__ __device__ constexpr uint32_t idesc_f16f8(bool neg_a) {
+  return (1u << 4) | (neg_a ? (1u << 13) : 0u) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -271,6 +295,10 @@ __device__ __forceinline__ float bf2f(__nv_bfloat16 x) { return __bfloat162float
 // values of every BF16X2 row (the epilogue's Nyquist x DC correction operands)
 __device__ __forceinline__ float2 dc_nyq(const __nv_bfloat16* base, long long row, long long ld, int hp) {
   return *reinterpret_cast<const float2*>(base + row * ld + 6 * hp);
+}
+// F16F8 rows: float4 (Re'[0], Im'[0], output scale 2^-(s+5), 0)
+__device__ __forceinline__ float4 dc_nyq_sc(const __nv_bfloat16* base, long long row, long long ld, int hp) {
+  return *reinterpret_cast<const float4*>(base + row * ld + 6 * hp);
 }
 
 // Per-warp epilogue staging: the warp owning TMEM lanes 32q..32q+31 stages its
@@ -441,7 +469,7 @@ __device__ __forceinline__ void tmem_wait_ld_tie(uint32_t (&u)[32]) {
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
-contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+contract_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                        const __grid_constant__ OutMaps outm, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // keep the shared address space visible to the compiler (LDS/STS, not LD/ST)
@@ -450,7 +478,8 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
   uint8_t* staging = stages + STAGES * STAGE_BYTES;  // [2] x {direct 8 KB, mirror 8 KB}
   float* col_re0 = reinterpret_cast<float*>(staging + STG_BYTES);
   float* col_im0 = col_re0 + BN;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
+  float* col_sc = col_im0 + BN;          // F16F8: per-column output scale
+  uint64_t* bars = reinterpret_cast<uint64_t*>(col_sc + BN);
   uint64_t* full = bars;                 // [STAGES]
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
@@ -515,6 +544,30 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         tc_fence_after();
         if (lane == 0) {
           const uint32_t base = su32(stages + stage * STAGE_BYTES);
+          if (p.f8) {
+            // F16F8 block [fp16 hi 64 B | e4m3 hi 32 B | e4m3 residual 32 B]:
+            // hi.hi as two K=16 fp16 MMAs, the cross terms as K=32 e4m3 MMAs
+            constexpr uint32_t IF = idesc_f16f8(false), IFN = idesc_f16f8(true);
+            const uint32_t are = base + 0 * TILE_BYTES, aim = base + 2 * TILE_BYTES;
+            const uint32_t bre = base + 4 * TILE_BYTES, bim = base + 6 * TILE_BYTES;
+            const uint32_t acc0 = kb ? 1u : 0u;
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint32_t off = ks * 32;
+              umma_f16(d_phi, desc_sw128(are + off), desc_sw128(bre + off), IF, ks ? 1u : acc0);
+              umma_f16(d_phi, desc_sw128(aim + off), desc_sw128(bim + off), IF, 1);
+              umma_f16(d_psi, desc_sw128(aim + off), desc_sw128(bre + off), IF, ks ? 1u : acc0);
+              umma_f16(d_psi, desc_sw128(are + off), desc_sw128(bim + off), IFN, 1);
+            }
+            umma_f8(d_phi, desc_sw128(are + 64), desc_sw128(bre + 96), IF, 1);
+            umma_f8(d_phi, desc_sw128(are + 96), desc_sw128(bre + 64), IF, 1);
+            umma_f8(d_phi, desc_sw128(aim + 64), desc_sw128(bim + 96), IF, 1);
+            umma_f8(d_phi, desc_sw128(aim + 96), desc_sw128(bim + 64), IF, 1);
+            umma_f8(d_psi, desc_sw128(aim + 64), desc_sw128(bre + 96), IF, 1);
+            umma_f8(d_psi, desc_sw128(aim + 96), desc_sw128(bre + 64), IF, 1);
+            umma_f8(d_psi, desc_sw128(are + 64), desc_sw128(bim + 96), IFN, 1);
+            umma_f8(d_psi, desc_sw128(are + 96), desc_sw128(bim + 64), IFN, 1);
+          } else
 #pragma unroll
           for (int ks = 0; ks < KB / 16; ++ks) {
             const uint32_t off = ks * 32;  // 16 bf16 = 32 bytes along K
@@ -524,19 +577,19 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             const uint64_t bim_h = desc_sw128(base + 6 * TILE_BYTES + off), bim_l = desc_sw128(base + 6 * TILE_BYTES + 64 + off);
             const uint32_t acc0 = (kb | ks) ? 1u : 0u;
             // sync  += Re.Re + Im.Im          (hi.hi + hi.lo + lo.hi each)
-            umma_bf16(d_phi, are_h, bre_h, ID, acc0);
-            umma_bf16(d_phi, are_h, bre_l, ID, 1);
-            umma_bf16(d_phi, are_l, bre_h, ID, 1);
-            umma_bf16(d_phi, aim_h, bim_h, ID, 1);
-            umma_bf16(d_phi, aim_h, bim_l, ID, 1);
-            umma_bf16(d_phi, aim_l, bim_h, ID, 1);
+            umma_f16(d_phi, are_h, bre_h, ID, acc0);
+            umma_f16(d_phi, are_h, bre_l, ID, 1);
+            umma_f16(d_phi, are_l, bre_h, ID, 1);
+            umma_f16(d_phi, aim_h, bim_h, ID, 1);
+            umma_f16(d_phi, aim_h, bim_l, ID, 1);
+            umma_f16(d_phi, aim_l, bim_h, ID, 1);
             // async += Im.Re - Re.Im
-            umma_bf16(d_psi, aim_h, bre_h, ID, acc0);
-            umma_bf16(d_psi, aim_h, bre_l, ID, 1);
-            umma_bf16(d_psi, aim_l, bre_h, ID, 1);
-            umma_bf16(d_psi, are_h, bim_h, IDN, 1);
-            umma_bf16(d_psi, are_h, bim_l, IDN, 1);
-            umma_bf16(d_psi, are_l, bim_h, IDN, 1);
+            umma_f16(d_psi, aim_h, bre_h, ID, acc0);
+            umma_f16(d_psi, aim_h, bre_l, ID, 1);
+            umma_f16(d_psi, aim_l, bre_h, ID, 1);
+            umma_f16(d_psi, are_h, bim_h, IDN, 1);
+            umma_f16(d_psi, are_h, bim_l, IDN, 1);
+            umma_f16(d_psi, are_l, bim_h, IDN, 1);
           }
           umma_commit(&empty[stage]);                 // smem stage free when these finish
           if (kb == nkb - 1) umma_commit(&tfull[acc]); // accumulators ready
@@ -568,23 +621,39 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
       decode_tile(p, t, I, J, mode);
       const int i0 = I * BM, j0 = J * BN;
       const int gi = i0 + r;                   // direct row / mirrored column
-      float row_re0 = 0.f, row_im0 = 0.f;
-      if (p.even) {
-        if (gi < p.n1) {
-          const float2 d = dc_nyq(p.a, gi, p.ld_pack, p.hp);
-          row_re0 = d.x;
-          row_im0 = d.y;
-        }
+      float row_re0 = 0.f, row_im0 = 0.f, row_sc = 1.f;
+      if (p.even || p.f8) {
         const int gj = j0 + eid;
-        float cre = 0.f, cim = 0.f;
-        if (gj < p.n2) {
-          const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
-          cre = d.x;
-          cim = d.y;
+        float cre = 0.f, cim = 0.f, csc = 0.f;
+        if (p.f8) {
+          if (gi < p.n1) {
+            const float4 d = dc_nyq_sc(p.a, gi, p.ld_pack, p.hp);
+            row_re0 = d.x;
+            row_im0 = d.y;
+            row_sc = d.z;
+          }
+          if (gj < p.n2) {
+            const float4 d = dc_nyq_sc(p.b, gj, p.ld_pack, p.hp);
+            cre = d.x;
+            cim = d.y;
+            csc = d.z;
+          }
+        } else {
+          if (gi < p.n1) {
+            const float2 d = dc_nyq(p.a, gi, p.ld_pack, p.hp);
+            row_re0 = d.x;
+            row_im0 = d.y;
+          }
+          if (gj < p.n2) {
+            const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+            cre = d.x;
+            cim = d.y;
+          }
         }
         epi_bar();   // previous tile finished reading col_* vectors
         col_re0[eid] = cre;
         col_im0[eid] = cim;
+        col_sc[eid] = csc;
         epi_bar();
       }
       const bool direct = (mode != kTransOnly) && gi < p.row1;
@@ -606,6 +675,10 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
           float v[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(u[k]);
+          if (p.f8) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[k] *= row_sc * col_sc[c * CH + k];
+          }
           if (plane == 1 && p.even) {
 #pragma unroll
             for (int k = 0; k < 16; ++k)
@@ -694,6 +767,7 @@ contract_bf16x3_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
 
 struct Params2 {
   int n1, n2, hp, homo, even, tma_store;
+  int f8;                 // operands in CORR2D_PACK_F16F8 layout (else BF16X2)
   int store_pol;          // L2 policy of the output stores: 0 evict_first, 1 normal, 2 evict_last
   int dbg;                // profiling switches: 1 = no output stores, 2 = no MMAs (results invalid)
   long long* trace;       // profiling (CORR2D_TRACE=1): per-CTA stall cycles, 8 counters each
@@ -759,11 +833,18 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* ma
       ::"r"(su32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "l"(pol)
       : "memory");
 }
-__device__ __forceinline__ void umma2_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+__device__ __forceinline__ void umma2_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+}
+__device__ __forceinline__ void umma2_f8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}\n"
       ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
 }
 __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
@@ -775,6 +856,10 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
 // M = 256 (pair), N = 256
 __host__ __device__ constexpr uint32_t idesc_bf16_2sm() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+// F16 x F16 (kind::f16) / E4M3 x E4M3 (kind::f8f6f4), M = 256, N = 256
+__host__ __device__ constexpr uint32_t idesc_f16f8_2sm() {
+  return (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
 // Grouped raster order: row pairs are taken kGroup at a time and, inside a
@@ -975,34 +1060,51 @@ __device__ __forceinline__ void umma2_commit_mask(uint64_t* bar, uint16_t mask) 
 // tile ahead so the L2 latency is hidden behind the previous tile's stores.
 struct NyqOperands {
   // raw loads; consumed only in finish(), so they are not waited on where issued
-  float2 rw, cl[4];
-  float row_re0, row_im0, cre4[4], cim4[4];
+  float4 rw, cl[4];
+  float row_re0, row_im0, row_sc, cre4[4], cim4[4], csc4[4];
   __device__ __forceinline__ void load(const Params2& p, int gi, int j0, int lane) {
-    rw = make_float2(0.f, 0.f);
+    rw = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) cl[k] = make_float2(0.f, 0.f);
+    for (int k = 0; k < 4; ++k) cl[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p.f8) {      // F16F8 rows also carry the output scale
+      if (gi < p.n1) rw = dc_nyq_sc(p.a, gi, p.ld_pack, p.hp);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int gj = j0 + 32 * c4 + lane;
+        if (gj < p.n2) cl[c4] = dc_nyq_sc(p.b, gj, p.ld_pack, p.hp);
+      }
+      return;
+    }
     if (!p.even) return;
-    if (gi < p.n1) rw = dc_nyq(p.a, gi, p.ld_pack, p.hp);
+    if (gi < p.n1) {
+      const float2 d = dc_nyq(p.a, gi, p.ld_pack, p.hp);
+      rw = make_float4(d.x, d.y, 0.f, 0.f);
+    }
 #pragma unroll
     for (int c4 = 0; c4 < 4; ++c4) {
       const int gj = j0 + 32 * c4 + lane;
-      if (gj < p.n2) cl[c4] = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+      if (gj < p.n2) {
+        const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+        cl[c4] = make_float4(d.x, d.y, 0.f, 0.f);
+      }
     }
   }
   __device__ __forceinline__ void finish() {
     row_re0 = rw.x;
     row_im0 = rw.y;
+    row_sc = rw.z;
 #pragma unroll
     for (int c4 = 0; c4 < 4; ++c4) {
       cre4[c4] = cl[c4].x;
       cim4[c4] = cl[c4].y;
+      csc4[c4] = cl[c4].z;
     }
   }
 };
 
 template <int NPAIR>
 __global__ void __launch_bounds__(THREADS2, 1)
-contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                            const __grid_constant__ OutMaps outm, const Params2 p) {
   // 4 operand stages of 16 slots (128 KB) + 32-column epilogue chunks
   // (128-B row segments in both the tile and its mirror).
@@ -1016,7 +1118,8 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
   uint8_t* staging = stages + STAGES * STAGE_BYTES;
   float* col_re0 = reinterpret_cast<float*>(staging + STG2_BYTES);
   float* col_im0 = col_re0 + BN;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(col_im0 + BN);
+  float* col_sc = col_im0 + BN;          // F16F8: per-column output scale
+  uint64_t* bars = reinterpret_cast<uint64_t*>(col_sc + BN);
   uint64_t* full = bars;                 // [STAGES] (used in the pair leader)
   uint64_t* empty = bars + STAGES;       // [STAGES]
   uint64_t* tfull = bars + 2 * STAGES;   // [2]
@@ -1110,7 +1213,30 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_t(&full[stage], phase, tr ? &tr_wait : nullptr);
           tc_fence_after();
-          if (lane == 0) {
+          if (lane == 0 && p.f8) {
+            // F16F8 block [fp16 hi 64 B | e4m3 hi 32 B | e4m3 residual 32 B]:
+            // hi.hi as two K=16 fp16 MMAs per operand pair, the cross terms as
+            // K=32 e4m3 MMAs (twice the fp16 rate) -- 8 MMAs per k-block
+            // against bf16x3's 12
+            constexpr uint32_t IF = idesc_f16f8_2sm();
+            const uint32_t base = su32(stages + stage * STAGE_BYTES);
+            const uint32_t are = base, aim = base + 2 * TILE_BYTES;
+            const uint32_t bx = base + 4 * TILE_BYTES, by = base + 6 * TILE_BYTES;
+            if (!(p.dbg & 2)) {
+#pragma unroll
+              for (int ks = 0; ks < 2; ++ks) {
+                const uint32_t off = ks * 32;
+                umma2_f16(d, desc_sw128(are + off), desc_sw128(bx + off), IF, (kb | ks) ? 1u : 0u);
+                umma2_f16(d, desc_sw128(aim + off), desc_sw128(by + off), IF, 1);
+              }
+              umma2_f8(d, desc_sw128(are + 64), desc_sw128(bx + 96), IF, 1);
+              umma2_f8(d, desc_sw128(are + 96), desc_sw128(bx + 64), IF, 1);
+              umma2_f8(d, desc_sw128(aim + 64), desc_sw128(by + 96), IF, 1);
+              umma2_f8(d, desc_sw128(aim + 96), desc_sw128(by + 64), IF, 1);
+            }
+            umma2_commit_mask(&empty[stage], all_mask);
+            if (kb == nkb - 1) umma2_commit_mask(&tfull[acc], pair_mask);
+          } else if (lane == 0) {
             const uint32_t base = su32(stages + stage * STAGE_BYTES);
 #pragma unroll
             for (int ks = 0; ks < KB / 16; ++ks) {
@@ -1121,12 +1247,12 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               const uint64_t by_h = desc_sw128(base + 6 * TILE_BYTES + off), by_l = desc_sw128(base + 6 * TILE_BYTES + 64 + off);
               const uint32_t acc0 = (kb | ks) ? 1u : 0u;
               if (p.dbg & 2) continue;
-              umma2_bf16(d, are_h, bx_h, ID, acc0);
-              umma2_bf16(d, are_h, bx_l, ID, 1);
-              umma2_bf16(d, are_l, bx_h, ID, 1);
-              umma2_bf16(d, aim_h, by_h, ID, 1);
-              umma2_bf16(d, aim_h, by_l, ID, 1);
-              umma2_bf16(d, aim_l, by_h, ID, 1);
+              umma2_f16(d, are_h, bx_h, ID, acc0);
+              umma2_f16(d, are_h, bx_l, ID, 1);
+              umma2_f16(d, are_l, bx_h, ID, 1);
+              umma2_f16(d, aim_h, by_h, ID, 1);
+              umma2_f16(d, aim_h, by_l, ID, 1);
+              umma2_f16(d, aim_l, by_h, ID, 1);
             }
             // stage s is free only when every pair of the cluster has consumed it
             // (NPAIR == 2: A was multicast into both pairs); the accumulator is
@@ -1154,6 +1280,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
     int acc = 0;
     uint32_t acc_phase = 0;
     float mphi = 0.f, mpsi = 0.f, chk = 0.f;
+    uint32_t nchunk = 0;
     PairWalk walk;
     walk.init(p, p.tile0 + cid);
     // the NEXT tile's correction operands are prefetched one tile ahead
@@ -1186,19 +1313,27 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
         // shuffles -- no CTA-wide barrier on the common path
         nyq.finish();
         const float row_re0 = nyq.row_re0, row_im0 = nyq.row_im0;
-        if (p.even) {
+        if (p.even || p.f8) {
           if (!use_tma) {
             const int gj = j0 + eid;
-            float cre = 0.f, cim = 0.f;
+            float cre = 0.f, cim = 0.f, csc = 0.f;
             if (eid < BN && gj < p.n2) {
-              const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
-              cre = d.x;
-              cim = d.y;
+              if (p.f8) {
+                const float4 d = dc_nyq_sc(p.b, gj, p.ld_pack, p.hp);
+                cre = d.x;
+                cim = d.y;
+                csc = d.z;
+              } else {
+                const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+                cre = d.x;
+                cim = d.y;
+              }
             }
             epi_bar256();   // diagonal tiles only: every epilogue warp of the CTA takes this branch
             if (eid < BN) {
               col_re0[eid] = cre;
               col_im0[eid] = cim;
+              col_sc[eid] = csc;
             }
             epi_bar256();
           }
@@ -1219,7 +1354,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
           for (int c = 0; c < BN / CH2; ++c) {
 #pragma unroll 1
             for (int plane = pw; plane < pw + PPW2; ++plane) {
-              uint8_t* wst = staging + (warp - 2) * WSTG2;
+              uint8_t* wst = staging + (warp - 2) * WSTG2 + (STGBUF2 > 1 ? (nchunk++ & 1) * 2 * BOX2 : 0);
               const float tsign = plane == 0 ? 1.f : -1.f;
               float mx = 0.f;
               uint32_t ua[CH2];
@@ -1230,12 +1365,16 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               float v[CH2];
 #pragma unroll
               for (int k = 0; k < CH2; ++k) v[k] = __uint_as_float(ua[k]);
+              const int c4 = (c * CH2) >> 5, l0 = (c * CH2) & 31;
+              float cr = nyq.cre4[0], ci = nyq.cim4[0], cs = nyq.csc4[0];
+              if (c4 == 1) { cr = nyq.cre4[1]; ci = nyq.cim4[1]; cs = nyq.csc4[1]; }
+              if (c4 == 2) { cr = nyq.cre4[2]; ci = nyq.cim4[2]; cs = nyq.csc4[2]; }
+              if (c4 == 3) { cr = nyq.cre4[3]; ci = nyq.cim4[3]; cs = nyq.csc4[3]; }
+              if (p.f8) {   // undo the F16F8 operand scales: 2^-(s_i+5) 2^-(s_j+5)
+#pragma unroll
+                for (int k = 0; k < CH2; ++k) v[k] *= nyq.row_sc * __shfl_sync(0xffffffffu, cs, l0 + k);
+              }
               if (plane == 1 && p.even) {
-                const int c4 = (c * CH2) >> 5, l0 = (c * CH2) & 31;
-                float cr = nyq.cre4[0], ci = nyq.cim4[0];
-                if (c4 == 1) { cr = nyq.cre4[1]; ci = nyq.cim4[1]; }
-                if (c4 == 2) { cr = nyq.cre4[2]; ci = nyq.cim4[2]; }
-                if (c4 == 3) { cr = nyq.cre4[3]; ci = nyq.cim4[3]; }
 #pragma unroll
                 for (int k = 0; k < CH2; ++k)
                   v[k] -= row_im0 * __shfl_sync(0xffffffffu, cr, l0 + k) - row_re0 * __shfl_sync(0xffffffffu, ci, l0 + k);
@@ -1257,7 +1396,7 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
               }
               const long long ts0 = tr ? clock64() : 0;
               if (!(p.dbg & 1))
-                stage_and_store_32_plane<0>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
+                stage_and_store_32_plane<STGBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
                                             j0 + c * CH2, i0 + 32 * q, drop);
               if (tr) tr_store += clock64() - ts0;
               if (plane == 0) mphi = fmaxf(mphi, mx); else mpsi = fmaxf(mpsi, mx);
@@ -1277,6 +1416,10 @@ contract_bf16x3_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __g
             float v[16];
 #pragma unroll
             for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(u[k]);
+            if (p.f8) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) v[k] *= nyq.row_sc * col_sc[c * CH + k];
+            }
             if (plane == 1 && p.even) {
 #pragma unroll
               for (int k = 0; k < 16; ++k)
@@ -1452,23 +1595,24 @@ extern "C" int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int
   return tiles_1sm(n1, n2, homo, row0, row1);
 }
 
-extern "C" int corr2d_contract_bf16x3(
-    const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
+extern "C" int corr2d_contract_tc(
+    int pack_kind, const void* a, const void* b, int64_t ld_pack,
     int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
   using namespace corr2d::tc;
-  if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: null pointer");
-  if (n1 < 1 || n2 < 1 || m < 2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad sizes");
-  (void)split_a;
-  (void)split_b;  // planes are interleaved per k-block (ABI v2); kept for signature stability
-  if (mp != corr2d_packed_depth(m, CORR2D_PACK_BF16X2) || ld_pack < 2 * (long long)mp + 64 || (ld_pack % 64) != 0)
+  if (pack_kind != CORR2D_PACK_BF16X2 && pack_kind != CORR2D_PACK_F16F8)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: pack_kind must be BF16X2 or F16F8");
+  const long long split_a = 0, split_b = 0;
+  if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: null pointer");
+  if (n1 < 1 || n2 < 1 || m < 2) return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: bad sizes");
+  if (mp != corr2d_packed_depth(m, pack_kind) || ld_pack < 2 * (long long)mp + 64 || (ld_pack % 64) != 0)
     return fail(CORR2D_ERR_DATA,
-                "corr2d_contract_bf16x3: packed depth / ld_pack mismatch (ld_pack >= 2*mp + 64, % 64 == 0)");
-  if (row0 < 0 || row1 > n1 || row0 >= row1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad row range");
-  if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: ld_out < n2");
-  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: homo needs n1 == n2");
+                "corr2d_contract_tc: packed depth / ld_pack mismatch (ld_pack >= 2*mp + 64, % 64 == 0)");
+  if (row0 < 0 || row1 > n1 || row0 >= row1) return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: bad row range");
+  if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: ld_out < n2");
+  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: homo needs n1 == n2");
   if (row0 % BM != 0 || (row1 != n1 && row1 % BM != 0))
-    return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: row shard bounds must be multiples of 128 (or n1)");
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: row shard bounds must be multiples of 128 (or n1)");
   // TMA stores need 16-byte aligned planes and a leading dimension that is a
   // multiple of 4 floats; otherwise the epilogue stores from registers.
   const bool aligned = (ld_out % 4 == 0) && ((reinterpret_cast<uintptr_t>(phi) & 15) == 0) &&
@@ -1499,12 +1643,13 @@ extern "C" int corr2d_contract_bf16x3(
   const long long total = variant == 2 ? tiles_quad(n1, n2, homo)
                         : (variant == 1 ? tiles_2sm(n1, n2, homo) : tiles_1sm(n1, n2, homo, row0, row1));
   if (tile1 < 0 || tile1 > total) tile1 = total;
-  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_bf16x3: bad tile range");
+  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_tc: bad tile range");
   const long long work = tile1 - tile0;
   if (work == 0) return CORR2D_OK;
   if (two_sm) {
     Params2 p{};
     p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = 1;
+    p.f8 = pack_kind == CORR2D_PACK_F16F8;
     const char* sp = getenv("CORR2D_STORE_POLICY");
     p.store_pol = sp ? atoi(sp) : 0;
     const char* dbg = getenv("CORR2D_DEBUG_SKIP");
@@ -1522,7 +1667,7 @@ extern "C" int corr2d_contract_bf16x3(
     p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
     p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
     const int csize = 2 * variant;  // CTAs per cluster
-    auto kern = variant == 2 ? contract_bf16x3_2sm_kernel<2> : contract_bf16x3_2sm_kernel<1>;
+    auto kern = variant == 2 ? contract_tc_2sm_kernel<2> : contract_tc_2sm_kernel<1>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2_BYTES);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
@@ -1558,18 +1703,29 @@ extern "C" int corr2d_contract_bf16x3(
               "wait-tempty %.0f | epi wait-tfull %.0f tmem-ld %.0f store %.0f decode %.0f preamble %.0f\n", acc[4], acc[0],
               2 * acc[1], 2 * acc[2], acc[3], acc[5], acc[6], acc[7], acc[8]);
     }
-    return check_launch(variant == 2 ? "contract_bf16x3_2sm_kernel<2>" : "contract_bf16x3_2sm_kernel<1>");
+    return check_launch(variant == 2 ? "contract_tc_2sm_kernel<2>" : "contract_tc_2sm_kernel<1>");
   }
   Params p{};
   p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = aligned ? 1 : 0;
+  p.f8 = pack_kind == CORR2D_PACK_F16F8;
   p.row0 = row0; p.row1 = row1; p.I0 = row0 / BM; p.I1 = (row1 + BM - 1) / BM; p.T = (n2 + BN - 1) / BN;
   p.tile0 = tile0;
   p.ntiles = tile1;
   p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);
   p.ld_pack = ld_pack; p.split_a = split_a; p.split_b = split_b;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
-  cudaFuncSetAttribute(contract_bf16x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+  cudaFuncSetAttribute(contract_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   const long long grid = work < sms ? work : sms;
-  contract_bf16x3_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, om, p);
-  return check_launch("contract_bf16x3_kernel");
+  contract_tc_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, st>>>(ma, mb, om, p);
+  return check_launch("contract_tc_kernel");
+}
+
+extern "C" int corr2d_contract_bf16x3(
+    const void* a, const void* b, int64_t ld_pack, int64_t split_a, int64_t split_b,
+    int n1, int n2, int mp, int m, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
+    float* phi, float* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
+  (void)split_a;
+  (void)split_b;  // planes are interleaved per k-block (ABI v2); kept for signature stability
+  return corr2d_contract_tc(CORR2D_PACK_BF16X2, a, b, ld_pack, n1, n2, mp, m, homo, row0, row1, tile0, tile1,
+                            phi, psi, ld_out, stats, stream);
 }

@@ -523,6 +523,71 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       if (p.pack_roles & CORR2D_ROLE_B) put(p.b);
     }
   }
+  // 5c. fp16 + e4m3 layout (CORR2D_PACK_F16F8, see corr2d.h): same thirds and
+  //     32-slot blocks of 128 B, [fp16 hi x 2^5 | e4m3 hi | e4m3 residual x 2^10]
+  //     of the channel scaled by its power-of-two sc; pass 1 finds max|slot|.
+  if (p.pack_kind == CORR2D_PACK_F16F8) {
+    __shared__ unsigned chmax[64];
+    const int hp = p.mp / 3;
+    const int h = even ? m / 2 : (m + 1) / 2;
+    const double sn1 = sqrt(p.norm), sn2 = sqrt(2.0 * p.norm);
+    auto slot = [&](int c, int q, float& vr, float& vi) {
+      vr = 0.f;
+      vi = 0.f;
+      if (q < h) {
+        const double2 y = channel_bin(X, q, c, m, CPc);
+        vr = (float)(y.x * (q == 0 ? sn1 : sn2));
+        vi = (float)((q == 0) ? (even ? channel_bin(X, m / 2, c, m, CPc).x * sn1 : 0.0) : y.y * sn2);
+      }
+    };
+    for (int c = tid; c < nc; c += blockDim.x) chmax[c] = 0u;
+    __syncthreads();
+    for (int idx = tid; idx < nc * h; idx += blockDim.x) {
+      const int c = idx / h, q = idx - c * h;
+      float vr, vi;
+      slot(c, q, vr, vi);
+      atomicMax(&chmax[c], max(__float_as_uint(vr) & 0x7fffffffu, __float_as_uint(vi) & 0x7fffffffu));
+    }
+    __syncthreads();
+    const int q4n = hp / 4;
+    for (int idx = tid; idx < nc * q4n; idx += blockDim.x) {
+      const int c = idx / q4n, q0 = (idx - c * q4n) * 4;
+      const int sh = f16f8_shift(chmax[c]);
+      const float sc = pow2f(sh);
+      float vr[4], vi[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) slot(c, q0 + u, vr[u], vi[u]);
+      uint32_t rh[2], ih[2];
+      uint16_t rh8[2], rl8[2], ih8[2], il8[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        f16f8_split2(vr[2 * u] * sc, vr[2 * u + 1] * sc, rh[u], rh8[u], rl8[u]);
+        f16f8_split2(vi[2 * u] * sc, vi[2 * u + 1] * sc, ih[u], ih8[u], il8[u]);
+      }
+      // byte offsets inside a third: block q0/32 at 128 B, slot i = q0 % 32 at
+      // 2i (fp16), 64 + i (e4m3 hi), 96 + i (e4m3 residual)
+      const long long row = (long long)(c0 + c) * p.ld_pack * 2;
+      const int o = (q0 >> 5) * 128 + (q0 & 31);
+      auto put = [&](void* base) {
+        uint8_t* b = static_cast<uint8_t*>(base) + row;
+        const uint32_t thr[3] = {0u, (uint32_t)(4 * hp), (uint32_t)(8 * hp)};
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3) {
+          const uint32_t n16 = t3 == 2 ? 0x80008000u : 0u, n8 = t3 == 2 ? 0x80808080u : 0u;
+          const uint32_t* h16 = t3 == 0 ? rh : ih;
+          const uint16_t* h8 = t3 == 0 ? rh8 : ih8;
+          const uint16_t* l8 = t3 == 0 ? rl8 : il8;
+          *reinterpret_cast<uint2*>(b + thr[t3] + o + (q0 & 31)) = make_uint2(h16[0] ^ n16, h16[1] ^ n16);
+          *reinterpret_cast<uint32_t*>(b + thr[t3] + o + 64) = ((uint32_t)h8[0] | ((uint32_t)h8[1] << 16)) ^ n8;
+          *reinterpret_cast<uint32_t*>(b + thr[t3] + o + 96) = ((uint32_t)l8[0] | ((uint32_t)l8[1] << 16)) ^ n8;
+        }
+        if (q0 == 0)
+          *reinterpret_cast<float4*>(b + 12 * hp) = make_float4(vr[0], vi[0], pow2f(-sh - 5), 0.f);
+      };
+      if (p.pack_roles & CORR2D_ROLE_A) put(p.a_phi);
+      if (p.pack_roles & CORR2D_ROLE_B) put(p.b);
+    }
+  }
   __syncthreads();
   mark(6);
 }
@@ -820,6 +885,103 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
 
   const int H = M / 2;
   if constexpr (BF) {
+   if (p.pack_kind == CORR2D_PACK_F16F8) {
+    // CORR2D_PACK_F16F8 row image: thirds [Re' | Im' | -Im'] of hp = H slots,
+    // 32-slot blocks of 128 B [fp16 hi x 2^5 | e4m3 hi | e4m3 residual x 2^10]
+    // of the channel scaled by its power-of-two sc (warp max first), then
+    // float4 (Re'[0], Im'[0], 2^-(s+5), 0) at 12 hp; 16-byte chunks swizzled
+    // as in the bf16 image.
+    const int hp = H;
+    const int img = 6 * hp * 2 + 128;
+    auto swz = [](int byte) { return byte ^ (((byte >> 7) & 7) << 4); };
+    const float sn1 = (float)sqrt(p.norm), sn2 = (float)sqrt(2.0 * p.norm);
+    C2 ye[R], yo[R];
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) split(k1, ye[k1], yo[k1]);
+    const float nyq0 = __shfl_sync(0xffffffffu, (float)ye[0].x, 1);
+    const float nyq1 = __shfl_sync(0xffffffffu, (float)yo[0].x, 1);
+    const int q0 = R * k2;
+    auto slot = [&](int e, int k1, float& vr, float& vi) {
+      const C2 y = e ? yo[k1] : ye[k1];
+      const int q = q0 + k1;
+      vr = (float)y.x * (q == 0 ? sn1 : sn2);
+      vi = q == 0 ? (e ? nyq1 : nyq0) * sn1 : (float)y.y * sn2;
+    };
+    uint32_t mb[2] = {0u, 0u};
+    if (q0 < H) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int k1 = 0; k1 < R; ++k1) {
+          float vr, vi;
+          slot(e, k1, vr, vi);
+          mb[e] = max(mb[e], max(__float_as_uint(vr) & 0x7fffffffu, __float_as_uint(vi) & 0x7fffffffu));
+        }
+    }
+    const int sh[2] = {f16f8_shift(__reduce_max_sync(0xffffffffu, mb[0])),
+                       f16f8_shift(__reduce_max_sync(0xffffffffu, mb[1]))};
+    if (q0 < H) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        uint8_t* rb = work + (size_t)(2 * warp + e) * img;
+        const float sc = pow2f(sh[e]);
+        __align__(16) uint32_t re_h[R / 2], im_h[R / 2];
+        __align__(16) uint16_t re_h8[R / 2], re_l8[R / 2], im_h8[R / 2], im_l8[R / 2];
+#pragma unroll
+        for (int k1 = 0; k1 < R; k1 += 2) {
+          float vr0, vi0, vr1, vi1;
+          slot(e, k1, vr0, vi0);
+          slot(e, k1 + 1, vr1, vi1);
+          f16f8_split2(vr0 * sc, vr1 * sc, re_h[k1 / 2], re_h8[k1 / 2], re_l8[k1 / 2]);
+          f16f8_split2(vi0 * sc, vi1 * sc, im_h[k1 / 2], im_h8[k1 / 2], im_l8[k1 / 2]);
+        }
+        const int blk = (q0 >> 5) * 128, i0 = q0 & 31;
+        // NB bytes from v (contiguous, NB | 16-byte chunk), optionally negated
+        auto put = [&](int off, const void* v, int nb, uint32_t neg) {
+          const uint32_t* w = static_cast<const uint32_t*>(v);
+          if (nb >= 16) {
+            for (int j = 0; j < nb / 16; ++j)
+              *reinterpret_cast<uint4*>(rb + swz(off + 16 * j)) =
+                  make_uint4(w[4 * j] ^ neg, w[4 * j + 1] ^ neg, w[4 * j + 2] ^ neg, w[4 * j + 3] ^ neg);
+          } else if (nb == 8) {
+            *reinterpret_cast<uint2*>(rb + swz(off)) = make_uint2(w[0] ^ neg, w[1] ^ neg);
+          } else if (nb == 4) {
+            *reinterpret_cast<uint32_t*>(rb + swz(off)) = w[0] ^ neg;
+          } else {
+            *reinterpret_cast<uint16_t*>(rb + swz(off)) =
+                (uint16_t)(*static_cast<const uint16_t*>(v) ^ (uint16_t)neg);
+          }
+        };
+#pragma unroll
+        for (int t3 = 0; t3 < 3; ++t3) {
+          const int tb = t3 * 4 * hp + blk;
+          const uint32_t n16 = t3 == 2 ? 0x80008000u : 0u, n8 = t3 == 2 ? 0x80808080u : 0u;
+          put(tb + 2 * i0, t3 == 0 ? re_h : im_h, 2 * R, n16);
+          put(tb + 64 + i0, t3 == 0 ? re_h8 : im_h8, R, n8);
+          put(tb + 96 + i0, t3 == 0 ? re_l8 : im_l8, R, n8);
+        }
+        if (q0 == 0) {
+          float vr, vi;
+          slot(e, 0, vr, vi);
+          *reinterpret_cast<float4*>(rb + swz(12 * hp)) = make_float4(vr, vi, pow2f(-sh[e] - 5), 0.f);
+        }
+      }
+    }
+    __syncwarp();
+    const int vec = (6 * hp * 2 + 16) / 16;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 2 * warp + e;
+      if (c >= nc) continue;
+      const uint8_t* src = work + (size_t)c * img;
+      for (int role = 0; role < 2; ++role) {
+        if (!(p.pack_roles & (role ? CORR2D_ROLE_B : CORR2D_ROLE_A))) continue;
+        uint8_t* base = static_cast<uint8_t*>(role ? p.b : p.a_phi);
+        uint4* dst = reinterpret_cast<uint4*>(base + (long long)(c0 + c) * p.ld_pack * 2);
+        for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(src + swz(16 * i));
+      }
+    }
+   } else {
     // row image: thirds [Re' | Im' | -Im'] of hp = H slots, 32-slot blocks
     // [hi 32 | lo 32], then float2 (hi + lo of Re'[0], Im'[0]) at 6 hp.  A
     // lane's R consecutive bins land as 2R contiguous bytes per (third, plane);
@@ -898,6 +1060,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
         for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(src + swz(16 * i));
       }
     }
+   }
   } else {
     // CORR2D_PACK_F64 (M <= 128): slot s < K -> Re Y(s), K <= s < m -> Im Y(s - K + 1);
     // images A_phi | A_psi | B of M doubles each
@@ -948,14 +1111,14 @@ static bool fast_eligible(const PrepParams& p) {
     if (e[0] == '0') return false;
   if (p.resample_kind != CORR2D_RESAMPLE_NONE || p.values_out || p.half_out) return false;
   if (p.m != 64 && p.m != 128 && p.m != 256 && p.m != 512) return false;
-  if (p.pack_kind == CORR2D_PACK_BF16X2) return p.mp == 3 * (p.m / 2);
+  if (p.pack_kind == CORR2D_PACK_BF16X2 || p.pack_kind == CORR2D_PACK_F16F8) return p.mp == 3 * (p.m / 2);
   return p.pack_kind == CORR2D_PACK_F64 && p.m <= 128 && p.mp == p.m;
 }
 
 static size_t fast_smem(const PrepParams& p) {
   const int M = p.m;
   const size_t raw = (size_t)kFastCh * (M + 1) * (p.in_f32 ? 4 : 8);
-  const size_t img = p.pack_kind == CORR2D_PACK_BF16X2 ? (size_t)kFastCh * (6 * (M / 2) * 2 + 128)
+  const size_t img = p.pack_kind != CORR2D_PACK_F64 ? (size_t)kFastCh * (6 * (M / 2) * 2 + 128)
                                                        : (size_t)kFastCh * 3 * M * 8;
   return (size_t)M * sizeof(double2) + (raw > img ? raw : img);
 }
@@ -973,7 +1136,7 @@ static void launch_fast_rb(const PrepParams& p, size_t smem, cudaStream_t st) {
 }
 template <int R>
 static void launch_fast_r(const PrepParams& p, size_t smem, cudaStream_t st) {
-  if (p.pack_kind == CORR2D_PACK_BF16X2) launch_fast_rb<R, true>(p, smem, st);
+  if (p.pack_kind == CORR2D_PACK_BF16X2 || p.pack_kind == CORR2D_PACK_F16F8) launch_fast_rb<R, true>(p, smem, st);
   else if constexpr (R <= 4) launch_fast_rb<R, false>(p, smem, st);   // F64 packing: m <= 128
 }
 
@@ -1025,7 +1188,7 @@ extern "C" int corr2d_fft_factors(int m, int* factors, int max_factors) {
 
 extern "C" int corr2d_packed_depth(int m, int pack_kind) {
   if (m < 2) return fail(CORR2D_ERR_DATA, "need m >= 2");
-  if (pack_kind == CORR2D_PACK_BF16X2) {
+  if (pack_kind == CORR2D_PACK_BF16X2 || pack_kind == CORR2D_PACK_F16F8) {
     const int h = (m % 2 == 0) ? m / 2 : (m + 1) / 2;
     return 3 * ((h + 31) / 32 * 32);
   }
@@ -1064,14 +1227,15 @@ extern "C" int corr2d_prep(
   p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack; p.split_plane = split_plane;
   p.values_out = values_out; p.ld_values = ld_values; p.half_out = half_out;
   p.ref_out = ref_out; p.sigma_out = sigma_out; p.status = status;
-  if (pack_kind < CORR2D_PACK_NONE || pack_kind > CORR2D_PACK_F64_TIME)
+  if (pack_kind < CORR2D_PACK_NONE || pack_kind > CORR2D_PACK_F16F8)
     return fail(CORR2D_ERR_DATA, "corr2d_prep: bad pack_kind");
-  p.do_fft = (half_out != nullptr) || (pack_kind == CORR2D_PACK_F64 || pack_kind == CORR2D_PACK_BF16X2);
+  const bool tc_pack = pack_kind == CORR2D_PACK_BF16X2 || pack_kind == CORR2D_PACK_F16F8;
+  p.do_fft = (half_out != nullptr) || pack_kind == CORR2D_PACK_F64 || tc_pack;
   if (pack_kind != CORR2D_PACK_NONE) {
     p.mp = corr2d_packed_depth(m, pack_kind);
-    if (pack_kind == CORR2D_PACK_BF16X2) {
+    if (tc_pack) {
       if (ld_pack < 2 * (long long)p.mp + 64 || ld_pack % 64)
-        return fail(CORR2D_ERR_DATA, "corr2d_prep: bf16 ld_pack must be >= 2 * packed depth + 64 and a multiple of 64");
+        return fail(CORR2D_ERR_DATA, "corr2d_prep: bf16 / f16f8 ld_pack must be >= 2 * packed depth + 64 and a multiple of 64");
     } else if (ld_pack < p.mp) {
       return fail(CORR2D_ERR_DATA, "corr2d_prep: ld_pack < packed depth");
     }

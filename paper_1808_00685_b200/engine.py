@@ -13,6 +13,7 @@ status words into the reference's exceptions and copies results to the host.
 
 from __future__ import annotations
 
+import os
 import warnings
 from dataclasses import dataclass
 
@@ -23,6 +24,18 @@ from .engine_core import channel_chunk, gather_rows
 from .errors import DataError, NumericError
 
 _torch = None
+
+
+def fp32_pack_kind() -> int:
+    """Operand format of the float32 (tensor-core) path: CORR2D_PACK_F16F8
+    (fp16 hi.hi + e4m3 cross terms, default) or CORR2D_PACK_BF16X2 (bf16x3);
+    CORR2D_FP32_FORMAT=bf16x3 selects the latter (include/corr2d.h)."""
+    fmt = os.environ.get("CORR2D_FP32_FORMAT", "f16f8").lower()
+    if fmt == "bf16x3":
+        return _abi.PACK_BF16X2
+    if fmt == "f16f8":
+        return _abi.PACK_F16F8
+    raise DataError(f"CORR2D_FP32_FORMAT must be f16f8 or bf16x3, got {fmt!r}")
 
 
 def torch():
@@ -278,7 +291,7 @@ class CorrelationPlan:
         elif self.dtype == np.float64:
             self.pack_kind, odt, pdt = _abi.PACK_F64, t.float64, t.float64
         elif self.dtype == np.float32:
-            self.pack_kind, odt, pdt = _abi.PACK_BF16X2, t.float32, t.bfloat16
+            self.pack_kind, odt, pdt = fp32_pack_kind(), t.float32, t.bfloat16
         else:
             raise DataError(f"unsupported compute dtype {dtype}")
         self.mp = self.lib.corr2d_packed_depth(self.m, self.pack_kind)
@@ -287,7 +300,7 @@ class CorrelationPlan:
         self.row0, self.row1 = (0, self.n1) if rows is None else (int(rows[0]), int(rows[1]))
         # tile-range partition of the (shard's) tile enumeration; -1 = to the end
         self.tile0, self.tile1 = (0, -1) if tiles is None else (int(tiles[0]), int(tiles[1]))
-        bf16 = self.pack_kind == _abi.PACK_BF16X2
+        bf16 = self.pack_kind in (_abi.PACK_BF16X2, _abi.PACK_F16F8)
         # row pitch of the packed operands: bf16 rows carry hi and lo of every
         # slot, interleaved per 32-slot block, then the fp32 DC / Nyquist pair
         # in a 128-byte pad (include/corr2d.h)
@@ -365,7 +378,7 @@ class CorrelationPlan:
     def launch_prep_only(self):
         lib = self.lib
         roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
-        if self.pack_kind == _abi.PACK_BF16X2 and self.homo:
+        if self.pack_kind in (_abi.PACK_BF16X2, _abi.PACK_F16F8) and self.homo:
             roles1 = _abi.ROLE_A
         if self.shard is not None:
             self._prep_sharded(self.raw1, self.recipe1, self.n1, roles1, self.a_phi, self.a_psi,
@@ -425,8 +438,8 @@ class CorrelationPlan:
                 homo, self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi),
                 self.n2, ptr(self.stats), stream_handle())
         else:
-            code = lib.corr2d_contract_bf16x3(
-                ptr(self.a_phi), ptr(self.bop), self.ld_pack, 0, 0, self.n1, self.n2, self.mp, self.m, homo,
+            code = lib.corr2d_contract_tc(
+                self.pack_kind, ptr(self.a_phi), ptr(self.bop), self.ld_pack, self.n1, self.n2, self.mp, self.m, homo,
                 self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
                 ptr(self.stats), stream_handle())
         _abi.check(code, lib)

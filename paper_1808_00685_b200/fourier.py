@@ -10,7 +10,7 @@ GPU execution: K1 (``corr2d_prep``) computes the DFT of every channel in
 shared memory and packs the half spectrum into an exact real contraction of
 depth m (weights and Norm folded into the row operand); K2
 (``corr2d_contract_f64`` on the FP64 tensor pipe, or
-``corr2d_contract_bf16x3`` on tcgen05 for ``dtype="float32"``) writes the
+``corr2d_contract_tc`` on tcgen05 for ``dtype="float32"``) writes the
 sync / async planes directly -- no complex intermediate, no concatenate, no
 Re/Im split copies, no O(n^2) host validation.  ``workers`` keeps its
 reference meaning of host threads; results are identical for every value.

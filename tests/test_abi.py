@@ -45,16 +45,18 @@ def test_sm100a_cubin_present():
 
 def test_host_helpers():
     lib = _abi.load()
-    assert lib.corr2d_abi_version() == 2
+    assert lib.corr2d_abi_version() == 3
     assert lib.corr2d_packed_depth(11, _abi.PACK_F64) == 12
     assert lib.corr2d_packed_depth(64, _abi.PACK_F64) == 64
     assert lib.corr2d_packed_depth(512, _abi.PACK_BF16X2) == 768   # [Re' | Im' | -Im'], 256 each
     assert lib.corr2d_packed_depth(37, _abi.PACK_BF16X2) == 96
+    assert lib.corr2d_packed_depth(512, _abi.PACK_F16F8) == 768     # same slots, fp16 + e4m3 bytes
     # tile enumerations: fp64 64-tiles upper triangle; bf16 whole map = CTA-pair tiles
     assert lib.corr2d_contract_tile_count(_abi.PACK_F64, 16384, 16384, 1, 0, 16384, 16384) == 256 * 257 // 2
     T, P = 256, 128
     assert lib.corr2d_contract_tile_count(_abi.PACK_BF16X2, 32768, 32768, 1, 0, 32768, 32768) == P * T - P * (P - 1)
     assert lib.corr2d_contract_tile_count(_abi.PACK_BF16X2, 32768, 32768, 1, 0, 16384, 32768) == 128 * 256 - 128 * 127 // 2
+    assert lib.corr2d_contract_tile_count(_abi.PACK_F16F8, 32768, 32768, 1, 0, 32768, 32768) == P * T - P * (P - 1)
     buf = (ctypes.c_int * 24)()
     k = lib.corr2d_fft_factors(512, buf, 24)
     assert list(buf[:k]) == [8, 8, 8]

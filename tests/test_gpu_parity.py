@@ -217,7 +217,12 @@ def test_row_shards_bit_identical_to_full():
             assert np.array_equal(sh.asyn.cpu().numpy(), full.asyn[r0:r1])
 
 
-def test_fp32_path_small():
+FP32_FORMATS = ("f16f8", "bf16x3")     # CORR2D_FP32_FORMAT: operand formats of the tensor-core path
+
+
+@pytest.mark.parametrize("fmt", FP32_FORMATS)
+def test_fp32_path_small(fmt, monkeypatch):
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
     rng = np.random.default_rng(11)
     for m, n in [(64, 300), (512, 200), (37, 129)]:
         v = rng.normal(size=(m, n))
@@ -229,9 +234,11 @@ def test_fp32_path_small():
         assert np.array_equal(res.sync, res.sync.T) and np.array_equal(res.asyn, -res.asyn.T)
 
 
-def test_fp32_tile_ranges_and_both_tensor_core_kernels(monkeypatch):
+@pytest.mark.parametrize("fmt", FP32_FORMATS)
+def test_fp32_tile_ranges_and_both_tensor_core_kernels(fmt, monkeypatch):
     """Tile-range partition (multi-GPU unit) is bit-identical to the whole map,
     for the 2-SM (CTA pair) kernel and the 1-SM kernel; both match the oracle."""
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
     from paper_1808_00685_b200 import engine
     from paper_1808_00685_b200.engine_core import tile_range
     rng = np.random.default_rng(21)
@@ -261,10 +268,12 @@ def test_fp32_tile_ranges_and_both_tensor_core_kernels(monkeypatch):
         assert np.array_equal(plan.psi.cpu().numpy(), full.asyn)
 
 
+@pytest.mark.parametrize("fmt", FP32_FORMATS)
 @pytest.mark.parametrize("n1,n2,m", [(300, 257, 64), (129, 1000, 37), (700, 65, 512), (5, 3, 2), (1025, 511, 21)])
-def test_fp32_hetero_ragged(n1, n2, m):
-    """bf16x3 path, hetero: CTA-pair kernel for aligned planes, the register-store
+def test_fp32_hetero_ragged(n1, n2, m, fmt, monkeypatch):
+    """Tensor-core path, hetero: CTA-pair kernel for aligned planes, the register-store
     epilogue for n2 % 4 != 0, odd / even m, tiny and ragged shapes."""
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
     rng = np.random.default_rng(n1 * 7 + n2 * 13 + m)
     v1 = rng.normal(size=(m, n1))
     v2 = rng.normal(size=(m, n2))
@@ -277,9 +286,11 @@ def test_fp32_hetero_ragged(n1, n2, m):
     assert rel_err(res.sync, s, sc) <= TOL32 and rel_err(res.asyn, a, sc) <= TOL32
 
 
-def test_fp32_row_shards_match_whole_map():
+@pytest.mark.parametrize("fmt", FP32_FORMATS)
+def test_fp32_row_shards_match_whole_map(fmt, monkeypatch):
     """Row shards (the 1-SM kernel with transpose-only tiles) reproduce the
     whole fp32 map bit for bit."""
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
     from paper_1808_00685_b200.engine_core import tile_aligned_blocks
     v = np.random.default_rng(8).normal(size=(96, 600))
     d = dyn_from_values(v)
@@ -297,3 +308,32 @@ def test_fp32_row_shards_match_whole_map():
     s, a, _ = O.correlate_ft(v)
     sc = scale_of(s, a)
     assert rel_err(full.sync.cpu().numpy(), s, sc) <= TOL32 and rel_err(whole1, s, sc) <= TOL32
+
+
+@pytest.mark.parametrize("fmt", FP32_FORMATS)
+@pytest.mark.parametrize("m", [64, 96, 512])
+def test_fp32_channel_dynamic_range(fmt, m, monkeypatch):
+    """Channels spanning 24 decades plus an all-zero pair: the per-channel
+    power-of-two operand scale (F16F8) keeps every block of the map accurate
+    relative to its OWN magnitude, not only to max|sync|; zero channels give
+    exact zeros.  Magnitudes are shared by channel pairs (2k, 2k+1): K1's fp32
+    path transforms a pair as one complex FFT, so a channel's error floor is
+    ~2^-24 of its partner's magnitude."""
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
+    rng = np.random.default_rng(m)
+    n = 300
+    v = rng.normal(size=(m, n))
+    mag = np.repeat(10.0 ** rng.uniform(-12, 12, size=n // 2), 2)
+    v *= mag
+    v[:, 6:8] = 0.0
+    res = P.correlate_ft(dyn_from_values(v), dtype="float32")
+    s, a, _ = O.correlate_ft(v)
+    sc = scale_of(s, a)
+    assert rel_err(res.sync, s, sc) <= TOL32 and rel_err(res.asyn, a, sc) <= TOL32
+    assert not res.sync[7].any() and not res.asyn[7].any()
+    # every element against the product of its two channels' own scales
+    own = np.sqrt(np.abs(np.diag(s)))
+    denom = np.outer(own, own)
+    denom[denom == 0] = 1.0
+    assert np.max(np.abs(res.sync - s) / denom) <= TOL32
+    assert np.max(np.abs(res.asyn - a) / denom) <= TOL32

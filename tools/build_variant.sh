@@ -14,5 +14,5 @@ for src in paper_1808_00685_b200/csrc/*.cu; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o _variants/libcorr2d_$name.so "${objs[@]}" -cudart static
-grep -A2 "2sm_kernelILi1" $out/contract_bf16x3.ptxas.txt | grep -E "registers|spill" | head -2
+grep -A2 "2sm_kernelILi1" $out/contract_tc.ptxas.txt | grep -E "registers|spill" | head -2
 echo _variants/libcorr2d_$name.so
