@@ -1058,10 +1058,34 @@ __device__ __forceinline__ void umma2_commit_mask(uint64_t* bar, uint16_t mask) 
 // Even-m Nyquist x DC correction operands of one pair tile for one epilogue
 // lane: its row (re0, im0) and the columns j0 + lane + 32 c (c < 4).  Loaded a
 // tile ahead so the L2 latency is hidden behind the previous tile's stores.
+#ifndef CORR2D_PAIR_COLSMEM
+#define CORR2D_PAIR_COLSMEM 1
+#endif
 struct NyqOperands {
   // raw loads; consumed only in finish(), so they are not waited on where issued
   float4 rw, cl[4];
   float row_re0, row_im0, row_sc, cre4[4], cim4[4], csc4[4];
+  // CORR2D_PAIR_COLSMEM: each epilogue thread loads ONE column (j0 + eid) of the
+  // tile; the CTA publishes the 128 columns in shared memory once per tile
+  __device__ __forceinline__ void load_col(const Params2& p, int gi, int j0, int eid) {
+    rw = make_float4(0.f, 0.f, 0.f, 0.f);
+    cl[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!p.even && !p.f8) return;
+    const int gj = j0 + eid;
+    if (p.f8) {
+      if (gi < p.n1) rw = dc_nyq_sc(p.a, gi, p.ld_pack, p.hp);
+      if (gj < p.n2) cl[0] = dc_nyq_sc(p.b, gj, p.ld_pack, p.hp);
+      return;
+    }
+    if (gi < p.n1) {
+      const float2 d = dc_nyq(p.a, gi, p.ld_pack, p.hp);
+      rw = make_float4(d.x, d.y, 0.f, 0.f);
+    }
+    if (gj < p.n2) {
+      const float2 d = dc_nyq(p.b, gj, p.ld_pack, p.hp);
+      cl[0] = make_float4(d.x, d.y, 0.f, 0.f);
+    }
+  }
   __device__ __forceinline__ void load(const Params2& p, int gi, int j0, int lane) {
     rw = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
@@ -1289,7 +1313,8 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
     if (p.tile0 + cid < p.tile1) {
       if (NPAIR == 1) walk.get(p, rank, P, J, mode);
       else cluster_tile<NPAIR>(p, p.tile0 + cid, rank, P, J, mode);
-      nyq_next.load(p, (2 * P + (int)prank) * BM + r, J * BN, lane);
+      if (CORR2D_PAIR_COLSMEM) nyq_next.load_col(p, (2 * P + (int)prank) * BM + r, J * BN, eid);
+      else nyq_next.load(p, (2 * P + (int)prank) * BM + r, J * BN, lane);
     }
     for (long long t = p.tile0 + cid; t < p.tile1; t += ncl) {
       const long long tp0 = tr ? clock64() : 0;
@@ -1302,7 +1327,10 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         walk.advance((int)ncl);
         if (NPAIR == 1) walk.get(p, rank, P, J, mode);
         else cluster_tile<NPAIR>(p, t + ncl, rank, P, J, mode);
-        if (mode != kSkip) nyq_next.load(p, (2 * P + (int)prank) * BM + r, J * BN, lane);
+        if (mode != kSkip) {
+          if (CORR2D_PAIR_COLSMEM) nyq_next.load_col(p, (2 * P + (int)prank) * BM + r, J * BN, eid);
+          else nyq_next.load(p, (2 * P + (int)prank) * BM + r, J * BN, lane);
+        }
       }
       if (tr) tr_dec += clock64() - tp0;
       if (cur_mode != kSkip) {
@@ -1313,7 +1341,15 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         // shuffles -- no CTA-wide barrier on the common path
         nyq.finish();
         const float row_re0 = nyq.row_re0, row_im0 = nyq.row_im0;
-        if (p.even || p.f8) {
+        if (CORR2D_PAIR_COLSMEM && (p.even || p.f8)) {
+          // publish this tile's column operands (one column per epilogue thread);
+          // the first barrier retires the previous tile's readers
+          epi_bar256();
+          col_re0[eid] = nyq.cre4[0];
+          col_im0[eid] = nyq.cim4[0];
+          col_sc[eid] = nyq.csc4[0];
+          epi_bar256();
+        } else if (p.even || p.f8) {
           if (!use_tma) {
             const int gj = j0 + eid;
             float cre = 0.f, cim = 0.f, csc = 0.f;
@@ -1365,6 +1401,37 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
               float v[CH2];
 #pragma unroll
               for (int k = 0; k < CH2; ++k) v[k] = __uint_as_float(ua[k]);
+              if (CORR2D_PAIR_COLSMEM) {
+                // column operands from shared memory: broadcast LDS.128, packed
+                // f32x2 arithmetic
+                if (p.f8) {   // undo the F16F8 operand scales: 2^-(s_i+5) 2^-(s_j+5)
+                  const float4* cs4 = reinterpret_cast<const float4*>(col_sc + c * CH2);
+                  const float2 rs = make_float2(nyq.row_sc, nyq.row_sc);
+#pragma unroll
+                  for (int k4 = 0; k4 < CH2 / 4; ++k4) {
+                    const float4 sc = cs4[k4];
+                    float2 a = __fmul2_rn(make_float2(v[4 * k4], v[4 * k4 + 1]), make_float2(sc.x, sc.y));
+                    float2 b = __fmul2_rn(make_float2(v[4 * k4 + 2], v[4 * k4 + 3]), make_float2(sc.z, sc.w));
+                    a = __fmul2_rn(a, rs);
+                    b = __fmul2_rn(b, rs);
+                    v[4 * k4] = a.x; v[4 * k4 + 1] = a.y; v[4 * k4 + 2] = b.x; v[4 * k4 + 3] = b.y;
+                  }
+                }
+                if (plane == 1 && p.even) {
+                  const float4* cr4 = reinterpret_cast<const float4*>(col_re0 + c * CH2);
+                  const float4* ci4 = reinterpret_cast<const float4*>(col_im0 + c * CH2);
+                  const float2 nim = make_float2(-row_im0, -row_im0), re = make_float2(row_re0, row_re0);
+#pragma unroll
+                  for (int k4 = 0; k4 < CH2 / 4; ++k4) {
+                    const float4 cr = cr4[k4], ci = ci4[k4];
+                    float2 a = __ffma2_rn(nim, make_float2(cr.x, cr.y), make_float2(v[4 * k4], v[4 * k4 + 1]));
+                    float2 b = __ffma2_rn(nim, make_float2(cr.z, cr.w), make_float2(v[4 * k4 + 2], v[4 * k4 + 3]));
+                    a = __ffma2_rn(re, make_float2(ci.x, ci.y), a);
+                    b = __ffma2_rn(re, make_float2(ci.z, ci.w), b);
+                    v[4 * k4] = a.x; v[4 * k4 + 1] = a.y; v[4 * k4 + 2] = b.x; v[4 * k4 + 3] = b.y;
+                  }
+                }
+              } else {
               const int c4 = (c * CH2) >> 5, l0 = (c * CH2) & 31;
               float cr = nyq.cre4[0], ci = nyq.cim4[0], cs = nyq.csc4[0];
               if (c4 == 1) { cr = nyq.cre4[1]; ci = nyq.cim4[1]; cs = nyq.csc4[1]; }
@@ -1378,6 +1445,7 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
 #pragma unroll
                 for (int k = 0; k < CH2; ++k)
                   v[k] -= row_im0 * __shfl_sync(0xffffffffu, cr, l0 + k) - row_re0 * __shfl_sync(0xffffffffu, ci, l0 + k);
+              }
               }
               {
                 // max |v| and the finite check in one integer-max tree: |v|'s
