@@ -17,7 +17,7 @@ CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 $CMD > $OUT/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/launches_cfg5.csv $CMD > $OUT/ncu_launch.log 2>&1
 # 3. full captures: contraction + K1 on cfg5 and cfg3, the peak scan on cfg5
-ncu --set full --clock-control none --import-source on -k regex:"contract_tc|prep_fast" -c 2 -o $OUT/full_cfg5 $CMD > $OUT/ncu_full5.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"contract_tc_2sm|prep_fast" -c 2 -o $OUT/full_cfg5 $CMD > $OUT/ncu_full5.log 2>&1
 CMD3="python bench.py --config 3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 $CMD3 > $OUT/plain3.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"contract_f64|prep_fast" -c 2 -o $OUT/full_cfg3 $CMD3 > $OUT/ncu_full3.log 2>&1

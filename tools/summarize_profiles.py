@@ -163,8 +163,8 @@ def readme(rnd, dst):
     L.append("")
     L.append("* roofline frac = algorithmic work / K2 time / measured peak (MEASURED_PEAKS.json). fp64 configs "
              "exceed 1.0 because the homo map is computed once per mirrored tile pair (algorithmic flops count "
-             "the full map); executed frac counts the flops the kernel actually issues (bf16x3: three MMA "
-             "products, padded K).")
+             "the full map); executed frac counts the flops the kernel actually issues, in fp16-equivalents (F16F8: the "
+             "fp16 hi.hi product + two e4m3 cross products at twice the rate = 2; bf16x3: 3).")
     ref = _load(dst / f"{rnd}_bench_reference_cfg5.json")
     if ref and b5:
         L.append(f"* Reference arm ({ref['cpu_baseline']['kind']} on {ref['cpu_baseline']['cores']} host threads, "
