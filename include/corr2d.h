@@ -134,8 +134,8 @@ int corr2d_prep(
  * so sync is exactly symmetric and async exactly skew-symmetric with a zero
  * diagonal (dataset.py:159-170).  stats (device uint64[3], reset on the
  * stream by this call) receives
- * [0] = max|sync| and [1] = max|async| as IEEE bits (uint64), [2] = count of
- * non-finite outputs (engine_core.py:139-140).
+ * [0] = max|sync| and [1] = max|async| as IEEE bits (uint64), [2] = nonzero iff
+ * an output is non-finite (the number of flagging threads; engine_core.py:139-140).
  */
 int corr2d_contract_f64(
     const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,

@@ -118,12 +118,22 @@ __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int
 // homo tiles above the diagonal; fused max|.| / finite check into p.stats.
 // direct_done: the direct tile was already written from registers by the
 // caller, whose max / finite partials come in through mphi0 / mpsi0 / bad0.
+// max|x| and the finite check on the INTEGER pipe: |x|'s bit pattern orders
+// like |x| and Inf / NaN patterns exceed every finite one.  (fp64 fmax / fabs /
+// isfinite would queue on the FP64 pipe behind the DMMAs of the co-resident CTAs.)
+constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
+__device__ __forceinline__ unsigned long long absbits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
+}
+__device__ __forceinline__ double dneg(double x) {   // sign flip as an integer op
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
+}
+
 __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, int i0, int j0,
                                            const double* Cphi, const double* Cpsi, int tid, int nthreads,
-                                           int lane, bool direct_done = false, double mphi0 = 0.0,
-                                           double mpsi0 = 0.0, int bad0 = 0) {
-  double mphi = mphi0, mpsi = mpsi0;
-  int bad = bad0;
+                                           int lane, bool direct_done = false, unsigned long long bphi0 = 0,
+                                           unsigned long long bpsi0 = 0) {
+  unsigned long long bphi = bphi0, bpsi = bpsi0;
   for (int idx = tid; idx < kBM * kBN; idx += nthreads) {
     if (mode == kTransOnly || direct_done) break;
     const int r = idx >> 6, c = idx & 63;
@@ -134,7 +144,7 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
       if (r <= c) { vphi = Cphi[r * kCS + c]; } else { vphi = Cphi[c * kCS + r]; }
       if (r < c) vpsi = Cpsi[r * kCS + c];
       else if (r == c) vpsi = 0.0;
-      else vpsi = -Cpsi[c * kCS + r];
+      else vpsi = dneg(Cpsi[c * kCS + r]);
     } else {
       vphi = Cphi[r * kCS + c];
       vpsi = Cpsi[r * kCS + c];
@@ -142,9 +152,8 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
     const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
     __stcs(p.phi + o, vphi);
     __stcs(p.psi + o, vpsi);
-    mphi = fmax(mphi, fabs(vphi));
-    mpsi = fmax(mpsi, fabs(vpsi));
-    bad += !(isfinite(vphi) && isfinite(vpsi));
+    bphi = max(bphi, absbits(vphi));
+    bpsi = max(bpsi, absbits(vpsi));
   }
   if (mode == kMirror || mode == kTransOnly) {
     // out[j][i] = sync[i][j], -async[i][j] for the tile below the diagonal
@@ -153,16 +162,18 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
       const int gi = j0 + rr, gj = i0 + cc;
       if (gi >= p.row1 || gj >= p.n2 || gi < p.row0) continue;
       const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
-      const double vphi = Cphi[cc * kCS + rr], vpsi = -Cpsi[cc * kCS + rr];
+      const double vphi = Cphi[cc * kCS + rr], vpsi = dneg(Cpsi[cc * kCS + rr]);
       __stcs(p.phi + o, vphi);
       __stcs(p.psi + o, vpsi);
       if (mode == kTransOnly) {
-        mphi = fmax(mphi, fabs(vphi));
-        mpsi = fmax(mpsi, fabs(vpsi));
-        bad += !(isfinite(vphi) && isfinite(vpsi));
+        bphi = max(bphi, absbits(vphi));
+        bpsi = max(bpsi, absbits(vpsi));
       }
     }
   }
+  int bad = (bphi >= kInfBits) + (bpsi >= kInfBits);   // lanes holding a non-finite value
+  double mphi = __longlong_as_double((long long)min(bphi, kInfBits));
+  double mpsi = __longlong_as_double((long long)min(bpsi, kInfBits));
   mphi = warp_max(mphi);
   mpsi = warp_max(mpsi);
   bad = warp_sum(bad);
@@ -214,7 +225,9 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
     const int vec = kc / 2;              // 16-byte chunks per row
     if (k0 > 0) __syncthreads();
     for (int idx = tid; idx < kBM * vec; idx += kThreads) {
-      const int r = idx / vec, v = idx - r * vec;
+      // full chunks: vec = kKC / 2 is a power of two (shifts, not a division)
+      const int r = kc == kKC ? idx / (kKC / 2) : idx / vec;
+      const int v = idx - r * vec;
       const int gi = i0 + r, gj = j0 + r;
       const bool va = gi < p.n1, vb = gj < p.n2;
       const long long oa = (long long)(va ? gi : 0) * p.ld_pack + k0 + 2 * v;
@@ -254,8 +267,7 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
   //      are staged in shared memory for the transposed mirror and for the
   //      symmetrised diagonal tiles, then written as coalesced rows ----
   const bool reg_direct = p.vec_direct && (mode == kPlain || mode == kMirror);
-  double dphi = 0.0, dpsi = 0.0;
-  int dbad = 0;
+  unsigned long long dphi = 0, dpsi = 0;
   if (reg_direct) {
 #pragma unroll
     for (int mt = 0; mt < kMT; ++mt)
@@ -272,19 +284,17 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
           if (gj + 1 < p.n2) {
             __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
             __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
-            dphi = fmax(dphi, fmax(fabs(f0), fabs(f1)));
-            dpsi = fmax(dpsi, fmax(fabs(s0), fabs(s1)));
-            dbad += !(isfinite(f0) && isfinite(f1) && isfinite(s0) && isfinite(s1));
+            dphi = max(dphi, max(absbits(f0), absbits(f1)));
+            dpsi = max(dpsi, max(absbits(s0), absbits(s1)));
           } else {
             __stcs(p.phi + o, f0);
             __stcs(p.psi + o, s0);
-            dphi = fmax(dphi, fabs(f0));
-            dpsi = fmax(dpsi, fabs(s0));
-            dbad += !(isfinite(f0) && isfinite(s0));
+            dphi = max(dphi, absbits(f0));
+            dpsi = max(dpsi, absbits(s0));
           }
         }
     if (mode == kPlain) {       // nothing left to stage
-      write_tile(p, kPlain, i0, j0, nullptr, nullptr, tid, kThreads, lane, true, dphi, dpsi, dbad);
+      write_tile(p, kPlain, i0, j0, nullptr, nullptr, tid, kThreads, lane, true, dphi, dpsi);
       return;
     }
   }
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
     }
   __syncthreads();
 
-  write_tile(p, mode, i0, j0, Cphi, Cpsi, tid, kThreads, lane, reg_direct, dphi, dpsi, dbad);
+  write_tile(p, mode, i0, j0, Cphi, Cpsi, tid, kThreads, lane, reg_direct, dphi, dpsi);
 }
 
 }  // namespace corr2d
