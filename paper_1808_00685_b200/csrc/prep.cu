@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
       const TIN* v = reinterpret_cast<const TIN*>(&buf[u]);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        bad += !isfinite((double)v[e]);
+        bad += !isfinite(v[e]);
         raw_s[(g * V + e) * (M + 1) + r] = v[e];
       }
     }
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
       TIN v = (TIN)0;
       if (c < nc) {
         v = raw[(long long)r * p.ld_raw + c0 + c];
-        bad += !isfinite((double)v);
+        bad += !isfinite(v);
       }
       raw_s[c * (M + 1) + r] = v;
     }
@@ -877,8 +877,10 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
   const int src0 = (int)(__brev((unsigned)((32 - k2) & 31)) >> 27);
   auto split = [&](int k1, C2& ye, C2& yo) {
     const C2 zr = k1 == 0 ? shfl_c(z[0], src0) : shfl_xor_c(z[R - k1], 31);
-    ye = cmake<C2>(0.5 * ((double)z[k1].x + (double)zr.x), 0.5 * ((double)z[k1].y - (double)zr.y));
-    yo = cmake<C2>(0.5 * ((double)z[k1].y + (double)zr.y), -0.5 * ((double)z[k1].x - (double)zr.x));
+    // (a + b) / 2 rounds the same in the transform's own precision (halving is
+    // exact), so the fp32 path needs no fp64 round trip
+    ye = cmake<C2>((CT)0.5 * (z[k1].x + zr.x), (CT)0.5 * (z[k1].y - zr.y));
+    yo = cmake<C2>((CT)0.5 * (z[k1].y + zr.y), (CT)-0.5 * (z[k1].x - zr.x));
   };
   mark(2);
   __syncthreads();  // raw block consumed: the area now holds the packed row images
