@@ -18,11 +18,15 @@
 // reference bit-for-bit; the FFT is a mixed-radix Stockham transform.
 #include "common.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -62,6 +66,8 @@ struct PrepParams {
   int* status;
   int do_fft;
   long long* trace;        // profiling (CORR2D_PREP_TRACE=1): per-phase cycles, summed over CTAs
+  int fast_tma;            // fast kernel: persistent CTAs, raw blocks double-buffered by TMA
+  int fast_buf;            // fast kernel: bytes per block buffer (multiple of 1024)
   int C;
   int nfactors;
   int factors[kMaxFactors];
@@ -689,18 +695,57 @@ __device__ __forceinline__ float2 shfl_xor_c(float2 v, int mask) {
 
 // BF: CORR2D_PACK_BF16X2 -- the transform runs in fp32 (the spectra are then
 // split into bf16 hi + lo, ~16 bits, far below fp32's rounding), else fp64.
+// --- TMA / mbarrier helpers of the persistent fast kernel
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void fast_mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fast_mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "FAST_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra FAST_DONE;\n\t"
+      "bra FAST_WAIT;\n\t"
+      "FAST_DONE:\n\t}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// raw rows [r0, M) x channels [c0, c0 + 16) of block `blk` into `dst` (row-major,
+// 16 * sizeof(TIN) bytes per row, SWIZZLE_64B for fp32 / SWIZZLE_128B for fp64)
+template <int M, typename TIN>
+__device__ __forceinline__ void fast_issue(const CUtensorMap* map, uint8_t* dst, uint64_t* bar, int blk) {
+  constexpr int BOX = M < 256 ? M : 256;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"((uint32_t)(M * kFastCh * sizeof(TIN))) : "memory");
+#pragma unroll
+  for (int r0 = 0; r0 < M; r0 += BOX)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+        ::"r"(smem_u32(dst + (size_t)r0 * kFastCh * sizeof(TIN))), "l"(reinterpret_cast<uint64_t>(map)),
+          "r"(blk * kFastCh), "r"(r0), "r"(smem_u32(bar)) : "memory");
+}
+
+// BF: tensor-core packing (CORR2D_PACK_BF16X2 / F16F8) -- the transform runs in
+// fp32 (the spectra are then split into ~16-bit operands, far below fp32's
+// rounding), else fp64.
+// p.fast_tma: persistent CTAs; each loops over 16-channel blocks, the raw block
+// of the block after next is fetched by TMA into the buffer this block has just
+// finished with, so DRAM reads overlap the statistics / FFT / packing of the
+// blocks in flight.  Otherwise one block per CTA, loaded through registers.
 template <int R, typename TIN, bool BF>
-__global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepParams p) {
+__global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepParams p,
+                                                                    const __grid_constant__ CUtensorMap rawmap) {
   constexpr int M = 32 * R;
+  constexpr int SZ = (int)sizeof(TIN);
   using C2 = typename std::conditional<BF, float2, double2>::type;
   using CT = typename std::conditional<BF, float, double>::type;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(1024) double smem[];
   C2* tw = reinterpret_cast<C2*>(smem);                               // M
-  uint8_t* work = reinterpret_cast<uint8_t*>(smem) + M * sizeof(double2);   // raw block, later row images
-  TIN* raw_s = reinterpret_cast<TIN*>(work);                           // [16][M + 1]
+  uint8_t* bufs = reinterpret_cast<uint8_t*>(smem) + M * sizeof(double2);
+  bufs += (1024u - (smem_u32(bufs) & 1023u)) & 1023u;                 // TMA swizzle alignment
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bufs + 2 * (size_t)p.fast_buf);
+  const bool tma = p.fast_tma != 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int c0 = blockIdx.x * kFastCh;
-  const int nc = min(kFastCh, p.n - c0);
+  const int nblk = (p.n + kFastCh - 1) / kFastCh;
   long long tr_t = (p.trace && tid == 0) ? clock64() : 0;
   auto mark = [&](int ph) {
     if (p.trace && tid == 0) {
@@ -710,14 +755,40 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     }
   };
 
+  if (tma && tid == 0) {
+    fast_mbar_init(&bars[0]);
+    fast_mbar_init(&bars[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&rawmap)) : "memory");
+    for (int s = 0; s < 2; ++s) {
+      const int b = blockIdx.x + s * gridDim.x;
+      if (b < nblk) fast_issue<M, TIN>(&rawmap, bufs + s * (size_t)p.fast_buf, &bars[s], b);
+    }
+  }
   for (int q = tid; q < M; q += kFastThreads) {
     double sv, cv;
     sincospi(-2.0 * (double)q / (double)M, &sv, &cv);
     tw[q] = cmake<C2>(cv, sv);
   }
+  __syncthreads();
+
+  int it = 0;
+  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+  uint8_t* work = bufs + (tma ? (it & 1) * (size_t)p.fast_buf : 0);   // raw block, later row images
+  TIN* raw_s = reinterpret_cast<TIN*>(work);                           // [16][M + 1] (register path)
+  const int c0 = blk * kFastCh;
+  const int nc = min(kFastCh, p.n - c0);
+  // sample r of channel c of the staged block (TMA: swizzled row-major rows)
+  auto raw_at = [&](int c, int r) -> double {
+    if (!tma) return (double)raw_s[c * (M + 1) + r];
+    const int byte = r * kFastCh * SZ + ((((c * SZ) >> 4) ^ (SZ == 4 ? ((r >> 1) & 3) : (r & 7))) << 4) + ((c * SZ) & 15);
+    return (double)*reinterpret_cast<const TIN*>(work + byte);
+  };
+
+  int bad = 0;
+  if (!tma) {
   // raw block, channel-major in shared memory; full aligned blocks use 16-byte
   // loads, all of a thread's loads issued before the first store
-  int bad = 0;
   const TIN* raw = static_cast<const TIN*>(p.raw);
   constexpr int V = 16 / (int)sizeof(TIN), G = kFastCh / V;      // channels per vector, vectors per row
   const bool vec = nc == kFastCh && ((reinterpret_cast<uintptr_t>(raw) & 15) == 0) &&
@@ -751,17 +822,43 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
       raw_s[c * (M + 1) + r] = v;
     }
   }
-  bad = warp_sum(bad);
-  if (lane == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
   __syncthreads();
+  } else {
+    fast_mbar_wait(&bars[it & 1], (uint32_t)(it >> 1) & 1u);
+  }
   mark(0);
 
   // this warp's channel pair, samples l + 32 t
   double xv[2][R];
+  if (tma) {
+    // the pair (2w, 2w+1) shares one 16-byte chunk: one 8 / 16-byte load per row
 #pragma unroll
-  for (int e = 0; e < 2; ++e)
+    for (int t = 0; t < R; ++t) {
+      const int r = lane + 32 * t, c = 2 * warp;
+      const int byte = r * kFastCh * SZ + ((((c * SZ) >> 4) ^ (SZ == 4 ? ((r >> 1) & 3) : (r & 7))) << 4) + ((c * SZ) & 15);
+      if constexpr (SZ == 4) {
+        const float2 v = *reinterpret_cast<const float2*>(work + byte);
+        xv[0][t] = v.x;
+        xv[1][t] = v.y;
+      } else {
+        const double2 v = *reinterpret_cast<const double2*>(work + byte);
+        xv[0][t] = v.x;
+        xv[1][t] = v.y;
+      }
+    }
 #pragma unroll
-    for (int t = 0; t < R; ++t) xv[e][t] = (double)raw_s[(2 * warp + e) * (M + 1) + lane + 32 * t];
+    for (int e = 0; e < 2; ++e)
+      if (2 * warp + e < nc)
+#pragma unroll
+        for (int t = 0; t < R; ++t) bad += !isfinite(xv[e][t]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int t = 0; t < R; ++t) xv[e][t] = (double)raw_s[(2 * warp + e) * (M + 1) + lane + 32 * t];
+  }
+  bad = warp_sum(bad);
+  if (lane == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
 
   // per-channel statistics (generic kernel's summation orders), normalisation
   const bool normalise = p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0;
@@ -770,19 +867,21 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     for (int e = 0; e < 2; ++e) {
       const int c = 2 * warp + e;
       if (c >= nc) continue;   // padding channels stay 0 (warp-uniform branch)
-      const TIN* col = raw_s + c * (M + 1);
       double ref = 0.0;
       if (p.ref_mode == CORR2D_REF_PROVIDED) {
         ref = c < nc ? __ldg(p.ref_in + c0 + c) : 0.0;
       } else if (p.ref_mode == CORR2D_REF_MEAN) {
         double sum = 0.0;
         if (M <= kSeqStatsMax) {        // numpy's axis-0 order, left to right
-          if (lane == 0) {
-            double cv[M];
+          if (lane == 0) {   // 16 loads in flight ahead of the dependent adds
 #pragma unroll
-            for (int k = 0; k < M; ++k) cv[k] = (double)col[k];
+            for (int k0 = 0; k0 < M; k0 += 16) {
+              double cv[16];
 #pragma unroll
-            for (int k = 0; k < M; ++k) sum = __dadd_rn(sum, cv[k]);
+              for (int u = 0; u < 16; ++u) cv[u] = raw_at(c, k0 + u);
+#pragma unroll
+              for (int u = 0; u < 16; ++u) sum = __dadd_rn(sum, cv[u]);
+            }
           }
           sum = __shfl_sync(0xffffffffu, sum, 0);
         } else {                        // lane partials over k = lane + 32 t, xor tree
@@ -802,14 +901,17 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
           double ss = 0.0;
           if (M <= kSeqStatsMax) {
             if (lane == 0) {
-              double dv[M];
 #pragma unroll
-              for (int k = 0; k < M; ++k) {
-                const double d = __dsub_rn((double)col[k], ref);
-                dv[k] = __dmul_rn(d, d);
+              for (int k0 = 0; k0 < M; k0 += 16) {
+                double dv[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                  const double d = __dsub_rn(raw_at(c, k0 + u), ref);
+                  dv[u] = __dmul_rn(d, d);
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) ss = __dadd_rn(ss, dv[u]);
               }
-#pragma unroll
-              for (int k = 0; k < M; ++k) ss = __dadd_rn(ss, dv[k]);
             }
             ss = __shfl_sync(0xffffffffu, ss, 0);
           } else {
@@ -1106,6 +1208,15 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     }
   }
   mark(3);
+  __syncthreads();   // row images copied out: the buffer is free
+  if (tma && tid == 0) {
+    const int nb = blk + 2 * (int)gridDim.x;
+    if (nb < nblk) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes before the TMA overwrite
+      fast_issue<M, TIN>(&rawmap, work, &bars[it & 1], nb);
+    }
+  }
+  }  // blocks of this CTA
 }
 
 static bool fast_eligible(const PrepParams& p) {
@@ -1117,24 +1228,80 @@ static bool fast_eligible(const PrepParams& p) {
   return p.pack_kind == CORR2D_PACK_F64 && p.m <= 128 && p.mp == p.m;
 }
 
-static size_t fast_smem(const PrepParams& p) {
+// bytes of one block buffer: the raw block (TMA rows or the register path's
+// channel-major copy) and, after it is consumed, the packed row images
+static int fast_buf_bytes(const PrepParams& p) {
   const int M = p.m;
-  const size_t raw = (size_t)kFastCh * (M + 1) * (p.in_f32 ? 4 : 8);
+  const size_t sz = p.in_f32 ? 4 : 8;
+  const size_t raw = (size_t)kFastCh * (M + 1) * sz;
   const size_t img = p.pack_kind != CORR2D_PACK_F64 ? (size_t)kFastCh * (6 * (M / 2) * 2 + 128)
-                                                       : (size_t)kFastCh * 3 * M * 8;
-  return (size_t)M * sizeof(double2) + (raw > img ? raw : img);
+                                                    : (size_t)kFastCh * 3 * M * 8;
+  const size_t b = raw > img ? raw : img;
+  return (int)((b + 1023) / 1024 * 1024);
+}
+
+static size_t fast_smem(const PrepParams& p) {
+  return (size_t)p.m * sizeof(double2) + 1024 + 2 * (size_t)fast_buf_bytes(p) + 16;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 prep_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// TMA map of the raw m x n block matrix: boxes of 16 channels x min(m, 256) rows
+// (64-B rows SWIZZLE_64B for fp32, 128-B rows SWIZZLE_128B for fp64); channels
+// past n read as zeros.  false when the layout does not allow TMA.
+static bool fast_raw_map(const PrepParams& p, CUtensorMap* map) {
+  const size_t sz = p.in_f32 ? 4 : 8;
+  if (const char* e = getenv("CORR2D_PREP_TMA"))
+    if (e[0] == '0') return false;
+  if ((reinterpret_cast<uintptr_t>(p.raw) & 15) || ((size_t)p.ld_raw * sz) % 16) return false;
+  auto fn = prep_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)p.n, (cuuint64_t)p.m};
+  cuuint64_t strides[1] = {(cuuint64_t)p.ld_raw * sz};
+  cuuint32_t box[2] = {(cuuint32_t)kFastCh, (cuuint32_t)(p.m < 256 ? p.m : 256)};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, p.in_f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+            const_cast<void*>(p.raw), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            p.in_f32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename K>
+static void launch_fast_kernel(K kern, PrepParams p, size_t smem, cudaStream_t st) {
+  const int nblk = (p.n + kFastCh - 1) / kFastCh;
+  CUtensorMap map;
+  memset(&map, 0, sizeof(map));
+  p.fast_buf = fast_buf_bytes(p);
+  p.fast_tma = fast_raw_map(p, &map) ? 1 : 0;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int grid = nblk;
+  if (p.fast_tma) {   // persistent: as many CTAs as fit, never more than the blocks
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFastThreads, smem) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    grid = std::min(nblk, per_sm * sms);
+  }
+  kern<<<grid, kFastThreads, smem, st>>>(p, map);
 }
 
 template <int R, bool BF>
 static void launch_fast_rb(const PrepParams& p, size_t smem, cudaStream_t st) {
-  const int grid = (p.n + kFastCh - 1) / kFastCh;
-  if (p.in_f32) {
-    cudaFuncSetAttribute(prep_fast_kernel<R, float, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    prep_fast_kernel<R, float, BF><<<grid, kFastThreads, smem, st>>>(p);
-  } else {
-    cudaFuncSetAttribute(prep_fast_kernel<R, double, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    prep_fast_kernel<R, double, BF><<<grid, kFastThreads, smem, st>>>(p);
-  }
+  if (p.in_f32) launch_fast_kernel(prep_fast_kernel<R, float, BF>, p, smem, st);
+  else launch_fast_kernel(prep_fast_kernel<R, double, BF>, p, smem, st);
 }
 template <int R>
 static void launch_fast_r(const PrepParams& p, size_t smem, cudaStream_t st) {
