@@ -68,6 +68,7 @@ struct PrepParams {
   long long* trace;        // profiling (CORR2D_PREP_TRACE=1): per-phase cycles, summed over CTAs
   int fast_tma;            // fast kernel: persistent CTAs, raw blocks double-buffered by TMA
   int fast_buf;            // fast kernel: bytes per block buffer (multiple of 1024)
+  int fast_store;          // fast kernel (tensor-core packing, TMA mode): row images leave by one TMA store
   int C;
   int nfactors;
   int factors[kMaxFactors];
@@ -733,7 +734,9 @@ __device__ __forceinline__ void fast_issue(const CUtensorMap* map, uint8_t* dst,
 // blocks in flight.  Otherwise one block per CTA, loaded through registers.
 template <int R, typename TIN, bool BF>
 __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepParams p,
-                                                                    const __grid_constant__ CUtensorMap rawmap) {
+                                                                    const __grid_constant__ CUtensorMap rawmap,
+                                                                    const __grid_constant__ CUtensorMap outA,
+                                                                    const __grid_constant__ CUtensorMap outB) {
   constexpr int M = 32 * R;
   constexpr int SZ = (int)sizeof(TIN);
   using C2 = typename std::conditional<BF, float2, double2>::type;
@@ -773,6 +776,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
   __syncthreads();
 
   int it = 0;
+  int pend_blk = -1;   // fast_store: raw load deferred until the row-image store has read its buffer
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
   uint8_t* work = bufs + (tma ? (it & 1) * (size_t)p.fast_buf : 0);   // raw block, later row images
   TIN* raw_s = reinterpret_cast<TIN*>(work);                           // [16][M + 1] (register path)
@@ -986,6 +990,13 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
   };
   mark(2);
   __syncthreads();  // raw block consumed: the area now holds the packed row images
+  if (pend_blk >= 0 && tid == 0) {
+    // the previous block's row-image store has had the statistics / FFT of this
+    // block to read its buffer; then the block after this one lands there
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    fast_issue<M, TIN>(&rawmap, bufs + ((it + 1) & 1) * (size_t)p.fast_buf, &bars[(it + 1) & 1], pend_blk);
+  }
+  pend_blk = -1;
 
   const int H = M / 2;
   if constexpr (BF) {
@@ -997,7 +1008,9 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     // as in the bf16 image.
     const int hp = H;
     const int img = 6 * hp * 2 + 128;
-    auto swz = [](int byte) { return byte ^ (((byte >> 7) & 7) << 4); };
+    // 16-byte chunks XOR-swizzled by the 128-byte line index of the whole block
+    // buffer (the TMA SWIZZLE_128B pattern of the copy-out)
+    auto aswz = [](int x) { return x ^ (((x >> 7) & 7) << 4); };
     const float sn1 = (float)sqrt(p.norm), sn2 = (float)sqrt(2.0 * p.norm);
     C2 ye[R], yo[R];
 #pragma unroll
@@ -1027,7 +1040,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     if (q0 < H) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        uint8_t* rb = work + (size_t)(2 * warp + e) * img;
+        const int rbo = (2 * warp + e) * img;
         const float sc = pow2f(sh[e]);
         __align__(16) uint32_t re_h[R / 2], im_h[R / 2];
         __align__(16) uint16_t re_h8[R / 2], re_l8[R / 2], im_h8[R / 2], im_l8[R / 2];
@@ -1045,14 +1058,14 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
           const uint32_t* w = static_cast<const uint32_t*>(v);
           if (nb >= 16) {
             for (int j = 0; j < nb / 16; ++j)
-              *reinterpret_cast<uint4*>(rb + swz(off + 16 * j)) =
+              *reinterpret_cast<uint4*>(work + aswz(rbo + off + 16 * j)) =
                   make_uint4(w[4 * j] ^ neg, w[4 * j + 1] ^ neg, w[4 * j + 2] ^ neg, w[4 * j + 3] ^ neg);
           } else if (nb == 8) {
-            *reinterpret_cast<uint2*>(rb + swz(off)) = make_uint2(w[0] ^ neg, w[1] ^ neg);
+            *reinterpret_cast<uint2*>(work + aswz(rbo + off)) = make_uint2(w[0] ^ neg, w[1] ^ neg);
           } else if (nb == 4) {
-            *reinterpret_cast<uint32_t*>(rb + swz(off)) = w[0] ^ neg;
+            *reinterpret_cast<uint32_t*>(work + aswz(rbo + off)) = w[0] ^ neg;
           } else {
-            *reinterpret_cast<uint16_t*>(rb + swz(off)) =
+            *reinterpret_cast<uint16_t*>(work + aswz(rbo + off)) =
                 (uint16_t)(*static_cast<const uint16_t*>(v) ^ (uint16_t)neg);
           }
         };
@@ -1067,12 +1080,13 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
         if (q0 == 0) {
           float vr, vi;
           slot(e, 0, vr, vi);
-          *reinterpret_cast<float4*>(rb + swz(12 * hp)) = make_float4(vr, vi, pow2f(-sh[e] - 5), 0.f);
+          *reinterpret_cast<float4*>(work + aswz(rbo + 12 * hp)) = make_float4(vr, vi, pow2f(-sh[e] - 5), 0.f);
         }
       }
     }
     __syncwarp();
     const int vec = (6 * hp * 2 + 16) / 16;
+    if (!p.fast_store)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int c = 2 * warp + e;
@@ -1082,7 +1096,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
         if (!(p.pack_roles & (role ? CORR2D_ROLE_B : CORR2D_ROLE_A))) continue;
         uint8_t* base = static_cast<uint8_t*>(role ? p.b : p.a_phi);
         uint4* dst = reinterpret_cast<uint4*>(base + (long long)(c0 + c) * p.ld_pack * 2);
-        for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(src + swz(16 * i));
+        for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(work + aswz(c * img + 16 * i));
       }
     }
    } else {
@@ -1093,7 +1107,9 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     // index (bank spread), undone by the copy-out.
     const int hp = H;
     const int img = 6 * hp * 2 + 128;
-    auto swz = [](int byte) { return byte ^ (((byte >> 7) & 7) << 4); };
+    // 16-byte chunks XOR-swizzled by the 128-byte line index of the whole block
+    // buffer (the TMA SWIZZLE_128B pattern of the copy-out)
+    auto aswz = [](int x) { return x ^ (((x >> 7) & 7) << 4); };
     const float sn1 = (float)sqrt(p.norm), sn2 = (float)sqrt(2.0 * p.norm);
     C2 ye[R], yo[R];
 #pragma unroll
@@ -1104,7 +1120,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     if (q0 < H) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        uint8_t* rb = work + (size_t)(2 * warp + e) * img;
+        const int rbo = (2 * warp + e) * img;
         __align__(16) __nv_bfloat16 re_h[R], re_l[R], im_h[R], im_l[R], ng_h[R], ng_l[R];
         // two adjacent bins per conversion instruction (F2FP pack)
 #pragma unroll
@@ -1134,24 +1150,25 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
           if constexpr (2 * R >= 16) {
 #pragma unroll
             for (int j = 0; j < 2 * R / 16; ++j)
-              *reinterpret_cast<uint4*>(rb + swz(off + 16 * j)) = reinterpret_cast<const uint4*>(v)[j];
+              *reinterpret_cast<uint4*>(work + aswz(rbo + off + 16 * j)) = reinterpret_cast<const uint4*>(v)[j];
           } else if constexpr (2 * R == 8) {
-            *reinterpret_cast<uint2*>(rb + swz(off)) = *reinterpret_cast<const uint2*>(v);
+            *reinterpret_cast<uint2*>(work + aswz(rbo + off)) = *reinterpret_cast<const uint2*>(v);
           } else {
-            *reinterpret_cast<uint32_t*>(rb + swz(off)) = *reinterpret_cast<const uint32_t*>(v);
+            *reinterpret_cast<uint32_t*>(work + aswz(rbo + off)) = *reinterpret_cast<const uint32_t*>(v);
           }
         };
         put(o, re_h); put(o + 64, re_l);
         put(4 * hp + o, im_h); put(4 * hp + o + 64, im_l);
         put(8 * hp + o, ng_h); put(8 * hp + o + 64, ng_l);
         if (q0 == 0)
-          *reinterpret_cast<float2*>(rb + swz(12 * hp)) =
+          *reinterpret_cast<float2*>(work + aswz(rbo + 12 * hp)) =
               make_float2(__bfloat162float(re_h[0]) + __bfloat162float(re_l[0]),
                           __bfloat162float(im_h[0]) + __bfloat162float(im_l[0]));
       }
     }
     __syncwarp();
     const int vec = (6 * hp * 2 + 8 + 15) / 16;      // 16-byte chunks incl. the float2 pad
+    if (!p.fast_store)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int c = 2 * warp + e;
@@ -1161,7 +1178,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
         if (!(p.pack_roles & (role ? CORR2D_ROLE_B : CORR2D_ROLE_A))) continue;
         __nv_bfloat16* base = static_cast<__nv_bfloat16*>(role ? p.b : p.a_phi);
         uint4* dst = reinterpret_cast<uint4*>(base + (long long)(c0 + c) * p.ld_pack);
-        for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(src + swz(16 * i));
+        for (int i = lane; i < vec; i += 32) dst[i] = *reinterpret_cast<const uint4*>(work + aswz(c * img + 16 * i));
       }
     }
    }
@@ -1208,15 +1225,29 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
     }
   }
   mark(3);
-  __syncthreads();   // row images copied out: the buffer is free
+  if (p.fast_store) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // images -> async proxy
+  __syncthreads();   // row images complete (copied out, or ready for the TMA store)
   if (tma && tid == 0) {
     const int nb = blk + 2 * (int)gridDim.x;
-    if (nb < nblk) {
+    if (p.fast_store) {
+      // one TMA tensor store of the block's 16 row images (box {64, L, 16},
+      // SWIZZLE_128B = the images' chunk swizzle); the buffer is reloaded once
+      // the store has read it (next iteration)
+      if (p.pack_roles & CORR2D_ROLE_A)
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                     ::"l"(reinterpret_cast<uint64_t>(&outA)), "r"(0), "r"(0), "r"(c0), "r"(smem_u32(work)) : "memory");
+      if (p.pack_roles & CORR2D_ROLE_B)
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n"
+                     ::"l"(reinterpret_cast<uint64_t>(&outB)), "r"(0), "r"(0), "r"(c0), "r"(smem_u32(work)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      if (nb < nblk) pend_blk = nb;
+    } else if (nb < nblk) {
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes before the TMA overwrite
       fast_issue<M, TIN>(&rawmap, work, &bars[it & 1], nb);
     }
   }
   }  // blocks of this CTA
+  if (p.fast_store && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
 static bool fast_eligible(const PrepParams& p) {
@@ -1276,13 +1307,41 @@ static bool fast_raw_map(const PrepParams& p, CUtensorMap* map) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// TMA map of a tensor-core packed operand array viewed as {64 x 2 B, L lines of
+// 128 B, n rows}: one box {64, L, 16} = the 16 row images of a block, in the
+// SWIZZLE_128B layout the images are written in.
+static bool fast_out_map(const PrepParams& p, void* base, CUtensorMap* map) {
+  if (!base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const int hp = p.m / 2;
+  const int L = (12 * hp + 128) / 128;
+  if (L > 256 || (long long)p.ld_pack * 2 < (long long)L * 128) return false;
+  auto fn = prep_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)L, (cuuint64_t)p.n};
+  cuuint64_t strides[2] = {128, (cuuint64_t)p.ld_pack * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)L, (cuuint32_t)kFastCh};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename K>
 static void launch_fast_kernel(K kern, PrepParams p, size_t smem, cudaStream_t st) {
   const int nblk = (p.n + kFastCh - 1) / kFastCh;
-  CUtensorMap map;
+  CUtensorMap map, oa, ob;
   memset(&map, 0, sizeof(map));
+  memset(&oa, 0, sizeof(oa));
+  memset(&ob, 0, sizeof(ob));
   p.fast_buf = fast_buf_bytes(p);
   p.fast_tma = fast_raw_map(p, &map) ? 1 : 0;
+  p.fast_store = 0;
+  if (p.fast_tma && p.pack_kind != CORR2D_PACK_F64) {
+    const char* e = getenv("CORR2D_PREP_TMA_STORE");
+    bool ok = !(e && e[0] == '0');
+    if (ok && (p.pack_roles & CORR2D_ROLE_A)) ok = fast_out_map(p, p.a_phi, &oa);
+    if (ok && (p.pack_roles & CORR2D_ROLE_B)) ok = fast_out_map(p, p.b, &ob);
+    p.fast_store = ok ? 1 : 0;
+  }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = nblk;
   if (p.fast_tma) {   // persistent: as many CTAs as fit, never more than the blocks
@@ -1295,7 +1354,7 @@ static void launch_fast_kernel(K kern, PrepParams p, size_t smem, cudaStream_t s
     }
     grid = std::min(nblk, per_sm * sms);
   }
-  kern<<<grid, kFastThreads, smem, st>>>(p, map);
+  kern<<<grid, kFastThreads, smem, st>>>(p, map, oa, ob);
 }
 
 template <int R, bool BF>
