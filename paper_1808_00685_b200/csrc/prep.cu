@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
         }
-        ref = __ddiv_rn(sum, (double)M);
+        ref = __dmul_rn(sum, 1.0 / (double)M);   // M = 32 R is a power of two: the same bits as sum / M
       }
       double scale = 1.0;
       if (p.alpha > 0.0) {
