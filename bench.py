@@ -227,7 +227,12 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 over gloo, to run
+        # the multi-rank code path on a one-GPU box (its timings mean nothing)
+        one_dev = os.environ.get("BENCH_ONE_DEVICE") == "1"
+        if one_dev:
+            local = 0
+        backend = "nccl" if torch.cuda.is_available() and not one_dev else "gloo"
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
@@ -276,24 +281,40 @@ def run_b200(args, case, wl, world, rank, local):
     #      step's events, so every timed step starts from a cold L2.
     flush = wl["out_bytes"] + wl["in_bytes"] <= 4 * 126e6
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
-    step_graph, timed_graph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
     evs = [tuple(torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)) for _ in range(args.steps)]
-    cap = torch.cuda.Stream(device=dev)
-    cap.wait_stream(stream)
-    with torch.cuda.stream(cap):
-        plan.launch()                     # settle allocator / attributes before capture
-        with torch.cuda.graph(step_graph, stream=cap):
-            plan.launch()
-        with torch.cuda.graph(timed_graph, stream=cap):
-            for a, mid, b in evs:
-                if flush:
-                    flush_buf.fill_(1)
-                a.record(cap)
-                plan.launch_prep_only()
-                mid.record(cap)
-                plan.launch_contract()
-                b.record(cap)
-    stream.wait_stream(cap)
+
+    def timed_steps(s):
+        for a, mid, b in evs:
+            if flush:
+                flush_buf.fill_(1)
+            a.record(s)
+            plan.launch_prep_only()
+            mid.record(s)
+            plan.launch_contract()
+            b.record(s)
+
+    # gloo (BENCH_ONE_DEVICE test mode) collectives stage through the host and
+    # cannot be graph-captured: that mode launches eagerly
+    import torch.distributed as dist
+    eager = world > 1 and dist.get_backend() != "nccl"
+    if eager:
+        class _Eager:
+            def __init__(self, fn):
+                self.replay = fn
+        step_graph = _Eager(plan.launch)
+        timed_graph = _Eager(lambda: timed_steps(stream))
+        plan.launch()
+    else:
+        step_graph, timed_graph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            plan.launch()                     # settle allocator / attributes before capture
+            with torch.cuda.graph(step_graph, stream=cap):
+                plan.launch()
+            with torch.cuda.graph(timed_graph, stream=cap):
+                timed_steps(cap)
+        stream.wait_stream(cap)
     torch.cuda.synchronize()
 
     def step():
@@ -516,7 +537,8 @@ def allreduce_max(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    gpu = torch.cuda.is_available() and dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if gpu else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
