@@ -65,7 +65,8 @@ constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + STG_
 // slower on cfg5 and removed: 16-slot boxes in 4 x 32 KB stages, half-k-block
 // ring slots, 16-column chunks, 8 epilogue warps, register-written mirrors, split
 // tile / mirror bulk groups, 2 stages with double-buffered staging, 16-column
-// chunks double-buffered in the same 8 KB per warp (F16F8: 2.62 vs 2.43 ms).
+// chunks double-buffered in the same 8 KB per warp (F16F8: 2.62 vs 2.43 ms),
+// tile rows stored from registers with only the mirror staged (3.09 ms).
 constexpr int KB2 = 32;
 static_assert(KB2 == KB, "operand boxes are 2*KB bf16 wide in both kernels");
 constexpr int TILE2_BYTES = BM * KB2 * 2;    // 8 KB
