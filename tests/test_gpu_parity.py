@@ -337,3 +337,30 @@ def test_fp32_channel_dynamic_range(fmt, m, monkeypatch):
     denom[denom == 0] = 1.0
     assert np.max(np.abs(res.sync - s) / denom) <= TOL32
     assert np.max(np.abs(res.asyn - a) / denom) <= TOL32
+
+
+@pytest.mark.parametrize("fmt", FP32_FORMATS)
+def test_fp32_errors_and_edge_inputs(fmt, monkeypatch):
+    """The tensor-core path raises the reference's errors (non-finite input,
+    zero-variance channel under alpha > 0, through the fast and the generic K1)
+    and maps all-zero / constant data to exact zeros; fp32 overflow of the
+    planes is reported as a non-finite output, never returned silently."""
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
+    for m in (64, 37):                       # fast K1 (m = 32 R) and generic K1
+        v = np.random.default_rng(m).normal(size=(m, 300))
+        v[3, 17] = np.inf
+        with pytest.raises(P.NumericError, match="non-finite"):
+            P.correlate_ft(dyn_from_values(v), dtype="float32")
+        raw = np.random.default_rng(m + 1).normal(size=(m, 200)).astype(np.float32)
+        raw[:, 5] = 2.5
+        ds = P.SpectralDataset(np.arange(200.0), np.arange(float(m)), raw, dtype=np.float32)
+        with pytest.raises(P.NumericError, match="zero-variance spectral channel"):
+            P.corr2d(ds, alpha=0.5, dtype="float32")
+        zero = P.correlate_ft(dyn_from_values(np.zeros((m, 150))), dtype="float32")
+        assert not zero.sync.any() and not zero.asyn.any()
+        const = P.corr2d(P.SpectralDataset(np.arange(150.0), np.arange(float(m)),
+                                           np.full((m, 150), 3.0, np.float32), dtype=np.float32), dtype="float32")
+        assert not const.sync.any() and not const.asyn.any()
+        big = np.random.default_rng(m + 2).normal(size=(m, 140)) * 1e25
+        with pytest.raises(P.NumericError, match="non-finite"):
+            P.correlate_ft(dyn_from_values(big), dtype="float32")
