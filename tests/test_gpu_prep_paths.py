@@ -56,3 +56,22 @@ def test_prep_paths_agree(monkeypatch, m, n1, n2, dtype, fmt):
     scale = float(max(np.abs(generic[0]).max(), np.abs(generic[1]).max()))
     tol = 1e-12 if dtype == "float64" else 1e-4   # fp32: both paths carry the F16F8 / bf16x3 rounding
     assert rel_err(base[0], generic[0], scale) <= tol and rel_err(base[1], generic[1], scale) <= tol
+
+
+@pytest.mark.parametrize("m,n1,n2,alpha", [(11, 1000, None, 0.0), (21, 2000, 1500, 0.0), (5, 33, 17, 0.5),
+                                           (32, 301, None, 1.0), (2, 40, None, 0.5)])
+def test_small_m_path_matches_generic(monkeypatch, m, n1, n2, alpha):
+    """m <= 32 fp64 (cfg1 / cfg2 shapes): the warp-per-channel-pair K1 against the
+    generic kernel -- statistics bit-identical (same sequential operations), maps
+    within 1e-13 (a direct DFT instead of the Stockham stages)."""
+    def run(env):
+        monkeypatch.delenv("CORR2D_PREP_SMALL", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        d1 = _ds(m, n1, 3 + m, "float64")
+        d2 = None if n2 is None else _ds(m, n2, 4 + m, "float64")
+        return P.corr2d(d1, d2, alpha=alpha)
+    small, generic = run({}), run({"CORR2D_PREP_SMALL": "0"})
+    assert np.array_equal(small.ref1, generic.ref1) and np.array_equal(small.ref2, generic.ref2)
+    scale = float(max(np.abs(generic.sync).max(), np.abs(generic.asyn).max()))
+    assert rel_err(small.sync, generic.sync, scale) <= 1e-13 and rel_err(small.asyn, generic.asyn, scale) <= 1e-13
