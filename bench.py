@@ -395,7 +395,7 @@ def run_b200(args, case, wl, world, rank, local):
         "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_burst": peak_burst, "frac_vs_burst": achieved / peak_burst,
-                     "kernel": contract_kernel_name(case),
+                     "kernel": contract_kernel_name(case, plan),
                      "kernel_ms": k2_avg,
                      "algorithmic": ("output + input bytes" if bound == "hbm" else "8*K flops per complex output element"),
                      "t_roof_ms": max(t_hbm, t_tc) * 1e3,
@@ -495,6 +495,8 @@ def executed_flops(plan, case, tc_peak, k2_ms):
         hp = plan.mp // 3
         products = 3 if fp32_format() == "bf16x3" else 2
         per_tile = products * 2 * 2 * 256 * 256 * hp       # products, x + y MMAs, 2 flops/MAC, depth hp
+    elif getattr(plan, "small", False):
+        per_tile = 2 * 2 * 32 * 32 * plan.ld_pack           # fused small-m kernel: 32 x 32 tiles, depth padded to 8
     else:
         per_tile = 2 * 2 * 64 * 64 * plan.mp                # two planes, 2 flops/MAC
     f = float(tiles) * per_tile
@@ -507,8 +509,10 @@ def fp32_format():
     return os.environ.get("CORR2D_FP32_FORMAT", "f16f8").lower()
 
 
-def contract_kernel_name(case):
+def contract_kernel_name(case, plan=None):
     """The contraction kernel the C ABI dispatches to (bf16_variant() in contract_tc.cu)."""
+    if plan is not None and getattr(plan, "small", False):
+        return "small_fused_kernel (K1 + contraction, one launch)"
     if case.dtype != "float32":
         return "contract_f64_kernel"
     if os.environ.get("CORR2D_BF16_1SM") == "1":

@@ -184,6 +184,49 @@ int corr2d_contract_bf16x3(
 int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int row0, int row1,
                                    int64_t ld_out);
 
+/* ------------------------------- small m: the whole call in one launch ---- */
+/*
+ * fp64 Fourier route for 2 <= m <= 32 without resampling (cfg1 m = 11, cfg2
+ * m = 21): K1 of dataset 1 (and of dataset 2 unless raw2 == NULL, the homo
+ * case) + the contraction, as ONE kernel (each output tile waits for the K1
+ * of its own two channel blocks)
+ * (csrc/small.cu).  Replaces the corr2d_prep + corr2d_contract_f64 sequence
+ * that preprocess_dataset / dft_channels / correlate_ft (preprocess.py:262-275,
+ * fourier.py:61-125) map onto; same argument meanings as those two calls.
+ *   a_phi / a_psi / b : packed operand scratch (n1 / n1 / n2 rows of ld_pack
+ *                       doubles, 16-B aligned; homo: b is its own n1 rows),
+ *                       depth corr2d_small_depth(m) = m rounded up to 8 (zero
+ *                       padded), ld_pack even and >= that depth
+ *   ref_out* / sigma_out* : as corr2d_prep (either may be NULL)
+ *   rows [row0, row1) (multiples of 32, or row1 = n1) and tiles [tile0, tile1)
+ *   of corr2d_small_tile_count's enumeration (32 x 32 tiles; -1 = to the end)
+ *                       select a row shard / a rank's share; every element has
+ *                       the same bits for any partition
+ *   status1 / status2  : device int32[4] each, the corr2d_prep status words
+ *                       (status2 unused when homo); written by the call
+ *   stats              : device uint64[3], as corr2d_contract_f64; written by the call
+ *   work               : device int32[16 + 5 * (ceil(n1/32) + ceil(n2/32))]
+ *                       (homo: no n2 term), zero-filled by the caller ONCE
+ *                       before the first call on it: status / stat accumulators
+ *                       (left zero by every call), a launch epoch and ready
+ *                       flags per 32-channel block and 4-bin group (tiles wait
+ *                       for their two blocks' K1 instead of a grid barrier).
+ *                       One work buffer per concurrently running call.
+ */
+int corr2d_small_depth(int m);
+int64_t corr2d_small_tile_count(int n1, int n2, int homo, int row0, int row1);
+int corr2d_correlate_small_f64(
+    int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
+    int m, int n1, int n2,
+    int ref_mode1, const double* ref_in1, const double* sigma_in1,
+    int ref_mode2, const double* ref_in2, const double* sigma_in2,
+    double alpha, int substitute_zero_var, double norm_const,
+    double* a_phi, double* a_psi, double* b, int64_t ld_pack,
+    double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
+    int row0, int row1, int64_t tile0, int64_t tile1,
+    double* phi, double* psi, int64_t ld_out,
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream);
+
 /* ------------------------------------------------- K3: peak candidates ---- */
 /*
  * max |x| over an n1 x n2 plane (dtype CORR2D_F64 / CORR2D_F32, leading

@@ -192,6 +192,13 @@ class PrepRecipe:
     substitute: bool = False
 
 
+def small_fused_enabled() -> bool:
+    """The one-launch small-m path (CORR2D_SMALL_FUSED=0 selects the two-kernel
+    path, for A/B comparisons)."""
+    import os
+    return os.environ.get("CORR2D_SMALL_FUSED", "1") != "0"
+
+
 def launch_prep(lib, raw, recipe: PrepRecipe, *, norm=0.0, pack_kind=_abi.PACK_NONE, roles=0,
                 a_phi=None, a_psi=None, b=None, ld_pack=0, split_plane=0,
                 values_out=None, half_out=None, ref_out=None, sigma_out=None, status=None):
@@ -305,6 +312,17 @@ class CorrelationPlan:
         # slot, interleaved per 32-slot block, then the fp32 DC / Nyquist pair
         # in a 128-byte pad (include/corr2d.h)
         self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
+        # small m (fp64 Fourier route, m <= 32, no resampling): the whole call is
+        # ONE launch (csrc/small.cu: K1 + grid barrier + warp-tile contraction);
+        # its operand rows are zero padded to a multiple of 8 slots
+        self.small = (route == "fourier" and self.dtype == np.float64 and self.shard is None
+                      and small_fused_enabled() and 2 <= self.m <= 32
+                      and all(r is None or (r.resample is None and r.m_in == r.m) for r in (recipe1, recipe2))
+                      and (recipe2 is None or (recipe2.alpha == recipe1.alpha
+                                               and recipe2.substitute == recipe1.substitute))
+                      and self.row0 % 32 == 0 and (self.row1 == self.n1 or self.row1 % 32 == 0))
+        if self.small:
+            self.ld_pack = self.lib.corr2d_small_depth(self.m)
         dev = self.dev
         R1, R2 = self._rows(self.n1), self._rows(self.n2)
         alloc = t.zeros if self.shard else t.empty
@@ -332,6 +350,9 @@ class CorrelationPlan:
                 f"out of memory assembling the complex correlation matrix; it needs "
                 f"16*{self.n1}*{self.n2} bytes = {16 * self.n1 * self.n2 / 1e9:.2f} GB") from None
         self.stats = t.zeros(4, dtype=t.int64, device=dev)
+        # fused small-m path: self-resetting K1 status accumulators + grid barrier words
+        self.work = (t.zeros(16 + 5 * ((self.n1 + 31) // 32 + (0 if self.homo else (self.n2 + 31) // 32)),
+                             dtype=t.int32, device=dev) if self.small else None)
         self.status1 = t.zeros(4, dtype=t.int32, device=dev)
         self.status2 = t.zeros(4, dtype=t.int32, device=dev)
         self.ref1 = alloc(R1, dtype=t.float64, device=dev) if want_ref else None
@@ -359,6 +380,11 @@ class CorrelationPlan:
     def tile_count(self) -> int:
         """Tiles in the contraction kernel's enumeration for this plan (the unit
         of the multi-GPU tile-range partition; include/corr2d.h)."""
+        if self.small:
+            n = self.lib.corr2d_small_tile_count(self.n1, self.n2, 1 if self.homo else 0, self.row0, self.row1)
+            if n < 0:
+                raise DataError("bad contraction shape")
+            return int(n)
         n = self.lib.corr2d_contract_tile_count(self.pack_kind, self.n1, self.n2, 1 if self.homo else 0,
                                                 self.row0, self.row1, self.n2)
         if n < 0:
@@ -367,7 +393,10 @@ class CorrelationPlan:
 
     @property
     def launches_per_step(self) -> int:
-        """Kernels of ours one launch() enqueues: K1 per dataset + K2."""
+        """Kernels of ours one launch() enqueues: K1 per dataset + K2 (one fused
+        kernel on the small-m path)."""
+        if self.small:
+            return 1
         return (1 if self.homo else 2) + (2 if self.route == "hilbert" else 1)
 
     def launch(self):
@@ -376,6 +405,8 @@ class CorrelationPlan:
         self.launch_contract()
 
     def launch_prep_only(self):
+        if self.small:
+            return                      # K1 runs inside the fused kernel (launch_contract)
         lib = self.lib
         roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
         if self.pack_kind in (_abi.PACK_BF16X2, _abi.PACK_F16F8) and self.homo:
@@ -424,6 +455,9 @@ class CorrelationPlan:
 
     def launch_contract(self):
         lib = self.lib
+        if self.small:
+            self._launch_small()
+            return
         homo = 1 if self.homo else 0
         if self.route == "hilbert":
             # A_psi[i, s] = sum_k A_phi[i, k] * (-N[s, k]) = -Norm (N y1)[s, i]
@@ -443,6 +477,24 @@ class CorrelationPlan:
                 self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
                 ptr(self.stats), stream_handle())
         _abi.check(code, lib)
+
+    def _launch_small(self):
+        t = torch()
+        raw1, raw2 = self.raw1, self.raw2
+        if raw1.dtype not in (t.float64, t.float32) or (raw2 is not None and raw2.dtype != raw1.dtype):
+            raise DataError(f"unsupported intensity dtype {raw1.dtype}")
+        r1, r2 = self.recipe1, self.recipe2 or self.recipe1
+        code = self.lib.corr2d_correlate_small_f64(
+            _abi.F64 if raw1.dtype == t.float64 else _abi.F32,
+            ptr(raw1), raw1.stride(0), ptr(raw2), raw2.stride(0) if raw2 is not None else 0,
+            self.m, self.n1, self.n2,
+            int(r1.ref_mode), ptr(r1.ref_in), ptr(r1.sigma_in), int(r2.ref_mode), ptr(r2.ref_in), ptr(r2.sigma_in),
+            float(r1.alpha), 1 if r1.substitute else 0, self.norm,
+            ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.ld_pack,
+            ptr(self.ref1), ptr(self.sigma1), ptr(self.ref2), ptr(self.sigma2),
+            self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
+            ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle())
+        _abi.check(code, self.lib)
 
     def check(self, axes=(None, None), labels=("first", "second")):
         """After the stream synchronised: raise the reference's errors, apply

@@ -87,6 +87,9 @@ def _shard_worker(rank, world, port, out):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    # the all-gather scheme belongs to the two-kernel path (K1, collective, K2);
+    # the one-launch small-m path recomputes its spectra -- compare like with like
+    os.environ["CORR2D_SMALL_FUSED"] = "0"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
     import paper_1808_00685_b200 as P

@@ -61,17 +61,23 @@ def test_prep_paths_agree(monkeypatch, m, n1, n2, dtype, fmt):
 @pytest.mark.parametrize("m,n1,n2,alpha", [(11, 1000, None, 0.0), (21, 2000, 1500, 0.0), (5, 33, 17, 0.5),
                                            (32, 301, None, 1.0), (2, 40, None, 0.5)])
 def test_small_m_path_matches_generic(monkeypatch, m, n1, n2, alpha):
-    """m <= 32 fp64 (cfg1 / cfg2 shapes): the warp-per-channel-pair K1 against the
-    generic kernel -- statistics bit-identical (same sequential operations), maps
-    within 1e-13 (a direct DFT instead of the Stockham stages)."""
+    """m <= 32 fp64 (cfg1 / cfg2 shapes): the one-launch fused path (default), the
+    two-kernel path with the warp-per-channel-pair K1 and the two-kernel path with
+    the generic K1 -- statistics bit-identical (same sequential operations), maps
+    within 1e-13 (a direct DFT instead of the Stockham stages, another
+    contraction order)."""
     def run(env):
-        monkeypatch.delenv("CORR2D_PREP_SMALL", raising=False)
+        for k in ("CORR2D_PREP_SMALL", "CORR2D_SMALL_FUSED"):
+            monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         d1 = _ds(m, n1, 3 + m, "float64")
         d2 = None if n2 is None else _ds(m, n2, 4 + m, "float64")
         return P.corr2d(d1, d2, alpha=alpha)
-    small, generic = run({}), run({"CORR2D_PREP_SMALL": "0"})
-    assert np.array_equal(small.ref1, generic.ref1) and np.array_equal(small.ref2, generic.ref2)
+    fused = run({})
+    small = run({"CORR2D_SMALL_FUSED": "0"})
+    generic = run({"CORR2D_SMALL_FUSED": "0", "CORR2D_PREP_SMALL": "0"})
     scale = float(max(np.abs(generic.sync).max(), np.abs(generic.asyn).max()))
-    assert rel_err(small.sync, generic.sync, scale) <= 1e-13 and rel_err(small.asyn, generic.asyn, scale) <= 1e-13
+    for r in (fused, small):
+        assert np.array_equal(r.ref1, generic.ref1) and np.array_equal(r.ref2, generic.ref2)
+        assert rel_err(r.sync, generic.sync, scale) <= 1e-13 and rel_err(r.asyn, generic.asyn, scale) <= 1e-13

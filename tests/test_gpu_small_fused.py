@@ -1,0 +1,169 @@
+"""The one-launch small-m fp64 path (csrc/small.cu, corr2d_correlate_small_f64):
+K1 of both datasets + grid barrier + warp-tile contraction in one cooperative
+kernel.  Parity against the CPU oracle (1e-10 of max|sync|, BASELINE.json
+north_star), exact homo symmetry, bit-identity under row shards and tile-range
+partitions (the multi-GPU units), and the self-resetting status / barrier words
+(an error call must not leak into the next call)."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from oracle import corr2d_oracle as O
+import paper_1808_00685_b200 as P
+from paper_1808_00685_b200 import engine
+from paper_1808_00685_b200.errors import NumericError
+
+pytestmark = pytest.mark.gpu
+TOL64 = 1e-10
+
+
+def dyn(values, alpha=0.0):
+    values = np.asarray(values, dtype=float)
+    m, n = values.shape
+    return P.DynamicSpectra(np.arange(n, dtype=float) + 1.0, np.arange(m, dtype=float), values,
+                            np.zeros(n), scaling_exponent=alpha)
+
+
+def scale_of(s, a):
+    return max(float(np.abs(s).max()), float(np.abs(a).max()), 1e-300)
+
+
+def _plan_is_small(n1, n2, m, homo=True):
+    recipe = engine.PrepRecipe(m_in=m, m=m, ref_mode=P._abi.REF_NONE)
+    plan = engine.CorrelationPlan(n1=n1, n2=n2, m=m, recipe1=recipe, recipe2=None if homo else recipe,
+                                  norm=1.0, want_ref=False)
+    return plan.small
+
+
+def test_small_plans_take_the_fused_path():
+    assert _plan_is_small(1000, 1000, 11) and _plan_is_small(2000, 1500, 21, homo=False)
+    assert _plan_is_small(5, 5, 2) and _plan_is_small(64, 64, 32)
+    assert not _plan_is_small(64, 64, 33)
+
+
+@pytest.mark.parametrize("n1,n2,m", [(1, 1, 2), (3, 5, 3), (31, 33, 8), (63, 65, 5), (64, 64, 12),
+                                     (65, 130, 21), (517, 300, 32), (1000, 999, 11)])
+def test_fused_matches_oracle_homo_and_hetero(n1, n2, m):
+    rng = np.random.default_rng(n1 * 7 + n2 + m)
+    v1 = rng.normal(size=(m, n1))
+    v2 = rng.normal(size=(m, n2))
+    res = P.correlate_ft(dyn(v1), dyn(v2))
+    s, a, _ = O.correlate_ft(v1, v2)
+    sc = scale_of(s, a)
+    assert rel_err(res.sync, s, sc) <= TOL64 and rel_err(res.asyn, a, sc) <= TOL64
+    homo = P.correlate_ft(dyn(v1))
+    s, a, _ = O.correlate_ft(v1)
+    sc = scale_of(s, a)
+    assert rel_err(homo.sync, s, sc) <= TOL64 and rel_err(homo.asyn, a, sc) <= TOL64
+    assert np.array_equal(homo.sync, homo.sync.T) and np.array_equal(homo.asyn, -homo.asyn.T)
+    assert np.all(np.diag(homo.asyn) == 0)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_fused_full_pipeline_inputs(dtype):
+    """Raw intensities (mean reference, alpha scaling, float32 storage) through corr2d()."""
+    rng = np.random.default_rng(5)
+    m, n = 21, 777
+    t = np.linspace(0, 100, m)
+    x = (rng.normal(size=(m, n)) + np.outer(np.sin(t / 9.0), rng.uniform(1, 3, n))).astype(dtype)
+    ds = P.SpectralDataset(np.arange(n, dtype=float), t, x, dtype=x.dtype)
+    for alpha in (0.0, 0.5):
+        res = P.corr2d(ds, alpha=alpha)
+        vals = np.asarray(x, dtype=np.float64)
+        ref = vals.mean(axis=0)
+        y = vals - ref
+        if alpha:
+            y = y / (np.sqrt(((vals - ref) ** 2).sum(axis=0) / (m - 1)) ** alpha)
+        s, a, _ = O.correlate_ft(y)
+        sc = scale_of(s, a)
+        assert rel_err(res.sync, s, sc) <= TOL64 and rel_err(res.asyn, a, sc) <= TOL64
+        assert np.array_equal(res.ref1, ref) or rel_err(res.ref1, ref) <= 1e-15
+
+
+def test_fused_row_shards_bit_identical_to_full():
+    from paper_1808_00685_b200.engine_core import tile_aligned_blocks
+    v = np.random.default_rng(3).normal(size=(11, 517))
+    d = dyn(v)
+    full = P.correlate_ft(d)
+    for parts in (2, 3, 8):
+        for r0, r1 in tile_aligned_blocks(517, parts):
+            sh = P.correlate_ft(d, rows=(r0, r1), return_device=True)
+            assert np.array_equal(sh.sync.cpu().numpy(), full.sync[r0:r1])
+            assert np.array_equal(sh.asyn.cpu().numpy(), full.asyn[r0:r1])
+
+
+@pytest.mark.parametrize("homo", [True, False])
+def test_fused_tile_ranges_bit_identical(homo):
+    """The multi-GPU unit: contiguous ranges of the warp-tile enumeration, one
+    per rank, reassemble the whole map bit for bit."""
+    from paper_1808_00685_b200.engine_core import tile_range
+    rng = np.random.default_rng(9)
+    m, n1, n2 = 21, 700, (700 if homo else 333)
+    v1 = rng.normal(size=(m, n1))
+    v2 = v1 if homo else rng.normal(size=(m, n2))
+    full = P.correlate_ft(dyn(v1)) if homo else P.correlate_ft(dyn(v1), dyn(v2))
+    recipe = engine.PrepRecipe(m_in=m, m=m, ref_mode=P._abi.REF_NONE)
+    plan = engine.CorrelationPlan(n1=n1, n2=n2, m=m, recipe1=recipe, recipe2=None if homo else recipe,
+                                  norm=1.0 / (np.pi * (m - 1)), want_ref=False)
+    assert plan.small
+    dev = plan.dev
+    plan.bind(dyn(v1).device_values(dev), None if homo else dyn(v2).device_values(dev))
+    total = plan.tile_count()
+    plan.phi.zero_()
+    plan.psi.zero_()
+    for rank in range(5):
+        plan.tile0, plan.tile1 = tile_range(total, 5, rank)
+        plan.launch()
+    engine.sync()
+    assert np.array_equal(plan.phi.cpu().numpy(), full.sync)
+    assert np.array_equal(plan.psi.cpu().numpy(), full.asyn)
+
+
+def test_fused_status_words_reset_between_calls():
+    """A call that flags non-finite input / zero variance must not leak its
+    counters into the next call on the same plan (self-resetting accumulators)."""
+    rng = np.random.default_rng(2)
+    m, n = 11, 300
+    t = np.arange(m, dtype=float)
+    x = rng.normal(size=(m, n))
+    bad = x.copy()
+    bad[3, 17] = np.nan
+    with pytest.raises(Exception):
+        P.corr2d(P.SpectralDataset(np.arange(n, dtype=float), t, bad))
+    good = P.corr2d(P.SpectralDataset(np.arange(n, dtype=float), t, x))
+    assert np.isfinite(good.sync).all()
+    # one plan, launched repeatedly: identical bits, clean status every time
+    from paper_1808_00685_b200 import api
+    ds = P.SpectralDataset(np.arange(n, dtype=float), t, x)
+    plan, _ = api.build_plan(ds, None, P.PreprocessSpec(), dtype="float64")
+    assert plan.small
+    outs = []
+    for _ in range(3):
+        plan.launch()
+        engine.sync()
+        plan.check()
+        outs.append(plan.phi.cpu().numpy().copy())
+        w = plan.work.cpu().numpy()
+        assert not w[:9].any() and not w[10:16].any()   # accumulators reset; [9] epoch, [16:] block flags
+    assert all(np.array_equal(o, outs[0]) for o in outs)
+    # zero variance with alpha > 0: the error policy raises, the substitute policy warns
+    flat = x.copy()
+    flat[:, 40] = 2.5
+    dsf = P.SpectralDataset(np.arange(n, dtype=float), t, flat)
+    with pytest.raises(NumericError, match="zero-variance"):
+        P.corr2d(dsf, alpha=0.5)
+    res = P.corr2d(P.SpectralDataset(np.arange(n, dtype=float), t, x), alpha=0.5)
+    assert np.isfinite(res.sync).all()
+
+
+def test_fused_and_two_kernel_paths_agree(monkeypatch):
+    rng = np.random.default_rng(4)
+    v = rng.normal(size=(21, 1500))
+    fused = P.correlate_ft(dyn(v))
+    monkeypatch.setenv("CORR2D_SMALL_FUSED", "0")
+    two = P.correlate_ft(dyn(v))
+    sc = scale_of(two.sync, two.asyn)
+    assert rel_err(fused.sync, two.sync, sc) <= 1e-13 and rel_err(fused.asyn, two.asyn, sc) <= 1e-13
