@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -216,7 +217,7 @@ def config_block(case, wl, args):
             "alpha": case.alpha, "compute": f"{fp32_format()} tcgen05 -> fp32 planes" if case.dtype == "float32"
             else "fp64 DMMA -> fp64 planes",
             "l2": "outputs per step >> 126 MB L2 (cold L2 each step)" if wl["out_bytes"] + wl["in_bytes"] > 4 * 126e6
-            else "L2 flushed between timed steps (256 MB write outside each step's event pair)",
+            else "rotating over independent input / output buffers whose total exceeds 4 x the 126 MB L2 (no flush needed)",
             "parallelism": (f"tile-range x{args.gpus}, spectra {args.spectra}" if args.gpus > 1 else "single GPU")}
 
 
@@ -279,19 +280,45 @@ def run_b200(args, case, wl, world, rank, local):
     #      duration are measured live inside the timed steps, back to back;
     #      maps that fit in L2 get a 256 MB write between steps, outside the
     #      step's events, so every timed step starts from a cold L2.
-    flush = wl["out_bytes"] + wl["in_bytes"] <= 4 * 126e6
-    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    #      Maps that fit in L2 (cfg1 / cfg2) instead ROTATE over R independent
+    #      plans (own inputs, operands and output planes; R * (in + out) > 4 x
+    #      126 MB), so no step finds its data in L2, and the timed graph holds
+    #      only the K steps (an event-record node costs ~3 us, as much as the
+    #      cfg1 step's own write time); a second, diagnostic graph of the same
+    #      steps with per-step events gives the median / best and the
+    #      contraction-kernel split.
+    foot = wl["out_bytes"] + wl["in_bytes"]
+    rotate = foot <= 4 * 126e6
+    plans = [plan]
+    if rotate:
+        for _ in range(int(math.ceil(4 * 126e6 / foot)) - 1):
+            q, _ = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev, spectra_shard=shard)
+            if world > 1:
+                q.tile0, q.tile1 = plan.tile0, plan.tile1
+            plans.append(q)
     evs = [tuple(torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)) for _ in range(args.steps)]
+    ev_all = tuple(torch.cuda.Event(enable_timing=True) for _ in range(2))
+
+    def one_step(k):
+        q = plans[k % len(plans)]
+        q.launch_prep_only()
+        q.launch_contract()
+
+    def event_steps(s):
+        for k, (a, mid, b) in enumerate(evs):
+            q = plans[k % len(plans)]
+            a.record(s)
+            q.launch_prep_only()
+            mid.record(s)
+            q.launch_contract()
+            b.record(s)
 
     def timed_steps(s):
-        for a, mid, b in evs:
-            if flush:
-                flush_buf.fill_(1)
-            a.record(s)
-            plan.launch_prep_only()
-            mid.record(s)
-            plan.launch_contract()
-            b.record(s)
+        if not rotate:
+            event_steps(s)
+            return
+        for k in range(args.steps):
+            one_step(k)
 
     # gloo (BENCH_ONE_DEVICE test mode) collectives stage through the host and
     # cannot be graph-captured: that mode launches eagerly
@@ -303,22 +330,30 @@ def run_b200(args, case, wl, world, rank, local):
                 self.replay = fn
         step_graph = _Eager(plan.launch)
         timed_graph = _Eager(lambda: timed_steps(stream))
+        diag_graph = _Eager(lambda: event_steps(stream)) if rotate else None
         plan.launch()
     else:
         step_graph, timed_graph = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        diag_graph = torch.cuda.CUDAGraph() if rotate else None
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
-            plan.launch()                     # settle allocator / attributes before capture
+            for q in plans:
+                q.launch()                    # settle allocator / attributes before capture
             with torch.cuda.graph(step_graph, stream=cap):
                 plan.launch()
             with torch.cuda.graph(timed_graph, stream=cap):
                 timed_steps(cap)
+            if rotate:
+                with torch.cuda.graph(diag_graph, stream=cap):
+                    event_steps(cap)
         stream.wait_stream(cap)
     torch.cuda.synchronize()
 
     def step():
         step_graph.replay()
+
+    clocks_extra = {}
 
     def measure():
         with ClockSampler(local) as clocks:
@@ -336,11 +371,27 @@ def run_b200(args, case, wl, world, rank, local):
             #      barrier + sync on both sides
             barrier(world)
             torch.cuda.synchronize()
+            ev_all[0].record()
             timed_graph.replay()
+            ev_all[1].record()
             torch.cuda.synchronize()
             barrier(world)
+            if rotate:
+                total = ev_all[0].elapsed_time(ev_all[1])
+                diag_graph.replay()               # per-step events (diagnostics), same steps
+                torch.cuda.synchronize()
             per_step = [a.elapsed_time(b) for a, _, b in evs]
             per_k2 = [mid.elapsed_time(b) for _, mid, b in evs]
+            if rotate:
+                # value from the event-free timed graph; the per-step events of
+                # the diagnostic graph carry ~3 us of event-node time each
+                diag = {"per_step_events_ms_median": statistics.median(per_step),
+                        "contraction_span_events_ms_avg": sum(per_k2) / len(per_k2)}
+                fused = getattr(plan, "small", False)
+                per_step = [total / args.steps] * args.steps
+                if fused:          # the fused kernel is the whole step
+                    per_k2 = list(per_step)
+                clocks_extra.update(diag)
             if os.environ.get("BENCH_DUMP_STEPS"):
                 print("per-step ms:", [round(x, 4) for x in per_step], file=sys.stderr)
             t_load = time.time()
@@ -404,6 +455,9 @@ def run_b200(args, case, wl, world, rank, local):
                      "peak_source": peaks["_source"] + (" (bf16 sustained; burst in peak_burst)" if case.dtype == "float32"
                                                         else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
         "clocks": clock_summary,
+        "timing": ({"mode": f"event-free graph of K steps rotating over {len(plans)} plans "
+                            f"({len(plans) * foot / 1e6:.0f} MB of inputs + outputs > 126 MB L2)", **clocks_extra}
+                   if rotate else {"mode": "graph of K steps, per-step event pairs (outputs >> L2)"}),
         "gpu_launches": plan.launches_per_step * args.steps,
         "parity": parity,
     }

@@ -205,7 +205,7 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  *   status1 / status2  : device int32[4] each, the corr2d_prep status words
  *                       (status2 unused when homo); written by the call
  *   stats              : device uint64[3], as corr2d_contract_f64; written by the call
- *   work               : device int32[16 + 5 * (ceil(n1/32) + ceil(n2/32))]
+ *   work               : device int32[20 + 5 * (ceil(n1/32) + ceil(n2/32))]
  *                       (homo: no n2 term), zero-filled by the caller ONCE
  *                       before the first call on it: status / stat accumulators
  *                       (left zero by every call), a launch epoch and ready

@@ -234,7 +234,8 @@ constexpr int kWStatus2 = 4;   // [4, 8)  dataset 2
 constexpr int kWDone = 8;      // CTAs finished (the last one publishes and resets)
 constexpr int kWEpoch = 9;     // launch epoch: block flags of this launch read epoch + 1
 constexpr int kWStats = 10;    // [10, 16) max|sync|, max|async|, non-finite count (3 x uint64)
-constexpr int kWFlags = 16;    // ready flags: kMaxGroups per 32-channel block
+constexpr int kWK1Done = 16;   // K1 tasks finished (phase-2 warps stop checking flags once all are)
+constexpr int kWFlags = 20;    // ready flags: kMaxGroups per 32-channel block
 constexpr int kMaxGroups = 5;  // 4-bin groups of K = m / 2 + 1 <= 17
 
 enum FusedMode { kFPlain = 0, kFMirror = 1, kFDiag = 2, kFTransOnly = 3 };
@@ -299,10 +300,10 @@ __device__ __forceinline__ void wait_flag(const int* flag, int want) {
   // a thousand warps polling one L2 line slow down the K1 they are waiting
   // for), then one acquire load
   const unsigned long long t0 = global_ns();
-  unsigned ns = 128;
+  unsigned ns = 64;
   while (ld_relaxed(flag) != want) {
     __nanosleep(ns);
-    ns = ns < 1024 ? 2 * ns : 1024;
+    ns = ns < 256 ? 2 * ns : 256;
     if (global_ns() - t0 > 20000000000ull) __trap();
   }
   (void)ld_acquire(flag);
@@ -512,8 +513,10 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
       __threadfence();                             // this lane's rows, before the flag
       __syncwarp();
       if (tr && task == slot && lane == 0) tr[7] = global_ns();
-      if (lane == 0)
+      if (lane == 0) {
         asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flags + kMaxGroups * blk + g), "r"(want) : "memory");
+        atomicAdd(p.work + kWK1Done, 1);
+      }
     }
   }
   if (tr) { __syncthreads(); if (threadIdx.x == 0) tr[1] = global_ns(); }
@@ -525,17 +528,28 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   const int fB = p.homo ? 0 : p.nb1;
   unsigned long long mphi = 0, mpsi = 0;
   bool first = true;
-  for (long long u = gw; u < 2 * p.tiles; u += W) {
+  bool all_ready = false;                          // every K1 task of this launch seen finished
+  const int k1_tasks = (p.nb1 + (p.homo ? 0 : (p.n2 + 31) / 32)) * G;
+  const long long units = 2 * p.tiles;
+  // static round robin (a shared claim counter measured slower: thousands of
+  // warps serialise on one L2 atomic)
+  for (long long u = gw; u < units;) {
     int I, J, mode;
     fused_decode(p, p.tile0 + (u >> 1), I, J, mode);
     const int h = (int)(u & 1);
     const int r0 = I * kFT + h * 16;
-    if (r0 >= p.n1) continue;
-    if (lane < G) {
-      wait_flag(flags + kMaxGroups * I + lane, want);
-      wait_flag(flags + kMaxGroups * (fB + J) + lane, want);
+    if (!all_ready) {
+      int done = 0;
+      if (lane == 0) done = ld_acquire(p.work + kWK1Done);
+      all_ready = __shfl_sync(0xffffffffu, done, 0) == k1_tasks;
+      if (!all_ready && lane < G) {
+        wait_flag(flags + kMaxGroups * I + lane, want);
+        wait_flag(flags + kMaxGroups * (fB + J) + lane, want);
+      }
+      __syncwarp();
     }
-    __syncwarp();
+    u += W;
+    if (r0 >= p.n1) continue;
     if (tr && first && lane == 0 && warp == 0) tr[2] = global_ns();
     first = false;
     double aphi[4][4], apsi[4][4];
@@ -689,6 +703,7 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
         av[k] = 0ull;
       }
       wv[kWDone] = 0;
+      wv[kWK1Done] = 0;
       wv[kWEpoch] = want;
       __threadfence();
     }

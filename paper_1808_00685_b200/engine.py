@@ -351,7 +351,7 @@ class CorrelationPlan:
                 f"16*{self.n1}*{self.n2} bytes = {16 * self.n1 * self.n2 / 1e9:.2f} GB") from None
         self.stats = t.zeros(4, dtype=t.int64, device=dev)
         # fused small-m path: self-resetting K1 status accumulators + grid barrier words
-        self.work = (t.zeros(16 + 5 * ((self.n1 + 31) // 32 + (0 if self.homo else (self.n2 + 31) // 32)),
+        self.work = (t.zeros(20 + 5 * ((self.n1 + 31) // 32 + (0 if self.homo else (self.n2 + 31) // 32)),
                              dtype=t.int32, device=dev) if self.small else None)
         self.status1 = t.zeros(4, dtype=t.int32, device=dev)
         self.status2 = t.zeros(4, dtype=t.int32, device=dev)

@@ -147,7 +147,7 @@ def test_fused_status_words_reset_between_calls():
         plan.check()
         outs.append(plan.phi.cpu().numpy().copy())
         w = plan.work.cpu().numpy()
-        assert not w[:9].any() and not w[10:16].any()   # accumulators reset; [9] epoch, [16:] block flags
+        assert not w[:9].any() and not w[10:20].any()   # accumulators / counters reset; [9] epoch, [20:] block flags
     assert all(np.array_equal(o, outs[0]) for o in outs)
     # zero variance with alpha > 0: the error policy raises, the substitute policy warns
     flat = x.copy()
