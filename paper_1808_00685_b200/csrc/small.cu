@@ -205,7 +205,33 @@ int launch_prep_small(const PrepParams& p, cudaStream_t st) {
 constexpr int kFT = 32;          // warp tile edge (output rows and columns)
 // one CTA per SM (every CTA resident: the flag waits cannot deadlock), as many
 // warps as the register file holds: 16 at <= 128 registers (depth <= 16), 12 above
-template <int NCH> __host__ __device__ constexpr int fused_warps() { return NCH <= 2 ? 16 : 12; }
+// CORR2D_SMALL_TMA: full units leave through a per-warp shared-memory staging
+// tile and bulk (TMA) copies, so a warp's output drains while it runs the next
+// unit's MMAs (register stores made the warps alternate, in step, between a
+// DMMA-bound and a store-bound phase); 8 warps then fit the staging tiles.
+#ifndef CORR2D_SMALL_TMA
+#define CORR2D_SMALL_TMA 0
+#endif
+#if CORR2D_SMALL_TMA
+#ifndef CORR2D_SMALL_W12
+#define CORR2D_SMALL_W12 8
+#endif
+#ifndef CORR2D_SMALL_W34
+#define CORR2D_SMALL_W34 8
+#endif
+#else
+#ifndef CORR2D_SMALL_W12
+#define CORR2D_SMALL_W12 16
+#endif
+#ifndef CORR2D_SMALL_W34
+#define CORR2D_SMALL_W34 12
+#endif
+#endif
+// staging tile per warp (doubles): direct [2 planes][16 rows][34], mirror [2][32 rows][18]
+// (padded rows: conflict-light fragment writes; each row is its own bulk copy)
+constexpr int kSD = 34, kSM = 18;
+constexpr int kStgPerWarp = 2 * 16 * kSD + 2 * 32 * kSM;
+template <int NCH> __host__ __device__ constexpr int fused_warps() { return NCH <= 2 ? CORR2D_SMALL_W12 : CORR2D_SMALL_W34; }
 
 struct SmallParams {
   PrepParams p1, p2;        // K1 of dataset 1 (roles A, and B when homo) and dataset 2 (role B)
@@ -473,6 +499,23 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// Operand loads.  L1-cached: a warp reads a channel block only after an
+// acquire that saw its K1 flag (or the all-done count), and every acquire
+// invalidates the SM's L1 (CCTL.IVALL), so no line of operand data cached
+// before it was final survives; neighbouring tiles of a CTA then share rows.
+#ifndef CORR2D_SMALL_L1
+#define CORR2D_SMALL_L1 1
+#endif
+__device__ __forceinline__ double2 ld_op(const double* a) {
+#if CORR2D_SMALL_L1
+  double2 v;
+  asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a));
+  return v;
+#else
+  return __ldcg(reinterpret_cast<const double2*>(a));
+#endif
+}
+
 __device__ __forceinline__ unsigned long long abits(double x) {
   return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
 }
@@ -483,6 +526,7 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   constexpr int kK1Warps = 4;                     // warps per CTA that take K1 blocks
   __shared__ double2 tw[32];
   __shared__ double ys[kK1Warps][32 * 32];        // K1 sample columns [t][lane] per warp
+  extern __shared__ __align__(128) double stg[];   // CORR2D_SMALL_TMA: per-warp output staging tiles
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // global warp index, CTA-minor: consecutive work items land on different SMs
   const int gw = warp * (int)gridDim.x + blockIdx.x;
@@ -490,7 +534,8 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   // this launch's epoch (bumped only by the last CTA of the previous launch)
   const int want = *reinterpret_cast<volatile const int*>(p.work + kWEpoch) + 1;
   int* flags = p.work + kWFlags;
-  unsigned long long* tr = p.trace ? p.trace + 8 * blockIdx.x : nullptr;
+  unsigned long long* tr = p.trace ? p.trace + 32 * blockIdx.x : nullptr;
+  int unit_no = 0;
   if (tr && threadIdx.x == 0) tr[0] = global_ns();
 
   // ---- phase 1: K1, one warp per 32-channel block, one lane per channel ----
@@ -531,9 +576,22 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   bool all_ready = false;                          // every K1 task of this launch seen finished
   const int k1_tasks = (p.nb1 + (p.homo ? 0 : (p.n2 + 31) / 32)) * G;
   const long long units = 2 * p.tiles;
-  // static round robin (a shared claim counter measured slower: thousands of
-  // warps serialise on one L2 atomic)
-  for (long long u = gw; u < units;) {
+#ifndef CORR2D_SMALL_CHUNK
+#define CORR2D_SMALL_CHUNK 0
+#endif
+  // static assignment (a shared claim counter measured slower: thousands of
+  // warps serialise on one L2 atomic).  CHUNK: every CTA owns a contiguous run
+  // of units (neighbouring tiles share their row operands, served from L1),
+  // its warps interleaved inside it; else a grid-wide round robin.
+#if CORR2D_SMALL_CHUNK
+  const long long per = (units + gridDim.x - 1) / gridDim.x;
+  const long long u_end = min(units, per * (blockIdx.x + 1));
+  const long long u_step = kFusedWarps;
+  for (long long u = per * blockIdx.x + warp; u < u_end;) {
+#else
+  const long long u_end = units, u_step = W;
+  for (long long u = gw; u < u_end;) {
+#endif
     int I, J, mode;
     fused_decode(p, p.tile0 + (u >> 1), I, J, mode);
     const int h = (int)(u & 1);
@@ -548,8 +606,12 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
       }
       __syncwarp();
     }
-    u += W;
+    u += u_step;
     if (r0 >= p.n1) continue;
+    if (tr && blockIdx.x == 0 && warp == 0 && lane == 0 && unit_no > 0 && unit_no <= 6) tr[10 + 3 * (unit_no - 1)] = global_ns();
+    const bool ut = tr && blockIdx.x == 0 && warp == 0 && lane == 0 && unit_no < 6;
+    if (tr) ++unit_no;
+    if (ut) tr[8 + 3 * (unit_no - 1)] = global_ns();
     if (tr && first && lane == 0 && warp == 0) tr[2] = global_ns();
     first = false;
     double aphi[4][4], apsi[4][4];
@@ -570,13 +632,13 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     // (second) of A and B alike -- a permutation of the depth, exact
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
-      const double2 a0 = __ldcg(reinterpret_cast<const double2*>(pa + 8 * ch));
-      const double2 a1 = __ldcg(reinterpret_cast<const double2*>(pb + 8 * ch));
-      const double2 s0 = __ldcg(reinterpret_cast<const double2*>(sa + 8 * ch));
-      const double2 s1 = __ldcg(reinterpret_cast<const double2*>(sb + 8 * ch));
+      const double2 a0 = ld_op(pa + 8 * ch);
+      const double2 a1 = ld_op(pb + 8 * ch);
+      const double2 s0 = ld_op(sa + 8 * ch);
+      const double2 s1 = ld_op(sb + 8 * ch);
       double2 bf[4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = __ldcg(reinterpret_cast<const double2*>(bc[nt] + 8 * ch));
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = ld_op(bc[nt] + 8 * ch);
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) {
         dmma(aphi[nt], a0.x, a1.x, bf[nt].x);
@@ -588,9 +650,68 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
         dmma(apsi[nt], s0.y, s1.y, bf[nt].y);
       }
     }
+    if (ut) {
+      double z = 0.0;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) z += aphi[nt][0] + apsi[nt][3];   // wait for the accumulators
+      tr[9 + 3 * (unit_no - 1)] = global_ns() + (z == 12345.678 ? 1 : 0);
+    }
     // ---- epilogue: lane holds rows (lr, lr + 8) x columns (2 lk, 2 lk + 1) of each n8 tile
     const bool interior = mode != kFDiag && p.vec && r0 + 16 <= min(p.n1, p.row1) && (J + 1) * kFT <= p.n2 &&
                           (mode == kFPlain || (J * kFT >= p.row0 && (J + 1) * kFT <= p.row1));
+#if CORR2D_SMALL_TMA
+    if (interior) {
+      // full 16 x 32 unit: fragments -> this warp's staging tile -> bulk copies
+      // (256-B direct rows, 128-B mirror rows); the copies drain while the warp
+      // moves on, and the tile is rewritten only after they have read it
+      const bool direct = mode != kFTransOnly, mirror = mode != kFPlain;
+      double* sd = stg + warp * kStgPerWarp;
+      double* sm = sd + 2 * 16 * kSD;
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      __syncwarp();
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int rl = lr + 8 * hh, cl = nt * 8 + 2 * lk;
+          const double f0 = aphi[nt][2 * hh], f1 = aphi[nt][2 * hh + 1];
+          const double s0 = apsi[nt][2 * hh], s1 = apsi[nt][2 * hh + 1];
+          mphi = max(mphi, max(abits(f0), abits(f1)));
+          mpsi = max(mpsi, max(abits(s0), abits(s1)));
+          if (direct) {
+            *reinterpret_cast<double2*>(sd + rl * kSD + cl) = make_double2(f0, f1);
+            *reinterpret_cast<double2*>(sd + 16 * kSD + rl * kSD + cl) = make_double2(s0, s1);
+          }
+          if (mirror) {
+            sm[cl * kSM + rl] = f0;
+            sm[(cl + 1) * kSM + rl] = f1;
+            sm[32 * kSM + cl * kSM + rl] = -s0;
+            sm[32 * kSM + (cl + 1) * kSM + rl] = -s1;
+          }
+        }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (direct) {
+        const int plane = lane >> 4, row = lane & 15;
+        const double* src = sd + plane * 16 * kSD + row * kSD;
+        double* dst = (plane ? p.psi : p.phi) + (long long)(r0 + row - p.row0) * p.ld_out + J * kFT;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;\n"
+                     ::"l"(dst), "r"(static_cast<unsigned>(__cvta_generic_to_shared(src))) : "memory");
+      }
+      if (mirror) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int c = lane + 32 * k, plane = c >> 5, row = c & 31;
+          const double* src = sm + plane * 32 * kSM + row * kSM;
+          double* dst = (plane ? p.psi : p.phi) + (long long)(J * kFT + row - p.row0) * p.ld_out + r0;
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;\n"
+                       ::"l"(dst), "r"(static_cast<unsigned>(__cvta_generic_to_shared(src))) : "memory");
+        }
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      continue;
+    }
+#else
     if (interior) {
       // branch-free fast path: full 16 x 32 unit, 16-byte direct stores, 8-byte mirror stores
       const bool direct = mode != kFTransOnly, mirror = mode != kFPlain;
@@ -618,6 +739,7 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
         }
       continue;
     }
+#endif
     const bool direct = mode != kFTransOnly;
     const bool mirror = mode != kFPlain;
 #pragma unroll
@@ -676,6 +798,9 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     mpsi = max(mpsi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mpsi, o));
   }
   bad = warp_sum(bad);
+#if CORR2D_SMALL_TMA
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+#endif
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWStats);
   if (lane == 0) {
     if (mphi) atomicMax(&acc[0], mphi);
@@ -717,20 +842,25 @@ static long long fused_tile_count(int n1, int n2, int homo, int row0, int row1) 
 }
 
 template <int NCH>
+static int fused_smem() { return CORR2D_SMALL_TMA ? fused_warps<NCH>() * kStgPerWarp * (int)sizeof(double) : 0; }
+
+template <int NCH>
 static int launch_fused(const SmallParams& p, cudaStream_t st) {
   static int grid = 0;
   if (grid == 0) {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fused_kernel<NCH>, 32 * fused_warps<NCH>(), 0);
+    cudaFuncSetAttribute(small_fused_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem<NCH>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fused_kernel<NCH>, 32 * fused_warps<NCH>(),
+                                                  fused_smem<NCH>());
     if (per_sm < 1) return fail(CORR2D_ERR_CUDA, "small_fused_kernel: no resident CTA");
     grid = per_sm * sms;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(32 * fused_warps<NCH>());
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = fused_smem<NCH>();
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
@@ -748,23 +878,23 @@ static int launch_fused(const SmallParams& p, cudaStream_t st) {
   const bool want_trace = te && te[0] == '1';
   SmallParams q = p;
   if (want_trace) {
-    if (!trace) cudaMalloc(&trace, 8 * sizeof(unsigned long long) * grid);
-    cudaMemsetAsync(trace, 0, 8 * sizeof(unsigned long long) * grid, st);
+    if (!trace) cudaMalloc(&trace, 32 * sizeof(unsigned long long) * grid);
+    cudaMemsetAsync(trace, 0, 32 * sizeof(unsigned long long) * grid, st);
     q.trace = trace;
   }
   cudaLaunchKernelEx(&cfg, small_fused_kernel<NCH>, q);
   if (want_trace) {
-    std::vector<unsigned long long> h(8 * (size_t)grid);
+    std::vector<unsigned long long> h(32 * (size_t)grid);
     cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     unsigned long long t0 = ~0ull;
-    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[8 * b]);
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[32 * b]);
     double mx[8] = {0}, avg[8] = {0};
     int cnt[8] = {0};
     for (int b = 0; b < grid; ++b)
       for (int k = 0; k < 8; ++k) {
-        if (!h[8 * b + k]) continue;
-        const double v = (double)(h[8 * b + k] - t0);
+        if (!h[32 * b + k]) continue;
+        const double v = (double)(h[32 * b + k] - t0);
         mx[k] = std::max(mx[k], v);
         avg[k] += v;
         ++cnt[k];
@@ -772,6 +902,10 @@ static int launch_fused(const SmallParams& p, cudaStream_t st) {
     const char* names[8] = {"start", "phase1", "first-unit", "end", "k1-loaded", "k1-stats", "k1-packed", "k1-fenced"};
     fprintf(stderr, "small_fused trace (ns, max/avg):");
     for (int k = 0; k < 8; ++k) fprintf(stderr, " %s %.0f/%.0f", names[k], mx[k], cnt[k] ? avg[k] / cnt[k] : 0.0);
+    fprintf(stderr, "\nwarp 0 of CTA 0, per unit (ns: flags-ok, mma-done, stored):");
+    for (int u = 0; u < 6; ++u)
+      if (h[8 + 3 * u]) fprintf(stderr, " [%.0f %.0f %.0f]", (double)(h[8 + 3 * u] - t0), (double)(h[9 + 3 * u] - t0),
+                                (double)(h[10 + 3 * u] - t0));
     fprintf(stderr, "\n");
   }
   return check_launch("small_fused_kernel");

@@ -22,4 +22,10 @@ CMD3="python bench.py --config 3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-st
 $CMD3 > $OUT/plain3.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"contract_f64|prep_fast" -c 2 -o $OUT/full_cfg3 $CMD3 > $OUT/ncu_full3.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"peaks_vec" -c 1 -o $OUT/full_peaks5 python tools/bench_extras.py > $OUT/ncu_peaks.log 2>&1
+# the one-launch small-m kernel (cfg1 / cfg2) and its launch lists
+for c in 1 2; do
+  CMDS="python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+  ncu --set full --clock-control none --import-source on -k regex:"small_fused" -c 1 -o $OUT/full_cfg$c $CMDS > $OUT/ncu_full$c.log 2>&1
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file $OUT/launches_cfg$c.csv $CMDS > $OUT/ncu_launch$c.log 2>&1
+done
 ls -la $OUT

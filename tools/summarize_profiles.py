@@ -105,17 +105,18 @@ def main():
         text = f.read_text().strip()
         if text:
             (dst / f"{rnd}_{f.name}").write_text(json.dumps(json.loads(text.splitlines()[-1]), indent=1) + "\n")
-    if (src / "launches_cfg5.csv").exists():
-        shutil.copy(src / "launches_cfg5.csv", dst / f"{rnd}_launches_cfg5.csv")
-        (dst / f"{rnd}_launch_shares_cfg5.json").write_text(
-            json.dumps(launch_shares(src / "launches_cfg5.csv"), indent=1) + "\n")
+    for c in (5, 1, 2):
+        if (src / f"launches_cfg{c}.csv").exists():
+            shutil.copy(src / f"launches_cfg{c}.csv", dst / f"{rnd}_launches_cfg{c}.csv")
+            (dst / f"{rnd}_launch_shares_cfg{c}.json").write_text(
+                json.dumps(launch_shares(src / f"launches_cfg{c}.csv"), indent=1) + "\n")
     tpath = dst / "traffic.json"
     traffic = json.loads(tpath.read_text()) if tpath.exists() else {}
     for rep in sorted(src.glob("full_cfg*.ncu-rep")):
         cfg = rep.stem.split("cfg")[1]
         ks = ncu_raw(rep)
         (dst / f"{rnd}_ncu_cfg{cfg}.json").write_text(json.dumps(ks, indent=1) + "\n")
-        con = [k for k in ks if "contract" in k["kernel"]]
+        con = [k for k in ks if "contract" in k["kernel"] or "small_fused" in k["kernel"]]
         if con:
             k = con[-1]
             traffic[cfg] = k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
@@ -164,7 +165,10 @@ def readme(rnd, dst):
     L.append("* roofline frac = algorithmic work / K2 time / measured peak (MEASURED_PEAKS.json). fp64 configs "
              "exceed 1.0 because the homo map is computed once per mirrored tile pair (algorithmic flops count "
              "the full map); executed frac counts the flops the kernel actually issues, in fp16-equivalents (F16F8: the "
-             "fp16 hi.hi product + two e4m3 cross products at twice the rate = 2; bf16x3: 3).")
+             "fp16 hi.hi product + two e4m3 cross products at twice the rate = 2; bf16x3: 3). cfg1 / cfg2 run as ONE "
+             "kernel (small_fused_kernel: K1 + contraction), so their 'K2 ms' is the whole step, timed as an "
+             "event-free graph rotating over independent buffers (> 4x L2); the two-kernel path's K2-only "
+             "fraction is not comparable.")
     ref = _load(dst / f"{rnd}_bench_reference_cfg5.json")
     if ref and b5:
         L.append(f"* Reference arm ({ref['cpu_baseline']['kind']} on {ref['cpu_baseline']['cores']} host threads, "
@@ -178,7 +182,7 @@ def readme(rnd, dst):
     L += ["", "## ncu (cold, serialised launches; per-launch numbers)", "",
           "| kernel | config | duration ms | DRAM read MB | DRAM write MB | tensor pipe active % | SM MHz |",
           "|---|---|---|---|---|---|---|"]
-    for tag in ("cfg5", "cfg3", "peaks5"):
+    for tag in ("cfg5", "cfg3", "cfg1", "cfg2", "peaks5"):
         ks = _load(dst / f"{rnd}_ncu_{tag}.json") or []
         for k in ks:
             tp = k.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 0.0)
