@@ -141,11 +141,12 @@ def readme(rnd, dst):
          f"Produced by `tools/profile_round.sh` under gpurun and summarised by "
          f"`tools/summarize_profiles.py {rnd}`; every number below is read from the JSON files here.", "",
          f"Files: `{rnd}_bench_cfg{{1..5}}.json` (bench.py lines), `{rnd}_bench_reference_cfg5.json` "
-         f"(reference arm), `{rnd}_launches_cfg5.csv` + `{rnd}_launch_shares_cfg5.json` (ncu launch list of "
-         f"the headline command), `{rnd}_ncu_cfg{{5,3}}.json`, `{rnd}_ncu_peaks5.json` (selected metrics of "
+         f"(reference arm), `{rnd}_launches_cfg{{5,1,2}}.csv` + `{rnd}_launch_shares_cfg{{5,1,2}}.json` (ncu launch "
+         f"lists of the bench commands), `{rnd}_ncu_cfg{{5,3,1,2}}.json`, `{rnd}_ncu_peaks5.json` (selected metrics of "
          f"`ncu --set full` captures), `{rnd}_extras.json` (tools/bench_extras.py: Hilbert route, find_peaks, "
          f"serialization), `traffic.json` (dram bytes per K2 launch, read by bench.py for `roofline.traffic`).",
-         "", "## Headline (bench.py, CUDA events over a graph of K steps, clocks sampled during the timed region)",
+         "", "## Headline (bench.py: CUDA events around a graph of K steps -- per-step event pairs for cfg3-5, "
+         "event-free rotation over independent buffers for cfg1 / cfg2; clocks sampled during the timed region)",
          "", "| config | ms/step | GElem/s | K2 ms | roofline frac | executed frac | e2e GElem/s | SM MHz (reasons) |",
          "|---|---|---|---|---|---|---|---|"]
     b5 = None
