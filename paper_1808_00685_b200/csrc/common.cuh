@@ -17,6 +17,25 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 int check_launch(const char* what);
 
+// Sign flip and |x| bit pattern on the INTEGER pipe.  Written as inline PTX:
+// plain C++ bit tricks (xor / and on __double_as_longlong) are turned back into
+// DADD -x / DADD |x| by the compiler, which queue on the FP64 pipe behind the
+// DMMAs of co-resident CTAs (ncu: ~10 % of contract_f64's samples were
+// "math pipe throttle" stalls on those DADDs).
+// (ptxas also recognises a 64-bit xor / and of the sign bit as fneg / fabs, so
+// the sign bit is flipped by a 32-bit add on the high word.)
+__device__ __forceinline__ double neg_bits(double x) {
+  int hi = __double2hiint(x), lo = __double2loint(x);
+  asm volatile("add.s32 %0, %0, 0x80000000;" : "+r"(hi));
+  return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  unsigned hi = (unsigned)__double2hiint(x), lo = (unsigned)__double2loint(x);
+  asm volatile("shl.b32 %0, %0, 1;" : "+r"(hi));   // drop the sign bit ...
+  asm volatile("shr.b32 %0, %0, 1;" : "+r"(hi));   // ... without an and-mask ptxas could fold
+  return ((unsigned long long)hi << 32) | lo;
+}
+
 // Positive doubles order like their bit patterns: atomicMax on uint64 bits.
 __device__ __forceinline__ void atomic_max_abs(unsigned long long* dst, double v) {
   unsigned long long bits = __double_as_longlong(fabs(v));

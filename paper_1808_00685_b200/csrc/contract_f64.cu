@@ -122,12 +122,8 @@ __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int
 // like |x| and Inf / NaN patterns exceed every finite one.  (fp64 fmax / fabs /
 // isfinite would queue on the FP64 pipe behind the DMMAs of the co-resident CTAs.)
 constexpr unsigned long long kInfBits = 0x7ff0000000000000ull;
-__device__ __forceinline__ unsigned long long absbits(double x) {
-  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffull;
-}
-__device__ __forceinline__ double dneg(double x) {   // sign flip as an integer op
-  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
-}
+__device__ __forceinline__ unsigned long long absbits(double x) { return abs_bits(x); }
+__device__ __forceinline__ double dneg(double x) { return neg_bits(x); }   // sign flip, integer pipe
 
 __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, int i0, int j0,
                                            const double* Cphi, const double* Cpsi, int tid, int nthreads,
