@@ -94,9 +94,11 @@ __device__ __forceinline__ void decode_tile(const ContractParams& p, int& I, int
   }
   // row tile I0 + d owns columns [0, I0) U [I0 + d, T): count T - d.
   // S(d) = d T - d (d - 1) / 2 tiles precede it.
-  const double T = (double)p.T;
-  const double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)b;
-  long long d = (long long)floor(((2.0 * T + 1.0) - sqrt(fmax(disc, 0.0))) * 0.5);
+  // first guess in fp32 (an fp64 sqrt would queue on the FP64 pipe behind the
+  // DMMAs of co-resident CTAs), corrected exactly below
+  const long long t2 = 2LL * p.T + 1;
+  const long long disc = t2 * t2 - 8LL * b;
+  long long d = (long long)((float)t2 - sqrtf((float)(disc > 0 ? disc : 0))) / 2;
   auto S = [&](long long dd) { return dd * (long long)p.T - dd * (dd - 1) / 2; };
   if (d < 0) d = 0;
   while (d > 0 && S(d) > b) --d;
@@ -168,29 +170,33 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
     }
   }
   int bad = (bphi >= kInfBits) + (bpsi >= kInfBits);   // lanes holding a non-finite value
-  double mphi = __longlong_as_double((long long)min(bphi, kInfBits));
-  double mpsi = __longlong_as_double((long long)min(bpsi, kInfBits));
-  mphi = warp_max(mphi);
-  mpsi = warp_max(mpsi);
+  bphi = min(bphi, kInfBits);
+  bpsi = min(bpsi, kInfBits);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {   // integer max of the bit patterns (fmax would use the FP64 pipe)
+    bphi = max(bphi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)bphi, o));
+    bpsi = max(bpsi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)bpsi, o));
+  }
   bad = warp_sum(bad);
-  // one set of atomics per CTA (tens of thousands of CTAs hit the same three words)
-  __shared__ double red_m[2][8];
+  // one set of atomics per CTA (tens of thousands of CTAs hit the same three
+  // words); the max stays on bit patterns (non-negative doubles order like them)
+  __shared__ unsigned long long red_m[2][8];
   __shared__ int red_b[8];
   const int w = tid >> 5, nw = nthreads >> 5;
   if (lane == 0) {
-    red_m[0][w] = mphi;
-    red_m[1][w] = mpsi;
+    red_m[0][w] = bphi;
+    red_m[1][w] = bpsi;
     red_b[w] = bad;
   }
   __syncthreads();
   if (tid == 0) {
     for (int i = 1; i < nw; ++i) {
-      mphi = fmax(mphi, red_m[0][i]);
-      mpsi = fmax(mpsi, red_m[1][i]);
+      bphi = max(bphi, red_m[0][i]);
+      bpsi = max(bpsi, red_m[1][i]);
       bad += red_b[i];
     }
-    atomic_max_abs(&p.stats[0], mphi);
-    atomic_max_abs(&p.stats[1], mpsi);
+    if (bphi) atomicMax(&p.stats[0], bphi);
+    if (bpsi) atomicMax(&p.stats[1], bpsi);
     if (bad) atomicAdd(&p.stats[2], (unsigned long long)bad);
   }
 }

@@ -278,9 +278,11 @@ __device__ __forceinline__ void fused_decode(const SmallParams& p, long long b, 
     mode = kFPlain;
     return;
   }
-  const double T = (double)p.T;
-  const double disc = (2.0 * T + 1.0) * (2.0 * T + 1.0) - 8.0 * (double)b;
-  long long d = (long long)floor(((2.0 * T + 1.0) - sqrt(fmax(disc, 0.0))) * 0.5);
+  // first guess in fp32 (an fp64 sqrt would queue on the FP64 pipe behind the
+  // DMMAs of co-resident CTAs), corrected exactly below
+  const long long t2 = 2LL * p.T + 1;
+  const long long disc = t2 * t2 - 8LL * b;
+  long long d = (long long)((float)t2 - sqrtf((float)(disc > 0 ? disc : 0))) / 2;
   auto S = [&](long long dd) { return dd * (long long)p.T - dd * (dd - 1) / 2; };
   if (d < 0) d = 0;
   while (d > 0 && S(d) > b) --d;
