@@ -531,8 +531,7 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   // global warp index, CTA-minor: consecutive work items land on different SMs
   const int gw = warp * (int)gridDim.x + blockIdx.x;
   const int W = gridDim.x * kFusedWarps;
-  // this launch's epoch (bumped only by the last CTA of the previous launch)
-  const int want = *reinterpret_cast<volatile const int*>(p.work + kWEpoch) + 1;
+
   int* flags = p.work + kWFlags;
   unsigned long long* tr = p.trace ? p.trace + 32 * blockIdx.x : nullptr;
   int unit_no = 0;
@@ -544,7 +543,12 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     sincospi(-2.0 * (double)q / (double)p.p1.m, &sv, &cv);
     tw[q] = make_double2(cv, sv);
   }
+  // programmatic dependent launch: everything above overlapped the previous
+  // kernel's tail; from here on memory written by it is visible
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
   __syncthreads();
+  // this launch's epoch (bumped only by the last CTA of the previous launch)
+  const int want = *reinterpret_cast<volatile const int*>(p.work + kWEpoch) + 1;
   const int G = (p.p1.m / 2 + 1 + 3) / 4;         // 4-bin groups per channel block (<= kMaxGroups)
   if (warp < kK1Warps) {
     // K1 tasks (block, bin group) on the first kK1Warps warps of every CTA, CTA-minor
@@ -838,6 +842,7 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
       __threadfence();
     }
   }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
 static long long fused_tile_count(int n1, int n2, int homo, int row0, int row1) {
@@ -867,9 +872,15 @@ static int launch_fused(const SmallParams& p, cudaStream_t st) {
   cfg.blockDim = dim3(32 * fused_warps<NCH>());
   cfg.dynamicSmemBytes = fused_smem<NCH>();
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  // programmatic dependent launch: this grid's launch and prologue overlap the
+  // previous kernel's tail (griddepcontrol.wait in the kernel orders memory);
+  // CORR2D_SMALL_PDL=0 disables
+  static const int pdl = [] { const char* e = getenv("CORR2D_SMALL_PDL"); return e && e[0] == '0' ? 0 : 1; }();
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl;
+  attr[1].id = cudaLaunchAttributeCooperative;
+  attr[1].val.cooperative = 1;
   cfg.attrs = attr;
   // the cooperative attribute (guaranteed co-residency) costs ~7 us per launch in
   // a graph (cfg1: 22 vs 15 us per step); with one CTA per SM from the occupancy
@@ -877,7 +888,7 @@ static int launch_fused(const SmallParams& p, cudaStream_t st) {
   // barrier traps rather than hangs if that is ever violated.  CORR2D_SMALL_COOP=1
   // restores the attribute.
   static const int coop = [] { const char* e = getenv("CORR2D_SMALL_COOP"); return e && e[0] == '1' ? 1 : 0; }();
-  cfg.numAttrs = coop;
+  cfg.numAttrs = 1 + coop;
   static unsigned long long* trace = nullptr;
   const char* te = getenv("CORR2D_SMALL_TRACE");   // read per launch (experiments toggle it)
   const bool want_trace = te && te[0] == '1';
