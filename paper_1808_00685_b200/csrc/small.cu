@@ -856,16 +856,21 @@ static int fused_smem() { return CORR2D_SMALL_TMA ? fused_warps<NCH>() * kStgPer
 
 template <int NCH>
 static int launch_fused(const SmallParams& p, cudaStream_t st) {
-  static int grid = 0;
+  // one CTA per SM of the CURRENT device (cached per device: the grid must
+  // never exceed what is co-resident, or the flag waits could not complete)
+  static int grids[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(CORR2D_ERR_UNSUPPORTED, "small_fused_kernel: device index >= 64");
+  int& grid = grids[dev];
   if (grid == 0) {
-    int dev = 0, sms = 148, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(small_fused_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem<NCH>());
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fused_kernel<NCH>, 32 * fused_warps<NCH>(),
                                                   fused_smem<NCH>());
-    if (per_sm < 1) return fail(CORR2D_ERR_CUDA, "small_fused_kernel: no resident CTA");
-    grid = per_sm * sms;
+    if (per_sm < 1 || sms < 1) return fail(CORR2D_ERR_CUDA, "small_fused_kernel: no resident CTA");
+    grid = sms;   // one per SM even if more would fit: one K1 slot set and one arrival per SM
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
