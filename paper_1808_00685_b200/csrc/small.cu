@@ -205,32 +205,15 @@ int launch_prep_small(const PrepParams& p, cudaStream_t st) {
 constexpr int kFT = 32;          // warp tile edge (output rows and columns)
 // one CTA per SM (every CTA resident: the flag waits cannot deadlock), as many
 // warps as the register file holds: 16 at <= 128 registers (depth <= 16), 12 above
-// CORR2D_SMALL_TMA: full units leave through a per-warp shared-memory staging
-// tile and bulk (TMA) copies, so a warp's output drains while it runs the next
-// unit's MMAs (register stores made the warps alternate, in step, between a
-// DMMA-bound and a store-bound phase); 8 warps then fit the staging tiles.
-#ifndef CORR2D_SMALL_TMA
-#define CORR2D_SMALL_TMA 0
-#endif
-#if CORR2D_SMALL_TMA
-#ifndef CORR2D_SMALL_W12
-#define CORR2D_SMALL_W12 8
-#endif
-#ifndef CORR2D_SMALL_W34
-#define CORR2D_SMALL_W34 8
-#endif
-#else
+// Warps per CTA (one CTA per SM): 16 at <= 128 registers (depth <= 16), 12 above.
+// (Measured alternatives: 8 / 16 warps at depth 24, a bulk-copy
+// staging epilogue, CTA-contiguous unit ranges -- none faster.)
 #ifndef CORR2D_SMALL_W12
 #define CORR2D_SMALL_W12 16
 #endif
 #ifndef CORR2D_SMALL_W34
 #define CORR2D_SMALL_W34 12
 #endif
-#endif
-// staging tile per warp (doubles): direct [2 planes][16 rows][34], mirror [2][32 rows][18]
-// (padded rows: conflict-light fragment writes; each row is its own bulk copy)
-constexpr int kSD = 34, kSM = 18;
-constexpr int kStgPerWarp = 2 * 16 * kSD + 2 * 32 * kSM;
 template <int NCH> __host__ __device__ constexpr int fused_warps() { return NCH <= 2 ? CORR2D_SMALL_W12 : CORR2D_SMALL_W34; }
 
 struct SmallParams {
@@ -526,7 +509,6 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   constexpr int kK1Warps = 4;                     // warps per CTA that take K1 blocks
   __shared__ double2 tw[32];
   __shared__ double ys[kK1Warps][32 * 32];        // K1 sample columns [t][lane] per warp
-  extern __shared__ __align__(128) double stg[];   // CORR2D_SMALL_TMA: per-warp output staging tiles
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // global warp index, CTA-minor: consecutive work items land on different SMs
   const int gw = warp * (int)gridDim.x + blockIdx.x;
@@ -580,22 +562,11 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
   bool all_ready = false;                          // every K1 task of this launch seen finished
   const int k1_tasks = (p.nb1 + (p.homo ? 0 : (p.n2 + 31) / 32)) * G;
   const long long units = 2 * p.tiles;
-#ifndef CORR2D_SMALL_CHUNK
-#define CORR2D_SMALL_CHUNK 0
-#endif
-  // static assignment (a shared claim counter measured slower: thousands of
-  // warps serialise on one L2 atomic).  CHUNK: every CTA owns a contiguous run
-  // of units (neighbouring tiles share their row operands, served from L1),
-  // its warps interleaved inside it; else a grid-wide round robin.
-#if CORR2D_SMALL_CHUNK
-  const long long per = (units + gridDim.x - 1) / gridDim.x;
-  const long long u_end = min(units, per * (blockIdx.x + 1));
-  const long long u_step = kFusedWarps;
-  for (long long u = per * blockIdx.x + warp; u < u_end;) {
-#else
-  const long long u_end = units, u_step = W;
-  for (long long u = gw; u < u_end;) {
-#endif
+  // static round robin over every warp of the grid (a shared claim counter
+  // measured slower -- thousands of warps serialise on one L2 atomic -- and so
+  // did CTA-contiguous unit ranges)
+  const long long u_step = W;
+  for (long long u = gw; u < units;) {
     int I, J, mode;
     fused_decode(p, p.tile0 + (u >> 1), I, J, mode);
     const int h = (int)(u & 1);
@@ -616,11 +587,6 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     const bool ut = tr && blockIdx.x == 0 && warp == 0 && lane == 0 && unit_no < 6;
     if (tr) ++unit_no;
     if (ut) tr[8 + 3 * (unit_no - 1)] = global_ns();
-#ifdef CORR2D_SMALL_DESYNC
-    // experiment: odd warps start half a unit late, so that DMMA and store phases
-    // of the two warp halves alternate instead of running in step
-    if (first && (warp & 1)) __nanosleep(CORR2D_SMALL_DESYNC);
-#endif
     if (tr && first && lane == 0 && warp == 0) tr[2] = global_ns();
     first = false;
     double aphi[4][4], apsi[4][4];
@@ -668,59 +634,6 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     // ---- epilogue: lane holds rows (lr, lr + 8) x columns (2 lk, 2 lk + 1) of each n8 tile
     const bool interior = mode != kFDiag && p.vec && r0 + 16 <= min(p.n1, p.row1) && (J + 1) * kFT <= p.n2 &&
                           (mode == kFPlain || (J * kFT >= p.row0 && (J + 1) * kFT <= p.row1));
-#if CORR2D_SMALL_TMA
-    if (interior) {
-      // full 16 x 32 unit: fragments -> this warp's staging tile -> bulk copies
-      // (256-B direct rows, 128-B mirror rows); the copies drain while the warp
-      // moves on, and the tile is rewritten only after they have read it
-      const bool direct = mode != kFTransOnly, mirror = mode != kFPlain;
-      double* sd = stg + warp * kStgPerWarp;
-      double* sm = sd + 2 * 16 * kSD;
-      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-      __syncwarp();
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int rl = lr + 8 * hh, cl = nt * 8 + 2 * lk;
-          const double f0 = aphi[nt][2 * hh], f1 = aphi[nt][2 * hh + 1];
-          const double s0 = apsi[nt][2 * hh], s1 = apsi[nt][2 * hh + 1];
-          mphi = max(mphi, max(abits(f0), abits(f1)));
-          mpsi = max(mpsi, max(abits(s0), abits(s1)));
-          if (direct) {
-            *reinterpret_cast<double2*>(sd + rl * kSD + cl) = make_double2(f0, f1);
-            *reinterpret_cast<double2*>(sd + 16 * kSD + rl * kSD + cl) = make_double2(s0, s1);
-          }
-          if (mirror) {
-            sm[cl * kSM + rl] = f0;
-            sm[(cl + 1) * kSM + rl] = f1;
-            sm[32 * kSM + cl * kSM + rl] = neg_bits(s0);
-            sm[32 * kSM + (cl + 1) * kSM + rl] = neg_bits(s1);
-          }
-        }
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (direct) {
-        const int plane = lane >> 4, row = lane & 15;
-        const double* src = sd + plane * 16 * kSD + row * kSD;
-        double* dst = (plane ? p.psi : p.phi) + (long long)(r0 + row - p.row0) * p.ld_out + J * kFT;
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 256;\n"
-                     ::"l"(dst), "r"(static_cast<unsigned>(__cvta_generic_to_shared(src))) : "memory");
-      }
-      if (mirror) {
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const int c = lane + 32 * k, plane = c >> 5, row = c & 31;
-          const double* src = sm + plane * 32 * kSM + row * kSM;
-          double* dst = (plane ? p.psi : p.phi) + (long long)(J * kFT + row - p.row0) * p.ld_out + r0;
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 128;\n"
-                       ::"l"(dst), "r"(static_cast<unsigned>(__cvta_generic_to_shared(src))) : "memory");
-        }
-      }
-      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      continue;
-    }
-#else
     if (interior) {
       // branch-free fast path: full 16 x 32 unit, 16-byte direct stores, 8-byte mirror stores
       const bool direct = mode != kFTransOnly, mirror = mode != kFPlain;
@@ -748,7 +661,6 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
         }
       continue;
     }
-#endif
     const bool direct = mode != kFTransOnly;
     const bool mirror = mode != kFPlain;
 #pragma unroll
@@ -807,9 +719,6 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     mpsi = max(mpsi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mpsi, o));
   }
   bad = warp_sum(bad);
-#if CORR2D_SMALL_TMA
-  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-#endif
   unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWStats);
   if (lane == 0) {
     if (mphi) atomicMax(&acc[0], mphi);
@@ -852,9 +761,6 @@ static long long fused_tile_count(int n1, int n2, int homo, int row0, int row1) 
 }
 
 template <int NCH>
-static int fused_smem() { return CORR2D_SMALL_TMA ? fused_warps<NCH>() * kStgPerWarp * (int)sizeof(double) : 0; }
-
-template <int NCH>
 static int launch_fused(const SmallParams& p, cudaStream_t st) {
   // one CTA per SM of the CURRENT device (cached per device: the grid must
   // never exceed what is co-resident, or the flag waits could not complete)
@@ -866,16 +772,14 @@ static int launch_fused(const SmallParams& p, cudaStream_t st) {
   if (grid == 0) {
     int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(small_fused_kernel<NCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, fused_smem<NCH>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fused_kernel<NCH>, 32 * fused_warps<NCH>(),
-                                                  fused_smem<NCH>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fused_kernel<NCH>, 32 * fused_warps<NCH>(), 0);
     if (per_sm < 1 || sms < 1) return fail(CORR2D_ERR_CUDA, "small_fused_kernel: no resident CTA");
     grid = sms;   // one per SM even if more would fit: one K1 slot set and one arrival per SM
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(32 * fused_warps<NCH>());
-  cfg.dynamicSmemBytes = fused_smem<NCH>();
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   // programmatic dependent launch: this grid's launch and prologue overlap the
