@@ -317,6 +317,32 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
             dpsi = max(dpsi, absbits(s0));
           }
         }
+#ifndef CORR2D_F64_REG_MIRROR
+#define CORR2D_F64_REG_MIRROR 1
+#endif
+#if CORR2D_F64_REG_MIRROR
+    // whole mirrored tile in bounds: the transpose also leaves straight from the
+    // fragments (8-byte stores, 4 rows x 64 B per warp instruction) -- no
+    // shared-memory staging, no barriers
+    if (mode == kMirror && j0 >= p.row0 && j0 + kBN <= p.row1 && i0 + kBM <= p.n2) {
+#pragma unroll
+      for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gi = i0 + wm * 16 * kMT + mt * 16 + lr + 8 * h;
+            const int gj = j0 + wn * 32 + nt * 8 + 2 * lk;
+            const long long o = (long long)(gj - p.row0) * p.ld_out + gi;
+            __stcs(p.phi + o, acc_phi[mt][nt][2 * h]);
+            __stcs(p.psi + o, dneg(acc_psi[mt][nt][2 * h]));
+            __stcs(p.phi + o + p.ld_out, acc_phi[mt][nt][2 * h + 1]);
+            __stcs(p.psi + o + p.ld_out, dneg(acc_psi[mt][nt][2 * h + 1]));
+          }
+      write_tile(p, kPlain, i0, j0, nullptr, nullptr, tid, kThreads, lane, true, dphi, dpsi);
+      return;
+    }
+#endif
     if (mode == kPlain) {       // nothing left to stage
       write_tile(p, kPlain, i0, j0, nullptr, nullptr, tid, kThreads, lane, true, dphi, dpsi);
       return;
