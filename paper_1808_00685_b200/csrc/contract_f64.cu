@@ -34,8 +34,13 @@ constexpr int kBN = 64;
 #define CORR2D_F64_MINB 3
 #endif
 constexpr int kKC = CORR2D_F64_KC; // depth chunk
+#ifndef CORR2D_F64_NBUF
+#define CORR2D_F64_NBUF 1
+#endif
+constexpr int kNBuf = CORR2D_F64_NBUF;                // operand buffers (2: double buffering)
 constexpr int kKS = kKC + 4;       // smem row stride (doubles): conflict-free fragments
 constexpr int kCS = kBN + 1;       // epilogue staging stride
+constexpr int kBufStride = 3 * 64 * (kKC + 4);   // doubles per operand buffer (A_phi, A_psi, B)
 // MT m16 row tiles per warp: 2 -> 4 warps of 32 x 32 (128 threads); 1 -> 8 warps
 // of 16 x 32 (256 threads, half the accumulator registers per thread)
 #ifndef CORR2D_F64_MT
@@ -225,9 +230,9 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
 
 __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel(const ContractParams p) {
   extern __shared__ __align__(16) double sm[];
-  double* As = sm;                     // [kBM][kKS]  A_phi
-  double* Ps = As + kBM * kKS;         // [kBM][kKS]  A_psi
-  double* Bs = Ps + kBM * kKS;         // [kBN][kKS]  B
+  double* As = sm;                     // [kNBuf][kBM][kKS]  A_phi (buffer stride kBufStride)
+  double* Ps = As + kBM * kKS;         // A_psi
+  double* Bs = Ps + kBM * kKS;         // B
 
   int I, J, mode;
   decode_tile(p, I, J, mode);
@@ -244,10 +249,14 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc_phi[a][bq][c] = acc_psi[a][bq][c] = 0.0;
 
-  for (int k0 = 0; k0 < p.mp; k0 += kKC) {
+  // depth chunks through NBUF shared-memory buffers (CORR2D_F64_NBUF = 2: the
+  // next chunk's cp.async overlaps this chunk's DMMAs)
+  auto issue = [&](int k0, int buf) {
     const int kc = min(kKC, p.mp - k0);  // multiple of 4
     const int vec = kc / 2;              // 16-byte chunks per row
-    if (k0 > 0) __syncthreads();
+    double* A = As + buf * kBufStride;
+    double* Pq = Ps + buf * kBufStride;
+    double* B = Bs + buf * kBufStride;
     for (int idx = tid; idx < kBM * vec; idx += kThreads) {
       // full chunks: vec = kKC / 2 is a power of two (shifts, not a division)
       const int r = kc == kKC ? idx / (kKC / 2) : idx / vec;
@@ -256,25 +265,39 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
       const bool va = gi < p.n1, vb = gj < p.n2;
       const long long oa = (long long)(va ? gi : 0) * p.ld_pack + k0 + 2 * v;
       const long long ob = (long long)(vb ? gj : 0) * p.ld_pack + k0 + 2 * v;
-      cp_async16(As + r * kKS + 2 * v, p.a_phi + oa, va);
-      cp_async16(Ps + r * kKS + 2 * v, p.a_psi + oa, va);
-      cp_async16(Bs + r * kKS + 2 * v, p.b + ob, vb);
+      cp_async16(A + r * kKS + 2 * v, p.a_phi + oa, va);
+      cp_async16(Pq + r * kKS + 2 * v, p.a_psi + oa, va);
+      cp_async16(B + r * kKS + 2 * v, p.b + ob, vb);
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  issue(0, 0);
+  for (int k0 = 0, c = 0; k0 < p.mp; k0 += kKC, ++c) {
+    const int kc = min(kKC, p.mp - k0);
+    const int buf = c % kNBuf;
+    if (kNBuf > 1 && k0 + kKC < p.mp) {
+      issue(k0 + kKC, (c + 1) % kNBuf);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
     __syncthreads();
+    const double* A = As + buf * kBufStride;
+    const double* Pq = Ps + buf * kBufStride;
+    const double* B = Bs + buf * kBufStride;
 #pragma unroll 4
     for (int kk = 0; kk < kc; kk += 4) {
       double ap[2][2], as[2][2], bf[4];
 #pragma unroll
       for (int mt = 0; mt < kMT; ++mt) {
         const int r = wm * 16 * kMT + mt * 16 + lr;
-        ap[mt][0] = As[r * kKS + kk + lk];
-        ap[mt][1] = As[(r + 8) * kKS + kk + lk];
-        as[mt][0] = Ps[r * kKS + kk + lk];
-        as[mt][1] = Ps[(r + 8) * kKS + kk + lk];
+        ap[mt][0] = A[r * kKS + kk + lk];
+        ap[mt][1] = A[(r + 8) * kKS + kk + lk];
+        as[mt][0] = Pq[r * kKS + kk + lk];
+        as[mt][1] = Pq[(r + 8) * kKS + kk + lk];
       }
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = B[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
 #pragma unroll
       for (int mt = 0; mt < kMT; ++mt)
 #pragma unroll
@@ -283,6 +306,8 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
           dmma_16x8x4(acc_psi[mt][nt], as[mt][0], as[mt][1], bf[nt]);
         }
     }
+    if (kNBuf == 1 || k0 + kKC < p.mp) __syncthreads();   // buffer free before it is refilled
+    if (kNBuf == 1 && k0 + kKC < p.mp) issue(k0 + kKC, 0);
   }
 
   // ---- epilogue.  Plain / mirrored tiles write their direct part straight
@@ -409,7 +434,7 @@ extern "C" int corr2d_contract_f64(
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
   if (tiles == 0) return CORR2D_OK;
-  const size_t smem_ops = 3 * (size_t)kBM * kKS * sizeof(double);
+  const size_t smem_ops = (size_t)kNBuf * kBufStride * sizeof(double);
   const size_t smem_epi = 2 * (size_t)kBM * kCS * sizeof(double);
   const size_t smem = smem_ops > smem_epi ? smem_ops : smem_epi;
   cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
