@@ -72,6 +72,7 @@ def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: Preproce
     return plan, homo
 
 
+@engine.on_device
 def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, reference="mean",
            resample: int | None = None, resample_to_common: int | None = None,
            interpolant: str = "spline", alpha: float = 0.0, norm=None, workers: int = 1,

@@ -784,6 +784,17 @@ struct Params2 {
   unsigned long long* stats;
 };
 
+// work-skipping switches exist only in profiling builds; the release kernel
+// compiles them away (constant 0), so it can never return skipped results
+template <class P> __device__ __forceinline__ int dbg_bits(const P& p) {
+#ifdef CORR2D_PROFILING
+  return p.dbg;
+#else
+  (void)p;
+  return 0;
+#endif
+}
+
 enum PairMode { kSkip = 4 };
 
 // Profiling: mbar_wait that adds the cycles it spent to a counter.
@@ -1202,7 +1213,7 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_t(&empty[stage], phase ^ 1, tr ? &tr_wait : nullptr);
           const uint32_t lbar = mapa_rank(su32(&full[stage]), lrank);
-          if (p.dbg & 4) {            // profiling: no operand traffic at all
+          if (dbg_bits(p) & 4) {            // profiling: no operand traffic at all
             mbar_arrive_remote(lbar);
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
@@ -1248,7 +1259,7 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             const uint32_t base = su32(stages + stage * STAGE_BYTES);
             const uint32_t are = base, aim = base + 2 * TILE_BYTES;
             const uint32_t bx = base + 4 * TILE_BYTES, by = base + 6 * TILE_BYTES;
-            if (!(p.dbg & 2)) {
+            if (!(dbg_bits(p) & 2)) {
 #pragma unroll
               for (int ks = 0; ks < 2; ++ks) {
                 const uint32_t off = ks * 32;
@@ -1272,7 +1283,7 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
               const uint64_t bx_h = desc_sw128(base + 4 * TILE_BYTES + off), bx_l = desc_sw128(base + 4 * TILE_BYTES + 64 + off);
               const uint64_t by_h = desc_sw128(base + 6 * TILE_BYTES + off), by_l = desc_sw128(base + 6 * TILE_BYTES + 64 + off);
               const uint32_t acc0 = (kb | ks) ? 1u : 0u;
-              if (p.dbg & 2) continue;
+              if (dbg_bits(p) & 2) continue;
               umma2_f16(d, are_h, bx_h, ID, acc0);
               umma2_f16(d, are_h, bx_l, ID, 1);
               umma2_f16(d, are_l, bx_h, ID, 1);
@@ -1465,7 +1476,7 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
                 else mx = __uint_as_float(mb[0]);
               }
               const long long ts0 = tr ? clock64() : 0;
-              if (!(p.dbg & 1))
+              if (!(dbg_bits(p) & 1))
                 stage_and_store_32_plane<STGBUF2 - 1>(wst, lane, v, mir, tsign, &outm.m[plane][0], &outm.m[plane][1],
                                             j0 + c * CH2, i0 + 32 * q, drop);
               if (tr) tr_store += clock64() - ts0;
@@ -1720,6 +1731,10 @@ extern "C" int corr2d_contract_tc(
     Params2 p{};
     p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = 1;
     p.f8 = pack_kind == CORR2D_PACK_F16F8;
+#ifdef CORR2D_PROFILING
+    // profiling builds only (tools/build_variant.sh -DCORR2D_PROFILING): store
+    // policy, work-skipping switches (results invalid) and per-role stall traces.
+    // The release library never reads them: p.dbg stays 0.
     const char* sp = getenv("CORR2D_STORE_POLICY");
     p.store_pol = sp ? atoi(sp) : 0;
     const char* dbg = getenv("CORR2D_DEBUG_SKIP");
@@ -1731,6 +1746,7 @@ extern "C" int corr2d_contract_tc(
       cudaMemsetAsync(trace_buf, 0, 1024 * 16 * sizeof(long long), st);
       p.trace = trace_buf;
     }
+#endif
     p.T1 =(n1 + BM - 1) / BM; p.T2 = (n2 + BN - 1) / BN;
     p.tile0 = tile0; p.tile1 = tile1;
     p.a = static_cast<const __nv_bfloat16*>(a); p.b = static_cast<const __nv_bfloat16*>(b);

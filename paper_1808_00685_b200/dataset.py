@@ -92,27 +92,32 @@ class SpectralDataset:
                 and tuple(self.axis_labels) == tuple(other.axis_labels))
 
 
+@dataclass(eq=False)
 class CorrelationSpectra:
     """Synchronous (sync = Phi) and asynchronous (asyn = Psi) correlation planes
-    with provenance (dataset.py:111-170)."""
+    with provenance (dataset.py:111-170): the reference's dataclass fields, so
+    ``dataclasses.fields`` / ``replace`` / ``asdict`` behave as on the reference
+    type (``replace`` re-validates, as there).  ``stats`` (device-side max|.|)
+    is a plain attribute, not a field."""
+
+    axis1: np.ndarray
+    axis2: np.ndarray
+    sync: np.ndarray
+    asyn: np.ndarray
+    ref1: np.ndarray
+    ref2: np.ndarray
+    normalization: float
+    engine: str
+    is_homo: bool
+    scaling_exponent: float = 0.0
 
     SYMMETRY_TOL = 1e-12
-    __slots__ = ("axis1", "axis2", "sync", "asyn", "ref1", "ref2", "normalization",
-                 "engine", "is_homo", "scaling_exponent", "stats")
+    stats = None
 
-    def __init__(self, axis1, axis2, sync, asyn, ref1, ref2, normalization, engine,
-                 is_homo, scaling_exponent=0.0):
-        self.axis1 = np.asarray(axis1, dtype=np.float64)
-        self.axis2 = np.asarray(axis2, dtype=np.float64)
-        self.sync = np.asarray(sync, dtype=np.float64)
-        self.asyn = np.asarray(asyn, dtype=np.float64)
-        self.ref1 = np.asarray(ref1, dtype=np.float64)
-        self.ref2 = np.asarray(ref2, dtype=np.float64)
-        self.normalization = normalization
-        self.engine = engine
-        self.is_homo = bool(is_homo)
-        self.scaling_exponent = scaling_exponent
-        self.stats = None
+    def __post_init__(self):
+        for name in ("axis1", "axis2", "sync", "asyn", "ref1", "ref2"):
+            setattr(self, name, np.asarray(getattr(self, name), dtype=np.float64))
+        self.is_homo = bool(self.is_homo)
         self.validate()
 
     @classmethod

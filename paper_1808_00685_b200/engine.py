@@ -61,6 +61,46 @@ def require_device(device=None):
     return lib, dev
 
 
+class device_scope:
+    """Run a call on `dev`: makes it the current CUDA device (the C entry points
+    read the SM count and launch on the current device) and its current stream
+    the one kernels are launched on."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self._ctx = None
+
+    def __enter__(self):
+        t = torch()
+        if self.dev is not None and self.dev.type == "cuda" and self.dev.index != t.cuda.current_device():
+            self._ctx = t.cuda.device(self.dev)
+            self._ctx.__enter__()
+        return self.dev
+
+    def __exit__(self, *exc):
+        if self._ctx is not None:
+            self._ctx.__exit__(*exc)
+        return False
+
+
+def on_device(fn):
+    """Decorator for public entry points with a ``device=`` keyword: the whole
+    call (plan build, launches, synchronisation, copies) runs with that device
+    current, so kernels, streams and pointers all belong to it."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        device = kwargs.get("device")
+        if device is None:
+            return fn(*args, **kwargs)
+        _, dev = require_device(device)
+        kwargs["device"] = dev
+        with device_scope(dev):
+            return fn(*args, **kwargs)
+    return wrapper
+
+
 def stream_handle():
     return ctypes_void(torch().cuda.current_stream().cuda_stream)
 
@@ -570,7 +610,9 @@ def run_streamed(make_plan, n1: int, n2: int, dtype, blocks, out=None, check=Non
         hs, ha = out
     stats = {"max_abs_sync": 0.0, "max_abs_async": 0.0}
     first = None
+    plan = None
     for k, (r0, r1) in enumerate(blocks):
+        plan = None                   # release the previous block's planes first
         plan = make_plan((r0, r1))
         plan.launch()
         sync()

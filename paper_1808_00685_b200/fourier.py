@@ -95,6 +95,7 @@ class DeviceCorrelationSpectra:
         return CorrelationSpectra._trusted(sync=s, asyn=a, **self.meta)
 
 
+@engine.on_device
 def correlate_ft(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers: int = 1, *,
                  dtype="float64", out=None, return_device: bool = False, device=None, rows=None):
     """Synchronous and asynchronous correlation via the Fourier route

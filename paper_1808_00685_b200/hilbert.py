@@ -53,6 +53,7 @@ def _plan(dyn1, dyn2, norm, rows, device):
     return plan, homo, dyn2, constant
 
 
+@engine.on_device
 def correlate_ht(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers: int = 1, *,
                  out=None, return_device: bool = False, device=None, rows=None) -> CorrelationSpectra:
     """Synchronous and asynchronous correlation via the Hilbert route
@@ -87,6 +88,7 @@ def correlate_ht(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers
     return CorrelationSpectra._trusted(sync=s, asyn=a, **meta)
 
 
+@engine.on_device
 def sync_direct(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers: int = 1, *,
                 device=None) -> np.ndarray:
     """Synchronous matrix by direct summation (hilbert.py:71-89)."""

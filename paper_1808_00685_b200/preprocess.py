@@ -84,56 +84,69 @@ class PreprocessSpec:
             raise DataError(f"scaling exponent must lie in [0, 1], got {self.scaling_exponent}")
 
 
+@dataclass(eq=False)
 class DynamicSpectra:
     """Reference-subtracted (optionally scaled) m x n matrix with provenance
-    (preprocess.py:90-120).  ``values`` may live on the device (a CUDA tensor);
-    the host copy is made lazily on first access."""
+    (preprocess.py:90-120): the same dataclass fields, so ``dataclasses.fields``
+    / ``replace`` / ``asdict`` work as on the reference type.
 
-    def __init__(self, spectral_axis, perturbation_axis, values, reference_used,
-                 scaling_exponent=0.0, sigma=None):
-        self.spectral_axis = np.asarray(spectral_axis, dtype=np.float64)
-        self.perturbation_axis = np.asarray(perturbation_axis, dtype=np.float64)
-        self._host = None
-        self._dev = None
-        if _is_tensor(values):
-            self._dev = values
-            shape = tuple(values.shape)
-        else:
-            self._host = np.asarray(values, dtype=np.float64)
-            shape = self._host.shape
-        self.reference_used = np.asarray(reference_used, dtype=np.float64)
-        self.scaling_exponent = scaling_exponent
-        self.sigma = sigma
+    ``values`` is a plain field from the caller's point of view.  When K1
+    produced it (``preprocess_dataset``), it stays in HBM until Python first
+    reads it; from then on -- and whenever it was set from a host array -- the
+    HOST array is authoritative and every device use uploads it again, so an
+    in-place edit of ``dyn.values`` (or of the caller's float64 array, which
+    ``np.asarray`` aliases exactly as the reference does) is always honoured,
+    as the reference re-reads ``dyn.values`` on every call."""
+
+    spectral_axis: np.ndarray
+    perturbation_axis: np.ndarray
+    values: np.ndarray
+    reference_used: np.ndarray
+    scaling_exponent: float = 0.0
+    sigma: np.ndarray | None = None
+
+    def __post_init__(self):
+        self.spectral_axis = np.asarray(self.spectral_axis, dtype=np.float64)
+        self.perturbation_axis = np.asarray(self.perturbation_axis, dtype=np.float64)
+        self.reference_used = np.asarray(self.reference_used, dtype=np.float64)
+        shape = tuple(self._dev.shape) if self._host is None else self._host.shape
         m, n = self.perturbation_axis.size, self.spectral_axis.size
         if shape != (m, n):
             raise DataError(f"dynamic matrix shape {shape} does not match axes ({m}, {n})")
         if self.reference_used.shape != (n,):
             raise DataError("reference_used length does not match the spectral axis")
 
-    @property
-    def values(self) -> np.ndarray:
+    def _get_values(self) -> np.ndarray:
         if self._host is None:
+            # first host read: from now on the host array is the source of truth
             self._host = self._dev.double().cpu().numpy()
+            self._dev = None
         return self._host
 
-    @values.setter
-    def values(self, v):
+    def _set_values(self, v):
         if _is_tensor(v):
             self._dev, self._host = v, None
         else:
             self._host, self._dev = np.asarray(v, dtype=np.float64), None
 
     def device_values(self, dev):
-        """The values as a contiguous CUDA tensor on `dev` (uploaded once)."""
+        """The values as a contiguous CUDA tensor on `dev`: the K1 output itself
+        while Python never saw the values, else a fresh upload of the host
+        array (no cache that could go stale)."""
         t = engine.torch()
-        if self._dev is None or self._dev.device != dev:
-            src = self._host if self._host is not None else self._dev
-            self._dev = engine.to_device(src, dev)
-        if not self._dev.is_contiguous():
-            self._dev = self._dev.contiguous()
-        if self._dev.dtype not in (t.float64, t.float32):
-            self._dev = self._dev.double()
-        return self._dev
+        if self._host is not None:
+            return engine.to_device(self._host, dev)
+        d = self._dev
+        if d.device != dev:
+            d = d.to(dev)
+        if d.dtype not in (t.float64, t.float32):
+            d = d.double()
+        return d.contiguous()
+
+    def device_identity(self):
+        """The device tensor while it is authoritative (else None): lets the
+        homo test compare two K1 outputs on the device."""
+        return self._dev if self._host is None else None
 
     @property
     def m(self) -> int:
@@ -142,6 +155,13 @@ class DynamicSpectra:
     @property
     def n(self) -> int:
         return int(self.spectral_axis.size)
+
+
+# `values` is a dataclass field (in __init__, fields(), replace(), asdict())
+# backed by the lazy host/device storage above.
+DynamicSpectra._host = None
+DynamicSpectra._dev = None
+DynamicSpectra.values = property(DynamicSpectra._get_values, DynamicSpectra._set_values)
 
 
 def _is_tensor(x) -> bool:
@@ -275,7 +295,8 @@ def apply_scaling(dyn: DynamicSpectra, sigma, alpha: float,
     if sigma.shape != (dyn.n,):
         raise DataError(f"sigma length {sigma.size} does not match n = {dyn.n}")
     if alpha == 0.0:
-        return DynamicSpectra(dyn.spectral_axis, dyn.perturbation_axis, dyn._dev if dyn._host is None else dyn._host,
+        src = dyn.device_identity()
+        return DynamicSpectra(dyn.spectral_axis, dyn.perturbation_axis, dyn.values if src is None else src,
                               dyn.reference_used, 0.0, sigma)
     _, dev = engine.require_device()
     sig = _zero_variance(dyn.spectral_axis, sigma, alpha, on_zero_variance)
