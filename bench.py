@@ -12,13 +12,14 @@ fp16 + e4m3 (F16F8) tcgen05 kernel) -- the largest map, the one BASELINE.json's 
 quoted on; it fits one GPU.  Outputs (8.6 GB per step) are far larger than the
 126 MB L2, so each step starts with a cold L2.
 
-Multi-GPU (torchrun, one process per GPU, NCCL): the homo tile enumeration is
-split into equal contiguous tile ranges (every tile computed once, mirrors
-included, so total work equals the 1-GPU work).  The packed spectra come from
-K1 over all channels on every rank with no collective (--spectra recompute, the
-default: cfg5 K1 takes 0.073 ms, less than moving its 105 MB output over NVLink)
-or from K1 on each rank's channel chunk plus one in-place NCCL all-gather
-(--spectra allgather).  Total work is fixed: "strong".
+Multi-GPU (torchrun, one process per GPU, NCCL): the public distributed call
+(sharded.py) -- each rank owns an area-balanced band of rows of
+the map (homo: the upper-triangle part; the mirror is implied), K1 runs on the
+rank's own channel chunk and the owners NCCL-broadcast their packed spectra
+(--spectra broadcast, the default) or every rank transforms every channel
+(--spectra recompute); the band's diagonal square is contracted while the
+broadcasts fly, then one rectangle piece per later owner.  Total work is fixed:
+"strong".
 
 --impl reference: the reference CPU path (oracle port of corrtwo's
 preprocess_dataset + correlate_ft, oracle/corr2d_oracle.py) on rank 0 with all
@@ -218,7 +219,7 @@ def config_block(case, wl, args):
             else "fp64 DMMA -> fp64 planes",
             "l2": "outputs per step >> 126 MB L2 (cold L2 each step)" if wl["out_bytes"] + wl["in_bytes"] > 4 * 126e6
             else "rotating over independent input / output buffers whose total exceeds 4 x the 126 MB L2 (no flush needed)",
-            "parallelism": (f"tile-range x{args.gpus}, spectra {args.spectra}" if args.gpus > 1 else "single GPU")}
+            "parallelism": (f"row bands x{args.gpus}, spectra {args.spectra}" if args.gpus > 1 else "single GPU")}
 
 
 def dist_setup(args):
@@ -244,7 +245,6 @@ def run_b200(args, case, wl, world, rank, local):
     import torch
     import paper_1808_00685_b200 as P
     from paper_1808_00685_b200 import api, engine
-    from paper_1808_00685_b200.engine_core import tile_range
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
@@ -257,20 +257,19 @@ def run_b200(args, case, wl, world, rank, local):
     spec = P.PreprocessSpec(
         resample=None if case.resample is None else P.ResampleSpec(case.resample, P.InterpolantKind.from_name(case.interpolant)),
         scaling_exponent=case.alpha)
-    # N > 1: K1 on this rank's channel chunk + one NCCL all-gather of the packed
-    # spectra (--spectra allgather), or K1 over all channels on every
-    # rank with no collective at all (--spectra recompute)
-    shard = (rank, world) if world > 1 and args.spectra == "allgather" else None
-    plan, homo = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev, spectra_shard=shard)
-    if world > 1:
-        # equal contiguous share of the contraction kernel's own tile enumeration
-        plan.tile0, plan.tile1 = tile_range(plan.tile_count(), world, rank)
+    # N > 1: this rank's band of the map through the public distributed plan
+    # (K1 on its chunk + owners' NCCL broadcasts, or K1 everywhere)
+    dist_kw = dict(group=None, spectra=args.spectra) if world > 1 else None
+    plan, homo = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev, distributed=dist_kw)
     stream = torch.cuda.current_stream()
 
     # ---- parity gate before timing (bench.py:98-115 style): sampled rows vs the oracle
     plan.launch()
     torch.cuda.synchronize()
-    plan.check(axes=(ds1.spectral_axis, (ds2 or ds1).spectral_axis))
+    if world > 1:
+        plan.finish(axes=(ds1.spectral_axis, (ds2 or ds1).spectral_axis))
+    else:
+        plan.check(axes=(ds1.spectral_axis, (ds2 or ds1).spectral_axis))
     parity = parity_gate(case, plan, world) if rank == 0 and world == 1 else None
 
     # ---- CUDA graphs: one step (K1, with the spectra all-gather for N > 1,
@@ -292,9 +291,7 @@ def run_b200(args, case, wl, world, rank, local):
     plans = [plan]
     if rotate:
         for _ in range(int(math.ceil(4 * 126e6 / foot)) - 1):
-            q, _ = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev, spectra_shard=shard)
-            if world > 1:
-                q.tile0, q.tile1 = plan.tile0, plan.tile1
+            q, _ = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=dev, distributed=dist_kw)
             plans.append(q)
     evs = [tuple(torch.cuda.Event(enable_timing=True, external=True) for _ in range(3)) for _ in range(args.steps)]
     ev_all = tuple(torch.cuda.Event(enable_timing=True) for _ in range(2))
@@ -320,10 +317,10 @@ def run_b200(args, case, wl, world, rank, local):
         for k in range(args.steps):
             one_step(k)
 
-    # gloo (BENCH_ONE_DEVICE test mode) collectives stage through the host and
-    # cannot be graph-captured: that mode launches eagerly
-    import torch.distributed as dist
-    eager = world > 1 and dist.get_backend() != "nccl"
+    # N > 1 launches eagerly (no CUDA graph): the band pieces wait on the NCCL
+    # broadcasts' work handles (stream waits, no host sync), and gloo
+    # (BENCH_ONE_DEVICE test mode) stages its collectives through the host
+    eager = world > 1
     if eager:
         class _Eager:
             def __init__(self, fn):
@@ -551,6 +548,8 @@ def executed_flops(plan, case, tc_peak, k2_ms):
         per_tile = products * 2 * 2 * 256 * 256 * hp       # products, x + y MMAs, 2 flops/MAC, depth hp
     elif getattr(plan, "small", False):
         per_tile = 2 * 2 * 32 * 32 * plan.ld_pack           # fused small-m kernel: 32 x 32 tiles, depth padded to 8
+    elif getattr(plan, "gauss", False):
+        per_tile = 2 * 64 * 64 * plan.mp                    # 3 kg slots, each feeding ONE plane's accumulator
     else:
         per_tile = 2 * 2 * 64 * 64 * plan.mp                # two planes, 2 flops/MAC
     f = float(tiles) * per_tile
@@ -610,8 +609,8 @@ def main(argv=None):
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--spectra", default="recompute", choices=["allgather", "recompute"],
-                    help="N > 1: shard K1 + NCCL all-gather of the packed spectra, or recompute K1 on every rank")
+    ap.add_argument("--spectra", default="broadcast", choices=["broadcast", "recompute"],
+                    help="N > 1: K1 on each rank's chunk + owners' NCCL broadcasts, or K1 on every rank")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -57,7 +57,8 @@ enum corr2d_pack {
   CORR2D_PACK_F64 = 1,       /* float64 operands (fp64 DMMA contraction)            */
   CORR2D_PACK_BF16X2 = 2,    /* bf16 hi/lo, k-block interleaved (bf16x3 tcgen05 contraction) */
   CORR2D_PACK_F64_TIME = 3,  /* float64 time-domain values, no DFT (Hilbert route, hilbert.py) */
-  CORR2D_PACK_F16F8 = 4      /* scaled fp16 hi + e4m3 hi / residual (fp16+fp8 tcgen05 contraction) */
+  CORR2D_PACK_F16F8 = 4,     /* scaled fp16 hi + e4m3 hi / residual (fp16+fp8 tcgen05 contraction) */
+  CORR2D_PACK_F64_GAUSS = 5  /* float64 three-product (Gauss) operands: corr2d_contract_f64_gauss */
 };
 
 enum corr2d_ref_mode { CORR2D_REF_MEAN = 0, CORR2D_REF_PROVIDED = 1, CORR2D_REF_NONE = 2 };
@@ -109,6 +110,18 @@ int corr2d_fft_factors(int m, int* factors, int max_factors);
  * (>= mp for F64; for BF16X2 and F16F8, in 2-byte units, >= 2 * mp + 64 and a
  * multiple of 64; both layouts are described at corr2d_contract_tc).  split_plane is unused (ABI v1 kept
  * the bf16 lo values in a separate plane; v2 interleaves them).
+ * CORR2D_PACK_F64_GAUSS: the complex product Y1 conj(Y2) with THREE real
+ * products instead of four (Gauss).  With a = Norm w Re Y1, b = Norm w Im Y1,
+ * c = Re Y2, d = -Im Y2 per bin: P1 = (a + b) c, P2 = a (d - c), P3 = b (c + d),
+ * sync = P1 - P3, async = P1 + P2.  A row (a_phi, ROLE_A) and a B row (b,
+ * ROLE_B) hold three segments of kg = corr2d_packed_depth(m, GAUSS) / 3 slots:
+ *   seg 1  A = a + b, B = c      : DC bin at slot 0, interior bins 1..I at 1..I
+ *   seg 2  A = a,     B = d - c  : the same bins
+ *   seg 3  A = -b,    B = c + d  : interior bins at 0..I-1; even m: the Nyquist
+ *                                  bin at slot I as A = a, B = c
+ * (I = ceil(m/2) - 1 interior bins; unused slots 0; a_psi is unused).  The DC /
+ * Nyquist bins are real, so the segments reproduce the exact weighted
+ * half-spectrum sum with 3 kg <= 3/4 of the 2 m multiply-adds of CORR2D_PACK_F64.
  * Any output pointer may be NULL.  `status` (device int32[4]; reset on the
  * stream by this call) receives the counters above; the host raises the
  * reference's errors from them after the stream synchronises.
@@ -140,6 +153,19 @@ int corr2d_prep(
 int corr2d_contract_f64(
     const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,
     int n1, int n2, int mp, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
+    double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream);
+
+/*
+ * The same contraction from CORR2D_PACK_F64_GAUSS operands (a: A rows, b: B
+ * rows, 3 kg slots each, kg a multiple of 4): one accumulator runs P1 over
+ * segment 1, is copied, then segment 3 goes into the sync accumulator and
+ * segment 2 into the async one -- 25 % fewer FP64 tensor-core MMAs than
+ * corr2d_contract_f64 for the same map.  Tiles, shards, mirroring, stats and
+ * errors as corr2d_contract_f64.  Reference: fourier.py:107-123.
+ */
+int corr2d_contract_f64_gauss(
+    const double* a, const double* b, int64_t ld_pack, int n1, int n2, int kg, int homo,
+    int row0, int row1, int64_t tile0, int64_t tile1,
     double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream);
 
 /*
@@ -186,44 +212,32 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
 
 /* ------------------------------- small m: the whole call in one launch ---- */
 /*
- * fp64 Fourier route for 2 <= m <= 32 without resampling (cfg1 m = 11, cfg2
- * m = 21): K1 of dataset 1 (and of dataset 2 unless raw2 == NULL, the homo
- * case) + the contraction, as ONE kernel (each output tile waits for the K1
- * of its own two channel blocks)
- * (csrc/small.cu).  Replaces the corr2d_prep + corr2d_contract_f64 sequence
- * that preprocess_dataset / dft_channels / correlate_ft (preprocess.py:262-275,
- * fourier.py:61-125) map onto; same argument meanings as those two calls.
- *   a_phi / a_psi / b : packed operand scratch (n1 / n1 / n2 rows of ld_pack
- *                       doubles, 16-B aligned; homo: b is its own n1 rows),
- *                       depth corr2d_small_depth(m) = m rounded up to 8 (zero
- *                       padded), ld_pack even and >= that depth
+ * fp64, 2 <= m <= 32, no resampling (cfg1 / cfg2 shapes): preprocess + DFT +
+ * contraction of a whole map in ONE kernel launch (csrc/small.cu).  Replaces
+ * the corr2d_prep + corr2d_contract_f64_gauss sequence that preprocess_dataset
+ * / dft_channels / correlate_ft (preprocess.py:262-275, fourier.py:61-125) map
+ * onto; same argument meanings as those two calls.  Every CTA owns one 64 x 64
+ * output block (corr2d_small_block_count blocks: homo the upper triangle,
+ * mirrored) and recomputes K1 for the block's channels into shared memory:
+ * CTAs never wait for each other (no co-residency requirement).
  *   ref_out* / sigma_out* : as corr2d_prep (either may be NULL)
- *   rows [row0, row1) (multiples of 32, or row1 = n1) and tiles [tile0, tile1)
- *   of corr2d_small_tile_count's enumeration (32 x 32 tiles; -1 = to the end)
- *                       select a row shard / a rank's share; every element has
- *                       the same bits for any partition
  *   status1 / status2  : device int32[4] each, the corr2d_prep status words
  *                       (status2 unused when homo); written by the call
  *   stats              : device uint64[3], as corr2d_contract_f64; written by the call
- *   work               : device int32[20 + 5 * (ceil(n1/32) + ceil(n2/32))]
- *                       (homo: no n2 term), zero-filled by the caller ONCE
- *                       before the first call on it: status / stat accumulators
- *                       (left zero by every call), a launch epoch and ready
- *                       flags per 32-channel block and 4-bin group (tiles wait
- *                       for their two blocks' K1 instead of a grid barrier).
- *                       One work buffer per concurrently running call.
+ *   work               : device int32[16], zero-filled by the caller ONCE before
+ *                       the first call on it: status / stat accumulators and an
+ *                       arrival counter, left zero by every call (the last CTA
+ *                       publishes and resets them).  One work buffer per
+ *                       concurrently running call.
  */
-int corr2d_small_depth(int m);
-int64_t corr2d_small_tile_count(int n1, int n2, int homo, int row0, int row1);
+int64_t corr2d_small_block_count(int n1, int n2, int homo);
 int corr2d_correlate_small_f64(
     int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
     int m, int n1, int n2,
     int ref_mode1, const double* ref_in1, const double* sigma_in1,
     int ref_mode2, const double* ref_in2, const double* sigma_in2,
     double alpha, int substitute_zero_var, double norm_const,
-    double* a_phi, double* a_psi, double* b, int64_t ld_pack,
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
-    int row0, int row1, int64_t tile0, int64_t tile1,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream);
 

@@ -19,7 +19,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcorr2d.so"
 OK, ERR_DATA, ERR_NUMERIC, ERR_OOM, ERR_CUDA, ERR_UNSUPPORTED = range(6)
 F64, F32 = 0, 1
 RESAMPLE_NONE, RESAMPLE_LINEAR, RESAMPLE_MATRIX = 0, 1, 2
-PACK_NONE, PACK_F64, PACK_BF16X2, PACK_F64_TIME, PACK_F16F8 = 0, 1, 2, 3, 4
+PACK_NONE, PACK_F64, PACK_BF16X2, PACK_F64_TIME, PACK_F16F8, PACK_F64_GAUSS = 0, 1, 2, 3, 4, 5
 ROLE_A, ROLE_B = 1, 2
 REF_MEAN, REF_PROVIDED, REF_NONE = 0, 1, 2
 ST_NONFINITE, ST_ZEROVAR, ST_FIRST_ZEROVAR = 0, 1, 2
@@ -28,9 +28,9 @@ INT32_MAX = 2**31 - 1
 # every symbol include/corr2d.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
-    "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
+    "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
     "corr2d_contract_tc", "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
-    "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_depth", "corr2d_small_tile_count",
+    "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count",
     "corr2d_correlate_small_f64",
 )
 
@@ -65,6 +65,10 @@ def _declare(lib):
         c_void, c_void, c_void, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_i64, c_i64,
         c_void, c_void, c_i64, c_void, c_void,
     ]
+    lib.corr2d_contract_f64_gauss.argtypes = [
+        c_void, c_void, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_i64, c_i64,
+        c_void, c_void, c_i64, c_void, c_void,
+    ]
     lib.corr2d_contract_bf16x3.argtypes = [
         c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
         c_i64, c_i64, c_void, c_void, c_i64, c_void, c_void,
@@ -81,22 +85,19 @@ def _declare(lib):
     lib.corr2d_format_repr.argtypes = [c_void, c_i64, c_void, c_i64, c_void]
     lib.corr2d_format_rows.argtypes = [c_int, c_void, c_void, c_void, c_void, c_i64, c_int, c_int, c_int,
                                        ctypes.c_char, c_int, c_int, c_void, c_i64, c_void]
-    lib.corr2d_small_depth.argtypes = [c_int]
-    lib.corr2d_small_tile_count.argtypes = [c_int, c_int, c_int, c_int, c_int]
-    lib.corr2d_small_tile_count.restype = c_i64
+    lib.corr2d_small_block_count.argtypes = [c_int, c_int, c_int]
+    lib.corr2d_small_block_count.restype = c_i64
     lib.corr2d_correlate_small_f64.argtypes = [
         c_int, c_void, c_i64, c_void, c_i64,          # in_dtype raw1 ld_raw1 raw2 ld_raw2
         c_int, c_int, c_int,                          # m n1 n2
         c_int, c_void, c_void, c_int, c_void, c_void,  # ref_mode1 ref_in1 sigma_in1, same for dataset 2
         c_double, c_int, c_double,                    # alpha substitute norm
-        c_void, c_void, c_void, c_i64,                # a_phi a_psi b ld_pack
         c_void, c_void, c_void, c_void,               # ref_out1 sigma_out1 ref_out2 sigma_out2
-        c_int, c_int, c_i64, c_i64,                   # row0 row1 tile0 tile1
         c_void, c_void, c_i64,                        # phi psi ld_out
         c_void, c_void, c_void, c_void, c_void,       # status1 status2 stats work stream
     ]
-    for name in ("corr2d_format_repr", "corr2d_format_rows", "corr2d_small_depth", "corr2d_correlate_small_f64",
-                 "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_bf16x3",
+    for name in ("corr2d_format_repr", "corr2d_format_rows", "corr2d_correlate_small_f64",
+                 "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
                  "corr2d_contract_tc", "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
                  "corr2d_plane_absmax", "corr2d_find_peaks"):
         getattr(lib, name).restype = c_int

@@ -44,7 +44,7 @@ def _norm_spec(norm, engine_name="fourier") -> NormalizationSpec:
 
 def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: PreprocessSpec, *,
                norm=None, on_zero_variance="error", dtype="float64", rows=None, device=None,
-               engine_name="fourier", spectra_shard=None):
+               engine_name="fourier", spectra_shard=None, distributed=None):
     """A bound :class:`engine.CorrelationPlan` for the fused raw -> planes pipeline."""
     from .preprocess import _raw_device, _recipe_for
     _, dev = engine.require_device(device)
@@ -62,6 +62,17 @@ def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: Preproce
     if engine_name not in ("fourier", "hilbert"):
         raise DataError(f"unknown engine {engine_name!r} (use 'fourier' or 'hilbert')")
     constant = _norm_spec(norm, engine_name).constant(m)
+    if distributed is not None:
+        # one band of a multi-GPU map (sharded.py); distributed = dict(group=, spectra=)
+        from .sharded import ShardedCorrelationPlan
+        if engine_name != "fourier":
+            raise DataError("distributed=True supports the Fourier route")
+        plan = ShardedCorrelationPlan(n1=ds1.n, n2=(ds1 if homo else ds2).n, m=m, recipe1=r1, recipe2=r2,
+                                      norm=constant, dtype=dtype, device=dev, **distributed)
+        plan.bind(_raw_device(ds1, dev), None if homo else _raw_device(ds2, dev))
+        plan.constant = constant
+        plan.t_axis = plan1.t_new if plan1 is not None else ds1.perturbation_axis
+        return plan, homo
     plan = engine.CorrelationPlan(
         n1=ds1.n, n2=(ds1 if homo else ds2).n, m=m, recipe1=r1, recipe2=r2, norm=constant,
         dtype=dtype, rows=rows, device=dev, want_ref=True, want_sigma=r1.alpha > 0.0,
@@ -77,7 +88,8 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
            resample: int | None = None, resample_to_common: int | None = None,
            interpolant: str = "spline", alpha: float = 0.0, norm=None, workers: int = 1,
            on_zero_variance: str = "error", dtype="float64", out=None,
-           return_device: bool = False, device=None, engine: str = "fourier") -> CorrelationSpectra:
+           return_device: bool = False, device=None, engine: str = "fourier",
+           distributed: bool = False, group=None, spectra: str = "broadcast") -> CorrelationSpectra:
     """Generalised 2D correlation of one (homo) or two (hetero) spectral series.
 
     Keyword arguments follow the reference CLI (`corrtwo correlate`): reference
@@ -86,6 +98,14 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
     (NormalizationSpec, "noda" | "unit" | "custom:c", or a float; default noda
     for the Fourier route, unit for the Hilbert route), engine ("fourier" |
     "hilbert", cli.py:332-344; the Hilbert route computes in float64).
+
+    ``distributed=True`` (one process per GPU, torch.distributed initialised,
+    e.g. under torchrun): every rank calls ``corr2d`` with the same inputs and
+    gets a :class:`~.sharded.ShardedCorrelationSpectra` holding ITS band of
+    the map in HBM (``.gather(root)`` assembles the whole map on one rank);
+    ``group`` selects the process group, ``spectra`` the K1 scheme
+    ("broadcast": each rank transforms its chunk, owners NCCL-broadcast;
+    "recompute": every rank transforms every channel).
     """
     if workers < 1:
         raise DataError("correlate: --workers must be >= 1")
@@ -103,6 +123,14 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
                           scaling_exponent=float(alpha))
     homo = ds2 is None or ds2 is ds1 or ds1.equals(ds2)
     dsb = ds1 if homo else ds2
+    if distributed:
+        from . import sharded
+        plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance, dtype=dtype,
+                                device=device, engine_name=engine,
+                                distributed=dict(group=group, spectra=spectra))
+        meta = dict(axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, normalization=plan.constant,
+                    engine=engine, is_homo=homo, scaling_exponent=float(alpha) if alpha > 0 else 0.0)
+        return sharded.run(plan, meta, axes=(ds1.spectral_axis, dsb.spectral_axis))
     blocks = None
     if not return_device:
         _, dev = _engine_mod.require_device(device)

@@ -60,6 +60,7 @@ struct ContractParams {
   const double* b;
   long long ld_pack;
   int n1, n2, mp;
+  int kg;           // Gauss operands (CORR2D_PACK_F64_GAUSS): slots per segment, mp = 3 kg
   int homo;
   int row0, row1;
   int I0, I1, T;  // row-tile range of the shard, number of column tiles
@@ -228,6 +229,29 @@ __device__ __forceinline__ void write_tile(const ContractParams& p, int mode, in
   }
 }
 
+// One depth chunk [k0, k0 + kc) of ONE operand pair (Gauss segment) into ONE
+// accumulator set: A rows from As, B rows from Bs (row stride kKS).
+__device__ __forceinline__ void mma_chunk1(double (&acc)[kMT][4][4], const double* A, const double* B, int kc,
+                                           int wm, int wn, int lr, int lk) {
+#pragma unroll 4
+  for (int kk = 0; kk < kc; kk += 4) {
+    double ap[2][2], bf[4];
+#pragma unroll
+    for (int mt = 0; mt < kMT; ++mt) {
+      const int r = wm * 16 * kMT + mt * 16 + lr;
+      ap[mt][0] = A[r * kKS + kk + lk];
+      ap[mt][1] = A[(r + 8) * kKS + kk + lk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = B[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
+#pragma unroll
+    for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], ap[mt][0], ap[mt][1], bf[nt]);
+  }
+}
+
+template <bool GAUSS>
 __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel(const ContractParams p) {
   extern __shared__ __align__(16) double sm[];
   double* As = sm;                     // [kNBuf][kBM][kKS]  A_phi (buffer stride kBufStride)
@@ -248,6 +272,60 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
     for (int bq = 0; bq < 4; ++bq)
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc_phi[a][bq][c] = acc_psi[a][bq][c] = 0.0;
+
+  if constexpr (GAUSS) {
+    // three products per bin (corr2d.h CORR2D_PACK_F64_GAUSS): segment 0 (P1)
+    // into the sync accumulator, copied into the async one, then segment 2
+    // (-P3) into sync and segment 1 (P2) into async -- two accumulator sets,
+    // 3 kg multiply-adds per element instead of 2 m.  Depth chunks are double
+    // buffered: chunk c + 1 streams in (cp.async) while chunk c is multiplied.
+    const int cps = (p.kg + kKC - 1) / kKC;          // chunks per segment
+    const int nch = 3 * cps;
+    constexpr int kGBuf = 2 * kBM * kKS;             // doubles per buffer (A and B)
+    auto issue = [&](int ch) {
+      const int si = ch / cps, k0 = (ch - si * cps) * kKC;
+      const int seg = si == 0 ? 0 : (si == 1 ? 2 : 1);
+      const int kc = min(kKC, p.kg - k0);
+      const int vec = kc / 2;
+      const int kbase = seg * p.kg + k0;
+      double* A = sm + (ch & 1) * kGBuf;
+      double* B = A + kBM * kKS;
+      for (int idx = tid; idx < kBM * vec; idx += kThreads) {
+        const int r = kc == kKC ? idx / (kKC / 2) : idx / vec;
+        const int v = idx - r * vec;
+        const int gi = i0 + r, gj = j0 + r;
+        const bool va = gi < p.n1, vb = gj < p.n2;
+        cp_async16(A + r * kKS + 2 * v, p.a_phi + (long long)(va ? gi : 0) * p.ld_pack + kbase + 2 * v, va);
+        cp_async16(B + r * kKS + 2 * v, p.b + (long long)(vb ? gj : 0) * p.ld_pack + kbase + 2 * v, vb);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    issue(0);
+    for (int ch = 0; ch < nch; ++ch) {
+      if (ch + 1 < nch) {
+        issue(ch + 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncthreads();
+      const int si = ch / cps, k0 = (ch - si * cps) * kKC;
+      const int kc = min(kKC, p.kg - k0);
+      const double* A = sm + (ch & 1) * kGBuf;
+      const double* B = A + kBM * kKS;
+      if (si == 2) mma_chunk1(acc_psi, A, B, kc, wm, wn, lr, lk);
+      else mma_chunk1(acc_phi, A, B, kc, wm, wn, lr, lk);
+      if (si == 0 && k0 + kKC >= p.kg) {             // P1 complete: the async accumulator starts from it
+#pragma unroll
+        for (int a = 0; a < kMT; ++a)
+#pragma unroll
+          for (int bq = 0; bq < 4; ++bq)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc_psi[a][bq][c] = acc_phi[a][bq][c];
+      }
+      __syncthreads();                               // buffer (ch & 1) free for chunk ch + 2
+    }
+  } else {
 
   // depth chunks through NBUF shared-memory buffers (CORR2D_F64_NBUF = 2: the
   // next chunk's cp.async overlaps this chunk's DMMAs)
@@ -309,6 +387,7 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
     if (kNBuf == 1 || k0 + kKC < p.mp) __syncthreads();   // buffer free before it is refilled
     if (kNBuf == 1 && k0 + kKC < p.mp) issue(k0 + kKC, 0);
   }
+  }  // !GAUSS
 
   // ---- epilogue.  Plain / mirrored tiles write their direct part straight
   //      from the DMMA fragments (a thread holds 2 adjacent columns of 2 rows:
@@ -400,44 +479,80 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
 
 using namespace corr2d;
 
+static int launch_contract(ContractParams p, bool gauss, int64_t tile0, int64_t tile1, void* stream,
+                           const char* who) {
+  long long tiles;
+  const long long R = p.I1 - p.I0;
+  if (p.homo) tiles = R * p.T - R * (R - 1) / 2;   // sum_{d<R} (T - d)
+  else tiles = R * p.T;
+  if (tile1 < 0 || tile1 > tiles) tile1 = tiles;
+  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, std::string(who) + ": bad tile range");
+  p.tile0 = tile0;
+  tiles = tile1 - tile0;
+  if (tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, std::string(who) + ": tile count out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(p.stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
+  if (tiles == 0) return CORR2D_OK;
+  const size_t smem_ops = gauss ? (size_t)4 * kBM * kKS * sizeof(double) : (size_t)kNBuf * kBufStride * sizeof(double);
+  const size_t smem_epi = 2 * (size_t)kBM * kCS * sizeof(double);
+  const size_t smem = smem_ops > smem_epi ? smem_ops : smem_epi;
+  if (gauss) {
+    cudaFuncSetAttribute(contract_f64_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    contract_f64_kernel<true><<<(unsigned)tiles, kThreads, smem, st>>>(p);
+    return check_launch("contract_f64_kernel<gauss>");
+  }
+  cudaFuncSetAttribute(contract_f64_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  contract_f64_kernel<false><<<(unsigned)tiles, kThreads, smem, st>>>(p);
+  return check_launch("contract_f64_kernel");
+}
+
+static int check_common(const char* who, int n1, int n2, int homo, int row0, int row1, int64_t ld_out) {
+  if (n1 < 1 || n2 < 1) return fail(CORR2D_ERR_DATA, std::string(who) + ": bad sizes");
+  if (row0 < 0 || row1 > n1 || row0 >= row1) return fail(CORR2D_ERR_DATA, std::string(who) + ": bad row range");
+  if (ld_out < n2) return fail(CORR2D_ERR_DATA, std::string(who) + ": ld_out < n2");
+  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, std::string(who) + ": homo needs n1 == n2");
+  if (row0 % kBM != 0 || (row1 != n1 && row1 % kBM != 0))
+    return fail(CORR2D_ERR_DATA, std::string(who) + ": row shard bounds must be multiples of 64 (or n1)");
+  return CORR2D_OK;
+}
+
+static ContractParams make_params(int n1, int n2, int homo, int row0, int row1, double* phi, double* psi,
+                                  int64_t ld_out, unsigned long long* stats) {
+  ContractParams p{};
+  p.n1 = n1; p.n2 = n2; p.homo = homo; p.row0 = row0; p.row1 = row1;
+  p.I0 = row0 / kBM; p.I1 = (row1 + kBM - 1) / kBM; p.T = (n2 + kBN - 1) / kBN;
+  p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
+  p.vec_direct = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
+  return p;
+}
+
 extern "C" int corr2d_contract_f64(
     const double* a_phi, const double* a_psi, const double* b, int64_t ld_pack,
     int n1, int n2, int mp, int homo, int row0, int row1, int64_t tile0, int64_t tile1,
     double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
   if (!a_phi || !a_psi || !b || !phi || !psi || !stats)
     return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: null pointer");
-  if (n1 < 1 || n2 < 1 || mp < 4 || (mp % 4) != 0)
+  if (mp < 4 || (mp % 4) != 0)
     return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: bad sizes (mp must be a positive multiple of 4)");
   if (ld_pack < mp || (ld_pack % 2) != 0)
     return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: ld_pack must be even and >= mp");
-  if (row0 < 0 || row1 > n1 || row0 >= row1)
-    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: bad row range");
-  if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: ld_out < n2");
-  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: homo needs n1 == n2");
-  if (row0 % kBM != 0 || (row1 != n1 && row1 % kBM != 0))
-    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: row shard bounds must be multiples of 64 (or n1)");
-  ContractParams p{};
-  p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack;
-  p.n1 = n1; p.n2 = n2; p.mp = mp; p.homo = homo; p.row0 = row0; p.row1 = row1;
-  p.I0 = row0 / kBM; p.I1 = (row1 + kBM - 1) / kBM; p.T = (n2 + kBN - 1) / kBN;
-  p.phi = phi; p.psi = psi; p.ld_out = ld_out; p.stats = stats;
-  p.vec_direct = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
-  long long tiles;
-  const long long R = p.I1 - p.I0;
-  if (homo) tiles = R * p.T - R * (R - 1) / 2;   // sum_{d<R} (T - d)
-  else tiles = R * p.T;
-  if (tile1 < 0 || tile1 > tiles) tile1 = tiles;
-  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64: bad tile range");
-  p.tile0 = tile0;
-  tiles = tile1 - tile0;
-  if (tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_contract_f64: tile count out of range");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
-  if (tiles == 0) return CORR2D_OK;
-  const size_t smem_ops = (size_t)kNBuf * kBufStride * sizeof(double);
-  const size_t smem_epi = 2 * (size_t)kBM * kCS * sizeof(double);
-  const size_t smem = smem_ops > smem_epi ? smem_ops : smem_epi;
-  cudaFuncSetAttribute(contract_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  contract_f64_kernel<<<(unsigned)tiles, kThreads, smem, st>>>(p);
-  return check_launch("contract_f64_kernel");
+  if (int rc = check_common("corr2d_contract_f64", n1, n2, homo, row0, row1, ld_out)) return rc;
+  ContractParams p = make_params(n1, n2, homo, row0, row1, phi, psi, ld_out, stats);
+  p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack; p.mp = mp;
+  return launch_contract(p, false, tile0, tile1, stream, "corr2d_contract_f64");
+}
+
+extern "C" int corr2d_contract_f64_gauss(
+    const double* a, const double* b, int64_t ld_pack, int n1, int n2, int kg, int homo,
+    int row0, int row1, int64_t tile0, int64_t tile1,
+    double* phi, double* psi, int64_t ld_out, unsigned long long* stats, void* stream) {
+  if (!a || !b || !phi || !psi || !stats) return fail(CORR2D_ERR_DATA, "corr2d_contract_f64_gauss: null pointer");
+  if (kg < 4 || (kg % 4) != 0)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64_gauss: kg must be a positive multiple of 4");
+  if (ld_pack < 3LL * kg || (ld_pack % 2) != 0)
+    return fail(CORR2D_ERR_DATA, "corr2d_contract_f64_gauss: ld_pack must be even and >= 3 kg");
+  if (int rc = check_common("corr2d_contract_f64_gauss", n1, n2, homo, row0, row1, ld_out)) return rc;
+  ContractParams p = make_params(n1, n2, homo, row0, row1, phi, psi, ld_out, stats);
+  p.a_phi = a; p.a_psi = a; p.b = b; p.ld_pack = ld_pack; p.mp = 3 * kg; p.kg = kg;
+  return launch_contract(p, true, tile0, tile1, stream, "corr2d_contract_f64_gauss");
 }

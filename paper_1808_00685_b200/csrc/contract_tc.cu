@@ -1666,7 +1666,7 @@ static long long tiles_2sm(int n1, int n2, int homo) {
 extern "C" int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int row0, int row1,
                                               int64_t ld_out) {
   if (n1 < 1 || n2 < 1 || row0 < 0 || row1 > n1 || row0 >= row1) return -1;
-  if (pack_kind == CORR2D_PACK_F64) {
+  if (pack_kind == CORR2D_PACK_F64 || pack_kind == CORR2D_PACK_F64_GAUSS || pack_kind == CORR2D_PACK_F64_TIME) {
     const long long T = (n2 + 63) / 64, R = (row1 + 63) / 64 - row0 / 64;
     return homo ? R * T - R * (R - 1) / 2 : R * T;
   }

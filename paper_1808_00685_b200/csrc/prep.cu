@@ -440,6 +440,24 @@ __global__ void __launch_bounds__(kPrepThreads) prep_kernel(const PrepParams p) 
       if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, vb);
     }
   }
+  // 5a'. fp64 Gauss layout (corr2d.h CORR2D_PACK_F64_GAUSS): A = [a+b | a | -b],
+  //      B = [c | d-c | c+d] over three segments of kg slots
+  if (p.pack_kind == CORR2D_PACK_F64_GAUSS) {
+    const int mp = p.mp, kg = mp / 3;
+    for (int idx = tid; idx < nc * mp; idx += blockDim.x) {
+      const int c = idx / mp, s = idx - c * mp;
+      const int seg = s / kg, j = s - seg * kg;
+      const int w = gauss_bin(seg, j, m);
+      double va = 0.0, vb = 0.0;
+      if (w >= 0) {
+        const double2 y = channel_bin(X, w, c, m, CPc);
+        gauss_values(seg, w, m, p.norm, y.x, y.y, va, vb);
+      }
+      const long long row = (long long)(c0 + c) * p.ld_pack + s;
+      if (p.pack_roles & CORR2D_ROLE_A) store_pack(p, p.a_phi, row, va);
+      if (p.pack_roles & CORR2D_ROLE_B) store_pack(p, p.b, row, vb);
+    }
+  }
   // 5b. bf16 layout (see corr2d.h): [Re' | Im' | -Im'] thirds of hp slots each,
   //     Re'[s] = R_s (s < h), Im'[0] = R_{m/2} (even m) or 0, Im'[s] = I_s,
   //     every slot scaled by sqrt(Norm * weight) so A and B share one format;
@@ -1146,11 +1164,37 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
    }
   } else {
     // CORR2D_PACK_F64 (M <= 128): slot s < K -> Re Y(s), K <= s < m -> Im Y(s - K + 1);
-    // images A_phi | A_psi | B of M doubles each
+    // images A_phi | A_psi | B of M doubles each.
+    // CORR2D_PACK_F64_GAUSS (M <= 128, kg = M / 2, no padding slots): images
+    // A | B of 3 kg = 3 M / 2 doubles each (same bytes)
     const int K = H + 1;
     const int img = 3 * M * 8;
+    const bool gauss = p.pack_kind == CORR2D_PACK_F64_GAUSS;
 #pragma unroll
-    for (int k1 = 0; k1 < R; ++k1) {
+    for (int k1 = 0; k1 < R && gauss; ++k1) {
+      C2 yy[2];
+      split(k1, yy[0], yy[1]);
+      const int w = k1 + R * k2;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (w > H) continue;
+        double* row = reinterpret_cast<double*>(work + (size_t)(2 * warp + e) * img);
+        const int kg = M / 2, G = 3 * kg;
+        double va, vb;
+        if (w < H) {                                  // DC / interior: segments 0 and 1 at slot w
+          gauss_values(0, w, M, p.norm, yy[e].x, (double)yy[e].y, va, vb);
+          row[w] = va; row[G + w] = vb;
+          gauss_values(1, w, M, p.norm, yy[e].x, (double)yy[e].y, va, vb);
+          row[kg + w] = va; row[G + kg + w] = vb;
+        }
+        if (w >= 1) {                                 // interior at w - 1, Nyquist (w = H) at H - 1
+          gauss_values(2, w, M, p.norm, yy[e].x, (double)yy[e].y, va, vb);
+          row[2 * kg + w - 1] = va; row[G + 2 * kg + w - 1] = vb;
+        }
+      }
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < R && !gauss; ++k1) {
       C2 yy[2];
       split(k1, yy[0], yy[1]);
       const int w = k1 + R * k2;
@@ -1177,6 +1221,14 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
       if (c >= nc) continue;
       const double* src = reinterpret_cast<const double*>(work + (size_t)c * img);
       const long long o = (long long)(c0 + c) * p.ld_pack;
+      if (gauss) {
+        const int G = 3 * (M / 2);
+        for (int s = lane; s < G; s += 32) {
+          if (p.pack_roles & CORR2D_ROLE_A) static_cast<double*>(p.a_phi)[o + s] = src[s];
+          if (p.pack_roles & CORR2D_ROLE_B) static_cast<double*>(p.b)[o + s] = src[G + s];
+        }
+        continue;
+      }
       for (int s = lane; s < M; s += 32) {
         if (p.pack_roles & CORR2D_ROLE_A) {
           static_cast<double*>(p.a_phi)[o + s] = src[s];
@@ -1218,6 +1270,7 @@ static bool fast_eligible(const PrepParams& p) {
   if (p.resample_kind != CORR2D_RESAMPLE_NONE || p.values_out || p.half_out) return false;
   if (p.m != 64 && p.m != 128 && p.m != 256 && p.m != 512) return false;
   if (p.pack_kind == CORR2D_PACK_BF16X2 || p.pack_kind == CORR2D_PACK_F16F8) return p.mp == 3 * (p.m / 2);
+  if (p.pack_kind == CORR2D_PACK_F64_GAUSS) return p.m <= 128 && p.mp == 3 * (p.m / 2);
   return p.pack_kind == CORR2D_PACK_F64 && p.m <= 128 && p.mp == p.m;
 }
 
@@ -1227,7 +1280,8 @@ static int fast_buf_bytes(const PrepParams& p) {
   const int M = p.m;
   const size_t sz = p.in_f32 ? 4 : 8;
   const size_t raw = (size_t)kFastCh * (M + 1) * sz;
-  const size_t img = p.pack_kind != CORR2D_PACK_F64 ? (size_t)kFastCh * (6 * (M / 2) * 2 + 128)
+  const bool f64 = p.pack_kind == CORR2D_PACK_F64 || p.pack_kind == CORR2D_PACK_F64_GAUSS;
+  const size_t img = !f64 ? (size_t)kFastCh * (6 * (M / 2) * 2 + 128)
                                                     : (size_t)kFastCh * 3 * M * 8;
   const size_t b = raw > img ? raw : img;
   return (int)((b + 1023) / 1024 * 1024);
@@ -1297,7 +1351,7 @@ static void launch_fast_kernel(K kern, PrepParams p, size_t smem, cudaStream_t s
   p.fast_buf = fast_buf_bytes(p);
   p.fast_tma = fast_raw_map(p, &map) ? 1 : 0;
   p.fast_store = 0;
-  if (p.fast_tma && p.pack_kind != CORR2D_PACK_F64) {
+  if (p.fast_tma && (p.pack_kind == CORR2D_PACK_BF16X2 || p.pack_kind == CORR2D_PACK_F16F8)) {
     const char* e = getenv("CORR2D_PREP_TMA_STORE");
     bool ok = !(e && e[0] == '0');
     if (ok && (p.pack_roles & CORR2D_ROLE_A)) ok = fast_out_map(p, p.a_phi, &oa);
@@ -1382,6 +1436,7 @@ extern "C" int corr2d_packed_depth(int m, int pack_kind) {
     const int h = (m % 2 == 0) ? m / 2 : (m + 1) / 2;
     return 3 * ((h + 31) / 32 * 32);
   }
+  if (pack_kind == CORR2D_PACK_F64_GAUSS) return 3 * gauss_kg(m);
   return (m + 3) / 4 * 4;
 }
 
@@ -1417,10 +1472,10 @@ extern "C" int corr2d_prep(
   p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack; p.split_plane = split_plane;
   p.values_out = values_out; p.ld_values = ld_values; p.half_out = half_out;
   p.ref_out = ref_out; p.sigma_out = sigma_out; p.status = status;
-  if (pack_kind < CORR2D_PACK_NONE || pack_kind > CORR2D_PACK_F16F8)
+  if (pack_kind < CORR2D_PACK_NONE || pack_kind > CORR2D_PACK_F64_GAUSS)
     return fail(CORR2D_ERR_DATA, "corr2d_prep: bad pack_kind");
   const bool tc_pack = pack_kind == CORR2D_PACK_BF16X2 || pack_kind == CORR2D_PACK_F16F8;
-  p.do_fft = (half_out != nullptr) || pack_kind == CORR2D_PACK_F64 || tc_pack;
+  p.do_fft = (half_out != nullptr) || pack_kind == CORR2D_PACK_F64 || pack_kind == CORR2D_PACK_F64_GAUSS || tc_pack;
   if (pack_kind != CORR2D_PACK_NONE) {
     p.mp = corr2d_packed_depth(m, pack_kind);
     if (tc_pack) {

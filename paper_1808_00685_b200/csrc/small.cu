@@ -1,17 +1,17 @@
 // Small-m path (m <= 32, no resampling, fp64 operands: cfg1 m = 11, cfg2 m = 21).
 //
 //  * prep_small_kernel -- K1 alone (corr2d_prep): one warp per channel pair.
-//  * small_fused_kernel -- the whole correlation in ONE launch
-//    (corr2d_correlate_small_f64): K1 with one lane per channel (32-channel
-//    blocks, each publishing a ready flag), then the contraction in 16 x 32
-//    halves of 32 x 32 warp tiles, each waiting only for its two channel
-//    blocks, straight from L2-resident operands into registers (DMMA, no
-//    shared-memory staging, no grid or CTA barriers) and from the accumulators
-//    to HBM.  At these sizes the step
-//    is bound by launch latency and the output write (cfg1: 16 MB of planes,
-//    2.5 us at HBM peak), so the two-kernel path's second launch, its two
-//    memset nodes and its one-CTA-per-64x64-tile grid (4 warps per SM) were
-//    the cost; the status / stat words are self-resetting instead.
+//  * small_block_kernel -- the whole correlation in ONE launch
+//    (corr2d_correlate_small_f64): every CTA owns one 64 x 64 output block,
+//    recomputes K1 for the 128 channels that block needs (one lane per
+//    channel: statistics, a folded direct real DFT, the three-product Gauss
+//    operand slots) into SHARED memory, contracts them on the FP64 tensor pipe
+//    and stores both planes (plus the mirror of homo blocks) from registers.
+//    No CTA ever waits for another: no ready flags, no grid barrier, no
+//    co-residency assumption (any grid size, any SM partition).  At these sizes
+//    the step is bound by launch latency, one DRAM round trip and the output
+//    write (cfg1: 16 MB of planes, 2.5 us at HBM peak); the status / stat
+//    words are self-resetting (the last CTA to finish publishes them).
 //
 // Reference path: preprocess.py:123-137, :198-259 (reference, sigma, scaling),
 // fourier.py:61-82 (rfft along the perturbation axis), fourier.py:107-123
@@ -200,281 +200,48 @@ int launch_prep_small(const PrepParams& p, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused small-m correlation: one launch per call.
+// Fused small-m correlation: one launch per call, independent CTAs.
 // ---------------------------------------------------------------------------
-constexpr int kFT = 32;          // warp tile edge (output rows and columns)
-// one CTA per SM (every CTA resident: the flag waits cannot deadlock), as many
-// warps as the register file holds: 16 at <= 128 registers (depth <= 16), 12 above
-// Warps per CTA (one CTA per SM): 16 at <= 128 registers (depth <= 16), 12 above.
-// (Measured alternatives: 8 / 16 warps at depth 24, a bulk-copy
-// staging epilogue, CTA-contiguous unit ranges -- none faster.)
-#ifndef CORR2D_SMALL_W12
-#define CORR2D_SMALL_W12 16
-#endif
-#ifndef CORR2D_SMALL_W34
-#define CORR2D_SMALL_W34 12
-#endif
-template <int NCH> __host__ __device__ constexpr int fused_warps() { return NCH <= 2 ? CORR2D_SMALL_W12 : CORR2D_SMALL_W34; }
+constexpr int kSB = 64;                 // output block edge (rows and columns)
+constexpr int kSThreads = 128;          // 4 warps: one lane per K1 channel, 32 x 32 warp tiles
+constexpr int kSMaxM = 32;
 
 struct SmallParams {
-  PrepParams p1, p2;        // K1 of dataset 1 (roles A, and B when homo) and dataset 2 (role B)
-  int homo, n1, n2;
-  int nb1;                  // 32-channel blocks of dataset 1 (flags [0, nb1); dataset 2 follows)
-  int row0, row1, I0, I1, T;
-  long long tile0, tiles;   // this launch's range of the warp-tile enumeration
-  const double* a_phi;
-  const double* a_psi;
-  const double* b;
-  long long ld_pack;
+  const void* raw1;
+  const void* raw2;
+  long long ld1, ld2;
+  int in_f32;
+  int m, n1, n2, homo;
+  int ref_mode1, ref_mode2;
+  const double* ref_in1;
+  const double* ref_in2;
+  const double* sigma_in1;
+  const double* sigma_in2;
+  double alpha;
+  int substitute;
+  double norm;
+  double* ref_out1;
+  double* sigma_out1;
+  double* ref_out2;
+  double* sigma_out2;
+  int kg, ks;               // Gauss slots per segment; shared-memory row stride (doubles, = 4 mod 16)
+  int T1, T2;               // 64-blocks along rows / columns
   double* phi;
   double* psi;
   long long ld_out;
   int vec;                  // planes 16-B aligned with an even ld_out: 16-byte direct stores
-  unsigned long long* stats;
-  int* work;                // see kW* below; zero-filled once by the caller
   int* status1;
   int* status2;
-  unsigned long long* trace;  // CORR2D_SMALL_TRACE=1: per-CTA globaltimer stamps (start, phase 1 done, first unit, end)
+  unsigned long long* stats;
+  int* work;                // kW* words, zero-filled once by the caller
 };
 
-// work-buffer words (int32 indices)
+// work-buffer words (int32 indices); every launch leaves them zero
 constexpr int kWStatus1 = 0;   // [0, 4)  K1 status accumulator, dataset 1
 constexpr int kWStatus2 = 4;   // [4, 8)  dataset 2
 constexpr int kWDone = 8;      // CTAs finished (the last one publishes and resets)
-constexpr int kWEpoch = 9;     // launch epoch: block flags of this launch read epoch + 1
 constexpr int kWStats = 10;    // [10, 16) max|sync|, max|async|, non-finite count (3 x uint64)
-constexpr int kWK1Done = 16;   // K1 tasks finished (phase-2 warps stop checking flags once all are)
-constexpr int kWFlags = 20;    // ready flags: kMaxGroups per 32-channel block
-constexpr int kMaxGroups = 5;  // 4-bin groups of K = m / 2 + 1 <= 17
-
-enum FusedMode { kFPlain = 0, kFMirror = 1, kFDiag = 2, kFTransOnly = 3 };
-
-// The warp-tile enumeration of a row shard [I0, I1) of 32-row tiles (the
-// enumeration of contract_f64's decode_tile at 32 x 32): homo row tile I0 + d
-// owns column tiles [0, I0) (lower tiles outside the shard's square, computed
-// as their globally-upper mirror and written through the transpose) and
-// [I0 + d, T); every element gets the same bits for any partition.
-__device__ __forceinline__ void fused_decode(const SmallParams& p, long long b, int& I, int& J, int& mode) {
-  if (!p.homo) {
-    I = p.I0 + (int)(b / p.T);
-    J = (int)(b % p.T);
-    mode = kFPlain;
-    return;
-  }
-  // first guess in fp32 (an fp64 sqrt would queue on the FP64 pipe behind the
-  // DMMAs of co-resident CTAs), corrected exactly below
-  const long long t2 = 2LL * p.T + 1;
-  const long long disc = t2 * t2 - 8LL * b;
-  long long d = (long long)((float)t2 - sqrtf((float)(disc > 0 ? disc : 0))) / 2;
-  auto S = [&](long long dd) { return dd * (long long)p.T - dd * (dd - 1) / 2; };
-  if (d < 0) d = 0;
-  while (d > 0 && S(d) > b) --d;
-  while (S(d + 1) <= b) ++d;
-  I = p.I0 + (int)d;
-  const long long o = b - S(d);
-  if (o < p.I0) {
-    J = I;
-    I = (int)o;
-    mode = kFTransOnly;
-  } else {
-    J = I + (int)(o - p.I0);
-    mode = (J == I) ? kFDiag : (J < p.I1 ? kFMirror : kFPlain);
-  }
-}
-
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ int ld_acquire(const int* a) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-
-// Spin (one lane) until a block flag carries this launch's epoch.  The flags
-// are set by phase-1 warps that never wait on anything, and every CTA is
-// resident (one per SM, grid from the occupancy calculator), so the wait ends;
-// if residency were ever violated the kernel traps after 20 s instead of
-// hanging the device.
-__device__ __forceinline__ int ld_relaxed(const int* a) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void wait_flag(const int* flag, int want) {
-  if (ld_acquire(flag) == want) return;
-  // relaxed polls with exponential back-off (an acquire load invalidates L1 and
-  // a thousand warps polling one L2 line slow down the K1 they are waiting
-  // for), then one acquire load
-  const unsigned long long t0 = global_ns();
-  unsigned ns = 64;
-  while (ld_relaxed(flag) != want) {
-    __nanosleep(ns);
-    ns = ns < 256 ? 2 * ns : 256;
-    if (global_ns() - t0 > 20000000000ull) __trap();
-  }
-  (void)ld_acquire(flag);
-}
-
-// The K1 fields one dataset's lanes read, loaded once per block (the kernel
-// parameter of the selected dataset would otherwise be re-read through a
-// generic pointer on every use).
-struct ChanArgs {
-  const void* raw;
-  long long ld_raw, ld_pack;
-  const double* ref_in;
-  const double* sigma_in;
-  double* ref_out;
-  double* sigma_out;
-  double* a_phi;
-  double* a_psi;
-  double* b;
-  int* status;
-  double alpha, norm;
-  int n, m, mp, in_f32, ref_mode, substitute, roles;
-};
-
-__device__ __forceinline__ ChanArgs chan_args(const PrepParams& p) {
-  ChanArgs a;
-  a.raw = p.raw; a.ld_raw = p.ld_raw; a.ld_pack = p.ld_pack; a.ref_in = p.ref_in; a.sigma_in = p.sigma_in;
-  a.ref_out = p.ref_out; a.sigma_out = p.sigma_out;
-  a.a_phi = static_cast<double*>(p.a_phi); a.a_psi = static_cast<double*>(p.a_psi); a.b = static_cast<double*>(p.b);
-  a.status = p.status; a.alpha = p.alpha; a.norm = p.norm; a.n = p.n; a.m = p.m; a.mp = p.mp;
-  a.in_f32 = p.in_f32; a.ref_mode = p.ref_mode; a.substitute = p.substitute; a.roles = p.pack_roles;
-  return a;
-}
-
-// K1 of one spectral channel per lane (channel c): the reference's statistics
-// in its order -- sequential sums, the same IEEE operations as the generic /
-// small K1 kernels, so reference, sigma and values have the same bits -- then
-// a direct real DFT of bins 4g .. 4g + 3 (ceil(K / 4) warps share a block, each
-// redoing the cheap statistics), packed straight into the channel's operand
-// rows (fp64 slots, zero padded to mp).
-// One warp runs this once per launch on an SM, so its cost is latency: the
-// samples arrive by cp.async into the warp's shared column block ys[t][lane]
-// (all m copies in flight at once), and every step is a short runtime loop --
-// straight-line unrolled code here is fetched cold, line by line, and cost
-// microseconds of instruction-fetch stalls.
-__device__ __forceinline__ void chan_lane(const ChanArgs& p, const double2* tw, double* ys, int c, int lane, int g,
-                                          unsigned long long* tr = nullptr) {
-  const bool owner = g == 0;                     // group 0 reports status / reference / sigma
-  const int m = p.m;
-  const bool valid = c < p.n;
-  const int cc = valid ? c : p.n - 1;
-  {
-    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + lane));
-    if (p.in_f32) {
-      const float* r = static_cast<const float*>(p.raw) + cc;
-      for (int t = 0; t < m; ++t)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 256u * t), "l"(r + (long long)t * p.ld_raw) : "memory");
-    } else {
-      const double* r = static_cast<const double*>(p.raw) + cc;
-      for (int t = 0; t < m; ++t)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 256u * t), "l"(r + (long long)t * p.ld_raw) : "memory");
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-  }
-  // samples -> double in place (f32: the low word of each slot); non-finite count
-  int bad = 0;
-  for (int t = 0; t < m; ++t) {
-    double v = p.in_f32 ? (double)reinterpret_cast<const float*>(ys + 32 * t + lane)[0] : ys[32 * t + lane];
-    ys[32 * t + lane] = v;
-    bad += !isfinite(v);
-  }
-  bad = valid ? bad : 0;
-  bad = warp_sum(bad);
-  if (tr && lane == 0) tr[4] = global_ns();
-  if (owner && lane == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
-  if (!valid) return;                            // no warp-collective operation follows
-  if (p.ref_mode != CORR2D_REF_NONE || p.alpha > 0.0) {
-    double ref = 0.0;
-    if (p.ref_mode == CORR2D_REF_PROVIDED) {
-      ref = __ldg(p.ref_in + c);
-    } else if (p.ref_mode == CORR2D_REF_MEAN) {
-      double sum = 0.0;                          // left to right (numpy's axis-0 order)
-      for (int t = 0; t < m; ++t) sum = __dadd_rn(sum, ys[32 * t + lane]);
-      ref = __ddiv_rn(sum, (double)m);
-    }
-    double scale = 1.0;
-    if (p.alpha > 0.0) {
-      double sigma;
-      if (p.sigma_in) {
-        sigma = __ldg(p.sigma_in + c);
-      } else {
-        double ss = 0.0;
-        for (int t = 0; t < m; ++t) {
-          const double d = __dsub_rn(ys[32 * t + lane], ref);
-          ss = __dadd_rn(ss, __dmul_rn(d, d));
-        }
-        sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
-      }
-      if (owner && p.sigma_out) p.sigma_out[c] = sigma;
-      if (owner && sigma == 0.0) {
-        atomicAdd(&p.status[CORR2D_ST_ZEROVAR], 1);
-        atomicMax(&p.status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - c);
-      }
-      if (sigma == 0.0 && p.substitute) sigma = 1.0;
-      scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
-    }
-    if (owner && p.ref_out) p.ref_out[c] = ref;
-    const bool sub = p.ref_mode != CORR2D_REF_NONE, div = p.alpha > 0.0;
-    for (int t = 0; t < m; ++t) {
-      double v = ys[32 * t + lane];
-      if (sub) v = __dsub_rn(v, ref);
-      if (div) v = __ddiv_rn(v, scale);
-      ys[32 * t + lane] = v;
-    }
-  }
-  if (tr && lane == 0) tr[5] = global_ns();
-  // Y(w) = sum_t y_t W^(w t), w < K; slots: s < K -> Re Y(s), K <= s < m -> Im Y(s - K + 1)
-  const int K = m / 2 + 1;
-  const bool even = (m % 2) == 0;
-  double* aphi = p.a_phi + (long long)c * p.ld_pack;
-  double* apsi = p.a_psi + (long long)c * p.ld_pack;
-  double* bb = p.b + (long long)c * p.ld_pack;
-  const bool roleA = p.roles & CORR2D_ROLE_A, roleB = p.roles & CORR2D_ROLE_B;
-  {
-    const int w0 = 4 * g;                        // this warp's bins w0 .. w0 + 3
-    double re[4] = {0.0, 0.0, 0.0, 0.0}, im[4] = {0.0, 0.0, 0.0, 0.0};
-    int q[4] = {0, 0, 0, 0};
-#pragma unroll 2
-    for (int t = 0; t < m; ++t) {
-      const double yt = ys[32 * t + lane];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const double2 wv = tw[q[k]];
-        re[k] = fma(yt, wv.x, re[k]);
-        im[k] = fma(yt, wv.y, im[k]);
-        q[k] += w0 + k;
-        if (q[k] >= m) q[k] -= m;
-      }
-    }
-    for (int k = 0; k < 4; ++k) {
-      const int w = w0 + k;
-      if (w >= K) break;
-      const bool edge = (w == 0 || (even && w == m / 2));
-      const double R = re[k], I = edge ? 0.0 : im[k];
-      double nr = p.norm * R, ni = p.norm * I;
-      if (!edge) { nr *= 2.0; ni *= 2.0; }
-      if (roleA) { aphi[w] = nr; apsi[w] = ni; }
-      if (roleB) bb[w] = R;
-      const int s = K + w - 1;                   // the Im slot of bin w
-      if (w >= 1 && s < m) {
-        if (roleA) { aphi[s] = ni; apsi[s] = -nr; }
-        if (roleB) bb[s] = I;
-      }
-    }
-  }
-  for (int s = m; owner && s < p.mp; ++s) {
-    if (roleA) { aphi[s] = 0.0; apsi[s] = 0.0; }
-    if (roleB) bb[s] = 0.0;
-  }
-  if (tr && lane == 0) tr[6] = global_ns();
-}
+constexpr int kWWords = 16;
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
   asm volatile(
@@ -484,231 +251,293 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Operand loads.  L1-cached: a warp reads a channel block only after an
-// acquire that saw its K1 flag (or the all-done count), and every acquire
-// invalidates the SM's L1 (CCTL.IVALL), so no line of operand data cached
-// before it was final survives; neighbouring tiles of a CTA then share rows.
-#ifndef CORR2D_SMALL_L1
-#define CORR2D_SMALL_L1 1
-#endif
-__device__ __forceinline__ double2 ld_op(const double* a) {
-#if CORR2D_SMALL_L1
-  double2 v;
-  asm volatile("ld.global.ca.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(a));
-  return v;
-#else
-  return __ldcg(reinterpret_cast<const double2*>(a));
-#endif
+// Block b of the enumeration -> (row block I, column block J).  homo: the upper
+// triangle J >= I, row by row (row I owns T - I blocks).
+__device__ __forceinline__ void small_decode(const SmallParams& p, long long b, int& I, int& J) {
+  if (!p.homo) {
+    I = (int)(b / p.T2);
+    J = (int)(b - (long long)I * p.T2);
+    return;
+  }
+  const long long T = p.T1;
+  const long long t2 = 2 * T + 1;
+  const long long disc = t2 * t2 - 8 * b;
+  long long d = (long long)((float)t2 - sqrtf((float)(disc > 0 ? disc : 0))) / 2;   // fp32 guess, exact fix-up
+  auto S = [&](long long dd) { return dd * T - dd * (dd - 1) / 2; };
+  if (d < 0) d = 0;
+  while (d > 0 && S(d) > b) --d;
+  while (S(d + 1) <= b) ++d;
+  I = (int)d;
+  J = I + (int)(b - S(d));
 }
 
-__device__ __forceinline__ unsigned long long abits(double x) { return abs_bits(x); }
+// K1 of one channel in one lane: the reference's statistics in its order
+// (sequential sums, the IEEE operations of the other K1 kernels: bitwise-equal
+// reference / sigma / values), a direct real DFT folded over t <-> m - t, then
+// the CORR2D_PACK_F64_GAUSS slots of role A (row operand, x Norm x weight)
+// and / or role B (column operand) into shared-memory rows.
+// ys: this lane's samples at ys[t * kSThreads]; tw: cos / sin of 2 pi q / m.
+__device__ __forceinline__ void tiny_k1(const SmallParams& p, int set, int c, bool valid, bool owner,
+                                        double* ys, const double2* tw, double* rowA, double* rowB) {
+  const int m = p.m;
+  const int ref_mode = set ? p.ref_mode2 : p.ref_mode1;
+  const double* ref_in = set ? p.ref_in2 : p.ref_in1;
+  const double* sigma_in = set ? p.sigma_in2 : p.sigma_in1;
+  int* status = p.work + (set ? kWStatus2 : kWStatus1);
+  double ref = 0.0, scale = 1.0;
+  int bad = 0;
+  for (int t = 0; t < m; ++t) bad += !isfinite(ys[t * kSThreads]);
+  if (owner && valid && bad) atomicAdd(&status[CORR2D_ST_NONFINITE], bad);
+  if (ref_mode == CORR2D_REF_PROVIDED) {
+    ref = valid ? __ldg(ref_in + c) : 0.0;
+  } else if (ref_mode == CORR2D_REF_MEAN) {
+    double sum = 0.0;                                  // left to right (numpy's axis-0 order)
+    for (int t = 0; t < m; ++t) sum = __dadd_rn(sum, ys[t * kSThreads]);
+    ref = __ddiv_rn(sum, (double)m);
+  }
+  if (p.alpha > 0.0) {
+    double sigma;
+    if (sigma_in) {
+      sigma = valid ? __ldg(sigma_in + c) : 1.0;
+    } else {
+      double ss = 0.0;
+      for (int t = 0; t < m; ++t) {
+        const double d = __dsub_rn(ys[t * kSThreads], ref);
+        ss = __dadd_rn(ss, __dmul_rn(d, d));
+      }
+      sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
+    }
+    if (owner && valid) {
+      double* so = set ? p.sigma_out2 : p.sigma_out1;
+      if (so) so[c] = sigma;
+      if (sigma == 0.0) {
+        atomicAdd(&status[CORR2D_ST_ZEROVAR], 1);
+        atomicMax(&status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - c);
+      }
+    }
+    if (sigma == 0.0 && p.substitute) sigma = 1.0;
+    scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
+  }
+  if (owner && valid) {
+    double* ro = set ? p.ref_out2 : p.ref_out1;
+    if (ro && ref_mode != CORR2D_REF_NONE) ro[c] = ref;
+  }
+  // dynamic values y_t, in place in the lane's shared-memory column; then the
+  // folded pairs u_t = y_t + y_{m-t} (at t) and v_t = y_t - y_{m-t} (at m - t)
+  const bool sub = ref_mode != CORR2D_REF_NONE, div = p.alpha > 0.0;
+  for (int t = 0; t < m; ++t) {
+    double v = ys[t * kSThreads];
+    if (sub) v = __dsub_rn(v, ref);
+    if (div) v = __ddiv_rn(v, scale);
+    ys[t * kSThreads] = valid ? v : 0.0;
+  }
+  const int F = (m - 1) / 2;
+  const bool even = (m % 2) == 0;
+  for (int t = 1; t <= F; ++t) {
+    const double a = ys[t * kSThreads], b = ys[(m - t) * kSThreads];
+    ys[t * kSThreads] = a + b;
+    ys[(m - t) * kSThreads] = a - b;
+  }
+  const double y0 = ys[0], yh = even ? ys[(m / 2) * kSThreads] : 0.0;
+  const int kg = p.kg;
+  const int H = m / 2;                                 // last bin (Nyquist when m is even)
+  for (int w = 0; w <= H; ++w) {
+    double re = y0, im = 0.0;
+    int q = 0;
+    for (int t = 1; t <= F; ++t) {
+      q += w;
+      if (q >= m) q -= m;
+      const double2 cs = tw[q];
+      re = fma(ys[t * kSThreads], cs.x, re);
+      im = fma(-ys[(m - t) * kSThreads], cs.y, im);
+    }
+    if (even) re = (w & 1) ? re - yh : re + yh;
+    // the Gauss slots of bin w (corr2d.h CORR2D_PACK_F64_GAUSS)
+    double va, vb;
+    if (w < H || !even) {                              // DC / interior: segments 0 and 1 at slot w
+      gauss_values(0, w, m, p.norm, re, im, va, vb);
+      if (rowA) rowA[w] = va;
+      if (rowB) rowB[w] = vb;
+      gauss_values(1, w, m, p.norm, re, im, va, vb);
+      if (rowA) rowA[kg + w] = va;
+      if (rowB) rowB[kg + w] = vb;
+    }
+    if (w >= 1) {                                      // interior at w - 1; Nyquist at slot F
+      gauss_values(2, w, m, p.norm, re, im, va, vb);
+      if (rowA) rowA[2 * kg + w - 1] = va;
+      if (rowB) rowB[2 * kg + w - 1] = vb;
+    }
+  }
+  // zero pads: segments 0 / 1 past slot F (interior F bins + DC); segment 2 past its bins
+  const int used2 = even ? F + 1 : F;
+  for (int j = F + 1; j < kg; ++j) {
+    if (rowA) { rowA[j] = 0.0; rowA[kg + j] = 0.0; }
+    if (rowB) { rowB[j] = 0.0; rowB[kg + j] = 0.0; }
+  }
+  for (int j = used2; j < kg; ++j) {
+    if (rowA) rowA[2 * kg + j] = 0.0;
+    if (rowB) rowB[2 * kg + j] = 0.0;
+  }
+}
 
-template <int NCH>
-__global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel(const __grid_constant__ SmallParams p) {
-  constexpr int kFusedWarps = fused_warps<NCH>();
-  constexpr int kK1Warps = 4;                     // warps per CTA that take K1 blocks
-  __shared__ double2 tw[32];
-  __shared__ double ys[kK1Warps][32 * 32];        // K1 sample columns [t][lane] per warp
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // global warp index, CTA-minor: consecutive work items land on different SMs
-  const int gw = warp * (int)gridDim.x + blockIdx.x;
-  const int W = gridDim.x * kFusedWarps;
+// One Gauss segment of the depth (kg slots) into one accumulator set.
+__device__ __forceinline__ void small_mma_seg(double (&acc)[2][4][4], const double* As, const double* Bs, int ks,
+                                              int k0, int kg, int wm, int wn, int lr, int lk) {
+  for (int kk = 0; kk < kg; kk += 4) {
+    double ap[2][2], bf[4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = wm * 32 + mt * 16 + lr;
+      ap[mt][0] = As[r * ks + k0 + kk + lk];
+      ap[mt][1] = As[(r + 8) * ks + k0 + kk + lk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(wn * 32 + nt * 8 + lr) * ks + k0 + kk + lk];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], ap[mt][0], ap[mt][1], bf[nt]);
+  }
+}
 
-  int* flags = p.work + kWFlags;
-  unsigned long long* tr = p.trace ? p.trace + 32 * blockIdx.x : nullptr;
-  int unit_no = 0;
-  if (tr && threadIdx.x == 0) tr[0] = global_ns();
+__global__ void __launch_bounds__(kSThreads) small_block_kernel(const __grid_constant__ SmallParams p) {
+  extern __shared__ __align__(16) double sm[];
+  const int m = p.m, ks = p.ks;
+  double2* tw = reinterpret_cast<double2*>(sm);                 // [32]
+  double* ys = sm + 2 * kSMaxM;                                  // [m][kSThreads]
+  double* As = ys + (size_t)m * kSThreads;                       // [64][ks]
+  double* Bs = As + (size_t)kSB * ks;                            // [64][ks]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // ---- phase 1: K1, one warp per 32-channel block, one lane per channel ----
-  for (int q = threadIdx.x; q < p.p1.m; q += blockDim.x) {
+  for (int q = tid; q < m; q += kSThreads) {
     double sv, cv;
-    sincospi(-2.0 * (double)q / (double)p.p1.m, &sv, &cv);
+    sincospi(2.0 * (double)q / (double)m, &sv, &cv);
     tw[q] = make_double2(cv, sv);
   }
+  int I, J;
+  small_decode(p, blockIdx.x, I, J);
+  const bool diag = p.homo && I == J;
   // programmatic dependent launch: everything above overlapped the previous
   // kernel's tail; from here on memory written by it is visible
   asm volatile("griddepcontrol.wait;\n" ::: "memory");
-  __syncthreads();
-  // this launch's epoch (bumped only by the last CTA of the previous launch)
-  const int want = *reinterpret_cast<volatile const int*>(p.work + kWEpoch) + 1;
-  const int G = (p.p1.m / 2 + 1 + 3) / 4;         // 4-bin groups per channel block (<= kMaxGroups)
-  if (warp < kK1Warps) {
-    // K1 tasks (block, bin group) on the first kK1Warps warps of every CTA, CTA-minor
-    const int nb2 = p.homo ? 0 : (p.n2 + 31) / 32;
-    const int slot = warp * (int)gridDim.x + blockIdx.x;
-    for (int task = slot; task < (p.nb1 + nb2) * G; task += kK1Warps * (int)gridDim.x) {
-      const int blk = task / G, g = task - blk * G;
-      const bool one = blk < p.nb1;                 // one call site: the K1 code is inlined once
-      const ChanArgs args = chan_args(one ? p.p1 : p.p2);
-      chan_lane(args, tw, ys[warp], 32 * (one ? blk : blk - p.nb1) + lane, lane, g, task == slot ? tr : nullptr);
-      __threadfence();                             // this lane's rows, before the flag
-      __syncwarp();
-      if (tr && task == slot && lane == 0) tr[7] = global_ns();
-      if (lane == 0) {
-        asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(flags + kMaxGroups * blk + g), "r"(want) : "memory");
-        atomicAdd(p.work + kWK1Done, 1);
-      }
-    }
-  }
-  if (tr) { __syncthreads(); if (threadIdx.x == 0) tr[1] = global_ns(); }
 
-  // ---- phase 2: 16-row halves of 32 x 32 tiles, operands straight from L2,
-  //      each unit waiting only for its two channel blocks ----
-  const int lr = lane >> 2, lk = lane & 3;
-  const long long ld = p.ld_pack;
-  const int fB = p.homo ? 0 : p.nb1;
+  // ---- K1 for the block's channels: lanes 0..63 the 64 row channels (role A;
+  //      homo diagonal blocks also role B), lanes 64..127 the 64 column
+  //      channels (role B; idle on diagonal blocks) ----
+  const bool col_lane = tid >= kSB;
+  const int set = (col_lane && !p.homo) ? 1 : 0;
+  const int c = col_lane ? J * kSB + tid - kSB : I * kSB + tid;
+  const int n = set ? p.n2 : (col_lane ? p.n2 : p.n1);
+  const bool active = !(diag && col_lane);
+  const bool valid = c < n;
+  if (active) {
+    const void* raw = set ? p.raw2 : p.raw1;
+    const long long ld = set ? p.ld2 : p.ld1;
+    const int cc = valid ? c : n - 1;
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + tid));
+    if (p.in_f32) {
+      const float* r = static_cast<const float*>(raw) + cc;
+      for (int t = 0; t < m; ++t)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 8u * kSThreads * t), "l"(r + (long long)t * ld) : "memory");
+    } else {
+      const double* r = static_cast<const double*>(raw) + cc;
+      for (int t = 0; t < m; ++t)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * kSThreads * t), "l"(r + (long long)t * ld) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    if (p.in_f32)
+      for (int t = 0; t < m; ++t) ys[t * kSThreads + tid] = (double)reinterpret_cast<const float*>(ys + t * kSThreads + tid)[0];
+  }
+  __syncthreads();                                  // twiddles
+  if (active) {
+    // the channel's statistics / status are reported by one block only: the
+    // diagonal block (homo), column block 0 (dataset 1) or row block 0 (dataset 2)
+    const bool owner = p.homo ? diag : (col_lane ? I == 0 : J == 0);
+    double* rowA = col_lane ? nullptr : As + (size_t)tid * ks;
+    double* rowB = col_lane ? Bs + (size_t)(tid - kSB) * ks : (diag ? Bs + (size_t)tid * ks : nullptr);
+    tiny_k1(p, set, c, valid, owner, ys + tid, tw, rowA, rowB);
+  }
+  __syncthreads();
+
+  // ---- contraction (Gauss): P1 -> sync, copy to async; -P3 -> sync, P2 -> async ----
+  const int wm = warp >> 1, wn = warp & 1, lr = lane >> 2, lk = lane & 3;
+  double aphi[2][4][4], apsi[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) aphi[a][b][q] = 0.0;
+  const int kg = p.kg;
+  small_mma_seg(aphi, As, Bs, ks, 0, kg, wm, wn, lr, lk);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) apsi[a][b][q] = aphi[a][b][q];
+  small_mma_seg(aphi, As, Bs, ks, 2 * kg, kg, wm, wn, lr, lk);
+  small_mma_seg(apsi, As, Bs, ks, kg, kg, wm, wn, lr, lk);
+
+  // ---- epilogue from registers: lane holds rows (lr, lr + 8) x columns
+  //      (2 lk, 2 lk + 1) of each m16n8 tile ----
   unsigned long long mphi = 0, mpsi = 0;
-  bool first = true;
-  bool all_ready = false;                          // every K1 task of this launch seen finished
-  const int k1_tasks = (p.nb1 + (p.homo ? 0 : (p.n2 + 31) / 32)) * G;
-  const long long units = 2 * p.tiles;
-  // static round robin over every warp of the grid (a shared claim counter
-  // measured slower -- thousands of warps serialise on one L2 atomic -- and so
-  // did CTA-contiguous unit ranges)
-  const long long u_step = W;
-  for (long long u = gw; u < units;) {
-    int I, J, mode;
-    fused_decode(p, p.tile0 + (u >> 1), I, J, mode);
-    const int h = (int)(u & 1);
-    const int r0 = I * kFT + h * 16;
-    if (!all_ready) {
-      int done = 0;
-      if (lane == 0) done = ld_acquire(p.work + kWK1Done);
-      all_ready = __shfl_sync(0xffffffffu, done, 0) == k1_tasks;
-      if (!all_ready && lane < G) {
-        wait_flag(flags + kMaxGroups * I + lane, want);
-        wait_flag(flags + kMaxGroups * (fB + J) + lane, want);
-      }
-      __syncwarp();
-    }
-    u += u_step;
-    if (r0 >= p.n1) continue;
-    if (tr && blockIdx.x == 0 && warp == 0 && lane == 0 && unit_no > 0 && unit_no <= 6) tr[10 + 3 * (unit_no - 1)] = global_ns();
-    const bool ut = tr && blockIdx.x == 0 && warp == 0 && lane == 0 && unit_no < 6;
-    if (tr) ++unit_no;
-    if (ut) tr[8 + 3 * (unit_no - 1)] = global_ns();
-    if (tr && first && lane == 0 && warp == 0) tr[2] = global_ns();
-    first = false;
-    double aphi[4][4], apsi[4][4];
+  const int i0 = I * kSB + wm * 32, j0 = J * kSB + wn * 32;
+  const bool mirror = p.homo && !diag;
+  const bool full = p.vec && i0 + 32 <= p.n1 && j0 + 32 <= p.n2 && !diag;
+  if (full) {
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) aphi[nt][c] = apsi[nt][c] = 0.0;
-    const int ra = min(r0 + lr, p.n1 - 1), rb = min(r0 + lr + 8, p.n1 - 1);
-    const double* pa = p.a_phi + (long long)ra * ld + 2 * lk;
-    const double* pb = p.a_phi + (long long)rb * ld + 2 * lk;
-    const double* sa = p.a_psi + (long long)ra * ld + 2 * lk;
-    const double* sb = p.a_psi + (long long)rb * ld + 2 * lk;
-    const double* bc[4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
-      bc[nt] = p.b + (long long)min(J * kFT + nt * 8 + lr, p.n2 - 1) * ld + 2 * lk;
-    // depth chunks of 8: lane lk supplies slots 2 lk (first MMA) and 2 lk + 1
-    // (second) of A and B alike -- a permutation of the depth, exact
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) {
-      const double2 a0 = ld_op(pa + 8 * ch);
-      const double2 a1 = ld_op(pb + 8 * ch);
-      const double2 s0 = ld_op(sa + 8 * ch);
-      const double2 s1 = ld_op(sb + 8 * ch);
-      double2 bf[4];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = ld_op(bc[nt] + 8 * ch);
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        dmma(aphi[nt], a0.x, a1.x, bf[nt].x);
-        dmma(apsi[nt], s0.x, s1.x, bf[nt].x);
-      }
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) {
-        dmma(aphi[nt], a0.y, a1.y, bf[nt].y);
-        dmma(apsi[nt], s0.y, s1.y, bf[nt].y);
-      }
-    }
-    if (ut) {
-      double z = 0.0;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) z += aphi[nt][0] + apsi[nt][3];   // wait for the accumulators
-      tr[9 + 3 * (unit_no - 1)] = global_ns() + (z == 12345.678 ? 1 : 0);
-    }
-    // ---- epilogue: lane holds rows (lr, lr + 8) x columns (2 lk, 2 lk + 1) of each n8 tile
-    const bool interior = mode != kFDiag && p.vec && r0 + 16 <= min(p.n1, p.row1) && (J + 1) * kFT <= p.n2 &&
-                          (mode == kFPlain || (J * kFT >= p.row0 && (J + 1) * kFT <= p.row1));
-    if (interior) {
-      // branch-free fast path: full 16 x 32 unit, 16-byte direct stores, 8-byte mirror stores
-      const bool direct = mode != kFTransOnly, mirror = mode != kFPlain;
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int gi = r0 + lr + 8 * hh, gj = J * kFT + nt * 8 + 2 * lk;
-          const double f0 = aphi[nt][2 * hh], f1 = aphi[nt][2 * hh + 1];
-          const double s0 = apsi[nt][2 * hh], s1 = apsi[nt][2 * hh + 1];
-          mphi = max(mphi, max(abits(f0), abits(f1)));
-          mpsi = max(mpsi, max(abits(s0), abits(s1)));
-          if (direct) {
-            const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
-            __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
-            __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
-          }
+        for (int h = 0; h < 2; ++h) {
+          const int gi = i0 + mt * 16 + lr + 8 * h, gj = j0 + nt * 8 + 2 * lk;
+          const double f0 = aphi[mt][nt][2 * h], f1 = aphi[mt][nt][2 * h + 1];
+          const double s0 = apsi[mt][nt][2 * h], s1 = apsi[mt][nt][2 * h + 1];
+          mphi = max(mphi, max(abs_bits(f0), abs_bits(f1)));
+          mpsi = max(mpsi, max(abs_bits(s0), abs_bits(s1)));
+          const long long o = (long long)gi * p.ld_out + gj;
+          __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
+          __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
           if (mirror) {
-            const long long o = (long long)(gj - p.row0) * p.ld_out + gi;
-            __stcs(p.phi + o, f0);
-            __stcs(p.psi + o, neg_bits(s0));
-            __stcs(p.phi + o + p.ld_out, f1);
-            __stcs(p.psi + o + p.ld_out, neg_bits(s1));
+            const long long om = (long long)gj * p.ld_out + gi;
+            __stcs(p.phi + om, f0);
+            __stcs(p.psi + om, neg_bits(s0));
+            __stcs(p.phi + om + p.ld_out, f1);
+            __stcs(p.psi + om + p.ld_out, neg_bits(s1));
           }
         }
-      continue;
-    }
-    const bool direct = mode != kFTransOnly;
-    const bool mirror = mode != kFPlain;
+  } else {
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int rl = h * 16 + lr + 8 * hh, cl = nt * 8 + 2 * lk;   // tile-local
-        const int gi = I * kFT + rl, gj = J * kFT + cl;
-        double f0 = aphi[nt][2 * hh], f1 = aphi[nt][2 * hh + 1];
-        double s0 = apsi[nt][2 * hh], s1 = apsi[nt][2 * hh + 1];
-        bool d0 = direct, d1 = direct, m0 = mirror, m1 = mirror;
-        if (mode == kFDiag) {               // upper part incl. the diagonal, mirrored below it
-          d0 = rl <= cl; d1 = rl <= cl + 1;
-          m0 = rl < cl; m1 = rl < cl + 1;
-          if (rl == cl) s0 = 0.0;
-          if (rl == cl + 1) s1 = 0.0;
-        }
-        if (gi >= p.n1) { d0 = d1 = m0 = m1 = false; }
-        if (gj >= p.n2) { d0 = m0 = false; }
-        if (gj + 1 >= p.n2) { d1 = m1 = false; }
-        if (gi >= p.row1) { d0 = d1 = false; }
-        if (d0 || m0) { mphi = max(mphi, abits(f0)); mpsi = max(mpsi, abits(s0)); }
-        if (d1 || m1) { mphi = max(mphi, abits(f1)); mpsi = max(mpsi, abits(s1)); }
-        if (d0 || d1) {
-          const long long o = (long long)(gi - p.row0) * p.ld_out + gj;
-          if (d0 && d1 && p.vec) {
-            __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
-            __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
-          } else {
-            if (d0) { __stcs(p.phi + o, f0); __stcs(p.psi + o, s0); }
-            if (d1) { __stcs(p.phi + o + 1, f1); __stcs(p.psi + o + 1, s1); }
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int gi = i0 + mt * 16 + lr + 8 * h, gj = j0 + nt * 8 + 2 * lk + e;
+            double f = aphi[mt][nt][2 * h + e], s = apsi[mt][nt][2 * h + e];
+            if (gi >= p.n1 || gj >= p.n2) continue;
+            bool direct = true, mir = mirror;
+            if (diag) {                      // upper part incl. the diagonal, mirrored below it
+              direct = gi <= gj;
+              mir = gi < gj;
+              if (gi == gj) s = 0.0;
+            }
+            if (!direct) continue;
+            mphi = max(mphi, abs_bits(f));
+            mpsi = max(mpsi, abs_bits(s));
+            __stcs(p.phi + (long long)gi * p.ld_out + gj, f);
+            __stcs(p.psi + (long long)gi * p.ld_out + gj, s);
+            if (mir) {
+              __stcs(p.phi + (long long)gj * p.ld_out + gi, f);
+              __stcs(p.psi + (long long)gj * p.ld_out + gi, neg_bits(s));
+            }
           }
-        }
-        // mirror: out[j][i] = sync[i][j], -async[i][j] (rows j of the shard only)
-        if (m0 && gj >= p.row0 && gj < p.row1) {
-          const long long o = (long long)(gj - p.row0) * p.ld_out + gi;
-          __stcs(p.phi + o, f0);
-          __stcs(p.psi + o, neg_bits(s0));
-        }
-        if (m1 && gj + 1 >= p.row0 && gj + 1 < p.row1) {
-          const long long o = (long long)(gj + 1 - p.row0) * p.ld_out + gi;
-          __stcs(p.phi + o, f1);
-          __stcs(p.psi + o, neg_bits(s1));
-        }
-      }
   }
-  // ---- max|.| and the finite check (integer pipe, as contract_f64): one set of
-  //      atomics per warp into the accumulator words
+  // ---- max|.| and the finite check (integer pipe), one set of atomics per CTA ----
   constexpr unsigned long long kInf = 0x7ff0000000000000ull;
   int bad = (mphi >= kInf) + (mpsi >= kInf);
   mphi = min(mphi, kInf);
@@ -719,17 +548,26 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
     mpsi = max(mpsi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mpsi, o));
   }
   bad = warp_sum(bad);
-  unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWStats);
+  __shared__ unsigned long long red[3][4];
   if (lane == 0) {
-    if (mphi) atomicMax(&acc[0], mphi);
-    if (mpsi) atomicMax(&acc[1], mpsi);
-    if (bad) atomicAdd(&acc[2], (unsigned long long)bad);
+    red[0][warp] = mphi;
+    red[1][warp] = mpsi;
+    red[2][warp] = (unsigned long long)bad;
   }
-  // ---- the last CTA publishes status / stats and leaves the work words zero
-  //      (flags keep their epoch; the epoch moves on)
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (tr) tr[3] = global_ns();
+  if (tid == 0) {
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWStats);
+    unsigned long long a0 = 0, a1 = 0, a2 = 0;
+    for (int w = 0; w < kSThreads / 32; ++w) {
+      a0 = max(a0, red[0][w]);
+      a1 = max(a1, red[1][w]);
+      a2 += red[2][w];
+    }
+    if (a0) atomicMax(&acc[0], a0);
+    if (a1) atomicMax(&acc[1], a1);
+    if (a2) atomicAdd(&acc[2], a2);
+    // the last CTA to finish publishes status / stats and leaves the words zero
+    // (an arrival counter, never a wait)
     __threadfence();
     if (atomicAdd(p.work + kWDone, 1) == (int)gridDim.x - 1) {
       __threadfence();
@@ -746,105 +584,24 @@ __global__ void __launch_bounds__(32 * fused_warps<NCH>(), 1) small_fused_kernel
         av[k] = 0ull;
       }
       wv[kWDone] = 0;
-      wv[kWK1Done] = 0;
-      wv[kWEpoch] = want;
       __threadfence();
     }
   }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
-static long long fused_tile_count(int n1, int n2, int homo, int row0, int row1) {
-  const long long I0 = row0 / kFT, I1 = (row1 + kFT - 1) / kFT, T = (n2 + kFT - 1) / kFT;
-  const long long R = I1 - I0;
-  return homo ? R * T - R * (R - 1) / 2 : R * T;
-}
-
-template <int NCH>
-static int launch_fused(const SmallParams& p, cudaStream_t st) {
-  // one CTA per SM of the CURRENT device (cached per device: the grid must
-  // never exceed what is co-resident, or the flag waits could not complete)
-  static int grids[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return fail(CORR2D_ERR_UNSUPPORTED, "small_fused_kernel: device index >= 64");
-  int& grid = grids[dev];
-  if (grid == 0) {
-    int sms = 0, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_fused_kernel<NCH>, 32 * fused_warps<NCH>(), 0);
-    if (per_sm < 1 || sms < 1) return fail(CORR2D_ERR_CUDA, "small_fused_kernel: no resident CTA");
-    grid = sms;   // one per SM even if more would fit: one K1 slot set and one arrival per SM
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(32 * fused_warps<NCH>());
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  // programmatic dependent launch: this grid's launch and prologue overlap the
-  // previous kernel's tail (griddepcontrol.wait in the kernel orders memory);
-  // CORR2D_SMALL_PDL=0 disables
-  static const int pdl = [] { const char* e = getenv("CORR2D_SMALL_PDL"); return e && e[0] == '0' ? 0 : 1; }();
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl;
-  attr[1].id = cudaLaunchAttributeCooperative;
-  attr[1].val.cooperative = 1;
-  cfg.attrs = attr;
-  // the cooperative attribute (guaranteed co-residency) costs ~7 us per launch in
-  // a graph (cfg1: 22 vs 15 us per step); with one CTA per SM from the occupancy
-  // calculator every CTA is resident once the stream reaches the kernel, and the
-  // barrier traps rather than hangs if that is ever violated.  CORR2D_SMALL_COOP=1
-  // restores the attribute.
-  static const int coop = [] { const char* e = getenv("CORR2D_SMALL_COOP"); return e && e[0] == '1' ? 1 : 0; }();
-  cfg.numAttrs = 1 + coop;
-  static unsigned long long* trace = nullptr;
-  const char* te = getenv("CORR2D_SMALL_TRACE");   // read per launch (experiments toggle it)
-  const bool want_trace = te && te[0] == '1';
-  SmallParams q = p;
-  if (want_trace) {
-    if (!trace) cudaMalloc(&trace, 32 * sizeof(unsigned long long) * grid);
-    cudaMemsetAsync(trace, 0, 32 * sizeof(unsigned long long) * grid, st);
-    q.trace = trace;
-  }
-  cudaLaunchKernelEx(&cfg, small_fused_kernel<NCH>, q);
-  if (want_trace) {
-    std::vector<unsigned long long> h(32 * (size_t)grid);
-    cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    unsigned long long t0 = ~0ull;
-    for (int b = 0; b < grid; ++b) t0 = std::min(t0, h[32 * b]);
-    double mx[8] = {0}, avg[8] = {0};
-    int cnt[8] = {0};
-    for (int b = 0; b < grid; ++b)
-      for (int k = 0; k < 8; ++k) {
-        if (!h[32 * b + k]) continue;
-        const double v = (double)(h[32 * b + k] - t0);
-        mx[k] = std::max(mx[k], v);
-        avg[k] += v;
-        ++cnt[k];
-      }
-    const char* names[8] = {"start", "phase1", "first-unit", "end", "k1-loaded", "k1-stats", "k1-packed", "k1-fenced"};
-    fprintf(stderr, "small_fused trace (ns, max/avg):");
-    for (int k = 0; k < 8; ++k) fprintf(stderr, " %s %.0f/%.0f", names[k], mx[k], cnt[k] ? avg[k] / cnt[k] : 0.0);
-    fprintf(stderr, "\nwarp 0 of CTA 0, per unit (ns: flags-ok, mma-done, stored):");
-    for (int u = 0; u < 6; ++u)
-      if (h[8 + 3 * u]) fprintf(stderr, " [%.0f %.0f %.0f]", (double)(h[8 + 3 * u] - t0), (double)(h[9 + 3 * u] - t0),
-                                (double)(h[10 + 3 * u] - t0));
-    fprintf(stderr, "\n");
-  }
-  return check_launch("small_fused_kernel");
+static long long small_blocks(int n1, int n2, int homo) {
+  const long long T1 = (n1 + kSB - 1) / kSB, T2 = (n2 + kSB - 1) / kSB;
+  return homo ? T1 * (T1 + 1) / 2 : T1 * T2;
 }
 
 }  // namespace corr2d
 
 using namespace corr2d;
 
-extern "C" int corr2d_small_depth(int m) { return (m >= 2 && m <= 32) ? (m + 7) / 8 * 8 : -1; }
-
-extern "C" int64_t corr2d_small_tile_count(int n1, int n2, int homo, int row0, int row1) {
-  if (n1 < 1 || n2 < 1 || row0 < 0 || row1 > n1 || row0 >= row1 || (homo && n1 != n2)) return -1;
-  return fused_tile_count(n1, n2, homo, row0, row1);
+extern "C" int64_t corr2d_small_block_count(int n1, int n2, int homo) {
+  if (n1 < 1 || n2 < 1 || (homo && n1 != n2)) return -1;
+  return small_blocks(n1, n2, homo);
 }
 
 extern "C" int corr2d_correlate_small_f64(
@@ -853,61 +610,59 @@ extern "C" int corr2d_correlate_small_f64(
     int ref_mode1, const double* ref_in1, const double* sigma_in1,
     int ref_mode2, const double* ref_in2, const double* sigma_in2,
     double alpha, int substitute_zero_var, double norm_const,
-    double* a_phi, double* a_psi, double* b, int64_t ld_pack,
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
-    int row0, int row1, int64_t tile0, int64_t tile1,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream) {
   const bool homo = raw2 == nullptr;
-  if (!raw1 || !a_phi || !a_psi || !b || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
+  if (!raw1 || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
   if (in_dtype != CORR2D_F64 && in_dtype != CORR2D_F32) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad dtype");
-  const int mp = corr2d_small_depth(m);
-  if (mp < 0) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: needs 2 <= m <= 32");
+  if (m < 2 || m > kSMaxM) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: needs 2 <= m <= 32");
   if (n1 < 1 || n2 < 1) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad sizes");
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: homo needs n1 == n2");
   if (ld_raw1 < n1 || (!homo && ld_raw2 < n2)) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_raw < n");
-  if (ld_pack < mp || ld_pack % 2 || (reinterpret_cast<uintptr_t>(a_phi) | reinterpret_cast<uintptr_t>(a_psi) |
-                                      reinterpret_cast<uintptr_t>(b)) & 15)
-    return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_pack must be even and >= the packed depth, operands 16-B aligned");
   if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_out < n2");
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(CORR2D_ERR_DATA, "scaling exponent must lie in [0, 1]");
-  if (row0 < 0 || row1 > n1 || row0 >= row1 || row0 % kFT || (row1 != n1 && row1 % kFT))
-    return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: row shard bounds must be multiples of 32 (or n1)");
   for (int r : {ref_mode1, ref_mode2})
     if (r < CORR2D_REF_MEAN || r > CORR2D_REF_NONE) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad ref_mode");
   if ((ref_mode1 == CORR2D_REF_PROVIDED && !ref_in1) || (!homo && ref_mode2 == CORR2D_REF_PROVIDED && !ref_in2))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: provided reference missing");
 
   SmallParams p{};
-  auto prep = [&](PrepParams& q, const void* raw, int64_t ld_raw, int n, int ref_mode, const double* ref_in,
-                  const double* sigma_in, int roles, double* ref_out, double* sigma_out, int* acc) {
-    q.raw = raw; q.in_f32 = in_dtype == CORR2D_F32; q.ld_raw = ld_raw; q.m_in = m; q.n = n;
-    q.resample_kind = CORR2D_RESAMPLE_NONE; q.m = m;
-    q.ref_mode = ref_mode; q.ref_in = ref_in; q.sigma_in = sigma_in; q.alpha = alpha;
-    q.substitute = substitute_zero_var; q.norm = norm_const;
-    q.pack_kind = CORR2D_PACK_F64; q.pack_roles = roles;
-    q.a_phi = a_phi; q.a_psi = a_psi; q.b = b; q.ld_pack = ld_pack; q.mp = mp;
-    q.ref_out = ref_out; q.sigma_out = sigma_out; q.status = acc; q.do_fft = 1;
-  };
-  prep(p.p1, raw1, ld_raw1, n1, ref_mode1, ref_in1, sigma_in1,
-       CORR2D_ROLE_A | (homo ? CORR2D_ROLE_B : 0), ref_out1, sigma_out1, work);
-  if (!homo) prep(p.p2, raw2, ld_raw2, n2, ref_mode2, ref_in2, sigma_in2, CORR2D_ROLE_B, ref_out2, sigma_out2, work + 4);
-  p.homo = homo; p.n1 = n1; p.n2 = n2; p.nb1 = (n1 + 31) / 32;
-  p.row0 = row0; p.row1 = row1; p.I0 = row0 / kFT; p.I1 = (row1 + kFT - 1) / kFT; p.T = (n2 + kFT - 1) / kFT;
-  const long long tiles = fused_tile_count(n1, n2, homo, row0, row1);
-  if (tile1 < 0 || tile1 > tiles) tile1 = tiles;
-  if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad tile range");
-  p.tile0 = tile0; p.tiles = tile1 - tile0;
-  p.a_phi = a_phi; p.a_psi = a_psi; p.b = b; p.ld_pack = ld_pack;
+  p.raw1 = raw1; p.raw2 = raw2; p.ld1 = ld_raw1; p.ld2 = ld_raw2; p.in_f32 = in_dtype == CORR2D_F32;
+  p.m = m; p.n1 = n1; p.n2 = n2; p.homo = homo;
+  p.ref_mode1 = ref_mode1; p.ref_mode2 = ref_mode2; p.ref_in1 = ref_in1; p.ref_in2 = ref_in2;
+  p.sigma_in1 = sigma_in1; p.sigma_in2 = sigma_in2; p.alpha = alpha; p.substitute = substitute_zero_var;
+  p.norm = norm_const;
+  p.ref_out1 = ref_out1; p.sigma_out1 = sigma_out1; p.ref_out2 = ref_out2; p.sigma_out2 = sigma_out2;
+  p.kg = gauss_kg(m);
+  p.ks = (3 * p.kg + 11) / 16 * 16 + 4;
+  p.T1 = (n1 + kSB - 1) / kSB; p.T2 = (n2 + kSB - 1) / kSB;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out;
   p.vec = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
-  p.stats = stats; p.work = work; p.status1 = status1; p.status2 = homo ? nullptr : status2;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  switch (mp / 8) {
-    case 1: return launch_fused<1>(p, st);
-    case 2: return launch_fused<2>(p, st);
-    case 3: return launch_fused<3>(p, st);
-    default: return launch_fused<4>(p, st);
+  p.status1 = status1; p.status2 = homo ? nullptr : status2; p.stats = stats; p.work = work;
+  const long long blocks = small_blocks(n1, n2, homo);
+  if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
+  const size_t smem = (2 * kSMaxM + (size_t)m * kSThreads + 2 * (size_t)kSB * p.ks) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(small_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((2 * kSMaxM + (size_t)kSMaxM * kSThreads + 2 * (size_t)kSB * 52) * sizeof(double)));
+    attr_set = true;
   }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kSThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  // programmatic dependent launch: this grid's launch and prologue overlap the
+  // previous kernel's tail (griddepcontrol.wait orders memory).  No CTA waits
+  // for another, so the grid needs no co-residency.
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, small_block_kernel, p);
+  return check_launch("small_block_kernel");
 }

@@ -38,6 +38,32 @@ def fp32_pack_kind() -> int:
     raise DataError(f"CORR2D_FP32_FORMAT must be f16f8 or bf16x3, got {fmt!r}")
 
 
+def f64_pack_kind() -> int:
+    """Operand format of the float64 Fourier route: CORR2D_PACK_F64_GAUSS (three
+    real products per bin, default) or CORR2D_PACK_F64 (four; CORR2D_F64_FORMAT=
+    four), both exact rewrites of the complex half-spectrum sum (corr2d.h)."""
+    fmt = os.environ.get("CORR2D_F64_FORMAT", "gauss").lower()
+    if fmt == "gauss":
+        return _abi.PACK_F64_GAUSS
+    if fmt == "four":
+        return _abi.PACK_F64
+    raise DataError(f"CORR2D_F64_FORMAT must be gauss or four, got {fmt!r}")
+
+
+def launch_contract_f64(lib, pack_kind, a_phi, a_psi, b, ld_pack, n1, n2, mp, homo, row0, row1, tile0, tile1,
+                        phi, psi, ld_out, stats):
+    """The fp64 contraction for either operand format (pointers are tensors)."""
+    if pack_kind == _abi.PACK_F64_GAUSS:
+        code = lib.corr2d_contract_f64_gauss(
+            ptr(a_phi), ptr(b), ld_pack, n1, n2, mp // 3, homo, row0, row1, tile0, tile1,
+            ptr(phi), ptr(psi), ld_out, ptr(stats), stream_handle())
+    else:
+        code = lib.corr2d_contract_f64(
+            ptr(a_phi), ptr(a_psi), ptr(b), ld_pack, n1, n2, mp, homo, row0, row1, tile0, tile1,
+            ptr(phi), ptr(psi), ld_out, ptr(stats), stream_handle())
+    _abi.check(code, lib)
+
+
 def torch():
     global _torch
     if _torch is None:
@@ -336,11 +362,12 @@ class CorrelationPlan:
                 raise DataError("the Hilbert route computes in float64 only")
             self.pack_kind, odt, pdt = _abi.PACK_F64_TIME, t.float64, t.float64
         elif self.dtype == np.float64:
-            self.pack_kind, odt, pdt = _abi.PACK_F64, t.float64, t.float64
+            self.pack_kind, odt, pdt = f64_pack_kind(), t.float64, t.float64
         elif self.dtype == np.float32:
             self.pack_kind, odt, pdt = fp32_pack_kind(), t.float32, t.bfloat16
         else:
             raise DataError(f"unsupported compute dtype {dtype}")
+        self.gauss = self.pack_kind == _abi.PACK_F64_GAUSS
         self.mp = self.lib.corr2d_packed_depth(self.m, self.pack_kind)
         if self.mp <= 0:
             _abi.check(_abi.ERR_DATA, self.lib)
@@ -352,23 +379,22 @@ class CorrelationPlan:
         # slot, interleaved per 32-slot block, then the fp32 DC / Nyquist pair
         # in a 128-byte pad (include/corr2d.h)
         self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
-        # small m (fp64 Fourier route, m <= 32, no resampling): the whole call is
-        # ONE launch (csrc/small.cu: K1 + grid barrier + warp-tile contraction);
-        # its operand rows are zero padded to a multiple of 8 slots
+        # small m (fp64 Fourier route, m <= 32, no resampling, whole map): the
+        # whole call is ONE launch (csrc/small.cu: independent CTAs, each
+        # recomputing K1 for its 64 x 64 block's channels in shared memory)
         self.small = (route == "fourier" and self.dtype == np.float64 and self.shard is None
                       and small_fused_enabled() and 2 <= self.m <= 32
                       and all(r is None or (r.resample is None and r.m_in == r.m) for r in (recipe1, recipe2))
                       and (recipe2 is None or (recipe2.alpha == recipe1.alpha
                                                and recipe2.substitute == recipe1.substitute))
-                      and self.row0 % 32 == 0 and (self.row1 == self.n1 or self.row1 % 32 == 0))
-        if self.small:
-            self.ld_pack = self.lib.corr2d_small_depth(self.m)
+                      and self.row0 == 0 and self.row1 == self.n1 and tiles is None)
         dev = self.dev
         R1, R2 = self._rows(self.n1), self._rows(self.n2)
         alloc = t.zeros if self.shard else t.empty
-        self.a_phi = alloc((R1, self.ld_pack), dtype=pdt, device=dev)
+        O1, O2 = (0, 0) if self.small else (R1, R2)   # small: operands live in the fused kernel's smem
+        self.a_phi = alloc((O1, self.ld_pack), dtype=pdt, device=dev)
         # bf16: one format for both roles (a_psi unused, homo B == A)
-        self.a_psi = None if bf16 else alloc((R1, self.ld_pack), dtype=pdt, device=dev)
+        self.a_psi = None if (bf16 or self.gauss) else alloc((O1, self.ld_pack), dtype=pdt, device=dev)
         if route == "hilbert":
             # A_psi = -Norm * (N y1) comes from one contraction of A_phi = Norm * y1
             # against the rows of -N (m x mp, zero padded); columns m..mp of
@@ -376,9 +402,9 @@ class CorrelationPlan:
             self.a_psi = t.zeros((R1, self.ld_pack), dtype=pdt, device=dev)
             self.noda_neg = t.from_numpy(_noda_rows(self.m, self.ld_pack)).to(dev)
             self.noda_scratch = t.empty((self.n1, self.ld_pack), dtype=pdt, device=dev)
-        self.b = alloc((R2, self.ld_pack), dtype=pdt, device=dev) if not self.homo else None
+        self.b = alloc((O2, self.ld_pack), dtype=pdt, device=dev) if not self.homo else None
         if self.homo:
-            self.b_homo = self.a_phi if bf16 else alloc((R1, self.ld_pack), dtype=pdt, device=dev)
+            self.b_homo = self.a_phi if bf16 else alloc((O1, self.ld_pack), dtype=pdt, device=dev)
         else:
             self.b_homo = None
         nrows = self.row1 - self.row0
@@ -390,9 +416,8 @@ class CorrelationPlan:
                 f"out of memory assembling the complex correlation matrix; it needs "
                 f"16*{self.n1}*{self.n2} bytes = {16 * self.n1 * self.n2 / 1e9:.2f} GB") from None
         self.stats = t.zeros(4, dtype=t.int64, device=dev)
-        # fused small-m path: self-resetting K1 status accumulators + grid barrier words
-        self.work = (t.zeros(20 + 5 * ((self.n1 + 31) // 32 + (0 if self.homo else (self.n2 + 31) // 32)),
-                             dtype=t.int32, device=dev) if self.small else None)
+        # fused small-m path: self-resetting K1 status / stat accumulators
+        self.work = t.zeros(16, dtype=t.int32, device=dev) if self.small else None
         self.status1 = t.zeros(4, dtype=t.int32, device=dev)
         self.status2 = t.zeros(4, dtype=t.int32, device=dev)
         self.ref1 = alloc(R1, dtype=t.float64, device=dev) if want_ref else None
@@ -421,7 +446,7 @@ class CorrelationPlan:
         """Tiles in the contraction kernel's enumeration for this plan (the unit
         of the multi-GPU tile-range partition; include/corr2d.h)."""
         if self.small:
-            n = self.lib.corr2d_small_tile_count(self.n1, self.n2, 1 if self.homo else 0, self.row0, self.row1)
+            n = self.lib.corr2d_small_block_count(self.n1, self.n2, 1 if self.homo else 0)
             if n < 0:
                 raise DataError("bad contraction shape")
             return int(n)
@@ -506,11 +531,11 @@ class CorrelationPlan:
                 0, 0, self.n1, 0, -1, ptr(self.a_psi), ptr(self.noda_scratch), self.ld_pack,
                 ptr(self.stats), stream_handle())
             _abi.check(code, lib)
-        if self.pack_kind in (_abi.PACK_F64, _abi.PACK_F64_TIME):
-            code = lib.corr2d_contract_f64(
-                ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.ld_pack, self.n1, self.n2, self.mp,
-                homo, self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi),
-                self.n2, ptr(self.stats), stream_handle())
+        if self.pack_kind in (_abi.PACK_F64, _abi.PACK_F64_TIME, _abi.PACK_F64_GAUSS):
+            launch_contract_f64(lib, self.pack_kind, self.a_phi, self.a_psi, self.bop, self.ld_pack, self.n1,
+                                self.n2, self.mp, homo, self.row0, self.row1, self.tile0, self.tile1,
+                                self.phi, self.psi, self.n2, self.stats)
+            return
         else:
             code = lib.corr2d_contract_tc(
                 self.pack_kind, ptr(self.a_phi), ptr(self.bop), self.ld_pack, self.n1, self.n2, self.mp, self.m, homo,
@@ -530,9 +555,8 @@ class CorrelationPlan:
             self.m, self.n1, self.n2,
             int(r1.ref_mode), ptr(r1.ref_in), ptr(r1.sigma_in), int(r2.ref_mode), ptr(r2.ref_in), ptr(r2.sigma_in),
             float(r1.alpha), 1 if r1.substitute else 0, self.norm,
-            ptr(self.a_phi), ptr(self.a_psi), ptr(self.bop), self.ld_pack,
             ptr(self.ref1), ptr(self.sigma1), ptr(self.ref2), ptr(self.sigma2),
-            self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
+            ptr(self.phi), ptr(self.psi), self.n2,
             ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle())
         _abi.check(code, self.lib)
 

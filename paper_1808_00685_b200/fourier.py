@@ -97,12 +97,16 @@ class DeviceCorrelationSpectra:
 
 @engine.on_device
 def correlate_ft(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers: int = 1, *,
-                 dtype="float64", out=None, return_device: bool = False, device=None, rows=None):
+                 dtype="float64", out=None, return_device: bool = False, device=None, rows=None,
+                 distributed: bool = False, group=None, spectra: str = "broadcast"):
     """Synchronous and asynchronous correlation via the Fourier route
     (fourier.py:85-125).  Extras (keyword-only): ``dtype="float32"`` selects
-    the bf16x3 tensor-core path with float32 planes; ``out=(sync, asyn)``
-    host buffers to fill; ``return_device`` keeps the planes in HBM;
-    ``rows=(row0, row1)`` computes one row shard (multi-GPU ownership)."""
+    the tensor-core path (fp16 + e4m3 split products) with float32 planes;
+    ``out=(sync, asyn)`` host buffers to fill; ``return_device`` keeps the
+    planes in HBM; ``rows=(row0, row1)`` computes one row shard;
+    ``distributed=True`` (one process per GPU under torch.distributed) returns
+    this rank's band of the map (:class:`~.sharded.ShardedCorrelationSpectra`,
+    see ``corr2d``)."""
     homo = dyn2 is None or is_same_dynamic(dyn1, dyn2)
     if dyn2 is None:
         dyn2 = dyn1
@@ -124,6 +128,14 @@ def correlate_ft(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers
     meta = dict(axis1=dyn1.spectral_axis, axis2=dyn2.spectral_axis, ref1=dyn1.reference_used,
                 ref2=dyn2.reference_used, normalization=constant, engine="fourier",
                 is_homo=homo, scaling_exponent=dyn1.scaling_exponent)
+    if distributed:
+        # this rank's band of a multi-GPU map (sharded.py)
+        from . import sharded
+        plan = sharded.ShardedCorrelationPlan(n1=dyn1.n, n2=dyn2.n, m=m, recipe1=recipe,
+                                              recipe2=None if homo else recipe, norm=constant, dtype=dtype,
+                                              device=dev, group=group, spectra=spectra)
+        plan.bind(dyn1.device_values(dev), None if homo else dyn2.device_values(dev))
+        return sharded.run(plan, meta, axes=(dyn1.spectral_axis, dyn2.spectral_axis))
     if not return_device and rows is None:
         odt = np.dtype(dtype)
         blocks = engine.stream_blocks(dyn1.n, dyn2.n, odt.itemsize, engine.device_budget(dev))

@@ -88,59 +88,41 @@ def test_gpu_entry_points_fail_loudly_without_device():
     assert lib.corr2d_device_info(0, ctypes.byref(sms), None, None) == _abi.ERR_CUDA
 
 
-def _small_decode(b, T, I0, I1, homo, T2=None):
-    """Python restatement of fused_decode (csrc/small.cu) -- the 32 x 32 tile
-    enumeration of a row shard [I0, I1) that the one-kernel small-m path and the
-    multi-GPU tile ranges index."""
+def _small_decode(b, T1, T2, homo):
+    """Python restatement of small_decode (csrc/small.cu): block b of the
+    one-kernel small-m path -> (row block I, column block J); homo: the upper
+    triangle row by row."""
     if not homo:
-        return I0 + b // T2, b % T2, "plain"
+        return b // T2, b % T2
     d = 0
-    S = lambda dd: dd * T - dd * (dd - 1) // 2
+    S = lambda dd: dd * T1 - dd * (dd - 1) // 2
     while S(d + 1) <= b:
         d += 1
-    I = I0 + d
-    o = b - S(d)
-    if o < I0:
-        return o, I, "trans"
-    J = I + (o - I0)
-    return I, J, ("diag" if J == I else ("mirror" if J < I1 else "plain"))
+    return d, d + (b - S(d))
 
 
-@pytest.mark.parametrize("n,rows", [(1000, (0, 1000)), (517, (0, 517)), (517, (64, 320)), (33, (0, 33)),
-                                    (700, (32, 96)), (700, (640, 700))])
-def test_small_path_tile_enumeration_covers_each_output_tile_once(n, rows):
-    """corr2d_small_tile_count (host code, no GPU needed) matches the enumeration,
-    and the enumeration writes every 32 x 32 output tile of the shard exactly
-    once (homo: direct, mirrored or transposed), the property behind the
-    bit-identity of row shards and tile-range partitions."""
+@pytest.mark.parametrize("n", [1000, 517, 64, 33, 2000])
+def test_small_path_blocks_cover_the_map_once(n):
+    """corr2d_small_block_count (host code, no GPU needed) matches the
+    enumeration, and every 64 x 64 output block is written exactly once
+    (homo: directly or as the mirror of an upper block)."""
     lib = _abi.load()
-    r0, r1 = rows
-    T = (n + 31) // 32
-    I0, I1 = r0 // 32, (r1 + 31) // 32
     for homo in (1, 0):
-        n2 = n if homo else n - 7
-        T2 = (n2 + 31) // 32
-        count = lib.corr2d_small_tile_count(n, n2, homo, r0, r1)
-        R = I1 - I0
-        assert count == (R * T - R * (R - 1) // 2 if homo else R * T2)
+        n2 = n if homo else max(1, n - 77)
+        T1, T2 = (n + 63) // 64, (n2 + 63) // 64
+        count = lib.corr2d_small_block_count(n, n2, homo)
+        assert count == (T1 * (T1 + 1) // 2 if homo else T1 * T2)
         written = {}
         for b in range(count):
-            I, J, mode = _small_decode(b, T, I0, I1, homo, T2)
-            targets = []
-            if mode in ("plain", "mirror", "diag"):
-                targets.append((I, J))
-            if mode in ("mirror", "trans"):
-                targets.append((J, I))
+            I, J = _small_decode(b, T1, T2, homo)
+            targets = [(I, J)] + ([(J, I)] if homo and J != I else [])
             for t in targets:
-                if I0 <= t[0] < I1:
-                    written[t] = written.get(t, 0) + 1
-        want = {(i, j) for i in range(I0, I1) for j in range(T if homo else T2)}
+                written[t] = written.get(t, 0) + 1
+        want = {(i, j) for i in range(T1) for j in range(T2)}
         assert set(written) == want and all(v == 1 for v in written.values())
 
 
-def test_small_path_depth_and_bad_arguments():
+def test_small_path_bad_arguments():
     lib = _abi.load()
-    assert [lib.corr2d_small_depth(m) for m in (2, 8, 11, 21, 32)] == [8, 8, 16, 24, 32]
-    assert lib.corr2d_small_depth(1) < 0 and lib.corr2d_small_depth(33) < 0
-    assert lib.corr2d_small_tile_count(10, 12, 1, 0, 10) < 0       # homo needs n1 == n2
-    assert lib.corr2d_small_tile_count(64, 64, 1, 0, 65) < 0       # rows past n1
+    assert lib.corr2d_small_block_count(10, 12, 1) < 0        # homo needs n1 == n2
+    assert lib.corr2d_small_block_count(0, 12, 0) < 0

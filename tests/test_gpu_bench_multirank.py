@@ -1,5 +1,5 @@
-"""bench.py's multi-rank path (torchrun, tile-range partition, both spectra
-schemes) end to end on one GPU: BENCH_ONE_DEVICE=1 puts both ranks on cuda:0
+"""bench.py's multi-rank path (torchrun, row bands through the public
+distributed plan, both spectra schemes) end to end on one GPU: BENCH_ONE_DEVICE=1 puts both ranks on cuda:0
 over gloo, so the launch / partition / reduction / JSON contract is exercised
 even where only one device exists (the timings mean nothing there)."""
 
@@ -15,12 +15,13 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("spectra,port", [("recompute", 29531), ("allgather", 29532)])
-def test_bench_two_ranks_one_device(spectra, port):
+@pytest.mark.parametrize("spectra,port,config", [("recompute", 29531, 2), ("broadcast", 29532, 2),
+                                                 ("broadcast", 29533, 4)])
+def test_bench_two_ranks_one_device(spectra, port, config):
     env = dict(os.environ, BENCH_ONE_DEVICE="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
-           "--config", "2", "--steps", "2", "--warmup", "3", "--spectra", spectra]
+           "--config", str(config), "--steps", "2", "--warmup", "3", "--spectra", spectra]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
