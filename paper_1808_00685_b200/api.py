@@ -16,7 +16,7 @@ from . import _abi, engine
 from . import engine as _engine_mod
 from .dataset import CorrelationSpectra, SpectralDataset
 from .engine_core import NormalizationSpec
-from .errors import DataError
+from .errors import DataError, NumericError
 from .fourier import DeviceCorrelationSpectra
 from .preprocess import (InterpolantKind, PreprocessSpec, ReferenceSpec, ResampleSpec,
                          resample_to_axis)
@@ -83,6 +83,63 @@ def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: Preproce
     return plan, homo
 
 
+_PLAN_CACHE: "OrderedDict[tuple, object]" = None
+PLAN_CACHE_SIZE = 2                    # plans kept per process (LRU)
+PLAN_CACHE_MAX_BYTES = 1 << 30         # only maps whose two planes fit in 1 GB are kept
+
+
+def _axis_key(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return (a.size, hash(a.tobytes()))
+
+
+def _cached_plan(ds1, ds2, spec, *, norm, on_zero_variance, dtype, device, engine_name):
+    """A bound plan for a host-returning corr2d() call, reused across calls of
+    the same shape / recipe (its device buffers and launch configuration),
+    rebound to this call's inputs.  Maps larger than PLAN_CACHE_MAX_BYTES are
+    never kept.  Results never alias a cached plan: the planes are copied out
+    before the call returns."""
+    global _PLAN_CACHE
+    from collections import OrderedDict
+
+    from .preprocess import _raw_device
+    if _PLAN_CACHE is None:
+        _PLAN_CACHE = OrderedDict()
+    _, dev = engine.require_device(device)
+    homo = ds2 is None or ds2 is ds1 or ds1.equals(ds2)
+    dsb = ds1 if homo else ds2
+    odt = np.dtype(dtype)
+    if 2 * ds1.n * dsb.n * odt.itemsize > PLAN_CACHE_MAX_BYTES:
+        return build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance, dtype=dtype,
+                          device=device, engine_name=engine_name)
+    nkey = norm if isinstance(norm, (str, float, int, type(None))) else (norm.kind, norm.value)
+    rs = spec.resample
+    key = (str(dev), dtype, engine_name, on_zero_variance, nkey, spec.reference.kind, float(spec.scaling_exponent),
+           None if rs is None else (rs.target_count, rs.interpolant.value), homo,
+           ds1.n, ds1.intensities.dtype.str, _axis_key(ds1.perturbation_axis),
+           None if homo else (ds2.n, ds2.intensities.dtype.str, _axis_key(ds2.perturbation_axis)),
+           engine.f64_pack_kind() if odt == np.float64 else engine.fp32_pack_kind(),
+           engine.small_fused_enabled())
+    hit = _PLAN_CACHE.get(key)
+    if hit is None:
+        plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance, dtype=dtype,
+                                device=device, engine_name=engine_name)
+        _PLAN_CACHE[key] = plan
+        while len(_PLAN_CACHE) > PLAN_CACHE_SIZE:
+            _PLAN_CACHE.popitem(last=False)
+        return plan, homo
+    _PLAN_CACHE.move_to_end(key)
+    plan = hit
+    if spec.reference.kind == "provided":            # this call's reference vector
+        spec.reference.check_length(ds1.n)
+        plan.recipe1.ref_in = engine.to_device(spec.reference.spectrum, dev)
+        if plan.recipe2 is not None:
+            spec.reference.check_length(ds2.n)
+            plan.recipe2.ref_in = plan.recipe1.ref_in
+    plan.bind(_raw_device(ds1, dev), None if homo else _raw_device(ds2, dev))
+    return plan, homo
+
+
 @engine.on_device
 def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, reference="mean",
            resample: int | None = None, resample_to_common: int | None = None,
@@ -132,10 +189,19 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
                     engine=engine, is_homo=homo, scaling_exponent=float(alpha) if alpha > 0 else 0.0)
         return sharded.run(plan, meta, axes=(ds1.spectral_axis, dsb.spectral_axis))
     blocks = None
+    plan = None
     if not return_device:
         _, dev = _engine_mod.require_device(device)
         odt = np.dtype(dtype)
-        blocks = _engine_mod.stream_blocks(ds1.n, dsb.n, odt.itemsize, _engine_mod.device_budget(dev))
+        blocks = _engine_mod.maybe_stream_blocks(ds1.n, dsb.n, odt.itemsize, dev)
+        if blocks is None:
+            try:
+                plan, homo = _cached_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
+                                          dtype=dtype, device=device, engine_name=engine)
+            except NumericError as e:            # the device is fuller than the size check assumed
+                if "out of memory" not in str(e):
+                    raise
+                blocks = _engine_mod.stream_blocks(ds1.n, dsb.n, odt.itemsize, _engine_mod.device_budget(dev))
         if blocks is not None:        # planes larger than device memory: stream row blocks
             def make_plan(rws):
                 return build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance, dtype=dtype,
@@ -149,8 +215,9 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
                 sync=s, asyn=a, axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, ref1=first[0], ref2=first[1],
                 normalization=constant, engine=engine, is_homo=homo,
                 scaling_exponent=float(alpha) if alpha > 0 else 0.0, stats=info)
-    plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
-                            dtype=dtype, device=device, engine_name=engine)
+    if return_device:
+        plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
+                                dtype=dtype, device=device, engine_name=engine)
     plan.launch()
     _engine_mod.sync()
     ref1, ref2, _, _, info = plan.check(axes=(ds1.spectral_axis, dsb.spectral_axis),

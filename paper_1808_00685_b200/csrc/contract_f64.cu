@@ -61,6 +61,7 @@ struct ContractParams {
   long long ld_pack;
   int n1, n2, mp;
   int kg;           // Gauss operands (CORR2D_PACK_F64_GAUSS): slots per segment, mp = 3 kg
+  int dbg;          // profiling builds only (-DCORR2D_PROFILING): 1 = no output stores, 2 = no MMAs
   int homo;
   int row0, row1;
   int I0, I1, T;  // row-tile range of the shard, number of column tiles
@@ -251,6 +252,46 @@ __device__ __forceinline__ void mma_chunk1(double (&acc)[kMT][4][4], const doubl
   }
 }
 
+// Two operand pairs, two accumulator sets, interleaved per k-step: 16
+// independent DMMAs per warp and k-step.
+__device__ __forceinline__ void mma_chunk2(double (&acc0)[kMT][4][4], double (&acc1)[kMT][4][4],
+                                           const double* A0, const double* B0, const double* A1, const double* B1,
+                                           int kc, int wm, int wn, int lr, int lk) {
+#pragma unroll 2
+  for (int kk = 0; kk < kc; kk += 4) {
+    double a0[2][2], a1[2][2], b0[4], b1[4];
+#pragma unroll
+    for (int mt = 0; mt < kMT; ++mt) {
+      const int r = wm * 16 * kMT + mt * 16 + lr;
+      a0[mt][0] = A0[r * kKS + kk + lk];
+      a0[mt][1] = A0[(r + 8) * kKS + kk + lk];
+      a1[mt][0] = A1[r * kKS + kk + lk];
+      a1[mt][1] = A1[(r + 8) * kKS + kk + lk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      b0[nt] = B0[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
+      b1[nt] = B1[(wn * 32 + nt * 8 + lr) * kKS + kk + lk];
+    }
+#pragma unroll
+    for (int mt = 0; mt < kMT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        dmma_16x8x4(acc0[mt][nt], a0[mt][0], a0[mt][1], b0[nt]);
+        dmma_16x8x4(acc1[mt][nt], a1[mt][0], a1[mt][1], b1[nt]);
+      }
+  }
+}
+
+__device__ __forceinline__ int f64_dbg(const ContractParams& p) {
+#ifdef CORR2D_PROFILING
+  return p.dbg;
+#else
+  (void)p;
+  return 0;
+#endif
+}
+
 template <bool GAUSS>
 __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel(const ContractParams p) {
   extern __shared__ __align__(16) double sm[];
@@ -274,22 +315,19 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
       for (int c = 0; c < 4; ++c) acc_phi[a][bq][c] = acc_psi[a][bq][c] = 0.0;
 
   if constexpr (GAUSS) {
-    // three products per bin (corr2d.h CORR2D_PACK_F64_GAUSS): segment 0 (P1)
-    // into the sync accumulator, copied into the async one, then segment 2
-    // (-P3) into sync and segment 1 (P2) into async -- two accumulator sets,
-    // 3 kg multiply-adds per element instead of 2 m.  Depth chunks are double
-    // buffered: chunk c + 1 streams in (cp.async) while chunk c is multiplied.
-    const int cps = (p.kg + kKC - 1) / kKC;          // chunks per segment
-    const int nch = 3 * cps;
-    constexpr int kGBuf = 2 * kBM * kKS;             // doubles per buffer (A and B)
-    auto issue = [&](int ch) {
-      const int si = ch / cps, k0 = (ch - si * cps) * kKC;
-      const int seg = si == 0 ? 0 : (si == 1 ? 2 : 1);
+    // three products per bin (corr2d.h CORR2D_PACK_F64_GAUSS), 3 kg
+    // multiply-adds per element instead of 2 m.  Phase A runs two independent
+    // accumulator chains per k-step (DMMA latency hidden as in the four-product
+    // kernel): segment 0 (P1) into the async set and segment 2 (-P3) into the
+    // sync set; then sync += async gives P1 - P3, and phase B adds segment 1
+    // (P2) to the async set: P1 + P2.
+    constexpr int kTile = kBM * kKS;                 // doubles per operand tile
+    auto issue = [&](int seg, int k0, int slot) {
       const int kc = min(kKC, p.kg - k0);
       const int vec = kc / 2;
       const int kbase = seg * p.kg + k0;
-      double* A = sm + (ch & 1) * kGBuf;
-      double* B = A + kBM * kKS;
+      double* A = sm + 2 * slot * kTile;
+      double* B = A + kTile;
       for (int idx = tid; idx < kBM * vec; idx += kThreads) {
         const int r = kc == kKC ? idx / (kKC / 2) : idx / vec;
         const int v = idx - r * vec;
@@ -298,32 +336,28 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
         cp_async16(A + r * kKS + 2 * v, p.a_phi + (long long)(va ? gi : 0) * p.ld_pack + kbase + 2 * v, va);
         cp_async16(B + r * kKS + 2 * v, p.b + (long long)(vb ? gj : 0) * p.ld_pack + kbase + 2 * v, vb);
       }
-      asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    issue(0);
-    for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) {
-        issue(ch + 1);
-        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-      }
+    for (int k0 = 0; k0 < p.kg; k0 += kKC) {          // phase A: segments 0 and 2 together
+      issue(0, k0, 0);
+      issue(2, k0, 1);
+      cp_async_wait_all();
       __syncthreads();
-      const int si = ch / cps, k0 = (ch - si * cps) * kKC;
       const int kc = min(kKC, p.kg - k0);
-      const double* A = sm + (ch & 1) * kGBuf;
-      const double* B = A + kBM * kKS;
-      if (si == 2) mma_chunk1(acc_psi, A, B, kc, wm, wn, lr, lk);
-      else mma_chunk1(acc_phi, A, B, kc, wm, wn, lr, lk);
-      if (si == 0 && k0 + kKC >= p.kg) {             // P1 complete: the async accumulator starts from it
+      if (!(f64_dbg(p) & 2)) mma_chunk2(acc_psi, acc_phi, sm, sm + kTile, sm + 2 * kTile, sm + 3 * kTile, kc, wm, wn, lr, lk);
+      __syncthreads();
+    }
 #pragma unroll
-        for (int a = 0; a < kMT; ++a)
+    for (int a = 0; a < kMT; ++a)
 #pragma unroll
-          for (int bq = 0; bq < 4; ++bq)
+      for (int bq = 0; bq < 4; ++bq)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc_psi[a][bq][c] = acc_phi[a][bq][c];
-      }
-      __syncthreads();                               // buffer (ch & 1) free for chunk ch + 2
+        for (int c = 0; c < 4; ++c) acc_phi[a][bq][c] += acc_psi[a][bq][c];
+    for (int k0 = 0; k0 < p.kg; k0 += kKC) {          // phase B: segment 1
+      issue(1, k0, 0);
+      cp_async_wait_all();
+      __syncthreads();
+      if (!(f64_dbg(p) & 2)) mma_chunk1(acc_psi, sm, sm + kTile, min(kKC, p.kg - k0), wm, wn, lr, lk);
+      __syncthreads();
     }
   } else {
 
@@ -389,6 +423,16 @@ __global__ void __launch_bounds__(kThreads, CORR2D_F64_MINB) contract_f64_kernel
   }
   }  // !GAUSS
 
+#ifdef CORR2D_PROFILING
+  if (p.dbg & 1) {                    // profiling: everything but the output stores
+    unsigned long long z = 0;
+    for (int a = 0; a < kMT; ++a)
+      for (int b = 0; b < 4; ++b)
+        for (int c = 0; c < 4; ++c) z ^= abs_bits(acc_phi[a][b][c]) ^ abs_bits(acc_psi[a][b][c]);
+    if (z == 0x123456789ull) p.stats[3] = z;
+    return;
+  }
+#endif
   // ---- epilogue.  Plain / mirrored tiles write their direct part straight
   //      from the DMMA fragments (a thread holds 2 adjacent columns of 2 rows:
   //      16-byte stores, 8 x 64-B row segments per warp instruction); the planes
@@ -488,12 +532,15 @@ static int launch_contract(ContractParams p, bool gauss, int64_t tile0, int64_t 
   if (tile1 < 0 || tile1 > tiles) tile1 = tiles;
   if (tile0 < 0 || tile0 > tile1) return fail(CORR2D_ERR_DATA, std::string(who) + ": bad tile range");
   p.tile0 = tile0;
+#ifdef CORR2D_PROFILING
+  if (const char* e = getenv("CORR2D_DEBUG_SKIP")) p.dbg = atoi(e);
+#endif
   tiles = tile1 - tile0;
   if (tiles > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, std::string(who) + ": tile count out of range");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(p.stats, 0, 3 * sizeof(unsigned long long), st) != cudaSuccess) return check_launch("stats reset");
   if (tiles == 0) return CORR2D_OK;
-  const size_t smem_ops = gauss ? (size_t)4 * kBM * kKS * sizeof(double) : (size_t)kNBuf * kBufStride * sizeof(double);
+  const size_t smem_ops = gauss ? (size_t)4 * kBM * kKS * sizeof(double) : (size_t)kNBuf * kBufStride * sizeof(double);  // gauss: A0 B0 A2 B2
   const size_t smem_epi = 2 * (size_t)kBM * kCS * sizeof(double);
   const size_t smem = smem_ops > smem_epi ? smem_ops : smem_epi;
   if (gauss) {

@@ -1,0 +1,590 @@
+// The whole small-m correlation in ONE launch (corr2d_correlate_small_f64):
+// fp64, 2 <= m <= 32, no resampling -- the cfg1 (m = 11) and cfg2 (m = 21)
+// shapes, where the step is bound by launch latency, one DRAM round trip and
+// the output write (cfg1: 16 MB of planes, 2.5 us at HBM peak).
+//
+// small_block_kernel: every CTA owns one 64 x 64 output block and never waits
+// for another CTA (no ready flags, no grid barrier, no co-residency
+// assumption):
+//   1. K1 for the block's 128 channels (64 row + 64 column channels; 64 on
+//      homo diagonal blocks), one lane per channel: the reference's statistics
+//      in its order (sequential sums: bitwise-equal reference / sigma / values),
+//   2. the real DFT of the block's channels as an FP64 tensor-core product
+//      Y[bins x channels] = W[bins x t] . y[t x channels] (W: cos / -sin rows
+//      from a per-m host table), each warp transforming its own 32 lanes'
+//      channels,
+//   3. the CORR2D_PACK_F64_GAUSS slots (three real products per bin) into
+//      shared memory, then the 64 x 64 contraction on the FP64 tensor pipe,
+//   4. both planes staged in shared memory and written as coalesced rows --
+//      plus the mirror (sync^T, -async^T) of homo blocks above the diagonal,
+//      diagonal blocks symmetrised -- with the max|.| / finite reduction fused.
+// Status / stat words are self-resetting: the last CTA to finish (an arrival
+// counter, never a wait) publishes and re-zeroes them.
+//
+// Reference path: preprocess.py:123-137, :198-259 (reference, sigma, scaling),
+// fourier.py:61-82 (rfft along the perturbation axis), fourier.py:107-123
+// (weighted half-spectrum cross sum x Norm, split into sync / async),
+// engine_core.py:139-140 (finite check), dataset.py:159-170 (homo symmetry).
+#include "prep_params.cuh"
+
+#include <climits>
+#include <cmath>
+#include <mutex>
+#include <vector>
+
+namespace corr2d {
+
+constexpr int kSB = 64;          // output block edge (rows and columns)
+constexpr int kSThreads = 128;   // 4 warps: one lane per K1 channel, 32 x 32 warp tiles
+constexpr int kSMaxM = 32;
+constexpr int kYS = 132;         // sample rows [t][channel]: stride = 4 mod 16 doubles (conflict-free B fragments)
+constexpr int kCS = kSB + 1;     // epilogue staging stride
+
+struct SmallParams {
+  const void* raw1;
+  const void* raw2;
+  long long ld1, ld2;
+  int in_f32;
+  int m, n1, n2, homo;
+  int ref_mode1, ref_mode2;
+  const double* ref_in1;
+  const double* ref_in2;
+  const double* sigma_in1;
+  const double* sigma_in2;
+  double alpha;
+  int substitute;
+  double norm;
+  double* ref_out1;
+  double* sigma_out1;
+  double* ref_out2;
+  double* sigma_out2;
+  const double* W;          // DFT rows: [3 x 16][mpad] (cos bins 0..15 | -sin bins 0..15 | cos bins 16..31)
+  int mpad;                 // m rounded up to 4 (the DMMA k-step); samples past m are 0
+  int yrows;                // rows of the sample / spectrum region: max(mpad, 2 (m / 2 + 1))
+  int kg, ks;               // Gauss slots per segment; operand row stride (doubles, = 4 mod 16)
+  int T1, T2;               // 64-blocks along rows / columns
+  double* phi;
+  double* psi;
+  long long ld_out;
+  int vec;                  // planes 16-B aligned with an even ld_out: 16-byte stores
+  int* status1;
+  int* status2;
+  unsigned long long* stats;
+  int* work;                // kW* words, zero-filled once by the caller
+};
+
+// work-buffer words (int32 indices); every launch leaves them zero
+constexpr int kWStatus1 = 0;   // [0, 4)  K1 status accumulator, dataset 1
+constexpr int kWStatus2 = 4;   // [4, 8)  dataset 2
+constexpr int kWDone = 8;      // CTAs finished (the last one publishes and resets)
+constexpr int kWStats = 10;    // [10, 16) max|sync|, max|async|, non-finite count (3 x uint64)
+
+__device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 "
+      "{%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// Block b of the enumeration -> (row block I, column block J).  homo: the upper
+// triangle J >= I, row by row (row I owns T - I blocks).
+__device__ __forceinline__ void small_decode(const SmallParams& p, long long b, int& I, int& J) {
+  if (!p.homo) {
+    I = (int)(b / p.T2);
+    J = (int)(b - (long long)I * p.T2);
+    return;
+  }
+  const long long T = p.T1;
+  const long long t2 = 2 * T + 1;
+  const long long disc = t2 * t2 - 8 * b;
+  long long d = (long long)((float)t2 - sqrtf((float)(disc > 0 ? disc : 0))) / 2;   // fp32 guess, exact fix-up
+  auto S = [&](long long dd) { return dd * T - dd * (dd - 1) / 2; };
+  if (d < 0) d = 0;
+  while (d > 0 && S(d) > b) --d;
+  while (S(d + 1) <= b) ++d;
+  I = (int)d;
+  J = I + (int)(b - S(d));
+}
+
+// Statistics and dynamic values of one channel (one lane), in place in its
+// shared-memory column ys[t * kYS]: the IEEE operations of the other K1
+// kernels in the reference's order.  The owner lane reports status /
+// reference / sigma.
+__device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c, bool valid, bool owner,
+                                           double* ys) {
+  const int m = p.m;
+  const int ref_mode = set ? p.ref_mode2 : p.ref_mode1;
+  int* status = p.work + (set ? kWStatus2 : kWStatus1);
+  double ref = 0.0, scale = 1.0;
+  int bad = 0;
+  for (int t = 0; t < m; ++t) bad += !isfinite(ys[t * kYS]);
+  if (owner && valid && bad) atomicAdd(&status[CORR2D_ST_NONFINITE], bad);
+  if (ref_mode == CORR2D_REF_PROVIDED) {
+    ref = valid ? __ldg((set ? p.ref_in2 : p.ref_in1) + c) : 0.0;
+  } else if (ref_mode == CORR2D_REF_MEAN) {
+    double sum = 0.0;                                  // left to right (numpy's axis-0 order)
+    for (int t = 0; t < m; ++t) sum = __dadd_rn(sum, ys[t * kYS]);
+    ref = __ddiv_rn(sum, (double)m);
+  }
+  if (p.alpha > 0.0) {
+    const double* sigma_in = set ? p.sigma_in2 : p.sigma_in1;
+    double sigma;
+    if (sigma_in) {
+      sigma = valid ? __ldg(sigma_in + c) : 1.0;
+    } else {
+      double ss = 0.0;
+      for (int t = 0; t < m; ++t) {
+        const double d = __dsub_rn(ys[t * kYS], ref);
+        ss = __dadd_rn(ss, __dmul_rn(d, d));
+      }
+      sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
+    }
+    if (owner && valid) {
+      double* so = set ? p.sigma_out2 : p.sigma_out1;
+      if (so) so[c] = sigma;
+      if (sigma == 0.0) {
+        atomicAdd(&status[CORR2D_ST_ZEROVAR], 1);
+        atomicMax(&status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - c);
+      }
+    }
+    if (sigma == 0.0 && p.substitute) sigma = 1.0;
+    scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
+  }
+  if (owner && valid && ref_mode != CORR2D_REF_NONE) {
+    double* ro = set ? p.ref_out2 : p.ref_out1;
+    if (ro) ro[c] = ref;
+  }
+  const bool sub = ref_mode != CORR2D_REF_NONE, div = p.alpha > 0.0;
+  for (int t = 0; t < m; ++t) {
+    double v = ys[t * kYS];
+    if (sub) v = __dsub_rn(v, ref);
+    if (div) v = __ddiv_rn(v, scale);
+    ys[t * kYS] = valid ? v : 0.0;
+  }
+}
+
+// The Gauss slots of bin w (spectrum R + i I) of one channel into its operand
+// row(s) (corr2d.h CORR2D_PACK_F64_GAUSS).
+__device__ __forceinline__ void put_bin(int w, int m, int kg, double norm, double R, double I, double* rowA,
+                                        double* rowB) {
+  const int H = m / 2, Iint = gauss_interior(m);
+  if (w > H) return;
+  double va, vb;
+  if (w <= Iint) {                                     // DC / interior: segments 0 and 1 at slot w
+#pragma unroll
+    for (int seg = 0; seg < 2; ++seg) {
+      gauss_values(seg, w, m, norm, R, I, va, vb);
+      if (rowA) rowA[seg * kg + w] = va;
+      if (rowB) rowB[seg * kg + w] = vb;
+    }
+  }
+  if (w >= 1) {                                        // interior at w - 1, Nyquist at slot Iint
+    gauss_values(2, w, m, norm, R, I, va, vb);
+    if (rowA) rowA[2 * kg + w - 1] = va;
+    if (rowB) rowB[2 * kg + w - 1] = vb;
+  }
+}
+
+// One Gauss segment of the depth (kg slots) into one accumulator set.
+__device__ __forceinline__ void small_mma_seg(double (&acc)[2][4][4], const double* As, const double* Bs, int ks,
+                                              int k0, int kg, int wm, int wn, int lr, int lk) {
+  for (int kk = 0; kk < kg; kk += 4) {
+    double ap[2][2], bf[4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = wm * 32 + mt * 16 + lr;
+      ap[mt][0] = As[r * ks + k0 + kk + lk];
+      ap[mt][1] = As[(r + 8) * ks + k0 + kk + lk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = Bs[(wn * 32 + nt * 8 + lr) * ks + k0 + kk + lk];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], ap[mt][0], ap[mt][1], bf[nt]);
+  }
+}
+
+__global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_constant__ SmallParams p) {
+  extern __shared__ __align__(16) double sm[];
+  const int m = p.m, ks = p.ks, kg = p.kg, mpad = p.mpad;
+  double* ys = sm;                                   // [mpad][kYS]
+  double* As = ys + (size_t)p.yrows * kYS;          // [64][ks]
+  double* Bs = As + (size_t)kSB * ks;                // [64][ks]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+
+  int I, J;
+  small_decode(p, blockIdx.x, I, J);
+  const bool diag = p.homo && I == J;
+  // operand rows start at zero (pad slots stay zero)
+  for (int i = tid; i < kSB * ks; i += kSThreads) {
+    reinterpret_cast<double2*>(As)[i] = make_double2(0.0, 0.0);   // As and Bs: 2 * 64 * ks doubles
+  }
+  // programmatic dependent launch: everything above overlapped the previous
+  // kernel's tail; from here on memory written by it is visible
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+
+  // ---- 1. samples and statistics: lanes 0..63 the row channels (role A; on
+  //      homo diagonal blocks also role B), lanes 64..127 the column channels
+  //      (role B; idle on diagonal blocks) ----
+  const bool col_warp = warp >= 2;
+  const int set = (col_warp && !p.homo) ? 1 : 0;
+  const int c = col_warp ? J * kSB + tid - kSB : I * kSB + tid;
+  const int n = set ? p.n2 : (col_warp ? p.n2 : p.n1);
+  const bool active = !(diag && col_warp);
+  const bool valid = c < n;
+  if (active) {
+    const void* raw = set ? p.raw2 : p.raw1;
+    const long long ld = set ? p.ld2 : p.ld1;
+    const int cc = valid ? c : n - 1;
+    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + tid));
+    if (p.in_f32) {
+      const float* r = static_cast<const float*>(raw) + cc;
+      for (int t = 0; t < m; ++t)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 8u * kYS * t), "l"(r + (long long)t * ld) : "memory");
+    } else {
+      const double* r = static_cast<const double*>(raw) + cc;
+      for (int t = 0; t < m; ++t)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * kYS * t), "l"(r + (long long)t * ld) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    if (p.in_f32)
+      for (int t = 0; t < m; ++t) ys[t * kYS + tid] = (double)reinterpret_cast<const float*>(ys + t * kYS + tid)[0];
+    for (int t = m; t < mpad; ++t) ys[t * kYS + tid] = 0.0;
+    // the channel's statistics / status are reported by one block only: the
+    // diagonal block (homo), column block 0 (dataset 1) or row block 0 (dataset 2)
+    const bool owner = p.homo ? diag : (col_warp ? I == 0 : J == 0);
+    lane_stats(p, set, c, valid, owner, ys + tid);
+  }
+  __syncthreads();                                   // zeroed operand rows before the slot writes
+
+  // ---- 2. DFT of this warp's 32 channels on the FP64 tensor pipe:
+  //      Y[16 bins x 8 channels] tiles = W rows . y, k over t ----
+  if (active) {
+    const int nt3 = m / 2 >= 16 ? 3 : 2;             // bins 16.. only for m = 32
+    double acc[3][4][4];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[a][b][q] = 0.0;
+    const double* yw = ys + warp * 32;
+    for (int kk = 0; kk < mpad; kk += 4) {
+      double bf[4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = yw[(kk + lk) * kYS + nt * 8 + lr];
+#pragma unroll
+      for (int tl = 0; tl < 3; ++tl) {
+        if (tl == 2 && nt3 < 3) break;
+        const double a0 = __ldg(p.W + (tl * 16 + lr) * mpad + kk + lk);
+        const double a1 = __ldg(p.W + (tl * 16 + lr + 8) * mpad + kk + lk);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[tl][nt], a0, a1, bf[nt]);
+      }
+    }
+    // ---- 3. the spectra back into the warp's own sample columns (bin w: Re in
+    //      row 2 w, Im in row 2 w + 1), then each lane turns its channel's bins
+    //      into the Gauss operand slots ----
+    __syncwarp();                                    // the warp's DMMAs have read its columns
+    double* yl = ys + warp * 32;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int col = nt * 8 + 2 * lk + e, w = lr + 8 * h;
+          if (w > m / 2) continue;                       // rows past 2 H + 1 belong to the operand rows
+          yl[(2 * w) * kYS + col] = acc[0][nt][2 * h + e];
+          yl[(2 * w + 1) * kYS + col] = acc[1][nt][2 * h + e];
+          if (nt3 == 3 && h == 0 && lr == 0) {
+            yl[32 * kYS + col] = acc[2][nt][e];          // bin 16 (m = 32: Nyquist, real)
+            yl[33 * kYS + col] = 0.0;
+          }
+        }
+    __syncwarp();
+    const int rowc = col_warp ? tid - kSB : tid;
+    double* rowA = col_warp ? nullptr : As + (size_t)rowc * ks;
+    double* rowB = (col_warp || diag) ? Bs + (size_t)rowc * ks : nullptr;
+    for (int w = 0; w <= m / 2; ++w)
+      put_bin(w, m, kg, p.norm, ys[(2 * w) * kYS + tid], ys[(2 * w + 1) * kYS + tid], rowA, rowB);
+  }
+  __syncthreads();
+
+  // ---- 4. contraction (Gauss): P1 -> sync, copy to async; -P3 -> sync, P2 -> async ----
+  const int wm = warp >> 1, wn = warp & 1;
+  double aphi[2][4][4], apsi[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) aphi[a][b][q] = 0.0;
+  small_mma_seg(aphi, As, Bs, ks, 0, kg, wm, wn, lr, lk);
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) apsi[a][b][q] = aphi[a][b][q];
+  small_mma_seg(aphi, As, Bs, ks, 2 * kg, kg, wm, wn, lr, lk);
+  small_mma_seg(apsi, As, Bs, ks, kg, kg, wm, wn, lr, lk);
+  __syncthreads();                                   // operands consumed: the staging overlays them
+
+  // ---- 5. stage both planes, then coalesced row stores (+ mirror) ----
+  double* Cphi = sm;                                 // [64][kCS]
+  double* Cpsi = sm + kSB * kCS;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = wm * 32 + mt * 16 + lr + 8 * h, cl = wn * 32 + nt * 8 + 2 * lk;
+        Cphi[r * kCS + cl] = aphi[mt][nt][2 * h];
+        Cphi[r * kCS + cl + 1] = aphi[mt][nt][2 * h + 1];
+        Cpsi[r * kCS + cl] = apsi[mt][nt][2 * h];
+        Cpsi[r * kCS + cl + 1] = apsi[mt][nt][2 * h + 1];
+      }
+  __syncthreads();
+  unsigned long long mphi = 0, mpsi = 0;
+  const int i0 = I * kSB, j0 = J * kSB;
+  const bool rows_full = i0 + kSB <= p.n1, cols_full = j0 + kSB <= p.n2;
+  // direct block: rows i0.., a thread stores column pairs (32 pairs per row)
+  for (int idx = tid; idx < kSB * (kSB / 2); idx += kSThreads) {
+    const int r = idx >> 5, cp = (idx & 31) * 2;
+    const int gi = i0 + r, gj = j0 + cp;
+    if (gi >= p.n1 || gj >= p.n2) continue;
+    double f0, f1, s0, s1;
+    if (diag) {          // upper triangle incl. the diagonal; below it the mirror of the upper
+      f0 = r <= cp ? Cphi[r * kCS + cp] : Cphi[cp * kCS + r];
+      f1 = r <= cp + 1 ? Cphi[r * kCS + cp + 1] : Cphi[(cp + 1) * kCS + r];
+      s0 = r < cp ? Cpsi[r * kCS + cp] : (r == cp ? 0.0 : neg_bits(Cpsi[cp * kCS + r]));
+      s1 = r < cp + 1 ? Cpsi[r * kCS + cp + 1] : (r == cp + 1 ? 0.0 : neg_bits(Cpsi[(cp + 1) * kCS + r]));
+    } else {
+      f0 = Cphi[r * kCS + cp]; f1 = Cphi[r * kCS + cp + 1];
+      s0 = Cpsi[r * kCS + cp]; s1 = Cpsi[r * kCS + cp + 1];
+    }
+    mphi = max(mphi, abs_bits(f0));
+    mpsi = max(mpsi, abs_bits(s0));
+    const long long o = (long long)gi * p.ld_out + gj;
+    if (gj + 1 < p.n2) {
+      mphi = max(mphi, abs_bits(f1));
+      mpsi = max(mpsi, abs_bits(s1));
+      if (p.vec) {
+        __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
+        __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
+        continue;
+      }
+      __stcs(p.phi + o + 1, f1);
+      __stcs(p.psi + o + 1, s1);
+    }
+    __stcs(p.phi + o, f0);
+    __stcs(p.psi + o, s0);
+  }
+  // mirror block of a homo block above the diagonal: rows j0.., columns i0..
+  if (p.homo && !diag) {
+    for (int idx = tid; idx < kSB * (kSB / 2); idx += kSThreads) {
+      const int r = idx >> 5, cp = (idx & 31) * 2;        // mirror row r (= C column), columns cp, cp + 1 (= C rows)
+      const int gi = j0 + r, gj = i0 + cp;
+      if ((!cols_full && gi >= p.n2) || gj >= p.n1) continue;
+      const double f0 = Cphi[cp * kCS + r], f1 = Cphi[(cp + 1) * kCS + r];
+      const double s0 = neg_bits(Cpsi[cp * kCS + r]), s1 = neg_bits(Cpsi[(cp + 1) * kCS + r]);
+      const long long o = (long long)gi * p.ld_out + gj;
+      if (p.vec && (rows_full || gj + 1 < p.n1)) {
+        __stcs(reinterpret_cast<double2*>(p.phi + o), make_double2(f0, f1));
+        __stcs(reinterpret_cast<double2*>(p.psi + o), make_double2(s0, s1));
+      } else {
+        __stcs(p.phi + o, f0);
+        __stcs(p.psi + o, s0);
+        if (gj + 1 < p.n1) {
+          __stcs(p.phi + o + 1, f1);
+          __stcs(p.psi + o + 1, s1);
+        }
+      }
+    }
+  }
+  // ---- max|.| and the finite check (integer pipe), one set of atomics per CTA ----
+  constexpr unsigned long long kInf = 0x7ff0000000000000ull;
+  int bad = (mphi >= kInf) + (mpsi >= kInf);
+  mphi = min(mphi, kInf);
+  mpsi = min(mpsi, kInf);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mphi = max(mphi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mphi, o));
+    mpsi = max(mpsi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mpsi, o));
+  }
+  bad = warp_sum(bad);
+  __shared__ unsigned long long red[3][4];
+  if (lane == 0) {
+    red[0][warp] = mphi;
+    red[1][warp] = mpsi;
+    red[2][warp] = (unsigned long long)bad;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWStats);
+    unsigned long long a0 = 0, a1 = 0, a2 = 0;
+    for (int w = 0; w < kSThreads / 32; ++w) {
+      a0 = max(a0, red[0][w]);
+      a1 = max(a1, red[1][w]);
+      a2 += red[2][w];
+    }
+    if (a0) atomicMax(&acc[0], a0);
+    if (a1) atomicMax(&acc[1], a1);
+    if (a2) atomicAdd(&acc[2], a2);
+    // the last CTA to finish publishes status / stats and leaves the words zero
+    __threadfence();
+    if (atomicAdd(p.work + kWDone, 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      volatile int* wv = p.work;
+      for (int k = 0; k < 4; ++k) {
+        p.status1[k] = wv[kWStatus1 + k];
+        if (p.status2) p.status2[k] = wv[kWStatus2 + k];
+        wv[kWStatus1 + k] = 0;
+        wv[kWStatus2 + k] = 0;
+      }
+      volatile unsigned long long* av = acc;
+      for (int k = 0; k < 3; ++k) {
+        p.stats[k] = av[k];
+        av[k] = 0ull;
+      }
+      wv[kWDone] = 0;
+      __threadfence();
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+static long long small_blocks(int n1, int n2, int homo) {
+  const long long T1 = (n1 + kSB - 1) / kSB, T2 = (n2 + kSB - 1) / kSB;
+  return homo ? T1 * (T1 + 1) / 2 : T1 * T2;
+}
+
+// Per-(device, m) DFT row table W in device memory, built once on the host in
+// double precision: row 16 k + r, column t < m holds cos(2 pi w t / m) for
+// k = 0 (bins w = r), -sin(2 pi w t / m) for k = 1 (w = r), cos for k = 2
+// (w = 16 + r); bins past m / 2 and columns past m are zero.
+static const double* dft_table(int m, int mpad, cudaStream_t st, int* rc) {
+  constexpr int kDev = 64;
+  static double* tab[kDev][kSMaxM + 1] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kDev) {
+    *rc = fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: device index >= 64");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (tab[dev][m]) return tab[dev][m];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone) {
+    *rc = fail(CORR2D_ERR_UNSUPPORTED,
+               "corr2d_correlate_small_f64: the first call for this m on this device must not be graph-captured");
+    return nullptr;
+  }
+  std::vector<double> h((size_t)48 * mpad, 0.0);
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int k = 0; k < 3; ++k)
+    for (int r = 0; r < 16; ++r) {
+      const int w = (k == 2 ? 16 : 0) + r;
+      if (w > m / 2) continue;
+      for (int t = 0; t < m; ++t) {
+        const double ang = two_pi * (double)((w * t) % m) / (double)m;
+        h[(size_t)(16 * k + r) * mpad + t] = k == 1 ? -std::sin(ang) : std::cos(ang);
+      }
+    }
+  double* d = nullptr;
+  if (cudaMalloc(&d, h.size() * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+    *rc = check_launch("small DFT table");
+    return nullptr;
+  }
+  tab[dev][m] = d;
+  return d;
+}
+
+}  // namespace corr2d
+
+using namespace corr2d;
+
+extern "C" int64_t corr2d_small_block_count(int n1, int n2, int homo) {
+  if (n1 < 1 || n2 < 1 || (homo && n1 != n2)) return -1;
+  return small_blocks(n1, n2, homo);
+}
+
+extern "C" int corr2d_correlate_small_f64(
+    int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
+    int m, int n1, int n2,
+    int ref_mode1, const double* ref_in1, const double* sigma_in1,
+    int ref_mode2, const double* ref_in2, const double* sigma_in2,
+    double alpha, int substitute_zero_var, double norm_const,
+    double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
+    double* phi, double* psi, int64_t ld_out,
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream) {
+  const bool homo = raw2 == nullptr;
+  if (!raw1 || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
+    return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
+  if (in_dtype != CORR2D_F64 && in_dtype != CORR2D_F32) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad dtype");
+  if (m < 2 || m > kSMaxM) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: needs 2 <= m <= 32");
+  if (n1 < 1 || n2 < 1) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad sizes");
+  if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: homo needs n1 == n2");
+  if (ld_raw1 < n1 || (!homo && ld_raw2 < n2)) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_raw < n");
+  if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_out < n2");
+  if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(CORR2D_ERR_DATA, "scaling exponent must lie in [0, 1]");
+  for (int r : {ref_mode1, ref_mode2})
+    if (r < CORR2D_REF_MEAN || r > CORR2D_REF_NONE) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad ref_mode");
+  if ((ref_mode1 == CORR2D_REF_PROVIDED && !ref_in1) || (!homo && ref_mode2 == CORR2D_REF_PROVIDED && !ref_in2))
+    return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: provided reference missing");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  SmallParams p{};
+  p.raw1 = raw1; p.raw2 = raw2; p.ld1 = ld_raw1; p.ld2 = ld_raw2; p.in_f32 = in_dtype == CORR2D_F32;
+  p.m = m; p.n1 = n1; p.n2 = n2; p.homo = homo;
+  p.ref_mode1 = ref_mode1; p.ref_mode2 = ref_mode2; p.ref_in1 = ref_in1; p.ref_in2 = ref_in2;
+  p.sigma_in1 = sigma_in1; p.sigma_in2 = sigma_in2; p.alpha = alpha; p.substitute = substitute_zero_var;
+  p.norm = norm_const;
+  p.ref_out1 = ref_out1; p.sigma_out1 = sigma_out1; p.ref_out2 = ref_out2; p.sigma_out2 = sigma_out2;
+  p.mpad = (m + 3) / 4 * 4;
+  p.yrows = p.mpad > 2 * (m / 2 + 1) ? p.mpad : 2 * (m / 2 + 1);
+  int rc = CORR2D_OK;
+  p.W = dft_table(m, p.mpad, st, &rc);
+  if (!p.W) return rc;
+  p.kg = gauss_kg(m);
+  p.ks = (3 * p.kg + 11) / 16 * 16 + 4;
+  p.T1 = (n1 + kSB - 1) / kSB; p.T2 = (n2 + kSB - 1) / kSB;
+  p.phi = phi; p.psi = psi; p.ld_out = ld_out;
+  p.vec = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
+  p.status1 = status1; p.status2 = homo ? nullptr : status2; p.stats = stats; p.work = work;
+  const long long blocks = small_blocks(n1, n2, homo);
+  if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
+  const size_t ops = ((size_t)p.yrows * kYS + 2 * (size_t)kSB * p.ks) * sizeof(double);
+  const size_t stage = 2 * (size_t)kSB * kCS * sizeof(double);
+  const size_t smem = ops > stage ? ops : stage;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const size_t worst = ((size_t)(kSMaxM + 2) * kYS + 2 * (size_t)kSB * 52) * sizeof(double);
+    cudaFuncSetAttribute(small_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(worst > stage ? worst : stage));
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kSThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  // programmatic dependent launch: this grid's launch and prologue overlap the
+  // previous kernel's tail (griddepcontrol.wait orders memory).  No CTA waits
+  // for another, so the grid needs no co-residency.
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, small_block_kernel, p);
+  return check_launch("small_block_kernel");
+}

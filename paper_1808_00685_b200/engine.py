@@ -562,27 +562,30 @@ class CorrelationPlan:
 
     def check(self, axes=(None, None), labels=("first", "second")):
         """After the stream synchronised: raise the reference's errors, apply
-        the zero-variance policy; returns host (ref1, ref2, sigma1, sigma2, stats)."""
-        sts = [self.status1.cpu().numpy()]
-        if not self.homo:
-            sts.append(self.status2.cpu().numpy())
-        for st, lab in zip(sts, labels):
-            if int(st[_abi.ST_NONFINITE]):
+        the zero-variance policy; returns host (ref1, ref2, sigma1, sigma2, stats).
+        Every status / stat / reference / sigma word comes back in ONE
+        device -> host transfer."""
+        h = readback({"st1": self.status1, "st2": None if self.homo else self.status2, "stats": self.stats,
+                      "ref1": None if self.ref1 is None else self.ref1[:self.n1],
+                      "ref2": None if self.ref2 is None else self.ref2[:self.n2],
+                      "sig1": None if self.sigma1 is None else self.sigma1[:self.n1],
+                      "sig2": None if self.sigma2 is None else self.sigma2[:self.n2]})
+        for st, lab in ((h["st1"], labels[0]), (h["st2"], labels[1])):
+            if st is not None and int(st[_abi.ST_NONFINITE]):
                 raise NumericError(f"{lab} dynamic-spectra matrix contains non-finite values")
         sig = []
-        for recipe, sdev, axis, n in ((self.recipe1, self.sigma1, axes[0], self.n1),
-                                      (self.recipe2, self.sigma2, axes[1], self.n2)):
-            if recipe is None or sdev is None:
+        for recipe, sh, axis in ((self.recipe1, h["sig1"], axes[0]), (self.recipe2, h["sig2"], axes[1])):
+            if recipe is None or sh is None:
                 sig.append(None)
                 continue
-            sig.append(handle_zero_variance(axis, sdev[:n].cpu().numpy(), recipe.alpha, recipe.substitute))
-        stats = self.stats.cpu().numpy()
+            sig.append(handle_zero_variance(axis, sh, recipe.alpha, recipe.substitute))
+        stats = h["stats"]
         if int(stats[2]):
             raise NumericError("correlation produced non-finite values")
         info = {"max_abs_sync": float(stats[0:1].view(np.float64)[0]),
                 "max_abs_async": float(stats[1:2].view(np.float64)[0])}
-        ref1 = self.ref1[:self.n1].cpu().numpy() if self.ref1 is not None else None
-        ref2 = self.ref2[:self.n2].cpu().numpy() if self.ref2 is not None else ref1
+        ref1 = h["ref1"]
+        ref2 = h["ref2"] if h["ref2"] is not None else ref1
         if self.homo:
             sig.append(None)
             sig[1] = sig[0]
@@ -600,6 +603,29 @@ class CorrelationPlan:
         return hs.numpy(), ha.numpy()
 
 
+def readback(tensors: dict) -> dict:
+    """Small device tensors -> host numpy arrays with ONE device -> host copy
+    (their bytes concatenated on the device), instead of one synchronous
+    transfer each.  None entries stay None."""
+    t = torch()
+    live = [(k, x) for k, x in tensors.items() if x is not None and x.numel()]
+    out = {k: (None if x is None else np.empty(0, dtype=_np_dtype(x))) for k, x in tensors.items()}
+    if not live:
+        return out
+    flat = t.cat([x.contiguous().reshape(-1).view(t.uint8) for _, x in live]).cpu().numpy()
+    o = 0
+    for k, x in live:
+        nb = x.numel() * x.element_size()
+        out[k] = flat[o:o + nb].view(_np_dtype(x)).reshape(tuple(x.shape))
+        o += nb
+    return out
+
+
+def _np_dtype(x):
+    return {"torch.float64": np.float64, "torch.float32": np.float32, "torch.int32": np.int32,
+            "torch.int64": np.int64}[str(x.dtype)]
+
+
 def device_budget(dev) -> int:
     """Bytes of device memory the output planes of one launch may take:
     CORR2D_DEVICE_BUDGET (bytes) if set, else 85 % of the free memory."""
@@ -609,6 +635,30 @@ def device_budget(dev) -> int:
         return int(float(env))
     free, _ = torch().cuda.mem_get_info(dev)
     return int(free * 0.85)
+
+
+_total_mem = {}
+
+
+def planes_fit_easily(n1: int, n2: int, elem: int, dev) -> bool:
+    """True when the two output planes take under 1/8 of the device's total
+    memory: such maps never stream, and the call skips the (synchronising)
+    free-memory query of device_budget."""
+    import os
+    if os.environ.get("CORR2D_DEVICE_BUDGET"):
+        return False
+    key = str(dev)
+    if key not in _total_mem:
+        _total_mem[key] = torch().cuda.get_device_properties(dev).total_memory
+    return 2 * n1 * n2 * elem * 8 <= _total_mem[key]
+
+
+def maybe_stream_blocks(n1: int, n2: int, elem: int, dev):
+    """stream_blocks against the device budget, or None without querying the
+    free memory when the planes fit easily."""
+    if planes_fit_easily(n1, n2, elem, dev):
+        return None
+    return stream_blocks(n1, n2, elem, device_budget(dev))
 
 
 def stream_blocks(n1: int, n2: int, elem: int, budget: int, align: int = 128):

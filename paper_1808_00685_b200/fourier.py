@@ -138,11 +138,21 @@ def correlate_ft(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers
         return sharded.run(plan, meta, axes=(dyn1.spectral_axis, dyn2.spectral_axis))
     if not return_device and rows is None:
         odt = np.dtype(dtype)
-        blocks = engine.stream_blocks(dyn1.n, dyn2.n, odt.itemsize, engine.device_budget(dev))
+        blocks = engine.maybe_stream_blocks(dyn1.n, dyn2.n, odt.itemsize, dev)
+        plan = None
+        if blocks is None:
+            try:
+                plan = make_plan(rows)
+            except NumericError as e:          # the device is fuller than the size check assumed
+                if "out of memory" not in str(e):
+                    raise
+                blocks = engine.stream_blocks(dyn1.n, dyn2.n, odt.itemsize, engine.device_budget(dev))
         if blocks is not None:        # planes larger than device memory: stream row blocks
             s, a, info, _ = engine.run_streamed(make_plan, dyn1.n, dyn2.n, odt, blocks, out)
             return CorrelationSpectra._trusted(sync=s, asyn=a, stats=info, **meta)
-    plan = make_plan(rows)
+    else:
+        plan = None
+    plan = plan or make_plan(rows)
     plan.launch()
     engine.sync()
     *_, info = plan.check()

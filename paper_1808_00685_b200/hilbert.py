@@ -70,7 +70,7 @@ def correlate_ht(dyn1, dyn2=None, norm: NormalizationSpec | None = None, workers
                 is_homo=homo, scaling_exponent=dyn1.scaling_exponent)
     if not return_device and rows is None:
         _, dev = engine.require_device(device)
-        blocks = engine.stream_blocks(dyn1.n, dynb.n, 8, engine.device_budget(dev))
+        blocks = engine.maybe_stream_blocks(dyn1.n, dynb.n, 8, dev)
         if blocks is not None:        # planes larger than device memory: stream row blocks
             s, a, info, _ = engine.run_streamed(lambda rws: _plan(dyn1, d2, norm, rws, device)[0],
                                                 dyn1.n, dynb.n, np.float64, blocks, out)

@@ -102,7 +102,7 @@ def test_streaming_with_budget_from_free_memory():
     from paper_1808_00685_b200 import engine
     n = 6000
     rng = np.random.default_rng(8)
-    v = rng.normal(size=(32, n))
+    v = rng.normal(size=(40, n))                # m > 32: whole map and blocks take the same kernels
     dyn = _dyn(v)
     whole = P.correlate_ft(dyn)
     torch.cuda.empty_cache()
@@ -119,3 +119,90 @@ def test_streaming_with_budget_from_free_memory():
         del filler
         torch.cuda.empty_cache()
     assert np.array_equal(part.sync, whole.sync) and np.array_equal(part.asyn, whole.asyn)
+
+
+def test_corr2d_plan_cache_rebinds_every_input():
+    """corr2d() reuses a cached plan for repeated shapes (host-returning
+    calls): every call must see its own intensities and provided reference."""
+    from paper_1808_00685_b200 import api
+    rng = np.random.default_rng(12)
+    t = np.arange(11.0)
+    outs = []
+    for k in range(3):
+        raw1 = rng.normal(size=(11, 257)) + k
+        raw2 = rng.normal(size=(11, 130)) - k
+        ref = rng.normal(size=257)
+        ds1 = P.SpectralDataset(np.arange(257.0), t, raw1)
+        ds2 = P.SpectralDataset(np.arange(130.0), t, raw2)
+        homo = P.corr2d(ds1)
+        s, a, _ = O.correlate_ft(O.preprocess(t, raw1)[1])
+        assert _err(homo, s, a) <= 1e-10
+        het = P.corr2d(ds1, ds2)
+        s, a, _ = O.correlate_ft(O.preprocess(t, raw1)[1], O.preprocess(t, raw2)[1])
+        assert _err(het, s, a) <= 1e-10
+        prov = P.corr2d(ds1, reference=ref)
+        v = raw1 - ref[None, :]
+        s, a, _ = O.correlate_ft(v)
+        assert _err(prov, s, a) <= 1e-10 and np.array_equal(prov.ref1, ref)
+        outs.append(homo.sync)
+    assert len(api._PLAN_CACHE) <= api.PLAN_CACHE_SIZE
+    assert not np.array_equal(outs[0], outs[1])      # results never alias the cached planes
+
+
+def test_standalone_preprocess_functions_match_reference():
+    """Every standalone preprocessing function against the outputs the
+    reference produced on the same inputs (tests/golden/dropin_functions.npz,
+    make_golden_dropin.py): preprocess.py:123-259."""
+    import json
+    from conftest import GOLDEN, golden
+    g = golden("dropin_functions")
+    msgs = json.loads((GOLDEN / "dropin_messages.json").read_text())
+    ds = P.SpectralDataset(g["nu"], g["t"], g["raw"])
+    for kind, tag in ((P.InterpolantKind.LINEAR, "lin"), (P.InterpolantKind.CUBIC_SPLINE, "spl")):
+        tol = 0 if tag == "lin" else 1e-12               # linear: the reference's own idx / frac arithmetic
+        got = P.resample_to_axis(ds, g["new_axis"], kind)
+        assert np.array_equal(got.perturbation_axis, g["new_axis"])
+        assert np.max(np.abs(got.intensities - g[f"to_axis_{tag}"])) <= tol * np.abs(g["raw"]).max()
+        eq = P.resample_equidistant(ds, 16, kind)
+        assert np.array_equal(eq.perturbation_axis, g[f"equi_axis_{tag}"])
+        assert np.max(np.abs(eq.intensities - g[f"equi_{tag}"])) <= tol * np.abs(g["raw"]).max()
+    assert np.array_equal(P.mean_reference(ds), g["mean_ref"])
+    assert np.array_equal(P.dynamic_spectra(ds).values, g["dyn_values"])
+    prov = P.ReferenceSpec.provided(g["provided_ref"])
+    assert np.array_equal(P.dynamic_spectra(ds, prov).values, g["dyn_values_provided"])
+    assert np.allclose(P.stddev_spectrum(ds), g["sigma_mean"], rtol=1e-14, atol=0)
+    assert np.allclose(P.stddev_spectrum(ds, prov), g["sigma_provided"], rtol=1e-14, atol=0)
+    dyn = P.dynamic_spectra(ds)
+    for alpha in (0.5, 1.0, 0.25):
+        sc = P.apply_scaling(dyn, g["sigma_mean"], alpha)
+        assert sc.scaling_exponent == alpha
+        assert np.allclose(sc.values, g[f"scaled_{alpha}"], rtol=1e-14, atol=0)
+    dsf = P.SpectralDataset(g["nu"], g["t"], g["flat_raw"])
+    dynf = P.dynamic_spectra(dsf)
+    sig = P.stddev_spectrum(dsf)
+    assert sig[7] == 0.0 and np.allclose(sig, g["flat_sigma"], rtol=1e-14, atol=0)
+    with pytest.warns(RuntimeWarning) as w:
+        sub = P.apply_scaling(dynf, sig, 0.5, on_zero_variance="substitute")
+    assert str(w[0].message) == msgs["substitute_warning"]
+    assert np.allclose(sub.values, g["flat_scaled_substitute"], rtol=1e-14, atol=0)
+    with pytest.raises(P.NumericError) as e:
+        P.apply_scaling(dynf, sig, 0.5)
+    assert str(e.value) == msgs["zero_variance_error"]
+    with pytest.raises(P.DataError) as e:
+        P.resample_to_axis(ds, np.linspace(-1.0, 5.0, 4))
+    assert str(e.value) == msgs["target_beyond"][1]
+
+
+def test_corr2d_resample_to_common_matches_reference_cli_pipeline():
+    """corr2d(ds1, ds2, resample_to_common=N) = the reference CLI's common-axis
+    pipeline (cli.py:313-343) on the same inputs."""
+    from conftest import golden
+    g = golden("dropin_functions")
+    ds1 = P.SpectralDataset(g["nu"], g["t"], g["raw"])
+    ds2 = P.SpectralDataset(g["common_nu2"], g["common_t2"], g["common_raw2"])
+    res = P.corr2d(ds1, ds2, resample_to_common=20, interpolant="linear", alpha=0.5)
+    s, a = g["common_sync"], g["common_asyn"]
+    assert _err(res, s, a) <= 1e-10
+    assert res.normalization == float(g["common_norm"]) and not res.is_homo
+    assert np.allclose(res.ref1, g["common_ref1"], rtol=1e-14, atol=0)
+    assert np.allclose(res.ref2, g["common_ref2"], rtol=1e-14, atol=0)
