@@ -386,7 +386,7 @@ def run_b200(args, case, wl, world, rank, local):
                         "contraction_span_events_ms_avg": sum(per_k2) / len(per_k2)}
                 fused = getattr(plan, "small", False)
                 per_step = [total / args.steps] * args.steps
-                if fused:          # the fused kernel is the whole step
+                if fused:          # the small-m path (K1 + contraction kernels) is the whole step
                     per_k2 = list(per_step)
                 clocks_extra.update(diag)
             if os.environ.get("BENCH_DUMP_STEPS"):
@@ -550,7 +550,7 @@ def executed_flops(plan, case, tc_peak, k2_ms):
         products = 3 if fp32_format() == "bf16x3" else 2
         per_tile = products * 2 * 2 * 256 * 256 * hp       # products, x + y MMAs, 2 flops/MAC, depth hp
     elif getattr(plan, "small", False):
-        per_tile = 2 * 2 * 32 * 32 * plan.ld_pack           # fused small-m kernel: 32 x 32 tiles, depth padded to 8
+        per_tile = 2 * 64 * 64 * plan.ld_pack               # small-m path: 64 x 64 blocks, Gauss depth 3 kg
     elif getattr(plan, "gauss", False):
         per_tile = 2 * 64 * 64 * plan.mp                    # 3 kg slots, each feeding ONE plane's accumulator
     else:
@@ -568,7 +568,7 @@ def fp32_format():
 def contract_kernel_name(case, plan=None):
     """The contraction kernel the C ABI dispatches to (bf16_variant() in contract_tc.cu)."""
     if plan is not None and getattr(plan, "small", False):
-        return "small_fused_kernel (K1 + contraction, one launch)"
+        return "small_prep_kernel + small_contract_kernel (one call, PDL-chained)"
     if case.dtype != "float32":
         return "contract_f64_kernel"
     if os.environ.get("CORR2D_BF16_1SM") == "1":

@@ -210,16 +210,20 @@ int corr2d_contract_bf16x3(
 int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int row0, int row1,
                                    int64_t ld_out);
 
-/* ------------------------------- small m: the whole call in one launch ---- */
+/* ----------------------------------- small m: the whole call, one C call ---- */
 /*
  * fp64, 2 <= m <= 32, no resampling (cfg1 / cfg2 shapes): preprocess + DFT +
- * contraction of a whole map in ONE kernel launch (csrc/small.cu).  Replaces
- * the corr2d_prep + corr2d_contract_f64_gauss sequence that preprocess_dataset
- * / dft_channels / correlate_ft (preprocess.py:262-275, fourier.py:61-125) map
- * onto; same argument meanings as those two calls.  Every CTA owns one 64 x 64
- * output block (corr2d_small_block_count blocks: homo the upper triangle,
- * mirrored) and recomputes K1 for the block's channels into shared memory:
- * CTAs never wait for each other (no co-residency requirement).
+ * contraction of a whole map (csrc/small_path.cu).  Replaces the corr2d_prep +
+ * corr2d_contract_f64_gauss sequence that preprocess_dataset / dft_channels /
+ * correlate_ft (preprocess.py:262-275, fourier.py:61-125) map onto; same
+ * argument meanings as those two calls.  Two kernels chained by programmatic
+ * dependent launch: K1 once per channel (one lane per channel, DFT on the
+ * FP64 tensor pipe, Gauss operand rows into ops_a / ops_b), then one CTA per
+ * 64 x 64 output block (corr2d_small_block_count blocks: homo the upper
+ * triangle, mirrored).  No CTA ever waits for another CTA.
+ *   ops_a / ops_b      : device operand scratch, n1 (resp. n2; homo: n1) rows
+ *                       of ld_ops doubles, 16-B aligned, ld_ops even and >=
+ *                       corr2d_small_ops_depth(m)
  *   ref_out* / sigma_out* : as corr2d_prep (either may be NULL)
  *   status1 / status2  : device int32[4] each, the corr2d_prep status words
  *                       (status2 unused when homo); written by the call
@@ -229,14 +233,18 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  *                       arrival counter, left zero by every call (the last CTA
  *                       publishes and resets them).  One work buffer per
  *                       concurrently running call.
+ * The first call for a given m on a device builds a small DFT table (must not
+ * be inside a CUDA graph capture).
  */
 int64_t corr2d_small_block_count(int n1, int n2, int homo);
+int corr2d_small_ops_depth(int m);
 int corr2d_correlate_small_f64(
     int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
     int m, int n1, int n2,
     int ref_mode1, const double* ref_in1, const double* sigma_in1,
     int ref_mode2, const double* ref_in2, const double* sigma_in2,
     double alpha, int substitute_zero_var, double norm_const,
+    double* ops_a, double* ops_b, int64_t ld_ops,
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream);

@@ -30,7 +30,7 @@ EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
     "corr2d_contract_tc", "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
-    "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count",
+    "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count", "corr2d_small_ops_depth",
     "corr2d_correlate_small_f64",
 )
 
@@ -87,16 +87,18 @@ def _declare(lib):
                                        ctypes.c_char, c_int, c_int, c_void, c_i64, c_void]
     lib.corr2d_small_block_count.argtypes = [c_int, c_int, c_int]
     lib.corr2d_small_block_count.restype = c_i64
+    lib.corr2d_small_ops_depth.argtypes = [c_int]
     lib.corr2d_correlate_small_f64.argtypes = [
         c_int, c_void, c_i64, c_void, c_i64,          # in_dtype raw1 ld_raw1 raw2 ld_raw2
         c_int, c_int, c_int,                          # m n1 n2
         c_int, c_void, c_void, c_int, c_void, c_void,  # ref_mode1 ref_in1 sigma_in1, same for dataset 2
         c_double, c_int, c_double,                    # alpha substitute norm
+        c_void, c_void, c_i64,                        # ops_a ops_b ld_ops
         c_void, c_void, c_void, c_void,               # ref_out1 sigma_out1 ref_out2 sigma_out2
         c_void, c_void, c_i64,                        # phi psi ld_out
         c_void, c_void, c_void, c_void, c_void,       # status1 status2 stats work stream
     ]
-    for name in ("corr2d_format_repr", "corr2d_format_rows", "corr2d_correlate_small_f64",
+    for name in ("corr2d_format_repr", "corr2d_format_rows", "corr2d_correlate_small_f64", "corr2d_small_ops_depth",
                  "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
                  "corr2d_contract_tc", "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
                  "corr2d_plane_absmax", "corr2d_find_peaks"):

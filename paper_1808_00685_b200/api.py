@@ -215,9 +215,15 @@ def corr2d(ds1: SpectralDataset, ds2: SpectralDataset | None = None, *, referenc
                 sync=s, asyn=a, axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, ref1=first[0], ref2=first[1],
                 normalization=constant, engine=engine, is_homo=homo,
                 scaling_exponent=float(alpha) if alpha > 0 else 0.0, stats=info)
-    if return_device:
-        plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
-                                dtype=dtype, device=device, engine_name=engine)
+    if not return_device:
+        # planes' D2H queued right behind the kernels; status checks overlap it
+        s, a, (ref1, ref2, _, _, info) = plan.run_to_host(out, axes=(ds1.spectral_axis, dsb.spectral_axis))
+        return CorrelationSpectra._trusted(
+            sync=s, asyn=a, axis1=ds1.spectral_axis, axis2=dsb.spectral_axis, ref1=ref1, ref2=ref2,
+            normalization=plan.constant, engine=engine, is_homo=homo,
+            scaling_exponent=float(alpha) if alpha > 0 else 0.0, stats=info)
+    plan, homo = build_plan(ds1, ds2, spec, norm=norm, on_zero_variance=on_zero_variance,
+                            dtype=dtype, device=device, engine_name=engine)
     plan.launch()
     _engine_mod.sync()
     ref1, ref2, _, _, info = plan.check(axes=(ds1.spectral_axis, dsb.spectral_axis),

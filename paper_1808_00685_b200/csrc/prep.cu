@@ -1264,6 +1264,46 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
   if (p.fast_store && tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+// CORR2D_PACK_F64_TIME of already-dynamic values (the Hilbert route's
+// operands; hilbert.py:92-115) for ANY m -- no FFT, so no shared-memory limit
+// on m (the reference's Toeplitz branch above DENSE_LIMIT = 4096, hilbert.py:
+// 52-61, is the same matrix): a tiled transpose out[c][s] = Norm * v[s][c]
+// (role A) / v[s][c] (role B), zero padded to mp, with the finite count.
+__global__ void __launch_bounds__(256) time_pack_kernel(const PrepParams p) {
+  __shared__ double tile[32][33];
+  const int s0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  int bad = 0;
+  for (int r = ty; r < 32; r += 8) {
+    const int s = s0 + r, c = c0 + tx;
+    double v = 0.0;
+    if (s < p.m && c < p.n) {
+      const long long o = (long long)s * p.ld_raw + c;
+      v = p.in_f32 ? (double)static_cast<const float*>(p.raw)[o] : static_cast<const double*>(p.raw)[o];
+      bad += !isfinite(v);
+    }
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int c = c0 + r, s = s0 + tx;
+    if (c < p.n && s < p.mp) {
+      const double v = tile[tx][r];
+      const long long o = (long long)c * p.ld_pack + s;
+      if (p.pack_roles & CORR2D_ROLE_A) static_cast<double*>(p.a_phi)[o] = p.norm * v;
+      if (p.pack_roles & CORR2D_ROLE_B) static_cast<double*>(p.b)[o] = v;
+    }
+  }
+  bad = warp_sum(bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&p.status[CORR2D_ST_NONFINITE], bad);
+}
+
+static bool time_pack_eligible(const PrepParams& p) {
+  return p.pack_kind == CORR2D_PACK_F64_TIME && p.resample_kind == CORR2D_RESAMPLE_NONE &&
+         p.ref_mode == CORR2D_REF_NONE && p.alpha == 0.0 && !p.values_out && !p.half_out && !p.ref_out &&
+         !p.sigma_out && p.m == p.m_in;
+}
+
 static bool fast_eligible(const PrepParams& p) {
   if (const char* e = getenv("CORR2D_PREP_FAST"))
     if (e[0] == '0') return false;
@@ -1523,6 +1563,13 @@ extern "C" int corr2d_prep(
     return check_launch("prep_fast_kernel");
   }
 
+  if (time_pack_eligible(p)) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(status, 0, 4 * sizeof(int32_t), st) != cudaSuccess) return check_launch("status reset");
+    const dim3 grid((n + 31) / 32, (p.mp + 31) / 32);
+    time_pack_kernel<<<grid, 256, 0, st>>>(p);
+    return check_launch("time_pack_kernel");
+  }
   const bool resample = resample_kind != CORR2D_RESAMPLE_NONE;
   int C = 64;
   const int in_bytes = (in_dtype == CORR2D_F32) ? 4 : 8;

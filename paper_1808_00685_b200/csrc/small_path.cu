@@ -1,25 +1,25 @@
-// The whole small-m correlation in ONE launch (corr2d_correlate_small_f64):
-// fp64, 2 <= m <= 32, no resampling -- the cfg1 (m = 11) and cfg2 (m = 21)
-// shapes, where the step is bound by launch latency, one DRAM round trip and
-// the output write (cfg1: 16 MB of planes, 2.5 us at HBM peak).
+// The whole small-m correlation (corr2d_correlate_small_f64): fp64,
+// 2 <= m <= 32, no resampling -- the cfg1 (m = 11) and cfg2 (m = 21) shapes,
+// where a step is bound by launch latency, one DRAM round trip and the output
+// write (cfg1: 16 MB of planes, 2.5 us at HBM peak).  Two kernels, chained by
+// programmatic dependent launch (the second grid launches while the first
+// runs and waits at griddepcontrol.wait for its completion -- a kernel
+// boundary, never a wait of one CTA on another):
 //
-// small_block_kernel: every CTA owns one 64 x 64 output block and never waits
-// for another CTA (no ready flags, no grid barrier, no co-residency
-// assumption):
-//   1. K1 for the block's 128 channels (64 row + 64 column channels; 64 on
-//      homo diagonal blocks), one lane per channel: the reference's statistics
-//      in its order (sequential sums: bitwise-equal reference / sigma / values),
-//   2. the real DFT of the block's channels as an FP64 tensor-core product
-//      Y[bins x channels] = W[bins x t] . y[t x channels] (W: cos / -sin rows
-//      from a per-m host table), each warp transforming its own 32 lanes'
-//      channels,
-//   3. the CORR2D_PACK_F64_GAUSS slots (three real products per bin) into
-//      shared memory, then the 64 x 64 contraction on the FP64 tensor pipe,
-//   4. both planes staged in shared memory and written as coalesced rows --
-//      plus the mirror (sync^T, -async^T) of homo blocks above the diagonal,
-//      diagonal blocks symmetrised -- with the max|.| / finite reduction fused.
-// Status / stat words are self-resetting: the last CTA to finish (an arrival
-// counter, never a wait) publishes and re-zeroes them.
+// small_prep_kernel   -- K1 once per channel, one lane per channel: the
+//   reference's statistics in its order (sequential sums: bitwise-equal
+//   reference / sigma / values), the real DFT of each warp's 32 channels as an
+//   FP64 tensor-core product Y[bins x channels] = W[bins x t] . y[t x channels]
+//   (W: cos / -sin rows from a per-m host table), then the
+//   CORR2D_PACK_F64_GAUSS operand rows (three real products per bin).
+// small_contract_kernel -- one CTA per 64 x 64 output block (homo: the upper
+//   triangle, mirrored): operand rows from L2 into shared memory, the Gauss
+//   contraction on the FP64 tensor pipe with two independent accumulator
+//   chains, both planes staged in shared memory and written as coalesced rows
+//   plus the mirror (sync^T, -async^T), diagonal blocks symmetrised, with the
+//   max|.| / finite reduction fused.  Status / stat words are self-resetting:
+//   the last CTA to finish (an arrival counter, never a wait) publishes and
+//   re-zeroes them.
 //
 // Reference path: preprocess.py:123-137, :198-259 (reference, sigma, scaling),
 // fourier.py:61-82 (rfft along the perturbation axis), fourier.py:107-123
@@ -27,6 +27,7 @@
 // engine_core.py:139-140 (finite check), dataset.py:159-170 (homo symmetry).
 #include "prep_params.cuh"
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <mutex>
@@ -63,6 +64,10 @@ struct SmallParams {
   int yrows;                // rows of the sample / spectrum region: max(mpad, 2 (m / 2 + 1))
   int kg, ks;               // Gauss slots per segment; operand row stride (doubles, = 4 mod 16)
   int T1, T2;               // 64-blocks along rows / columns
+  int nb1;                  // 128-channel K1 blocks of dataset 1 (dataset 2's follow)
+  double* opsA;             // Gauss operand rows, role A (row operand), n1 x ld_ops
+  double* opsB;             // role B (column operand), n2 x ld_ops (homo: n1)
+  long long ld_ops;
   double* phi;
   double* psi;
   long long ld_out;
@@ -71,6 +76,7 @@ struct SmallParams {
   int* status2;
   unsigned long long* stats;
   int* work;                // kW* words, zero-filled once by the caller
+  unsigned long long* trace;  // profiling builds: per-CTA globaltimer stamps (NULL otherwise)
 };
 
 // work-buffer words (int32 indices); every launch leaves them zero
@@ -78,6 +84,24 @@ constexpr int kWStatus1 = 0;   // [0, 4)  K1 status accumulator, dataset 1
 constexpr int kWStatus2 = 4;   // [4, 8)  dataset 2
 constexpr int kWDone = 8;      // CTAs finished (the last one publishes and resets)
 constexpr int kWStats = 10;    // [10, 16) max|sync|, max|async|, non-finite count (3 x uint64)
+
+// profiling builds (-DCORR2D_PROFILING, CORR2D_SMALL_TRACE=1): thread 0 of
+// every CTA records %globaltimer at phase boundaries (K1 CTAs at slots
+// [8 b, 8 b + 8), contraction CTAs at [8 (kTraceK1 + b), ...)); release
+// builds compile the stamps away
+constexpr int kTraceK1 = 1024;
+#ifdef CORR2D_PROFILING
+#define SMALL_STAMP(base, k)                                                                   \
+  do {                                                                                         \
+    if (p.trace && threadIdx.x == 0) {                                                         \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      p.trace[8 * ((base) + blockIdx.x) + (k)] = t_;                                           \
+    }                                                                                          \
+  } while (0)
+#else
+#define SMALL_STAMP(base, k) do { } while (0)
+#endif
 
 __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, double b0) {
   asm volatile(
@@ -189,6 +213,7 @@ __device__ __forceinline__ void put_bin(int w, int m, int kg, double norm, doubl
 // One Gauss segment of the depth (kg slots) into one accumulator set.
 __device__ __forceinline__ void small_mma_seg(double (&acc)[2][4][4], const double* As, const double* Bs, int ks,
                                               int k0, int kg, int wm, int wn, int lr, int lk) {
+#pragma unroll 1
   for (int kk = 0; kk < kg; kk += 4) {
     double ap[2][2], bf[4];
 #pragma unroll
@@ -206,36 +231,65 @@ __device__ __forceinline__ void small_mma_seg(double (&acc)[2][4][4], const doub
   }
 }
 
-__global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_constant__ SmallParams p) {
+// Two Gauss segments into two accumulator sets, interleaved per k-step: 16
+// independent DMMAs per warp and k-step.
+__device__ __forceinline__ void small_mma_seg2(double (&acc0)[2][4][4], double (&acc1)[2][4][4], const double* As,
+                                               const double* Bs, int ks, int k0, int k1, int kg, int wm, int wn,
+                                               int lr, int lk) {
+#pragma unroll 1
+  for (int kk = 0; kk < kg; kk += 4) {
+    double a0[2][2], a1[2][2], b0[4], b1[4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r = wm * 32 + mt * 16 + lr;
+      a0[mt][0] = As[r * ks + k0 + kk + lk];
+      a0[mt][1] = As[(r + 8) * ks + k0 + kk + lk];
+      a1[mt][0] = As[r * ks + k1 + kk + lk];
+      a1[mt][1] = As[(r + 8) * ks + k1 + kk + lk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      b0[nt] = Bs[(wn * 32 + nt * 8 + lr) * ks + k0 + kk + lk];
+      b1[nt] = Bs[(wn * 32 + nt * 8 + lr) * ks + k1 + kk + lk];
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        dmma(acc0[mt][nt], a0[mt][0], a0[mt][1], b0[nt]);
+        dmma(acc1[mt][nt], a1[mt][0], a1[mt][1], b1[nt]);
+      }
+  }
+}
+
+// ---- K1: one lane per channel, 128 channels per CTA, each channel once ----
+__global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_constant__ SmallParams p) {
   extern __shared__ __align__(16) double sm[];
-  const int m = p.m, ks = p.ks, kg = p.kg, mpad = p.mpad;
-  double* ys = sm;                                   // [mpad][kYS]
-  double* As = ys + (size_t)p.yrows * kYS;          // [64][ks]
-  double* Bs = As + (size_t)kSB * ks;                // [64][ks]
+  const int m = p.m, mpad = p.mpad;
+  double* ys = sm;                                   // [yrows][kYS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lk = lane & 3;
-
-  int I, J;
-  small_decode(p, blockIdx.x, I, J);
-  const bool diag = p.homo && I == J;
-  // operand rows start at zero (pad slots stay zero)
-  for (int i = tid; i < kSB * ks; i += kSThreads) {
-    reinterpret_cast<double2*>(As)[i] = make_double2(0.0, 0.0);   // As and Bs: 2 * 64 * ks doubles
-  }
-  // programmatic dependent launch: everything above overlapped the previous
-  // kernel's tail; from here on memory written by it is visible
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-
-  // ---- 1. samples and statistics: lanes 0..63 the row channels (role A; on
-  //      homo diagonal blocks also role B), lanes 64..127 the column channels
-  //      (role B; idle on diagonal blocks) ----
-  const bool col_warp = warp >= 2;
-  const int set = (col_warp && !p.homo) ? 1 : 0;
-  const int c = col_warp ? J * kSB + tid - kSB : I * kSB + tid;
-  const int n = set ? p.n2 : (col_warp ? p.n2 : p.n1);
-  const bool active = !(diag && col_warp);
+  const int set = (int)blockIdx.x >= p.nb1 ? 1 : 0;
+  const int c = ((int)blockIdx.x - (set ? p.nb1 : 0)) * kSThreads + tid;
+  const int n = set ? p.n2 : p.n1;
   const bool valid = c < n;
-  if (active) {
+  // the contraction grid may launch now: it waits for this grid's completion
+  // (griddepcontrol.wait) before it reads the operand rows
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  SMALL_STAMP(0, 0);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // inputs written by earlier kernels are visible
+  SMALL_STAMP(0, 1);
+  // the DFT rows and the slot table into shared memory, in flight together
+  // with the samples (one DRAM round trip; the loops below then never touch
+  // global memory for them)
+  double* tab = ys + (size_t)p.yrows * kYS;
+  {
+    const int ntab = 48 * mpad + 5 * 3 * p.kg;       // even: 16-byte pieces
+    for (int i = tid; 2 * i < ntab; i += kSThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
+                   ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(tab + 2 * i))), "l"(p.W + 2 * i) : "memory");
+  }
+  {
     const void* raw = set ? p.raw2 : p.raw1;
     const long long ld = set ? p.ld2 : p.ld1;
     const int cc = valid ? c : n - 1;
@@ -253,68 +307,129 @@ __global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_
     if (p.in_f32)
       for (int t = 0; t < m; ++t) ys[t * kYS + tid] = (double)reinterpret_cast<const float*>(ys + t * kYS + tid)[0];
     for (int t = m; t < mpad; ++t) ys[t * kYS + tid] = 0.0;
-    // the channel's statistics / status are reported by one block only: the
-    // diagonal block (homo), column block 0 (dataset 1) or row block 0 (dataset 2)
-    const bool owner = p.homo ? diag : (col_warp ? I == 0 : J == 0);
-    lane_stats(p, set, c, valid, owner, ys + tid);
+    SMALL_STAMP(0, 2);
+    lane_stats(p, set, c, valid, true, ys + tid);
   }
-  __syncthreads();                                   // zeroed operand rows before the slot writes
-
-  // ---- 2. DFT of this warp's 32 channels on the FP64 tensor pipe:
-  //      Y[16 bins x 8 channels] tiles = W rows . y, k over t ----
-  if (active) {
-    const int nt3 = m / 2 >= 16 ? 3 : 2;             // bins 16.. only for m = 32
-    double acc[3][4][4];
+  __syncthreads();                                   // every thread's table pieces have landed
+  SMALL_STAMP(0, 3);
+  // DFT of this warp's 32 channels on the FP64 tensor pipe: Y[16 bins x 8
+  // channels] tiles = W rows . y, k over t
+  const int nt3 = m / 2 >= 16 ? 3 : 2;               // bins 16.. only for m = 32
+  double acc[3][4][4];
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
+  for (int a = 0; a < 3; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < 4; ++b)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[a][b][q] = 0.0;
-    const double* yw = ys + warp * 32;
-    for (int kk = 0; kk < mpad; kk += 4) {
-      double bf[4];
+      for (int q = 0; q < 4; ++q) acc[a][b][q] = 0.0;
+  double* yw = ys + warp * 32;
+  for (int kk = 0; kk < mpad; kk += 4) {
+    double bf[4];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) bf[nt] = yw[(kk + lk) * kYS + nt * 8 + lr];
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = yw[(kk + lk) * kYS + nt * 8 + lr];
 #pragma unroll
-      for (int tl = 0; tl < 3; ++tl) {
-        if (tl == 2 && nt3 < 3) break;
-        const double a0 = __ldg(p.W + (tl * 16 + lr) * mpad + kk + lk);
-        const double a1 = __ldg(p.W + (tl * 16 + lr + 8) * mpad + kk + lk);
+    for (int tl = 0; tl < 3; ++tl) {
+      if (tl == 2 && nt3 < 3) break;
+      const double a0 = tab[(tl * 16 + lr) * mpad + kk + lk];
+      const double a1 = tab[(tl * 16 + lr + 8) * mpad + kk + lk];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) dmma(acc[tl][nt], a0, a1, bf[nt]);
-      }
+      for (int nt = 0; nt < 4; ++nt) dmma(acc[tl][nt], a0, a1, bf[nt]);
     }
-    // ---- 3. the spectra back into the warp's own sample columns (bin w: Re in
-    //      row 2 w, Im in row 2 w + 1), then each lane turns its channel's bins
-    //      into the Gauss operand slots ----
-    __syncwarp();                                    // the warp's DMMAs have read its columns
-    double* yl = ys + warp * 32;
+  }
+  SMALL_STAMP(0, 4);
+  // the spectra back into the warp's own sample columns (bin w: Re in row 2 w,
+  // Im in row 2 w + 1), then each lane writes its channel's operand row(s)
+  __syncwarp();                                      // the warp's DMMAs have read its columns
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+  for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int col = nt * 8 + 2 * lk + e, w = lr + 8 * h;
-          if (w > m / 2) continue;                       // rows past 2 H + 1 belong to the operand rows
-          yl[(2 * w) * kYS + col] = acc[0][nt][2 * h + e];
-          yl[(2 * w + 1) * kYS + col] = acc[1][nt][2 * h + e];
-          if (nt3 == 3 && h == 0 && lr == 0) {
-            yl[32 * kYS + col] = acc[2][nt][e];          // bin 16 (m = 32: Nyquist, real)
-            yl[33 * kYS + col] = 0.0;
-          }
+      for (int e = 0; e < 2; ++e) {
+        const int col = nt * 8 + 2 * lk + e, w = lr + 8 * h;
+        if (w > m / 2) continue;                       // rows past 2 H + 1 are not part of the region
+        yw[(2 * w) * kYS + col] = acc[0][nt][2 * h + e];
+        yw[(2 * w + 1) * kYS + col] = acc[1][nt][2 * h + e];
+        if (nt3 == 3 && h == 0 && lr == 0) {
+          yw[32 * kYS + col] = acc[2][nt][e];          // bin 16 (m = 32: Nyquist, real)
+          yw[33 * kYS + col] = 0.0;
         }
-    __syncwarp();
-    const int rowc = col_warp ? tid - kSB : tid;
-    double* rowA = col_warp ? nullptr : As + (size_t)rowc * ks;
-    double* rowB = (col_warp || diag) ? Bs + (size_t)rowc * ks : nullptr;
-    for (int w = 0; w <= m / 2; ++w)
-      put_bin(w, m, kg, p.norm, ys[(2 * w) * kYS + tid], ys[(2 * w + 1) * kYS + tid], rowA, rowB);
+      }
+  __syncwarp();
+  if (!valid) return;
+  double* rowA = set ? nullptr : p.opsA + (long long)c * p.ld_ops;
+  double* rowB = (set || p.homo) ? p.opsB + (long long)c * p.ld_ops : nullptr;
+  // every slot once (pads are 0), from the per-slot table after W: bin w and
+  // small exact coefficients -- A = Norm (pa R + qa I), B = pb R + qb I
+  // (gauss_values' operands: a + b, a, -b | a at Nyquist; c, d - c, c + d)
+  const double* slot = tab + 48 * mpad;              // per slot: w (or -1), pa, qa, pb, qb
+  const int ns = 3 * p.kg;
+  for (int s = 0; s < ns; ++s, slot += 5) {
+    const int w = (int)slot[0];
+    double va = 0.0, vb = 0.0;
+    if (w >= 0) {
+      const double R = ys[(2 * w) * kYS + tid], I = ys[(2 * w + 1) * kYS + tid];
+      va = p.norm * fma(slot[1], R, slot[2] * I);
+      vb = fma(slot[3], R, slot[4] * I);
+    }
+    if (rowA) rowA[s] = va;
+    if (rowB) rowB[s] = vb;
+  }
+  SMALL_STAMP(0, 5);
+}
+
+// ---- contraction: one CTA per 64 x 64 output block ----
+__global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __grid_constant__ SmallParams p) {
+  extern __shared__ __align__(16) double sm[];
+  const int ks = p.ks, kg = p.kg;
+  double* As = sm;                                   // [64][ks]
+  double* Bs = As + (size_t)kSB * ks;                // [64][ks]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  int I, J;
+  small_decode(p, blockIdx.x, I, J);
+  const bool diag = p.homo && I == J;
+  __shared__ __align__(8) unsigned long long bar;
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+  const int rows_a = min(kSB, p.n1 - I * kSB), rows_b = min(kSB, p.n2 - J * kSB);
+  const unsigned row_bytes = 3u * kg * 8u;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-
-  // ---- 4. contraction (Gauss): P1 -> sync, copy to async; -P3 -> sync, P2 -> async ----
+  SMALL_STAMP(kTraceK1, 0);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // K1 complete, its operand rows visible
+  SMALL_STAMP(kTraceK1, 1);
+  // one bulk copy per operand row (thread t: A row t or B row t - 64), all
+  // completing on one mbarrier; rows past the map are zero-filled
+  if (tid == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 ::"r"(bar_s), "r"((unsigned)(rows_a + rows_b) * row_bytes) : "memory");
+  __syncthreads();                                   // expect_tx before any complete_tx
+  {
+    const bool is_b = tid >= kSB;
+    const int r = is_b ? tid - kSB : tid;
+    double* dst = (is_b ? Bs : As) + r * ks;
+    if (r < (is_b ? rows_b : rows_a)) {
+      const double* src = (is_b ? p.opsB : p.opsA) + (long long)((is_b ? J : I) * kSB + r) * p.ld_ops;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))), "l"(src), "r"(row_bytes), "r"(bar_s)
+                   : "memory");
+    } else {
+      for (int s = 0; s < 3 * kg; ++s) dst[s] = 0.0;
+    }
+  }
+  {
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}\n"
+                   : "=r"(done) : "r"(bar_s) : "memory");
+  }
+  __syncthreads();                                   // zero-filled rows visible
+  SMALL_STAMP(kTraceK1, 2);
+  // Gauss: P1 (segment 0) and -P3 (segment 2) as two independent chains, then
+  // sync = P1 - P3 and async = P1 + P2 (segment 1)
   const int wm = warp >> 1, wn = warp & 1;
   double aphi[2][4][4], apsi[2][4][4];
 #pragma unroll
@@ -322,17 +437,17 @@ __global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) aphi[a][b][q] = 0.0;
-  small_mma_seg(aphi, As, Bs, ks, 0, kg, wm, wn, lr, lk);
+      for (int q = 0; q < 4; ++q) aphi[a][b][q] = apsi[a][b][q] = 0.0;
+  small_mma_seg2(apsi, aphi, As, Bs, ks, 0, 2 * kg, kg, wm, wn, lr, lk);
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) apsi[a][b][q] = aphi[a][b][q];
-  small_mma_seg(aphi, As, Bs, ks, 2 * kg, kg, wm, wn, lr, lk);
+      for (int q = 0; q < 4; ++q) aphi[a][b][q] += apsi[a][b][q];
   small_mma_seg(apsi, As, Bs, ks, kg, kg, wm, wn, lr, lk);
   __syncthreads();                                   // operands consumed: the staging overlays them
+  SMALL_STAMP(kTraceK1, 3);
 
   // ---- 5. stage both planes, then coalesced row stores (+ mirror) ----
   double* Cphi = sm;                                 // [64][kCS]
@@ -353,6 +468,37 @@ __global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_
   unsigned long long mphi = 0, mpsi = 0;
   const int i0 = I * kSB, j0 = J * kSB;
   const bool rows_full = i0 + kSB <= p.n1, cols_full = j0 + kSB <= p.n2;
+  if (!diag && rows_full && cols_full && p.vec) {
+    // whole off-diagonal block: a thread owns one column pair of rows
+    // r0, r0 + 4, ... (and of the mirror block) -- pointer steps only
+    const int cp = (tid & 31) * 2, r0 = tid >> 5;
+    const long long step = 4 * p.ld_out;
+    const double* cph = Cphi + r0 * kCS + cp;
+    const double* cps = Cpsi + r0 * kCS + cp;
+    double* dph = p.phi + (long long)(i0 + r0) * p.ld_out + j0 + cp;
+    double* dps = p.psi + (dph - p.phi);
+#pragma unroll 4
+    for (int k = 0; k < kSB / 4; ++k) {
+      const double f0 = cph[0], f1 = cph[1], s0 = cps[0], s1 = cps[1];
+      mphi = max(mphi, max(abs_bits(f0), abs_bits(f1)));
+      mpsi = max(mpsi, max(abs_bits(s0), abs_bits(s1)));
+      __stcs(reinterpret_cast<double2*>(dph), make_double2(f0, f1));
+      __stcs(reinterpret_cast<double2*>(dps), make_double2(s0, s1));
+      cph += 4 * kCS; cps += 4 * kCS; dph += step; dps += step;
+    }
+    if (p.homo) {     // mirror rows j0 + r (C column r), columns i0 + cp, +1 (C rows)
+      const double* mph = Cphi + cp * kCS + r0;
+      const double* mps = Cpsi + cp * kCS + r0;
+      double* eph = p.phi + (long long)(j0 + r0) * p.ld_out + i0 + cp;
+      double* eps = p.psi + (eph - p.phi);
+#pragma unroll 4
+      for (int k = 0; k < kSB / 4; ++k) {
+        __stcs(reinterpret_cast<double2*>(eph), make_double2(mph[0], mph[kCS]));
+        __stcs(reinterpret_cast<double2*>(eps), make_double2(neg_bits(mps[0]), neg_bits(mps[kCS])));
+        mph += 4; mps += 4; eph += step; eps += step;
+      }
+    }
+  } else {
   // direct block: rows i0.., a thread stores column pairs (32 pairs per row)
   for (int idx = tid; idx < kSB * (kSB / 2); idx += kSThreads) {
     const int r = idx >> 5, cp = (idx & 31) * 2;
@@ -407,6 +553,8 @@ __global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_
       }
     }
   }
+  }  // general blocks
+  SMALL_STAMP(kTraceK1, 4);
   // ---- max|.| and the finite check (integer pipe), one set of atomics per CTA ----
   constexpr unsigned long long kInf = 0x7ff0000000000000ull;
   int bad = (mphi >= kInf) + (mpsi >= kInf);
@@ -456,6 +604,7 @@ __global__ void __launch_bounds__(kSThreads, 3) small_block_kernel(const __grid_
       __threadfence();
     }
   }
+  SMALL_STAMP(kTraceK1, 5);
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
@@ -487,17 +636,38 @@ static const double* dft_table(int m, int mpad, cudaStream_t st, int* rc) {
                "corr2d_correlate_small_f64: the first call for this m on this device must not be graph-captured");
     return nullptr;
   }
-  std::vector<double> h((size_t)48 * mpad, 0.0);
+  const int kg = gauss_kg(m), ns = 3 * kg;
+  std::vector<double> h((size_t)48 * mpad + 5 * (size_t)ns, 0.0);
   const double two_pi = 6.283185307179586476925286766559;
   for (int k = 0; k < 3; ++k)
     for (int r = 0; r < 16; ++r) {
       const int w = (k == 2 ? 16 : 0) + r;
       if (w > m / 2) continue;
       for (int t = 0; t < m; ++t) {
-        const double ang = two_pi * (double)((w * t) % m) / (double)m;
-        h[(size_t)(16 * k + r) * mpad + t] = k == 1 ? -std::sin(ang) : std::cos(ang);
+        const int q = (w * t) % m;
+        const double ang = two_pi * (double)q / (double)m;
+        // exact zeros of sin at 0 and pi (DC / Nyquist rows are real)
+        const double sn = (q == 0 || 2 * q == m) ? 0.0 : std::sin(ang);
+        h[(size_t)(16 * k + r) * mpad + t] = k == 1 ? -sn : std::cos(ang);
       }
     }
+  // per-slot table of the CORR2D_PACK_F64_GAUSS rows (corr2d.h; gauss_values):
+  // bin w, then A = Norm (pa R + qa I) and B = pb R + qb I, with a = k R,
+  // b = k I (k = 2, or 1 at DC / Nyquist where I = 0), c = R, d = -I
+  double* slot = h.data() + (size_t)48 * mpad;
+  for (int s = 0; s < ns; ++s, slot += 5) {
+    const int seg = s / kg, j = s - seg * kg, w = gauss_bin(seg, j, m);
+    slot[0] = w;
+    if (w < 0) continue;
+    const bool edge = w == 0 || (m % 2 == 0 && w == m / 2);
+    const double kk = edge ? 1.0 : 2.0, ki = edge ? 0.0 : 1.0;
+    double pa, qa, pb, qb;
+    if (seg == 0) { pa = kk; qa = kk * ki; pb = 1.0; qb = 0.0; }          // a + b, c
+    else if (seg == 1) { pa = kk; qa = 0.0; pb = -1.0; qb = -ki; }        // a, d - c
+    else if (edge) { pa = kk; qa = 0.0; pb = 1.0; qb = 0.0; }             // Nyquist: a, c
+    else { pa = 0.0; qa = -kk; pb = 1.0; qb = -1.0; }                     // -b, c + d
+    slot[1] = pa; slot[2] = qa; slot[3] = pb; slot[4] = qb;
+  }
   double* d = nullptr;
   if (cudaMalloc(&d, h.size() * sizeof(double)) != cudaSuccess ||
       cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
@@ -517,17 +687,20 @@ extern "C" int64_t corr2d_small_block_count(int n1, int n2, int homo) {
   return small_blocks(n1, n2, homo);
 }
 
+extern "C" int corr2d_small_ops_depth(int m) { return (m >= 2 && m <= kSMaxM) ? 3 * gauss_kg(m) : -1; }
+
 extern "C" int corr2d_correlate_small_f64(
     int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
     int m, int n1, int n2,
     int ref_mode1, const double* ref_in1, const double* sigma_in1,
     int ref_mode2, const double* ref_in2, const double* sigma_in2,
     double alpha, int substitute_zero_var, double norm_const,
+    double* ops_a, double* ops_b, int64_t ld_ops,
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream) {
   const bool homo = raw2 == nullptr;
-  if (!raw1 || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
+  if (!raw1 || !ops_a || !ops_b || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
   if (in_dtype != CORR2D_F64 && in_dtype != CORR2D_F32) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad dtype");
   if (m < 2 || m > kSMaxM) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: needs 2 <= m <= 32");
@@ -535,6 +708,10 @@ extern "C" int corr2d_correlate_small_f64(
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: homo needs n1 == n2");
   if (ld_raw1 < n1 || (!homo && ld_raw2 < n2)) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_raw < n");
   if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_out < n2");
+  if (ld_ops < corr2d_small_ops_depth(m) || ld_ops % 2 ||
+      ((reinterpret_cast<uintptr_t>(ops_a) | reinterpret_cast<uintptr_t>(ops_b)) & 15))
+    return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: operand rows must be 16-B aligned with "
+                                 "ld_ops even and >= corr2d_small_ops_depth(m)");
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(CORR2D_ERR_DATA, "scaling exponent must lie in [0, 1]");
   for (int r : {ref_mode1, ref_mode2})
     if (r < CORR2D_REF_MEAN || r > CORR2D_REF_NONE) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad ref_mode");
@@ -557,34 +734,77 @@ extern "C" int corr2d_correlate_small_f64(
   p.kg = gauss_kg(m);
   p.ks = (3 * p.kg + 11) / 16 * 16 + 4;
   p.T1 = (n1 + kSB - 1) / kSB; p.T2 = (n2 + kSB - 1) / kSB;
+  p.nb1 = (n1 + kSThreads - 1) / kSThreads;
+  p.opsA = ops_a; p.opsB = ops_b; p.ld_ops = ld_ops;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out;
   p.vec = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
   p.status1 = status1; p.status2 = homo ? nullptr : status2; p.stats = stats; p.work = work;
+#ifdef CORR2D_PROFILING
+  if (const char* e = getenv("CORR2D_SMALL_TRACE"))
+    if (e[0] == '1') {
+      static unsigned long long* tbuf = nullptr;
+      const size_t words = 8 * (size_t)(kTraceK1 + 65536);
+      if (!tbuf) cudaMalloc(&tbuf, words * 8);
+      cudaMemsetAsync(tbuf, 0, words * 8, st);
+      p.trace = tbuf;
+    }
+#endif
   const long long blocks = small_blocks(n1, n2, homo);
   if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
-  const size_t ops = ((size_t)p.yrows * kYS + 2 * (size_t)kSB * p.ks) * sizeof(double);
+  const int prep_blocks = p.nb1 + (homo ? 0 : (n2 + kSThreads - 1) / kSThreads);
+  const size_t prep_smem = ((size_t)p.yrows * kYS + 48 * (size_t)p.mpad + 15 * (size_t)p.kg) * sizeof(double);
+  const size_t ops = 2 * (size_t)kSB * p.ks * sizeof(double);
   const size_t stage = 2 * (size_t)kSB * kCS * sizeof(double);
   const size_t smem = ops > stage ? ops : stage;
   static bool attr_set = false;
   if (!attr_set) {
-    const size_t worst = ((size_t)(kSMaxM + 2) * kYS + 2 * (size_t)kSB * 52) * sizeof(double);
-    cudaFuncSetAttribute(small_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(worst > stage ? worst : stage));
+    const size_t worst_ops = 2 * (size_t)kSB * 52 * sizeof(double);
+    cudaFuncSetAttribute(small_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(worst_ops > stage ? worst_ops : stage));
+    cudaFuncSetAttribute(small_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16) * sizeof(double)));
     attr_set = true;
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(kSThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
+  // programmatic dependent launch for both grids: each launches while its
+  // predecessor drains and orders memory with griddepcontrol.wait -- a kernel
+  // boundary, so no grid needs co-residency
   cudaLaunchAttribute attr[1];
-  // programmatic dependent launch: this grid's launch and prologue overlap the
-  // previous kernel's tail (griddepcontrol.wait orders memory).  No CTA waits
-  // for another, so the grid needs no co-residency.
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kSThreads);
+  cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, small_block_kernel, p);
-  return check_launch("small_block_kernel");
+  cfg.gridDim = dim3((unsigned)prep_blocks);
+  cfg.dynamicSmemBytes = prep_smem;
+  cudaLaunchKernelEx(&cfg, small_prep_kernel, p);
+  if (int e = check_launch("small_prep_kernel")) return e;
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchKernelEx(&cfg, small_contract_kernel, p);
+  int code = check_launch("small_contract_kernel");
+#ifdef CORR2D_PROFILING
+  if (p.trace) {       // per-phase timeline (ns after the first K1 stamp): min / median / max over CTAs
+    std::vector<unsigned long long> h(8 * (size_t)(kTraceK1 + blocks));
+    cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < prep_blocks; ++b) t0 = std::min(t0, h[8 * b]);
+    auto row = [&](const char* name, int base, int nb, int k) {
+      std::vector<double> v;
+      for (int b = 0; b < nb; ++b)
+        if (h[8 * (base + b) + k]) v.push_back((double)(h[8 * (base + b) + k] - t0));
+      if (v.empty()) return;
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "  %-22s min %8.0f  med %8.0f  max %8.0f ns\n", name, v.front(), v[v.size() / 2], v.back());
+    };
+    fprintf(stderr, "small path trace (m %d, %d x %d, %s):\n", m, n1, n2, homo ? "homo" : "hetero");
+    const char* k1n[6] = {"K1 start", "K1 after wait", "K1 samples in", "K1 stats done", "K1 dft done", "K1 rows written"};
+    const char* k2n[6] = {"K2 start", "K2 after wait", "K2 operands in", "K2 mma done", "K2 stores issued", "K2 end"};
+    for (int k = 0; k < 6; ++k) row(k1n[k], 0, prep_blocks, k);
+    for (int k = 0; k < 6; ++k) row(k2n[k], kTraceK1, (int)blocks, k);
+  }
+#endif
+  return code;
 }

@@ -391,7 +391,11 @@ class CorrelationPlan:
         dev = self.dev
         R1, R2 = self._rows(self.n1), self._rows(self.n2)
         alloc = t.zeros if self.shard else t.empty
-        O1, O2 = (0, 0) if self.small else (R1, R2)   # small: operands live in the fused kernel's smem
+        if self.small:
+            # the small path's own Gauss operand rows (K1 -> contraction, L2-resident)
+            self.ld_pack = self.lib.corr2d_small_ops_depth(self.m)
+            self.mp = self.ld_pack
+        O1, O2 = (R1, R2)
         self.a_phi = alloc((O1, self.ld_pack), dtype=pdt, device=dev)
         # bf16: one format for both roles (a_psi unused, homo B == A)
         self.a_psi = None if (bf16 or self.gauss) else alloc((O1, self.ld_pack), dtype=pdt, device=dev)
@@ -458,10 +462,10 @@ class CorrelationPlan:
 
     @property
     def launches_per_step(self) -> int:
-        """Kernels of ours one launch() enqueues: K1 per dataset + K2 (one fused
-        kernel on the small-m path)."""
+        """Kernels of ours one launch() enqueues: K1 per dataset + K2 (the
+        small-m path: its K1 and contraction kernels)."""
         if self.small:
-            return 1
+            return 2
         return (1 if self.homo else 2) + (2 if self.route == "hilbert" else 1)
 
     def launch(self):
@@ -555,6 +559,7 @@ class CorrelationPlan:
             self.m, self.n1, self.n2,
             int(r1.ref_mode), ptr(r1.ref_in), ptr(r1.sigma_in), int(r2.ref_mode), ptr(r2.ref_in), ptr(r2.sigma_in),
             float(r1.alpha), 1 if r1.substitute else 0, self.norm,
+            ptr(self.a_phi), ptr(self.bop), self.ld_pack,
             ptr(self.ref1), ptr(self.sigma1), ptr(self.ref2), ptr(self.sigma2),
             ptr(self.phi), ptr(self.psi), self.n2,
             ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle())
@@ -591,16 +596,33 @@ class CorrelationPlan:
             sig[1] = sig[0]
         return ref1, ref2, sig[0], sig[1], info
 
-    def fetch(self, out=None):
-        """Device -> host copy of both planes (into `out` or fresh pinned buffers)."""
+    def fetch(self, out=None, wait: bool = True):
+        """Device -> host copy of both planes (into `out` or fresh pinned
+        buffers).  wait=False queues the copies behind the launched kernels
+        and returns (sync, asyn, done): done() waits for them."""
         t = torch()
         if out is None:
             hs = t.empty(self.phi.shape, dtype=self.phi.dtype, pin_memory=True)
             ha = t.empty(self.psi.shape, dtype=self.psi.dtype, pin_memory=True)
         else:
             hs, ha = (t.from_numpy(o) if isinstance(o, np.ndarray) else o for o in out)
-        copy_d2h([(hs, self.phi), (ha, self.psi)])
-        return hs.numpy(), ha.numpy()
+        done = copy_d2h([(hs, self.phi), (ha, self.psi)], wait=wait)
+        if wait:
+            return hs.numpy(), ha.numpy()
+        return hs.numpy(), ha.numpy(), done
+
+    def run_to_host(self, out=None, axes=(None, None), labels=("first", "second")):
+        """launch() + the planes' D2H queued right behind the kernels, the
+        status readback / error checks overlapping that transfer; returns
+        (sync, asyn, check() results).  The copies have landed when this
+        returns or raises."""
+        self.launch()
+        s, a, done = self.fetch(out, wait=False)
+        try:
+            res = self.check(axes=axes, labels=labels)
+        finally:
+            done()
+        return s, a, res
 
 
 def readback(tensors: dict) -> dict:
@@ -706,11 +728,13 @@ def run_streamed(make_plan, n1: int, n2: int, dtype, blocks, out=None, check=Non
 _copy_streams = {}
 
 
-def copy_d2h(pairs, streams: int = 4, chunk_bytes: int = 256 << 20):
+def copy_d2h(pairs, streams: int = 4, chunk_bytes: int = 256 << 20, wait: bool = True):
     """Device -> host copies of (host, device) tensor pairs, split into row
     chunks over several copy streams: one stream reaches ~51 GB/s on the B200
     boxes' PCIe link, four ~56 GB/s (tools/d2h_probe.py).  Ordered after the
-    current stream's work; returns when every chunk has landed."""
+    current stream's work; returns when every chunk has landed -- or, with
+    wait=False, at once, returning the function that waits for them (the
+    caller overlaps its status readback with the transfer)."""
     t = torch()
     cur = t.cuda.current_stream()
     dev = cur.device
@@ -728,8 +752,14 @@ def copy_d2h(pairs, streams: int = 4, chunk_bytes: int = 256 << 20):
             with t.cuda.stream(pool[k % len(pool)]):
                 host[r0:r0 + rows].copy_(src[r0:r0 + rows], non_blocking=True)
             k += 1
-    for st in pool:
-        st.synchronize()
+
+    def done():
+        for st in pool:
+            st.synchronize()
+    if wait:
+        done()
+        return None
+    return done
 
 
 def sync():
