@@ -222,17 +222,18 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  * 64 x 64 output block (corr2d_small_block_count blocks: homo the upper
  * triangle, mirrored).  No CTA ever waits for another CTA.
  *   ops_a / ops_b      : device operand scratch, n1 (resp. n2; homo: n1) rows
- *                       of ld_ops doubles, 16-B aligned, ld_ops even and >=
- *                       corr2d_small_ops_depth(m)
+ *                       of ld_ops doubles, 16-B aligned, ld_ops ==
+ *                       corr2d_small_ops_depth(m) (dense rows: K1 writes a
+ *                       warp's 32 rows as one coalesced run)
  *   ref_out* / sigma_out* : as corr2d_prep (either may be NULL)
  *   status1 / status2  : device int32[4] each, the corr2d_prep status words
  *                       (status2 unused when homo); written by the call
  *   stats              : device uint64[3], as corr2d_contract_f64; written by the call
  *   work               : device int32[16], zero-filled by the caller ONCE before
- *                       the first call on it: status / stat accumulators and an
- *                       arrival counter, left zero by every call (the last CTA
- *                       publishes and resets them).  One work buffer per
- *                       concurrently running call.
+ *                       the first call on it: K1's status accumulators, left
+ *                       zero by every call (the contraction grid publishes and
+ *                       resets them).  One work buffer per concurrently running
+ *                       call.
  * The first call for a given m on a device builds a small DFT table (must not
  * be inside a CUDA graph capture).
  */

@@ -82,8 +82,9 @@ struct SmallParams {
 // work-buffer words (int32 indices); every launch leaves them zero
 constexpr int kWStatus1 = 0;   // [0, 4)  K1 status accumulator, dataset 1
 constexpr int kWStatus2 = 4;   // [4, 8)  dataset 2
-constexpr int kWDone = 8;      // CTAs finished (the last one publishes and resets)
-constexpr int kWStats = 10;    // [10, 16) max|sync|, max|async|, non-finite count (3 x uint64)
+// (K1 accumulates into them; the contraction grid's CTA 0 publishes them to
+// status1 / status2 and re-zeroes them -- after K1 completed, before the next
+// call's K1 starts: both grids order memory with griddepcontrol.wait)
 
 // profiling builds (-DCORR2D_PROFILING, CORR2D_SMALL_TRACE=1): thread 0 of
 // every CTA records %globaltimer at phase boundaries (K1 CTAs at slots
@@ -142,13 +143,17 @@ __device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c,
   int* status = p.work + (set ? kWStatus2 : kWStatus1);
   double ref = 0.0, scale = 1.0;
   int bad = 0;
-  for (int t = 0; t < m; ++t) bad += !isfinite(ys[t * kYS]);
+  double sum = 0.0;                                    // left to right (numpy's axis-0 order)
+#pragma unroll 4
+  for (int t = 0; t < m; ++t) {
+    const double v = ys[t * kYS];
+    bad += !isfinite(v);
+    sum = __dadd_rn(sum, v);
+  }
   if (owner && valid && bad) atomicAdd(&status[CORR2D_ST_NONFINITE], bad);
   if (ref_mode == CORR2D_REF_PROVIDED) {
     ref = valid ? __ldg((set ? p.ref_in2 : p.ref_in1) + c) : 0.0;
   } else if (ref_mode == CORR2D_REF_MEAN) {
-    double sum = 0.0;                                  // left to right (numpy's axis-0 order)
-    for (int t = 0; t < m; ++t) sum = __dadd_rn(sum, ys[t * kYS]);
     ref = __ddiv_rn(sum, (double)m);
   }
   if (p.alpha > 0.0) {
@@ -180,10 +185,18 @@ __device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c,
     if (ro) ro[c] = ref;
   }
   const bool sub = ref_mode != CORR2D_REF_NONE, div = p.alpha > 0.0;
+  if (!div) {
+#pragma unroll 4
+    for (int t = 0; t < m; ++t) {
+      const double v = ys[t * kYS];
+      ys[t * kYS] = valid ? (sub ? __dsub_rn(v, ref) : v) : 0.0;
+    }
+    return;
+  }
   for (int t = 0; t < m; ++t) {
     double v = ys[t * kYS];
     if (sub) v = __dsub_rn(v, ref);
-    if (div) v = __ddiv_rn(v, scale);
+    v = __ddiv_rn(v, scale);
     ys[t * kYS] = valid ? v : 0.0;
   }
 }
@@ -279,6 +292,9 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
   SMALL_STAMP(0, 0);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");   // inputs written by earlier kernels are visible
   SMALL_STAMP(0, 1);
+  // this call's stats words start at zero (the contraction grid reduces into
+  // them only after this grid completed)
+  if (blockIdx.x == 0 && tid < 3) p.stats[tid] = 0ull;
   // the DFT rows and the slot table into shared memory, in flight together
   // with the samples (one DRAM round trip; the loops below then never touch
   // global memory for them)
@@ -356,27 +372,65 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
         }
       }
   __syncwarp();
-  if (!valid) return;
-  double* rowA = set ? nullptr : p.opsA + (long long)c * p.ld_ops;
-  double* rowB = (set || p.homo) ? p.opsB + (long long)c * p.ld_ops : nullptr;
   // every slot once (pads are 0), from the per-slot table after W: bin w and
   // small exact coefficients -- A = Norm (pa R + qa I), B = pb R + qb I
-  // (gauss_values' operands: a + b, a, -b | a at Nyquist; c, d - c, c + d)
-  const double* slot = tab + 48 * mpad;              // per slot: w (or -1), pa, qa, pb, qb
+  // (gauss_values' operands: a + b, a, -b | a at Nyquist; c, d - c, c + d).
+  // The rows are staged per warp in shared memory in their global layout
+  // (ld_ops = 3 kg: the warp's 32 rows are one contiguous run), then leave as
+  // coalesced 16-byte stores.
   const int ns = 3 * p.kg;
-  for (int s = 0; s < ns; ++s, slot += 5) {
-    const int w = (int)slot[0];
-    double va = 0.0, vb = 0.0;
-    if (w >= 0) {
-      const double R = ys[(2 * w) * kYS + tid], I = ys[(2 * w + 1) * kYS + tid];
-      va = p.norm * fma(slot[1], R, slot[2] * I);
-      vb = fma(slot[3], R, slot[4] * I);
+  double* stA = tab + 48 * mpad + 5 * ns + (size_t)warp * 32 * ns;   // [32][ns] per warp
+  double* stB = stA + (size_t)kSThreads * ns;
+  const bool wantA = !set, wantB = set || p.homo;
+  {
+    // zero the lane's staged rows (pad slots), then every bin's three Gauss
+    // slots from registers: no table lookups, no dependent loads
+    double2* zA = reinterpret_cast<double2*>(stA + lane * ns);
+    double2* zB = reinterpret_cast<double2*>(stB + lane * ns);
+    for (int i = 0; i < ns / 2; ++i) zA[i] = zB[i] = make_double2(0.0, 0.0);
+    const int kg = p.kg, H = m / 2, Iint = gauss_interior(m);
+    const double nrm = p.norm;
+    double* a = stA + lane * ns;
+    double* b = stB + lane * ns;
+    // a runtime loop: straight-line code is fetched cold, line by line, on
+    // every step of a stream that evicts L2 (the bench's rotation does)
+#pragma unroll 1
+    for (int w = 0; w <= H; ++w) {
+      const double R = ys[(2 * w) * kYS + tid];
+      const double I = (w == 0 || 2 * w == m) ? 0.0 : ys[(2 * w + 1) * kYS + tid];
+      const double k = (w == 0 || 2 * w == m) ? 1.0 : 2.0;
+      const double ra = nrm * (k * R), ia = nrm * (k * I);    // a, b (x 2 exact)
+      if (w <= Iint) {                               // DC / interior: segments 0 and 1 at slot w
+        a[w] = ra + ia;      b[w] = R;               // a + b, c
+        a[kg + w] = ra;      b[kg + w] = -I - R;     // a, d - c
+      }
+      if (w >= 1) {
+        if (w <= Iint) { a[2 * kg + w - 1] = -ia; b[2 * kg + w - 1] = R - I; }   // -b, c + d
+        else { a[2 * kg + Iint] = ra; b[2 * kg + Iint] = R; }                     // Nyquist: a, c
+      }
     }
-    if (rowA) rowA[s] = va;
-    if (rowB) rowB[s] = vb;
+  }
+  __syncwarp();
+  {
+    const int cw = c - lane;                         // the warp's first channel
+    const int nrow = min(32, n - cw);
+    if (nrow > 0) {
+      const int pieces = nrow * ns / 2;              // 16-byte pieces of the warp's rows
+      double2* gA = reinterpret_cast<double2*>(p.opsA + (long long)cw * p.ld_ops);
+      double2* gB = reinterpret_cast<double2*>(p.opsB + (long long)cw * p.ld_ops);
+      const double2* sA = reinterpret_cast<const double2*>(stA);
+      const double2* sB = reinterpret_cast<const double2*>(stB);
+      for (int i = lane; i < pieces; i += 32) {
+        if (wantA) gA[i] = sA[i];
+        if (wantB) gB[i] = sB[i];
+      }
+    }
   }
   SMALL_STAMP(0, 5);
 }
+
+__device__ __noinline__ void small_publish(const SmallParams& p, unsigned long long mphi, unsigned long long mpsi,
+                                           int lane, int warp, int tid);
 
 // ---- contraction: one CTA per 64 x 64 output block ----
 __global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __grid_constant__ SmallParams p) {
@@ -401,6 +455,14 @@ __global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __gr
   SMALL_STAMP(kTraceK1, 0);
   asm volatile("griddepcontrol.wait;\n" ::: "memory");   // K1 complete, its operand rows visible
   SMALL_STAMP(kTraceK1, 1);
+  // K1's status accumulators are final now: CTA 0 publishes them and leaves
+  // the words zero for the next call (whose K1 starts after this grid ends)
+  if (blockIdx.x == 0 && tid < 4) {
+    p.status1[tid] = p.work[kWStatus1 + tid];
+    p.work[kWStatus1 + tid] = 0;
+    if (p.status2) p.status2[tid] = p.work[kWStatus2 + tid];
+    p.work[kWStatus2 + tid] = 0;
+  }
   // one bulk copy per operand row (thread t: A row t or B row t - 64), all
   // completing on one mbarrier; rows past the map are zero-filled
   if (tid == 0)
@@ -449,7 +511,9 @@ __global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __gr
   __syncthreads();                                   // operands consumed: the staging overlays them
   SMALL_STAMP(kTraceK1, 3);
 
-  // ---- 5. stage both planes, then coalesced row stores (+ mirror) ----
+  const int i0 = I * kSB, j0 = J * kSB;
+  // ---- 5. stage both planes, then coalesced row stores (+ mirror), with
+  //      max|.| / the finite check folded into the stores' smem reads ----
   double* Cphi = sm;                                 // [64][kCS]
   double* Cpsi = sm + kSB * kCS;
 #pragma unroll
@@ -466,7 +530,6 @@ __global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __gr
       }
   __syncthreads();
   unsigned long long mphi = 0, mpsi = 0;
-  const int i0 = I * kSB, j0 = J * kSB;
   const bool rows_full = i0 + kSB <= p.n1, cols_full = j0 + kSB <= p.n2;
   if (!diag && rows_full && cols_full && p.vec) {
     // whole off-diagonal block: a thread owns one column pair of rows
@@ -555,7 +618,16 @@ __global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __gr
   }
   }  // general blocks
   SMALL_STAMP(kTraceK1, 4);
-  // ---- max|.| and the finite check (integer pipe), one set of atomics per CTA ----
+  // ---- 6. one set of fire-and-forget reductions per CTA (no fence, no wait) ----
+  small_publish(p, mphi, mpsi, lane, warp, tid);
+  SMALL_STAMP(kTraceK1, 5);
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// One set of atomics per CTA into the work words; the last CTA to arrive (an
+// arrival counter, never a wait) publishes status / stats and re-zeroes them.
+__device__ __noinline__ void small_publish(const SmallParams& p, unsigned long long mphi, unsigned long long mpsi,
+                                           int lane, int warp, int tid) {
   constexpr unsigned long long kInf = 0x7ff0000000000000ull;
   int bad = (mphi >= kInf) + (mpsi >= kInf);
   mphi = min(mphi, kInf);
@@ -574,38 +646,18 @@ __global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __gr
   }
   __syncthreads();
   if (tid == 0) {
-    unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWStats);
+    // fire-and-forget reductions straight into the caller's stats words
+    // (zeroed by this call's K1 grid, which completed before this grid began)
     unsigned long long a0 = 0, a1 = 0, a2 = 0;
     for (int w = 0; w < kSThreads / 32; ++w) {
       a0 = max(a0, red[0][w]);
       a1 = max(a1, red[1][w]);
       a2 += red[2][w];
     }
-    if (a0) atomicMax(&acc[0], a0);
-    if (a1) atomicMax(&acc[1], a1);
-    if (a2) atomicAdd(&acc[2], a2);
-    // the last CTA to finish publishes status / stats and leaves the words zero
-    __threadfence();
-    if (atomicAdd(p.work + kWDone, 1) == (int)gridDim.x - 1) {
-      __threadfence();
-      volatile int* wv = p.work;
-      for (int k = 0; k < 4; ++k) {
-        p.status1[k] = wv[kWStatus1 + k];
-        if (p.status2) p.status2[k] = wv[kWStatus2 + k];
-        wv[kWStatus1 + k] = 0;
-        wv[kWStatus2 + k] = 0;
-      }
-      volatile unsigned long long* av = acc;
-      for (int k = 0; k < 3; ++k) {
-        p.stats[k] = av[k];
-        av[k] = 0ull;
-      }
-      wv[kWDone] = 0;
-      __threadfence();
-    }
+    if (a0) atomicMax(&p.stats[0], a0);
+    if (a1) atomicMax(&p.stats[1], a1);
+    if (a2) atomicAdd(&p.stats[2], a2);
   }
-  SMALL_STAMP(kTraceK1, 5);
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
 static long long small_blocks(int n1, int n2, int homo) {
@@ -708,10 +760,10 @@ extern "C" int corr2d_correlate_small_f64(
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: homo needs n1 == n2");
   if (ld_raw1 < n1 || (!homo && ld_raw2 < n2)) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_raw < n");
   if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_out < n2");
-  if (ld_ops < corr2d_small_ops_depth(m) || ld_ops % 2 ||
+  if (ld_ops != corr2d_small_ops_depth(m) ||
       ((reinterpret_cast<uintptr_t>(ops_a) | reinterpret_cast<uintptr_t>(ops_b)) & 15))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: operand rows must be 16-B aligned with "
-                                 "ld_ops even and >= corr2d_small_ops_depth(m)");
+                                 "ld_ops == corr2d_small_ops_depth(m)");
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(CORR2D_ERR_DATA, "scaling exponent must lie in [0, 1]");
   for (int r : {ref_mode1, ref_mode2})
     if (r < CORR2D_REF_MEAN || r > CORR2D_REF_NONE) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad ref_mode");
@@ -752,7 +804,8 @@ extern "C" int corr2d_correlate_small_f64(
   const long long blocks = small_blocks(n1, n2, homo);
   if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
   const int prep_blocks = p.nb1 + (homo ? 0 : (n2 + kSThreads - 1) / kSThreads);
-  const size_t prep_smem = ((size_t)p.yrows * kYS + 48 * (size_t)p.mpad + 15 * (size_t)p.kg) * sizeof(double);
+  const size_t prep_smem = ((size_t)p.yrows * kYS + 48 * (size_t)p.mpad + 15 * (size_t)p.kg +
+                            2 * (size_t)kSThreads * 3 * p.kg) * sizeof(double);
   const size_t ops = 2 * (size_t)kSB * p.ks * sizeof(double);
   const size_t stage = 2 * (size_t)kSB * kCS * sizeof(double);
   const size_t smem = ops > stage ? ops : stage;
@@ -762,7 +815,8 @@ extern "C" int corr2d_correlate_small_f64(
     cudaFuncSetAttribute(small_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(worst_ops > stage ? worst_ops : stage));
     cudaFuncSetAttribute(small_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16) * sizeof(double)));
+                         (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16 + 2 * kSThreads * 48) *
+                               sizeof(double)));
     attr_set = true;
   }
   // programmatic dependent launch for both grids: each launches while its
