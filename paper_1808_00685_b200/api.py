@@ -44,7 +44,7 @@ def _norm_spec(norm, engine_name="fourier") -> NormalizationSpec:
 
 def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: PreprocessSpec, *,
                norm=None, on_zero_variance="error", dtype="float64", rows=None, device=None,
-               engine_name="fourier", spectra_shard=None, distributed=None):
+               engine_name="fourier", distributed=None):
     """A bound :class:`engine.CorrelationPlan` for the fused raw -> planes pipeline."""
     from .preprocess import _raw_device, _recipe_for
     _, dev = engine.require_device(device)
@@ -76,7 +76,7 @@ def build_plan(ds1: SpectralDataset, ds2: SpectralDataset | None, spec: Preproce
     plan = engine.CorrelationPlan(
         n1=ds1.n, n2=(ds1 if homo else ds2).n, m=m, recipe1=r1, recipe2=r2, norm=constant,
         dtype=dtype, rows=rows, device=dev, want_ref=True, want_sigma=r1.alpha > 0.0,
-        route=engine_name, spectra_shard=spectra_shard)
+        route=engine_name)
     plan.bind(_raw_device(ds1, dev), None if homo else _raw_device(ds2, dev))
     plan.constant = constant
     plan.t_axis = plan1.t_new if plan1 is not None else ds1.perturbation_axis

@@ -770,6 +770,8 @@ contract_tc_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_cons
 struct Params2 {
   int n1, n2, hp, homo, even, tma_store;
   int f8;                 // operands in CORR2D_PACK_F16F8 layout (else BF16X2)
+  int half_b;             // split-B MMAs: N=128 products, each CTA loads 64 B rows of Re' and Im'
+                          // (the negate-A bit forms -A_re.B_im), no -Im' third: 3/4 of the operand traffic
   int store_pol;          // L2 policy of the output stores: 0 evict_first, 1 normal, 2 evict_last
   int dbg;                // profiling switches: 1 = no output stores, 2 = no MMAs (results invalid)
   long long* trace;       // profiling (CORR2D_TRACE=1): per-CTA stall cycles, 8 counters each
@@ -873,6 +875,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16_2sm() {
 // F16 x F16 (kind::f16) / E4M3 x E4M3 (kind::f8f6f4), M = 256, N = 256
 __host__ __device__ constexpr uint32_t idesc_f16f8_2sm() {
   return (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+// split-B products: M = 256 (pair), N = 128, optional negate-A (bit 13)
+__host__ __device__ constexpr uint32_t idesc_f16f8_2sm_n128(bool neg_a) {
+  return (1u << 4) | (neg_a ? (1u << 13) : 0u) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_bf16_2sm_n128(bool neg_a) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (neg_a ? (1u << 13) : 0u) | ((uint32_t)(128 >> 3) << 17) |
+         ((uint32_t)(256 >> 4) << 24);
 }
 
 // Grouped raster order: row pairs are taken kGroup at a time and, inside a
@@ -1218,9 +1228,20 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
             continue;
           }
-          mbar_expect_tx_remote(lbar, STAGE_BYTES);
           uint8_t* base = stages + stage * STAGE_BYTES;
           const int k0 = kb * 2 * KB;
+          if (NPAIR == 1 && p.half_b) {
+            // A_re, A_im (128 rows each) + this CTA's 64-row halves of B_re and B_im
+            mbar_expect_tx_remote(lbar, 6 * TILE_BYTES);
+            const int bhalf = brow + 64 * (int)prank;
+            tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
+            tma_load_3d_2sm(base + 2 * TILE_BYTES, &tmap_a, 2 * p.hp + k0, arow, 0, lbar, keep);
+            tma_load_3d_2sm(base + 4 * TILE_BYTES, &tmap_b, k0, bhalf, 0, lbar, keep);
+            tma_load_3d_2sm(base + 5 * TILE_BYTES, &tmap_b, 2 * p.hp + k0, bhalf, 0, lbar, keep);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          mbar_expect_tx_remote(lbar, STAGE_BYTES);
           // each box: 128 rows x [hi KB | lo KB] slots (128-B rows, SWIZZLE_128B)
           if (NPAIR == 1) {
             tma_load_3d_2sm(base + 0 * TILE_BYTES, &tmap_a, k0, arow, 0, lbar, keep);
@@ -1250,7 +1271,61 @@ contract_tc_2sm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait_t(&full[stage], phase, tr ? &tr_wait : nullptr);
           tc_fence_after();
-          if (lane == 0 && p.f8) {
+          if (lane == 0 && p.half_b) {
+            // split-B: Phi = A_re.B_re^T + A_im.B_im^T and Psi = A_im.B_re^T - A_re.B_im^T
+            // as N = 128 products into the tile's two 128-column halves; the
+            // pair's 128 B rows are split 64 / 64 between its CTAs (same bins,
+            // same products as the N = 256 form, 3/4 of its operand traffic)
+            const uint32_t base = su32(stages + stage * STAGE_BYTES);
+            const uint32_t are = base, aim = base + 2 * TILE_BYTES;
+            const uint32_t bre = base + 4 * TILE_BYTES, bim = base + 5 * TILE_BYTES;
+            const uint32_t dphi = d, dpsi = d + 128;
+            if (!(dbg_bits(p) & 2)) {
+              if (p.f8) {
+                constexpr uint32_t IH = idesc_f16f8_2sm_n128(false), IN = idesc_f16f8_2sm_n128(true);
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                  const uint32_t off = ks * 32, first = (kb | ks) ? 1u : 0u;
+                  umma2_f16(dphi, desc_sw128(are + off), desc_sw128(bre + off), IH, first);
+                  umma2_f16(dphi, desc_sw128(aim + off), desc_sw128(bim + off), IH, 1);
+                  umma2_f16(dpsi, desc_sw128(aim + off), desc_sw128(bre + off), IH, first);
+                  umma2_f16(dpsi, desc_sw128(are + off), desc_sw128(bim + off), IN, 1);
+                }
+                umma2_f8(dphi, desc_sw128(are + 64), desc_sw128(bre + 96), IH, 1);
+                umma2_f8(dphi, desc_sw128(are + 96), desc_sw128(bre + 64), IH, 1);
+                umma2_f8(dphi, desc_sw128(aim + 64), desc_sw128(bim + 96), IH, 1);
+                umma2_f8(dphi, desc_sw128(aim + 96), desc_sw128(bim + 64), IH, 1);
+                umma2_f8(dpsi, desc_sw128(aim + 64), desc_sw128(bre + 96), IH, 1);
+                umma2_f8(dpsi, desc_sw128(aim + 96), desc_sw128(bre + 64), IH, 1);
+                umma2_f8(dpsi, desc_sw128(are + 64), desc_sw128(bim + 96), IN, 1);
+                umma2_f8(dpsi, desc_sw128(are + 96), desc_sw128(bim + 64), IN, 1);
+              } else {
+                constexpr uint32_t JH = idesc_bf16_2sm_n128(false), JN = idesc_bf16_2sm_n128(true);
+#pragma unroll
+                for (int ks = 0; ks < KB / 16; ++ks) {
+                  const uint32_t off = ks * 32, first = (kb | ks) ? 1u : 0u;
+                  const uint64_t ah = desc_sw128(are + off), al = desc_sw128(are + 64 + off);
+                  const uint64_t ih = desc_sw128(aim + off), il = desc_sw128(aim + 64 + off);
+                  const uint64_t bh = desc_sw128(bre + off), bl = desc_sw128(bre + 64 + off);
+                  const uint64_t jh = desc_sw128(bim + off), jl = desc_sw128(bim + 64 + off);
+                  umma2_f16(dphi, ah, bh, JH, first);
+                  umma2_f16(dphi, ah, bl, JH, 1);
+                  umma2_f16(dphi, al, bh, JH, 1);
+                  umma2_f16(dphi, ih, jh, JH, 1);
+                  umma2_f16(dphi, ih, jl, JH, 1);
+                  umma2_f16(dphi, il, jh, JH, 1);
+                  umma2_f16(dpsi, ih, bh, JH, first);
+                  umma2_f16(dpsi, ih, bl, JH, 1);
+                  umma2_f16(dpsi, il, bh, JH, 1);
+                  umma2_f16(dpsi, ah, jh, JN, 1);
+                  umma2_f16(dpsi, ah, jl, JN, 1);
+                  umma2_f16(dpsi, al, jh, JN, 1);
+                }
+              }
+            }
+            umma2_commit_mask(&empty[stage], all_mask);
+            if (kb == nkb - 1) umma2_commit_mask(&tfull[acc], pair_mask);
+          } else if (lane == 0 && p.f8) {
             // F16F8 block [fp16 hi 64 B | e4m3 hi 32 B | e4m3 residual 32 B]:
             // hi.hi as two K=16 fp16 MMAs per operand pair, the cross terms as
             // K=32 e4m3 MMAs (twice the fp16 rate) -- 8 MMAs per k-block
@@ -1591,12 +1666,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // hi and lo halves ([hi 32 | lo 32], 128-B rows, SWIZZLE_128B).  Measured with
 // tools/microbench/tmaloads.cu: 128-B box rows stream L2 -> SMEM at ~20 TB/s
 // chip-wide, the former 64-B rows (separate hi / lo planes) at ~11 TB/s.
-static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows) {
+static int make_operand_map(CUtensorMap* map, const void* base, long long ld, long long rows,
+                            unsigned box_rows = BM) {
   auto fn = encode_fn();
   if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, 1};
   cuuint64_t strides[2] = {(cuuint64_t)ld * 2, (cuuint64_t)ld * 2 * (cuuint64_t)rows};
-  cuuint32_t box[3] = {2 * KB, BM, 1};
+  cuuint32_t box[3] = {2 * KB, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1702,7 +1778,11 @@ extern "C" int corr2d_contract_tc(
   CUtensorMap ma, mb;
   int rc = make_operand_map(&ma, a, ld_pack, n1);
   if (rc) return rc;
-  rc = make_operand_map(&mb, b, ld_pack, n2);
+  // split-B CTA-pair MMAs (default; CORR2D_PAIR_SPLITB=0 keeps the N = 256 form
+  // over the -Im' third): each CTA loads 64-row boxes of B
+  static const int split_env = [] { const char* e = getenv("CORR2D_PAIR_SPLITB"); return e && e[0] == '0' ? 0 : 1; }();
+  const bool half_b = split_env && bf16_variant(n1, row0, row1, aligned) == 1;
+  rc = make_operand_map(&mb, b, ld_pack, n2, half_b ? 64u : (unsigned)BM);
   if (rc) return rc;
   OutMaps om;
   memset(&om, 0, sizeof(om));
@@ -1731,6 +1811,7 @@ extern "C" int corr2d_contract_tc(
     Params2 p{};
     p.n1 = n1; p.n2 = n2; p.hp = mp / 3; p.homo = homo; p.even = (m % 2) == 0; p.tma_store = 1;
     p.f8 = pack_kind == CORR2D_PACK_F16F8;
+    p.half_b = half_b ? 1 : 0;
 #ifdef CORR2D_PROFILING
     // profiling builds only (tools/build_variant.sh -DCORR2D_PROFILING): store
     // policy, work-skipping switches (results invalid) and per-role stall traces.

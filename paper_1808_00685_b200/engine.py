@@ -20,7 +20,6 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _abi
-from .engine_core import channel_chunk, gather_rows
 from .errors import DataError, NumericError
 
 _torch = None
@@ -339,13 +338,9 @@ class CorrelationPlan:
 
     def __init__(self, *, n1, n2, m, recipe1: PrepRecipe, recipe2: PrepRecipe | None,
                  norm: float, dtype="float64", rows=None, device=None, want_ref=True,
-                 want_sigma=False, tiles=None, route="fourier", spectra_shard=None):
+                 want_sigma=False, tiles=None, route="fourier"):
         self.lib, self.dev = require_device(device)
         t = torch()
-        # spectra_shard=(rank, world): K1 runs on this rank's channel chunk only and
-        # the packed spectra are all-gathered in place; the
-        # buffers then hold world * chunk rows, the tail rows zero
-        self.shard = tuple(spectra_shard) if spectra_shard and spectra_shard[1] > 1 else None
         self.homo = recipe2 is None
         if self.homo and n1 != n2:
             raise DataError("homo correlation needs n1 == n2")
@@ -380,17 +375,17 @@ class CorrelationPlan:
         # in a 128-byte pad (include/corr2d.h)
         self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
         # small m (fp64 Fourier route, m <= 32, no resampling, whole map): the
-        # whole call is ONE launch (csrc/small.cu: independent CTAs, each
-        # recomputing K1 for its 64 x 64 block's channels in shared memory)
-        self.small = (route == "fourier" and self.dtype == np.float64 and self.shard is None
+        # whole call is ONE C call (csrc/small_path.cu: K1 once per channel, then
+        # the block contraction, two PDL-chained kernels)
+        self.small = (route == "fourier" and self.dtype == np.float64
                       and small_fused_enabled() and 2 <= self.m <= 32
                       and all(r is None or (r.resample is None and r.m_in == r.m) for r in (recipe1, recipe2))
                       and (recipe2 is None or (recipe2.alpha == recipe1.alpha
                                                and recipe2.substitute == recipe1.substitute))
                       and self.row0 == 0 and self.row1 == self.n1 and tiles is None)
         dev = self.dev
-        R1, R2 = self._rows(self.n1), self._rows(self.n2)
-        alloc = t.zeros if self.shard else t.empty
+        R1, R2 = self.n1, self.n2
+        alloc = t.empty
         if self.small:
             # the small path's own Gauss operand rows (K1 -> contraction, L2-resident)
             self.ld_pack = self.lib.corr2d_small_ops_depth(self.m)
@@ -429,12 +424,6 @@ class CorrelationPlan:
         self.sigma1 = alloc(R1, dtype=t.float64, device=dev) if want_sigma else None
         self.sigma2 = (alloc(R2, dtype=t.float64, device=dev) if (want_sigma and not self.homo) else None)
         self.raw1 = self.raw2 = None
-
-    def _rows(self, n):
-        if self.shard is None:
-            return n
-        rank, world = self.shard
-        return channel_chunk(n, world, rank)[2] * world
 
     @property
     def bop(self):
@@ -480,13 +469,6 @@ class CorrelationPlan:
         roles1 = _abi.ROLE_A | (_abi.ROLE_B if self.homo else 0)
         if self.pack_kind in (_abi.PACK_BF16X2, _abi.PACK_F16F8) and self.homo:
             roles1 = _abi.ROLE_A
-        if self.shard is not None:
-            self._prep_sharded(self.raw1, self.recipe1, self.n1, roles1, self.a_phi, self.a_psi,
-                               self.b_homo if self.homo else None, self.ref1, self.sigma1, self.status1)
-            if not self.homo:
-                self._prep_sharded(self.raw2, self.recipe2, self.n2, _abi.ROLE_B, None, None, self.b,
-                                   self.ref2, self.sigma2, self.status2)
-            return
         launch_prep(lib, self.raw1, self.recipe1, norm=self.norm, pack_kind=self.pack_kind, roles=roles1,
                     a_phi=self.a_phi, a_psi=self.a_psi, b=self.b_homo if self.homo else None,
                     ld_pack=self.ld_pack, ref_out=self.ref1,
@@ -495,32 +477,6 @@ class CorrelationPlan:
             launch_prep(lib, self.raw2, self.recipe2, norm=self.norm, pack_kind=self.pack_kind,
                         roles=_abi.ROLE_B, b=self.b, ld_pack=self.ld_pack,
                         ref_out=self.ref2, sigma_out=self.sigma2, status=self.status2)
-
-    def _prep_sharded(self, raw, recipe, n, roles, a_phi, a_psi, b, ref, sigma, status):
-        """K1 over this rank's channel chunk, then one in-place all-gather per
-        packed buffer (and of ref / sigma); status words are all-reduced."""
-        import dataclasses
-
-        import torch.distributed as dist
-        rank, world = self.shard
-        c0, c1, chunk = channel_chunk(n, world, rank)
-        if c1 > c0:
-            sl = dataclasses.replace(
-                recipe, ref_in=None if recipe.ref_in is None else recipe.ref_in[c0:c1],
-                sigma_in=None if recipe.sigma_in is None else recipe.sigma_in[c0:c1])
-            rows = (lambda x: None if x is None else x[c0:])
-            launch_prep(self.lib, raw[:, c0:c1], sl, norm=self.norm, pack_kind=self.pack_kind, roles=roles,
-                        a_phi=rows(a_phi), a_psi=rows(a_psi), b=rows(b), ld_pack=self.ld_pack,
-                        ref_out=rows(ref), sigma_out=rows(sigma), status=status)
-        else:
-            status.zero_()
-        seen = set()
-        for buf in (a_phi, a_psi, b, ref, sigma):
-            if buf is not None and buf.data_ptr() not in seen:
-                seen.add(buf.data_ptr())
-                gather_rows(buf, chunk, world, rank)
-        dist.all_reduce(status[:2], op=dist.ReduceOp.SUM)
-        dist.all_reduce(status[2:3], op=dist.ReduceOp.MAX)
 
     def launch_contract(self):
         lib = self.lib

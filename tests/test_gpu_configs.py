@@ -79,61 +79,3 @@ def test_cfg5_whole_map_two_independent_kernels(monkeypatch):
         for r0 in range(0, x.shape[0], 4096):
             diff = max(diff, float(torch.abs(x[r0:r0 + 4096] - y[r0:r0 + 4096]).max()))
         assert diff <= 2e-5 * scale, diff / scale
-
-
-def _shard_worker(rank, world, port, out):
-    import os
-    import sys
-    import torch
-    import torch.distributed as dist
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
-    # the all-gather scheme belongs to the two-kernel path (K1, collective, K2);
-    # the one-launch small-m path recomputes its spectra -- compare like with like
-    os.environ["CORR2D_SMALL_FUSED"] = "0"
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parent.parent))
-    import paper_1808_00685_b200 as P
-    from paper_1808_00685_b200 import api, configs as C
-    for k in (4, 2):
-        case = C.make(k)
-        dt = np.float32 if case.dtype == "float32" else np.float64
-        ds1 = P.SpectralDataset(case.set1.spectral_axis, case.set1.perturbation_axis, case.set1.intensities, dtype=dt)
-        ds2 = None if case.set2 is None else P.SpectralDataset(case.set2.spectral_axis, case.set2.perturbation_axis,
-                                                                case.set2.intensities, dtype=dt)
-        spec = P.PreprocessSpec(resample=None if case.resample is None else P.ResampleSpec(
-            case.resample, P.InterpolantKind.from_name(case.interpolant)), scaling_exponent=case.alpha)
-        full, _ = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=torch.device("cuda", 0))
-        full.launch()
-        shard, _ = api.build_plan(ds1, ds2, spec, dtype=case.dtype, device=torch.device("cuda", 0),
-                                  spectra_shard=(rank, world))
-        shard.launch()
-        torch.cuda.synchronize()
-        r1 = full.check()
-        r2 = shard.check()
-        same = bool(torch.equal(full.phi, shard.phi) and torch.equal(full.psi, shard.psi))
-        same_ref = np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
-        out.put((rank, k, same, same_ref))
-    dist.destroy_process_group()
-
-
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_spectra_allgather_bit_identical(world):
-    """K1 sharded over `world` ranks (gloo, all on this GPU) + all-gather of the
-    packed spectra gives bit-identical maps and references to the unsharded
-    plan (cfg4: resample + alpha, homo; cfg2: hetero)."""
-    import socket
-    import torch.multiprocessing as mp
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=300) for _ in range(2 * world)]
-    for p in procs:
-        p.join(120)
-        assert p.exitcode == 0
-    assert all(same and same_ref for _, _, same, same_ref in res), res

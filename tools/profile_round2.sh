@@ -1,0 +1,53 @@
+#!/bin/bash
+# Round-2 evidence under gpurun, from the repo root: bench lines (both arms),
+# microbenchmarks (peaks, launch / store floors), whole-map parity evidence,
+# compute-sanitizer logs, the fp64 bound decomposition and the small-path
+# trace (profiling build), ncu launch lists and full captures.
+# Summarised into profiles/ by tools/summarize_round2.py.
+set -u
+OUT=gpurun_out/prof2
+mkdir -p $OUT/evidence
+nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,power.limit --format=csv > $OUT/gpu.csv 2>&1
+# 1. microbenchmarks
+./tools/microbench/peaks > $OUT/peaks.json 2> $OUT/peaks.err
+./tools/microbench/floor > $OUT/floor.json 2> $OUT/floor.err
+# 2. bench lines: headline (cfg5, with cpu_baseline), the other configs, the reference arm
+timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench_cfg5.json 2> $OUT/bench_cfg5.err
+for c in 1 2 3 4; do
+  timeout 600 python bench.py --config $c --steps 20 --warmup 5 --no-cpu-baseline > $OUT/bench_cfg$c.json 2> $OUT/bench_cfg$c.err
+done
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/bench_reference_cfg5.json 2> $OUT/bench_reference.err
+timeout 600 python tools/bench_extras.py > $OUT/extras.json 2> $OUT/extras.err
+# 3. whole-map parity + adversarial evidence (slow tests) and the full GPU suite
+CORR2D_EVIDENCE_DIR=$OUT/evidence timeout 1800 python -m pytest tests/test_gpu_wholemap.py -q > $OUT/wholemap_tests.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -q > $OUT/gpu_tests.log 2>&1
+# 4. fp64 bound decomposition and the small-path trace (profiling build)
+for c in 3 4; do
+  for skip in 0 1 2 3; do
+    CORR2D_LIB=_variants/libcorr2d_prof.so CORR2D_DEBUG_SKIP=$skip timeout 300 python tools/time_contract.py $c > $OUT/decomp_cfg${c}_skip$skip.json 2>&1
+  done
+done
+CORR2D_LIB=_variants/libcorr2d_prof.so timeout 300 python tools/dev/small_trace.py > $OUT/small_trace.txt 2>&1
+# 5. compute-sanitizer on one small invocation of every kernel
+CS=/usr/local/cuda/bin/compute-sanitizer
+timeout 1200 $CS --tool memcheck --target-processes all python tools/sanitize.py all > $OUT/sanitizer_memcheck.txt 2>&1
+for w in small f64 prep peaks hilbert; do
+  timeout 900 $CS --tool racecheck --target-processes all python tools/sanitize.py $w > $OUT/sanitizer_racecheck_$w.txt 2>&1
+done
+timeout 1200 $CS --tool synccheck --target-processes all python tools/sanitize.py all > $OUT/sanitizer_synccheck.txt 2>&1
+timeout 900 $CS --tool racecheck --target-processes all python tools/sanitize.py tc > $OUT/sanitizer_racecheck_tc.txt 2>&1
+# 6. ncu: launch lists of the bench commands, full captures of the hot kernels
+for c in 5 1 2 3; do
+  CMD="python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $OUT/launches_cfg$c.csv $CMD > $OUT/ncu_launch$c.log 2>&1
+done
+CMD5="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+ncu --set full --clock-control none --import-source on -k regex:"contract_tc_2sm|prep_fast" -c 2 -o $OUT/full_cfg5 $CMD5 > $OUT/ncu_full5.log 2>&1
+CMD3="python bench.py --config 3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+ncu --set full --clock-control none --import-source on -k regex:"contract_f64|prep_fast" -c 2 -o $OUT/full_cfg3 $CMD3 > $OUT/ncu_full3.log 2>&1
+for c in 1 2; do
+  CMDS="python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+  ncu --set full --clock-control none --import-source on -k regex:"small_" -c 2 -o $OUT/full_cfg$c $CMDS > $OUT/ncu_full$c.log 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:"peaks_vec" -c 1 -o $OUT/full_peaks5 python tools/bench_extras.py > $OUT/ncu_peaks.log 2>&1
+ls -la $OUT
