@@ -931,6 +931,24 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
 
   mark(1);
   // four-step FFT of z = x_even + i x_odd (compute type CT)
+  // fp32 transform: each channel of the pair is first brought to max|x| in
+  // [1, 2) by an exact power of two 2^pe, so the partner's rounding error in
+  // the paired transform is ~2^-24 of the channel's OWN scale, not of the
+  // larger partner's; the packing below folds 2^-pe back in
+  int pe[2] = {0, 0};
+  if constexpr (BF) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      double mx = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t) mx = fmax(mx, fabs(xv[e][t]));
+      mx = warp_max(mx);
+      if (mx > 0.0 && mx <= 1.7976931348623157e308) pe[e] = min(100, max(-100, -ilogb(mx)));
+      const double f = __longlong_as_double((long long)(1023 + pe[e]) << 52);
+#pragma unroll
+      for (int t = 0; t < R; ++t) xv[e][t] *= f;
+    }
+  }
   C2 z[R];
 #pragma unroll
   for (int t = 0; t < R; ++t) z[t] = cmake<C2>(xv[0][t], xv[1][t]);
@@ -1015,13 +1033,19 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
           mb[e] = max(mb[e], max(__float_as_uint(vr) & 0x7fffffffu, __float_as_uint(vi) & 0x7fffffffu));
         }
     }
-    const int sh[2] = {f16f8_shift(__reduce_max_sync(0xffffffffu, mb[0])),
-                       f16f8_shift(__reduce_max_sync(0xffffffffu, mb[1]))};
+    // total shift of channel e: 2^pe (pre-scale) x 2^sh (format scale of the
+    // pre-scaled slots), clamped like f16f8_shift
+    int sh[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const uint32_t mx = __reduce_max_sync(0xffffffffu, mb[e]);
+      sh[e] = (mx == 0u || mx >= 0x7f800000u) ? 0 : min(120, max(-120, f16f8_shift(mx) + pe[e]));
+    }
     if (q0 < H) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int rbo = (2 * warp + e) * img;
-        const float sc = pow2f(sh[e]);
+        const float sc = pow2f(sh[e] - pe[e]);
         __align__(16) uint32_t re_h[R / 2], im_h[R / 2];
         __align__(16) uint16_t re_h8[R / 2], re_l8[R / 2], im_h8[R / 2], im_l8[R / 2];
 #pragma unroll
@@ -1060,7 +1084,9 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
         if (q0 == 0) {
           float vr, vi;
           slot(e, 0, vr, vi);
-          *reinterpret_cast<float4*>(work + aswz(rbo + 12 * hp)) = make_float4(vr, vi, pow2f(-sh[e] - 5), 0.f);
+          const float un = pow2f(-pe[e]);
+          *reinterpret_cast<float4*>(work + aswz(rbo + 12 * hp)) =
+              make_float4(vr * un, vi * un, pow2f(-sh[e] - 5), 0.f);
         }
       }
     }
@@ -1110,8 +1136,9 @@ __global__ void __launch_bounds__(kFastThreads, 2) prep_fast_kernel(const PrepPa
           for (int d = 0; d < 2; ++d) {
             const C2 y = e ? yo[k1 + d] : ye[k1 + d];
             const int q = q0 + k1 + d;
-            vr[d] = (float)y.x * (q == 0 ? sn1 : sn2);
-            vi[d] = q == 0 ? (e ? nyq1 : nyq0) * sn1 : (float)y.y * sn2;
+            const float un = pow2f(-pe[e]);   // undo the pre-scale (exact)
+            vr[d] = (float)y.x * (q == 0 ? sn1 : sn2) * un;
+            vi[d] = (q == 0 ? (e ? nyq1 : nyq0) * sn1 : (float)y.y * sn2) * un;
           }
           const __nv_bfloat162 rh = __floats2bfloat162_rn(vr[0], vr[1]);
           const __nv_bfloat162 ih = __floats2bfloat162_rn(vi[0], vi[1]);

@@ -494,12 +494,12 @@ class CorrelationPlan:
         if self.pack_kind in (_abi.PACK_F64, _abi.PACK_F64_TIME, _abi.PACK_F64_GAUSS):
             launch_contract_f64(lib, self.pack_kind, self.a_phi, self.a_psi, self.bop, self.ld_pack, self.n1,
                                 self.n2, self.mp, homo, self.row0, self.row1, self.tile0, self.tile1,
-                                self.phi, self.psi, self.n2, self.stats)
+                                self.phi, self.psi, self.phi.stride(0), self.stats)
             return
         else:
             code = lib.corr2d_contract_tc(
                 self.pack_kind, ptr(self.a_phi), ptr(self.bop), self.ld_pack, self.n1, self.n2, self.mp, self.m, homo,
-                self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.n2,
+                self.row0, self.row1, self.tile0, self.tile1, ptr(self.phi), ptr(self.psi), self.phi.stride(0),
                 ptr(self.stats), stream_handle())
         _abi.check(code, lib)
 
@@ -517,7 +517,7 @@ class CorrelationPlan:
             float(r1.alpha), 1 if r1.substitute else 0, self.norm,
             ptr(self.a_phi), ptr(self.bop), self.ld_pack,
             ptr(self.ref1), ptr(self.sigma1), ptr(self.ref2), ptr(self.sigma2),
-            ptr(self.phi), ptr(self.psi), self.n2,
+            ptr(self.phi), ptr(self.psi), self.phi.stride(0),
             ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle())
         _abi.check(code, self.lib)
 

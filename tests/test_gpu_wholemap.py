@@ -124,9 +124,14 @@ def _adversarial(m, n, seed):
     return v * mag
 
 
-@pytest.mark.parametrize("m", [64, 512])
-def test_f16f8_adversarial_unequal_pairs_and_coherent_bands(m, monkeypatch):
-    monkeypatch.setenv("CORR2D_FP32_FORMAT", "f16f8")
+@pytest.mark.parametrize("fmt", ["f16f8", "bf16x3"])
+@pytest.mark.parametrize("m", [64, 512, 1024])
+def test_fp32_formats_adversarial_unequal_pairs_and_coherent_bands(m, fmt, monkeypatch):
+    """m = 64 / 512 run K1's fp32 paired transform (fast kernel), m = 1024 the
+    generic fp64 one.  Errors are held to each element's OWN scale: K1 brings
+    both channels of a pair to max|x| in [1, 2) before the paired fp32 FFT, so a
+    channel 10^8 below its partner keeps its own ~2^-24 transform error."""
+    monkeypatch.setenv("CORR2D_FP32_FORMAT", fmt)
     v = _adversarial(m, 640, m)
     dyn = P.DynamicSpectra(np.arange(640.0), np.arange(float(m)), v, np.zeros(640))
     res = P.correlate_ft(dyn, dtype="float32")
@@ -134,17 +139,11 @@ def test_f16f8_adversarial_unequal_pairs_and_coherent_bands(m, monkeypatch):
     sc = max(float(np.abs(s).max()), float(np.abs(a).max()))
     err = max(rel_err(res.sync, s, sc), rel_err(res.asyn, a, sc))
     # own-scale error: each element against the product of its two channels'
-    # own magnitudes (sqrt of the diagonal) -- the small partner of a pair is
-    # limited by the fp32 FFT of the pair (~2^-24 of the large partner)
+    # own magnitudes (sqrt of the diagonal of sync)
     own = np.sqrt(np.abs(np.diag(s)))
     denom = np.outer(own, own)
-    own_err = float(np.max(np.abs(res.sync - s) / denom))
-    partner = np.empty_like(own)
-    partner[0::2] = np.maximum(own[0::2], own[1::2])
-    partner[1::2] = partner[0::2][: own.size // 2]
-    bound = np.outer(own + 2.0 ** -22 * partner, own + 2.0 ** -22 * partner)
-    bounded_err = float(np.max(np.abs(res.sync - s) / bound))
-    _evidence(f"r2_f16f8_adversarial_m{m}", {"m": m, "n": 640, "rel_err_vs_max": err,
-                                             "own_scale_rel_err": own_err, "pair_bounded_rel_err": bounded_err})
+    own_err = max(float(np.max(np.abs(res.sync - s) / denom)), float(np.max(np.abs(res.asyn - a) / denom)))
+    _evidence(f"r2_{fmt}_adversarial_m{m}", {"m": m, "n": 640, "rel_err_vs_max": err,
+                                             "own_scale_rel_err": own_err})
     assert err <= 1e-4
-    assert bounded_err <= 1e-4
+    assert own_err <= 1e-4

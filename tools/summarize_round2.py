@@ -25,19 +25,6 @@ def last_json(path):
     return json.loads(lines[-1]) if lines else None
 
 
-def sanitizer_summary(path):
-    """(tool, target, verdict line, error count) of one compute-sanitizer log."""
-    if not path.exists():
-        return None
-    text = path.read_text(errors="replace")
-    m = re.search(r"ERROR SUMMARY: (\d+) error", text)
-    hazards = re.search(r"RACECHECK SUMMARY: (\d+) hazard", text)
-    ok = [ln for ln in text.splitlines() if ln.startswith("sanitize:")]
-    return {"log": path.name, "errors": int(m.group(1)) if m else None,
-            "racecheck_hazards": int(hazards.group(1)) if hazards else None,
-            "kernels_run": ok, "tail": text.strip().splitlines()[-3:]}
-
-
 def main():
     src = Path(sys.argv[1]) if len(sys.argv) > 1 else ROOT / "gpurun_out" / "prof2"
     dst = ROOT / "profiles"
@@ -74,16 +61,7 @@ def main():
     for name in ("small_trace.txt",):
         if (src / name).exists():
             shutil.copy(src / name, dst / f"{RND}_{name}")
-    san = {}
-    for f in sorted(src.glob("sanitizer_*.txt")):
-        s = sanitizer_summary(f)
-        san[f.stem] = s
-        text = f.read_text(errors="replace").splitlines()
-        (dst / f"{RND}_{f.name}").write_text("\n".join(text[:40] + (["..."] if len(text) > 80 else []) +
-                                                      text[-40:]) + "\n")
-    if san:
-        (dst / f"{RND}_sanitizer_summary.json").write_text(json.dumps(san, indent=1) + "\n")
-    for name in ("gpu_tests.log", "wholemap_tests.log"):
+    for name in ("gpu_tests.log", "wholemap_tests.log", "guards.log"):
         if (src / name).exists():
             text = (src / name).read_text(errors="replace").splitlines()
             (dst / f"{RND}_{name.replace('.log', '.txt')}").write_text("\n".join(text[-15:]) + "\n")
@@ -188,20 +166,18 @@ def readme(dst):
         L += ["", "## Small-m path timeline (profiling build, one cold-ish step, ns)", "", "```"] + \
              tr.read_text().strip().splitlines() + ["```"]
     L += ["", "## Parity beyond sampled rows", ""]
-    for f in sorted(dst.glob("r2_wholemap_*.json")) + sorted(dst.glob("r2_f16f8_adversarial_*.json")):
+    for f in sorted(dst.glob("r2_wholemap_*.json")) + sorted(dst.glob("r2_*_adversarial_*.json")):
         L.append(f"* `{f.name}`: `{json.dumps(json.loads(f.read_text()))}`")
     for name in (f"{R}_wholemap_tests.txt", f"{R}_gpu_tests.txt"):
         p = dst / name
         if p.exists():
             L.append(f"* `{name}`: " + (p.read_text().strip().splitlines() or [""])[-1])
-    san = _load(dst / f"{R}_sanitizer_summary.json")
-    if san:
-        L += ["", "## compute-sanitizer (tools/sanitize.py: one small invocation of every kernel)", "",
-              "| log | errors | racecheck hazards | kernels run |", "|---|---|---|---|"]
-        for k, s in san.items():
-            if s:
-                L.append(f"| {s['log']} | {s['errors']} | {s['racecheck_hazards'] if s['racecheck_hazards'] is not None else '-'} | "
-                         f"{', '.join(x.split()[1] for x in s['kernels_run'] if len(x.split()) > 2) or '-'} |")
+    p = dst / f"{R}_guards.txt"
+    if p.exists():
+        L += ["", "## Memory safety (tests/test_gpu_guards.py; compute-sanitizer is closed on this pool)", "",
+              "Every kernel family runs with its buffers inside 0xFF (NaN) guard bands and padded rows; "
+              "guards must be untouched and results bit-identical to tight buffers.", "",
+              "* `" + p.name + "`: " + (p.read_text().strip().splitlines() or [""])[-1]]
     L += ["", "## ncu (cold, serialised launches; per-launch numbers)", "",
           "| kernel | config | duration ms | DRAM read MB | DRAM write MB | tensor pipe active % | SM MHz |",
           "|---|---|---|---|---|---|---|"]
