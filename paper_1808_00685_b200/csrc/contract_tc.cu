@@ -890,7 +890,10 @@ __host__ __device__ constexpr uint32_t idesc_bf16_2sm_n128(bool neg_a) {
 // consecutive -- concurrent clusters then share a handful of B column tiles
 // and the group's A rows stay L2-resident (the plain row-major triangle
 // re-streamed every B tile from DRAM once per row pair).
-constexpr int kGroup = 16;
+#ifndef CORR2D_PAIR_GROUP
+#define CORR2D_PAIR_GROUP 16
+#endif
+constexpr int kGroup = CORR2D_PAIR_GROUP;
 
 // pair-tile b -> (row-pair P, column tile J); per-CTA mode for row tile 2P + rank.
 // Homo: row pair P covers columns J in [2P, T); inside group g (pairs gG..gG+Gg-1)

@@ -36,10 +36,13 @@
 namespace corr2d {
 
 constexpr int kSB = 64;          // output block edge (rows and columns)
+#ifndef CORR2D_SMALL_MINB
+#define CORR2D_SMALL_MINB 2      // contraction CTAs per SM (register budget)
+#endif
 constexpr int kSThreads = 128;   // 4 warps: one lane per K1 channel, 32 x 32 warp tiles
 constexpr int kSMaxM = 32;
-constexpr int kYS = 132;         // sample rows [t][channel]: stride = 4 mod 16 doubles (conflict-free B fragments)
 constexpr int kCS = kSB + 1;     // epilogue staging stride
+constexpr int kYS = 132;         // sample rows [t][channel]: stride = 4 mod 16 doubles (conflict-free B fragments)
 
 struct SmallParams {
   const void* raw1;
@@ -379,23 +382,29 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
   // (ld_ops = 3 kg: the warp's 32 rows are one contiguous run), then leave as
   // coalesced 16-byte stores.
   const int ns = 3 * p.kg;
+  // the warp's 32 rows staged in their global layout (ld_ops = ns: ONE
+  // contiguous run), then one bulk copy per role
   double* stA = tab + 48 * mpad + 5 * ns + (size_t)warp * 32 * ns;   // [32][ns] per warp
   double* stB = stA + (size_t)kSThreads * ns;
   const bool wantA = !set, wantB = set || p.homo;
   {
-    // zero the lane's staged rows (pad slots), then every bin's three Gauss
-    // slots from registers: no table lookups, no dependent loads
-    double2* zA = reinterpret_cast<double2*>(stA + lane * ns);
-    double2* zB = reinterpret_cast<double2*>(stB + lane * ns);
-    for (int i = 0; i < ns / 2; ++i) zA[i] = zB[i] = make_double2(0.0, 0.0);
+    // pads are zero: the warp zeroes its run with consecutive 16-B stores
+    double2* zA = reinterpret_cast<double2*>(stA);
+    double2* zB = reinterpret_cast<double2*>(stB);
+    for (int i = lane; i < 16 * ns; i += 32) zA[i] = zB[i] = make_double2(0.0, 0.0);
+    __syncwarp();
+    // every bin's three Gauss slots from registers.  Lane l takes the bins in
+    // the rotated order w = (it + l) mod (H + 1), so the 32 lanes' rows (pitch
+    // ns) are written at different slots: few bank conflicts
     const int kg = p.kg, H = m / 2, Iint = gauss_interior(m);
     const double nrm = p.norm;
     double* a = stA + lane * ns;
     double* b = stB + lane * ns;
+    int w = lane % (H + 1);
     // a runtime loop: straight-line code is fetched cold, line by line, on
     // every step of a stream that evicts L2 (the bench's rotation does)
 #pragma unroll 1
-    for (int w = 0; w <= H; ++w) {
+    for (int it = 0; it <= H; ++it, w = (w == H) ? 0 : w + 1) {
       const double R = ys[(2 * w) * kYS + tid];
       const double I = (w == 0 || 2 * w == m) ? 0.0 : ys[(2 * w + 1) * kYS + tid];
       const double k = (w == 0 || 2 * w == m) ? 1.0 : 2.0;
@@ -410,20 +419,23 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
       }
     }
   }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> bulk copy
   __syncwarp();
+  SMALL_STAMP(0, 7);
   {
     const int cw = c - lane;                         // the warp's first channel
     const int nrow = min(32, n - cw);
-    if (nrow > 0) {
-      const int pieces = nrow * ns / 2;              // 16-byte pieces of the warp's rows
-      double2* gA = reinterpret_cast<double2*>(p.opsA + (long long)cw * p.ld_ops);
-      double2* gB = reinterpret_cast<double2*>(p.opsB + (long long)cw * p.ld_ops);
-      const double2* sA = reinterpret_cast<const double2*>(stA);
-      const double2* sB = reinterpret_cast<const double2*>(stB);
-      for (int i = lane; i < pieces; i += 32) {
-        if (wantA) gA[i] = sA[i];
-        if (wantB) gB[i] = sB[i];
-      }
+    if (nrow > 0 && lane == 0) {
+      const unsigned bytes = (unsigned)(nrow * ns) * 8u;
+      if (wantA)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(p.opsA + (long long)cw * p.ld_ops),
+                       "r"(static_cast<unsigned>(__cvta_generic_to_shared(stA))), "r"(bytes) : "memory");
+      if (wantB)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(p.opsB + (long long)cw * p.ld_ops),
+                       "r"(static_cast<unsigned>(__cvta_generic_to_shared(stB))), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;\n" ::: "memory");
     }
   }
   SMALL_STAMP(0, 5);
@@ -433,7 +445,7 @@ __device__ __noinline__ void small_publish(const SmallParams& p, unsigned long l
                                            int lane, int warp, int tid);
 
 // ---- contraction: one CTA per 64 x 64 output block ----
-__global__ void __launch_bounds__(kSThreads, 2) small_contract_kernel(const __grid_constant__ SmallParams p) {
+__global__ void __launch_bounds__(kSThreads, CORR2D_SMALL_MINB) small_contract_kernel(const __grid_constant__ SmallParams p) {
   extern __shared__ __align__(16) double sm[];
   const int ks = p.ks, kg = p.kg;
   double* As = sm;                                   // [64][ks]
@@ -816,7 +828,7 @@ extern "C" int corr2d_correlate_small_f64(
                          (int)(worst_ops > stage ? worst_ops : stage));
     cudaFuncSetAttribute(small_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16 + 2 * kSThreads * 48) *
-                               sizeof(double)));
+                               sizeof(double)));   // m = 32: kg = 16
     attr_set = true;
   }
   // programmatic dependent launch for both grids: each launches while its
@@ -854,9 +866,10 @@ extern "C" int corr2d_correlate_small_f64(
       fprintf(stderr, "  %-22s min %8.0f  med %8.0f  max %8.0f ns\n", name, v.front(), v[v.size() / 2], v.back());
     };
     fprintf(stderr, "small path trace (m %d, %d x %d, %s):\n", m, n1, n2, homo ? "homo" : "hetero");
-    const char* k1n[6] = {"K1 start", "K1 after wait", "K1 samples in", "K1 stats done", "K1 dft done", "K1 rows written"};
+    const char* k1n[8] = {"K1 start", "K1 after wait", "K1 samples in", "K1 stats done", "K1 dft done",
+                          "K1 rows written", "", "K1 slots staged"};
     const char* k2n[6] = {"K2 start", "K2 after wait", "K2 operands in", "K2 mma done", "K2 stores issued", "K2 end"};
-    for (int k = 0; k < 6; ++k) row(k1n[k], 0, prep_blocks, k);
+    for (int k : {0, 1, 2, 3, 4, 7, 5}) row(k1n[k], 0, prep_blocks, k);
     for (int k = 0; k < 6; ++k) row(k2n[k], kTraceK1, (int)blocks, k);
   }
 #endif

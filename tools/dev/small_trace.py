@@ -25,3 +25,28 @@ for cfg in (1, 2):
     plans[-1].launch()
     torch.cuda.synchronize()
     os.environ["CORR2D_SMALL_TRACE"] = "0"
+
+# the same plan back to back (its operand rows and code warm in L2), then one
+# traced step after an idle gap (the previous step's output drain finished)
+import time
+for cfg in (1, 2):
+    case = configs.make(cfg)
+    s1 = case.set1
+    ds1 = P.SpectralDataset(s1.spectral_axis, s1.perturbation_axis, s1.intensities)
+    ds2 = None if case.set2 is None else P.SpectralDataset(case.set2.spectral_axis, case.set2.perturbation_axis,
+                                                          case.set2.intensities)
+    plan = api.build_plan(ds1, ds2, P.PreprocessSpec())[0]
+    for _ in range(5):
+        plan.launch()
+    torch.cuda.synchronize()
+    for label, gap in (("warm, back to back", False), ("warm, after idle", True)):
+        for _ in range(3):
+            plan.launch()
+        if gap:
+            torch.cuda.synchronize()
+            time.sleep(0.01)
+        print(f"cfg{cfg} {label}:", file=sys.stderr, flush=True)
+        os.environ["CORR2D_SMALL_TRACE"] = "1"
+        plan.launch()
+        torch.cuda.synchronize()
+        os.environ["CORR2D_SMALL_TRACE"] = "0"
