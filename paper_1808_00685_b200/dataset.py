@@ -4,7 +4,8 @@
 invariants and error messages.  Differences, all opt-in:
 
 * ``SpectralDataset(..., dtype=np.float32)`` keeps single-precision storage for
-  the fp32 (bf16x3 tensor-core) path; the default is float64 like the reference.
+  the fp32 tensor-core path (F16F8 by default, bf16x3 optional); the default is
+  float64 like the reference.
 * ``CorrelationSpectra`` built by the GPU engine skips the O(n^2) host
   re-validation (dataset.py:141-170): symmetry/skew-symmetry hold by
   construction (mirrored tiles) and finiteness was checked on the device in the

@@ -28,6 +28,9 @@ for c in 3 4; do
   done
 done
 CORR2D_LIB=_variants/libcorr2d_prof.so timeout 300 python tools/dev/small_trace.py > $OUT/small_trace.txt 2>&1
+# cfg5 power decomposition (sustained, clocks / power sampled): full, no stores,
+# MMA only, stores only (profiling build)
+CORR2D_LIB=_variants/libcorr2d_prof.so timeout 600 python tools/ab_power.py 0 1 5 6 > $OUT/power_cfg5.txt 2>&1
 # 5. memory-safety: guard-band tests (compute-sanitizer is closed on this pool)
 timeout 900 python -m pytest tests/test_gpu_guards.py -q -rA > $OUT/guards.log 2>&1
 # 6. ncu: launch lists of the bench commands, full captures of the hot kernels

@@ -58,7 +58,7 @@ def main():
                       "profiling build (-DCORR2D_PROFILING) with CORR2D_DEBUG_SKIP=1 (no output stores), "
                       "2 (no MMAs), 3 (neither: operand loads + epilogue arithmetic only)")
         (dst / f"{RND}_f64_decomposition.json").write_text(json.dumps(dec, indent=1) + "\n")
-    for name in ("small_trace.txt",):
+    for name in ("small_trace.txt", "power_cfg5.txt"):
         if (src / name).exists():
             shutil.copy(src / name, dst / f"{RND}_{name}")
     for name in ("gpu_tests.log", "wholemap_tests.log", "guards.log"):
