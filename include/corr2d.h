@@ -238,6 +238,9 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  * be inside a CUDA graph capture).
  */
 int64_t corr2d_small_block_count(int n1, int n2, int homo);
+/* Kernels one corr2d_correlate_small_f64 call launches on the current device:
+ * 1 (the fused kernel: blocks <= SMs) or 2 (K1 + contraction); -1 on bad sizes. */
+int corr2d_small_launches(int n1, int n2, int homo);
 int corr2d_small_ops_depth(int m);
 int corr2d_correlate_small_f64(
     int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,

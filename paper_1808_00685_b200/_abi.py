@@ -30,7 +30,7 @@ EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
     "corr2d_contract_tc", "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
-    "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count", "corr2d_small_ops_depth",
+    "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count", "corr2d_small_launches", "corr2d_small_ops_depth",
     "corr2d_correlate_small_f64",
 )
 
@@ -87,6 +87,8 @@ def _declare(lib):
                                        ctypes.c_char, c_int, c_int, c_void, c_i64, c_void]
     lib.corr2d_small_block_count.argtypes = [c_int, c_int, c_int]
     lib.corr2d_small_block_count.restype = c_i64
+    lib.corr2d_small_launches.argtypes = [c_int, c_int, c_int]
+    lib.corr2d_small_launches.restype = c_int
     lib.corr2d_small_ops_depth.argtypes = [c_int]
     lib.corr2d_correlate_small_f64.argtypes = [
         c_int, c_void, c_i64, c_void, c_i64,          # in_dtype raw1 ld_raw1 raw2 ld_raw2

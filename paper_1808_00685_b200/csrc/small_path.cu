@@ -27,9 +27,14 @@
 // engine_core.py:139-140 (finite check), dataset.py:159-170 (homo symmetry).
 #include "prep_params.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstring>
+#include <string>
 #include <mutex>
 #include <vector>
 
@@ -742,6 +747,852 @@ static const double* dft_table(int m, int mpad, cudaStream_t st, int* rc) {
   return d;
 }
 
+// =====================================================================
+// The fused small-m path (default): ONE persistent kernel, no operand rows in
+// global memory and no kernel boundary between the per-channel work and the
+// contraction.  CTA c owns a contiguous run of the 64 x 64 output blocks
+// (homo: the upper triangle, row by row) and, per block,
+//   * loads the raw samples of the block's 64 row channels (only when the
+//     row block changes) and 64 column channels (cp.async, prefetched during
+//     the previous block's contraction),
+//   * centres / scales them in the reference's order (lane per channel),
+//   * turns them into the CORR2D_PACK_F64_GAUSS operand rows with ONE FP64
+//     tensor-core product per role: rows[ch][s] = sum_t y[t][ch] G[s][t], G the
+//     DFT rows already combined into the three Gauss segments (the rfft of
+//     fourier.py:73 and the slot algebra of gauss_values, folded on the host),
+//   * contracts them (two accumulator chains) and stages both planes in shared
+//     memory, from where they leave by bulk asynchronous copies (one per row):
+//     no warp ever waits on its own output stores, so the next block's loads,
+//     centring and DMMAs overlap the previous block's HBM write stream.
+// Status / stat words: owner CTAs (tile (I, first column) for the rows, tile
+// (0, J) for a hetero column block) report each channel's status once; the
+// last CTA to arrive (an arrival counter, never a wait) publishes and
+// re-zeroes the accumulators.
+// =====================================================================
+constexpr int kFYP = 68;   // sample pitch (doubles): [t][64 channels + 4]
+constexpr int kWFStat1 = 0, kWFStat2 = 4, kWFAcc = 8 /* 3 x u64 at byte 32 */, kWFCount = 14;
+
+struct FusedParams {
+  const void* raw1;
+  const void* raw2;
+  long long ld1, ld2;
+  int in_f32;
+  int al1, al2;             // fp64 rows of raw1 / raw2 16-B aligned (16-byte sample copies)
+  int mirror_buf;           // homo: a second staging buffer for the mirrored block
+  int m, mpad, gp, n1, n2, homo;
+  int ref_mode1, ref_mode2;
+  const double* ref_in1;
+  const double* ref_in2;
+  const double* sigma_in1;
+  const double* sigma_in2;
+  double alpha;
+  int substitute;
+  double norm;
+  double* ref_out1;
+  double* sigma_out1;
+  double* ref_out2;
+  double* sigma_out2;
+  const double* G;          // [2][nsp][gp]: role-A rows (x Norm in the kernel), then role-B rows
+  int kg, ns, nsp, ks;      // Gauss slots per segment, 3 kg, 3 kg rounded to 8, operand row pitch
+  int T1, T2;
+  long long tiles;
+  int nctas;
+  double* phi;
+  double* psi;
+  long long ld_out;
+  int vec;
+  int* status1;
+  int* status2;
+  unsigned long long* stats;
+  int* work;
+  unsigned long long* trace;
+};
+
+__device__ __forceinline__ void fused_decode(const FusedParams& p, long long b, int& I, int& J) {
+  if (!p.homo) {
+    I = (int)(b / p.T2);
+    J = (int)(b - (long long)I * p.T2);
+    return;
+  }
+  const long long T = p.T1;
+  const long long t2 = 2 * T + 1;
+  const long long disc = t2 * t2 - 8 * b;
+  long long d = (long long)((float)t2 - sqrtf((float)(disc > 0 ? disc : 0))) / 2;
+  auto S = [&](long long dd) { return dd * T - dd * (dd - 1) / 2; };
+  if (d < 0) d = 0;
+  while (d > 0 && S(d) > b) --d;
+  while (S(d + 1) <= b) ++d;
+  I = (int)d;
+  J = I + (int)(b - S(d));
+}
+
+// first tile of row block I in the enumeration (homo: the diagonal block)
+__device__ __forceinline__ long long fused_row_start(const FusedParams& p, int I) {
+  const long long d = I;
+  return p.homo ? d * p.T1 - d * (d - 1) / 2 : d * p.T2;
+}
+
+#ifdef CORR2D_PROFILING
+#define FUSED_STAMP(k)                                                                         \
+  do {                                                                                         \
+    if (p.trace && threadIdx.x == 0) {                                                         \
+      unsigned long long t_;                                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+      p.trace[8 * blockIdx.x + (k)] = t_;                                                      \
+    }                                                                                          \
+  } while (0)
+#else
+#define FUSED_STAMP(k) do { } while (0)
+#endif
+
+// Raw samples of 64 channels [c0, c0 + 64) of dataset `set` -> ys[t][ch]
+// (cp.async, zero-filled past n; fp32 inputs land in the low half of the slot).
+__device__ __forceinline__ void fused_load(const FusedParams& p, int set, int c0, double* ys) {
+  const int n = set ? p.n2 : p.n1;
+  const long long ld = set ? p.ld2 : p.ld1;
+  const void* raw = set ? p.raw2 : p.raw1;
+  const int tid = threadIdx.x;
+  if (!p.in_f32 && (set ? p.al2 : p.al1) && c0 + 64 <= n) {
+    // whole block, 16-B aligned rows: a thread copies channel pairs of rows t, t + 4, ...
+    const double* src = static_cast<const double*>(raw) + c0 + 2 * (tid & 31) + (long long)(tid >> 5) * ld;
+    unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + 2 * (tid & 31) + (tid >> 5) * kFYP));
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+#pragma unroll 1
+    for (int t = tid >> 5; t < p.m; t += 4, src += 4 * ld, dst += 8u * 4 * kFYP)
+      asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "l"(pol)
+                   : "memory");
+  } else {
+    const int total = p.m * 64;
+#pragma unroll 1
+    for (int idx = tid; idx < total; idx += kSThreads) {
+      const int t = idx >> 6, ch = idx & 63, c = c0 + ch;
+      const bool v = c < n;
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + t * kFYP + ch));
+      if (p.in_f32) {
+        const float* src = static_cast<const float*>(raw) + (long long)t * ld + (v ? c : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 4 : 0) : "memory");
+      } else {
+        const double* src = static_cast<const double*>(raw) + (long long)t * ld + (v ? c : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0) : "memory");
+      }
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
+// One channel's statistics and dynamic values in place in its column
+// ys[t * kFYP] -- the IEEE operations of the other K1 kernels in the
+// reference's order (preprocess.py:123-137, :198-259).  The owner lane reports
+// status / reference / sigma.
+__device__ __noinline__ void fused_f32_column(double* ys, int m) {
+  for (int t = 0; t < m; ++t) ys[t * kFYP] = (double)reinterpret_cast<const float*>(ys + t * kFYP)[0];
+}
+
+// sigma about ref (preprocess.py:198-211) -> the division scale sigma**alpha
+// (:214-259), in place; the owner lane reports sigma and zero variance.
+__device__ __noinline__ void fused_scale_column(const FusedParams& p, int set, int c, bool valid, bool report,
+                                                double ref, bool sub, double* ys) {
+  const int m = p.m;
+  const double* sigma_in = set ? p.sigma_in2 : p.sigma_in1;
+  int* status = p.work + (set ? kWFStat2 : kWFStat1);
+  double sigma;
+  if (sigma_in) {
+    sigma = valid ? __ldg(sigma_in + c) : 1.0;
+  } else {
+    double ss = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double d = __dsub_rn(ys[t * kFYP], ref);
+      ss = __dadd_rn(ss, __dmul_rn(d, d));
+    }
+    sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
+  }
+  if (report) {
+    double* so = set ? p.sigma_out2 : p.sigma_out1;
+    if (so) so[c] = sigma;
+    if (sigma == 0.0) {
+      atomicAdd(&status[CORR2D_ST_ZEROVAR], 1);
+      atomicMax(&status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - c);
+      __threadfence();
+    }
+  }
+  if (sigma == 0.0 && p.substitute) sigma = 1.0;
+  const double scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
+  for (int t = 0; t < m; ++t) {
+    double v = ys[t * kFYP];
+    if (sub) v = __dsub_rn(v, ref);
+    ys[t * kFYP] = valid ? __ddiv_rn(v, scale) : 0.0;
+  }
+}
+
+// One channel's statistics and dynamic values in place in its column
+// ys[t * kFYP] -- the IEEE operations of the other K1 kernels in the
+// reference's order (preprocess.py:123-137, :198-259).  The owner lane reports
+// status / reference / sigma.  Scaling and fp32 inputs are out of line.
+__device__ __forceinline__ void fused_stats(const FusedParams& p, int set, int c, bool valid, bool owner,
+                                            double* ys) {
+  const int m = p.m;
+  if (p.in_f32) fused_f32_column(ys, m);
+  const int ref_mode = set ? p.ref_mode2 : p.ref_mode1;
+  double ref = 0.0;
+  int bad = 0;
+  double sum = 0.0;                                    // left to right (numpy's axis-0 order)
+#pragma unroll 4
+  for (int t = 0; t < m; ++t) {
+    const double v = ys[t * kFYP];
+    bad += (unsigned)(__double2hiint(v) & 0x7ff00000) == 0x7ff00000u;   // !isfinite, integer pipe
+    sum = __dadd_rn(sum, v);
+  }
+  const bool report = owner && valid;
+  if (report && bad) {
+    atomicAdd(&p.work[(set ? kWFStat2 : kWFStat1) + CORR2D_ST_NONFINITE], bad);
+    __threadfence();
+  }
+  if (ref_mode == CORR2D_REF_PROVIDED) {
+    ref = valid ? __ldg((set ? p.ref_in2 : p.ref_in1) + c) : 0.0;
+  } else if (ref_mode == CORR2D_REF_MEAN) {
+    ref = __ddiv_rn(sum, (double)m);
+  }
+  if (report && ref_mode != CORR2D_REF_NONE) {
+    double* ro = set ? p.ref_out2 : p.ref_out1;
+    if (ro) ro[c] = ref;
+  }
+  const bool sub = ref_mode != CORR2D_REF_NONE;
+  if (p.alpha > 0.0) {
+    fused_scale_column(p, set, c, valid, report, ref, sub, ys);
+    return;
+  }
+#pragma unroll 4
+  for (int t = 0; t < m; ++t) {
+    const double v = ys[t * kFYP];
+    ys[t * kFYP] = valid ? (sub ? __dsub_rn(v, ref) : v) : 0.0;
+  }
+}
+
+// Compile-time shape of the Gauss rows for KG slots per segment (KG = gauss_kg(m)
+// in {4, 8, 12, 16}): NS = 3 KG slots, padded to NSP (whole 8-column DMMA tiles),
+// operand row pitch KS = NSP + 4 doubles (conflict-free fragment loads).
+template <int KG>
+struct FShape {
+  static constexpr int NS = 3 * KG, NSP = (NS + 7) / 8 * 8, NNT = NSP / 8, KS = NSP + 4;
+};
+
+// Gauss operand rows of 64 channels: out[ch][s] = scale * sum_t ys[t][ch] G[s][t]
+// on the FP64 tensor pipe (warp w: channels 16 w .. 16 w + 15, all slots).
+template <int KG>
+__device__ __forceinline__ void fused_transform(int mpad, int gp, const double* ys, const double* Gt, double* out,
+                                                double scale, int warp, int lr, int lk) {
+  using S = FShape<KG>;
+  double acc[S::NNT][4];
+#pragma unroll
+  for (int a = 0; a < S::NNT; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[a][q] = 0.0;
+  const int ch = 16 * warp + lr;
+  const double* y = ys + lk * kFYP + ch;
+  const double* g = Gt + lr * gp + lk;
+#pragma unroll 2
+  for (int kk = 0; kk < mpad; kk += 4) {
+    const double a0 = y[kk * kFYP];
+    const double a1 = y[kk * kFYP + 8];
+#pragma unroll
+    for (int nt = 0; nt < S::NNT; ++nt) dmma(acc[nt], a0, a1, g[nt * 8 * gp + kk]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < S::NNT; ++nt) {
+    const int c = nt * 8 + 2 * lk;
+    *reinterpret_cast<double2*>(out + ch * S::KS + c) = make_double2(acc[nt][0] * scale, acc[nt][1] * scale);
+    *reinterpret_cast<double2*>(out + (ch + 8) * S::KS + c) = make_double2(acc[nt][2] * scale, acc[nt][3] * scale);
+  }
+}
+
+// Both roles at once (independent accumulator chains interleaved): A rows
+// (x scaleA) from ysA, B rows from ysB.
+template <int KG>
+__device__ __forceinline__ void fused_transform2(int mpad, int gp, const double* ysA, const double* GA, double* outA,
+                                                 double scaleA, const double* ysB, const double* GB, double* outB,
+                                                 int warp, int lr, int lk) {
+  using S = FShape<KG>;
+  double acc[2][S::NNT][4];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int a = 0; a < S::NNT; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[r][a][q] = 0.0;
+  const int ch = 16 * warp + lr;
+  const double* ya = ysA + lk * kFYP + ch;
+  const double* yb = ysB + lk * kFYP + ch;
+  const double* ga = GA + lr * gp + lk;
+  const double* gb = GB + lr * gp + lk;
+#pragma unroll 1
+  for (int kk = 0; kk < mpad; kk += 4) {
+    const double a0 = ya[kk * kFYP], a1 = ya[kk * kFYP + 8];
+    const double c0 = yb[kk * kFYP], c1 = yb[kk * kFYP + 8];
+#pragma unroll
+    for (int nt = 0; nt < S::NNT; ++nt) {
+      dmma(acc[0][nt], a0, a1, ga[nt * 8 * gp + kk]);
+      dmma(acc[1][nt], c0, c1, gb[nt * 8 * gp + kk]);
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < S::NNT; ++nt) {
+    const int c = nt * 8 + 2 * lk;
+    *reinterpret_cast<double2*>(outA + ch * S::KS + c) = make_double2(acc[0][nt][0] * scaleA, acc[0][nt][1] * scaleA);
+    *reinterpret_cast<double2*>(outA + (ch + 8) * S::KS + c) = make_double2(acc[0][nt][2] * scaleA, acc[0][nt][3] * scaleA);
+    *reinterpret_cast<double2*>(outB + ch * S::KS + c) = make_double2(acc[1][nt][0], acc[1][nt][1]);
+    *reinterpret_cast<double2*>(outB + (ch + 8) * S::KS + c) = make_double2(acc[1][nt][2], acc[1][nt][3]);
+  }
+}
+
+// KG/4 k-steps of one Gauss segment into one accumulator set (32 x 32 warp tile).
+template <int KG>
+__device__ __forceinline__ void fused_seg1(double (&acc)[2][4][4], const double* A, const double* B) {
+  constexpr int KS = FShape<KG>::KS;
+#pragma unroll
+  for (int kk = 0; kk < KG; kk += 4) {
+    double ap[2][2], bf[4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      ap[mt][0] = A[(mt * 16) * KS + kk];
+      ap[mt][1] = A[(mt * 16 + 8) * KS + kk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = B[(nt * 8) * KS + kk];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], ap[mt][0], ap[mt][1], bf[nt]);
+  }
+}
+// Two segments (operand offsets o0 / o1) into two accumulator sets, interleaved:
+// 16 independent DMMAs per warp and k-step.
+template <int KG>
+__device__ __forceinline__ void fused_seg2(double (&acc0)[2][4][4], double (&acc1)[2][4][4], const double* A,
+                                           const double* B, int o0, int o1) {
+  constexpr int KS = FShape<KG>::KS;
+#pragma unroll
+  for (int kk = 0; kk < KG; kk += 4) {
+    double a0[2][2], a1[2][2], b0[4], b1[4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      a0[mt][0] = A[(mt * 16) * KS + o0 + kk];
+      a0[mt][1] = A[(mt * 16 + 8) * KS + o0 + kk];
+      a1[mt][0] = A[(mt * 16) * KS + o1 + kk];
+      a1[mt][1] = A[(mt * 16 + 8) * KS + o1 + kk];
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      b0[nt] = B[(nt * 8) * KS + o0 + kk];
+      b1[nt] = B[(nt * 8) * KS + o1 + kk];
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        dmma(acc0[mt][nt], a0[mt][0], a0[mt][1], b0[nt]);
+        dmma(acc1[mt][nt], a1[mt][0], a1[mt][1], b1[nt]);
+      }
+  }
+}
+
+// Staging of one 64 x 64 fp64 plane as the four 64-row x 16-column boxes of a
+// SWIZZLE_128B tensor map (box q = columns 16 q .. 16 q + 15; the 16-byte
+// chunk of each 128-B box row XORed with the row): conflict-free fragment
+// writes, and one TMA tensor store per box.
+__device__ __forceinline__ int swz(int r, int c) {
+  return ((c >> 4) << 10) + (r << 4) + ((((c >> 1) & 7) ^ (r & 7)) << 1) + (c & 1);
+}
+
+// The planes stream out with an evict-first L2 policy, so they do not push the
+// raw samples (re-read by every block of a row / column) out of L2.
+__device__ __forceinline__ void tma_store_box(const CUtensorMap* map, unsigned src, int col, int row, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;\n"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(row), "r"(src), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
+// Both staged planes (8 boxes at shared address S) -> output rows r0..,
+// columns c0.. (TMA clips the boxes at the map's edges).  One thread.
+__device__ __forceinline__ void fused_store_tile(const CUtensorMap* mphi, const CUtensorMap* mpsi, unsigned S,
+                                                 int r0, int c0) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    tma_store_box(mphi, S + q * 8192, c0 + 16 * q, r0, pol);
+    tma_store_box(mpsi, S + 32768 + q * 8192, c0 + 16 * q, r0, pol);
+  }
+  bulk_commit();
+}
+
+// max |.| bit patterns over the in-map fragment elements of an edge or
+// diagonal block (diagonal: r <= c for sync, r < c for async).
+__device__ __forceinline__ void fused_max_edge(const double (&aphi)[2][4][4], const double (&apsi)[2][4][4], int rows,
+                                            int cols, bool diag, int wm, int wn, int lr, int lk,
+                                            unsigned long long& mphi, unsigned long long& mpsi) {
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+        const bool in = r < rows && c < cols;
+        const unsigned long long f = abs_bits(aphi[mt][nt][q]), s = abs_bits(apsi[mt][nt][q]);
+        if (in && (!diag || r <= c)) mphi = max(mphi, f);
+        if (in && (!diag || r < c)) mpsi = max(mpsi, s);
+      }
+}
+
+__device__ __noinline__ void fused_publish(const FusedParams& p, unsigned long long mphi, unsigned long long mpsi,
+                                           int lane, int warp, int tid);
+
+template <int KG>
+__global__ void __launch_bounds__(kSThreads, 1)
+small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant__ CUtensorMap map_phi,
+                   const __grid_constant__ CUtensorMap map_psi) {
+  using SH = FShape<KG>;
+  constexpr int KS = SH::KS;
+  extern __shared__ __align__(1024) double sm_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1;
+  // staging first, at a 1024-B boundary (SWIZZLE_128B boxes); every region is
+  // an offset into the shared array (shared-window loads and stores, no
+  // generic addressing)
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm_raw));
+  double* Cst = sm_raw + (((1024u - (sbase & 1023u)) & 1023u) >> 3);
+  double* const Cst0 = Cst;
+  const unsigned cst_s = static_cast<unsigned>(__cvta_generic_to_shared(Cst));
+  double* const Cmir = Cst + 8192;                     // mirror staging (homo, when it fits)
+  const unsigned cmir_s = cst_s + 65536u;
+  const int gp = p.gp, mpad = p.mpad;
+  double* Gs = Cst + (p.mirror_buf ? 16384 : 8192);    // [2][NSP][gp]
+  double* YA = Gs + 2 * SH::NSP * gp;                  // [mpad][kFYP]
+  double* YB = YA + mpad * kFYP;
+  double* As = YB + mpad * kFYP;                       // [64][KS]
+  double* Bs = As + 64 * KS;
+  const long long b0 = (long long)blockIdx.x * p.tiles / p.nctas;
+  const long long b1 = (long long)(blockIdx.x + 1) * p.tiles / p.nctas;
+  FUSED_STAMP(0);
+  if (tid == 0 && p.vec) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_phi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_psi)) : "memory");
+  }
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // earlier kernels' writes visible, their reads done
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  FUSED_STAMP(1);
+  {
+    const int nt = SH::NSP * gp;                       // 16-byte pieces of both tables
+    for (int i = tid; i < nt; i += kSThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
+                   ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(Gs + 2 * i))), "l"(p.G + 2 * i) : "memory");
+    for (int i = tid; i < (mpad - p.m) * 64; i += kSThreads) {   // sample rows past m stay zero
+      const int t = p.m + (i >> 6), ch = i & 63;
+      YA[t * kFYP + ch] = 0.0;
+      YB[t * kFYP + ch] = 0.0;
+    }
+  }
+  int I, J;
+  fused_decode(p, b0, I, J);
+  fused_load(p, 0, I * kSB, YA);
+  bool diag = p.homo && I == J;
+  if (!diag) fused_load(p, p.homo ? 0 : 1, J * kSB, YB);
+  int curI = -1;
+  unsigned long long mphi = 0, mpsi = 0;
+  const double* Aw = As + (wm * 32 + lr) * KS + lk;    // this lane's operand fragment bases
+  const double* Bw = Bs + (wn * 32 + lr) * KS + lk;
+#pragma unroll 1
+  for (long long b = b0; b < b1; ++b) {
+    const bool newA = I != curI;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();                                   // this block's samples (and the tables) landed
+    if (b == b0) FUSED_STAMP(2);
+    // ---- centring / scaling: threads 0..63 the row channels, 64..127 the column channels
+    if (tid < 64) {
+      if (newA) {
+        const int c = I * kSB + tid;
+        fused_stats(p, 0, c, c < p.n1, fused_row_start(p, I) >= b0, YA + tid);
+      }
+    } else if (!diag) {
+      const int c = J * kSB + tid - 64;
+      const int set = p.homo ? 0 : 1;
+      const int n = set ? p.n2 : p.n1;
+      fused_stats(p, set, c, c < n, !p.homo && I == 0, YB + tid - 64);
+    }
+    __syncthreads();
+    // ---- operand rows: role A (x Norm) of the row channels, role B of the
+    //      column channels (a diagonal block: of the same channels)
+    if (newA)
+      fused_transform2<KG>(mpad, gp, YA, Gs, As, p.norm, diag ? YA : YB, Gs + SH::NSP * gp, Bs, warp, lr, lk);
+    else
+      fused_transform<KG>(mpad, gp, YB, Gs + SH::NSP * gp, Bs, 1.0, warp, lr, lk);
+    __syncthreads();                                   // operand rows ready, sample buffers free
+    if (b == b0) FUSED_STAMP(3);
+    const int i0 = I * kSB, j0 = J * kSB;
+    const bool mirror = p.homo && !diag;
+    curI = I;
+    // ---- prefetch the next block's samples (overlaps this block's contraction and stores)
+    int nI = I, nJ = J;
+    bool ndiag = diag;
+    if (b + 1 < b1) {
+      fused_decode(p, b + 1, nI, nJ);
+      ndiag = p.homo && nI == nJ;
+      if (nI != I) fused_load(p, 0, nI * kSB, YA);
+      if (!ndiag) fused_load(p, p.homo ? 0 : 1, nJ * kSB, YB);
+    }
+    // ---- Gauss contraction: sync = P1 - P3, async = P1 + P2
+    double aphi[2][4][4], apsi[2][4][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) aphi[a][q][e] = apsi[a][q][e] = 0.0;
+    fused_seg2<KG>(apsi, aphi, Aw, Bw, 0, 2 * KG);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) aphi[a][q][e] += apsi[a][q][e];
+    fused_seg1<KG>(apsi, Aw + KG, Bw + KG);
+    if (b == b0) FUSED_STAMP(4);
+    // ---- max|.| / finite check from the fragments, on |x|'s bit pattern
+    //      (integer pipe; Inf / NaN patterns exceed every finite one, so the
+    //      maxima also carry the finite check).  Diagonal blocks: the upper
+    //      triangle, which is what gets stored.
+    const int rows = min(kSB, p.n1 - i0), cols = min(kSB, p.n2 - j0);
+    if (!diag && rows == kSB && cols == kSB) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            mphi = max(mphi, abs_bits(aphi[mt][nt][q]));
+            mpsi = max(mpsi, abs_bits(apsi[mt][nt][q]));
+          }
+    } else {
+      fused_max_edge(aphi, apsi, rows, cols, diag, wm, wn, lr, lk, mphi, mpsi);
+    }
+    // ---- stage both planes (the previous block's stores must have read the staging)
+    if (tid == 0) bulk_wait_read();
+    __syncthreads();
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm * 32 + mt * 16 + lr + 8 * h, c = wn * 32 + nt * 8 + 2 * lk;
+          const int o = swz(r, c);
+          *reinterpret_cast<double2*>(Cst + o) = make_double2(aphi[mt][nt][2 * h], aphi[mt][nt][2 * h + 1]);
+          *reinterpret_cast<double2*>(Cst + 4096 + o) = make_double2(apsi[mt][nt][2 * h], apsi[mt][nt][2 * h + 1]);
+        }
+    if (diag) {        // below the diagonal: the transpose of the upper triangle (exact symmetry)
+      __syncthreads();
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+            if (r < c) {
+              const int o = swz(c, r);
+              Cst[o] = aphi[mt][nt][q];
+              Cst[4096 + o] = neg_bits(apsi[mt][nt][q]);
+            } else if (r == c) {
+              Cst[4096 + swz(r, r)] = 0.0;
+            }
+          }
+    }
+    if (b == b0) FUSED_STAMP(5);
+    if (p.vec) {
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> TMA
+      __syncthreads();
+      // odd n2: the maps cover the even width (TMA writes whole 16-byte
+      // pieces at the right edge), the last column leaves by plain stores
+      if ((p.n2 & 1) && j0 + cols == p.n2 && tid < rows) {
+        __stcs(p.phi + (long long)(i0 + tid) * p.ld_out + p.n2 - 1, Cst[swz(tid, cols - 1)]);
+        __stcs(p.psi + (long long)(i0 + tid) * p.ld_out + p.n2 - 1, Cst[4096 + swz(tid, cols - 1)]);
+      }
+      if (tid == 0) fused_store_tile(&map_phi, &map_psi, cst_s, i0, j0);
+      if (mirror) {    // the transposed block (sync^T, -async^T): rows j0.., columns i0..
+        if (!p.mirror_buf) {                           // one staging buffer: wait until it was read
+          if (tid == 0) bulk_wait_read();
+          __syncthreads();
+        }
+        double* Cst = p.mirror_buf ? Cmir : Cst0;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+              const int o = swz(c, r);
+              Cst[o] = aphi[mt][nt][q];
+              Cst[4096 + o] = neg_bits(apsi[mt][nt][q]);
+            }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncthreads();
+        if (tid == 0) fused_store_tile(&map_phi, &map_psi, p.mirror_buf ? cmir_s : cst_s, j0, i0);
+      }
+    } else {           // planes not 16-B aligned / odd ld_out: plain stores from the staging
+      __syncthreads();
+#pragma unroll 1
+      for (int idx = tid; idx < kSB * kSB; idx += kSThreads) {
+        const int r = idx >> 6, c = idx & 63;
+        if (r >= rows || c >= cols) continue;
+        const double f = Cst[swz(r, c)], s = Cst[4096 + swz(r, c)];
+        __stcs(p.phi + (long long)(i0 + r) * p.ld_out + j0 + c, f);
+        __stcs(p.psi + (long long)(i0 + r) * p.ld_out + j0 + c, s);
+        if (mirror) {
+          __stcs(p.phi + (long long)(j0 + c) * p.ld_out + i0 + r, f);
+          __stcs(p.psi + (long long)(j0 + c) * p.ld_out + i0 + r, neg_bits(s));
+        }
+      }
+      __syncthreads();                                 // staging reads done before the next block's writes
+    }
+    if (b == b0) FUSED_STAMP(6);
+    I = nI;
+    J = nJ;
+    diag = ndiag;
+  }
+  fused_publish(p, mphi, mpsi, lane, warp, tid);
+  if (tid == 0) bulk_wait_read();                     // the staging must outlive the stores' reads
+  FUSED_STAMP(7);
+}
+
+
+// One set of atomics per CTA into the accumulator words; the last CTA to
+// arrive publishes status / stats and leaves every work word zero.
+__device__ __noinline__ void fused_publish(const FusedParams& p, unsigned long long mphi, unsigned long long mpsi,
+                                           int lane, int warp, int tid) {
+  constexpr unsigned long long kInf = 0x7ff0000000000000ull;
+  int bad = (mphi >= kInf) + (mpsi >= kInf);
+  mphi = min(mphi, kInf);
+  mpsi = min(mpsi, kInf);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mphi = max(mphi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mphi, o));
+    mpsi = max(mpsi, (unsigned long long)__shfl_xor_sync(0xffffffffu, (long long)mpsi, o));
+  }
+  bad = warp_sum(bad);
+  __shared__ unsigned long long red[3][4];
+  __shared__ int last;
+  if (lane == 0) {
+    red[0][warp] = mphi;
+    red[1][warp] = mpsi;
+    red[2][warp] = (unsigned long long)bad;
+  }
+  __syncthreads();
+  unsigned long long* acc = reinterpret_cast<unsigned long long*>(p.work + kWFAcc);
+  if (tid == 0) {
+    unsigned long long a0 = 0, a1 = 0, a2 = 0;
+    for (int w = 0; w < kSThreads / 32; ++w) {
+      a0 = max(a0, red[0][w]);
+      a1 = max(a1, red[1][w]);
+      a2 += red[2][w];
+    }
+    if (a0) atomicMax(&acc[0], a0);
+    if (a1) atomicMax(&acc[1], a1);
+    if (a2) atomicAdd(&acc[2], a2);
+    __threadfence();
+    last = atomicAdd(&p.work[kWFCount], 1) == p.nctas - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid < 3) p.stats[tid] = atomicExch(&acc[tid], 0ull);
+  if (tid >= 32 && tid < 36) p.status1[tid - 32] = atomicExch(&p.work[kWFStat1 + tid - 32], 0);
+  if (tid >= 64 && tid < 68) {
+    const int v = atomicExch(&p.work[kWFStat2 + tid - 64], 0);
+    if (p.status2) p.status2[tid - 64] = v;
+  }
+  if (tid == 96) atomicExch(&p.work[kWFCount], 0);
+}
+
+// Per-(device, m) table of the fused path: [2][nsp][gp] doubles -- role A rows
+// s (slot of the Gauss segments, corr2d.h CORR2D_PACK_F64_GAUSS) hold
+// pa cos(2 pi w t / m) + qa (-sin(2 pi w t / m)) for t < m (Norm is applied in
+// the kernel), role B rows pb cos + qb (-sin); pads are zero.
+static const double* fused_table(int m, int nsp, int gp, cudaStream_t st, int* rc) {
+  constexpr int kDev = 64;
+  static double* tab[kDev][kSMaxM + 1] = {};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kDev) {
+    *rc = fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: device index >= 64");
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  if (tab[dev][m]) return tab[dev][m];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone) {
+    *rc = fail(CORR2D_ERR_UNSUPPORTED,
+               "corr2d_correlate_small_f64: the first call for this m on this device must not be graph-captured");
+    return nullptr;
+  }
+  const int kg = gauss_kg(m), ns = 3 * kg;
+  std::vector<double> h((size_t)2 * nsp * gp, 0.0);
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int s = 0; s < ns; ++s) {
+    const int seg = s / kg, j = s - seg * kg, w = gauss_bin(seg, j, m);
+    if (w < 0) continue;
+    const bool edge = w == 0 || (m % 2 == 0 && w == m / 2);
+    const double kk = edge ? 1.0 : 2.0, ki = edge ? 0.0 : 1.0;
+    double pa, qa, pb, qb;
+    if (seg == 0) { pa = kk; qa = kk * ki; pb = 1.0; qb = 0.0; }          // a + b, c
+    else if (seg == 1) { pa = kk; qa = 0.0; pb = -1.0; qb = -ki; }        // a, d - c
+    else if (edge) { pa = kk; qa = 0.0; pb = 1.0; qb = 0.0; }             // Nyquist: a, c
+    else { pa = 0.0; qa = -kk; pb = 1.0; qb = -1.0; }                     // -b, c + d
+    for (int t = 0; t < m; ++t) {
+      const int q = (w * t) % m;
+      const double ang = two_pi * (double)q / (double)m;
+      const double c = std::cos(ang);
+      const double ns_ = (q == 0 || 2 * q == m) ? 0.0 : -std::sin(ang);   // Im part of exp(-i ang): exact 0 at 0, pi
+      h[(size_t)s * gp + t] = pa * c + qa * ns_;
+      h[(size_t)(nsp + s) * gp + t] = pb * c + qb * ns_;
+    }
+  }
+  double* d = nullptr;
+  if (cudaMalloc(&d, h.size() * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+    *rc = check_launch("small fused table");
+    return nullptr;
+  }
+  tab[dev][m] = d;
+  return d;
+}
+
+static int device_sms() {
+  constexpr int kDev = 64;
+  static int sms[kDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kDev) return 148;
+  if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  return sms[dev] > 0 ? sms[dev] : 148;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 fused_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) == cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// Output plane (rows x cols fp64, leading dimension ld): 64-row x 16-column
+// boxes, SWIZZLE_128B (the staging layout of swz()).
+static int fused_plane_map(CUtensorMap* map, double* base, long long ld, long long rows, long long cols) {
+  auto fn = fused_encode_fn();
+  if (!fn) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {16, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled(small planes) failed (" + std::to_string((int)r) + ")");
+  return CORR2D_OK;
+}
+
+static int launch_fused(const SmallParams& q, cudaStream_t st) {
+  FusedParams p{};
+  p.raw1 = q.raw1; p.raw2 = q.raw2; p.ld1 = q.ld1; p.ld2 = q.ld2; p.in_f32 = q.in_f32;
+  p.al1 = (reinterpret_cast<uintptr_t>(q.raw1) & 15) == 0 && q.ld1 % 2 == 0;
+  p.al2 = q.raw2 && (reinterpret_cast<uintptr_t>(q.raw2) & 15) == 0 && q.ld2 % 2 == 0;
+  p.m = q.m; p.mpad = q.mpad; p.gp = q.mpad + 2; p.n1 = q.n1; p.n2 = q.n2; p.homo = q.homo;
+  p.ref_mode1 = q.ref_mode1; p.ref_mode2 = q.ref_mode2; p.ref_in1 = q.ref_in1; p.ref_in2 = q.ref_in2;
+  p.sigma_in1 = q.sigma_in1; p.sigma_in2 = q.sigma_in2; p.alpha = q.alpha; p.substitute = q.substitute;
+  p.norm = q.norm;
+  p.ref_out1 = q.ref_out1; p.sigma_out1 = q.sigma_out1; p.ref_out2 = q.ref_out2; p.sigma_out2 = q.sigma_out2;
+  p.kg = gauss_kg(q.m); p.ns = 3 * p.kg; p.nsp = (p.ns + 7) / 8 * 8; p.ks = p.nsp + 4;
+  p.T1 = q.T1; p.T2 = q.T2;
+  p.tiles = small_blocks(q.n1, q.n2, q.homo);
+  const int sms = device_sms();
+  p.nctas = (int)std::min<long long>(p.tiles, sms);
+  p.phi = q.phi; p.psi = q.psi; p.ld_out = q.ld_out; p.vec = q.vec && q.n2 >= 2;
+  p.status1 = q.status1; p.status2 = q.status2; p.stats = q.stats; p.work = q.work; p.trace = q.trace;
+  int rc = CORR2D_OK;
+  p.G = fused_table(p.m, p.nsp, p.gp, st, &rc);
+  if (!p.G) return rc;
+  CUtensorMap map_phi, map_psi;
+  memset(&map_phi, 0, sizeof(map_phi));
+  memset(&map_psi, 0, sizeof(map_psi));
+  if (p.vec) {
+    if (int e = fused_plane_map(&map_phi, p.phi, p.ld_out, p.n1, p.n2 & ~1)) return e;
+    if (int e = fused_plane_map(&map_psi, p.psi, p.ld_out, p.n1, p.n2 & ~1)) return e;
+  }
+  size_t smem = 1024 + (8192 + 2 * (size_t)p.nsp * p.gp + 2 * (size_t)p.mpad * kFYP + 2 * 64 * (size_t)p.ks) *
+                           sizeof(double);
+  if (p.homo && smem + 65536 <= 226 * 1024) {
+    p.mirror_buf = 1;
+    smem += 65536;
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    const int worst = 226 * 1024;   // 227 KB per block minus the static 1 KB
+    cudaFuncSetAttribute(small_fused_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+    cudaFuncSetAttribute(small_fused_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+    cudaFuncSetAttribute(small_fused_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+    cudaFuncSetAttribute(small_fused_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+    attr_set = true;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kSThreads);
+  cfg.gridDim = dim3((unsigned)p.nctas);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (p.kg) {
+    case 4: cudaLaunchKernelEx(&cfg, small_fused_kernel<4>, p, map_phi, map_psi); break;
+    case 8: cudaLaunchKernelEx(&cfg, small_fused_kernel<8>, p, map_phi, map_psi); break;
+    case 12: cudaLaunchKernelEx(&cfg, small_fused_kernel<12>, p, map_phi, map_psi); break;
+    default: cudaLaunchKernelEx(&cfg, small_fused_kernel<16>, p, map_phi, map_psi); break;
+  }
+  const int code = check_launch("small_fused_kernel");
+#ifdef CORR2D_PROFILING
+  if (p.trace) {
+    std::vector<unsigned long long> h(8 * (size_t)p.nctas);
+    cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < p.nctas; ++b) t0 = std::min(t0, h[8 * b]);
+    const char* nm[8] = {"start", "after wait", "samples in", "prep done", "mma done", "staged",
+                         "stores issued", "end"};
+    fprintf(stderr, "small fused trace (m %d, %d x %d, %s, %d CTAs, %lld tiles; first tile of each CTA):\n",
+            p.m, p.n1, p.n2, p.homo ? "homo" : "hetero", p.nctas, p.tiles);
+    for (int k = 0; k < 8; ++k) {
+      std::vector<double> v;
+      for (int b = 0; b < p.nctas; ++b)
+        if (h[8 * b + k]) v.push_back((double)(h[8 * b + k] - t0));
+      if (v.empty()) continue;
+      std::sort(v.begin(), v.end());
+      fprintf(stderr, "  %-16s min %8.0f  med %8.0f  max %8.0f ns\n", nm[k], v.front(), v[v.size() / 2], v.back());
+    }
+  }
+#endif
+  return code;
+}
+
 }  // namespace corr2d
 
 using namespace corr2d;
@@ -749,6 +1600,17 @@ using namespace corr2d;
 extern "C" int64_t corr2d_small_block_count(int n1, int n2, int homo) {
   if (n1 < 1 || n2 < 1 || (homo && n1 != n2)) return -1;
   return small_blocks(n1, n2, homo);
+}
+
+extern "C" int corr2d_small_launches(int n1, int n2, int homo) {
+  if (n1 < 1 || n2 < 1 || (homo && n1 != n2)) return -1;
+#if defined(CORR2D_SMALL_FORCE_FUSED)
+  return 1;
+#elif defined(CORR2D_SMALL_TWO_KERNEL)
+  return 2;
+#else
+  return small_blocks(n1, n2, homo) <= device_sms() ? 1 : 2;
+#endif
 }
 
 extern "C" int corr2d_small_ops_depth(int m) { return (m >= 2 && m <= kSMaxM) ? 3 * gauss_kg(m) : -1; }
@@ -764,7 +1626,7 @@ extern "C" int corr2d_correlate_small_f64(
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream) {
   const bool homo = raw2 == nullptr;
-  if (!raw1 || !ops_a || !ops_b || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
+  if (!raw1 || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
   if (in_dtype != CORR2D_F64 && in_dtype != CORR2D_F32) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: bad dtype");
   if (m < 2 || m > kSMaxM) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: needs 2 <= m <= 32");
@@ -772,8 +1634,8 @@ extern "C" int corr2d_correlate_small_f64(
   if (homo && n1 != n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: homo needs n1 == n2");
   if (ld_raw1 < n1 || (!homo && ld_raw2 < n2)) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_raw < n");
   if (ld_out < n2) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: ld_out < n2");
-  if (ld_ops != corr2d_small_ops_depth(m) ||
-      ((reinterpret_cast<uintptr_t>(ops_a) | reinterpret_cast<uintptr_t>(ops_b)) & 15))
+  if ((ops_a || ops_b) && (ld_ops != corr2d_small_ops_depth(m) ||
+      ((reinterpret_cast<uintptr_t>(ops_a) | reinterpret_cast<uintptr_t>(ops_b)) & 15)))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: operand rows must be 16-B aligned with "
                                  "ld_ops == corr2d_small_ops_depth(m)");
   if (!(alpha >= 0.0 && alpha <= 1.0)) return fail(CORR2D_ERR_DATA, "scaling exponent must lie in [0, 1]");
@@ -792,14 +1654,8 @@ extern "C" int corr2d_correlate_small_f64(
   p.ref_out1 = ref_out1; p.sigma_out1 = sigma_out1; p.ref_out2 = ref_out2; p.sigma_out2 = sigma_out2;
   p.mpad = (m + 3) / 4 * 4;
   p.yrows = p.mpad > 2 * (m / 2 + 1) ? p.mpad : 2 * (m / 2 + 1);
-  int rc = CORR2D_OK;
-  p.W = dft_table(m, p.mpad, st, &rc);
-  if (!p.W) return rc;
   p.kg = gauss_kg(m);
-  p.ks = (3 * p.kg + 11) / 16 * 16 + 4;
   p.T1 = (n1 + kSB - 1) / kSB; p.T2 = (n2 + kSB - 1) / kSB;
-  p.nb1 = (n1 + kSThreads - 1) / kSThreads;
-  p.opsA = ops_a; p.opsB = ops_b; p.ld_ops = ld_ops;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out;
   p.vec = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
   p.status1 = status1; p.status2 = homo ? nullptr : status2; p.stats = stats; p.work = work;
@@ -813,6 +1669,25 @@ extern "C" int corr2d_correlate_small_f64(
       p.trace = tbuf;
     }
 #endif
+  // one fused kernel when every output block has its own SM (no block's
+  // channels are prepared twice on one SM, and there is no second wave);
+  // otherwise K1 once per channel, then the contraction (the operand rows
+  // stay in L2 between the two kernels)
+#if defined(CORR2D_SMALL_FORCE_FUSED)
+  const bool fused = true;
+#elif defined(CORR2D_SMALL_TWO_KERNEL)
+  const bool fused = false;
+#else
+  const bool fused = small_blocks(n1, n2, homo) <= device_sms() || !ops_a || !ops_b;
+#endif
+  if (fused) return launch_fused(p, st);
+  if (!ops_a || !ops_b) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
+  int rc = CORR2D_OK;
+  p.W = dft_table(m, p.mpad, st, &rc);
+  if (!p.W) return rc;
+  p.ks = (3 * p.kg + 11) / 16 * 16 + 4;
+  p.nb1 = (n1 + kSThreads - 1) / kSThreads;
+  p.opsA = ops_a; p.opsB = ops_b; p.ld_ops = ld_ops;
   const long long blocks = small_blocks(n1, n2, homo);
   if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
   const int prep_blocks = p.nb1 + (homo ? 0 : (n2 + kSThreads - 1) / kSThreads);

@@ -375,8 +375,8 @@ class CorrelationPlan:
         # in a 128-byte pad (include/corr2d.h)
         self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
         # small m (fp64 Fourier route, m <= 32, no resampling, whole map): the
-        # whole call is ONE C call (csrc/small_path.cu: K1 once per channel, then
-        # the block contraction, two PDL-chained kernels)
+        # whole call is ONE kernel (csrc/small_path.cu small_fused_kernel: each
+        # CTA builds its blocks' operand rows in shared memory and contracts them)
         self.small = (route == "fourier" and self.dtype == np.float64
                       and small_fused_enabled() and 2 <= self.m <= 32
                       and all(r is None or (r.resample is None and r.m_in == r.m) for r in (recipe1, recipe2))
@@ -387,7 +387,9 @@ class CorrelationPlan:
         R1, R2 = self.n1, self.n2
         alloc = t.empty
         if self.small:
-            # the small path's own Gauss operand rows (K1 -> contraction, L2-resident)
+            # the small path's Gauss operand rows (the two-kernel variant's K1 ->
+            # contraction, L2-resident; the one-kernel variant keeps them in
+            # shared memory)
             self.ld_pack = self.lib.corr2d_small_ops_depth(self.m)
             self.mp = self.ld_pack
         O1, O2 = (R1, R2)
@@ -452,9 +454,9 @@ class CorrelationPlan:
     @property
     def launches_per_step(self) -> int:
         """Kernels of ours one launch() enqueues: K1 per dataset + K2 (the
-        small-m path: its K1 and contraction kernels)."""
+        small-m path: one fused kernel, or K1 + contraction)."""
         if self.small:
-            return 2
+            return int(self.lib.corr2d_small_launches(self.n1, self.n2, 1 if self.homo else 0))
         return (1 if self.homo else 2) + (2 if self.route == "hilbert" else 1)
 
     def launch(self):
