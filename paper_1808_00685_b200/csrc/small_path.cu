@@ -838,7 +838,7 @@ __device__ __forceinline__ long long fused_row_start(const FusedParams& p, int I
     if (p.trace && threadIdx.x == 0) {                                                         \
       unsigned long long t_;                                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
-      p.trace[8 * blockIdx.x + (k)] = t_;                                                      \
+      p.trace[16 * blockIdx.x + (k)] = t_;                                                     \
     }                                                                                          \
   } while (0)
 #else
@@ -1164,7 +1164,6 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
   // generic addressing)
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm_raw));
   double* Cst = sm_raw + (((1024u - (sbase & 1023u)) & 1023u) >> 3);
-  double* const Cst0 = Cst;
   const unsigned cst_s = static_cast<unsigned>(__cvta_generic_to_shared(Cst));
   double* const Cmir = Cst + 8192;                     // mirror staging (homo, when it fits)
   const unsigned cmir_s = cst_s + 65536u;
@@ -1207,9 +1206,11 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
 #pragma unroll 1
   for (long long b = b0; b < b1; ++b) {
     const bool newA = I != curI;
+    if (b == b0 + 1) FUSED_STAMP(14);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();                                   // this block's samples (and the tables) landed
     if (b == b0) FUSED_STAMP(2);
+    if (b == b0 + 1) FUSED_STAMP(15);
     // ---- centring / scaling: threads 0..63 the row channels, 64..127 the column channels
     if (tid < 64) {
       if (newA) {
@@ -1222,6 +1223,8 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
       const int n = set ? p.n2 : p.n1;
       fused_stats(p, set, c, c < n, !p.homo && I == 0, YB + tid - 64);
     }
+    if (b == b0) FUSED_STAMP(8);
+    if (b == b0 + 1) FUSED_STAMP(9);
     __syncthreads();
     // ---- operand rows: role A (x Norm) of the row channels, role B of the
     //      column channels (a diagonal block: of the same channels)
@@ -1229,8 +1232,10 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
       fused_transform2<KG>(mpad, gp, YA, Gs, As, p.norm, diag ? YA : YB, Gs + SH::NSP * gp, Bs, warp, lr, lk);
     else
       fused_transform<KG>(mpad, gp, YB, Gs + SH::NSP * gp, Bs, 1.0, warp, lr, lk);
+    if (b == b0) FUSED_STAMP(10);
     __syncthreads();                                   // operand rows ready, sample buffers free
     if (b == b0) FUSED_STAMP(3);
+    if (b == b0 + 1) FUSED_STAMP(11);
     const int i0 = I * kSB, j0 = J * kSB;
     const bool mirror = p.homo && !diag;
     curI = I;
@@ -1260,6 +1265,7 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
         for (int e = 0; e < 4; ++e) aphi[a][q][e] += apsi[a][q][e];
     fused_seg1<KG>(apsi, Aw + KG, Bw + KG);
     if (b == b0) FUSED_STAMP(4);
+    if (b == b0 + 1) FUSED_STAMP(12);
     // ---- max|.| / finite check from the fragments, on |x|'s bit pattern
     //      (integer pipe; Inf / NaN patterns exceed every finite one, so the
     //      maxima also carry the finite check).  Diagonal blocks: the upper
@@ -1292,6 +1298,19 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
           *reinterpret_cast<double2*>(Cst + o) = make_double2(aphi[mt][nt][2 * h], aphi[mt][nt][2 * h + 1]);
           *reinterpret_cast<double2*>(Cst + 4096 + o) = make_double2(apsi[mt][nt][2 * h], apsi[mt][nt][2 * h + 1]);
         }
+    if (mirror && p.mirror_buf && p.vec) {   // the transposed block into the second buffer, now
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+            const int o = swz(c, r);
+            Cmir[o] = aphi[mt][nt][q];
+            Cmir[4096 + o] = neg_bits(apsi[mt][nt][q]);
+          }
+    }
     if (diag) {        // below the diagonal: the transpose of the upper triangle (exact symmetry)
       __syncthreads();
 #pragma unroll
@@ -1321,12 +1340,11 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
         __stcs(p.psi + (long long)(i0 + tid) * p.ld_out + p.n2 - 1, Cst[4096 + swz(tid, cols - 1)]);
       }
       if (tid == 0) fused_store_tile(&map_phi, &map_psi, cst_s, i0, j0);
-      if (mirror) {    // the transposed block (sync^T, -async^T): rows j0.., columns i0..
-        if (!p.mirror_buf) {                           // one staging buffer: wait until it was read
-          if (tid == 0) bulk_wait_read();
-          __syncthreads();
-        }
-        double* Cst = p.mirror_buf ? Cmir : Cst0;
+      if (mirror && p.mirror_buf) {
+        if (tid == 0) fused_store_tile(&map_phi, &map_psi, cmir_s, j0, i0);   // staged with the block
+      } else if (mirror) {   // the transposed block (sync^T, -async^T): rows j0.., columns i0..
+        if (tid == 0) bulk_wait_read();                // one staging buffer: wait until it was read
+        __syncthreads();
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -1340,7 +1358,7 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
             }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncthreads();
-        if (tid == 0) fused_store_tile(&map_phi, &map_psi, p.mirror_buf ? cmir_s : cst_s, j0, i0);
+        if (tid == 0) fused_store_tile(&map_phi, &map_psi, cst_s, j0, i0);
       }
     } else {           // planes not 16-B aligned / odd ld_out: plain stores from the staging
       __syncthreads();
@@ -1359,6 +1377,7 @@ small_fused_kernel(const __grid_constant__ FusedParams p, const __grid_constant_
       __syncthreads();                                 // staging reads done before the next block's writes
     }
     if (b == b0) FUSED_STAMP(6);
+    if (b == b0 + 1) FUSED_STAMP(13);
     I = nI;
     J = nJ;
     diag = ndiag;
@@ -1571,19 +1590,20 @@ static int launch_fused(const SmallParams& q, cudaStream_t st) {
   const int code = check_launch("small_fused_kernel");
 #ifdef CORR2D_PROFILING
   if (p.trace) {
-    std::vector<unsigned long long> h(8 * (size_t)p.nctas);
+    std::vector<unsigned long long> h(16 * (size_t)p.nctas);
     cudaMemcpyAsync(h.data(), p.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     unsigned long long t0 = ~0ull;
-    for (int b = 0; b < p.nctas; ++b) t0 = std::min(t0, h[8 * b]);
-    const char* nm[8] = {"start", "after wait", "samples in", "prep done", "mma done", "staged",
-                         "stores issued", "end"};
+    for (int b = 0; b < p.nctas; ++b) t0 = std::min(t0, h[16 * b]);
+    const char* nm[16] = {"start", "after wait", "samples in", "prep done", "mma done", "staged",
+                          "stores issued", "end", "stats done (t0)", "stats done (t1)", "transforms done",
+                          "prep done (t1)", "mma done (t1)", "stores issued (t1)", "tile 1 top", "samples in (t1)"};
     fprintf(stderr, "small fused trace (m %d, %d x %d, %s, %d CTAs, %lld tiles; first tile of each CTA):\n",
             p.m, p.n1, p.n2, p.homo ? "homo" : "hetero", p.nctas, p.tiles);
-    for (int k = 0; k < 8; ++k) {
+    for (int k : {0, 1, 2, 8, 10, 3, 4, 5, 6, 14, 15, 9, 11, 12, 13, 7}) {
       std::vector<double> v;
       for (int b = 0; b < p.nctas; ++b)
-        if (h[8 * b + k]) v.push_back((double)(h[8 * b + k] - t0));
+        if (h[16 * b + k]) v.push_back((double)(h[16 * b + k] - t0));
       if (v.empty()) continue;
       std::sort(v.begin(), v.end());
       fprintf(stderr, "  %-16s min %8.0f  med %8.0f  max %8.0f ns\n", nm[k], v.front(), v[v.size() / 2], v.back());
@@ -1663,7 +1683,7 @@ extern "C" int corr2d_correlate_small_f64(
   if (const char* e = getenv("CORR2D_SMALL_TRACE"))
     if (e[0] == '1') {
       static unsigned long long* tbuf = nullptr;
-      const size_t words = 8 * (size_t)(kTraceK1 + 65536);
+      const size_t words = 16 * (size_t)(kTraceK1 + 65536);
       if (!tbuf) cudaMalloc(&tbuf, words * 8);
       cudaMemsetAsync(tbuf, 0, words * 8, st);
       p.trace = tbuf;
