@@ -216,15 +216,22 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  * contraction of a whole map (csrc/small_path.cu).  Replaces the corr2d_prep +
  * corr2d_contract_f64_gauss sequence that preprocess_dataset / dft_channels /
  * correlate_ft (preprocess.py:262-275, fourier.py:61-125) map onto; same
- * argument meanings as those two calls.  Two kernels chained by programmatic
- * dependent launch: K1 once per channel (one lane per channel, DFT on the
- * FP64 tensor pipe, Gauss operand rows into ops_a / ops_b), then one CTA per
- * 64 x 64 output block (corr2d_small_block_count blocks: homo the upper
- * triangle, mirrored).  No CTA ever waits for another CTA.
+ * argument meanings as those two calls.  Maps with at most one 64 x 64 output
+ * block per SM (corr2d_small_block_count <= SMs; homo: the upper triangle,
+ * mirrored) run as ONE kernel: each CTA centres its block's channels, builds
+ * their Gauss operand rows in shared memory and contracts them.  Larger maps
+ * run two kernels chained by programmatic dependent launch: K1 once per
+ * channel (one lane per channel, DFT on the FP64 tensor pipe, Gauss operand
+ * rows into ops_a / ops_b), then a persistent contraction (one CTA per SM,
+ * one bulk copy per role and block, TMA tensor stores of the planes; planes
+ * that are not 16-B aligned with an even ld_out: one CTA per block, plain
+ * stores).  No CTA ever waits for another CTA.
  *   ops_a / ops_b      : device operand scratch, n1 (resp. n2; homo: n1) rows
  *                       of ld_ops doubles, 16-B aligned, ld_ops ==
- *                       corr2d_small_ops_depth(m) (dense rows: K1 writes a
- *                       warp's 32 rows as one coalesced run)
+ *                       corr2d_small_ops_depth(m) (3 kg Gauss slots padded to
+ *                       4 or 12 mod 16 doubles: a 64-row block is one
+ *                       contiguous run, fragment loads conflict-free); may be
+ *                       NULL for a one-kernel map
  *   ref_out* / sigma_out* : as corr2d_prep (either may be NULL)
  *   status1 / status2  : device int32[4] each, the corr2d_prep status words
  *                       (status2 unused when homo); written by the call

@@ -85,6 +85,9 @@ struct SmallParams {
   unsigned long long* stats;
   int* work;                // kW* words, zero-filled once by the caller
   unsigned long long* trace;  // profiling builds: per-CTA globaltimer stamps (NULL otherwise)
+  long long tiles;          // streamed contraction: 64 x 64 blocks, CTAs, 64-KB staging slots
+  int nctas, nslots;
+  int dbg;                  // profiling builds only (CORR2D_DEBUG_SKIP): 1 no stores, 2 no DMMAs
 };
 
 // work-buffer words (int32 indices); every launch leaves them zero
@@ -142,13 +145,17 @@ __device__ __forceinline__ void small_decode(const SmallParams& p, long long b, 
 
 // Statistics and dynamic values of one channel (one lane), in place in its
 // shared-memory column ys[t * kYS]: the IEEE operations of the other K1
-// kernels in the reference's order.  The owner lane reports status /
-// reference / sigma.
-__device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c, bool valid, bool owner,
-                                           double* ys) {
+// kernels in the reference's order.  No global writes (K1 computes before its
+// griddepcontrol.wait); lane_report publishes the channel's status /
+// reference / sigma afterwards.
+struct LaneStat {
+  double ref, sigma;
+  int bad;
+};
+__device__ __forceinline__ LaneStat lane_stats(const SmallParams& p, int set, int c, bool valid, double* ys) {
   const int m = p.m;
   const int ref_mode = set ? p.ref_mode2 : p.ref_mode1;
-  int* status = p.work + (set ? kWStatus2 : kWStatus1);
+  LaneStat st{0.0, 0.0, 0};
   double ref = 0.0, scale = 1.0;
   int bad = 0;
   double sum = 0.0;                                    // left to right (numpy's axis-0 order)
@@ -158,12 +165,13 @@ __device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c,
     bad += !isfinite(v);
     sum = __dadd_rn(sum, v);
   }
-  if (owner && valid && bad) atomicAdd(&status[CORR2D_ST_NONFINITE], bad);
+  st.bad = bad;
   if (ref_mode == CORR2D_REF_PROVIDED) {
     ref = valid ? __ldg((set ? p.ref_in2 : p.ref_in1) + c) : 0.0;
   } else if (ref_mode == CORR2D_REF_MEAN) {
     ref = __ddiv_rn(sum, (double)m);
   }
+  st.ref = ref;
   if (p.alpha > 0.0) {
     const double* sigma_in = set ? p.sigma_in2 : p.sigma_in1;
     double sigma;
@@ -177,20 +185,9 @@ __device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c,
       }
       sigma = __dsqrt_rn(__ddiv_rn(ss, (double)(m - 1)));
     }
-    if (owner && valid) {
-      double* so = set ? p.sigma_out2 : p.sigma_out1;
-      if (so) so[c] = sigma;
-      if (sigma == 0.0) {
-        atomicAdd(&status[CORR2D_ST_ZEROVAR], 1);
-        atomicMax(&status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - c);
-      }
-    }
+    st.sigma = sigma;
     if (sigma == 0.0 && p.substitute) sigma = 1.0;
     scale = (p.alpha == 0.5) ? __dsqrt_rn(sigma) : (p.alpha == 1.0 ? sigma : pow(sigma, p.alpha));
-  }
-  if (owner && valid && ref_mode != CORR2D_REF_NONE) {
-    double* ro = set ? p.ref_out2 : p.ref_out1;
-    if (ro) ro[c] = ref;
   }
   const bool sub = ref_mode != CORR2D_REF_NONE, div = p.alpha > 0.0;
   if (!div) {
@@ -199,13 +196,32 @@ __device__ __forceinline__ void lane_stats(const SmallParams& p, int set, int c,
       const double v = ys[t * kYS];
       ys[t * kYS] = valid ? (sub ? __dsub_rn(v, ref) : v) : 0.0;
     }
-    return;
+    return st;
   }
   for (int t = 0; t < m; ++t) {
     double v = ys[t * kYS];
     if (sub) v = __dsub_rn(v, ref);
     v = __ddiv_rn(v, scale);
     ys[t * kYS] = valid ? v : 0.0;
+  }
+  return st;
+}
+
+// The channel's status words, sigma and reference (after griddepcontrol.wait).
+__device__ __forceinline__ void lane_report(const SmallParams& p, int set, int c, const LaneStat& st) {
+  int* status = p.work + (set ? kWStatus2 : kWStatus1);
+  if (st.bad) atomicAdd(&status[CORR2D_ST_NONFINITE], st.bad);
+  if (p.alpha > 0.0) {
+    double* so = set ? p.sigma_out2 : p.sigma_out1;
+    if (so) so[c] = st.sigma;
+    if (st.sigma == 0.0) {
+      atomicAdd(&status[CORR2D_ST_ZEROVAR], 1);
+      atomicMax(&status[CORR2D_ST_FIRST_ZEROVAR], INT_MAX - c);
+    }
+  }
+  if ((set ? p.ref_mode2 : p.ref_mode1) != CORR2D_REF_NONE) {
+    double* ro = set ? p.ref_out2 : p.ref_out1;
+    if (ro) ro[c] = st.ref;
   }
 }
 
@@ -294,15 +310,21 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
   const int c = ((int)blockIdx.x - (set ? p.nb1 : 0)) * kSThreads + tid;
   const int n = set ? p.n2 : p.n1;
   const bool valid = c < n;
+  LaneStat lst;
   // the contraction grid may launch now: it waits for this grid's completion
   // (griddepcontrol.wait) before it reads the operand rows
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   SMALL_STAMP(0, 0);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // inputs written by earlier kernels are visible
+  // Everything up to the operand rows' copy-out only READS global memory (the
+  // samples, the tables, provided reference / sigma vectors), so it runs
+  // before griddepcontrol.wait: when the previous kernel in the stream is the
+  // contraction of an earlier call (launched with programmatic serialization),
+  // this grid starts on the SMs its CTAs free and overlaps its tail.  That
+  // contraction triggers only after its own griddepcontrol.wait, i.e. once
+  // every earlier kernel -- the writers of these inputs -- completed; its own
+  // reads of the operand rows and work words end before this grid's writes,
+  // which all follow the wait below.
   SMALL_STAMP(0, 1);
-  // this call's stats words start at zero (the contraction grid reduces into
-  // them only after this grid completed)
-  if (blockIdx.x == 0 && tid < 3) p.stats[tid] = 0ull;
   // the DFT rows and the slot table into shared memory, in flight together
   // with the samples (one DRAM round trip; the loops below then never touch
   // global memory for them)
@@ -332,7 +354,7 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
       for (int t = 0; t < m; ++t) ys[t * kYS + tid] = (double)reinterpret_cast<const float*>(ys + t * kYS + tid)[0];
     for (int t = m; t < mpad; ++t) ys[t * kYS + tid] = 0.0;
     SMALL_STAMP(0, 2);
-    lane_stats(p, set, c, valid, true, ys + tid);
+    lst = lane_stats(p, set, c, valid, ys + tid);
   }
   __syncthreads();                                   // every thread's table pieces have landed
   SMALL_STAMP(0, 3);
@@ -386,25 +408,25 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
   // The rows are staged per warp in shared memory in their global layout
   // (ld_ops = 3 kg: the warp's 32 rows are one contiguous run), then leave as
   // coalesced 16-byte stores.
-  const int ns = 3 * p.kg;
-  // the warp's 32 rows staged in their global layout (ld_ops = ns: ONE
-  // contiguous run), then one bulk copy per role
-  double* stA = tab + 48 * mpad + 5 * ns + (size_t)warp * 32 * ns;   // [32][ns] per warp
-  double* stB = stA + (size_t)kSThreads * ns;
+  const int ns = 3 * p.kg, ldo = (int)p.ld_ops;
+  // the warp's 32 rows staged in their global layout (row pitch ld_ops, pads
+  // zero: ONE contiguous run), then one bulk copy per role
+  double* stA = tab + 48 * mpad + 5 * ns + (size_t)warp * 32 * ldo;   // [32][ldo] per warp
+  double* stB = stA + (size_t)kSThreads * ldo;
   const bool wantA = !set, wantB = set || p.homo;
   {
     // pads are zero: the warp zeroes its run with consecutive 16-B stores
     double2* zA = reinterpret_cast<double2*>(stA);
     double2* zB = reinterpret_cast<double2*>(stB);
-    for (int i = lane; i < 16 * ns; i += 32) zA[i] = zB[i] = make_double2(0.0, 0.0);
+    for (int i = lane; i < 16 * ldo; i += 32) zA[i] = zB[i] = make_double2(0.0, 0.0);
     __syncwarp();
     // every bin's three Gauss slots from registers.  Lane l takes the bins in
     // the rotated order w = (it + l) mod (H + 1), so the 32 lanes' rows (pitch
     // ns) are written at different slots: few bank conflicts
     const int kg = p.kg, H = m / 2, Iint = gauss_interior(m);
     const double nrm = p.norm;
-    double* a = stA + lane * ns;
-    double* b = stB + lane * ns;
+    double* a = stA + lane * ldo;
+    double* b = stB + lane * ldo;
     int w = lane % (H + 1);
     // a runtime loop: straight-line code is fetched cold, line by line, on
     // every step of a stream that evicts L2 (the bench's rotation does)
@@ -427,11 +449,16 @@ __global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_cons
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> bulk copy
   __syncwarp();
   SMALL_STAMP(0, 7);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // the previous call's contraction is done
+  // this call's stats words start at zero (the contraction grid reduces into
+  // them only after this grid completed)
+  if (blockIdx.x == 0 && tid < 3) p.stats[tid] = 0ull;
+  if (valid) lane_report(p, set, c, lst);
   {
     const int cw = c - lane;                         // the warp's first channel
     const int nrow = min(32, n - cw);
     if (nrow > 0 && lane == 0) {
-      const unsigned bytes = (unsigned)(nrow * ns) * 8u;
+      const unsigned bytes = (unsigned)(nrow * ldo) * 8u;
       if (wantA)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
                      ::"l"(p.opsA + (long long)cw * p.ld_ops),
@@ -972,6 +999,11 @@ __device__ __forceinline__ void fused_stats(const FusedParams& p, int set, int c
 // Compile-time shape of the Gauss rows for KG slots per segment (KG = gauss_kg(m)
 // in {4, 8, 12, 16}): NS = 3 KG slots, padded to NSP (whole 8-column DMMA tiles),
 // operand row pitch KS = NSP + 4 doubles (conflict-free fragment loads).
+// Row pitch (doubles) of the small path's Gauss operand rows in global and
+// shared memory: 3 kg slots, padded to 4 or 12 mod 16 (conflict-free DMMA
+// fragment loads straight from the dense rows)
+__host__ __device__ constexpr int small_ops_pitch(int kg) { return 3 * kg + ((3 * kg) % 16 == 0 || (3 * kg) % 16 == 8 ? 4 : 0); }
+
 template <int KG>
 struct FShape {
   static constexpr int NS = 3 * KG, NSP = (NS + 7) / 8 * 8, NNT = NSP / 8, KS = NSP + 4;
@@ -1046,9 +1078,8 @@ __device__ __forceinline__ void fused_transform2(int mpad, int gp, const double*
 }
 
 // KG/4 k-steps of one Gauss segment into one accumulator set (32 x 32 warp tile).
-template <int KG>
+template <int KG, int KS = FShape<KG>::KS>
 __device__ __forceinline__ void fused_seg1(double (&acc)[2][4][4], const double* A, const double* B) {
-  constexpr int KS = FShape<KG>::KS;
 #pragma unroll
   for (int kk = 0; kk < KG; kk += 4) {
     double ap[2][2], bf[4];
@@ -1067,10 +1098,9 @@ __device__ __forceinline__ void fused_seg1(double (&acc)[2][4][4], const double*
 }
 // Two segments (operand offsets o0 / o1) into two accumulator sets, interleaved:
 // 16 independent DMMAs per warp and k-step.
-template <int KG>
+template <int KG, int KS = FShape<KG>::KS>
 __device__ __forceinline__ void fused_seg2(double (&acc0)[2][4][4], double (&acc1)[2][4][4], const double* A,
                                            const double* B, int o0, int o1) {
-  constexpr int KS = FShape<KG>::KS;
 #pragma unroll
   for (int kk = 0; kk < KG; kk += 4) {
     double a0[2][2], a1[2][2], b0[4], b1[4];
@@ -1436,6 +1466,262 @@ __device__ __noinline__ void fused_publish(const FusedParams& p, unsigned long l
   if (tid == 96) atomicExch(&p.work[kWFCount], 0);
 }
 
+// =====================================================================
+// Streamed contraction (maps with more 64 x 64 blocks than SMs, after
+// small_prep_kernel): one persistent CTA per SM walks a contiguous run of
+// blocks.  Per block the operand rows arrive by one bulk copy per row into one
+// of two buffers (the next block's rows land while this block contracts),
+// the Gauss contraction runs on the FP64 tensor pipe, and both planes (plus
+// the homo mirror) are staged swizzled and leave by TMA tensor stores issued
+// by one thread -- no warp waits on its own output stores, so the next
+// block's DMMAs overlap this block's HBM write stream.  With two 64-KB staging
+// slots, consecutive single-tile blocks alternate between them (the slot is
+// reused only after the store two blocks back has read it).
+// =====================================================================
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done)
+    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+}
+
+// Operand rows of block (I, J) into buffer (As, Bs) -- the block's 64 rows of
+// each role are one contiguous run of the dense operand arrays, so ONE bulk
+// copy per role (per-row copies cost ~20 ns of TMA issue each), completing on
+// `bar` (count 1: thread 0 arrives with the byte count).  Rows past the map
+// are zeroed by the other threads (visible after the consumer's barrier).
+template <int KG>
+__device__ __forceinline__ void stream_load(const SmallParams& p, int I, int J, double* As, double* Bs, unsigned bar) {
+  constexpr int OP = small_ops_pitch(KG);
+  const int tid = threadIdx.x;
+  const int ra = min(kSB, p.n1 - I * kSB), rb = min(kSB, p.n2 - J * kSB);
+  if (tid == 0) {
+    const unsigned ba = (unsigned)ra * OP * 8u, bb = (unsigned)rb * OP * 8u;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // earlier generic reads of the buffer
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(ba + bb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(As))), "l"(p.opsA + (long long)I * kSB * OP),
+                   "r"(ba), "r"(bar) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(Bs))), "l"(p.opsB + (long long)J * kSB * OP),
+                   "r"(bb), "r"(bar) : "memory");
+  }
+  if (ra < kSB)
+    for (int i = ra * OP + 2 * tid; i < kSB * OP; i += 2 * kSThreads) *reinterpret_cast<double2*>(As + i) = make_double2(0.0, 0.0);
+  if (rb < kSB)
+    for (int i = rb * OP + 2 * tid; i < kSB * OP; i += 2 * kSThreads) *reinterpret_cast<double2*>(Bs + i) = make_double2(0.0, 0.0);
+}
+
+// Fragments -> one staged tile at Cs (swizzled boxes); transposed: the mirror
+// (sync^T, -async^T).
+__device__ __forceinline__ void stage_tile(double* Cs, const double (&aphi)[2][4][4], const double (&apsi)[2][4][4],
+                                           bool transposed, int wm, int wn, int lr, int lk) {
+  if (!transposed) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm * 32 + mt * 16 + lr + 8 * h, c = wn * 32 + nt * 8 + 2 * lk;
+          const int o = swz(r, c);
+          *reinterpret_cast<double2*>(Cs + o) = make_double2(aphi[mt][nt][2 * h], aphi[mt][nt][2 * h + 1]);
+          *reinterpret_cast<double2*>(Cs + 4096 + o) = make_double2(apsi[mt][nt][2 * h], apsi[mt][nt][2 * h + 1]);
+        }
+  } else {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+          const int o = swz(c, r);
+          Cs[o] = aphi[mt][nt][q];
+          Cs[4096 + o] = neg_bits(apsi[mt][nt][q]);
+        }
+  }
+}
+
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+
+// NB operand buffers: 2 (one CTA per SM, the next block's rows prefetched)
+// or 1 (two CTAs per SM, each loading its next block once its contraction has
+// read the buffer; the other CTA's work covers the load)
+template <int KG, int NB>
+__global__ void __launch_bounds__(kSThreads, 3 - NB)
+small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant__ CUtensorMap map_phi,
+                    const __grid_constant__ CUtensorMap map_psi) {
+  constexpr int KS = small_ops_pitch(KG);
+  extern __shared__ __align__(1024) double sm_raw[];
+  __shared__ __align__(8) unsigned long long bars[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int wm = warp >> 1, wn = warp & 1;
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm_raw));
+  double* Cst = sm_raw + (((1024u - (sbase & 1023u)) & 1023u) >> 3);   // staging slots (64 KB each)
+  const unsigned cst_s = static_cast<unsigned>(__cvta_generic_to_shared(Cst));
+  double* Ops = Cst + 8192 * p.nslots;                 // [NB buffers][A | B][64][KS]
+  const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(bars));
+  const long long b0 = (long long)blockIdx.x * p.tiles / p.nctas;
+  const long long b1 = (long long)(blockIdx.x + 1) * p.tiles / p.nctas;
+  SMALL_STAMP(kTraceK1, 0);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_phi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_psi)) : "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // K1 complete, its operand rows visible
+  // the next kernel (the next call's K1) may launch now: everything before
+  // this grid completed, and K1 writes nothing before its own wait
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  SMALL_STAMP(kTraceK1, 1);
+  // K1's status accumulators are final now: CTA 0 publishes them and leaves
+  // the words zero for the next call (whose K1 starts after this grid ends)
+  if (blockIdx.x == 0 && tid < 4) {
+    p.status1[tid] = p.work[kWStatus1 + tid];
+    p.work[kWStatus1 + tid] = 0;
+    if (p.status2) p.status2[tid] = p.work[kWStatus2 + tid];
+    p.work[kWStatus2 + tid] = 0;
+  }
+  int I, J;
+  small_decode(p, b0, I, J);
+  stream_load<KG>(p, I, J, Ops, Ops + 64 * KS, bar_s);
+  unsigned long long mphi = 0, mpsi = 0;
+  int prev_mask = 0;                                   // staging slots the most recent store group reads
+#pragma unroll 1
+  for (long long b = b0; b < b1; ++b) {
+    const int k = (int)(b - b0), buf = NB == 2 ? (k & 1) : 0;
+    const double* As = Ops + buf * 128 * KS;
+    const double* Bs = As + 64 * KS;
+    mbar_wait(bar_s + 8 * buf, (k / NB) & 1);
+    __syncthreads();                                   // zero-filled rows visible; the other buffer is free
+    if (b == b0) SMALL_STAMP(kTraceK1, 2);
+    if (b == b0 + 2) SMALL_STAMP(kTraceK1, 6);
+    const bool diag = p.homo && I == J;
+    const int i0 = I * kSB, j0 = J * kSB;
+    int nI = I, nJ = J;
+    if (b + 1 < b1) small_decode(p, b + 1, nI, nJ);
+    if (NB == 2 && b + 1 < b1) {                       // the next block's rows land during this contraction
+      double* nA = Ops + (buf ^ 1) * 128 * KS;
+      stream_load<KG>(p, nI, nJ, nA, nA + 64 * KS, bar_s + 8 * (buf ^ 1));
+    }
+    // ---- Gauss contraction: sync = P1 - P3, async = P1 + P2
+    const double* Aw = As + (wm * 32 + lr) * KS + lk;
+    const double* Bw = Bs + (wn * 32 + lr) * KS + lk;
+    double aphi[2][4][4], apsi[2][4][4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) aphi[a][q][e] = apsi[a][q][e] = 0.0;
+#ifdef CORR2D_PROFILING
+    if (!(p.dbg & 2)) {
+#endif
+    fused_seg2<KG, KS>(apsi, aphi, Aw, Bw, 0, 2 * KG);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) aphi[a][q][e] += apsi[a][q][e];
+    fused_seg1<KG, KS>(apsi, Aw + KG, Bw + KG);
+#ifdef CORR2D_PROFILING
+    }
+#endif
+    if (b == b0) SMALL_STAMP(kTraceK1, 3);
+    // ---- max|.| / finite check on |x|'s bit pattern (diagonal: the upper triangle)
+    const int rows = min(kSB, p.n1 - i0), cols = min(kSB, p.n2 - j0);
+    if (!diag && rows == kSB && cols == kSB) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            mphi = max(mphi, abs_bits(aphi[mt][nt][q]));
+            mpsi = max(mpsi, abs_bits(apsi[mt][nt][q]));
+          }
+    } else {
+      fused_max_edge(aphi, apsi, rows, cols, diag, wm, wn, lr, lk, mphi, mpsi);
+    }
+    // ---- staging slots: a mirrored block takes both (or stores twice through one)
+    const bool mirror = p.homo && !diag;
+    int s0 = 0;
+    const bool both = mirror && p.nslots == 2;
+    if (tid == 0) {
+      if (both || p.nslots == 1 || prev_mask == 3) bulk_wait_read();
+      else bulk_wait_read1();                          // the previous block's group may still read its slot
+    }
+    if (!both && p.nslots == 2 && prev_mask == 1) s0 = 1;
+    prev_mask = both ? 3 : (1 << s0);
+    __syncthreads();                                   // every warp's DMMAs have read the operand buffer
+    double* C0 = Cst + 8192 * s0;
+    stage_tile(C0, aphi, apsi, false, wm, wn, lr, lk);
+    if (both) stage_tile(Cst + 8192, aphi, apsi, true, wm, wn, lr, lk);
+    if (diag) {        // below the diagonal: the transpose of the upper triangle (exact symmetry)
+      __syncthreads();
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+            if (r < c) {
+              const int o = swz(c, r);
+              C0[o] = aphi[mt][nt][q];
+              C0[4096 + o] = neg_bits(apsi[mt][nt][q]);
+            } else if (r == c) {
+              C0[4096 + swz(r, r)] = 0.0;
+            }
+          }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> TMA
+    __syncthreads();
+    // odd n2: the maps cover the even width, the last column leaves by plain stores
+    if ((p.n2 & 1) && j0 + cols == p.n2 && tid < rows) {
+      __stcs(p.phi + (long long)(i0 + tid) * p.ld_out + p.n2 - 1, C0[swz(tid, cols - 1)]);
+      __stcs(p.psi + (long long)(i0 + tid) * p.ld_out + p.n2 - 1, C0[4096 + swz(tid, cols - 1)]);
+    }
+#ifdef CORR2D_PROFILING
+    if (p.dbg & 1) {
+      if (NB == 1 && b + 1 < b1) stream_load<KG>(p, nI, nJ, Ops, Ops + 64 * KS, bar_s);
+      if (b == b0) SMALL_STAMP(kTraceK1, 4);
+      I = nI; J = nJ;
+      continue;
+    }
+#endif
+    if (tid == 0) {
+      fused_store_tile(&map_phi, &map_psi, cst_s + 65536u * s0, i0, j0);
+      if (both) fused_store_tile(&map_phi, &map_psi, cst_s + 65536u, j0, i0);
+    }
+    if (mirror && !both) {   // one slot: the mirror goes through it once the direct tile was read
+      if (tid == 0) bulk_wait_read();
+      __syncthreads();
+      stage_tile(C0, aphi, apsi, true, wm, wn, lr, lk);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      if (tid == 0) fused_store_tile(&map_phi, &map_psi, cst_s, j0, i0);
+    }
+    // one operand buffer: the next block's rows, issued after this block's
+    // proxy fences (a fence.proxy.async in the issuing thread would otherwise
+    // wait for the copies to land)
+    if (NB == 1 && b + 1 < b1) stream_load<KG>(p, nI, nJ, Ops, Ops + 64 * KS, bar_s);
+    if (b == b0) SMALL_STAMP(kTraceK1, 4);
+    if (b == b0 + 2) SMALL_STAMP(kTraceK1, 7);
+    I = nI;
+    J = nJ;
+  }
+  small_publish(p, mphi, mpsi, lane, warp, tid);
+  if (tid == 0) bulk_wait_read();                     // the staging must outlive the stores' reads
+  SMALL_STAMP(kTraceK1, 5);
+}
+
 // Per-(device, m) table of the fused path: [2][nsp][gp] doubles -- role A rows
 // s (slot of the Gauss segments, corr2d.h CORR2D_PACK_F64_GAUSS) hold
 // pa cos(2 pi w t / m) + qa (-sin(2 pi w t / m)) for t < m (Norm is applied in
@@ -1527,6 +1813,27 @@ static int fused_plane_map(CUtensorMap* map, double* base, long long ld, long lo
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(CORR2D_ERR_CUDA, "cuTensorMapEncodeTiled(small planes) failed (" + std::to_string((int)r) + ")");
   return CORR2D_OK;
+}
+
+// operand row pitch of the streamed contraction
+static int stream_ks(int kg) { return small_ops_pitch(kg); }
+
+// CORR2D_SMALL_STREAM=0 (read once) selects the one-CTA-per-block contraction
+static bool stream_disabled() {
+  static const int v = [] {
+    const char* e = getenv("CORR2D_SMALL_STREAM");
+    return (e && e[0] == '0') ? 1 : 0;
+  }();
+  return v != 0;
+}
+
+// CORR2D_SMALL_STREAM_NB=2 (read once): one streamed-contraction CTA per SM
+static int stream_nb() {
+  static const int v = [] {
+    const char* e = getenv("CORR2D_SMALL_STREAM_NB");
+    return (e && e[0] == '2') ? 2 : 0;
+  }();
+  return v;
 }
 
 static int launch_fused(const SmallParams& q, cudaStream_t st) {
@@ -1633,7 +1940,7 @@ extern "C" int corr2d_small_launches(int n1, int n2, int homo) {
 #endif
 }
 
-extern "C" int corr2d_small_ops_depth(int m) { return (m >= 2 && m <= kSMaxM) ? 3 * gauss_kg(m) : -1; }
+extern "C" int corr2d_small_ops_depth(int m) { return (m >= 2 && m <= kSMaxM) ? small_ops_pitch(gauss_kg(m)) : -1; }
 
 extern "C" int corr2d_correlate_small_f64(
     int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
@@ -1680,6 +1987,7 @@ extern "C" int corr2d_correlate_small_f64(
   p.vec = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
   p.status1 = status1; p.status2 = homo ? nullptr : status2; p.stats = stats; p.work = work;
 #ifdef CORR2D_PROFILING
+  if (const char* e = getenv("CORR2D_DEBUG_SKIP")) p.dbg = atoi(e);
   if (const char* e = getenv("CORR2D_SMALL_TRACE"))
     if (e[0] == '1') {
       static unsigned long long* tbuf = nullptr;
@@ -1712,7 +2020,7 @@ extern "C" int corr2d_correlate_small_f64(
   if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
   const int prep_blocks = p.nb1 + (homo ? 0 : (n2 + kSThreads - 1) / kSThreads);
   const size_t prep_smem = ((size_t)p.yrows * kYS + 48 * (size_t)p.mpad + 15 * (size_t)p.kg +
-                            2 * (size_t)kSThreads * 3 * p.kg) * sizeof(double);
+                            2 * (size_t)kSThreads * ld_ops) * sizeof(double);
   const size_t ops = 2 * (size_t)kSB * p.ks * sizeof(double);
   const size_t stage = 2 * (size_t)kSB * kCS * sizeof(double);
   const size_t smem = ops > stage ? ops : stage;
@@ -1722,7 +2030,7 @@ extern "C" int corr2d_correlate_small_f64(
     cudaFuncSetAttribute(small_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(worst_ops > stage ? worst_ops : stage));
     cudaFuncSetAttribute(small_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16 + 2 * kSThreads * 48) *
+                         (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16 + 2 * kSThreads * 52) *
                                sizeof(double)));   // m = 32: kg = 16
     attr_set = true;
   }
@@ -1741,10 +2049,57 @@ extern "C" int corr2d_correlate_small_f64(
   cfg.dynamicSmemBytes = prep_smem;
   cudaLaunchKernelEx(&cfg, small_prep_kernel, p);
   if (int e = check_launch("small_prep_kernel")) return e;
-  cfg.gridDim = dim3((unsigned)blocks);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchKernelEx(&cfg, small_contract_kernel, p);
-  int code = check_launch("small_contract_kernel");
+  // streamed contraction (persistent, TMA stores) when the planes take 16-B
+  // tensor stores; the one-CTA-per-block kernel otherwise
+  const bool streamed = p.vec && n2 >= 2 && !stream_disabled();
+  long long k2_ctas = blocks;
+  if (streamed) {
+    p.tiles = blocks;
+    // two CTAs per SM (one operand buffer and one staging slot each) when
+    // both fit, else one CTA per SM with a prefetch buffer (and two slots when
+    // they fit); CORR2D_SMALL_STREAM_NB=2 forces the latter
+    const size_t ops1 = 128 * (size_t)stream_ks(p.kg) * sizeof(double);
+    const int nb = (2 * (1024 + 65536 + ops1 + 1024) <= 228 * 1024 && stream_nb() != 2) ? 1 : 2;
+    p.nctas = (int)std::min<long long>(blocks, (long long)(3 - nb) * device_sms());
+    k2_ctas = p.nctas;
+    const size_t ops_b = nb * ops1;
+    p.nslots = (nb == 2 && 1024 + 2 * 65536 + ops_b <= 226 * 1024) ? 2 : 1;
+    CUtensorMap map_phi, map_psi;
+    memset(&map_phi, 0, sizeof(map_phi));
+    memset(&map_psi, 0, sizeof(map_psi));
+    if (int e = fused_plane_map(&map_phi, p.phi, p.ld_out, p.n1, p.n2 & ~1)) return e;
+    if (int e = fused_plane_map(&map_psi, p.psi, p.ld_out, p.n1, p.n2 & ~1)) return e;
+    static bool sattr = false;
+    if (!sattr) {
+      const int worst = 226 * 1024;
+      cudaFuncSetAttribute(small_stream_kernel<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<12, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<12, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      cudaFuncSetAttribute(small_stream_kernel<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst);
+      sattr = true;
+    }
+    cfg.gridDim = dim3((unsigned)p.nctas);
+    cfg.dynamicSmemBytes = 1024 + (size_t)p.nslots * 65536 + ops_b;
+    switch (p.kg * 4 + nb) {
+      case 17: cudaLaunchKernelEx(&cfg, small_stream_kernel<4, 1>, p, map_phi, map_psi); break;
+      case 33: cudaLaunchKernelEx(&cfg, small_stream_kernel<8, 1>, p, map_phi, map_psi); break;
+      case 49: cudaLaunchKernelEx(&cfg, small_stream_kernel<12, 1>, p, map_phi, map_psi); break;
+      case 65: cudaLaunchKernelEx(&cfg, small_stream_kernel<16, 1>, p, map_phi, map_psi); break;
+      case 18: cudaLaunchKernelEx(&cfg, small_stream_kernel<4, 2>, p, map_phi, map_psi); break;
+      case 34: cudaLaunchKernelEx(&cfg, small_stream_kernel<8, 2>, p, map_phi, map_psi); break;
+      case 50: cudaLaunchKernelEx(&cfg, small_stream_kernel<12, 2>, p, map_phi, map_psi); break;
+      default: cudaLaunchKernelEx(&cfg, small_stream_kernel<16, 2>, p, map_phi, map_psi); break;
+    }
+  } else {
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchKernelEx(&cfg, small_contract_kernel, p);
+  }
+  int code = check_launch(streamed ? "small_stream_kernel" : "small_contract_kernel");
 #ifdef CORR2D_PROFILING
   if (p.trace) {       // per-phase timeline (ns after the first K1 stamp): min / median / max over CTAs
     std::vector<unsigned long long> h(8 * (size_t)(kTraceK1 + blocks));
@@ -1763,9 +2118,10 @@ extern "C" int corr2d_correlate_small_f64(
     fprintf(stderr, "small path trace (m %d, %d x %d, %s):\n", m, n1, n2, homo ? "homo" : "hetero");
     const char* k1n[8] = {"K1 start", "K1 after wait", "K1 samples in", "K1 stats done", "K1 dft done",
                           "K1 rows written", "", "K1 slots staged"};
-    const char* k2n[6] = {"K2 start", "K2 after wait", "K2 operands in", "K2 mma done", "K2 stores issued", "K2 end"};
+    const char* k2n[8] = {"K2 start", "K2 after wait", "K2 operands in", "K2 mma done", "K2 stores issued", "K2 end",
+                          "K2 block 2 top", "K2 block 2 issued"};
     for (int k : {0, 1, 2, 3, 4, 7, 5}) row(k1n[k], 0, prep_blocks, k);
-    for (int k = 0; k < 6; ++k) row(k2n[k], kTraceK1, (int)blocks, k);
+    for (int k : {0, 1, 2, 3, 4, 6, 7, 5}) row(k2n[k], kTraceK1, (int)k2_ctas, k);
   }
 #endif
   return code;

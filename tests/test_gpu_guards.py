@@ -146,6 +146,10 @@ CASES = [
     ("hilbert", 300, None, 50, "float64", None, None, "hilbert"),
     ("small-homo", 500, None, 16, "float64", None, None, "fourier"),
     ("small-hetero", 200, 333, 31, "float64", None, None, "fourier"),
+    # more 64 x 64 blocks than SMs: K1 + the streamed (persistent, TMA-store) contraction
+    ("small-stream-homo", 1100, None, 21, "float64", None, None, "fourier"),
+    ("small-stream-homo-1slot", 1090, None, 32, "float64", None, None, "fourier"),
+    ("small-stream-hetero", 1000, 1023, 11, "float64", None, None, "fourier"),
 ]
 
 

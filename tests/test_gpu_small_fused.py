@@ -161,3 +161,55 @@ def test_fused_and_two_kernel_paths_agree(monkeypatch):
     two = P.correlate_ft(dyn(v))
     sc = scale_of(two.sync, two.asyn)
     assert rel_err(fused.sync, two.sync, sc) <= 1e-13 and rel_err(fused.asyn, two.asyn, sc) <= 1e-13
+
+
+# maps with more 64 x 64 blocks than SMs: K1 + the streamed contraction
+# (small_stream_kernel: persistent CTAs, double-buffered operand rows, TMA
+# tensor stores from one or two staging slots; m = 29..32 has one slot, so a
+# mirrored block stores twice through it)
+@pytest.mark.parametrize("n1,n2,m", [(1100, 1100, 21), (1090, 1090, 32), (1000, 1023, 11), (2000, 1500, 21),
+                                     (1153, 700, 5), (700, 1153, 30), (1201, 1201, 2), (9000, 130, 13)])
+def test_streamed_contraction_matches_oracle(n1, n2, m):
+    from paper_1808_00685_b200 import _abi
+    lib = _abi.load()
+    homo = n1 == n2
+    assert lib.corr2d_small_launches(n1, n2, 1 if homo else 0) == 2
+    rng = np.random.default_rng(n1 + 3 * n2 + m)
+    v1 = rng.normal(size=(m, n1)) * np.linspace(0.5, 4.0, n1)
+    if homo:
+        res = P.correlate_ft(dyn(v1))
+        s, a, _ = O.correlate_ft(v1)
+    else:
+        v2 = rng.normal(size=(m, n2))
+        res = P.correlate_ft(dyn(v1), dyn(v2))
+        s, a, _ = O.correlate_ft(v1, v2)
+    sc = scale_of(s, a)
+    assert rel_err(res.sync, s, sc) <= TOL64 and rel_err(res.asyn, a, sc) <= TOL64
+    if homo:
+        assert np.array_equal(res.sync, res.sync.T) and np.array_equal(res.asyn, -res.asyn.T)
+        assert np.all(np.diag(res.asyn) == 0)
+
+
+def test_streamed_contraction_flags_nonfinite_and_resets():
+    """The streamed contraction's stats: a non-finite input is reported, and the
+    next call on the same plan is clean (K1 zeroes, the contraction publishes)."""
+    from paper_1808_00685_b200 import api
+    rng = np.random.default_rng(8)
+    m, n = 21, 1300
+    t = np.arange(m, dtype=float)
+    x = rng.normal(size=(m, n))
+    bad = x.copy()
+    bad[5, 1234] = np.inf
+    with pytest.raises(Exception):
+        P.corr2d(P.SpectralDataset(np.arange(n, dtype=float), t, bad))
+    ds = P.SpectralDataset(np.arange(n, dtype=float), t, x)
+    plan, _ = api.build_plan(ds, None, P.PreprocessSpec(), dtype="float64")
+    assert plan.small and plan.launches_per_step == 2
+    outs = []
+    for _ in range(3):
+        plan.launch()
+        engine.sync()
+        plan.check()
+        outs.append(plan.phi.cpu().numpy().copy())
+        assert not plan.work.cpu().numpy().any()
+    assert all(np.array_equal(o, outs[0]) for o in outs)

@@ -4,6 +4,8 @@
 //   0: 128 one-row bulk copies (cp.async.bulk, 512 B each) per tile
 //   1: 8 TMA tensor stores per tile (64-row x 16-column fp64 boxes, SWIZZLE_128B)
 //   2: plain 16-byte st.global.cs by all 128 threads, from the staging
+//   3: as 1, with two staging slots (a slot is restaged once the store two
+//      tiles back has read it: cp.async.bulk.wait_group.read 1)
 // Ring of independent output buffers > 4 x L2, CUDA events around each launch.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -23,7 +25,12 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
   for (int t = 0; t < p.tiles; ++t) {
     const long long b = (long long)blockIdx.x * p.tiles + t;
     const int I = (int)(b / p.T2), J = (int)(b % p.T2);
-    if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    if (p.mode == 3) {
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      Cphi = sm + (t & 1) * 8192;
+    } else if (warp == 0) {
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
     __syncthreads();
     for (int i = tid; i < 64 * 32; i += 128) {   // "stage": touch every 16 B
       reinterpret_cast<double2*>(Cphi)[i] = make_double2(t, i);
@@ -41,7 +48,7 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
         }
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
-    } else if (p.mode == 1) {
+    } else if (p.mode == 1 || p.mode == 3) {
       if (tid == 0) {
         for (int q = 0; q < 4; ++q) {
           asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n"
@@ -59,7 +66,7 @@ __global__ void __launch_bounds__(128, 1) k(const __grid_constant__ CUtensorMap 
       }
     }
   }
-  if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+  if (tid == 0 || warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
 }
 
 int main() {
@@ -85,12 +92,13 @@ int main() {
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
   }
-  const size_t smem = 2 * 64 * 66 * 8;
+  const size_t smem = 2 * 65536;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  const char* names[3] = {"bulk rows (128 x 512 B)", "TMA tensor boxes (8 x 8 KB)", "st.global.cs v2"};
+  const char* names[4] = {"bulk rows (128 x 512 B)", "TMA tensor boxes (8 x 8 KB)", "st.global.cs v2",
+                          "TMA boxes, 2 staging slots"};
   for (int tp : {1, 6}) {
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
       std::vector<float> v;
       for (int it = 0; it < 60; ++it) {
         const int r = it % R;
