@@ -1,25 +1,31 @@
 // The whole small-m correlation (corr2d_correlate_small_f64): fp64,
 // 2 <= m <= 32, no resampling -- the cfg1 (m = 11) and cfg2 (m = 21) shapes,
-// where a step is bound by launch latency, one DRAM round trip and the output
-// write (cfg1: 16 MB of planes, 2.5 us at HBM peak).  Two kernels, chained by
-// programmatic dependent launch (the second grid launches while the first
-// runs and waits at griddepcontrol.wait for its completion -- a kernel
-// boundary, never a wait of one CTA on another):
+// where a step is bound by latency, one DRAM round trip and the output write
+// (cfg1: 16 MB of planes, cfg2: 48 MB).  Every kernel here chains to its
+// predecessor by programmatic dependent launch and orders memory with
+// griddepcontrol.wait -- a kernel boundary, never a wait of one CTA on another.
 //
-// small_prep_kernel   -- K1 once per channel, one lane per channel: the
-//   reference's statistics in its order (sequential sums: bitwise-equal
-//   reference / sigma / values), the real DFT of each warp's 32 channels as an
-//   FP64 tensor-core product Y[bins x channels] = W[bins x t] . y[t x channels]
-//   (W: cos / -sin rows from a per-m host table), then the
-//   CORR2D_PACK_F64_GAUSS operand rows (three real products per bin).
-// small_contract_kernel -- one CTA per 64 x 64 output block (homo: the upper
-//   triangle, mirrored): operand rows from L2 into shared memory, the Gauss
-//   contraction on the FP64 tensor pipe with two independent accumulator
-//   chains, both planes staged in shared memory and written as coalesced rows
-//   plus the mirror (sync^T, -async^T), diagonal blocks symmetrised, with the
-//   max|.| / finite reduction fused.  Status / stat words are self-resetting:
-//   the last CTA to finish (an arrival counter, never a wait) publishes and
-//   re-zeroes them.
+// small_fused_kernel (maps with at most one 64 x 64 output block per SM; cfg1)
+//   -- ONE kernel: each CTA centres its block's channels, builds their Gauss
+//   operand rows with one FP64 tensor-core product per role, contracts them
+//   and writes both planes (+ the homo mirror) by TMA tensor stores.
+// Larger maps (cfg2): two kernels.
+//   small_rows_kernel -- K1 once per channel: 64 channels per CTA, the
+//   reference's statistics in its order (one lane per channel, sequential
+//   sums: bitwise-equal reference / sigma / values), then the
+//   CORR2D_PACK_F64_GAUSS operand rows of every role as ONE FP64 tensor-core
+//   product (the rfft rows already combined into the Gauss slots), copied out
+//   by one bulk copy per warp and role.  It only reads global memory before
+//   its griddepcontrol.wait, so it overlaps the previous call's contraction.
+//   small_stream_kernel -- persistent contraction, two CTAs per SM, each
+//   walking a contiguous run of 64 x 64 blocks: operand rows by cp.async
+//   (issued as soon as the block's DMMAs have read the buffer), the Gauss
+//   contraction with two accumulator chains, both planes staged swizzled and
+//   written by TMA tensor stores issued by one thread (no warp waits on its
+//   own stores); max|.| / finite folded into the fragments.
+//   small_contract_kernel -- one CTA per block with plain stores, for planes
+//   that are not 16-B aligned with an even row pitch.
+// Status / stat words are self-resetting (no CTA ever waits for another).
 //
 // Reference path: preprocess.py:123-137, :198-259 (reference, sigma, scaling),
 // fourier.py:61-82 (rfft along the perturbation axis), fourier.py:107-123
@@ -47,7 +53,6 @@ constexpr int kSB = 64;          // output block edge (rows and columns)
 constexpr int kSThreads = 128;   // 4 warps: one lane per K1 channel, 32 x 32 warp tiles
 constexpr int kSMaxM = 32;
 constexpr int kCS = kSB + 1;     // epilogue staging stride
-constexpr int kYS = 132;         // sample rows [t][channel]: stride = 4 mod 16 doubles (conflict-free B fragments)
 
 struct SmallParams {
   const void* raw1;
@@ -67,9 +72,7 @@ struct SmallParams {
   double* sigma_out1;
   double* ref_out2;
   double* sigma_out2;
-  const double* W;          // DFT rows: [3 x 16][mpad] (cos bins 0..15 | -sin bins 0..15 | cos bins 16..31)
   int mpad;                 // m rounded up to 4 (the DMMA k-step); samples past m are 0
-  int yrows;                // rows of the sample / spectrum region: max(mpad, 2 (m / 2 + 1))
   int kg, ks;               // Gauss slots per segment; operand row stride (doubles, = 4 mod 16)
   int T1, T2;               // 64-blocks along rows / columns
   int nb1;                  // 128-channel K1 blocks of dataset 1 (dataset 2's follow)
@@ -88,6 +91,8 @@ struct SmallParams {
   long long tiles;          // streamed contraction: 64 x 64 blocks, CTAs, 64-KB staging slots
   int nctas, nslots;
   int dbg;                  // profiling builds only (CORR2D_DEBUG_SKIP): 1 no stores, 2 no DMMAs
+  int tma_ops;              // streamed contraction, one buffer: operand rows by bulk copy (else cp.async)
+  const double* G;          // small_rows_kernel: [2][nsp][gp] Gauss-row table (fused_table), gp = mpad + 2
 };
 
 // work-buffer words (int32 indices); every launch leaves them zero
@@ -152,6 +157,7 @@ struct LaneStat {
   double ref, sigma;
   int bad;
 };
+template <int kYS>                                     // the column's sample pitch (doubles)
 __device__ __forceinline__ LaneStat lane_stats(const SmallParams& p, int set, int c, bool valid, double* ys) {
   const int m = p.m;
   const int ref_mode = set ? p.ref_mode2 : p.ref_mode1;
@@ -225,28 +231,6 @@ __device__ __forceinline__ void lane_report(const SmallParams& p, int set, int c
   }
 }
 
-// The Gauss slots of bin w (spectrum R + i I) of one channel into its operand
-// row(s) (corr2d.h CORR2D_PACK_F64_GAUSS).
-__device__ __forceinline__ void put_bin(int w, int m, int kg, double norm, double R, double I, double* rowA,
-                                        double* rowB) {
-  const int H = m / 2, Iint = gauss_interior(m);
-  if (w > H) return;
-  double va, vb;
-  if (w <= Iint) {                                     // DC / interior: segments 0 and 1 at slot w
-#pragma unroll
-    for (int seg = 0; seg < 2; ++seg) {
-      gauss_values(seg, w, m, norm, R, I, va, vb);
-      if (rowA) rowA[seg * kg + w] = va;
-      if (rowB) rowB[seg * kg + w] = vb;
-    }
-  }
-  if (w >= 1) {                                        // interior at w - 1, Nyquist at slot Iint
-    gauss_values(2, w, m, norm, R, I, va, vb);
-    if (rowA) rowA[2 * kg + w - 1] = va;
-    if (rowB) rowB[2 * kg + w - 1] = vb;
-  }
-}
-
 // One Gauss segment of the depth (kg slots) into one accumulator set.
 __device__ __forceinline__ void small_mma_seg(double (&acc)[2][4][4], const double* As, const double* Bs, int ks,
                                               int k0, int kg, int wm, int wn, int lr, int lk) {
@@ -297,180 +281,6 @@ __device__ __forceinline__ void small_mma_seg2(double (&acc0)[2][4][4], double (
         dmma(acc1[mt][nt], a1[mt][0], a1[mt][1], b1[nt]);
       }
   }
-}
-
-// ---- K1: one lane per channel, 128 channels per CTA, each channel once ----
-__global__ void __launch_bounds__(kSThreads) small_prep_kernel(const __grid_constant__ SmallParams p) {
-  extern __shared__ __align__(16) double sm[];
-  const int m = p.m, mpad = p.mpad;
-  double* ys = sm;                                   // [yrows][kYS]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lr = lane >> 2, lk = lane & 3;
-  const int set = (int)blockIdx.x >= p.nb1 ? 1 : 0;
-  const int c = ((int)blockIdx.x - (set ? p.nb1 : 0)) * kSThreads + tid;
-  const int n = set ? p.n2 : p.n1;
-  const bool valid = c < n;
-  LaneStat lst;
-  // the contraction grid may launch now: it waits for this grid's completion
-  // (griddepcontrol.wait) before it reads the operand rows
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  SMALL_STAMP(0, 0);
-  // Everything up to the operand rows' copy-out only READS global memory (the
-  // samples, the tables, provided reference / sigma vectors), so it runs
-  // before griddepcontrol.wait: when the previous kernel in the stream is the
-  // contraction of an earlier call (launched with programmatic serialization),
-  // this grid starts on the SMs its CTAs free and overlaps its tail.  That
-  // contraction triggers only after its own griddepcontrol.wait, i.e. once
-  // every earlier kernel -- the writers of these inputs -- completed; its own
-  // reads of the operand rows and work words end before this grid's writes,
-  // which all follow the wait below.
-  SMALL_STAMP(0, 1);
-  // the DFT rows and the slot table into shared memory, in flight together
-  // with the samples (one DRAM round trip; the loops below then never touch
-  // global memory for them)
-  double* tab = ys + (size_t)p.yrows * kYS;
-  {
-    const int ntab = 48 * mpad + 5 * 3 * p.kg;       // even: 16-byte pieces
-    for (int i = tid; 2 * i < ntab; i += kSThreads)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
-                   ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(tab + 2 * i))), "l"(p.W + 2 * i) : "memory");
-  }
-  {
-    const void* raw = set ? p.raw2 : p.raw1;
-    const long long ld = set ? p.ld2 : p.ld1;
-    const int cc = valid ? c : n - 1;
-    const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + tid));
-    if (p.in_f32) {
-      const float* r = static_cast<const float*>(raw) + cc;
-      for (int t = 0; t < m; ++t)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 8u * kYS * t), "l"(r + (long long)t * ld) : "memory");
-    } else {
-      const double* r = static_cast<const double*>(raw) + cc;
-      for (int t = 0; t < m; ++t)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8u * kYS * t), "l"(r + (long long)t * ld) : "memory");
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-    if (p.in_f32)
-      for (int t = 0; t < m; ++t) ys[t * kYS + tid] = (double)reinterpret_cast<const float*>(ys + t * kYS + tid)[0];
-    for (int t = m; t < mpad; ++t) ys[t * kYS + tid] = 0.0;
-    SMALL_STAMP(0, 2);
-    lst = lane_stats(p, set, c, valid, ys + tid);
-  }
-  __syncthreads();                                   // every thread's table pieces have landed
-  SMALL_STAMP(0, 3);
-  // DFT of this warp's 32 channels on the FP64 tensor pipe: Y[16 bins x 8
-  // channels] tiles = W rows . y, k over t
-  const int nt3 = m / 2 >= 16 ? 3 : 2;               // bins 16.. only for m = 32
-  double acc[3][4][4];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[a][b][q] = 0.0;
-  double* yw = ys + warp * 32;
-  for (int kk = 0; kk < mpad; kk += 4) {
-    double bf[4];
-#pragma unroll
-    for (int nt = 0; nt < 4; ++nt) bf[nt] = yw[(kk + lk) * kYS + nt * 8 + lr];
-#pragma unroll
-    for (int tl = 0; tl < 3; ++tl) {
-      if (tl == 2 && nt3 < 3) break;
-      const double a0 = tab[(tl * 16 + lr) * mpad + kk + lk];
-      const double a1 = tab[(tl * 16 + lr + 8) * mpad + kk + lk];
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt) dmma(acc[tl][nt], a0, a1, bf[nt]);
-    }
-  }
-  SMALL_STAMP(0, 4);
-  // the spectra back into the warp's own sample columns (bin w: Re in row 2 w,
-  // Im in row 2 w + 1), then each lane writes its channel's operand row(s)
-  __syncwarp();                                      // the warp's DMMAs have read its columns
-#pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = nt * 8 + 2 * lk + e, w = lr + 8 * h;
-        if (w > m / 2) continue;                       // rows past 2 H + 1 are not part of the region
-        yw[(2 * w) * kYS + col] = acc[0][nt][2 * h + e];
-        yw[(2 * w + 1) * kYS + col] = acc[1][nt][2 * h + e];
-        if (nt3 == 3 && h == 0 && lr == 0) {
-          yw[32 * kYS + col] = acc[2][nt][e];          // bin 16 (m = 32: Nyquist, real)
-          yw[33 * kYS + col] = 0.0;
-        }
-      }
-  __syncwarp();
-  // every slot once (pads are 0), from the per-slot table after W: bin w and
-  // small exact coefficients -- A = Norm (pa R + qa I), B = pb R + qb I
-  // (gauss_values' operands: a + b, a, -b | a at Nyquist; c, d - c, c + d).
-  // The rows are staged per warp in shared memory in their global layout
-  // (ld_ops = 3 kg: the warp's 32 rows are one contiguous run), then leave as
-  // coalesced 16-byte stores.
-  const int ns = 3 * p.kg, ldo = (int)p.ld_ops;
-  // the warp's 32 rows staged in their global layout (row pitch ld_ops, pads
-  // zero: ONE contiguous run), then one bulk copy per role
-  double* stA = tab + 48 * mpad + 5 * ns + (size_t)warp * 32 * ldo;   // [32][ldo] per warp
-  double* stB = stA + (size_t)kSThreads * ldo;
-  const bool wantA = !set, wantB = set || p.homo;
-  {
-    // pads are zero: the warp zeroes its run with consecutive 16-B stores
-    double2* zA = reinterpret_cast<double2*>(stA);
-    double2* zB = reinterpret_cast<double2*>(stB);
-    for (int i = lane; i < 16 * ldo; i += 32) zA[i] = zB[i] = make_double2(0.0, 0.0);
-    __syncwarp();
-    // every bin's three Gauss slots from registers.  Lane l takes the bins in
-    // the rotated order w = (it + l) mod (H + 1), so the 32 lanes' rows (pitch
-    // ns) are written at different slots: few bank conflicts
-    const int kg = p.kg, H = m / 2, Iint = gauss_interior(m);
-    const double nrm = p.norm;
-    double* a = stA + lane * ldo;
-    double* b = stB + lane * ldo;
-    int w = lane % (H + 1);
-    // a runtime loop: straight-line code is fetched cold, line by line, on
-    // every step of a stream that evicts L2 (the bench's rotation does)
-#pragma unroll 1
-    for (int it = 0; it <= H; ++it, w = (w == H) ? 0 : w + 1) {
-      const double R = ys[(2 * w) * kYS + tid];
-      const double I = (w == 0 || 2 * w == m) ? 0.0 : ys[(2 * w + 1) * kYS + tid];
-      const double k = (w == 0 || 2 * w == m) ? 1.0 : 2.0;
-      const double ra = nrm * (k * R), ia = nrm * (k * I);    // a, b (x 2 exact)
-      if (w <= Iint) {                               // DC / interior: segments 0 and 1 at slot w
-        a[w] = ra + ia;      b[w] = R;               // a + b, c
-        a[kg + w] = ra;      b[kg + w] = -I - R;     // a, d - c
-      }
-      if (w >= 1) {
-        if (w <= Iint) { a[2 * kg + w - 1] = -ia; b[2 * kg + w - 1] = R - I; }   // -b, c + d
-        else { a[2 * kg + Iint] = ra; b[2 * kg + Iint] = R; }                     // Nyquist: a, c
-      }
-    }
-  }
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> bulk copy
-  __syncwarp();
-  SMALL_STAMP(0, 7);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // the previous call's contraction is done
-  // this call's stats words start at zero (the contraction grid reduces into
-  // them only after this grid completed)
-  if (blockIdx.x == 0 && tid < 3) p.stats[tid] = 0ull;
-  if (valid) lane_report(p, set, c, lst);
-  {
-    const int cw = c - lane;                         // the warp's first channel
-    const int nrow = min(32, n - cw);
-    if (nrow > 0 && lane == 0) {
-      const unsigned bytes = (unsigned)(nrow * ldo) * 8u;
-      if (wantA)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-                     ::"l"(p.opsA + (long long)cw * p.ld_ops),
-                       "r"(static_cast<unsigned>(__cvta_generic_to_shared(stA))), "r"(bytes) : "memory");
-      if (wantB)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
-                     ::"l"(p.opsB + (long long)cw * p.ld_ops),
-                       "r"(static_cast<unsigned>(__cvta_generic_to_shared(stB))), "r"(bytes) : "memory");
-      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;\n" ::: "memory");
-    }
-  }
-  SMALL_STAMP(0, 5);
 }
 
 __device__ __noinline__ void small_publish(const SmallParams& p, unsigned long long mphi, unsigned long long mpsi,
@@ -707,71 +517,6 @@ __device__ __noinline__ void small_publish(const SmallParams& p, unsigned long l
 static long long small_blocks(int n1, int n2, int homo) {
   const long long T1 = (n1 + kSB - 1) / kSB, T2 = (n2 + kSB - 1) / kSB;
   return homo ? T1 * (T1 + 1) / 2 : T1 * T2;
-}
-
-// Per-(device, m) DFT row table W in device memory, built once on the host in
-// double precision: row 16 k + r, column t < m holds cos(2 pi w t / m) for
-// k = 0 (bins w = r), -sin(2 pi w t / m) for k = 1 (w = r), cos for k = 2
-// (w = 16 + r); bins past m / 2 and columns past m are zero.
-static const double* dft_table(int m, int mpad, cudaStream_t st, int* rc) {
-  constexpr int kDev = 64;
-  static double* tab[kDev][kSMaxM + 1] = {};
-  static std::mutex mu;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= kDev) {
-    *rc = fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: device index >= 64");
-    return nullptr;
-  }
-  std::lock_guard<std::mutex> lock(mu);
-  if (tab[dev][m]) return tab[dev][m];
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(st, &cs);
-  if (cs != cudaStreamCaptureStatusNone) {
-    *rc = fail(CORR2D_ERR_UNSUPPORTED,
-               "corr2d_correlate_small_f64: the first call for this m on this device must not be graph-captured");
-    return nullptr;
-  }
-  const int kg = gauss_kg(m), ns = 3 * kg;
-  std::vector<double> h((size_t)48 * mpad + 5 * (size_t)ns, 0.0);
-  const double two_pi = 6.283185307179586476925286766559;
-  for (int k = 0; k < 3; ++k)
-    for (int r = 0; r < 16; ++r) {
-      const int w = (k == 2 ? 16 : 0) + r;
-      if (w > m / 2) continue;
-      for (int t = 0; t < m; ++t) {
-        const int q = (w * t) % m;
-        const double ang = two_pi * (double)q / (double)m;
-        // exact zeros of sin at 0 and pi (DC / Nyquist rows are real)
-        const double sn = (q == 0 || 2 * q == m) ? 0.0 : std::sin(ang);
-        h[(size_t)(16 * k + r) * mpad + t] = k == 1 ? -sn : std::cos(ang);
-      }
-    }
-  // per-slot table of the CORR2D_PACK_F64_GAUSS rows (corr2d.h; gauss_values):
-  // bin w, then A = Norm (pa R + qa I) and B = pb R + qb I, with a = k R,
-  // b = k I (k = 2, or 1 at DC / Nyquist where I = 0), c = R, d = -I
-  double* slot = h.data() + (size_t)48 * mpad;
-  for (int s = 0; s < ns; ++s, slot += 5) {
-    const int seg = s / kg, j = s - seg * kg, w = gauss_bin(seg, j, m);
-    slot[0] = w;
-    if (w < 0) continue;
-    const bool edge = w == 0 || (m % 2 == 0 && w == m / 2);
-    const double kk = edge ? 1.0 : 2.0, ki = edge ? 0.0 : 1.0;
-    double pa, qa, pb, qb;
-    if (seg == 0) { pa = kk; qa = kk * ki; pb = 1.0; qb = 0.0; }          // a + b, c
-    else if (seg == 1) { pa = kk; qa = 0.0; pb = -1.0; qb = -ki; }        // a, d - c
-    else if (edge) { pa = kk; qa = 0.0; pb = 1.0; qb = 0.0; }             // Nyquist: a, c
-    else { pa = 0.0; qa = -kk; pb = 1.0; qb = -1.0; }                     // -b, c + d
-    slot[1] = pa; slot[2] = qa; slot[3] = pb; slot[4] = qb;
-  }
-  double* d = nullptr;
-  if (cudaMalloc(&d, h.size() * sizeof(double)) != cudaSuccess ||
-      cudaMemcpy(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
-    *rc = check_launch("small DFT table");
-    return nullptr;
-  }
-  tab[dev][m] = d;
-  return d;
 }
 
 // =====================================================================
@@ -1512,6 +1257,29 @@ __device__ __forceinline__ void stream_load(const SmallParams& p, int I, int J, 
     for (int i = rb * OP + 2 * tid; i < kSB * OP; i += 2 * kSThreads) *reinterpret_cast<double2*>(Bs + i) = make_double2(0.0, 0.0);
 }
 
+// The same rows by cp.async (16 B per thread and copy, through L1 -- not
+// queued behind the SM's outgoing TMA tensor stores), all threads; rows past
+// the map zero-filled by a zero source size.  Completion: cp.async.wait_group.
+template <int KG>
+__device__ __forceinline__ void stream_load_lsu(const SmallParams& p, int I, int J, double* As, double* Bs) {
+  constexpr int OP = small_ops_pitch(KG);
+  constexpr int kPieces = kSB * OP / 2;                // 16-byte pieces per role
+  const int ra = min(kSB, p.n1 - I * kSB), rb = min(kSB, p.n2 - J * kSB);
+  const double* ga = p.opsA + (long long)I * kSB * OP;
+  const double* gb = p.opsB + (long long)J * kSB * OP;
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(As));
+  const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(Bs));
+#pragma unroll 4
+  for (int i = threadIdx.x; i < kPieces; i += kSThreads) {
+    const bool va = 2 * i < ra * OP, vb = 2 * i < rb * OP;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + 16u * i), "l"(ga + (va ? 2 * i : 0)),
+                 "r"(va ? 16 : 0) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sb + 16u * i), "l"(gb + (vb ? 2 * i : 0)),
+                 "r"(vb ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 // Fragments -> one staged tile at Cs (swizzled boxes); transposed: the mirror
 // (sync^T, -async^T).
 __device__ __forceinline__ void stage_tile(double* Cs, const double (&aphi)[2][4][4], const double (&apsi)[2][4][4],
@@ -1557,6 +1325,11 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
   __shared__ __align__(8) unsigned long long bars[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lk = lane & 3;
+  // accumulator row lr holds output row lrp (bits 0 and 2 of lr exchanged,
+  // through the A fragment rows): the two rows of a 16-B store's 8-lane phase
+  // then differ in bit 2, and their SWIZZLE_128B chunks in different halves
+  // of the 128-B line (no bank conflict when the planes are staged)
+  const int lrp = (lr & 2) | ((lr & 1) << 2) | (lr >> 2);
   const int wm = warp >> 1, wn = warp & 1;
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(sm_raw));
   double* Cst = sm_raw + (((1024u - (sbase & 1023u)) & 1023u) >> 3);   // staging slots (64 KB each)
@@ -1565,7 +1338,6 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
   const unsigned bar_s = static_cast<unsigned>(__cvta_generic_to_shared(bars));
   const long long b0 = (long long)blockIdx.x * p.tiles / p.nctas;
   const long long b1 = (long long)(blockIdx.x + 1) * p.tiles / p.nctas;
-  SMALL_STAMP(kTraceK1, 0);
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s) : "memory");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s + 8) : "memory");
@@ -1587,9 +1359,14 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     if (p.status2) p.status2[tid] = p.work[kWStatus2 + tid];
     p.work[kWStatus2 + tid] = 0;
   }
+#ifdef CORR2D_PROFILING
+  if (p.dbg & 4) return;                               // K1 + an empty contraction grid
+#endif
   int I, J;
   small_decode(p, b0, I, J);
-  stream_load<KG>(p, I, J, Ops, Ops + 64 * KS, bar_s);
+  const bool lsu = NB == 1 && !p.tma_ops;
+  if (lsu) stream_load_lsu<KG>(p, I, J, Ops, Ops + 64 * KS);
+  else stream_load<KG>(p, I, J, Ops, Ops + 64 * KS, bar_s);
   unsigned long long mphi = 0, mpsi = 0;
   int prev_mask = 0;                                   // staging slots the most recent store group reads
 #pragma unroll 1
@@ -1597,7 +1374,8 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     const int k = (int)(b - b0), buf = NB == 2 ? (k & 1) : 0;
     const double* As = Ops + buf * 128 * KS;
     const double* Bs = As + 64 * KS;
-    mbar_wait(bar_s + 8 * buf, (k / NB) & 1);
+    if (lsu) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    else mbar_wait(bar_s + 8 * buf, (k / NB) & 1);
     __syncthreads();                                   // zero-filled rows visible; the other buffer is free
     if (b == b0) SMALL_STAMP(kTraceK1, 2);
     if (b == b0 + 2) SMALL_STAMP(kTraceK1, 6);
@@ -1610,7 +1388,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
       stream_load<KG>(p, nI, nJ, nA, nA + 64 * KS, bar_s + 8 * (buf ^ 1));
     }
     // ---- Gauss contraction: sync = P1 - P3, async = P1 + P2
-    const double* Aw = As + (wm * 32 + lr) * KS + lk;
+    const double* Aw = As + (wm * 32 + lrp) * KS + lk;
     const double* Bw = Bs + (wn * 32 + lr) * KS + lk;
     double aphi[2][4][4], apsi[2][4][4];
 #pragma unroll
@@ -1633,7 +1411,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
 #ifdef CORR2D_PROFILING
     }
 #endif
-    if (b == b0) SMALL_STAMP(kTraceK1, 3);
+    if (b == b0 + 2) SMALL_STAMP(kTraceK1, 3);
     // ---- max|.| / finite check on |x|'s bit pattern (diagonal: the upper triangle)
     const int rows = min(kSB, p.n1 - i0), cols = min(kSB, p.n2 - j0);
     if (!diag && rows == kSB && cols == kSB) {
@@ -1647,7 +1425,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
             mpsi = max(mpsi, abs_bits(apsi[mt][nt][q]));
           }
     } else {
-      fused_max_edge(aphi, apsi, rows, cols, diag, wm, wn, lr, lk, mphi, mpsi);
+      fused_max_edge(aphi, apsi, rows, cols, diag, wm, wn, lrp, lk, mphi, mpsi);
     }
     // ---- staging slots: a mirrored block takes both (or stores twice through one)
     const bool mirror = p.homo && !diag;
@@ -1660,9 +1438,11 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     if (!both && p.nslots == 2 && prev_mask == 1) s0 = 1;
     prev_mask = both ? 3 : (1 << s0);
     __syncthreads();                                   // every warp's DMMAs have read the operand buffer
+    if (b == b0 + 2) SMALL_STAMP(kTraceK1, 0);
+    if (lsu && b + 1 < b1) stream_load_lsu<KG>(p, nI, nJ, Ops, Ops + 64 * KS);   // lands during the staging
     double* C0 = Cst + 8192 * s0;
-    stage_tile(C0, aphi, apsi, false, wm, wn, lr, lk);
-    if (both) stage_tile(Cst + 8192, aphi, apsi, true, wm, wn, lr, lk);
+    stage_tile(C0, aphi, apsi, false, wm, wn, lrp, lk);
+    if (both) stage_tile(Cst + 8192, aphi, apsi, true, wm, wn, lrp, lk);
     if (diag) {        // below the diagonal: the transpose of the upper triangle (exact symmetry)
       __syncthreads();
 #pragma unroll
@@ -1671,7 +1451,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int r = wm * 32 + mt * 16 + lr + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
+            const int r = wm * 32 + mt * 16 + lrp + 8 * (q >> 1), c = wn * 32 + nt * 8 + 2 * lk + (q & 1);
             if (r < c) {
               const int o = swz(c, r);
               C0[o] = aphi[mt][nt][q];
@@ -1681,6 +1461,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
             }
           }
     }
+    if (b == b0 + 2) SMALL_STAMP(kTraceK1, 4);
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> TMA
     __syncthreads();
     // odd n2: the maps cover the even width, the last column leaves by plain stores
@@ -1690,8 +1471,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     }
 #ifdef CORR2D_PROFILING
     if (p.dbg & 1) {
-      if (NB == 1 && b + 1 < b1) stream_load<KG>(p, nI, nJ, Ops, Ops + 64 * KS, bar_s);
-      if (b == b0) SMALL_STAMP(kTraceK1, 4);
+      if (NB == 1 && !lsu && b + 1 < b1) stream_load<KG>(p, nI, nJ, Ops, Ops + 64 * KS, bar_s);
       I = nI; J = nJ;
       continue;
     }
@@ -1703,7 +1483,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     if (mirror && !both) {   // one slot: the mirror goes through it once the direct tile was read
       if (tid == 0) bulk_wait_read();
       __syncthreads();
-      stage_tile(C0, aphi, apsi, true, wm, wn, lr, lk);
+      stage_tile(C0, aphi, apsi, true, wm, wn, lrp, lk);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncthreads();
       if (tid == 0) fused_store_tile(&map_phi, &map_psi, cst_s, j0, i0);
@@ -1711,8 +1491,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     // one operand buffer: the next block's rows, issued after this block's
     // proxy fences (a fence.proxy.async in the issuing thread would otherwise
     // wait for the copies to land)
-    if (NB == 1 && b + 1 < b1) stream_load<KG>(p, nI, nJ, Ops, Ops + 64 * KS, bar_s);
-    if (b == b0) SMALL_STAMP(kTraceK1, 4);
+    if (NB == 1 && !lsu && b + 1 < b1) stream_load<KG>(p, nI, nJ, Ops, Ops + 64 * KS, bar_s);
     if (b == b0 + 2) SMALL_STAMP(kTraceK1, 7);
     I = nI;
     J = nJ;
@@ -1720,6 +1499,131 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
   small_publish(p, mphi, mpsi, lane, warp, tid);
   if (tid == 0) bulk_wait_read();                     // the staging must outlive the stores' reads
   SMALL_STAMP(kTraceK1, 5);
+}
+
+// =====================================================================
+// K1 of the two-kernel path, operand rows by ONE tensor-core product: 64
+// channels per CTA (one lane each for the statistics), then per role
+// rows[ch][s] = scale * sum_t y[t][ch] G[s][t] on the FP64 tensor pipe (G =
+// the rfft rows of fourier.py:73 already combined into the Gauss slots, the
+// table of the fused kernel), written in the rows' global layout (pitch
+// small_ops_pitch) and copied out with one bulk copy per warp and role.
+// Everything before griddepcontrol.wait only reads global memory (see
+// small_prep_kernel).
+// =====================================================================
+template <int KG>
+__device__ __forceinline__ void rows_transform(int mpad, int gp, const double* ys, const double* Gt, double* out,
+                                               double scale, int warp, int lr, int lk) {
+  using S = FShape<KG>;
+  constexpr int OP = small_ops_pitch(KG);
+  double acc[S::NNT][4];
+#pragma unroll
+  for (int a = 0; a < S::NNT; ++a)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[a][q] = 0.0;
+  const int ch = 16 * warp + lr;
+  const double* y = ys + lk * kFYP + ch;
+  const double* g = Gt + lr * gp + lk;
+#pragma unroll 2
+  for (int kk = 0; kk < mpad; kk += 4) {
+    const double a0 = y[kk * kFYP];
+    const double a1 = y[kk * kFYP + 8];
+#pragma unroll
+    for (int nt = 0; nt < S::NNT; ++nt) dmma(acc[nt], a0, a1, g[nt * 8 * gp + kk]);
+  }
+#pragma unroll
+  for (int nt = 0; nt < S::NNT; ++nt) {
+    const int c = nt * 8 + 2 * lk;
+    if (c < 3 * KG) {                                  // slots past 3 kg: the row's pad (zeroed by the caller)
+      *reinterpret_cast<double2*>(out + ch * OP + c) = make_double2(acc[nt][0] * scale, acc[nt][1] * scale);
+      *reinterpret_cast<double2*>(out + (ch + 8) * OP + c) = make_double2(acc[nt][2] * scale, acc[nt][3] * scale);
+    }
+  }
+}
+
+template <int KG>
+__global__ void __launch_bounds__(kSThreads) small_rows_kernel(const __grid_constant__ SmallParams p) {
+  using SH = FShape<KG>;
+  constexpr int OP = small_ops_pitch(KG);
+  extern __shared__ __align__(16) double sm[];
+  const int m = p.m, mpad = p.mpad, gp = p.mpad + 2;
+  double* Gs = sm;                                     // [2][NSP][gp]
+  double* ys = Gs + 2 * SH::NSP * gp;                  // [mpad][kFYP]
+  double* rowsA = ys + mpad * kFYP;                    // [64][OP]
+  double* rowsB = rowsA + kSB * OP;                    // [64][OP]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lk = lane & 3;
+  const int set = (int)blockIdx.x >= p.nb1 ? 1 : 0;
+  const int c0 = ((int)blockIdx.x - (set ? p.nb1 : 0)) * kSB;
+  const int n = set ? p.n2 : p.n1;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+  SMALL_STAMP(0, 0);
+  {
+    const int nt = SH::NSP * gp;                       // 16-byte pieces of both tables
+    for (int i = tid; i < nt; i += kSThreads)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n"
+                   ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(Gs + 2 * i))), "l"(p.G + 2 * i) : "memory");
+    const void* raw = set ? p.raw2 : p.raw1;
+    const long long ld = set ? p.ld2 : p.ld1;
+#pragma unroll 1
+    for (int idx = tid; idx < m * kSB; idx += kSThreads) {
+      const int t = idx >> 6, ch = idx & 63, c = c0 + ch;
+      const bool v = c < n;
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(ys + t * kFYP + ch));
+      if (p.in_f32) {
+        const float* src = static_cast<const float*>(raw) + (long long)t * ld + (v ? c : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 4 : 0) : "memory");
+      } else {
+        const double* src = static_cast<const double*>(raw) + (long long)t * ld + (v ? c : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(v ? 8 : 0) : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    for (int i = tid; i < (mpad - m) * kSB; i += kSThreads)   // sample rows past m stay zero
+      ys[(m + (i >> 6)) * kFYP + (i & 63)] = 0.0;
+    if (OP > 3 * KG)                                   // row pads
+      for (int i = tid; i < 2 * kSB; i += kSThreads)
+        for (int s = 3 * KG; s < OP; ++s) rowsA[i * OP + s] = 0.0;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  }
+  __syncthreads();
+  SMALL_STAMP(0, 2);
+  LaneStat lst{0.0, 0.0, 0};
+  const int c = c0 + tid;
+  const bool valid = c < n;
+  if (tid < kSB) {
+    if (p.in_f32)
+      for (int t = 0; t < m; ++t) ys[t * kFYP + tid] = (double)reinterpret_cast<const float*>(ys + t * kFYP + tid)[0];
+    lst = lane_stats<kFYP>(p, set, c, valid, ys + tid);
+  }
+  __syncthreads();
+  SMALL_STAMP(0, 3);
+  const bool wantA = !set, wantB = set || p.homo;
+  if (wantA) rows_transform<KG>(mpad, gp, ys, Gs, rowsA, p.norm, warp, lr, lk);
+  if (wantB) rows_transform<KG>(mpad, gp, ys, Gs + SH::NSP * gp, rowsB, 1.0, warp, lr, lk);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> bulk copy
+  __syncwarp();
+  SMALL_STAMP(0, 7);
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // the previous call's contraction is done
+  if (blockIdx.x == 0 && tid < 3) p.stats[tid] = 0ull;
+  if (tid < kSB && valid) lane_report(p, set, c, lst);
+  {
+    const int cw = c0 + 16 * warp;                     // the warp's 16 rows
+    const int nrow = min(16, n - cw);
+    if (nrow > 0 && lane == 0) {
+      const unsigned bytes = (unsigned)(nrow * OP) * 8u;
+      if (wantA)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(p.opsA + (long long)cw * OP),
+                       "r"(static_cast<unsigned>(__cvta_generic_to_shared(rowsA + 16 * warp * OP))), "r"(bytes) : "memory");
+      if (wantB)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(p.opsB + (long long)cw * OP),
+                       "r"(static_cast<unsigned>(__cvta_generic_to_shared(rowsB + 16 * warp * OP))), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;\n" ::: "memory");
+    }
+  }
+  SMALL_STAMP(0, 5);
 }
 
 // Per-(device, m) table of the fused path: [2][nsp][gp] doubles -- role A rows
@@ -1825,6 +1729,12 @@ static bool stream_disabled() {
     return (e && e[0] == '0') ? 1 : 0;
   }();
   return v != 0;
+}
+
+// a 0/1 switch from the environment, read once per name
+static int env_flag(const char* name) {
+  const char* e = getenv(name);
+  return (e && e[0] == '1') ? 1 : 0;
 }
 
 // CORR2D_SMALL_STREAM_NB=2 (read once): one streamed-contraction CTA per SM
@@ -1980,7 +1890,6 @@ extern "C" int corr2d_correlate_small_f64(
   p.norm = norm_const;
   p.ref_out1 = ref_out1; p.sigma_out1 = sigma_out1; p.ref_out2 = ref_out2; p.sigma_out2 = sigma_out2;
   p.mpad = (m + 3) / 4 * 4;
-  p.yrows = p.mpad > 2 * (m / 2 + 1) ? p.mpad : 2 * (m / 2 + 1);
   p.kg = gauss_kg(m);
   p.T1 = (n1 + kSB - 1) / kSB; p.T2 = (n2 + kSB - 1) / kSB;
   p.phi = phi; p.psi = psi; p.ld_out = ld_out;
@@ -2011,16 +1920,16 @@ extern "C" int corr2d_correlate_small_f64(
   if (fused) return launch_fused(p, st);
   if (!ops_a || !ops_b) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
   int rc = CORR2D_OK;
-  p.W = dft_table(m, p.mpad, st, &rc);
-  if (!p.W) return rc;
+  const int nsp = (3 * p.kg + 7) / 8 * 8, gp = p.mpad + 2;
+  p.G = fused_table(m, nsp, gp, st, &rc);
+  if (!p.G) return rc;
   p.ks = (3 * p.kg + 11) / 16 * 16 + 4;
-  p.nb1 = (n1 + kSThreads - 1) / kSThreads;
+  p.nb1 = (n1 + kSB - 1) / kSB;
   p.opsA = ops_a; p.opsB = ops_b; p.ld_ops = ld_ops;
   const long long blocks = small_blocks(n1, n2, homo);
   if (blocks > 0x7fffffffLL) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_correlate_small_f64: too many blocks");
-  const int prep_blocks = p.nb1 + (homo ? 0 : (n2 + kSThreads - 1) / kSThreads);
-  const size_t prep_smem = ((size_t)p.yrows * kYS + 48 * (size_t)p.mpad + 15 * (size_t)p.kg +
-                            2 * (size_t)kSThreads * ld_ops) * sizeof(double);
+  const int prep_blocks = p.nb1 + (homo ? 0 : (n2 + kSB - 1) / kSB);
+  const size_t prep_smem = (2 * (size_t)nsp * gp + (size_t)p.mpad * kFYP + 2 * (size_t)kSB * ld_ops) * sizeof(double);
   const size_t ops = 2 * (size_t)kSB * p.ks * sizeof(double);
   const size_t stage = 2 * (size_t)kSB * kCS * sizeof(double);
   const size_t smem = ops > stage ? ops : stage;
@@ -2029,9 +1938,11 @@ extern "C" int corr2d_correlate_small_f64(
     const size_t worst_ops = 2 * (size_t)kSB * 52 * sizeof(double);
     cudaFuncSetAttribute(small_contract_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(worst_ops > stage ? worst_ops : stage));
-    cudaFuncSetAttribute(small_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(((size_t)(kSMaxM + 2) * kYS + 48 * kSMaxM + 15 * 16 + 2 * kSThreads * 52) *
-                               sizeof(double)));   // m = 32: kg = 16
+    const int worst_rows = (int)((2 * 48 * 34 + 32 * kFYP + 2 * kSB * 52) * sizeof(double));   // m = 32: kg = 16
+    cudaFuncSetAttribute(small_rows_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst_rows);
+    cudaFuncSetAttribute(small_rows_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst_rows);
+    cudaFuncSetAttribute(small_rows_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst_rows);
+    cudaFuncSetAttribute(small_rows_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, worst_rows);
     attr_set = true;
   }
   // programmatic dependent launch for both grids: each launches while its
@@ -2047,8 +1958,13 @@ extern "C" int corr2d_correlate_small_f64(
   cfg.numAttrs = 1;
   cfg.gridDim = dim3((unsigned)prep_blocks);
   cfg.dynamicSmemBytes = prep_smem;
-  cudaLaunchKernelEx(&cfg, small_prep_kernel, p);
-  if (int e = check_launch("small_prep_kernel")) return e;
+  switch (p.kg) {
+    case 4: cudaLaunchKernelEx(&cfg, small_rows_kernel<4>, p); break;
+    case 8: cudaLaunchKernelEx(&cfg, small_rows_kernel<8>, p); break;
+    case 12: cudaLaunchKernelEx(&cfg, small_rows_kernel<12>, p); break;
+    default: cudaLaunchKernelEx(&cfg, small_rows_kernel<16>, p); break;
+  }
+  if (int e = check_launch("small_rows_kernel")) return e;
   // streamed contraction (persistent, TMA stores) when the planes take 16-B
   // tensor stores; the one-CTA-per-block kernel otherwise
   const bool streamed = p.vec && n2 >= 2 && !stream_disabled();
@@ -2084,6 +2000,7 @@ extern "C" int corr2d_correlate_small_f64(
     }
     cfg.gridDim = dim3((unsigned)p.nctas);
     cfg.dynamicSmemBytes = 1024 + (size_t)p.nslots * 65536 + ops_b;
+    p.tma_ops = env_flag("CORR2D_SMALL_TMA_OPS");
     switch (p.kg * 4 + nb) {
       case 17: cudaLaunchKernelEx(&cfg, small_stream_kernel<4, 1>, p, map_phi, map_psi); break;
       case 33: cudaLaunchKernelEx(&cfg, small_stream_kernel<8, 1>, p, map_phi, map_psi); break;
@@ -2120,8 +2037,13 @@ extern "C" int corr2d_correlate_small_f64(
                           "K1 rows written", "", "K1 slots staged"};
     const char* k2n[8] = {"K2 start", "K2 after wait", "K2 operands in", "K2 mma done", "K2 stores issued", "K2 end",
                           "K2 block 2 top", "K2 block 2 issued"};
+    const char* k2s[8] = {"K2 blk2 stage begin", "K2 after wait", "K2 blk0 operands in", "K2 blk2 mma done",
+                          "K2 blk2 staged", "K2 end", "K2 blk2 top", "K2 blk2 issued"};
     for (int k : {0, 1, 2, 3, 4, 7, 5}) row(k1n[k], 0, prep_blocks, k);
-    for (int k : {0, 1, 2, 3, 4, 6, 7, 5}) row(k2n[k], kTraceK1, (int)k2_ctas, k);
+    if (streamed)
+      for (int k : {1, 2, 6, 3, 0, 4, 7, 5}) row(k2s[k], kTraceK1, (int)k2_ctas, k);
+    else
+      for (int k = 0; k < 6; ++k) row(k2n[k], kTraceK1, (int)k2_ctas, k);
   }
 #endif
   return code;
