@@ -356,13 +356,24 @@ def run_b200(args, case, wl, world, rank, local):
         with ClockSampler(local) as clocks:
             # ---- warmup (W steps), then keep the GPU under the same load for
             #      ~0.3 s so the clock sampler sees the steady state around the timed region
+            t_w = time.time()
             for _ in range(args.warmup):
                 step()
             torch.cuda.synchronize()
-            t_load = time.time()
-            while time.time() - t_load < 0.3:
-                step()
-                torch.cuda.synchronize()
+            n_load = 0
+            if world == 1:
+                t_load = time.time()
+                while time.time() - t_load < 0.3:
+                    step()
+                    torch.cuda.synchronize()
+            else:
+                # every rank must run the same number of steps (each step
+                # holds collectives): the count comes from the slowest rank
+                per = (time.time() - t_w) / max(1, args.warmup)
+                n_load = int(allreduce_max(float(min(2000, int(0.3 / max(per, 1e-6)) + 1)), world))
+                for _ in range(n_load):
+                    step()
+                    torch.cuda.synchronize()
 
             # ---- timed region: exactly K steps (one graph replay), device time,
             #      barrier + sync on both sides
@@ -391,10 +402,15 @@ def run_b200(args, case, wl, world, rank, local):
                 clocks_extra.update(diag)
             if os.environ.get("BENCH_DUMP_STEPS"):
                 print("per-step ms:", [round(x, 4) for x in per_step], file=sys.stderr)
-            t_load = time.time()
-            while time.time() - t_load < 0.3:
-                step()
-                torch.cuda.synchronize()
+            if world == 1:
+                t_load = time.time()
+                while time.time() - t_load < 0.3:
+                    step()
+                    torch.cuda.synchronize()
+            else:
+                for _ in range(n_load):
+                    step()
+                    torch.cuda.synchronize()
         return per_step, per_k2, clocks.summary()
 
     # a run that saw thermal / hardware slowdown is re-measured once (all ranks
@@ -568,7 +584,7 @@ def fp32_format():
 def contract_kernel_name(case, plan=None):
     """The contraction kernel the C ABI dispatches to (bf16_variant() in contract_tc.cu)."""
     if plan is not None and getattr(plan, "small", False):
-        return "small_prep_kernel + small_contract_kernel (one call, PDL-chained)"
+        return "small_rows_kernel + small_stream_kernel (one call, PDL-chained)"
     if case.dtype != "float32":
         return "contract_f64_kernel"
     if os.environ.get("CORR2D_BF16_1SM") == "1":

@@ -216,22 +216,21 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  * contraction of a whole map (csrc/small_path.cu).  Replaces the corr2d_prep +
  * corr2d_contract_f64_gauss sequence that preprocess_dataset / dft_channels /
  * correlate_ft (preprocess.py:262-275, fourier.py:61-125) map onto; same
- * argument meanings as those two calls.  Maps with at most one 64 x 64 output
- * block per SM (corr2d_small_block_count <= SMs; homo: the upper triangle,
- * mirrored) run as ONE kernel: each CTA centres its block's channels, builds
- * their Gauss operand rows in shared memory and contracts them.  Larger maps
- * run two kernels chained by programmatic dependent launch: K1 once per
- * channel (one lane per channel, DFT on the FP64 tensor pipe, Gauss operand
- * rows into ops_a / ops_b), then a persistent contraction (one CTA per SM,
- * one bulk copy per role and block, TMA tensor stores of the planes; planes
- * that are not 16-B aligned with an even ld_out: one CTA per block, plain
- * stores).  No CTA ever waits for another CTA.
+ * argument meanings as those two calls.  Two kernels chained by programmatic
+ * dependent launch: K1 once per channel (64 channels per CTA, the Gauss
+ * operand rows of every role as one FP64 tensor-core product, into ops_a /
+ * ops_b), then a persistent contraction over the 64 x 64 output blocks
+ * (corr2d_small_block_count blocks; homo: the upper triangle, mirrored) with
+ * TMA tensor stores of the planes (planes that are not 16-B aligned with an
+ * even ld_out: one CTA per block, plain stores).  With ops_a or ops_b NULL the
+ * call is ONE kernel instead: each CTA centres its blocks' channels and builds
+ * their operand rows in shared memory.  No CTA ever waits for another CTA.
  *   ops_a / ops_b      : device operand scratch, n1 (resp. n2; homo: n1) rows
  *                       of ld_ops doubles, 16-B aligned, ld_ops ==
  *                       corr2d_small_ops_depth(m) (3 kg Gauss slots padded to
  *                       4 or 12 mod 16 doubles: a 64-row block is one
- *                       contiguous run, fragment loads conflict-free); may be
- *                       NULL for a one-kernel map
+ *                       contiguous run, fragment loads conflict-free); NULL
+ *                       selects the one-kernel variant
  *   ref_out* / sigma_out* : as corr2d_prep (either may be NULL)
  *   status1 / status2  : device int32[4] each, the corr2d_prep status words
  *                       (status2 unused when homo); written by the call
@@ -245,8 +244,9 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  * be inside a CUDA graph capture).
  */
 int64_t corr2d_small_block_count(int n1, int n2, int homo);
-/* Kernels one corr2d_correlate_small_f64 call launches on the current device:
- * 1 (the fused kernel: blocks <= SMs) or 2 (K1 + contraction); -1 on bad sizes. */
+/* Kernels one corr2d_correlate_small_f64 call WITH operand scratch launches:
+ * 2 (K1 + contraction); a call with ops_a / ops_b NULL launches 1 (the fused
+ * kernel); -1 on bad sizes. */
 int corr2d_small_launches(int n1, int n2, int homo);
 int corr2d_small_ops_depth(int m);
 int corr2d_correlate_small_f64(

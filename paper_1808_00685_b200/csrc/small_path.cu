@@ -1843,10 +1843,8 @@ extern "C" int corr2d_small_launches(int n1, int n2, int homo) {
   if (n1 < 1 || n2 < 1 || (homo && n1 != n2)) return -1;
 #if defined(CORR2D_SMALL_FORCE_FUSED)
   return 1;
-#elif defined(CORR2D_SMALL_TWO_KERNEL)
-  return 2;
 #else
-  return small_blocks(n1, n2, homo) <= device_sms() ? 1 : 2;
+  return 2;
 #endif
 }
 
@@ -1906,16 +1904,14 @@ extern "C" int corr2d_correlate_small_f64(
       p.trace = tbuf;
     }
 #endif
-  // one fused kernel when every output block has its own SM (no block's
-  // channels are prepared twice on one SM, and there is no second wave);
-  // otherwise K1 once per channel, then the contraction (the operand rows
-  // stay in L2 between the two kernels)
+  // K1 once per channel, then the streamed contraction (the operand rows stay
+  // in L2 between the two kernels; K1 overlaps the previous call's
+  // contraction): cfg1 8.4 us vs 10.4 us for the one-kernel variant, which
+  // serves calls without operand scratch
 #if defined(CORR2D_SMALL_FORCE_FUSED)
   const bool fused = true;
-#elif defined(CORR2D_SMALL_TWO_KERNEL)
-  const bool fused = false;
 #else
-  const bool fused = small_blocks(n1, n2, homo) <= device_sms() || !ops_a || !ops_b;
+  const bool fused = !ops_a || !ops_b;
 #endif
   if (fused) return launch_fused(p, st);
   if (!ops_a || !ops_b) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");

@@ -258,10 +258,18 @@ class PrepRecipe:
 
 
 def small_fused_enabled() -> bool:
-    """The one-launch small-m path (CORR2D_SMALL_FUSED=0 selects the two-kernel
-    path, for A/B comparisons)."""
+    """The small-m path (csrc/small_path.cu; CORR2D_SMALL_FUSED=0 selects the
+    generic K1 + fp64 contraction instead, for A/B comparisons)."""
     import os
     return os.environ.get("CORR2D_SMALL_FUSED", "1") != "0"
+
+
+def small_one_kernel() -> bool:
+    """CORR2D_SMALL_ONEKERNEL=1: the small-m path's one-kernel variant
+    (small_fused_kernel: no operand rows in global memory) instead of K1 +
+    streamed contraction; read at every launch."""
+    import os
+    return os.environ.get("CORR2D_SMALL_ONEKERNEL", "0") == "1"
 
 
 def launch_prep(lib, raw, recipe: PrepRecipe, *, norm=0.0, pack_kind=_abi.PACK_NONE, roles=0,
@@ -375,8 +383,8 @@ class CorrelationPlan:
         # in a 128-byte pad (include/corr2d.h)
         self.ld_pack = 2 * self.mp + 64 if bf16 else self.mp
         # small m (fp64 Fourier route, m <= 32, no resampling, whole map): the
-        # whole call is ONE kernel (csrc/small_path.cu small_fused_kernel: each
-        # CTA builds its blocks' operand rows in shared memory and contracts them)
+        # whole call is one C call (csrc/small_path.cu): K1 once per channel +
+        # the streamed contraction, or the one-kernel variant
         self.small = (route == "fourier" and self.dtype == np.float64
                       and small_fused_enabled() and 2 <= self.m <= 32
                       and all(r is None or (r.resample is None and r.m_in == r.m) for r in (recipe1, recipe2))
@@ -456,7 +464,8 @@ class CorrelationPlan:
         """Kernels of ours one launch() enqueues: K1 per dataset + K2 (the
         small-m path: one fused kernel, or K1 + contraction)."""
         if self.small:
-            return int(self.lib.corr2d_small_launches(self.n1, self.n2, 1 if self.homo else 0))
+            return 1 if small_one_kernel() else int(self.lib.corr2d_small_launches(self.n1, self.n2,
+                                                                                   1 if self.homo else 0))
         return (1 if self.homo else 2) + (2 if self.route == "hilbert" else 1)
 
     def launch(self):
@@ -517,7 +526,7 @@ class CorrelationPlan:
             self.m, self.n1, self.n2,
             int(r1.ref_mode), ptr(r1.ref_in), ptr(r1.sigma_in), int(r2.ref_mode), ptr(r2.ref_in), ptr(r2.sigma_in),
             float(r1.alpha), 1 if r1.substitute else 0, self.norm,
-            ptr(self.a_phi), ptr(self.bop), self.ld_pack,
+            *((None, None) if small_one_kernel() else (ptr(self.a_phi), ptr(self.bop))), self.ld_pack,
             ptr(self.ref1), ptr(self.sigma1), ptr(self.ref2), ptr(self.sigma2),
             ptr(self.phi), ptr(self.psi), self.phi.stride(0),
             ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle())

@@ -146,6 +146,9 @@ CASES = [
     ("hilbert", 300, None, 50, "float64", None, None, "hilbert"),
     ("small-homo", 500, None, 16, "float64", None, None, "fourier"),
     ("small-hetero", 200, 333, 31, "float64", None, None, "fourier"),
+    # the one-kernel variant (no operand scratch: CORR2D_SMALL_ONEKERNEL=1)
+    ("small-1k-homo", 500, None, 16, "float64", None, None, "fourier"),
+    ("small-1k-hetero", 200, 333, 31, "float64", None, None, "fourier"),
     # more 64 x 64 blocks than SMs: K1 + the streamed (persistent, TMA-store) contraction
     ("small-stream-homo", 1100, None, 21, "float64", None, None, "fourier"),
     ("small-stream-homo-1slot", 1090, None, 32, "float64", None, None, "fourier"),
@@ -161,6 +164,8 @@ def test_guard_bands_intact_and_results_bit_identical(case, out_pad, monkeypatch
         monkeypatch.setenv("CORR2D_FP32_FORMAT", f32fmt)
     if f64fmt:
         monkeypatch.setenv("CORR2D_F64_FORMAT", f64fmt)
+    if "-1k-" in label:
+        monkeypatch.setenv("CORR2D_SMALL_ONEKERNEL", "1")
     ds1 = _dataset(n1, m, 1)
     ds2 = _dataset(n2, m, 2) if n2 else None
     plan = _run_guarded(lambda: _plan(ds1, ds2, dtype, eng), out_pad)

@@ -1,11 +1,11 @@
-"""The one-launch small-m fp64 path (csrc/small.cu, corr2d_correlate_small_f64):
-independent CTAs, each recomputing K1 for its 64 x 64 output block's channels
-and contracting them (Gauss three-product form) on the FP64 tensor pipe.
-Parity against the CPU oracle (1e-10 of max|sync|, BASELINE.json north_star)
-for every m it serves, exact homo symmetry, agreement with the two-kernel path,
-row shards (two-kernel path) bit-identical to that path's whole map, and the
-self-resetting status / stat words (an error call must not leak into the next
-call)."""
+"""The small-m fp64 path (csrc/small_path.cu, corr2d_correlate_small_f64) in
+both variants: K1 + the streamed contraction (the default) and the one-kernel
+variant (CORR2D_SMALL_ONEKERNEL=1: each CTA builds its blocks' operand rows in
+shared memory).  Parity against the CPU oracle (1e-10 of max|sync|,
+BASELINE.json north_star) for every m it serves, exact homo symmetry,
+agreement with the generic K1 + fp64 contraction, row shards (generic path)
+bit-identical to that path's whole map, and the self-resetting status / stat
+words (an error call must not leak into the next call)."""
 
 import warnings
 
@@ -20,6 +20,15 @@ from paper_1808_00685_b200.errors import NumericError
 
 pytestmark = pytest.mark.gpu
 TOL64 = 1e-10
+
+
+@pytest.fixture(params=["two-kernel", "one-kernel"])
+def variant(request, monkeypatch):
+    if request.param == "one-kernel":
+        monkeypatch.setenv("CORR2D_SMALL_ONEKERNEL", "1")
+    else:
+        monkeypatch.delenv("CORR2D_SMALL_ONEKERNEL", raising=False)
+    return request.param
 
 
 def dyn(values, alpha=0.0):
@@ -48,7 +57,7 @@ def test_small_plans_take_the_fused_path():
 
 @pytest.mark.parametrize("n1,n2,m", [(1, 1, 2), (3, 5, 3), (31, 33, 8), (63, 65, 5), (64, 64, 12),
                                      (65, 130, 21), (517, 300, 32), (1000, 999, 11)])
-def test_fused_matches_oracle_homo_and_hetero(n1, n2, m):
+def test_fused_matches_oracle_homo_and_hetero(n1, n2, m, variant):
     rng = np.random.default_rng(n1 * 7 + n2 + m)
     v1 = rng.normal(size=(m, n1))
     v2 = rng.normal(size=(m, n2))
@@ -102,7 +111,7 @@ def test_row_shards_bit_identical_to_two_kernel_map(monkeypatch):
 
 
 @pytest.mark.parametrize("m", list(range(2, 33)))
-def test_fused_every_m(m):
+def test_fused_every_m(m, variant):
     rng = np.random.default_rng(100 + m)
     v1 = rng.normal(size=(m, 150)) * np.linspace(0.1, 10.0, 150)
     v2 = rng.normal(size=(m, 97))
@@ -117,7 +126,7 @@ def test_fused_every_m(m):
     assert np.array_equal(homo.sync, homo.sync.T) and np.array_equal(homo.asyn, -homo.asyn.T)
 
 
-def test_fused_status_words_reset_between_calls():
+def test_fused_status_words_reset_between_calls(variant):
     """A call that flags non-finite input / zero variance must not leak its
     counters into the next call on the same plan (self-resetting accumulators)."""
     rng = np.random.default_rng(2)
