@@ -19,7 +19,7 @@ case = C.make(cfg)
 ds1 = P.SpectralDataset(case.set1.spectral_axis, case.set1.perturbation_axis, case.set1.intensities)
 ds2 = None if case.set2 is None else P.SpectralDataset(case.set2.spectral_axis, case.set2.perturbation_axis,
                                                         case.set2.intensities)
-R = 12 if cfg == 1 else 8
+R = int(sys.argv[3]) if len(sys.argv) > 3 else (12 if cfg == 1 else 8)
 plans = [api.build_plan(ds1, ds2, P.PreprocessSpec(), dtype="float64")[0] for _ in range(R)]
 for q in plans:
     q.launch()
