@@ -42,9 +42,12 @@ CMD5="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 ncu --set full --clock-control none --import-source on -k regex:"contract_tc_2sm|prep_fast" -c 2 -o $OUT/full_cfg5 $CMD5 > $OUT/ncu_full5.log 2>&1
 CMD3="python bench.py --config 3 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
 ncu --set full --clock-control none --import-source on -k regex:"contract_f64|prep_fast" -c 2 -o $OUT/full_cfg3 $CMD3 > $OUT/ncu_full3.log 2>&1
+# small-m path: both kernels of one step late in a rotation (--cache-control none: L2
+# already holds other steps' dirty planes, so DRAM traffic is the steady state's, not
+# an L2-resident capture's)
 for c in 1 2; do
-  CMDS="python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
-  ncu --set full --clock-control none --import-source on -k regex:"small_" -c 2 -o $OUT/full_cfg$c $CMDS > $OUT/ncu_full$c.log 2>&1
+  CMDS="python tools/dev/small_rot.py $c 16"
+  ncu --set full --clock-control none --cache-control none --import-source on -k regex:"small_" -s 300 -c 2 -o $OUT/full_cfg$c $CMDS > $OUT/ncu_full$c.log 2>&1
 done
 ncu --set full --clock-control none --import-source on -k regex:"peaks_vec" -c 1 -o $OUT/full_peaks5 python tools/bench_extras.py > $OUT/ncu_peaks.log 2>&1
 ls -la $OUT

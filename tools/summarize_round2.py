@@ -77,7 +77,10 @@ def main():
         ks = ncu_raw(rep)
         (dst / f"{RND}_ncu_cfg{cfg}.json").write_text(json.dumps(ks, indent=1) + "\n")
         con = [k for k in ks if "contract" in k["kernel"]]
-        if con:
+        small = [k for k in ks if "small_" in k["kernel"]]
+        if small and not con:        # small-m path: the step's two kernels together
+            traffic[cfg] = sum(k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for k in small[-2:])
+        elif con:
             k = con[-1]
             traffic[cfg] = k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
     tpath.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
