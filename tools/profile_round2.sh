@@ -28,6 +28,15 @@ for c in 3 4; do
   done
 done
 CORR2D_LIB=_variants/libcorr2d_prof.so timeout 300 python tools/dev/small_trace.py > $OUT/small_trace.txt 2>&1
+# small-m step decomposition in the bench's rotation graph (profiling build switches)
+{ for c in 1 2; do
+    timeout 120 python tools/dev/small_rot.py $c 64 2>&1 | tail -1 | sed "s/^/release: /"
+    for skip in 0 1 2 3 4; do
+      CORR2D_LIB=_variants/libcorr2d_prof.so CORR2D_DEBUG_SKIP=$skip timeout 120 python tools/dev/small_rot.py $c 64 2>&1 | tail -1 | sed "s/^/skip $skip: /"
+    done
+    CORR2D_SMALL_ONEKERNEL=1 timeout 120 python tools/dev/small_rot.py $c 64 2>&1 | tail -1 | sed "s/^/one-kernel variant: /"
+  done
+  echo "skip 1 = no plane stores, 2 = no DMMAs, 3 = neither, 4 = K1 + an empty contraction grid"; } > $OUT/small_decomp.txt
 # cfg5 power decomposition (sustained, clocks / power sampled): full, no stores,
 # MMA only, stores only (profiling build)
 CORR2D_LIB=_variants/libcorr2d_prof.so timeout 600 python tools/ab_power.py 0 1 5 6 > $OUT/power_cfg5.txt 2>&1

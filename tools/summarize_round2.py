@@ -58,7 +58,7 @@ def main():
                       "profiling build (-DCORR2D_PROFILING) with CORR2D_DEBUG_SKIP=1 (no output stores), "
                       "2 (no MMAs), 3 (neither: operand loads + epilogue arithmetic only)")
         (dst / f"{RND}_f64_decomposition.json").write_text(json.dumps(dec, indent=1) + "\n")
-    for name in ("small_trace.txt", "power_cfg5.txt"):
+    for name in ("small_trace.txt", "power_cfg5.txt", "small_decomp.txt"):
         if (src / name).exists():
             shutil.copy(src / name, dst / f"{RND}_{name}")
     for name in ("gpu_tests.log", "wholemap_tests.log", "guards.log"):
@@ -164,6 +164,10 @@ def readme(dst):
         L.append("* " + dec["how"] + ".  MMA-only and store-only each run near their own ceilings (DMMA ~84 % "
                  "of peak; stores at the tile + mirror pattern's ~5.6 TB/s); the full kernel is their "
                  "imperfect overlap.")
+    sd = dst / f"{R}_small_decomp.txt"
+    if sd.exists():
+        L += ["", "## Small-m path: step decomposition (tools/dev/small_rot.py, the bench's rotation graph, us/step)",
+              "", "```"] + sd.read_text().strip().splitlines() + ["```"]
     tr = dst / f"{R}_small_trace.txt"
     if tr.exists():
         L += ["", "## Small-m path timeline (profiling build, one cold-ish step, ns)", "", "```"] + \
