@@ -58,5 +58,10 @@ for c in 1 2; do
   CMDS="python tools/dev/small_rot.py $c 16"
   ncu --set full --clock-control none --cache-control none --import-source on -k regex:"small_" -s 300 -c 2 -o $OUT/full_cfg$c $CMDS > $OUT/ncu_full$c.log 2>&1
 done
+# small-m path: single-pass DRAM counters (no replay) of the step's kernels late in a rotation
+for c in 1 2; do
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --cache-control none \
+    -k regex:"small_" -s 400 -c 4 --csv python tools/dev/small_rot.py $c 16 > $OUT/traffic_cfg$c.csv 2> $OUT/traffic_cfg$c.err
+done
 ncu --set full --clock-control none --import-source on -k regex:"peaks_vec" -c 1 -o $OUT/full_peaks5 python tools/bench_extras.py > $OUT/ncu_peaks.log 2>&1
 ls -la $OUT

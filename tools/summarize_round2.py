@@ -83,6 +83,25 @@ def main():
         elif con:
             k = con[-1]
             traffic[cfg] = k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"]
+    # small-m path: single-pass DRAM counters of the step's two kernels late in
+    # the bench's rotation (--cache-control none: the steady state's evictions),
+    # averaged over the captured steps
+    import csv
+    for c in (1, 2):
+        p = src / f"traffic_cfg{c}.csv"
+        if not p.exists():
+            continue
+        rows = [r for r in csv.reader(ln for ln in p.read_text().splitlines() if ln.startswith('"'))]
+        hdr = rows[0]
+        ix = {k: hdr.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
+        per = {}
+        for r in rows[1:]:
+            if r[ix["Metric Name"]] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                per[r[ix["ID"]]] = per.get(r[ix["ID"]], 0.0) + float(r[ix["Metric Value"]].replace(",", ""))
+        if per:
+            steps = max(1, len(per) // 2)
+            traffic[str(c)] = sum(per.values()) / steps
+            shutil.copy(p, dst / f"{RND}_traffic_cfg{c}.csv")
     tpath.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
     for rep in sorted(src.glob("full_peaks*.ncu-rep")):
         (dst / f"{RND}_ncu_{rep.stem[5:]}.json").write_text(json.dumps(ncu_raw(rep), indent=1) + "\n")
@@ -126,7 +145,11 @@ def readme(dst):
           "homo configs exceed 1.0: the map is computed once per mirrored tile pair and, with the Gauss form, "
           "with 3 instead of 4 real products per bin; `executed frac` counts the DMMA / tensor-core flops the "
           "kernel actually issues against the same peak. cfg1 / cfg2 run the small-m path (two PDL-chained "
-          "kernels: K1 + contraction), so their 'K2 ms' is the whole step."]
+          "kernels: K1 + contraction), so their 'K2 ms' is the whole step.",
+          "* roofline `traffic` (profiles/traffic.json): ncu DRAM bytes of the dominant kernel per launch; for "
+          "cfg1 / cfg2 the step's two kernels late in the bench's rotation, single-pass counters with "
+          "`--cache-control none` (`r2_traffic_cfg*.csv`: the steady state's write-backs, ~15 / 48 MB against "
+          "16 / 48 MB of planes).  Bench lines record the file as it was when they ran."]
     ref = _load(dst / f"{R}_bench_reference_cfg5.json")
     if ref and b5:
         L.append(f"* Reference arm ({ref['cpu_baseline']['kind']} on {ref['cpu_baseline']['cores']} host threads): "
@@ -170,7 +193,10 @@ def readme(dst):
               "", "```"] + sd.read_text().strip().splitlines() + ["```"]
     tr = dst / f"{R}_small_trace.txt"
     if tr.exists():
-        L += ["", "## Small-m path timeline (profiling build, one cold-ish step, ns)", "", "```"] + \
+        L += ["", "## Small-m path timeline (profiling build, one cold-ish step, ns)", "",
+              "Eager launches: the gap between K1's last stamp and the contraction's `after wait` includes the "
+              "host's encoding / launch of the second kernel (a graph replay has none); the steady state is the "
+              "decomposition above.", "", "```"] + \
              tr.read_text().strip().splitlines() + ["```"]
     L += ["", "## Parity beyond sampled rows", ""]
     for f in sorted(dst.glob("r2_wholemap_*.json")) + sorted(dst.glob("r2_*_adversarial_*.json")):
