@@ -222,3 +222,62 @@ def test_streamed_contraction_flags_nonfinite_and_resets():
         outs.append(plan.phi.cpu().numpy().copy())
         assert not plan.work.cpu().numpy().any()
     assert all(np.array_equal(o, outs[0]) for o in outs)
+
+
+@pytest.mark.parametrize("n1,n2", [(1300, 1300), (1000, 1100), (400, 400)])
+def test_back_to_back_launches_with_rebound_inputs(n1, n2, variant):
+    """Programmatic dependent launch lets K1 of the next call start (reading
+    its inputs) while the previous call's contraction runs; its writes wait.
+    Back-to-back launches of ONE plan on alternating inputs -- without a host
+    sync or any copy in between -- must each produce their own map, status and
+    statistics: a non-finite input in call k flags call k only."""
+    import torch
+    from paper_1808_00685_b200 import api
+    rng = np.random.default_rng(n1 + n2)
+    m = 21
+    t = np.arange(m, dtype=float)
+    homo = n1 == n2
+    xs = [rng.normal(size=(m, n1)) * np.linspace(1.0, 3.0, n1) for _ in range(2)]
+    ys = [None, None] if homo else [rng.normal(size=(m, n2)) for _ in range(2)]
+    bad = xs[0].copy()
+    bad[4, 7] = np.nan
+    mk = lambda x, n: P.SpectralDataset(np.arange(n, dtype=float), t, x)
+    plan, _ = api.build_plan(mk(xs[0], n1), None if homo else mk(ys[0], n2), P.PreprocessSpec(), dtype="float64")
+    assert plan.small
+    dev = plan.phi.device
+    raws = [torch.from_numpy(x).to(dev) for x in (xs[0], xs[1], bad)]
+    raws2 = [None, None] if homo else [torch.from_numpy(y).to(dev) for y in ys]
+    oracle = []
+    for k in range(2):
+        if homo:
+            s, a, _ = O.correlate_ft(xs[k] - xs[k].mean(axis=0))
+        else:
+            s, a, _ = O.correlate_ft(xs[k] - xs[k].mean(axis=0), ys[k] - ys[k].mean(axis=0))
+        oracle.append((s, a))
+    # A, B, A, B back to back; the last call's outputs are B's
+    for k in (0, 1, 0, 1):
+        plan.bind(raws[k], raws2[k])
+        plan.launch()
+    engine.sync()
+    plan.check()
+    s, a = oracle[1]
+    sc = scale_of(s, a)
+    assert rel_err(plan.phi.cpu().numpy(), s, sc) <= TOL64 and rel_err(plan.psi.cpu().numpy(), a, sc) <= TOL64
+    # a bad call followed at once by a clean one: the clean call's status is clean
+    plan.bind(raws[2], raws2[0])
+    plan.launch()
+    plan.bind(raws[0], raws2[0])
+    plan.launch()
+    engine.sync()
+    plan.check()
+    s, a = oracle[0]
+    assert rel_err(plan.phi.cpu().numpy(), s, sc) <= TOL64 * 10
+    # and the other way round: the bad call is reported
+    plan.bind(raws[0], raws2[0])
+    plan.launch()
+    plan.bind(raws[2], raws2[0])
+    plan.launch()
+    engine.sync()
+    with pytest.raises(NumericError, match="non-finite"):
+        plan.check()
+    assert not plan.work.cpu().numpy().any()
