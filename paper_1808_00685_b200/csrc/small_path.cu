@@ -1261,7 +1261,8 @@ __device__ __forceinline__ void stream_load(const SmallParams& p, int I, int J, 
 // queued behind the SM's outgoing TMA tensor stores), all threads; rows past
 // the map zero-filled by a zero source size.  Completion: cp.async.wait_group.
 template <int KG>
-__device__ __forceinline__ void stream_load_lsu(const SmallParams& p, int I, int J, double* As, double* Bs) {
+__device__ __forceinline__ void stream_load_lsu(const SmallParams& p, int I, int J, double* As, double* Bs,
+                                                bool loadA = true) {
   constexpr int OP = small_ops_pitch(KG);
   constexpr int kPieces = kSB * OP / 2;                // 16-byte pieces per role
   const int ra = min(kSB, p.n1 - I * kSB), rb = min(kSB, p.n2 - J * kSB);
@@ -1272,8 +1273,9 @@ __device__ __forceinline__ void stream_load_lsu(const SmallParams& p, int I, int
 #pragma unroll 4
   for (int i = threadIdx.x; i < kPieces; i += kSThreads) {
     const bool va = 2 * i < ra * OP, vb = 2 * i < rb * OP;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + 16u * i), "l"(ga + (va ? 2 * i : 0)),
-                 "r"(va ? 16 : 0) : "memory");
+    if (loadA)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa + 16u * i), "l"(ga + (va ? 2 * i : 0)),
+                   "r"(va ? 16 : 0) : "memory");
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sb + 16u * i), "l"(gb + (vb ? 2 * i : 0)),
                  "r"(vb ? 16 : 0) : "memory");
   }
@@ -1439,7 +1441,8 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     prev_mask = both ? 3 : (1 << s0);
     __syncthreads();                                   // every warp's DMMAs have read the operand buffer
     if (b == b0 + 2) SMALL_STAMP(kTraceK1, 0);
-    if (lsu && b + 1 < b1) stream_load_lsu<KG>(p, nI, nJ, Ops, Ops + 64 * KS);   // lands during the staging
+    // (a run of blocks along one row block keeps its A rows: only B reloads)
+    if (lsu && b + 1 < b1) stream_load_lsu<KG>(p, nI, nJ, Ops, Ops + 64 * KS, nI != I);   // lands during the staging
     double* C0 = Cst + 8192 * s0;
     stage_tile(C0, aphi, apsi, false, wm, wn, lrp, lk);
     if (both) stage_tile(Cst + 8192, aphi, apsi, true, wm, wn, lrp, lk);
