@@ -553,9 +553,14 @@ def cpu_baseline_line(case, wl):
     threads = O.host_threads()
     rows, _ = cpu_rows_for(case, 10.0, threads)
     dt = cpu_sample(case, rows, threads)
+    # the same path on one thread (W = 1 and W = all host threads)
+    rows1, _ = cpu_rows_for(case, 4.0, 1)
+    dt1 = cpu_sample(case, rows1, 1)
     return {"value": rows * wl["n2"] / dt / 1e9, "unit": "GElem/s", "cores": threads, "kind": "port",
             "sample": f"rows 0..{rows} of the {wl['n1']}x{wl['n2']} map ({dt:.1f} s; preprocess + rfft + "
-                      f"row-block zgemm via the oracle restatement of corrtwo 0.1.0)"}
+                      f"row-block zgemm via the oracle restatement of corrtwo 0.1.0)",
+            "single_thread": {"value": rows1 * wl["n2"] / dt1 / 1e9, "unit": "GElem/s", "cores": 1,
+                              "sample": f"rows 0..{rows1} ({dt1:.1f} s)"}}
 
 
 def executed_flops(plan, case, tc_peak, k2_ms):
