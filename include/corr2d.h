@@ -259,6 +259,31 @@ int corr2d_correlate_small_f64(
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream);
+/*
+ * The same call, PIPELINED with the previous call of the same plan on the
+ * same stream (what corr2d() / correlate_ft() use): consecutive calls pass
+ * alternate scratch sets -- ops_a / ops_b, stats, work, status1 / status2 --
+ * as slot 0 / 1, and one `pipe` (device int32[6], zero-filled once, left zero
+ * by every completed call).  No kernel then waits for a whole earlier grid:
+ * K1 of call k runs while call k-1's contraction does (it only waits until
+ * call k-2's contraction, the previous user of its slot, has completed), the
+ * contraction starts once K1's CTAs have all written their rows, and it loads
+ * and contracts before it waits for call k-1's stores to complete -- so the
+ * two calls' planes are written in call order.  Calls that take the
+ * one-kernel or the plain-store variant ignore the pipe (they serialise as
+ * usual).
+ */
+int corr2d_correlate_small_f64_slot(
+    int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
+    int m, int n1, int n2,
+    int ref_mode1, const double* ref_in1, const double* sigma_in1,
+    int ref_mode2, const double* ref_in2, const double* sigma_in2,
+    double alpha, int substitute_zero_var, double norm_const,
+    double* ops_a, double* ops_b, int64_t ld_ops,
+    double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
+    double* phi, double* psi, int64_t ld_out,
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream,
+    int slot, int32_t* pipe);
 
 /* ------------------------------------------------- K3: peak candidates ---- */
 /*

@@ -31,7 +31,7 @@ EXPORTS = (
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
     "corr2d_contract_tc", "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
     "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count", "corr2d_small_launches", "corr2d_small_ops_depth",
-    "corr2d_correlate_small_f64",
+    "corr2d_correlate_small_f64", "corr2d_correlate_small_f64_slot",
 )
 
 
@@ -100,7 +100,11 @@ def _declare(lib):
         c_void, c_void, c_i64,                        # phi psi ld_out
         c_void, c_void, c_void, c_void, c_void,       # status1 status2 stats work stream
     ]
-    for name in ("corr2d_format_repr", "corr2d_format_rows", "corr2d_correlate_small_f64", "corr2d_small_ops_depth",
+    lib.corr2d_correlate_small_f64_slot.argtypes = list(lib.corr2d_correlate_small_f64.argtypes) + [
+        c_int, c_void,                                # slot pipe
+    ]
+    for name in ("corr2d_format_repr", "corr2d_format_rows", "corr2d_correlate_small_f64",
+                 "corr2d_correlate_small_f64_slot", "corr2d_small_ops_depth",
                  "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
                  "corr2d_contract_tc", "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
                  "corr2d_plane_absmax", "corr2d_find_peaks"):

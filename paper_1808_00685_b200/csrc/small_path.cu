@@ -93,7 +93,57 @@ struct SmallParams {
   int dbg;                  // profiling builds only (CORR2D_DEBUG_SKIP): 1 no stores, 2 no DMMAs
   int tma_ops;              // streamed contraction, one buffer: operand rows by bulk copy (else cp.async)
   const double* G;          // small_rows_kernel: [2][nsp][gp] Gauss-row table (fused_table), gp = mpad + 2
+  int slot;                 // pipelined calls: this call's scratch slot (0 / 1) ...
+  int* pipe;                // ... and the plan's int32[6] {busy[2], arrivals[2], rows ready[2]} (NULL: not pipelined)
+  int k1_ctas;              // pipelined calls: K1's grid (its CTAs count themselves into ready[slot])
 };
+
+// Pipelined calls (corr2d_correlate_small_f64_slot with a pipe): consecutive
+// calls of one plan alternate between two scratch slots (operand rows, stats,
+// work and status words), and no kernel waits for a whole earlier grid
+// (griddepcontrol.wait would: a grid launched early still completes in
+// stream order).  Instead, per slot s:
+//   ready[s]  -- K1's CTAs count themselves in once their rows, statistics and
+//                status words are written; the contraction starts on it;
+//   busy[s]   -- set by the contraction's CTA 0 once it has started (before it
+//                lets the next kernel launch), cleared by its last CTA once
+//                every CTA's stores have completed; K1 writes slot s only when
+//                it is clear (the previous user, two calls back, is done), and
+//                a contraction stores only once the OTHER slot's is clear (the
+//                previous call wrote the same planes: they land in call order).
+// Every wait is on a grid whose CTAs have all passed
+// griddepcontrol.launch_dependents, i.e. are resident (or done), so it cannot
+// wait for a CTA that is not running.  A wait that outlives ~8 s gives up and
+// flags the call (stats[2], the non-finite-output count).
+__device__ __forceinline__ int ld_acquire(const int* w) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(w) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* w, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(w), "r"(v) : "memory");
+}
+// The last CTA of a pipelined contraction releases its slot (after every
+// CTA's stores performed).
+__device__ __forceinline__ void pipe_release(const SmallParams& p, int tid) {
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;\n" ::: "memory");
+  __threadfence();
+  __syncthreads();
+  if (tid == 0 && atomicAdd(p.pipe + 2 + p.slot, 1) == p.nctas - 1) {
+    p.pipe[2 + p.slot] = 0;
+    p.pipe[4 + p.slot] = 0;
+    __threadfence();
+    st_release(p.pipe + p.slot, 0);
+  }
+}
+__device__ __noinline__ void pipe_wait_value(const SmallParams& p, const int* w, int value) {
+  for (long long i = 0; i < (1LL << 23); ++i) {
+    if (ld_acquire(w) == value) return;
+    __nanosleep(64);
+  }
+  atomicAdd(&p.stats[2], 1ull);                        // never expected: the call reports bad output
+}
+__device__ __forceinline__ void pipe_wait_idle(const SmallParams& p, const int* busy) { pipe_wait_value(p, busy, 0); }
 
 // work-buffer words (int32 indices); every launch leaves them zero
 constexpr int kWStatus1 = 0;   // [0, 4)  K1 status accumulator, dataset 1
@@ -1348,7 +1398,20 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_psi)) : "memory");
   }
   __syncthreads();
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // K1 complete, its operand rows visible
+  if (!p.pipe) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // K1 complete, its operand rows visible
+  } else {
+    // K1's CTAs all counted in (rows, stats and status words written); CTA 0
+    // marks the slot busy until our last CTA is done
+    if (tid == 0) {
+      pipe_wait_value(p, p.pipe + 4 + p.slot, p.k1_ctas);
+      if (blockIdx.x == 0) {
+        st_release(p.pipe + p.slot, 1);
+        __threadfence();
+      }
+    }
+    __syncthreads();
+  }
   // the next kernel (the next call's K1) may launch now: everything before
   // this grid completed, and K1 writes nothing before its own wait
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
@@ -1362,7 +1425,10 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     p.work[kWStatus2 + tid] = 0;
   }
 #ifdef CORR2D_PROFILING
-  if (p.dbg & 4) return;                               // K1 + an empty contraction grid
+  if (p.dbg & 4) {                                     // K1 + an empty contraction grid
+    if (p.pipe) pipe_release(p, tid);
+    return;
+  }
 #endif
   int I, J;
   small_decode(p, b0, I, J);
@@ -1436,6 +1502,9 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     if (tid == 0) {
       if (both || p.nslots == 1 || prev_mask == 3) bulk_wait_read();
       else bulk_wait_read1();                          // the previous block's group may still read its slot
+      // pipelined: the previous call's contraction (the other slot) writes
+      // the same planes -- our first store waits until all of its completed
+      if (p.pipe && b == b0) pipe_wait_idle(p, p.pipe + (p.slot ^ 1));
     }
     if (!both && p.nslots == 2 && prev_mask == 1) s0 = 1;
     prev_mask = both ? 3 : (1 << s0);
@@ -1500,7 +1569,13 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     J = nJ;
   }
   small_publish(p, mphi, mpsi, lane, warp, tid);
-  if (tid == 0) bulk_wait_read();                     // the staging must outlive the stores' reads
+  if (!p.pipe) {
+    if (tid == 0) bulk_wait_read();                   // the staging must outlive the stores' reads
+  } else {
+    // pipelined: every store of this CTA performed, then the slot's arrival
+    // count; the last CTA releases the slot (and the next call's stores)
+    pipe_release(p, tid);
+  }
   SMALL_STAMP(kTraceK1, 5);
 }
 
@@ -1607,7 +1682,12 @@ __global__ void __launch_bounds__(kSThreads) small_rows_kernel(const __grid_cons
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> bulk copy
   __syncwarp();
   SMALL_STAMP(0, 7);
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");   // the previous call's contraction is done
+  if (p.pipe) {                                        // this slot's previous user has completed
+    if (tid == 0) pipe_wait_idle(p, p.pipe + p.slot);
+    __syncthreads();
+  } else {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");   // the previous call's contraction is done
+  }
   if (blockIdx.x == 0 && tid < 3) p.stats[tid] = 0ull;
   if (tid < kSB && valid) lane_report(p, set, c, lst);
   {
@@ -1625,6 +1705,12 @@ __global__ void __launch_bounds__(kSThreads) small_rows_kernel(const __grid_cons
                        "r"(static_cast<unsigned>(__cvta_generic_to_shared(rowsB + 16 * warp * OP))), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group 0;\n" ::: "memory");
     }
+  }
+  if (p.pipe) {                                        // pipelined: count this CTA into ready[slot]
+    if (lane == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");   // the bulk-copied rows
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(p.pipe + 4 + p.slot, 1);
   }
   SMALL_STAMP(0, 5);
 }
@@ -1853,7 +1939,7 @@ extern "C" int corr2d_small_launches(int n1, int n2, int homo) {
 
 extern "C" int corr2d_small_ops_depth(int m) { return (m >= 2 && m <= kSMaxM) ? small_ops_pitch(gauss_kg(m)) : -1; }
 
-extern "C" int corr2d_correlate_small_f64(
+static int correlate_small(
     int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
     int m, int n1, int n2,
     int ref_mode1, const double* ref_in1, const double* sigma_in1,
@@ -1862,7 +1948,7 @@ extern "C" int corr2d_correlate_small_f64(
     double* ops_a, double* ops_b, int64_t ld_ops,
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
-    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream) {
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream, int slot, int32_t* pipe) {
   const bool homo = raw2 == nullptr;
   if (!raw1 || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
@@ -1896,6 +1982,7 @@ extern "C" int corr2d_correlate_small_f64(
   p.phi = phi; p.psi = psi; p.ld_out = ld_out;
   p.vec = (ld_out % 2 == 0) && ((reinterpret_cast<uintptr_t>(phi) | reinterpret_cast<uintptr_t>(psi)) & 15) == 0;
   p.status1 = status1; p.status2 = homo ? nullptr : status2; p.stats = stats; p.work = work;
+  if (pipe && (slot < 0 || slot > 1)) return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64_slot: slot must be 0 or 1");
 #ifdef CORR2D_PROFILING
   if (const char* e = getenv("CORR2D_DEBUG_SKIP")) p.dbg = atoi(e);
   if (const char* e = getenv("CORR2D_SMALL_TRACE"))
@@ -1955,6 +2042,15 @@ extern "C" int corr2d_correlate_small_f64(
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // streamed contraction (persistent, TMA stores) when the planes take 16-B
+  // tensor stores; the one-CTA-per-block kernel otherwise.  Only the streamed
+  // contraction takes part in pipelining.
+  const bool streamed = p.vec && n2 >= 2 && !stream_disabled();
+  if (streamed && pipe) {
+    p.slot = slot;
+    p.pipe = pipe;
+    p.k1_ctas = prep_blocks;
+  }
   cfg.gridDim = dim3((unsigned)prep_blocks);
   cfg.dynamicSmemBytes = prep_smem;
   switch (p.kg) {
@@ -1964,9 +2060,6 @@ extern "C" int corr2d_correlate_small_f64(
     default: cudaLaunchKernelEx(&cfg, small_rows_kernel<16>, p); break;
   }
   if (int e = check_launch("small_rows_kernel")) return e;
-  // streamed contraction (persistent, TMA stores) when the planes take 16-B
-  // tensor stores; the one-CTA-per-block kernel otherwise
-  const bool streamed = p.vec && n2 >= 2 && !stream_disabled();
   long long k2_ctas = blocks;
   if (streamed) {
     p.tiles = blocks;
@@ -2046,4 +2139,37 @@ extern "C" int corr2d_correlate_small_f64(
   }
 #endif
   return code;
+}
+
+extern "C" int corr2d_correlate_small_f64(
+    int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
+    int m, int n1, int n2,
+    int ref_mode1, const double* ref_in1, const double* sigma_in1,
+    int ref_mode2, const double* ref_in2, const double* sigma_in2,
+    double alpha, int substitute_zero_var, double norm_const,
+    double* ops_a, double* ops_b, int64_t ld_ops,
+    double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
+    double* phi, double* psi, int64_t ld_out,
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream) {
+  return correlate_small(in_dtype, raw1, ld_raw1, raw2, ld_raw2, m, n1, n2, ref_mode1, ref_in1, sigma_in1,
+                         ref_mode2, ref_in2, sigma_in2, alpha, substitute_zero_var, norm_const, ops_a, ops_b, ld_ops,
+                         ref_out1, sigma_out1, ref_out2, sigma_out2, phi, psi, ld_out, status1, status2, stats, work,
+                         stream, 0, nullptr);
+}
+
+extern "C" int corr2d_correlate_small_f64_slot(
+    int in_dtype, const void* raw1, int64_t ld_raw1, const void* raw2, int64_t ld_raw2,
+    int m, int n1, int n2,
+    int ref_mode1, const double* ref_in1, const double* sigma_in1,
+    int ref_mode2, const double* ref_in2, const double* sigma_in2,
+    double alpha, int substitute_zero_var, double norm_const,
+    double* ops_a, double* ops_b, int64_t ld_ops,
+    double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
+    double* phi, double* psi, int64_t ld_out,
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream,
+    int slot, int32_t* pipe) {
+  return correlate_small(in_dtype, raw1, ld_raw1, raw2, ld_raw2, m, n1, n2, ref_mode1, ref_in1, sigma_in1,
+                         ref_mode2, ref_in2, sigma_in2, alpha, substitute_zero_var, norm_const, ops_a, ops_b, ld_ops,
+                         ref_out1, sigma_out1, ref_out2, sigma_out2, phi, psi, ld_out, status1, status2, stats, work,
+                         stream, slot, pipe);
 }

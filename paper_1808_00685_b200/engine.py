@@ -434,6 +434,17 @@ class CorrelationPlan:
         self.sigma1 = alloc(R1, dtype=t.float64, device=dev) if want_sigma else None
         self.sigma2 = (alloc(R2, dtype=t.float64, device=dev) if (want_sigma and not self.homo) else None)
         self.raw1 = self.raw2 = None
+        if self.small:
+            # pipelined small-m calls (corr2d_correlate_small_f64_slot): two
+            # scratch slots -- operand rows, stats, work and status words --
+            # used by alternate launches, and the plan's {busy, arrival} words
+            names = ("a_phi", "b", "b_homo", "stats", "work", "status1", "status2")
+            second = {k: (None if getattr(self, k) is None else
+                          (t.zeros_like(getattr(self, k)) if k in ("stats", "work", "status1", "status2")
+                           else t.empty_like(getattr(self, k)))) for k in names}
+            self._slots = [{k: getattr(self, k) for k in names}, second]
+            self._slot = 0
+            self.pipe = t.zeros(8, dtype=t.int32, device=dev)
 
     @property
     def bop(self):
@@ -520,16 +531,23 @@ class CorrelationPlan:
         if raw1.dtype not in (t.float64, t.float32) or (raw2 is not None and raw2.dtype != raw1.dtype):
             raise DataError(f"unsupported intensity dtype {raw1.dtype}")
         r1, r2 = self.recipe1, self.recipe2 or self.recipe1
-        code = self.lib.corr2d_correlate_small_f64(
+        one = small_one_kernel()
+        # alternate scratch slots: this launch's K1 may run while the previous
+        # launch's contraction still reads the other slot
+        self._slot ^= 1
+        for k, v in self._slots[self._slot].items():
+            setattr(self, k, v)
+        code = self.lib.corr2d_correlate_small_f64_slot(
             _abi.F64 if raw1.dtype == t.float64 else _abi.F32,
             ptr(raw1), raw1.stride(0), ptr(raw2), raw2.stride(0) if raw2 is not None else 0,
             self.m, self.n1, self.n2,
             int(r1.ref_mode), ptr(r1.ref_in), ptr(r1.sigma_in), int(r2.ref_mode), ptr(r2.ref_in), ptr(r2.sigma_in),
             float(r1.alpha), 1 if r1.substitute else 0, self.norm,
-            *((None, None) if small_one_kernel() else (ptr(self.a_phi), ptr(self.bop))), self.ld_pack,
+            *((None, None) if one else (ptr(self.a_phi), ptr(self.bop))), self.ld_pack,
             ptr(self.ref1), ptr(self.sigma1), ptr(self.ref2), ptr(self.sigma2),
             ptr(self.phi), ptr(self.psi), self.phi.stride(0),
-            ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle())
+            ptr(self.status1), ptr(self.status2), ptr(self.stats), ptr(self.work), stream_handle(),
+            self._slot, ptr(self.pipe))
         _abi.check(code, self.lib)
 
     def check(self, axes=(None, None), labels=("first", "second")):

@@ -151,6 +151,7 @@ def test_fused_status_words_reset_between_calls(variant):
         plan.check()
         outs.append(plan.phi.cpu().numpy().copy())
         assert not plan.work.cpu().numpy().any()      # accumulators / arrival counter left zero
+        assert not plan.pipe.cpu().numpy().any()      # pipelined calls: slots released
     assert all(np.array_equal(o, outs[0]) for o in outs)
     # zero variance with alpha > 0: the error policy raises, the substitute policy warns
     flat = x.copy()
@@ -280,4 +281,22 @@ def test_back_to_back_launches_with_rebound_inputs(n1, n2, variant):
     engine.sync()
     with pytest.raises(NumericError, match="non-finite"):
         plan.check()
-    assert not plan.work.cpu().numpy().any()
+    assert not plan.work.cpu().numpy().any() and not plan.pipe.cpu().numpy().any()
+    # a longer back-to-back chain (graph-captured, as bench.py replays it):
+    # A, B alternating, the last launch's map is B's
+    s_, stream = torch.cuda.current_stream(), torch.cuda.Stream()
+    stream.wait_stream(s_)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for k in range(9):
+                plan.bind(raws[k % 2], raws2[k % 2])
+                plan.launch()
+    s_.wait_stream(stream)
+    for _ in range(3):
+        g.replay()
+    engine.sync()
+    s, a = oracle[0]                                   # k = 8: input A
+    sc = scale_of(s, a)
+    assert rel_err(plan.phi.cpu().numpy(), s, sc) <= TOL64 and rel_err(plan.psi.cpu().numpy(), a, sc) <= TOL64
+    assert not plan.pipe.cpu().numpy().any()

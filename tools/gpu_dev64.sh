@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_small_fused.py tests/test_gpu_guards.py tests/test_gpu_configs.py -x -q 2>&1 | tail -2
+for w in 8 4; do for c in 1 2; do echo "warps $w"; CORR2D_SMALL_WARPS=$w timeout 120 python tools/dev/small_rot.py $c 64 2>&1 | tail -1; done; done
