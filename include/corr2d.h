@@ -263,13 +263,13 @@ int corr2d_correlate_small_f64(
  * The same call, PIPELINED with the previous call of the same plan on the
  * same stream (what corr2d() / correlate_ft() use): consecutive calls pass
  * alternate scratch sets -- ops_a / ops_b, stats, work, status1 / status2 --
- * as slot 0 / 1, and one `pipe` (device int32[6], zero-filled once, left zero
- * by every completed call).  No kernel then waits for a whole earlier grid:
- * K1 of call k runs while call k-1's contraction does (it only waits until
- * call k-2's contraction, the previous user of its slot, has completed), the
+ * as slot 0 / 1, and one `pipe` (device uint64[16], zero-filled once; its
+ * monotonic counters order the calls).  No kernel then waits for a whole
+ * earlier grid: K1 of call k runs while earlier calls' contractions do (it
+ * writes its slot once that slot's previous use, call k-2, is complete), the
  * contraction starts once K1's CTAs have all written their rows, and it loads
- * and contracts before it waits for call k-1's stores to complete -- so the
- * two calls' planes are written in call order.  Calls that take the
+ * and contracts before it waits for every earlier call's stores to complete
+ * -- so the calls' planes are written in call order.  Calls that take the
  * one-kernel or the plain-store variant ignore the pipe (they serialise as
  * usual).
  */
@@ -283,7 +283,7 @@ int corr2d_correlate_small_f64_slot(
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream,
-    int slot, int32_t* pipe);
+    int slot, unsigned long long* pipe);
 
 /* ------------------------------------------------- K3: peak candidates ---- */
 /*

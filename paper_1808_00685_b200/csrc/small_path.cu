@@ -94,56 +94,73 @@ struct SmallParams {
   int tma_ops;              // streamed contraction, one buffer: operand rows by bulk copy (else cp.async)
   const double* G;          // small_rows_kernel: [2][nsp][gp] Gauss-row table (fused_table), gp = mpad + 2
   int slot;                 // pipelined calls: this call's scratch slot (0 / 1) ...
-  int* pipe;                // ... and the plan's int32[6] {busy[2], arrivals[2], rows ready[2]} (NULL: not pipelined)
-  int k1_ctas;              // pipelined calls: K1's grid (its CTAs count themselves into ready[slot])
+  unsigned long long* pipe; // ... and the plan's uint64[16] pipeline words (kP*; NULL: not pipelined)
+  int k1_ctas;              // pipelined calls: K1's grid (every K1 CTA takes one ticket per counter)
 };
 
 // Pipelined calls (corr2d_correlate_small_f64_slot with a pipe): consecutive
 // calls of one plan alternate between two scratch slots (operand rows, stats,
 // work and status words), and no kernel waits for a whole earlier grid
-// (griddepcontrol.wait would: a grid launched early still completes in
-// stream order).  Instead, per slot s:
-//   ready[s]  -- K1's CTAs count themselves in once their rows, statistics and
-//                status words are written; the contraction starts on it;
-//   busy[s]   -- set by the contraction's CTA 0 once it has started (before it
-//                lets the next kernel launch), cleared by its last CTA once
-//                every CTA's stores have completed; K1 writes slot s only when
-//                it is clear (the previous user, two calls back, is done), and
-//                a contraction stores only once the OTHER slot's is clear (the
-//                previous call wrote the same planes: they land in call order).
+// (griddepcontrol.wait would: a grid launched early still completes in stream
+// order, so the next call could never overlap this one).  Ordering comes from
+// monotonic 64-bit counters instead (uint64 words of the plan's pipe).  A
+// kernel's CTAs take their tickets BEFORE griddepcontrol.launch_dependents, so
+// all of a call's tickets precede the next call's, and ticket / (grid CTAs) is
+// the call's index on that counter:
+//   kPClaim + s   K1 tickets on slot s -> use index u of the slot;
+//   kPGen + s     completed uses of slot s: K1 writes its slot only when it
+//                 equals u (the slot's previous user has finished with it);
+//   kPReady + s   K1 CTAs of slot s that have written their rows, statistics
+//                 and status words (never reset): use u of the slot is
+//                 complete at (K1 CTAs) * (u + 1);
+//   kPSClaim + s  contraction tickets on slot s -> its use index, so it waits
+//                 for ITS K1 (not a stale count of the slot's previous use);
+//   kPSCall       contraction tickets on the plan -> call index c;
+//   kPPlanes      calls whose contraction has completed all its stores: a
+//                 contraction issues its first store only when it equals c
+//                 (every call writes the same planes: they land in call order);
+//   kPArrive + s  contraction CTAs done; the last one advances kPGen + s and
+//                 kPPlanes.
 // Every wait is on a grid whose CTAs have all passed
 // griddepcontrol.launch_dependents, i.e. are resident (or done), so it cannot
 // wait for a CTA that is not running.  A wait that outlives ~8 s gives up and
 // flags the call (stats[2], the non-finite-output count).
-__device__ __forceinline__ int ld_acquire(const int* w) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(w) : "memory");
+constexpr int kPClaim = 0, kPGen = 2, kPReady = 4, kPSClaim = 6, kPSCall = 8, kPPlanes = 9, kPArrive = 10;
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* w) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(w) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release(int* w, int v) {
-  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(w), "r"(v) : "memory");
+__device__ __forceinline__ void st_release(unsigned long long* w, unsigned long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;\n" ::"l"(w), "l"(v) : "memory");
 }
-// The last CTA of a pipelined contraction releases its slot (after every
-// CTA's stores performed).
-__device__ __forceinline__ void pipe_release(const SmallParams& p, int tid) {
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;\n" ::: "memory");
-  __threadfence();
-  __syncthreads();
-  if (tid == 0 && atomicAdd(p.pipe + 2 + p.slot, 1) == p.nctas - 1) {
-    p.pipe[2 + p.slot] = 0;
-    p.pipe[4 + p.slot] = 0;
-    __threadfence();
-    st_release(p.pipe + p.slot, 0);
-  }
-}
-__device__ __noinline__ void pipe_wait_value(const SmallParams& p, const int* w, int value) {
+__device__ __noinline__ void pipe_wait_at_least(const SmallParams& p, const unsigned long long* w,
+                                                unsigned long long value) {
   for (long long i = 0; i < (1LL << 23); ++i) {
-    if (ld_acquire(w) == value) return;
+    if (ld_acquire(w) >= value) return;
     __nanosleep(64);
   }
   atomicAdd(&p.stats[2], 1ull);                        // never expected: the call reports bad output
 }
-__device__ __forceinline__ void pipe_wait_idle(const SmallParams& p, const int* busy) { pipe_wait_value(p, busy, 0); }
+// counters only grow: "equals" is "reached"
+__device__ __forceinline__ void pipe_wait_value(const SmallParams& p, const unsigned long long* w,
+                                                unsigned long long value) {
+  pipe_wait_at_least(p, w, value);
+}
+// The last CTA of a pipelined contraction, once every CTA's stores have
+// performed: one more completed use of the slot and one more completed call.
+__device__ __forceinline__ void pipe_release(const SmallParams& p, int tid, unsigned long long call) {
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\nfence.proxy.async.global;\n" ::: "memory");
+  __threadfence();
+  __syncthreads();
+  if (tid == 0 && atomicAdd(p.pipe + kPArrive + p.slot, 1ull) == (unsigned long long)p.nctas - 1) {
+    p.pipe[kPArrive + p.slot] = 0;
+    __threadfence();
+    atomicAdd(p.pipe + kPGen + p.slot, 1ull);
+    __threadfence();
+    st_release(p.pipe + kPPlanes, call + 1);
+  }
+}
 
 // work-buffer words (int32 indices); every launch leaves them zero
 constexpr int kWStatus1 = 0;   // [0, 4)  K1 status accumulator, dataset 1
@@ -1398,23 +1415,26 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_psi)) : "memory");
   }
   __syncthreads();
+  __shared__ unsigned long long call_idx;
   if (!p.pipe) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");   // K1 complete, its operand rows visible
+    // the next kernel (the next call's K1) may launch now: everything before
+    // this grid completed, and K1 writes nothing before its own wait
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   } else {
-    // K1's CTAs all counted in (rows, stats and status words written); CTA 0
-    // marks the slot busy until our last CTA is done
+    // tickets first; then the next call's K1 may launch at once (it takes its
+    // tickets, computes, and writes its slot when that slot's previous use is
+    // complete); this call starts when all of its K1's CTAs have counted in
+    __shared__ unsigned long long use_idx;
     if (tid == 0) {
-      pipe_wait_value(p, p.pipe + 4 + p.slot, p.k1_ctas);
-      if (blockIdx.x == 0) {
-        st_release(p.pipe + p.slot, 1);
-        __threadfence();
-      }
+      use_idx = atomicAdd(p.pipe + kPSClaim + p.slot, 1ull) / (unsigned long long)p.nctas;
+      call_idx = atomicAdd(p.pipe + kPSCall, 1ull) / (unsigned long long)p.nctas;
     }
     __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (tid == 0) pipe_wait_at_least(p, p.pipe + kPReady + p.slot, (unsigned long long)p.k1_ctas * (use_idx + 1));
+    __syncthreads();
   }
-  // the next kernel (the next call's K1) may launch now: everything before
-  // this grid completed, and K1 writes nothing before its own wait
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   SMALL_STAMP(kTraceK1, 1);
   // K1's status accumulators are final now: CTA 0 publishes them and leaves
   // the words zero for the next call (whose K1 starts after this grid ends)
@@ -1426,7 +1446,11 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
   }
 #ifdef CORR2D_PROFILING
   if (p.dbg & 4) {                                     // K1 + an empty contraction grid
-    if (p.pipe) pipe_release(p, tid);
+    if (p.pipe) {
+      if (tid == 0) pipe_wait_value(p, p.pipe + kPPlanes, call_idx);
+      __syncthreads();
+      pipe_release(p, tid, call_idx);
+    }
     return;
   }
 #endif
@@ -1502,9 +1526,9 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
     if (tid == 0) {
       if (both || p.nslots == 1 || prev_mask == 3) bulk_wait_read();
       else bulk_wait_read1();                          // the previous block's group may still read its slot
-      // pipelined: the previous call's contraction (the other slot) writes
-      // the same planes -- our first store waits until all of its completed
-      if (p.pipe && b == b0) pipe_wait_idle(p, p.pipe + (p.slot ^ 1));
+      // pipelined: earlier calls write the same planes -- our first store
+      // waits until every earlier call's stores have completed
+      if (p.pipe && b == b0) pipe_wait_value(p, p.pipe + kPPlanes, call_idx);
     }
     if (!both && p.nslots == 2 && prev_mask == 1) s0 = 1;
     prev_mask = both ? 3 : (1 << s0);
@@ -1574,7 +1598,7 @@ small_stream_kernel(const __grid_constant__ SmallParams p, const __grid_constant
   } else {
     // pipelined: every store of this CTA performed, then the slot's arrival
     // count; the last CTA releases the slot (and the next call's stores)
-    pipe_release(p, tid);
+    pipe_release(p, tid, call_idx);
   }
   SMALL_STAMP(kTraceK1, 5);
 }
@@ -1634,6 +1658,11 @@ __global__ void __launch_bounds__(kSThreads) small_rows_kernel(const __grid_cons
   const int set = (int)blockIdx.x >= p.nb1 ? 1 : 0;
   const int c0 = ((int)blockIdx.x - (set ? p.nb1 : 0)) * kSB;
   const int n = set ? p.n2 : p.n1;
+  __shared__ unsigned long long use_idx;
+  if (p.pipe) {                                        // ticket first, then the next kernel may launch
+    if (tid == 0) use_idx = atomicAdd(p.pipe + kPClaim + p.slot, 1ull) / (unsigned long long)p.k1_ctas;
+    __syncthreads();
+  }
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   SMALL_STAMP(0, 0);
   {
@@ -1682,8 +1711,8 @@ __global__ void __launch_bounds__(kSThreads) small_rows_kernel(const __grid_cons
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic-proxy writes -> bulk copy
   __syncwarp();
   SMALL_STAMP(0, 7);
-  if (p.pipe) {                                        // this slot's previous user has completed
-    if (tid == 0) pipe_wait_idle(p, p.pipe + p.slot);
+  if (p.pipe) {                                        // this slot's previous user has finished with it
+    if (tid == 0) pipe_wait_value(p, p.pipe + kPGen + p.slot, use_idx);
     __syncthreads();
   } else {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");   // the previous call's contraction is done
@@ -1710,7 +1739,7 @@ __global__ void __launch_bounds__(kSThreads) small_rows_kernel(const __grid_cons
     if (lane == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");   // the bulk-copied rows
     __threadfence();
     __syncthreads();
-    if (tid == 0) atomicAdd(p.pipe + 4 + p.slot, 1);
+    if (tid == 0) atomicAdd(p.pipe + kPReady + p.slot, 1ull);
   }
   SMALL_STAMP(0, 5);
 }
@@ -1948,7 +1977,7 @@ static int correlate_small(
     double* ops_a, double* ops_b, int64_t ld_ops,
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
-    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream, int slot, int32_t* pipe) {
+    int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream, int slot, unsigned long long* pipe) {
   const bool homo = raw2 == nullptr;
   if (!raw1 || !phi || !psi || !status1 || !stats || !work || (!homo && !status2))
     return fail(CORR2D_ERR_DATA, "corr2d_correlate_small_f64: null pointer");
@@ -2167,7 +2196,7 @@ extern "C" int corr2d_correlate_small_f64_slot(
     double* ref_out1, double* sigma_out1, double* ref_out2, double* sigma_out2,
     double* phi, double* psi, int64_t ld_out,
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream,
-    int slot, int32_t* pipe) {
+    int slot, unsigned long long* pipe) {
   return correlate_small(in_dtype, raw1, ld_raw1, raw2, ld_raw2, m, n1, n2, ref_mode1, ref_in1, sigma_in1,
                          ref_mode2, ref_in2, sigma_in2, alpha, substitute_zero_var, norm_const, ops_a, ops_b, ld_ops,
                          ref_out1, sigma_out1, ref_out2, sigma_out2, phi, psi, ld_out, status1, status2, stats, work,

@@ -444,7 +444,7 @@ class CorrelationPlan:
                            else t.empty_like(getattr(self, k)))) for k in names}
             self._slots = [{k: getattr(self, k) for k in names}, second]
             self._slot = 0
-            self.pipe = t.zeros(8, dtype=t.int32, device=dev)
+            self.pipe = t.zeros(16, dtype=t.int64, device=dev)
 
     @property
     def bop(self):
