@@ -2080,6 +2080,27 @@ static int correlate_small(
     p.pipe = pipe;
     p.k1_ctas = prep_blocks;
   }
+  // everything that can fail is settled before K1 launches (a pipelined K1
+  // takes tickets that only its contraction retires)
+  int nb = 1;
+  size_t sops = 0;                                     // streamed: operand-buffer bytes
+  CUtensorMap map_phi, map_psi;
+  memset(&map_phi, 0, sizeof(map_phi));
+  memset(&map_psi, 0, sizeof(map_psi));
+  if (streamed) {
+    p.tiles = blocks;
+    // two CTAs per SM (one operand buffer and one staging slot each) when
+    // both fit, else one CTA per SM with a prefetch buffer (and two slots when
+    // they fit); CORR2D_SMALL_STREAM_NB=2 forces the latter
+    const size_t ops1 = 128 * (size_t)stream_ks(p.kg) * sizeof(double);
+    nb = (2 * (1024 + 65536 + ops1 + 1024) <= 228 * 1024 && stream_nb() != 2) ? 1 : 2;
+    p.nctas = (int)std::min<long long>(blocks, (long long)(3 - nb) * device_sms());
+    sops = nb * ops1;
+    p.nslots = (nb == 2 && 1024 + 2 * 65536 + sops <= 226 * 1024) ? 2 : 1;
+    if (int e = fused_plane_map(&map_phi, p.phi, p.ld_out, p.n1, p.n2 & ~1)) return e;
+    if (int e = fused_plane_map(&map_psi, p.psi, p.ld_out, p.n1, p.n2 & ~1)) return e;
+    p.tma_ops = env_flag("CORR2D_SMALL_TMA_OPS");
+  }
   cfg.gridDim = dim3((unsigned)prep_blocks);
   cfg.dynamicSmemBytes = prep_smem;
   switch (p.kg) {
@@ -2091,21 +2112,7 @@ static int correlate_small(
   if (int e = check_launch("small_rows_kernel")) return e;
   long long k2_ctas = blocks;
   if (streamed) {
-    p.tiles = blocks;
-    // two CTAs per SM (one operand buffer and one staging slot each) when
-    // both fit, else one CTA per SM with a prefetch buffer (and two slots when
-    // they fit); CORR2D_SMALL_STREAM_NB=2 forces the latter
-    const size_t ops1 = 128 * (size_t)stream_ks(p.kg) * sizeof(double);
-    const int nb = (2 * (1024 + 65536 + ops1 + 1024) <= 228 * 1024 && stream_nb() != 2) ? 1 : 2;
-    p.nctas = (int)std::min<long long>(blocks, (long long)(3 - nb) * device_sms());
     k2_ctas = p.nctas;
-    const size_t ops_b = nb * ops1;
-    p.nslots = (nb == 2 && 1024 + 2 * 65536 + ops_b <= 226 * 1024) ? 2 : 1;
-    CUtensorMap map_phi, map_psi;
-    memset(&map_phi, 0, sizeof(map_phi));
-    memset(&map_psi, 0, sizeof(map_psi));
-    if (int e = fused_plane_map(&map_phi, p.phi, p.ld_out, p.n1, p.n2 & ~1)) return e;
-    if (int e = fused_plane_map(&map_psi, p.psi, p.ld_out, p.n1, p.n2 & ~1)) return e;
     static bool sattr = false;
     if (!sattr) {
       const int worst = 226 * 1024;
@@ -2120,8 +2127,7 @@ static int correlate_small(
       sattr = true;
     }
     cfg.gridDim = dim3((unsigned)p.nctas);
-    cfg.dynamicSmemBytes = 1024 + (size_t)p.nslots * 65536 + ops_b;
-    p.tma_ops = env_flag("CORR2D_SMALL_TMA_OPS");
+    cfg.dynamicSmemBytes = 1024 + (size_t)p.nslots * 65536 + sops;
     switch (p.kg * 4 + nb) {
       case 17: cudaLaunchKernelEx(&cfg, small_stream_kernel<4, 1>, p, map_phi, map_psi); break;
       case 33: cudaLaunchKernelEx(&cfg, small_stream_kernel<8, 1>, p, map_phi, map_psi); break;
