@@ -224,7 +224,8 @@ int64_t corr2d_contract_tile_count(int pack_kind, int n1, int n2, int homo, int 
  * TMA tensor stores of the planes (planes that are not 16-B aligned with an
  * even ld_out: one CTA per block, plain stores).  With ops_a or ops_b NULL the
  * call is ONE kernel instead: each CTA centres its blocks' channels and builds
- * their operand rows in shared memory.  No CTA ever waits for another CTA.
+ * their operand rows in shared memory.  Within one call no CTA waits for
+ * another CTA (pipelined calls: see corr2d_correlate_small_f64_slot).
  *   ops_a / ops_b      : device operand scratch, n1 (resp. n2; homo: n1) rows
  *                       of ld_ops doubles, 16-B aligned, ld_ops ==
  *                       corr2d_small_ops_depth(m) (3 kg Gauss slots padded to

@@ -1,15 +1,16 @@
 // The whole small-m correlation (corr2d_correlate_small_f64): fp64,
 // 2 <= m <= 32, no resampling -- the cfg1 (m = 11) and cfg2 (m = 21) shapes,
 // where a step is bound by latency, one DRAM round trip and the output write
-// (cfg1: 16 MB of planes, cfg2: 48 MB).  Every kernel here chains to its
-// predecessor by programmatic dependent launch and orders memory with
-// griddepcontrol.wait -- a kernel boundary, never a wait of one CTA on another.
+// (cfg1: 16 MB of planes, cfg2: 48 MB).  Every kernel here is launched with
+// programmatic dependent launch.  Single calls order memory with
+// griddepcontrol.wait; pipelined calls (corr2d_correlate_small_f64_slot) with
+// monotonic tickets (see kPClaim below).
 //
-// small_fused_kernel (maps with at most one 64 x 64 output block per SM; cfg1)
-//   -- ONE kernel: each CTA centres its block's channels, builds their Gauss
-//   operand rows with one FP64 tensor-core product per role, contracts them
-//   and writes both planes (+ the homo mirror) by TMA tensor stores.
-// Larger maps (cfg2): two kernels.
+// Calls without operand scratch: small_fused_kernel -- ONE kernel: each CTA
+//   centres its blocks' channels, builds their Gauss operand rows with one
+//   FP64 tensor-core product per role, contracts them and writes both planes
+//   (+ the homo mirror) by TMA tensor stores.
+// Otherwise (the default) two kernels.
 //   small_rows_kernel -- K1 once per channel: 64 channels per CTA, the
 //   reference's statistics in its order (one lane per channel, sequential
 //   sums: bitwise-equal reference / sigma / values), then the
@@ -25,7 +26,9 @@
 //   own stores); max|.| / finite folded into the fragments.
 //   small_contract_kernel -- one CTA per block with plain stores, for planes
 //   that are not 16-B aligned with an even row pitch.
-// Status / stat words are self-resetting (no CTA ever waits for another).
+// Status / stat words are self-resetting.  Within one call no CTA waits for
+// another; pipelined calls (corr2d_correlate_small_f64_slot) order themselves
+// through monotonic tickets, waiting only on grids whose CTAs are resident.
 //
 // Reference path: preprocess.py:123-137, :198-259 (reference, sigma, scaling),
 // fourier.py:61-82 (rfft along the perturbation axis), fourier.py:107-123
