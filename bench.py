@@ -46,8 +46,17 @@ sys.path.insert(0, str(ROOT))
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 # FP64 tensor (DMMA) peak measured on this pool by tools/microbench/peaks.cu
-# (mma.sync m16n8k16 f64, 148 SMs): 37.0 TFLOP/s; DFMA 33.7 TFLOP/s.
+# (mma.sync f64 -> DMMA.8x8x4, 148 SMs), committed as profiles/r2_peaks.json;
+# 37.03 TFLOP/s is that file's figure (DFMA 33.7 TFLOP/s) if it is missing.
 FP64_DMMA_TFLOPS = 37.03
+
+
+def fp64_dmma_peak():
+    p = ROOT / "profiles" / "r2_peaks.json"
+    try:
+        return float(json.loads(p.read_text())["dmma_m8n8k4_tflops"]), f"measured ({p.relative_to(ROOT)})"
+    except (OSError, KeyError, ValueError):
+        return FP64_DMMA_TFLOPS, "tools/microbench/peaks.cu (constant)"
 
 
 def measured_peaks():
@@ -88,7 +97,8 @@ def roofline_peak(case, peaks):
         burst = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
         sus = float(peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"]))
         return "tensor", sus, "TFLOP/s", burst
-    return "tensor", FP64_DMMA_TFLOPS, "TFLOP/s", FP64_DMMA_TFLOPS
+    pk = fp64_dmma_peak()[0]
+    return "tensor", pk, "TFLOP/s", pk
 
 
 # --------------------------------------------------------------------------
@@ -472,7 +482,7 @@ def run_b200(args, case, wl, world, rank, local):
                      "executed": executed_flops(plan, case, tc_peak, k2_avg),
                      "hbm_floor_ms": (wl["out_bytes"] + wl["in_bytes"]) / (peaks["hbm_gbs"] * 1e9) * 1e3,
                      "peak_source": peaks["_source"] + (" (bf16 sustained; burst in peak_burst)" if case.dtype == "float32"
-                                                        else "; fp64 DMMA peak from tools/microbench/peaks.cu")},
+                                                        else "; fp64 DMMA peak " + fp64_dmma_peak()[1])},
         "clocks": clock_summary,
         "timing": ({"mode": f"event-free graph of K steps rotating over {len(plans)} plans "
                             f"({len(plans) * foot / 1e6:.0f} MB of inputs + outputs > 126 MB L2)", **clocks_extra}
