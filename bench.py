@@ -552,7 +552,10 @@ def run_e2e(args, case, ds1, ds2, world, rank, dev):
         steps += 1
         dt = time.perf_counter() - t0
     h2d = ds1.intensities.nbytes + (ds2.intensities.nbytes if ds2 is not None else 0)
-    d2h = 2 * n1 * n2 * (4 if case.dtype == "float32" else 8)
+    # plane bytes the last call moved (a whole homo map from 4096 rows sends its
+    # upper triangle only and the host fills the mirror: engine.fetch_mirrored)
+    from paper_1808_00685_b200 import engine as E
+    d2h = E.last_fetch_bytes
     return {"value": n1 * n2 * steps / dt / 1e9, "unit": "GElem/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "ms_per_step": 1e3 * dt / steps,
             "api": "paper_1808_00685_b200.corr2d(ds, ..., out=(pinned, pinned))"}

@@ -286,6 +286,26 @@ int corr2d_correlate_small_f64_slot(
     int32_t* status1, int32_t* status2, unsigned long long* stats, int32_t* work, void* stream,
     int slot, unsigned long long* pipe);
 
+/* ------------------------------------------ homo map: device -> host ---- */
+/*
+ * Device -> host copy of a homo map's planes (n x n, leading dimensions ld_dev
+ * on the device, ld_host on the host) that sends part of the lower triangle as
+ * its mirror image only:
+ * row band [r0, r0 + band) travels as columns [split, n), split = fill_pct %
+ * of r0 (rounded down to 64; 0 = a plain full copy, 100 = the upper triangle
+ * only), and `threads` host threads fill the band's columns [0, split) as
+ * sync(i, j) = sync(j, i), async(i, j) = -async(j, i) from rows that already
+ * landed, while later bands are in flight (csrc/fetch.cu).  band: a positive multiple of 256 (diagonal
+ * blocks travel whole).  Ordered after the work queued on `stream`; returns
+ * once both host planes are complete; *d2h_bytes (may be NULL) = bytes moved.
+ * Bit-identical to a full-plane copy of a map any homo contraction wrote.
+ * Replaces the reference's host-side result hand-off of a homo map
+ * (fourier.py:123 / dataset.py:133-170 assemble the full planes on the host).
+ */
+int corr2d_fetch_mirrored(int dtype, const void* d_sync, const void* d_async, int64_t ld_dev, int n,
+                          void* h_sync, void* h_async, int64_t ld_host, int band, int fill_pct, int threads,
+                          int64_t* d2h_bytes, void* stream);
+
 /* ------------------------------------------------- K3: peak candidates ---- */
 /*
  * max |x| over an n1 x n2 plane (dtype CORR2D_F64 / CORR2D_F32, leading

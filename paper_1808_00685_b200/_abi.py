@@ -30,6 +30,7 @@ EXPORTS = (
     "corr2d_last_error", "corr2d_abi_version", "corr2d_device_info", "corr2d_packed_depth",
     "corr2d_fft_factors", "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
     "corr2d_contract_tc", "corr2d_contract_tile_count", "corr2d_plane_absmax", "corr2d_find_peaks",
+    "corr2d_fetch_mirrored",
     "corr2d_format_repr", "corr2d_format_rows", "corr2d_small_block_count", "corr2d_small_launches", "corr2d_small_ops_depth",
     "corr2d_correlate_small_f64", "corr2d_correlate_small_f64_slot",
 )
@@ -80,6 +81,8 @@ def _declare(lib):
     lib.corr2d_contract_tile_count.argtypes = [c_int, c_int, c_int, c_int, c_int, c_int, c_i64]
     lib.corr2d_contract_tile_count.restype = c_i64
     lib.corr2d_plane_absmax.argtypes = [c_int, c_void, c_i64, c_int, c_int, c_void, c_void]
+    lib.corr2d_fetch_mirrored.argtypes = [c_int, c_void, c_void, c_i64, c_int, c_void, c_void, c_i64, c_int, c_int,
+                                          c_int, c_void, c_void]
     lib.corr2d_find_peaks.argtypes = [c_int, c_void, c_void, c_i64, c_int, c_int, c_int, c_double, c_double,
                                       c_void, c_i64, c_void, c_void]
     lib.corr2d_format_repr.argtypes = [c_void, c_i64, c_void, c_i64, c_void]
@@ -107,7 +110,7 @@ def _declare(lib):
                  "corr2d_correlate_small_f64_slot", "corr2d_small_ops_depth",
                  "corr2d_prep", "corr2d_contract_f64", "corr2d_contract_f64_gauss", "corr2d_contract_bf16x3",
                  "corr2d_contract_tc", "corr2d_device_info", "corr2d_packed_depth", "corr2d_fft_factors",
-                 "corr2d_plane_absmax", "corr2d_find_peaks"):
+                 "corr2d_plane_absmax", "corr2d_find_peaks", "corr2d_fetch_mirrored"):
         getattr(lib, name).restype = c_int
 
 

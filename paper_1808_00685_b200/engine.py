@@ -13,7 +13,9 @@ status words into the reference's exceptions and copies results to the host.
 
 from __future__ import annotations
 
+import ctypes
 import os
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -591,10 +593,28 @@ class CorrelationPlan:
             ha = t.empty(self.psi.shape, dtype=self.psi.dtype, pin_memory=True)
         else:
             hs, ha = (t.from_numpy(o) if isinstance(o, np.ndarray) else o for o in out)
-        done = copy_d2h([(hs, self.phi), (ha, self.psi)], wait=wait)
+        if self._fetch_mirrored_ok(hs, ha):
+            done = fetch_mirrored(self.lib, self.phi, self.psi, hs, ha, wait=wait)
+        else:
+            global last_fetch_bytes
+            last_fetch_bytes = hs.numel() * hs.element_size() + ha.numel() * ha.element_size()
+            done = copy_d2h([(hs, self.phi), (ha, self.psi)], wait=wait)
         if wait:
             return hs.numpy(), ha.numpy()
         return hs.numpy(), ha.numpy(), done
+
+    def _fetch_mirrored_ok(self, hs, ha) -> bool:
+        """A whole homo Fourier map of at least MIRROR_MIN_N rows, contiguous on
+        both sides, with a nonzero MIRROR_FILL_PCT: its D2H leaves part of the
+        lower triangle to the host (fetch_mirrored)."""
+        if os.environ.get("CORR2D_FETCH_FULL") == "1" or MIRROR_FILL_PCT <= 0:
+            return False
+        n = self.n1
+        return (self.homo and self.route == "fourier" and n >= MIRROR_MIN_N
+                and (self.row0, self.row1) == (0, n) and (self.tile0, self.tile1) == (0, -1)
+                and all(x.dim() == 2 and tuple(x.shape) == (n, n) and x.is_contiguous()
+                        for x in (self.phi, self.psi, hs, ha))
+                and hs.dtype == self.phi.dtype and ha.dtype == self.psi.dtype)
 
     def run_to_host(self, out=None, axes=(None, None), labels=("first", "second")):
         """launch() + the planes' D2H queued right behind the kernels, the
@@ -711,6 +731,70 @@ def run_streamed(make_plan, n1: int, n2: int, dtype, blocks, out=None, check=Non
 
 
 _copy_streams = {}
+
+
+# homo maps from this many rows on send only part of their lower triangle, the
+# host fills the rest as the mirror (fetch_mirrored); band = rows per transfer
+# band (a multiple of the 256-row contraction tile); fill_pct = the share of each
+# band's lower part the host fills.  0 (default) = the plain full-plane copy:
+# on the B200 boxes' 16-thread hosts the transpose fill competes with the DMA
+# for host memory bandwidth and the split gains at most 2-4 % (25 %), loses
+# beyond 45 % (profiles/r2_fetch_probe.txt); a host with more memory bandwidth
+# per link sets CORR2D_FETCH_FILL_PCT.
+MIRROR_MIN_N = 4096
+MIRROR_BAND = 1024
+MIRROR_FILL_PCT = int(os.environ.get("CORR2D_FETCH_FILL_PCT", "0"))
+last_fetch_bytes = 0   # device -> host bytes of the last plan fetch (bench.py's e2e line)
+
+
+def fetch_mirrored(lib, phi, psi, hs, ha, wait: bool = True, band: int = MIRROR_BAND, fill_pct: int | None = None,
+                   threads: int | None = None):
+    """Device -> host copy of a homo map's two n x n planes through
+    corr2d_fetch_mirrored: row bands cross PCIe without the first fill_pct %
+    of their lower part, which host threads fill as (sync^T, -async^T) from
+    rows already landed while later bands are in flight (csrc/fetch.cu);
+    bit-identical to a full-plane copy.  Ordered after the current stream's work; wait=False returns at once
+    with the function that waits for completion (the call runs on a helper
+    thread; ctypes releases the GIL)."""
+    global last_fetch_bytes
+    t = torch()
+    n = phi.shape[0]
+    dt = _abi.F64 if phi.dtype == t.float64 else _abi.F32
+    if threads is None:
+        threads = min(32, len(os.sched_getaffinity(0)))
+    if fill_pct is None:
+        fill_pct = MIRROR_FILL_PCT
+    dev = phi.device
+    stream = stream_handle()
+    nbytes = ctypes.c_int64(0)
+    box = {}
+
+    def run():
+        try:
+            with t.cuda.device(dev):
+                rc = lib.corr2d_fetch_mirrored(dt, phi.data_ptr(), psi.data_ptr(), n, n, hs.data_ptr(),
+                                               ha.data_ptr(), n, band, fill_pct, threads, ctypes.byref(nbytes), stream)
+                _abi.check(rc, lib)   # the error message is per thread: raise here
+        except Exception as e:        # re-raised by finish() on the caller's thread
+            box["exc"] = e
+
+    def finish():
+        if "exc" in box:
+            raise box["exc"]
+        global last_fetch_bytes
+        last_fetch_bytes = int(nbytes.value)
+
+    if wait:
+        run()
+        finish()
+        return None
+    th = threading.Thread(target=run, name="corr2d-fetch", daemon=True)
+    th.start()
+
+    def done():
+        th.join()
+        finish()
+    return done
 
 
 def copy_d2h(pairs, streams: int = 4, chunk_bytes: int = 256 << 20, wait: bool = True):
