@@ -41,26 +41,23 @@ constexpr int kTileEdge = 256;    // largest contraction tile edge (tcgen05 2-SM
 constexpr int kFillCols = 256;    // columns per host fill task
 constexpr int kBlk = 32;          // host transpose block
 
-struct Streams {
-  int device = -1;
-  cudaStream_t s[kCopyStreams] = {};
-};
+// per-device copy streams, created on first use (a fixed table: pointers handed
+// out stay valid while other devices add theirs)
+constexpr int kMaxDevices = 64;
 std::mutex g_mu;
-std::vector<Streams> g_streams;
+cudaStream_t g_streams[kMaxDevices][kCopyStreams] = {};
 
 int copy_streams(cudaStream_t** out) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return fail(CORR2D_ERR_CUDA, "corr2d_fetch_mirrored: no device");
+  if (dev < 0 || dev >= kMaxDevices) return fail(CORR2D_ERR_UNSUPPORTED, "corr2d_fetch_mirrored: device index");
   std::lock_guard<std::mutex> lk(g_mu);
-  for (auto& e : g_streams)
-    if (e.device == dev) { *out = e.s; return CORR2D_OK; }
-  Streams e;
-  e.device = dev;
-  for (auto& s : e.s)
-    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
-      return fail(CORR2D_ERR_CUDA, "corr2d_fetch_mirrored: stream creation failed");
-  g_streams.push_back(e);
-  *out = g_streams.back().s;
+  cudaStream_t* s = g_streams[dev];
+  if (!s[kCopyStreams - 1])
+    for (int k = 0; k < kCopyStreams; ++k)
+      if (!s[k] && cudaStreamCreateWithFlags(&s[k], cudaStreamNonBlocking) != cudaSuccess)
+        return fail(CORR2D_ERR_CUDA, "corr2d_fetch_mirrored: stream creation failed");
+  *out = s;
   return CORR2D_OK;
 }
 
