@@ -14,11 +14,12 @@
 // a multiple of every contraction's tile edge); the host result equals a
 // full-plane copy bit for bit (tests/test_gpu_fetch.py).
 //
-// Measured (profiles/r2_fetch_probe.txt): the host's transpose fill and the
-// DMA share the host's memory bandwidth.  On the B200 boxes' 16-thread hosts a
-// 25 % split gains 2-4 % and the upper-triangle-only transfer (100 %) loses
-// 30 % (cfg5: 192 vs 150 ms), so the Python layer keeps the plain full copy
-// by default (engine.MIRROR_FILL_PCT = 0, CORR2D_FETCH_FILL_PCT to opt in).
+// Measured (profiles/r2_fetch_probe.txt, r2_fetch_e2e_ab.txt): the host's
+// transpose fill and the DMA share the host's memory bandwidth.  On the B200
+// boxes' 16-thread hosts the upper-triangle-only transfer (100 %) loses 30 %
+// (cfg5: 192 vs 150 ms); a 25-35 % host share is the best split (public-call
+// e2e cfg5 154 -> 143-148 ms, cfg3 76.7 -> 75.0 ms), so the Python layer uses
+// 30 % (engine.MIRROR_FILL_PCT; CORR2D_FETCH_FILL_PCT=0 = full copy).
 #include <cuda_runtime.h>
 #include <emmintrin.h>
 

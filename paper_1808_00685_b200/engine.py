@@ -736,14 +736,14 @@ _copy_streams = {}
 # homo maps from this many rows on send only part of their lower triangle, the
 # host fills the rest as the mirror (fetch_mirrored); band = rows per transfer
 # band (a multiple of the 256-row contraction tile); fill_pct = the share of each
-# band's lower part the host fills.  0 (default) = the plain full-plane copy:
-# on the B200 boxes' 16-thread hosts the transpose fill competes with the DMA
-# for host memory bandwidth and the split gains at most 2-4 % (25 %), loses
-# beyond 45 % (profiles/r2_fetch_probe.txt); a host with more memory bandwidth
-# per link sets CORR2D_FETCH_FILL_PCT.
+# band's lower part the host fills.  The transpose fill competes with the DMA for
+# the host's memory bandwidth: on the B200 boxes' 16-thread hosts 25-35 % is
+# best (public-call e2e cfg5 154 -> 143-148 ms, cfg3 76.7 -> 75.0 ms), the
+# upper triangle alone (100 %) loses 30 % (profiles/r2_fetch_e2e_ab.txt,
+# r2_fetch_probe.txt).  CORR2D_FETCH_FILL_PCT=0 = the plain full-plane copy.
 MIRROR_MIN_N = 4096
 MIRROR_BAND = 1024
-MIRROR_FILL_PCT = int(os.environ.get("CORR2D_FETCH_FILL_PCT", "0"))
+MIRROR_FILL_PCT = int(os.environ.get("CORR2D_FETCH_FILL_PCT", "30"))
 last_fetch_bytes = 0   # device -> host bytes of the last plan fetch (bench.py's e2e line)
 
 

@@ -2,7 +2,7 @@
 (corr2d_fetch_mirrored, csrc/fetch.cu): the host planes must equal a
 full-plane copy bit for bit -- on exactly (anti)symmetric synthetic planes of
 ragged sizes and host fill shares, and on maps the contractions wrote (fp64,
-fp32 tcgen05) through the public corr2d() call against its default full copy."""
+fp32 tcgen05) through the public corr2d() call against the full copy."""
 
 import numpy as np
 import pytest
@@ -76,7 +76,8 @@ def test_public_call_mirrored_equals_full_copy(monkeypatch, dt, m, n):
     x = rng.standard_normal((m, n)).cumsum(axis=1)
     ds = P.SpectralDataset(np.linspace(0.0, 1.0, n), np.arange(m, dtype=float), x,
                            dtype=np.float32 if dt == "float32" else np.float64)
-    full = P.corr2d(ds, dtype=dt)      # default: the full-plane copy
+    monkeypatch.setattr(engine, "MIRROR_FILL_PCT", 0)
+    full = P.corr2d(ds, dtype=dt)      # the full-plane copy
     assert engine.last_fetch_bytes == 2 * n * n * full.sync.itemsize
     monkeypatch.setattr(engine, "MIRROR_FILL_PCT", 45)
     half = P.corr2d(ds, dtype=dt)
