@@ -741,9 +741,10 @@ _copy_streams = {}
 # best (public-call e2e cfg5 154 -> 143-148 ms, cfg3 76.7 -> 75.0 ms), the
 # upper triangle alone (100 %) loses 30 % (profiles/r2_fetch_e2e_ab.txt,
 # r2_fetch_probe.txt).  CORR2D_FETCH_FILL_PCT=0 = the plain full-plane copy.
-MIRROR_MIN_N = 4096
+MIRROR_MIN_N = 16384   # cfg4's 8192^2 fp64 map loses 7 % with it (19.3 -> 20.8 ms per call)
 MIRROR_BAND = 1024
 MIRROR_FILL_PCT = int(os.environ.get("CORR2D_FETCH_FILL_PCT", "30"))
+MIRROR_THREADS = int(os.environ.get("CORR2D_FETCH_THREADS", "0"))   # 0 = the host threads available (<= 32)
 last_fetch_bytes = 0   # device -> host bytes of the last plan fetch (bench.py's e2e line)
 
 
@@ -761,7 +762,7 @@ def fetch_mirrored(lib, phi, psi, hs, ha, wait: bool = True, band: int = MIRROR_
     n = phi.shape[0]
     dt = _abi.F64 if phi.dtype == t.float64 else _abi.F32
     if threads is None:
-        threads = min(32, len(os.sched_getaffinity(0)))
+        threads = MIRROR_THREADS or min(32, len(os.sched_getaffinity(0)))
     if fill_pct is None:
         fill_pct = MIRROR_FILL_PCT
     dev = phi.device

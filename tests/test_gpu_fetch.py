@@ -70,7 +70,7 @@ def test_mirrored_fetch_bad_arguments():
         engine.fetch_mirrored(_abi.load(), phi, psi, hs, ha, fill_pct=101)
 
 
-@pytest.mark.parametrize("dt,m,n", [("float64", 24, 4352), ("float32", 64, 5120)])
+@pytest.mark.parametrize("dt,m,n", [("float64", 24, 4352), ("float32", 64, 5120), ("float32", 32, 16384)])
 def test_public_call_mirrored_equals_full_copy(monkeypatch, dt, m, n):
     rng = np.random.default_rng(m)
     x = rng.standard_normal((m, n)).cumsum(axis=1)
@@ -80,6 +80,7 @@ def test_public_call_mirrored_equals_full_copy(monkeypatch, dt, m, n):
     full = P.corr2d(ds, dtype=dt)      # the full-plane copy
     assert engine.last_fetch_bytes == 2 * n * n * full.sync.itemsize
     monkeypatch.setattr(engine, "MIRROR_FILL_PCT", 45)
+    monkeypatch.setattr(engine, "MIRROR_MIN_N", 4096)
     half = P.corr2d(ds, dtype=dt)
     assert engine.last_fetch_bytes < 2 * n * n * full.sync.itemsize
     assert np.array_equal(_bits(half.sync), _bits(full.sync))
