@@ -154,8 +154,9 @@ def readme(dst):
     if ref and b5:
         L.append(f"* Reference arm ({ref['cpu_baseline']['kind']} on {ref['cpu_baseline']['cores']} host threads): "
                  f"{ref['value']:.4f} GElem/s -> e2e / reference = {b5['e2e']['value'] / ref['value']:.0f}x "
-                 f"(the e2e step is PCIe-bound: {b5['e2e']['d2h_bytes_per_step'] / 1e9:.1f} GB of planes D2H per "
-                 f"call), device-resident value / reference = {b5['value'] / ref['value']:.0f}x.")
+                 f"(the e2e step is bound by the PCIe link and the host's memory: "
+                 f"{b5['e2e']['d2h_bytes_per_step'] / 1e9:.1f} GB of the 8.6 GB of planes cross the link, host threads "
+                 f"fill the rest as the mirror), device-resident value / reference = {b5['value'] / ref['value']:.0f}x.")
     if b5 and "cpu_baseline" in b5:
         cb = b5["cpu_baseline"]
         L.append(f"* cpu_baseline in the cfg5 line: {cb['value']:.4f} GElem/s ({cb['cores']} threads; {cb['sample']}).")
