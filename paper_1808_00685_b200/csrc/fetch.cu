@@ -27,6 +27,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <system_error>
 #include <thread>
 #include <vector>
 
@@ -176,7 +177,13 @@ int fetch_impl(const T* ds, const T* da, int64_t ld_dev, int n, T* hs, T* ha, in
   };
   const int nt = std::max(1, std::min<int>(threads, (int)tasks.size()));
   std::vector<std::thread> pool;
-  for (int k = 1; k < nt; ++k) pool.emplace_back(worker_fenced);
+  for (int k = 1; k < nt; ++k) {
+    try {
+      pool.emplace_back(worker_fenced);
+    } catch (const std::system_error&) {   // fewer threads: the tasks still all run
+      break;
+    }
+  }
   worker_fenced();
   for (auto& th : pool) th.join();
   cudaError_t last = cudaSuccess;
